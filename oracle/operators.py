@@ -1,0 +1,207 @@
+"""ORACLE (test infrastructure only): assembled P2-P1 operators from the weak forms.
+
+Definitions followed:
+  A_ij = int 2 eta [ eps(phi_j) : eps(phi_i) - (1/dim) div phi_j div phi_i ]  (P:277-278,
+         with eta on BOTH terms -- reading R1: P:278 drops eta from the div-div
+         term, contradicted by tau := 2 eta eps_dot, the appendix
+         and "A symmetric positive semidefinite").  The factor 2/dim of
+         P:278 multiplies div.div with the eps:eps term weighted 2 -> 2 eta (1/3).
+  B_ij = - int (div phi_j^u) phi_i^p
+  C_ij = - int grad(ln rho) . phi_j^u phi_i^p,  grad ln rho = -gamma x/|x|
+  Pull-back to the reference tet through F and the blending B:
+      grad_x phi = (J_B^-1)^T (J_F^-1)^T grad_xi phi,  dx = |det J_B||det J_F| dxi
+  Viscosity as a P1 function interpolated at quadrature points.
+  Constraints: zero Dirichlet rows (surface) by block-row modification,
+  free-slip projection P_v at CMB nodes, u <- u - (u.n) n;
+  the constrained operator is (M P_v) A (P_v M).  diag(A) WITHOUT P_v.
+
+The element matrices are computed one quadrature point at a time from these
+formulas (numpy) and summed into scipy CSR matrices (assembly = the plain
+definition of the matrix-free apply).
+"""
+from __future__ import annotations
+
+import numpy as np
+import scipy.sparse as sp
+
+from . import fe
+from .refine import LevelMesh, node_bc, BC_DIRICHLET, BC_FREESLIP
+
+FORM_FULL, FORM_EPS = 0, 1
+
+
+def macro_blend(lm: LevelMesh):
+    """(nhat, c) of every macro tet (computed from macro vertices, reading R3)."""
+    return fe.shell_blend_params(lm.macro_verts[lm.macro_tets])
+
+
+def quad_geometry(lm: LevelMesh, tets: np.ndarray, blended: bool, blend_params=None):
+    """For the micro tets `tets`: per quadrature point the weight w_q |det J|, the physical
+    P2 gradients (T,Q,10,3), the blended point x_q (T,Q,3)."""
+    xi, w = fe.q4_rule()
+    X = lm.X[tets]                                          # (T,4,3)
+    JF = np.stack([X[:, 1] - X[:, 0], X[:, 2] - X[:, 0], X[:, 3] - X[:, 0]], axis=2)  # columns
+    G = fe.p2_grad(xi)                                      # (Q,10,3)
+    T, Q = len(tets), len(w)
+    W = np.empty((T, Q))
+    grads = np.empty((T, Q, 10, 3))
+    xq_all = np.empty((T, Q, 3))
+    if blended:
+        nhat_m, c_m = blend_params
+        mac = lm.tet_macro[tets]
+        nhat, c = nhat_m[mac], c_m[mac]
+    for q in range(Q):
+        xq = X[:, 0] + np.einsum("tij,j->ti", JF, xi[q])
+        if blended:
+            JB = fe.blend_jacobian(xq, nhat, c)
+            J = JB @ JF
+            xq_all[:, q] = fe.blend(xq, nhat, c)
+        else:
+            J = JF
+            xq_all[:, q] = xq
+        Jinv = np.linalg.inv(J)
+        W[:, q] = w[q] * np.abs(np.linalg.det(J))
+        # grad_x phi (row) = grad_xi phi (row) J^-1
+        grads[:, q] = np.einsum("am,tmd->tad", G[q], Jinv)
+    return W, grads, xq_all
+
+
+def element_A(W, grads, eta_q, form=FORM_FULL):
+    """(T,30,30) element matrices, local dof = 3*a + c (a = local node, c = component)."""
+    T, Q = W.shape
+    Ae = np.zeros((T, 30, 30))
+    eye = np.eye(3)
+    for q in range(Q):
+        g = grads[:, q]                                     # (T,10,3)
+        # grad of vector basis (a,c): Gr[i,j] = delta_ic g_a[j]
+        Gr = np.einsum("ci,taj->tacij", eye, g)             # (T,10,3,3,3)
+        eps = 0.5 * (Gr + Gr.transpose(0, 1, 2, 4, 3))
+        E = eps.reshape(T, 30, 9)
+        K = E @ E.transpose(0, 2, 1)                        # eps(phi_i):eps(phi_j)
+        if form == FORM_FULL:
+            # div(phi_a e_c) = d_c phi_a = g[a, c] -> flat index 3a+c
+            div = g.reshape(T, 30)
+            K = K - (1.0 / 3.0) * div[:, :, None] * div[:, None, :]
+        Ae += (2.0 * eta_q[:, q] * W[:, q])[:, None, None] * K
+    return Ae
+
+
+def element_B(W, grads):
+    """(T,4,30): B_K[p,(b,d)] = - sum_q W lam_p(xi_q) d_d phi_b."""
+    xi, _ = fe.q4_rule()
+    lam = fe.p1_basis(xi)                                   # (Q,4)
+    T, Q = W.shape
+    div = grads.reshape(T, Q, 30)
+    return -np.einsum("tq,qp,tqj->tpj", W, lam, div)
+
+
+def element_C(W, xq, gamma):
+    """(T,4,30): C_K[p,(b,d)] = - sum_q W lam_p (grad ln rho)_d phi_b,  grad ln rho = -gamma x/|x|."""
+    xi, _ = fe.q4_rule()
+    lam = fe.p1_basis(xi)
+    phi = fe.p2_basis(xi)                                   # (Q,10)
+    glr = -gamma * xq / np.linalg.norm(xq, axis=2, keepdims=True)   # (T,Q,3)
+    vals = np.einsum("qb,tqd->tqbd", phi, glr).reshape(xq.shape[0], xq.shape[1], 30)
+    return -np.einsum("tq,qp,tqj->tpj", W, lam, vals)
+
+
+def p2vec_dofs(tet_p2: np.ndarray) -> np.ndarray:
+    return (3 * tet_p2[:, :, None] + np.arange(3)[None, None, :]).reshape(tet_p2.shape[0], 30)
+
+
+class Discretisation:
+    """Assembled operators of one level.  eta_p1: nodal P1 viscosity (canonical order) or None (=1)."""
+
+    def __init__(self, lm: LevelMesh, blended: bool, eta_p1=None, gamma=0.0,
+                 bc_by_tag=None, form=FORM_FULL, chunk=20000, build=("A", "B", "C")):
+        self.lm = lm
+        self.blended = blended
+        self.blend_params = macro_blend(lm) if blended else None
+        self.gamma = gamma
+        self.form = form
+        n2, n1 = lm.n_p2, lm.n_p1
+        eta_p1 = np.ones(n1) if eta_p1 is None else np.asarray(eta_p1, dtype=np.float64)
+        self.eta_p1 = eta_p1
+        mats = {k: None for k in build}
+        for s in range(0, lm.n_tets, chunk):
+            tets = np.arange(s, min(s + chunk, lm.n_tets))
+            W, grads, xq = quad_geometry(lm, tets, blended, self.blend_params)
+            vd = p2vec_dofs(lm.tet_p2[tets])
+            pd = lm.tet_p1[tets]
+            if "A" in build:
+                xi, _ = fe.q4_rule()
+                eta_q = eta_p1[pd] @ fe.p1_basis(xi).T       # (T,Q) P1 interpolation
+                Ae = element_A(W, grads, eta_q, form)
+                M = _coo(Ae, vd, vd, 3 * n2, 3 * n2)
+                mats["A"] = M if mats["A"] is None else mats["A"] + M
+            if "B" in build:
+                Be = element_B(W, grads)
+                M = _coo(Be, pd, vd, n1, 3 * n2)
+                mats["B"] = M if mats["B"] is None else mats["B"] + M
+            if "C" in build:
+                Ce = element_C(W, xq, gamma) if gamma != 0.0 else np.zeros((len(tets), 4, 30))
+                M = _coo(Ce, pd, vd, n1, 3 * n2)
+                mats["C"] = M if mats["C"] is None else mats["C"] + M
+        self.A = mats.get("A")
+        self.B = mats.get("B")
+        self.C = mats.get("C")
+        # constraints
+        self.bc = node_bc(lm.p2_keys, lm.macro_tets, lm.macro_vtag, bc_by_tag or {})
+        self.Pm = constraint_matrix(lm.p2_xt, self.bc)
+
+    # constrained operators -------------------------------------------------
+    def Ac(self):
+        return (self.Pm @ self.A @ self.Pm).tocsr()
+
+    def diagA(self):
+        """diag(A) from the unprojected A; Dirichlet dofs keep their raw value."""
+        return self.A.diagonal().copy()
+
+    def project(self, u):
+        """P_v M u."""
+        return self.Pm @ u
+
+    def apply_A(self, u):
+        return self.Pm @ (self.A @ (self.Pm @ u))
+
+    def apply_BT(self, p):
+        return self.Pm @ (self.B.T @ p)
+
+    def apply_Bbar(self, u):
+        return (self.B + self.C) @ (self.Pm @ u)
+
+    def free_dofs(self):
+        m = np.ones(3 * self.lm.n_p2, dtype=bool)
+        d = np.nonzero(self.bc == BC_DIRICHLET)[0]
+        for c in range(3):
+            m[3 * d + c] = False
+        return m
+
+
+def _coo(E, rows, cols, nr, nc):
+    T, a, b = E.shape
+    r = np.broadcast_to(rows[:, :, None], (T, a, b))
+    c = np.broadcast_to(cols[:, None, :], (T, a, b))
+    return sp.coo_matrix((E.ravel(), (r.ravel(), c.ravel())), shape=(nr, nc)).tocsr()
+
+
+def constraint_matrix(xt: np.ndarray, bc: np.ndarray) -> sp.csr_matrix:
+    """P_v M as a sparse block-diagonal matrix: 0 on Dirichlet nodes, I - n n^T on free-slip
+    nodes with n = x/|x| (the blending preserves directions), I elsewhere."""
+    n = xt.shape[0]
+    rows, cols, vals = [], [], []
+    free = np.nonzero(bc == 0)[0]
+    for c in range(3):
+        rows.append(3 * free + c)
+        cols.append(3 * free + c)
+        vals.append(np.ones(len(free)))
+    fs = np.nonzero(bc == BC_FREESLIP)[0]
+    if len(fs):
+        nv = xt[fs] / np.linalg.norm(xt[fs], axis=1, keepdims=True)
+        for i in range(3):
+            for j in range(3):
+                rows.append(3 * fs + i)
+                cols.append(3 * fs + j)
+                vals.append((1.0 if i == j else 0.0) - nv[:, i] * nv[:, j])
+    return sp.coo_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
+                         shape=(3 * n, 3 * n)).tocsr()

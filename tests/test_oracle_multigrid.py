@@ -1,0 +1,113 @@
+"""Pins of oracle/multigrid.py: P2 prolongation exactness and its textbook weights, Chebyshev
+error propagator (closed form), power iteration on known spectra, CG exactness on small SPD
+systems, and V-cycle invariants (fixed point, zero rhs, contraction)."""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from oracle.refine import build_level, BC_DIRICHLET, BC_FREESLIP
+from oracle.operators import Discretisation
+from oracle.multigrid import p2_prolongation, chebyshev, power_iteration, pcg, Hierarchy
+from workload import icoshell, reference_tet, uniform_vec
+
+
+def _levels(mesh, Ls):
+    return {L: build_level(mesh.verts, mesh.tets, mesh.vtag, L) for L in Ls}
+
+
+def test_prolongation_exact_on_quadratics_and_textbook_weights():
+    m = icoshell(3, 2)
+    lv = _levels(m, (0, 1))
+    P = p2_prolongation(lv[0], lv[1])
+    rng = np.random.default_rng(0)
+    Q = rng.standard_normal((3, 3))
+    g = lambda x: np.einsum("ni,ij,nj->n", x, Q, x) + x @ np.array([1.0, -2.0, 0.5]) + 3.0
+    assert np.abs(P @ g(lv[0].p2_xt) - g(lv[1].p2_xt)).max() < 1e-13
+    assert np.abs(P @ np.ones(lv[0].n_p2) - 1.0).max() < 1e-15
+    # 1-D P2 interpolation at the quarter points of a coarse edge: weights 3/8, 3/4, -1/8
+    vals = set(np.round(P.data, 12))
+    assert {0.375, 0.75, -0.125, 1.0} <= vals
+    assert vals <= {1.0, 0.375, 0.75, -0.125, 0.5, 0.25, 0.0}
+
+
+def test_chebyshev_error_propagator_closed_form():
+    """With x0 = 0, f = A x*, the error after one degree-k sweep is T_k((theta-lam)/delta)/T_k(theta/delta) e0
+    per eigenpair of D^-1 A (diagonal toy, D = I)."""
+    lam = np.linspace(0.05, 2.0, 40)
+    A = sp.diags(lam).tocsr()
+    Pm = sp.identity(40, format="csr")
+    dinv = np.ones(40)
+    xs = np.random.default_rng(1).standard_normal(40)
+    b = 2.0 * 1.1
+    a = b / 10.0
+    theta, delta = (a + b) / 2, (b - a) / 2
+    for k in (1, 2, 3, 4):
+        x = chebyshev(A, dinv, Pm, A @ xs, np.zeros(40), k, b)
+        Tk = np.polynomial.chebyshev.Chebyshev.basis(k)
+        pred = Tk((theta - lam) / delta) / Tk(theta / delta) * xs
+        assert np.abs((xs - x) - pred).max() < 1e-13
+    # degree 1 == damped Jacobi with omega = 1/theta
+    x1 = chebyshev(A, dinv, Pm, A @ xs, np.zeros(40), 1, b)
+    assert np.abs(x1 - (A @ xs) / theta).max() < 1e-15
+
+
+def test_power_iteration_known_spectrum_and_homogeneity():
+    n = 50
+    A = sp.diags(np.arange(1.0, n + 1)).tocsr()
+    Pm = sp.identity(n, format="csr")
+    v0 = np.random.default_rng(2).uniform(-1, 1, n)
+    lam = power_iteration(A, np.ones(n), Pm, v0, 200)
+    assert abs(lam - n) / n < 1e-3
+    l20 = power_iteration(A, np.ones(n), Pm, v0, 20)
+    assert l20 <= n * (1 + 1e-14)
+    assert abs(power_iteration(3.0 * A, np.ones(n), Pm, v0, 20) - 3.0 * l20) < 1e-12 * l20
+    with pytest.raises(ZeroDivisionError):
+        power_iteration(0.0 * A, np.ones(n), Pm, v0, 3)
+
+
+def test_pcg_solves_small_spd_exactly():
+    rng = np.random.default_rng(3)
+    n = 30
+    M = rng.standard_normal((n, n))
+    A = sp.csr_matrix(M @ M.T + n * np.eye(n))
+    f = rng.standard_normal(n)
+    x = pcg(A, 1.0 / A.diagonal(), sp.identity(n, format="csr"), f, 50)
+    assert np.abs(A @ x - f).max() < 1e-10 * np.abs(f).max()
+    assert np.all(pcg(A, 1.0 / A.diagonal(), sp.identity(n, format="csr"), 0 * f, 50) == 0)
+
+
+@pytest.fixture(scope="module")
+def shell_hierarchy():
+    m = icoshell(3, 2)
+    discs, v0 = {}, {}
+    for L in (1, 2):
+        lm = build_level(m.verts, m.tets, m.vtag, L)
+        discs[L] = Discretisation(lm, True, None, 0.3781, {2: BC_DIRICHLET, 1: BC_FREESLIP}, build=("A",))
+        v0[L] = uniform_vec(lm.p2_keys, 6)
+    return discs, Hierarchy(discs, v0, pre=3, post=3, degree=3)
+
+
+def test_vcycle_invariants(shell_hierarchy):
+    discs, H = shell_hierarchy
+    lm = discs[2].lm
+    f = discs[2].project(uniform_vec(lm.p2_keys, 4))
+    assert np.all(H.vcycle(0 * f) == 0)
+    # symmetric smoothing + Galerkin-consistent transfer: iteration contracts (isoviscous)
+    A = H.Ac[2]
+    x = np.zeros_like(f)
+    res = []
+    for _ in range(3):
+        r = f - A @ x
+        res.append(np.linalg.norm(r))
+        x = x + H.vcycle(r)
+    assert res[1] / res[0] < 0.05 and res[2] / res[1] < 0.1
+    # the correction keeps the constraints: u.n = 0 on the CMB, 0 on the surface
+    y = H.vcycle(f)
+    assert np.abs(discs[2].project(y) - y).max() < 1e-14 * np.abs(y).max()
+    # power estimate is below the true largest eigenvalue of D^-1/2 A D^-1/2 and close to it
+    free = discs[2].free_dofs()
+    Af = A[free][:, free]
+    s = np.sqrt(H.dinv[2][free])
+    import scipy.sparse.linalg as sla
+    lmax = sla.eigsh(sp.diags(s) @ Af @ sp.diags(s), k=1, which="LA")[0][0]
+    assert 0.85 * lmax < H.lam[2] < 1.1 * lmax
