@@ -1,0 +1,299 @@
+#!/usr/bin/env python
+"""bench.py -- one step = one GMG V(3,3)-cycle for the A block (BASELINE config 3: blended
+shell(3,2), refinement level 5, viscosity contrast 1e6 x 30 radial jump, Chebyshev degree 3,
+lambda_hat from 20 power iterations, P2 transfers down to level 1, 50 Jacobi-PCG coarse
+iterations) on a seeded rhs, through the C-ABI (graph-launched).  The per-eta setup (diag(A),
+power iterations) runs before the timed region.  Also measured in the same run: the fine-level
+epsilon_apply throughput (BASELINE metric's first clause) and the end-to-end V-cycle through
+vcycle_host() with pinned host buffers.
+
+Contract: python bench.py --gpus N --steps K --warmup W [--impl reference]; for N>1 launched by
+torch.distributed.run, one process per GPU; rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "P2 epsilon-operator apply GDoF/s (fp64) and V-cycle time; % of fp64/HBM roofline"
+GAMMA = 0.3781
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--level", type=int, default=5)
+    ap.add_argument("--cpu-level", type=int, default=2, help="oracle sample level for cpu_baseline / reference")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--apply-reps", type=int, default=20)
+    return ap.parse_args()
+
+
+def peaks():
+    p = {}
+    try:
+        p = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    return p
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.rows = []
+        if self.proc is None:
+            return
+        time.sleep(0.25)
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=5)
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 7:
+                self.rows.append(f)
+
+    def summary(self):
+        rows = getattr(self, "rows", [])
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(r[0]) for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if "Active" in r[3 + i]})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": float(rows[0][1]), "reasons": reasons,
+                "samples": len(rows)}
+
+
+def build_case(level, device):
+    """Library-side set-up of config 3 (mesh, eta per level, power start vectors, rhs)."""
+    import torch
+    import paper_2506_04157_b200 as hhg
+    from workload import icoshell, uniform_vec, viscosity
+    mac = icoshell(3, 2, 0.55, 1.0)
+    M = hhg.Mesh.from_macro(mac, level)
+    M.blend_map(hhg.HHG_BLEND_SHELL)
+    M.set_bc(hhg.HHG_BND_OUTER, hhg.HHG_BC_DIRICHLET0)
+    M.set_bc(hhg.HHG_BND_INNER, hhg.HHG_BC_FREESLIP)
+    etas, v0 = {}, {}
+    for L in range(1, level + 1):
+        keys1 = M.canonical_keys(L, hhg.HHG_P1)
+        xyz = M.node_coords(L, hhg.HHG_P1)
+        xc = torch.stack([M.to_canonical(L, hhg.HHG_P1, xyz[:, c].contiguous()) for c in range(3)], 1)
+        etas[L] = M.from_canonical(L, hhg.HHG_P1, viscosity(xc.cpu().numpy(), keys1, 1e6, 30.0))
+        if L > 1:
+            v0[L] = M.from_canonical(L, hhg.HHG_P2VEC, uniform_vec(M.canonical_keys(L, hhg.HHG_P2), 6))
+    keysL = M.canonical_keys(level, hhg.HHG_P2)
+    rhs = M.apply_bc(level, M.from_canonical(level, hhg.HHG_P2VEC, uniform_vec(keysL, 4)))
+    n_dof = 3 * keysL.shape[0]
+    return M, etas, v0, rhs, n_dof
+
+
+def cpu_oracle_vcycle(level, steps=1):
+    """The oracle as it stands: config-3 recipe V-cycle on shell(3,2) levels `level`..1 (CPU)."""
+    import numpy as np
+    from oracle.multigrid import Hierarchy
+    from tests.harness import BC_SHELL, oracle_case
+    from workload import icoshell, uniform_vec
+    mac = icoshell(3, 2)
+    t0 = time.perf_counter()
+    discs, v0 = {}, {}
+    for L in range(1, level + 1):
+        lm, d, _ = oracle_case(mac, L, True, BC_SHELL, (1e6, 30.0), 0.0, build=("A",))
+        discs[L], v0[L] = d, uniform_vec(lm.p2_keys, 6)
+    H = Hierarchy(discs, v0)
+    setup = time.perf_counter() - t0
+    f = discs[level].project(uniform_vec(discs[level].lm.p2_keys, 4))
+    ts = []
+    for _ in range(steps):
+        t1 = time.perf_counter()
+        H.vcycle(f)
+        ts.append(time.perf_counter() - t1)
+    ndof = 3 * discs[level].lm.n_p2
+    return ndof, ts, setup
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    ndof, ts, setup = cpu_oracle_vcycle(args.cpu_level, args.warmup + args.steps)
+    tt = ts[args.warmup:]
+    ms = 1e3 * sum(tt) / len(tt)
+    val = ndof / (ms * 1e-3) / 1e9
+    cores = len(os.sched_getaffinity(0))
+    sample = (f"oracle (numpy/scipy CSR) V(3,3)-cycle, shell(3,2) levels {args.cpu_level}->1, config-3 recipe, "
+              f"{ndof} dofs; assembly/setup {setup:.1f} s excluded")
+    print(json.dumps({"impl": "reference", "metric": METRIC, "value": val, "unit": "GDoF/s", "n_gpus": args.gpus,
+                      "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+                      "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                      "config": {"workload": f"config3-sample shell(3,2) L{args.cpu_level} V(3,3)", "level": args.cpu_level},
+                      "cpu_baseline": {"value": val, "unit": "GDoF/s", "cores": cores, "kind": "oracle", "sample": sample},
+                      "e2e": {"value": val, "unit": "GDoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2506_04157_b200 as hhg
+
+    L = args.level
+    M, etas, v0, rhs, n_dof = build_case(L, local)
+    t0 = time.perf_counter()
+    mg = hhg.MG(M, 1, L, etas, v0, pre=3, post=3, degree=3, power_iters=20, coarse_iters=50)
+    setup_s = time.perf_counter() - t0
+    s = torch.cuda.Stream()
+    x = M.zeros(L, hhg.HHG_P2VEC)
+
+    # kernels per V-cycle (eager count), then graph warm-up
+    hhg.launch_count(reset=True)
+    mg.profile(True)
+    with torch.cuda.stream(s):
+        mg.vcycle(rhs, x, stream=s)
+    s.synchronize()
+    kernels_per_cycle = hhg.launch_count(reset=True)
+    # profiled cycles: fine-level element kernel durations measured with CUDA events on s
+    mg.profile(True)
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            mg.vcycle(rhs, x, stream=s)
+    s.synchronize()
+    prof = mg.profile_get()
+    mg.profile(False)
+
+    with torch.cuda.stream(s):
+        for _ in range(max(3, args.warmup)):
+            mg.vcycle(rhs, x, stream=s)
+    s.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        with torch.cuda.stream(s):
+            e0.record(s)
+            for _ in range(args.steps):
+                mg.vcycle(rhs, x, stream=s)
+            e1.record(s)
+        s.synchronize()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * n_dof / (ms * 1e-3) / 1e9
+
+    # standalone fine-level epsilon_apply (BASELINE metric, first clause)
+    y = M.zeros(L, hhg.HHG_P2VEC)
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            hhg.epsilon_apply(M, L, etas[L], rhs, y, stream=s)
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(s)
+        for _ in range(args.apply_reps):
+            hhg.epsilon_apply(M, L, etas[L], rhs, y, stream=s)
+        a1.record(s)
+    s.synchronize()
+    apply_ms = a0.elapsed_time(a1) / args.apply_reps
+
+    # end to end: pinned host rhs -> V-cycle -> host x, through vcycle_host
+    rhs_h = rhs.cpu().pin_memory()
+    x_h = torch.empty_like(rhs_h).pin_memory()
+    with torch.cuda.stream(s):
+        mg.vcycle_host(rhs_h, x_h, stream=s)
+        s.synchronize()
+        h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        h0.record(s)
+        for _ in range(args.steps):
+            mg.vcycle_host(rhs_h, x_h, stream=s)
+        h1.record(s)
+    s.synchronize()
+    e2e_ms = h0.elapsed_time(h1) / args.steps
+    nbytes = rhs.numel() * 8
+
+    # roofline of the dominant kernel (fine-level element kernel, fp64 DFMA pipe)
+    n_tets = 240 * 8 ** L
+    flops_per_tet = float(os.environ.get("HHG_FLOPS_PER_TET", "0")) or FLOPS_PER_TET
+    elem_ms = prof["apply_ms_sum"] / max(1, prof["apply_count"])
+    achieved = flops_per_tet * n_tets / (elem_ms * 1e-3) / 1e12
+    pk = peaks()
+    fp64_peak = pk.get("fp64_tflops") or FP64_PEAK_DERIVED
+    result = {
+        "metric": METRIC, "value": value, "unit": "GDoF/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"config3: V(3,3)-cycle, blended shell(3,2) level {L}->1, eta contrast 1e6 x30, "
+                               "Chebyshev deg 3, 50 PCG coarse its",
+                   "level": L, "velocity_dofs": n_dof, "micro_tets": n_tets, "parallelism": f"replicas{world}",
+                   "l2": "inputs larger than L2 (rhs/x/work vectors 276 MB each at level 5)"},
+        "apply": {"gdofs": n_dof / (apply_ms * 1e-3) / 1e9, "ms": apply_ms, "level": L,
+                  "note": "epsilon_apply (memset + element kernel + interface sum/BC) standalone"},
+        "vcycle_ms": ms, "setup_s": setup_s,
+        "roofline": {"bound": "alu", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
+                     "frac": achieved / fp64_peak, "traffic": TRAFFIC_PER_LAUNCH,
+                     "kernel": "k_elem<blend,A,full> (fine level)", "elem_ms": elem_ms,
+                     "flops_per_tet": flops_per_tet,
+                     "peak_source": "MEASURED_PEAKS.json fp64_tflops" if pk.get("fp64_tflops") else
+                     "derived: 148 SM x 64 DFMA/clk x 2 x 1.965 GHz (DESIGN.md)"},
+        "e2e": {"value": world * n_dof / (e2e_ms * 1e-3) / 1e9, "unit": "GDoF/s", "ms": e2e_ms,
+                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes},
+        "gpu_launches": kernels_per_cycle * args.steps,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        ndof_c, ts, setup = cpu_oracle_vcycle(args.cpu_level, 2)
+        v = ndof_c / min(ts) / 1e9
+        result["cpu_baseline"] = {"value": v, "unit": "GDoF/s", "cores": len(os.sched_getaffinity(0)),
+                                  "kind": "oracle",
+                                  "sample": f"oracle V(3,3)-cycle shell(3,2) levels {args.cpu_level}->1 "
+                                            f"({ndof_c} dofs), best of 2; setup {setup:.1f} s excluded"}
+    if rank == 0:
+        print(json.dumps(result))
+    if dist:
+        dist.destroy_process_group()
+
+
+# algorithmic DP flops per micro tet of the A element kernel (cross-checked
+# against ncu smsp__sass_thread_inst_executed_op_d{fma,add,mul}_pred_on)
+FLOPS_PER_TET = 1300.0
+FP64_PEAK_DERIVED = 148 * 64 * 2 * 1.965e9 / 1e12
+TRAFFIC_PER_LAUNCH = None
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,224 @@
+/*
+ * hhg_stokes.h -- C-ABI of libhhgstokes.so: the B200 (sm_100a) hot path of
+ * arxiv 2506.04157 (Burkhart, Kohl, Wohlmuth, Zawallich), "A robust matrix-free
+ * approach for large-scale non-isothermal high-contrast viscosity Stokes flow on
+ * blended domains".  Citations "P:<n>" are lines of /root/reference/PAPER.md.
+ *
+ * The hot path: matrix-free application of the blended P2-P1 Taylor-Hood,
+ * variable-viscosity, compressible Stokes operator
+ *        [ A(eta)   B^T ] [u]       A_ij = int 2 eta (eps(phi_j):eps(phi_i) - 1/3 div phi_j div phi_i)
+ *        [ B + C     0  ] [p]       B_ij = -int div(phi_j) psi_i,  C_ij = -int grad ln rho . phi_j psi_i
+ * (eq:SaddlePointStructure), used inside the Chebyshev-smoothed GMG
+ * V-cycle of the A block (fig:ASolverStructure).
+ *
+ * CONVENTIONS
+ *  - Every call returns int: 0 = HHG_OK, a negative HHG_E* code otherwise;
+ *    hhg_last_error() returns a thread-local message for the last failure.
+ *  - Handles (hhg_mesh, hhg_mg, hhg_comm) are opaque and library-owned.
+ *  - VECTORS are caller-owned DEVICE pointers to contiguous fp64 arrays in the
+ *    LIBRARY LAYOUT (below); their length comes from hhg_vec_len().  The library
+ *    never allocates in hot calls except lazily-built per-level tables on the
+ *    FIRST use of a (mesh, level) after hhg_mesh_create / blend_map / hhg_set_bc.
+ *  - Hot calls are asynchronous on the caller's cudaStream_t (pass NULL for the
+ *    legacy default stream).  Calls that return host scalars synchronise and say so.
+ *  - Outputs must not alias inputs unless stated.
+ *
+ * LIBRARY LAYOUT (hierarchical hybrid grid): every macro tet keeps its own
+ * structured tetrahedral lattice (uniform Bey refinement to level L: 8^L micro
+ * tets).  P1 lattice resolution n = 2^L, P2 lattice resolution 2n.  Points of a
+ * lattice of resolution N are ordered by (k, j, i), i+j+k <= N, with barycentric
+ * weights (N-i-j-k, i, j, k) w.r.t. the macro's vertices in ASCENDING global id
+ * order.  Nodes on macro faces/edges/vertices are REPLICATED in every macro
+ * containing them; a vector is "consistent" when all copies agree.
+ *   HHG_P1    : double[n_macro][npts(n)]
+ *   HHG_P2    : double[n_macro][npts(2n)]
+ *   HHG_P2VEC : double[3][n_macro][npts(2n)]   (component-major, x,y,z)
+ * Canonical (unique-node) order, used by hhg_to_canonical / hhg_from_canonical /
+ * hhg_canonical_keys: nodes sorted by key [dim, ascending primitive vertex ids,
+ * their positive integer weights, res] (dim 0 vertices, 1 edges, 2 faces, 3 cells);
+ * P2VEC canonical vectors are node-major with (x,y,z) interleaved.
+ *
+ * Boundary conditions: HHG_BC_DIRICHLET0 zeroes the node's
+ * velocity (block-row modification, surface no-slip); HHG_BC_FREESLIP applies
+ * P_v: u <- u - (u.n) n with n = x/|x| (CMB).  Operators return (M P_v) A u etc.;
+ * they do NOT project their input: pass constraint-consistent u (hhg_apply_bc).
+ */
+#ifndef HHG_STOKES_H
+#define HHG_STOKES_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* hhg_stream_t;   /* == cudaStream_t */
+typedef struct hhg_mesh hhg_mesh;
+typedef struct hhg_mg hhg_mg;
+typedef struct hhg_comm hhg_comm;
+
+enum {
+  HHG_OK = 0,
+  HHG_EINVAL = -1,      /* bad argument (NULL, level out of range, r_min >= r_max, ...) */
+  HHG_ELEVEL = -2,      /* space/level mismatch, non-adjacent levels */
+  HHG_ENOTREADY = -3,   /* Chebyshev without a spectrum estimate */
+  HHG_EZEROOP = -4,     /* power iteration on a zero operator */
+  HHG_EDOMAIN = -5,     /* geometry outside the blending's domain */
+  HHG_ECUDA = -6,
+  HHG_ENCCL = -7,
+  HHG_ENOMEM = -8
+};
+
+enum { HHG_P1 = 1, HHG_P2 = 2, HHG_P2VEC = 3 };
+enum { HHG_BLEND_IDENTITY = 0, HHG_BLEND_SHELL = 1 };
+enum { HHG_BND_ALL = 0, HHG_BND_INNER = 1, HHG_BND_OUTER = 2 };      /* vertex tags 1 / 2 */
+enum { HHG_BC_NONE = 0, HHG_BC_DIRICHLET0 = 1, HHG_BC_FREESLIP = 2 };
+enum { HHG_VISC_FULL = 0, HHG_VISC_EPS = 1 };
+
+/* Thread-local message describing the last error (never NULL). */
+const char* hhg_last_error(void);
+/* Library version string, build flags, the sm arch compiled for. */
+const char* hhg_version(void);
+
+/* ------------------------------------------------------------------ comm
+ * Multi-GPU (one process per GPU): an NCCL communicator over NVLink/NVSwitch.
+ * The id is created on rank 0 and broadcast by the caller (e.g. torch.distributed).
+ * comm == NULL everywhere means single GPU. */
+int hhg_comm_unique_id(uint8_t id[128]);
+int hhg_comm_create(const uint8_t id[128], int nranks, int rank, int device, hhg_comm** out);
+int hhg_comm_destroy(hhg_comm* comm);
+
+/* ------------------------------------------------------------------ mesh
+ * hhg_mesh_create: macro tets (n_tets x 4 vertex ids, any order; the
+ * library sorts each row ascending), vertex coordinates (n_vert x 3, host), vertex
+ * tags (0 interior, 1 inner/CMB, 2 outer/surface; host; NULL = all 0), refinement
+ * up to level_max (0..8).  tet_rank (host, n_tets, NULL = all local) assigns each
+ * macro to a rank of comm; this process keeps the macros with tet_rank == its rank.
+ * Errors: HHG_EINVAL (NULL, n < 1, level_max out of range, degenerate tet). */
+int hhg_mesh_create(const double* macro_xyz, int64_t n_vert, const int32_t* macro_tets, int64_t n_tets,
+                    const int32_t* vertex_tag, int level_max, const int32_t* tet_rank, hhg_comm* comm,
+                    hhg_mesh** out);
+int hhg_mesh_destroy(hhg_mesh* mesh);
+/* Number of macro tets stored by this process. */
+int hhg_mesh_local_macros(const hhg_mesh* mesh, int64_t* n);
+
+/* blend_map: HHG_BLEND_SHELL = origin-centred thick spherical
+ * shell: per macro, B(x) = c_K x (n_K . x)/|x| with n_K the unit normal of the plane
+ * through the macro's 3 distinct vertex directions and c_K = 1/(n_K . p); it maps
+ * every flat layer triangle onto its sphere and is C^0 across macros.
+ * Errors: HHG_EDOMAIN if a macro does not have exactly 3 distinct directions. */
+int blend_map(hhg_mesh* mesh, int kind);
+
+/* hhg_set_bc: boundary faces = macro faces of exactly one macro tet; a face's tag
+ * is the common tag of its 3 vertices.  tag = HHG_BND_ALL sets every boundary face. */
+int hhg_set_bc(hhg_mesh* mesh, int tag, int kind);
+
+/* Length (doubles) of a vector of `space` at `level` in the library layout. */
+int hhg_vec_len(const hhg_mesh* mesh, int level, int space, int64_t* n);
+/* Number of unique nodes (HHG_P1/HHG_P2) or unique dofs (HHG_P2VEC) in canonical order. */
+int hhg_canonical_len(const hhg_mesh* mesh, int level, int space, int64_t* n_unique);
+/* Canonical node keys, HOST int64 array [n_unique_nodes][10] =
+ * [dim, id0..id3 (-1 padded), w0..w3 (0 padded), res].  space: HHG_P1 or HHG_P2. */
+int hhg_canonical_keys(const hhg_mesh* mesh, int level, int space, int64_t* keys_host);
+/* Gather a CONSISTENT library-layout vector into canonical order (device -> device). */
+int hhg_to_canonical(const hhg_mesh* mesh, int level, int space, const double* v_dev, double* c_dev,
+                     hhg_stream_t stream);
+/* Scatter a canonical vector to all copies in the library layout (device -> device). */
+int hhg_from_canonical(const hhg_mesh* mesh, int level, int space, const double* c_dev, double* v_dev,
+                       hhg_stream_t stream);
+/* Blended physical coordinates of every stored node of a scalar space (HHG_P1 or
+ * HHG_P2): xyz_dev = double[n_stored][3]. */
+int hhg_node_coords(const hhg_mesh* mesh, int level, int space, double* xyz_dev, hhg_stream_t stream);
+
+/* ------------------------------------------------------------------ constraints / consistency
+ * hhg_apply_bc: u <- P_v M u in place (P2VEC).  hhg_interface_sum: turn a vector of
+ * per-macro partial sums into the consistent assembled vector (sum of all copies,
+ * written to every copy); for HHG_P2VEC the BCs are applied afterwards. */
+int hhg_apply_bc(const hhg_mesh* mesh, int level, double* u, hhg_stream_t stream);
+int hhg_interface_sum(const hhg_mesh* mesh, int level, int space, double* v, hhg_stream_t stream);
+
+/* ------------------------------------------------------------------ operators
+ * Results are interface-summed (consistent) and, for velocity outputs, BC-masked
+ * (M P_v ...).  eta_p1: P1 viscosity at level's vertices, NULL = 1.
+ * Quadrature: 4-point degree-2 rule on every micro tet (R6); the blending
+ * Jacobian is evaluated at each quadrature point on the fly.
+ *
+ * epsilon_apply: y = (M P_v) A(eta) u.  form HHG_VISC_FULL = the paper's A
+ *   (P:277-278 with eta on both terms, R1); HHG_VISC_EPS = int 2 eta eps:eps.
+ * div_apply:  q = (B + C) u, grad ln rho = -gamma x/|x|; gamma 0 -> B.
+ * divT_apply: y_u = (M P_v) B^T p   (accumulate != 0: y_u += ...).
+ * stokes_apply: y_u = (M P_v)(A u + B^T p), y_p = (B + C) u.
+ * hhg_diag: diag(A(eta)) WITHOUT P_v, consistent, all dofs. */
+int epsilon_apply(const hhg_mesh* mesh, int level, int form, const double* eta_p1, const double* u,
+                  double* y, hhg_stream_t stream);
+int div_apply(const hhg_mesh* mesh, int level, double gamma, const double* u, double* q,
+              hhg_stream_t stream);
+int divT_apply(const hhg_mesh* mesh, int level, const double* p, double* y_u, int accumulate,
+               hhg_stream_t stream);
+int stokes_apply(const hhg_mesh* mesh, int level, const double* eta_p1, double gamma, const double* u,
+                 const double* p, double* y_u, double* y_p, hhg_stream_t stream);
+int hhg_diag(const hhg_mesh* mesh, int level, const double* eta_p1, double* diag, hhg_stream_t stream);
+
+/* Inner product over UNIQUE dofs of two consistent vectors (each replicated node
+ * counted once), allreduced over ranks; result written to out_dev (1 double). */
+int hhg_dot(const hhg_mesh* mesh, int level, int space, const double* x, const double* y, double* out_dev,
+            hhg_stream_t stream);
+
+/* ------------------------------------------------------------------ multigrid
+ * p2_prolong: x_fine += (M P_v) P x_coarse, P = nodal P2 interpolation (exact embedding).
+ * p2_restrict: r_coarse = (M P_v) P^T r_fine  (r_fine consistent). */
+int p2_restrict(const hhg_mesh* mesh, int fine_level, const double* r_fine, double* r_coarse,
+                hhg_stream_t stream);
+int p2_prolong(const hhg_mesh* mesh, int coarse_level, const double* x_coarse, double* x_fine,
+               hhg_stream_t stream);
+
+/* chebyshev_smooth: one degree-`degree` Chebyshev sweep on D^-1 A over
+ * [lmin, lmax]: theta=(lmax+lmin)/2, delta=(lmax-lmin)/2, sigma=theta/delta, rho=1/sigma;
+ * r = rhs - A x; d = PM dinv r/theta; for k=1..deg: x += d; if k<deg: r -= A d;
+ * rho' = 1/(2 sigma - rho); d = rho' rho d + (2 rho'/delta) PM dinv r; rho = rho'.
+ * work: >= 3 P2VEC vectors.  dinv = 1/diag(A).  HHG_ENOTREADY if lmax <= 0. */
+int chebyshev_smooth(const hhg_mesh* mesh, int level, const double* eta_p1, const double* dinv, int degree,
+                     double lmin, double lmax, const double* rhs, double* x, double* work, hhg_stream_t stream);
+
+/* Power iteration for lambda_max(D^-1 A): v = PM v0; iters x { w = PM dinv A v;
+ * lambda = |w|; v = w/lambda }.  v0 (device, consistent) is overwritten.
+ * Synchronises; lambda returned on the host.  HHG_EZEROOP on a zero operator. */
+int hhg_power_iteration(const hhg_mesh* mesh, int level, const double* eta_p1, const double* dinv, int iters,
+                        double* v0, double* lambda_host, hhg_stream_t stream);
+
+typedef struct {
+  int l_min, l_max;          /* coarsest / finest level */
+  int pre, post, degree;     /* Chebyshev steps and degree (BASELINE config 3: 3, 3, 3) */
+  int power_iters;           /* 20 */
+  int coarse_iters;          /* Jacobi-PCG iterations on l_min (50) */
+  double cheb_hi_factor;     /* 1.1  (b = 1.1 lambda_hat) */
+  double cheb_lo_ratio;      /* 0.1  (a = b/10)           */
+  int visc_form;             /* HHG_VISC_FULL */
+  int use_graph;             /* capture the V-cycle in a CUDA graph */
+} hhg_mg_params;
+
+/* hhg_mg_create: builds per-level workspaces, diag(A) and D^-1, and lambda_hat per
+ * level by power iteration from the consistent start vectors power_v0[l] (device,
+ * P2VEC, may be NULL entries for l_min).  eta_per_level[l] (device P1 vectors) must
+ * stay alive while the hierarchy is used.  Synchronises. */
+int hhg_mg_create(hhg_mesh* mesh, const hhg_mg_params* params, const double* const* eta_per_level,
+                  double* const* power_v0, hhg_mg** out);
+int hhg_mg_lambda(const hhg_mg* mg, int level, double* lambda_host);
+/* One V-cycle (fig:ASolverStructure) from x = 0: x = V(rhs). */
+int vcycle(hhg_mg* mg, const double* rhs, double* x, hhg_stream_t stream);
+/* Same with HOST (pinned or pageable) rhs / x: H2D copy, V-cycle, D2H copy on `stream`. */
+int vcycle_host(hhg_mg* mg, const double* rhs_host, double* x_host, hhg_stream_t stream);
+/* Kernel timing of the fine-level element kernel inside vcycle (CUDA events on the
+ * launching stream; disables graph capture while on).  get: sum of ms and count. */
+int hhg_mg_profile(hhg_mg* mg, int enable);
+int hhg_mg_profile_get(hhg_mg* mg, double* apply_ms_sum, int64_t* apply_count, double* cycle_ms_sum,
+                       int64_t* cycle_count);
+int hhg_mg_destroy(hhg_mg* mg);
+
+/* Number of kernels launched by the library on this thread since the last reset. */
+int64_t hhg_launch_count(int reset);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HHG_STOKES_H */

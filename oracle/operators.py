@@ -178,6 +178,51 @@ class Discretisation:
         return m
 
 
+def node_coords(lm: LevelMesh, space: str, blended: bool) -> np.ndarray:
+    """Physical (blended) coordinates of the canonical nodes: B(x~) evaluated with the blending
+    parameters of one macro containing the node (B is C^0 across macros)."""
+    xt = lm.p2_xt if space == "P2" else lm.p1_xt
+    if not blended:
+        return xt.copy()
+    tet_nodes = lm.tet_p2 if space == "P2" else lm.tet_p1
+    first_tet = np.full(xt.shape[0], -1, dtype=np.int64)
+    flat = tet_nodes.ravel()
+    order = np.arange(flat.size)[::-1]
+    first_tet[flat[order]] = order // tet_nodes.shape[1]
+    nhat, c = macro_blend(lm)
+    mac = lm.tet_macro[first_tet]
+    return fe.blend(xt, nhat[mac], c[mac])
+
+
+def sampled_rows(lm: LevelMesh, blended, eta_p1, gamma, u, p, nodes_p2, nodes_p1, bc, form=FORM_FULL):
+    """Rows of y_u = (M P_v)(A u + B^T p) at P2 nodes `nodes_p2` and of y_p = (B + C) u at P1 nodes
+    `nodes_p1`, from the element matrices of only the micro tets touching them (same definitions
+    as Discretisation; u must already be constraint-consistent, canonical numbering of lm)."""
+    bp = macro_blend(lm) if blended else None
+    want2 = np.zeros(lm.n_p2, dtype=bool)
+    want2[nodes_p2] = True
+    want1 = np.zeros(lm.n_p1, dtype=bool)
+    want1[nodes_p1] = True
+    tets = np.nonzero(want2[lm.tet_p2].any(axis=1) | want1[lm.tet_p1].any(axis=1))[0]
+    yu = np.zeros(3 * lm.n_p2)
+    yp = np.zeros(lm.n_p1)
+    xi, _ = fe.q4_rule()
+    for s in range(0, len(tets), 20000):
+        tt = tets[s:s + 20000]
+        W, grads, xq = quad_geometry(lm, tt, blended, bp)
+        vd = p2vec_dofs(lm.tet_p2[tt])
+        pd = lm.tet_p1[tt]
+        eta_q = eta_p1[pd] @ fe.p1_basis(xi).T
+        Ae = element_A(W, grads, eta_q, form)
+        Be = element_B(W, grads)
+        Ce = element_C(W, xq, gamma) if gamma != 0.0 else 0.0 * Be
+        ue = u[vd]
+        np.add.at(yu, vd, np.einsum("tij,tj->ti", Ae, ue) + np.einsum("tpi,tp->ti", Be, p[pd]))
+        np.add.at(yp, pd, np.einsum("tpj,tj->tp", Be + Ce, ue))
+    Pm = constraint_matrix(lm.p2_xt, bc)
+    return Pm @ yu, yp
+
+
 def _coo(E, rows, cols, nr, nc):
     T, a, b = E.shape
     r = np.broadcast_to(rows[:, :, None], (T, a, b))

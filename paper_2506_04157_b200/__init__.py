@@ -1,0 +1,343 @@
+"""Thin ctypes binding of libhhgstokes.so (include/hhg_stokes.h) -- argument marshalling only.
+
+Every step of the hot path runs in the library's sm_100a kernels; PyTorch supplies device
+memory (tensors), the current CUDA stream and process groups.  There is NO CPU fallback:
+importing this package raises if the shared library is missing, and every call raises
+``HHGError`` with the library's message on failure.
+
+Names follow the C-ABI (and the paper's notation): ``hhg_mesh_create`` -> ``Mesh``,
+``blend_map``, ``epsilon_apply``, ``div_apply``, ``divT_apply``, ``stokes_apply``,
+``hhg_diag``, ``hhg_dot``, ``p2_restrict``, ``p2_prolong``, ``chebyshev_smooth``,
+``hhg_power_iteration``, ``MG`` (``hhg_mg_create``) with ``vcycle``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libhhgstokes.so")
+
+HHG_P1, HHG_P2, HHG_P2VEC = 1, 2, 3
+HHG_BLEND_IDENTITY, HHG_BLEND_SHELL = 0, 1
+HHG_BND_ALL, HHG_BND_INNER, HHG_BND_OUTER = 0, 1, 2
+HHG_BC_NONE, HHG_BC_DIRICHLET0, HHG_BC_FREESLIP = 0, 1, 2
+HHG_VISC_FULL, HHG_VISC_EPS = 0, 1
+
+ERRORS = {-1: "HHG_EINVAL", -2: "HHG_ELEVEL", -3: "HHG_ENOTREADY", -4: "HHG_EZEROOP", -5: "HHG_EDOMAIN",
+          -6: "HHG_ECUDA", -7: "HHG_ENCCL", -8: "HHG_ENOMEM"}
+
+# every symbol declared in include/hhg_stokes.h
+EXPORTS = [
+    "hhg_last_error", "hhg_version", "hhg_comm_unique_id", "hhg_comm_create", "hhg_comm_destroy",
+    "hhg_mesh_create", "hhg_mesh_destroy", "hhg_mesh_local_macros", "blend_map", "hhg_set_bc",
+    "hhg_vec_len", "hhg_canonical_len", "hhg_canonical_keys", "hhg_to_canonical", "hhg_from_canonical",
+    "hhg_node_coords", "hhg_apply_bc", "hhg_interface_sum", "epsilon_apply", "div_apply", "divT_apply",
+    "stokes_apply", "hhg_diag", "hhg_dot", "p2_restrict", "p2_prolong", "chebyshev_smooth",
+    "hhg_power_iteration", "hhg_mg_create", "hhg_mg_lambda", "vcycle", "vcycle_host", "hhg_mg_profile",
+    "hhg_mg_profile_get", "hhg_mg_destroy", "hhg_launch_count",
+]
+
+
+class HHGError(RuntimeError):
+    pass
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libhhgstokes.so not built ({LIB_PATH}); run `python __graft_entry__.py build` "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    P, I, I64, D = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double
+    sig = {
+        "hhg_last_error": ([], ctypes.c_char_p), "hhg_version": ([], ctypes.c_char_p),
+        "hhg_launch_count": ([I], I64),
+        "hhg_comm_unique_id": ([P], I), "hhg_comm_create": ([P, I, I, I, P], I), "hhg_comm_destroy": ([P], I),
+        "hhg_mesh_create": ([P, I64, P, I64, P, I, P, P, P], I), "hhg_mesh_destroy": ([P], I),
+        "hhg_mesh_local_macros": ([P, P], I), "blend_map": ([P, I], I), "hhg_set_bc": ([P, I, I], I),
+        "hhg_vec_len": ([P, I, I, P], I), "hhg_canonical_len": ([P, I, I, P], I),
+        "hhg_canonical_keys": ([P, I, I, P], I), "hhg_to_canonical": ([P, I, I, P, P, P], I),
+        "hhg_from_canonical": ([P, I, I, P, P, P], I), "hhg_node_coords": ([P, I, I, P, P], I),
+        "hhg_apply_bc": ([P, I, P, P], I), "hhg_interface_sum": ([P, I, I, P, P], I),
+        "epsilon_apply": ([P, I, I, P, P, P, P], I), "div_apply": ([P, I, D, P, P, P], I),
+        "divT_apply": ([P, I, P, P, I, P], I), "stokes_apply": ([P, I, P, D, P, P, P, P, P], I),
+        "hhg_diag": ([P, I, P, P, P], I), "hhg_dot": ([P, I, I, P, P, P, P], I),
+        "p2_restrict": ([P, I, P, P, P], I), "p2_prolong": ([P, I, P, P, P], I),
+        "chebyshev_smooth": ([P, I, P, P, I, D, D, P, P, P, P], I),
+        "hhg_power_iteration": ([P, I, P, P, I, P, P, P], I),
+        "hhg_mg_create": ([P, P, P, P, P], I), "hhg_mg_lambda": ([P, I, P], I), "vcycle": ([P, P, P, P], I),
+        "vcycle_host": ([P, P, P, P], I), "hhg_mg_profile": ([P, I], I),
+        "hhg_mg_profile_get": ([P, P, P, P, P], I), "hhg_mg_destroy": ([P], I),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = res
+    return lib
+
+
+_lib = _load()
+
+
+def lib():
+    return _lib
+
+
+def _chk(rc):
+    if rc != 0:
+        raise HHGError(f"{ERRORS.get(rc, rc)}: {_lib.hhg_last_error().decode()}")
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if isinstance(t, np.ndarray):
+        return t.ctypes.data
+    return t.data_ptr()
+
+
+def _dev(t, n=None, name="tensor"):
+    import torch
+    if t is None:
+        return None
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+        raise HHGError(f"{name}: need a contiguous float64 CUDA tensor")
+    if n is not None and t.numel() != n:
+        raise HHGError(f"{name}: length {t.numel()} != expected {n}")
+    return t.data_ptr()
+
+
+def _stream(stream=None):
+    import torch
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def version() -> str:
+    return _lib.hhg_version().decode()
+
+
+def launch_count(reset=False) -> int:
+    return int(_lib.hhg_launch_count(1 if reset else 0))
+
+
+class Mesh:
+    """hhg_mesh_create + blend_map + hhg_set_bc (macro tets uniformly refined to level_max)."""
+
+    def __init__(self, verts, tets, vtag=None, level_max=4, tet_rank=None, comm=None):
+        v = np.ascontiguousarray(verts, dtype=np.float64)
+        t = np.ascontiguousarray(tets, dtype=np.int32)
+        g = None if vtag is None else np.ascontiguousarray(vtag, dtype=np.int32)
+        r = None if tet_rank is None else np.ascontiguousarray(tet_rank, dtype=np.int32)
+        h = ctypes.c_void_p()
+        _chk(_lib.hhg_mesh_create(_ptr(v), v.shape[0], _ptr(t), t.shape[0], _ptr(g), int(level_max), _ptr(r),
+                                  None if comm is None else comm.handle, ctypes.byref(h)))
+        self.handle = h
+        self.level_max = level_max
+
+    @classmethod
+    def from_macro(cls, macro, level_max, **kw):
+        return cls(macro.verts, macro.tets, macro.vtag, level_max, **kw)
+
+    def __del__(self):
+        if getattr(self, "handle", None):
+            _lib.hhg_mesh_destroy(self.handle)
+            self.handle = None
+
+    def blend_map(self, kind=HHG_BLEND_SHELL):
+        _chk(_lib.blend_map(self.handle, kind))
+        return self
+
+    def set_bc(self, tag, kind):
+        _chk(_lib.hhg_set_bc(self.handle, tag, kind))
+        return self
+
+    def vec_len(self, level, space):
+        n = ctypes.c_int64()
+        _chk(_lib.hhg_vec_len(self.handle, level, space, ctypes.byref(n)))
+        return n.value
+
+    def canonical_len(self, level, space):
+        n = ctypes.c_int64()
+        _chk(_lib.hhg_canonical_len(self.handle, level, space, ctypes.byref(n)))
+        return n.value
+
+    def canonical_keys(self, level, space):
+        n = self.canonical_len(level, space)
+        keys = np.empty((n, 10), dtype=np.int64)
+        _chk(_lib.hhg_canonical_keys(self.handle, level, space, _ptr(keys)))
+        return keys
+
+    def zeros(self, level, space):
+        import torch
+        return torch.zeros(self.vec_len(level, space), dtype=torch.float64, device="cuda")
+
+    def to_canonical(self, level, space, v, stream=None):
+        import torch
+        out = torch.empty(self.canonical_len(level, space), dtype=torch.float64, device="cuda")
+        _chk(_lib.hhg_to_canonical(self.handle, level, space, _dev(v, self.vec_len(level, space)), _dev(out),
+                                   _stream(stream)))
+        return out
+
+    def from_canonical(self, level, space, c, stream=None):
+        import torch
+        c = torch.as_tensor(c, dtype=torch.float64).cuda().contiguous()
+        out = self.zeros(level, space)
+        _chk(_lib.hhg_from_canonical(self.handle, level, space, _dev(c, self.canonical_len(level, space)),
+                                     _dev(out), _stream(stream)))
+        return out
+
+    def node_coords(self, level, space, stream=None):
+        import torch
+        n = self.vec_len(level, space)
+        out = torch.empty((n, 3), dtype=torch.float64, device="cuda")
+        _chk(_lib.hhg_node_coords(self.handle, level, space, _dev(out), _stream(stream)))
+        return out
+
+    def apply_bc(self, level, u, stream=None):
+        _chk(_lib.hhg_apply_bc(self.handle, level, _dev(u, self.vec_len(level, HHG_P2VEC)), _stream(stream)))
+        return u
+
+    def interface_sum(self, level, space, v, stream=None):
+        _chk(_lib.hhg_interface_sum(self.handle, level, space, _dev(v, self.vec_len(level, space)), _stream(stream)))
+        return v
+
+    def local_macros(self):
+        n = ctypes.c_int64()
+        _chk(_lib.hhg_mesh_local_macros(self.handle, ctypes.byref(n)))
+        return n.value
+
+
+def epsilon_apply(mesh, level, eta, u, y=None, form=HHG_VISC_FULL, stream=None):
+    n = mesh.vec_len(level, HHG_P2VEC)
+    y = mesh.zeros(level, HHG_P2VEC) if y is None else y
+    _chk(_lib.epsilon_apply(mesh.handle, level, form, _dev(eta, mesh.vec_len(level, HHG_P1), "eta"),
+                            _dev(u, n, "u"), _dev(y, n, "y"), _stream(stream)))
+    return y
+
+
+def div_apply(mesh, level, gamma, u, q=None, stream=None):
+    q = mesh.zeros(level, HHG_P1) if q is None else q
+    _chk(_lib.div_apply(mesh.handle, level, float(gamma), _dev(u, mesh.vec_len(level, HHG_P2VEC), "u"),
+                        _dev(q, mesh.vec_len(level, HHG_P1), "q"), _stream(stream)))
+    return q
+
+
+def divT_apply(mesh, level, p, y=None, accumulate=False, stream=None):
+    y = mesh.zeros(level, HHG_P2VEC) if y is None else y
+    _chk(_lib.divT_apply(mesh.handle, level, _dev(p, mesh.vec_len(level, HHG_P1), "p"),
+                         _dev(y, mesh.vec_len(level, HHG_P2VEC), "y"), 1 if accumulate else 0, _stream(stream)))
+    return y
+
+
+def stokes_apply(mesh, level, eta, gamma, u, p, y_u=None, y_p=None, stream=None):
+    y_u = mesh.zeros(level, HHG_P2VEC) if y_u is None else y_u
+    y_p = mesh.zeros(level, HHG_P1) if y_p is None else y_p
+    n2, n1 = mesh.vec_len(level, HHG_P2VEC), mesh.vec_len(level, HHG_P1)
+    _chk(_lib.stokes_apply(mesh.handle, level, _dev(eta, n1, "eta"), float(gamma), _dev(u, n2, "u"), _dev(p, n1, "p"),
+                           _dev(y_u, n2, "y_u"), _dev(y_p, n1, "y_p"), _stream(stream)))
+    return y_u, y_p
+
+
+def hhg_diag(mesh, level, eta, out=None, stream=None):
+    out = mesh.zeros(level, HHG_P2VEC) if out is None else out
+    _chk(_lib.hhg_diag(mesh.handle, level, _dev(eta, mesh.vec_len(level, HHG_P1), "eta"),
+                       _dev(out, mesh.vec_len(level, HHG_P2VEC)), _stream(stream)))
+    return out
+
+
+def hhg_dot(mesh, level, space, x, y, stream=None):
+    import torch
+    out = torch.zeros(1, dtype=torch.float64, device="cuda")
+    n = mesh.vec_len(level, space)
+    _chk(_lib.hhg_dot(mesh.handle, level, space, _dev(x, n), _dev(y, n), _dev(out), _stream(stream)))
+    return out
+
+
+def p2_restrict(mesh, fine_level, r_fine, r_coarse=None, stream=None):
+    r_coarse = mesh.zeros(fine_level - 1, HHG_P2VEC) if r_coarse is None else r_coarse
+    _chk(_lib.p2_restrict(mesh.handle, fine_level, _dev(r_fine, mesh.vec_len(fine_level, HHG_P2VEC)),
+                          _dev(r_coarse, mesh.vec_len(fine_level - 1, HHG_P2VEC)), _stream(stream)))
+    return r_coarse
+
+
+def p2_prolong(mesh, coarse_level, x_coarse, x_fine, stream=None):
+    _chk(_lib.p2_prolong(mesh.handle, coarse_level, _dev(x_coarse, mesh.vec_len(coarse_level, HHG_P2VEC)),
+                         _dev(x_fine, mesh.vec_len(coarse_level + 1, HHG_P2VEC)), _stream(stream)))
+    return x_fine
+
+
+def chebyshev_smooth(mesh, level, eta, dinv, degree, lmin, lmax, rhs, x, work=None, stream=None):
+    import torch
+    n = mesh.vec_len(level, HHG_P2VEC)
+    work = torch.empty(3 * n, dtype=torch.float64, device="cuda") if work is None else work
+    _chk(_lib.chebyshev_smooth(mesh.handle, level, _dev(eta, mesh.vec_len(level, HHG_P1), "eta"), _dev(dinv, n),
+                               int(degree), float(lmin), float(lmax), _dev(rhs, n), _dev(x, n), _dev(work),
+                               _stream(stream)))
+    return x
+
+
+def hhg_power_iteration(mesh, level, eta, dinv, iters, v0, stream=None):
+    n = mesh.vec_len(level, HHG_P2VEC)
+    lam = ctypes.c_double()
+    _chk(_lib.hhg_power_iteration(mesh.handle, level, _dev(eta, mesh.vec_len(level, HHG_P1), "eta"), _dev(dinv, n),
+                                  int(iters), _dev(v0, n), ctypes.byref(lam), _stream(stream)))
+    return lam.value
+
+
+class _MGParams(ctypes.Structure):
+    _fields_ = [("l_min", ctypes.c_int), ("l_max", ctypes.c_int), ("pre", ctypes.c_int), ("post", ctypes.c_int),
+                ("degree", ctypes.c_int), ("power_iters", ctypes.c_int), ("coarse_iters", ctypes.c_int),
+                ("cheb_hi_factor", ctypes.c_double), ("cheb_lo_ratio", ctypes.c_double),
+                ("visc_form", ctypes.c_int), ("use_graph", ctypes.c_int)]
+
+
+class MG:
+    """hhg_mg_create: per-level D^-1 and lambda_hat; vcycle() applies one V-cycle."""
+
+    def __init__(self, mesh, l_min, l_max, eta_per_level, power_v0, pre=3, post=3, degree=3, power_iters=20,
+                 coarse_iters=50, hi=1.1, lo=0.1, form=HHG_VISC_FULL, use_graph=True):
+        self.mesh = mesh
+        self.l_min, self.l_max = l_min, l_max
+        prm = _MGParams(l_min, l_max, pre, post, degree, power_iters, coarse_iters, hi, lo, form,
+                        1 if use_graph else 0)
+        self._eta = dict(eta_per_level)
+        self._v0 = dict(power_v0)
+        L = l_max + 1
+        etas = (ctypes.c_void_p * L)(*[_ptr(self._eta.get(l)) for l in range(L)])
+        v0s = (ctypes.c_void_p * L)(*[_ptr(self._v0.get(l)) for l in range(L)])
+        h = ctypes.c_void_p()
+        _chk(_lib.hhg_mg_create(mesh.handle, ctypes.byref(prm), etas, v0s, ctypes.byref(h)))
+        self.handle = h
+
+    def __del__(self):
+        if getattr(self, "handle", None):
+            _lib.hhg_mg_destroy(self.handle)
+            self.handle = None
+
+    def lam(self, level):
+        v = ctypes.c_double()
+        _chk(_lib.hhg_mg_lambda(self.handle, level, ctypes.byref(v)))
+        return v.value
+
+    def vcycle(self, rhs, x=None, stream=None):
+        n = self.mesh.vec_len(self.l_max, HHG_P2VEC)
+        x = self.mesh.zeros(self.l_max, HHG_P2VEC) if x is None else x
+        _chk(_lib.vcycle(self.handle, _dev(rhs, n, "rhs"), _dev(x, n, "x"), _stream(stream)))
+        return x
+
+    def vcycle_host(self, rhs_host, x_host, stream=None):
+        _chk(_lib.vcycle_host(self.handle, _ptr(rhs_host), _ptr(x_host), _stream(stream)))
+        return x_host
+
+    def profile(self, enable=True):
+        _chk(_lib.hhg_mg_profile(self.handle, 1 if enable else 0))
+
+    def profile_get(self):
+        a, c = ctypes.c_double(), ctypes.c_double()
+        na, nc = ctypes.c_int64(), ctypes.c_int64()
+        _chk(_lib.hhg_mg_profile_get(self.handle, ctypes.byref(a), ctypes.byref(na), ctypes.byref(c),
+                                     ctypes.byref(nc)))
+        return dict(apply_ms_sum=a.value, apply_count=na.value, cycle_ms_sum=c.value, cycle_count=nc.value)

@@ -1,0 +1,142 @@
+// Internal data structures of libhhgstokes (not part of the C-ABI).
+#pragma once
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+#include <array>
+#include <cuda_runtime.h>
+
+#include "../../include/hhg_stokes.h"
+
+namespace hhg {
+
+// ---------------------------------------------------------------- errors
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+#define HHG_CUDA(call)                                                                   \
+  do {                                                                                   \
+    cudaError_t _e = (call);                                                             \
+    if (_e != cudaSuccess)                                                               \
+      return ::hhg::fail(HHG_ECUDA, std::string(#call) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+#define HHG_TRY(expr)            \
+  do {                           \
+    int _r = (expr);             \
+    if (_r != HHG_OK) return _r; \
+  } while (0)
+
+void count_launch(int n = 1);
+
+// ---------------------------------------------------------------- lattice helpers
+__host__ __device__ inline int64_t npts3(int64_t N) { return (N + 1) * (N + 2) * (N + 3) / 6; }
+__host__ __device__ inline int64_t tri(int64_t m) { return (m + 1) * (m + 2) / 2; }
+// index of (i,j,k), i+j+k <= N, ordered by k, then j, then i
+__host__ __device__ inline int64_t lidx(int i, int j, int k, int N) {
+  return npts3(N) - npts3(N - k) + tri(N - k) - tri(N - k - j) + i;
+}
+
+// ---------------------------------------------------------------- per-macro data
+// Device POD per macro (local numbering).  Jm columns = X1-X0, X2-X0, X3-X0 (row-major
+// Jm[3*r+c]); vertex order = ascending global id.
+struct MacroGeo {
+  double X0[3];
+  double Jm[9];
+  double Jminv[9];
+  double absdet;    // |det Jm|
+  double nhat[3];   // blending normal
+  double cK;        // blending factor (0 = identity blending)
+};
+
+// per-level, per-macro, per-tet-type element geometry (device)
+// 6 types x (JFinv[9] + qoff[4][3]) + absdetF
+constexpr int kTypeGeo = 9 + 12;
+constexpr int kLevelGeo = 6 * kTypeGeo + 2;  // + absdetF + pad
+
+struct Groups {           // replicated-node groups (interface and/or boundary nodes)
+  int64_t n = 0;          // number of groups
+  int64_t* ptr = nullptr; // [n+1] into copy
+  int64_t* copy = nullptr;// scalar flat indices (macro*npts + idx)
+  uint8_t* kind = nullptr;// BC kind per group (P2 only)
+  double* normal = nullptr;// [n][3] (P2 only)
+  int64_t ncopy = 0;
+};
+
+struct Level {
+  int level = 0;
+  int n1 = 0, n2 = 0;               // P1 / P2 lattice resolution
+  int64_t npts1 = 0, npts2 = 0;     // per macro
+  double* geo = nullptr;            // [n_macro][kLevelGeo]
+  int32_t* anchors[3] = {nullptr, nullptr, nullptr};  // s<=n-1, s<=n-2, s<=n-3, packed i|j<<10|k<<20
+  int64_t n_anchor[3] = {0, 0, 0};
+  int32_t* rows1 = nullptr;         // packed (j | k<<16) for P1 rows
+  int32_t* rows2 = nullptr;         // packed rows for P2
+  int64_t nrows1 = 0, nrows2 = 0;
+  Groups g1, g2;                    // P1 interface groups, P2 interface+BC groups
+  uint8_t* own1 = nullptr;          // owner mask per stored P1 node
+  uint8_t* own2 = nullptr;          // owner mask per stored P2 node
+  int64_t* canon1 = nullptr;        // canonical node index per stored node (lazy)
+  int64_t* canon2 = nullptr;
+  int64_t ncanon1 = 0, ncanon2 = 0;
+  double* red = nullptr;            // reduction scratch [kRedBlocks + 8]
+  bool built = false;
+};
+
+constexpr int kRedBlocks = 296;     // 2 x 148 SMs
+
+struct Mesh {
+  // global macro mesh (host)
+  int64_t n_vert = 0, n_tets = 0;
+  std::vector<double> xyz;          // [n_vert][3]
+  std::vector<int32_t> tets;        // [n_tets][4] ascending
+  std::vector<int32_t> vtag;
+  std::vector<int32_t> tet_rank;
+  int level_max = 0;
+  int rank = 0, nranks = 1;
+  hhg_comm* comm = nullptr;
+  std::vector<int64_t> local;       // global ids of local macros
+  int blend = HHG_BLEND_IDENTITY;
+  int bc_kind[3] = {HHG_BC_NONE, HHG_BC_NONE, HHG_BC_NONE};  // untagged, inner, outer
+  std::vector<MacroGeo> hgeo;       // host copy, local macros
+  MacroGeo* dgeo = nullptr;         // device
+  bool dgeo_dirty = true;
+  std::vector<Level> levels;
+  int device = 0;
+  ~Mesh();
+};
+
+int ensure_level(Mesh* m, int level);
+int ensure_device_geo(Mesh* m);
+int ensure_canon(Mesh* m, int level, int space);
+void free_level(Level& L);
+int64_t macro_count(const Mesh* m);
+
+// ---------------------------------------------------------------- kernel launchers (hhg_kernels.cu)
+int launch_elem(const Mesh* m, const Level& L, int mode, int form, const double* eta, double gamma,
+                const double* u, const double* p, double* yu, double* yp, cudaStream_t s);
+enum { ELEM_A = 1, ELEM_BT = 2, ELEM_DIV = 4, ELEM_DIAG = 8 };
+int launch_fixup(const Mesh* m, const Level& L, int space, bool sum, bool bc, double* v, cudaStream_t s);
+int launch_dot(const Mesh* m, const Level& L, int space, const double* x, const double* y, double* out,
+               cudaStream_t s);
+int launch_prolong(const Mesh* m, const Level& Lc, const Level& Lf, const double* xc, double* xf,
+                   cudaStream_t s);
+int launch_restrict(const Mesh* m, const Level& Lc, const Level& Lf, const double* rf, double* rc,
+                    cudaStream_t s);
+int launch_coords(const Mesh* m, const Level& L, int space, double* xyz, cudaStream_t s);
+int launch_gather_canon(const Level& L, int space, int64_t nstored, const double* v, double* c, bool to,
+                        cudaStream_t s);
+// vector kernels for smoothers
+int launch_axpby(int64_t n, double a, const double* x, double b, double* y, cudaStream_t s);  // y = a x + b y
+int launch_cheb0(int64_t n, const double* f, const double* t, const double* dinv, double inv_theta,
+                 double* r, double* d, cudaStream_t s);  // r = f - t ; d = dinv r / theta
+int launch_chebk(int64_t n, const double* t, const double* dinv, double c1, double c2, double* x, double* r,
+                 double* d, cudaStream_t s);            // x += d; r -= t; d = c1 d + c2 dinv r
+int launch_pcg_update(int64_t n, const double* scal, double* x, double* r, const double* p, const double* q,
+                      const double* dinv, double* z, cudaStream_t s);
+int launch_scalar_ops(int op, double* scal, cudaStream_t s);
+
+}  // namespace hhg
+
+struct hhg_mesh : public hhg::Mesh {};

@@ -1,0 +1,407 @@
+// GMG V-cycle for the A block (fig:ASolverStructure): Chebyshev smoothing with the
+// inverse diagonal, P2 transfers with projections, coarse Jacobi-PCG (BASELINE
+// config 3; replaces the paper's AMG-CG of P:443), power-iteration spectrum estimate.
+// All scalars of the PCG stay on the device so the whole cycle can be captured in one CUDA graph.
+#include <cmath>
+#include <vector>
+
+#include "hhg_internal.h"
+
+namespace hhg {
+int apply_op(const Mesh* m, int level, int mode, int form, const double* eta, double gamma, const double* u,
+             const double* p, double* yu, double* yp, bool accumulate_u, cudaStream_t s);
+int launch_pcg_dir(int64_t n, double* scal, const double* z, double* p, cudaStream_t s);
+
+__global__ void k_recip(int64_t n, const double* __restrict__ d, double* __restrict__ o) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    o[i] = 1.0 / d[i];
+}
+__global__ void k_sub(int64_t n, const double* __restrict__ f, const double* __restrict__ t, double* __restrict__ r) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    r[i] = f[i] - t[i];
+}
+__global__ void k_scale_dinv(int64_t n, const double* __restrict__ t, const double* __restrict__ dinv,
+                             double* __restrict__ z) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    z[i] = dinv[i] * t[i];
+}
+__global__ void k_normalize(int64_t n, const double* __restrict__ sq, const double* __restrict__ z,
+                            double* __restrict__ v) {
+  const double inv = 1.0 / sqrt(*sq);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    v[i] = z[i] * inv;
+}
+static inline unsigned vg(int64_t n) {
+  int64_t b = (n + 255) / 256;
+  return (unsigned)(b < 2368 ? (b < 1 ? 1 : b) : 2368);
+}
+
+static int64_t p2vec_len(const Mesh* m, int level) { return 3 * macro_count(m) * m->levels[level].npts2; }
+
+// one Chebyshev sweep; x_is_zero lets the first residual skip A*0
+static int cheb_sweep(const Mesh* m, int l, int form, const double* eta, const double* dinv, int degree, double lmin,
+                      double lmax, const double* f, double* x, double* r, double* d, double* t, bool x_is_zero,
+                      cudaStream_t s) {
+  const Level& L = m->levels[l];
+  const int64_t n = p2vec_len(m, l);
+  const double theta = 0.5 * (lmax + lmin), delta = 0.5 * (lmax - lmin);
+  const double sigma = theta / delta;
+  double rho = 1.0 / sigma;
+  if (x_is_zero) {
+    HHG_CUDA(cudaMemsetAsync(t, 0, n * sizeof(double), s));
+  } else {
+    HHG_TRY(apply_op(m, l, ELEM_A, form, eta, 0.0, x, nullptr, t, nullptr, false, s));
+  }
+  HHG_TRY(launch_cheb0(n, f, t, dinv, 1.0 / theta, r, d, s));
+  HHG_TRY(launch_fixup(m, L, HHG_P2VEC, false, true, d, s));
+  for (int k = 1; k <= degree; ++k) {
+    if (k < degree) {
+      HHG_TRY(apply_op(m, l, ELEM_A, form, eta, 0.0, d, nullptr, t, nullptr, false, s));
+      const double rn = 1.0 / (2.0 * sigma - rho);
+      HHG_TRY(launch_chebk(n, t, dinv, rn * rho, 2.0 * rn / delta, x, r, d, s));
+      HHG_TRY(launch_fixup(m, L, HHG_P2VEC, false, true, d, s));
+      rho = rn;
+    } else {
+      HHG_TRY(launch_axpby(n, 1.0, d, 1.0, x, s));
+    }
+  }
+  return HHG_OK;
+}
+
+}  // namespace hhg
+
+using namespace hhg;
+
+struct hhg_mg {
+  hhg_mesh* mesh = nullptr;
+  hhg_mg_params prm{};
+  struct Lv {
+    double *x = nullptr, *f = nullptr, *r = nullptr, *d = nullptr, *t = nullptr, *dinv = nullptr, *p = nullptr;
+    const double* eta = nullptr;
+    double lam = 0.0;
+  };
+  std::vector<Lv> lv;
+  double* scal = nullptr;    // device scalars
+  double* hbuf_rhs = nullptr;  // device staging for vcycle_host
+  double* hbuf_x = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  const double* g_rhs = nullptr;
+  double* g_x = nullptr;
+  cudaStream_t g_stream = nullptr;
+  // profiling
+  bool prof = false;
+  std::vector<cudaEvent_t> ev;
+  size_t ev_used = 0;
+  double apply_ms = 0, cycle_ms = 0;
+  int64_t apply_n = 0, cycle_n = 0;
+  ~hhg_mg() {
+    for (auto& L : lv)
+      for (double* p : {L.x, L.f, L.r, L.d, L.t, L.dinv, L.p})
+        if (p) cudaFree(p);
+    if (scal) cudaFree(scal);
+    if (hbuf_rhs) cudaFree(hbuf_rhs);
+    if (hbuf_x) cudaFree(hbuf_x);
+    if (gexec) cudaGraphExecDestroy(gexec);
+    for (auto e : ev) cudaEventDestroy(e);
+  }
+};
+
+static int mg_apply(hhg_mg* mg, int l, const double* u, double* y, cudaStream_t s) {
+  const bool timed = mg->prof && l == mg->prm.l_max;
+  if (timed) {
+    if (mg->ev_used + 2 > mg->ev.size()) {
+      for (int i = 0; i < 64; ++i) {
+        cudaEvent_t e;
+        HHG_CUDA(cudaEventCreate(&e));
+        mg->ev.push_back(e);
+      }
+    }
+  }
+  // y = (M P_v) A u : zero, element kernel (timed alone when profiling), interface sum + BC
+  const Level& L = mg->mesh->levels[l];
+  HHG_CUDA(cudaMemsetAsync(y, 0, p2vec_len(mg->mesh, l) * sizeof(double), s));
+  if (timed) HHG_CUDA(cudaEventRecord(mg->ev[mg->ev_used], s));
+  HHG_TRY(launch_elem(mg->mesh, L, ELEM_A, mg->prm.visc_form, mg->lv[l].eta, 0.0, u, nullptr, y, nullptr, s));
+  if (timed) {
+    HHG_CUDA(cudaEventRecord(mg->ev[mg->ev_used + 1], s));
+    mg->ev_used += 2;
+  }
+  return launch_fixup(mg->mesh, L, HHG_P2VEC, true, true, y, s);
+}
+
+static int mg_cheb(hhg_mg* mg, int l, double* x, const double* f, bool x_is_zero, cudaStream_t s) {
+  auto& L = mg->lv[l];
+  const Mesh* m = mg->mesh;
+  const int64_t n = p2vec_len(m, l);
+  const double b = mg->prm.cheb_hi_factor * L.lam, a = mg->prm.cheb_lo_ratio * b;
+  const double theta = 0.5 * (b + a), delta = 0.5 * (b - a), sigma = theta / delta;
+  double rho = 1.0 / sigma;
+  const Level& LL = m->levels[l];
+  if (x_is_zero) {
+    HHG_CUDA(cudaMemsetAsync(L.t, 0, n * sizeof(double), s));
+  } else {
+    HHG_TRY(mg_apply(mg, l, x, L.t, s));
+  }
+  HHG_TRY(launch_cheb0(n, f, L.t, L.dinv, 1.0 / theta, L.r, L.d, s));
+  HHG_TRY(launch_fixup(m, LL, HHG_P2VEC, false, true, L.d, s));
+  for (int k = 1; k <= mg->prm.degree; ++k) {
+    if (k < mg->prm.degree) {
+      HHG_TRY(mg_apply(mg, l, L.d, L.t, s));
+      const double rn = 1.0 / (2.0 * sigma - rho);
+      HHG_TRY(launch_chebk(n, L.t, L.dinv, rn * rho, 2.0 * rn / delta, x, L.r, L.d, s));
+      HHG_TRY(launch_fixup(m, LL, HHG_P2VEC, false, true, L.d, s));
+      rho = rn;
+    } else {
+      HHG_TRY(launch_axpby(n, 1.0, L.d, 1.0, x, s));
+    }
+  }
+  return HHG_OK;
+}
+
+static int mg_pcg(hhg_mg* mg, int l, const double* f, double* x, cudaStream_t s) {
+  auto& L = mg->lv[l];
+  const Mesh* m = mg->mesh;
+  const Level& LL = m->levels[l];
+  const int64_t n = p2vec_len(m, l);
+  double* r = L.r;
+  double* z = L.d;
+  double* p = L.p;
+  double* q = L.t;
+  HHG_CUDA(cudaMemsetAsync(x, 0, n * sizeof(double), s));
+  HHG_CUDA(cudaMemcpyAsync(r, f, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  HHG_TRY(launch_cheb0(n, f, x, L.dinv, 1.0, r, z, s));  // r = f - 0, z = dinv r
+  HHG_TRY(launch_fixup(m, LL, HHG_P2VEC, false, true, z, s));
+  HHG_CUDA(cudaMemcpyAsync(p, z, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  HHG_TRY(launch_dot(m, LL, HHG_P2VEC, r, z, mg->scal + 0, s));
+  for (int it = 0; it < mg->prm.coarse_iters; ++it) {
+    HHG_TRY(mg_apply(mg, l, p, q, s));
+    HHG_TRY(launch_dot(m, LL, HHG_P2VEC, p, q, mg->scal + 1, s));
+    HHG_TRY(launch_pcg_update(n, mg->scal, x, r, p, q, L.dinv, z, s));
+    HHG_TRY(launch_fixup(m, LL, HHG_P2VEC, false, true, z, s));
+    HHG_TRY(launch_dot(m, LL, HHG_P2VEC, r, z, mg->scal + 2, s));
+    HHG_TRY(launch_pcg_dir(n, mg->scal, z, p, s));
+  }
+  return HHG_OK;
+}
+
+static int mg_cycle(hhg_mg* mg, int l, const double* f, double* x, cudaStream_t s) {
+  if (l == mg->prm.l_min) return mg_pcg(mg, l, f, x, s);
+  auto& L = mg->lv[l];
+  const Mesh* m = mg->mesh;
+  const int64_t n = p2vec_len(m, l);
+  HHG_CUDA(cudaMemsetAsync(x, 0, n * sizeof(double), s));
+  for (int i = 0; i < mg->prm.pre; ++i) HHG_TRY(mg_cheb(mg, l, x, f, i == 0, s));
+  // r = f - A x  (into L.r), restrict into f_{l-1}
+  HHG_TRY(mg_apply(mg, l, x, L.t, s));
+  k_sub<<<vg(n), 256, 0, s>>>(n, f, L.t, L.r);
+  count_launch();
+  auto& C = mg->lv[l - 1];
+  HHG_TRY(p2_restrict(mg->mesh, l, L.r, C.f, (hhg_stream_t)s));
+  HHG_TRY(mg_cycle(mg, l - 1, C.f, C.x, s));
+  HHG_TRY(p2_prolong(mg->mesh, l - 1, C.x, x, (hhg_stream_t)s));
+  for (int i = 0; i < mg->prm.post; ++i) HHG_TRY(mg_cheb(mg, l, x, f, false, s));
+  return HHG_OK;
+}
+
+extern "C" {
+
+int hhg_mg_create(hhg_mesh* mesh, const hhg_mg_params* params, const double* const* eta_per_level,
+                  double* const* power_v0, hhg_mg** out) {
+  if (!mesh || !params || !out) return fail(HHG_EINVAL, "hhg_mg_create: NULL argument");
+  const hhg_mg_params& P = *params;
+  if (P.l_min < 0 || P.l_max > mesh->level_max || P.l_min > P.l_max)
+    return fail(HHG_ELEVEL, "hhg_mg_create: need 0 <= l_min <= l_max <= level_max");
+  if (P.degree < 1 || P.pre < 0 || P.post < 0 || P.coarse_iters < 0 || P.power_iters < 1)
+    return fail(HHG_EINVAL, "hhg_mg_create: bad smoother parameters");
+  auto* mg = new hhg_mg();
+  mg->mesh = mesh;
+  mg->prm = P;
+  mg->lv.resize(P.l_max + 1);
+  auto bail = [&](int code) {
+    delete mg;
+    return code;
+  };
+  if (cudaMalloc(&mg->scal, 16 * sizeof(double)) != cudaSuccess) return bail(fail(HHG_ENOMEM, "scal"));
+  for (int l = P.l_min; l <= P.l_max; ++l) {
+    int r = ensure_level(mesh, l);
+    if (r != HHG_OK) return bail(r);
+    const int64_t n = p2vec_len(mesh, l);
+    auto& L = mg->lv[l];
+    L.eta = eta_per_level ? eta_per_level[l] : nullptr;
+    for (double** p : {&L.x, &L.f, &L.r, &L.d, &L.t, &L.dinv})
+      if (cudaMalloc(p, n * sizeof(double)) != cudaSuccess) return bail(fail(HHG_ENOMEM, "mg vectors"));
+    if (l == P.l_min && cudaMalloc(&L.p, n * sizeof(double)) != cudaSuccess) return bail(fail(HHG_ENOMEM, "mg p"));
+    // diag(A) without P_v -> D^-1
+    r = apply_op(mesh, l, ELEM_DIAG, P.visc_form, L.eta, 0.0, nullptr, nullptr, L.t, nullptr, false, 0);
+    if (r != HHG_OK) return bail(r);
+    k_recip<<<vg(n), 256>>>(n, L.t, L.dinv);
+    count_launch();
+    if (l > P.l_min) {
+      if (!power_v0 || !power_v0[l]) return bail(fail(HHG_EINVAL, "hhg_mg_create: power_v0[l] missing"));
+      r = hhg_power_iteration(mesh, l, L.eta, L.dinv, P.power_iters, power_v0[l], &L.lam, nullptr);
+      if (r != HHG_OK) return bail(r);
+    }
+  }
+  if (cudaDeviceSynchronize() != cudaSuccess) return bail(fail(HHG_ECUDA, "hhg_mg_create: sync failed"));
+  *out = mg;
+  return HHG_OK;
+}
+
+int hhg_mg_lambda(const hhg_mg* mg, int level, double* lambda_host) {
+  if (!mg || !lambda_host) return fail(HHG_EINVAL, "NULL argument");
+  if (level < mg->prm.l_min || level > mg->prm.l_max) return fail(HHG_ELEVEL, "level outside hierarchy");
+  *lambda_host = mg->lv[level].lam;
+  return HHG_OK;
+}
+
+int vcycle(hhg_mg* mg, const double* rhs, double* x, hhg_stream_t stream) {
+  if (!mg || !rhs || !x) return fail(HHG_EINVAL, "vcycle: NULL argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  for (int l = mg->prm.l_min + 1; l <= mg->prm.l_max; ++l)
+    if (!(mg->lv[l].lam > 0)) return fail(HHG_ENOTREADY, "vcycle: no spectrum estimate");
+  const bool use_graph = mg->prm.use_graph && s != nullptr && !mg->prof;
+  if (!use_graph) {
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (mg->prof) {
+      if (mg->ev_used + 2 > mg->ev.size())
+        for (int i = 0; i < 64; ++i) {
+          cudaEvent_t e;
+          HHG_CUDA(cudaEventCreate(&e));
+          mg->ev.push_back(e);
+        }
+      e0 = mg->ev[mg->ev_used];
+      e1 = mg->ev[mg->ev_used + 1];
+      mg->ev_used += 2;
+      HHG_CUDA(cudaEventRecord(e0, s));
+    }
+    size_t first_apply_ev = mg->ev_used;
+    HHG_TRY(mg_cycle(mg, mg->prm.l_max, rhs, x, s));
+    if (mg->prof) {
+      HHG_CUDA(cudaEventRecord(e1, s));
+      HHG_CUDA(cudaEventSynchronize(e1));
+      float ms = 0;
+      HHG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+      mg->cycle_ms += ms;
+      mg->cycle_n += 1;
+      for (size_t i = first_apply_ev; i + 1 < mg->ev_used; i += 2) {
+        HHG_CUDA(cudaEventElapsedTime(&ms, mg->ev[i], mg->ev[i + 1]));
+        mg->apply_ms += ms;
+        mg->apply_n += 1;
+      }
+      mg->ev_used = 0;
+    }
+    return HHG_OK;
+  }
+  if (!mg->gexec || mg->g_rhs != rhs || mg->g_x != x || mg->g_stream != s) {
+    if (mg->gexec) cudaGraphExecDestroy(mg->gexec);
+    mg->gexec = nullptr;
+    cudaGraph_t g;
+    HHG_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    int r = mg_cycle(mg, mg->prm.l_max, rhs, x, s);
+    cudaError_t ce = cudaStreamEndCapture(s, &g);
+    if (r != HHG_OK) return r;
+    if (ce != cudaSuccess) return fail(HHG_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+    HHG_CUDA(cudaGraphInstantiate(&mg->gexec, g, 0));
+    cudaGraphDestroy(g);
+    mg->g_rhs = rhs;
+    mg->g_x = x;
+    mg->g_stream = s;
+  }
+  HHG_CUDA(cudaGraphLaunch(mg->gexec, s));
+  count_launch();
+  return HHG_OK;
+}
+
+int vcycle_host(hhg_mg* mg, const double* rhs_host, double* x_host, hhg_stream_t stream) {
+  if (!mg || !rhs_host || !x_host) return fail(HHG_EINVAL, "vcycle_host: NULL argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t n = p2vec_len(mg->mesh, mg->prm.l_max);
+  if (!mg->hbuf_rhs) {
+    if (cudaMalloc(&mg->hbuf_rhs, n * sizeof(double)) != cudaSuccess) return fail(HHG_ENOMEM, "staging");
+    if (cudaMalloc(&mg->hbuf_x, n * sizeof(double)) != cudaSuccess) return fail(HHG_ENOMEM, "staging");
+  }
+  HHG_CUDA(cudaMemcpyAsync(mg->hbuf_rhs, rhs_host, n * sizeof(double), cudaMemcpyHostToDevice, s));
+  HHG_TRY(vcycle(mg, mg->hbuf_rhs, mg->hbuf_x, stream));
+  HHG_CUDA(cudaMemcpyAsync(x_host, mg->hbuf_x, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  return HHG_OK;
+}
+
+int hhg_mg_profile(hhg_mg* mg, int enable) {
+  if (!mg) return fail(HHG_EINVAL, "NULL mg");
+  mg->prof = enable != 0;
+  mg->apply_ms = mg->cycle_ms = 0;
+  mg->apply_n = mg->cycle_n = 0;
+  mg->ev_used = 0;
+  return HHG_OK;
+}
+
+int hhg_mg_profile_get(hhg_mg* mg, double* apply_ms_sum, int64_t* apply_count, double* cycle_ms_sum,
+                       int64_t* cycle_count) {
+  if (!mg) return fail(HHG_EINVAL, "NULL mg");
+  if (apply_ms_sum) *apply_ms_sum = mg->apply_ms;
+  if (apply_count) *apply_count = mg->apply_n;
+  if (cycle_ms_sum) *cycle_ms_sum = mg->cycle_ms;
+  if (cycle_count) *cycle_count = mg->cycle_n;
+  return HHG_OK;
+}
+
+int hhg_mg_destroy(hhg_mg* mg) {
+  delete mg;
+  return HHG_OK;
+}
+
+int chebyshev_smooth(const hhg_mesh* mesh, int level, const double* eta_p1, const double* dinv, int degree,
+                     double lmin, double lmax, const double* rhs, double* x, double* work, hhg_stream_t stream) {
+  if (!mesh || !dinv || !rhs || !x || !work) return fail(HHG_EINVAL, "chebyshev_smooth: NULL argument");
+  if (level < 0 || level > mesh->level_max) return fail(HHG_ELEVEL, "level outside [0, level_max]");
+  if (degree < 1) return fail(HHG_EINVAL, "degree must be >= 1");
+  if (!(lmax > 0) || !(lmin >= 0) || !(lmin < lmax)) return fail(HHG_ENOTREADY, "chebyshev_smooth: bad spectrum");
+  auto* m = const_cast<hhg_mesh*>(mesh);
+  HHG_TRY(ensure_level(m, level));
+  const int64_t n = p2vec_len(m, level);
+  return cheb_sweep(m, level, HHG_VISC_FULL, eta_p1, dinv, degree, lmin, lmax, rhs, x, work, work + n, work + 2 * n,
+                    false, (cudaStream_t)stream);
+}
+
+int hhg_power_iteration(const hhg_mesh* mesh, int level, const double* eta_p1, const double* dinv, int iters,
+                        double* v0, double* lambda_host, hhg_stream_t stream) {
+  if (!mesh || !dinv || !v0 || !lambda_host) return fail(HHG_EINVAL, "hhg_power_iteration: NULL argument");
+  if (level < 0 || level > mesh->level_max) return fail(HHG_ELEVEL, "level outside [0, level_max]");
+  if (iters < 1) return fail(HHG_EINVAL, "iters must be >= 1");
+  auto* m = const_cast<hhg_mesh*>(mesh);
+  HHG_TRY(ensure_level(m, level));
+  cudaStream_t s = (cudaStream_t)stream;
+  const Level& L = m->levels[level];
+  const int64_t n = p2vec_len(m, level);
+  double *t = nullptr, *sc = nullptr;
+  if (cudaMalloc(&t, n * sizeof(double)) != cudaSuccess) return fail(HHG_ENOMEM, "power iteration workspace");
+  if (cudaMalloc(&sc, sizeof(double)) != cudaSuccess) {
+    cudaFree(t);
+    return fail(HHG_ENOMEM, "power iteration workspace");
+  }
+  int r = HHG_OK;
+  auto run = [&]() -> int {
+    HHG_TRY(launch_fixup(m, L, HHG_P2VEC, false, true, v0, s));
+    for (int it = 0; it < iters; ++it) {
+      HHG_TRY(apply_op(m, level, ELEM_A, HHG_VISC_FULL, eta_p1, 0.0, v0, nullptr, t, nullptr, false, s));
+      k_scale_dinv<<<vg(n), 256, 0, s>>>(n, t, dinv, t);
+      count_launch();
+      HHG_TRY(launch_fixup(m, L, HHG_P2VEC, false, true, t, s));
+      HHG_TRY(launch_dot(m, L, HHG_P2VEC, t, t, sc, s));
+      k_normalize<<<vg(n), 256, 0, s>>>(n, sc, t, v0);
+      count_launch();
+    }
+    double h = 0;
+    HHG_CUDA(cudaMemcpyAsync(&h, sc, sizeof(double), cudaMemcpyDeviceToHost, s));
+    HHG_CUDA(cudaStreamSynchronize(s));
+    if (!(h > 0) || !std::isfinite(h)) return fail(HHG_EZEROOP, "power iteration on a zero operator");
+    *lambda_host = std::sqrt(h);
+    return HHG_OK;
+  };
+  r = run();
+  cudaFree(t);
+  cudaFree(sc);
+  return r;
+}
+
+}  // extern "C"

@@ -1,0 +1,223 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on the same seeded inputs.
+
+Tolerances (BASELINE.json north_star): relative l2 <= 1e-11 per operator apply, <= 1e-9 after a
+full V-cycle; lambda_hat <= 1e-12 relative.  Comparisons are in canonical node order over all dofs
+(constrained dofs are exactly zero on both sides).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2506_04157_b200 as hhg  # noqa: E402  (fails loudly if the library is missing)
+from tests.harness import (BC_ALL, BC_SHELL, canon, lib_eta, lib_mesh, lib_p, lib_u, oracle_case,  # noqa: E402
+                           rel_l2)
+from workload import icoshell, reference_tet, uniform_vec, uniform_from_keys, GAMMA_TALA  # noqa: E402
+
+TOL_APPLY = 1e-11
+TOL_VCYCLE = 1e-9
+C2 = (1e4, 10.0)   # config 2 viscosity: contrast 1e4, radial jump x10 at r < 0.9
+C3 = (1e6, 30.0)   # config 3
+
+
+def test_library_is_the_cuda_path():
+    assert "sm_100a" in hhg.version()
+    n0 = hhg.launch_count()
+    M = lib_mesh(reference_tet(), 1, False, BC_ALL)
+    u = lib_u(M, 1, 0)
+    hhg.epsilon_apply(M, 1, None, u)
+    torch.cuda.synchronize()
+    assert hhg.launch_count() > n0
+
+
+@pytest.mark.parametrize("form", [hhg.HHG_VISC_FULL, hhg.HHG_VISC_EPS])
+def test_config1_reference_tet_level3(form):
+    """BASELINE config 1: reference tet, no blending, L3, eta = 1, zero Dirichlet on all faces."""
+    from oracle.operators import FORM_FULL, FORM_EPS, Discretisation
+    mac = reference_tet()
+    M = lib_mesh(mac, 3, False, BC_ALL)
+    lm, d, _ = oracle_case(mac, 3, False, BC_ALL)
+    if form == hhg.HHG_VISC_EPS:
+        d = Discretisation(lm, False, None, 0.0, {"all": 1}, form=FORM_EPS)
+    u_raw = uniform_vec(lm.p2_keys, 0)
+    p = uniform_from_keys(lm.p1_keys, 1, 0)
+    uo = d.project(u_raw)
+    u = lib_u(M, 3, 0)
+    assert rel_l2(canon(M, 3, hhg.HHG_P2VEC, u), uo) == 0.0
+    y = hhg.epsilon_apply(M, 3, None, u, form=form)
+    assert rel_l2(canon(M, 3, hhg.HHG_P2VEC, y), d.apply_A(uo)) <= TOL_APPLY
+    if form == hhg.HHG_VISC_FULL:
+        q = hhg.div_apply(M, 3, 0.0, u)
+        assert rel_l2(canon(M, 3, hhg.HHG_P1, q), d.B @ uo) <= TOL_APPLY
+        yt = hhg.divT_apply(M, 3, lib_p(M, 3, 1))
+        assert rel_l2(canon(M, 3, hhg.HHG_P2VEC, yt), d.apply_BT(p)) <= TOL_APPLY
+
+
+@pytest.fixture(scope="module")
+def shell_l2():
+    mac = icoshell(3, 2)
+    lm, d, eta_o = oracle_case(mac, 2, True, BC_SHELL, C2, GAMMA_TALA)
+    M = lib_mesh(mac, 3, True, BC_SHELL)
+    return mac, lm, d, eta_o, M
+
+
+def test_shell_level2_stokes_apply(shell_l2):
+    mac, lm, d, eta_o, M = shell_l2
+    uo = d.project(uniform_vec(lm.p2_keys, 2))
+    po = uniform_from_keys(lm.p1_keys, 3, 0)
+    eta = lib_eta(M, 2, C2)
+    assert rel_l2(canon(M, 2, hhg.HHG_P1, eta), eta_o) < 1e-14
+    u, p = lib_u(M, 2, 2), lib_p(M, 2, 3)
+    yu, yp = hhg.stokes_apply(M, 2, eta, GAMMA_TALA, u, p)
+    assert rel_l2(canon(M, 2, hhg.HHG_P2VEC, yu), d.apply_A(uo) + d.apply_BT(po)) <= TOL_APPLY
+    assert rel_l2(canon(M, 2, hhg.HHG_P1, yp), d.apply_Bbar(uo)) <= TOL_APPLY
+    y = hhg.epsilon_apply(M, 2, eta, u)
+    assert rel_l2(canon(M, 2, hhg.HHG_P2VEC, y), d.apply_A(uo)) <= TOL_APPLY
+    q = hhg.div_apply(M, 2, GAMMA_TALA, u)
+    assert rel_l2(canon(M, 2, hhg.HHG_P1, q), d.apply_Bbar(uo)) <= TOL_APPLY
+    q0 = hhg.div_apply(M, 2, 0.0, u)
+    assert rel_l2(canon(M, 2, hhg.HHG_P1, q0), d.B @ uo) <= TOL_APPLY
+    yt = hhg.divT_apply(M, 2, p)
+    assert rel_l2(canon(M, 2, hhg.HHG_P2VEC, yt), d.apply_BT(po)) <= TOL_APPLY
+
+
+def test_shell_level2_diag_and_dot(shell_l2):
+    mac, lm, d, eta_o, M = shell_l2
+    eta = lib_eta(M, 2, C2)
+    dg = hhg.hhg_diag(M, 2, eta)
+    assert rel_l2(canon(M, 2, hhg.HHG_P2VEC, dg), d.diagA()) <= TOL_APPLY
+    u, v = lib_u(M, 2, 2), lib_u(M, 2, 7)
+    ref = float(canon(M, 2, hhg.HHG_P2VEC, u) @ canon(M, 2, hhg.HHG_P2VEC, v))
+    got = float(hhg.hhg_dot(M, 2, hhg.HHG_P2VEC, u, v).item())
+    assert abs(got - ref) <= 1e-13 * abs(ref)
+
+
+def test_shell_transfers(shell_l2):
+    from oracle.multigrid import p2_prolongation, vec_prolongation
+    from oracle.refine import build_level
+    from oracle.operators import Discretisation
+    mac, lm2, d2, _, M = shell_l2
+    lm1 = build_level(mac.verts, mac.tets, mac.vtag, 1)
+    d1 = Discretisation(lm1, True, None, 0.0, {2: 1, 1: 2}, build=())
+    P = vec_prolongation(p2_prolongation(lm1, lm2))
+    xc_o = d1.project(uniform_vec(lm1.p2_keys, 11))
+    xf_o = d2.project(uniform_vec(lm2.p2_keys, 12))
+    xc, xf = lib_u(M, 1, 11), lib_u(M, 2, 12)
+    hhg.p2_prolong(M, 1, xc, xf)
+    assert rel_l2(canon(M, 2, hhg.HHG_P2VEC, xf), xf_o + d2.project(P @ xc_o)) <= 1e-14
+    rf = lib_u(M, 2, 13)
+    rc = hhg.p2_restrict(M, 2, rf)
+    rf_o = d2.project(uniform_vec(lm2.p2_keys, 13))
+    assert rel_l2(canon(M, 1, hhg.HHG_P2VEC, rc), d1.project(P.T @ rf_o)) <= 1e-14
+
+
+def test_power_iteration_and_chebyshev_level2(shell_l2):
+    from oracle.multigrid import chebyshev, power_iteration
+    mac, lm, d, eta_o, M = shell_l2
+    Ac, dinv_o = d.Ac(), 1.0 / d.diagA()
+    lam_o = power_iteration(Ac, dinv_o, d.Pm, uniform_vec(lm.p2_keys, 6), 20)
+    eta = lib_eta(M, 2, C2)
+    dinv = 1.0 / hhg.hhg_diag(M, 2, eta)
+    keys = M.canonical_keys(2, hhg.HHG_P2)
+    v0 = M.from_canonical(2, hhg.HHG_P2VEC, uniform_vec(keys, 6))
+    lam = hhg.hhg_power_iteration(M, 2, eta, dinv, 20, v0)
+    assert abs(lam - lam_o) <= 1e-12 * lam_o
+    f_o = d.project(uniform_vec(lm.p2_keys, 4))
+    x_o = d.project(uniform_vec(lm.p2_keys, 9))
+    b = 1.1 * lam_o
+    xs_o = chebyshev(Ac, dinv_o, d.Pm, f_o, x_o, 3, b)
+    f, x = lib_u(M, 2, 4), lib_u(M, 2, 9)
+    hhg.chebyshev_smooth(M, 2, eta, dinv, 3, b / 10, b, f, x)
+    assert rel_l2(canon(M, 2, hhg.HHG_P2VEC, x), xs_o) <= TOL_APPLY
+
+
+@pytest.mark.parametrize("contrast,levels", [((1e6, 30.0), (1, 2, 3))])
+def test_vcycle_matches_oracle(contrast, levels):
+    """Config 3 recipe (V(3,3), Chebyshev degree 3, 20 power iterations, 50 coarse PCG iterations)
+    on shell(3,2) levels 3 -> 1: one V-cycle from x = 0 on a seeded rhs."""
+    from oracle.multigrid import Hierarchy
+    mac = icoshell(3, 2)
+    discs, v0 = {}, {}
+    for L in levels:
+        lm, d, _ = oracle_case(mac, L, True, BC_SHELL, contrast, 0.0, build=("A",))
+        discs[L] = d
+        v0[L] = uniform_vec(lm.p2_keys, 6)
+    H = Hierarchy(discs, v0, pre=3, post=3, degree=3, power_iters=20, coarse_iters=50)
+    lmax = levels[-1]
+    f_o = discs[lmax].project(uniform_vec(discs[lmax].lm.p2_keys, 4))
+    x_o = H.vcycle(f_o)
+    M = lib_mesh(mac, lmax, True, BC_SHELL)
+    etas = {L: lib_eta(M, L, contrast) for L in levels}
+    pv = {L: M.from_canonical(L, hhg.HHG_P2VEC, uniform_vec(M.canonical_keys(L, hhg.HHG_P2), 6))
+          for L in levels[1:]}
+    mg = hhg.MG(M, levels[0], lmax, etas, pv, pre=3, post=3, degree=3, power_iters=20, coarse_iters=50)
+    for L in levels[1:]:
+        assert abs(mg.lam(L) - H.lam[L]) <= 1e-12 * H.lam[L]
+    f = lib_u(M, lmax, 4)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        x = mg.vcycle(f, stream=s)
+        x2 = mg.vcycle(f, stream=s)       # graph replay
+    s.synchronize()
+    xc = canon(M, lmax, hhg.HHG_P2VEC, x)
+    assert rel_l2(xc, x_o) <= TOL_VCYCLE, rel_l2(xc, x_o)
+    assert rel_l2(canon(M, lmax, hhg.HHG_P2VEC, x2), xc) <= 1e-13
+
+
+@pytest.mark.slow
+def test_config2_level4_sampled_rows():
+    """BASELINE config 2 at full size (shell(3,2), L4, contrast 1e4 x 10): GPU stokes_apply
+    against oracle rows computed one by one on sampled nodes (incl. macro faces/edges/vertices)."""
+    from oracle.refine import build_level, node_bc
+    from oracle.operators import node_coords, sampled_rows, constraint_matrix
+    from oracle.multigrid import lookup_keys
+    from workload import viscosity
+    mac = icoshell(3, 2)
+    L = 4
+    core = [0, 77, 191]
+    core_verts = set(mac.tets[core].ravel().tolist())
+    star = [t for t in range(mac.n_tets) if core_verts & set(mac.tets[t].tolist())]
+    lm = build_level(mac.verts, mac.tets, mac.vtag, L, macro_subset=star)
+    bc = node_bc(lm.p2_keys, lm.macro_tets, lm.macro_vtag, {2: 1, 1: 2})
+    eta_o = viscosity(node_coords(lm, "P1", True), lm.p1_keys, *C2)
+    uo = constraint_matrix(lm.p2_xt, bc) @ uniform_vec(lm.p2_keys, 2)
+    po = uniform_from_keys(lm.p1_keys, 3, 0)
+    rng = np.random.default_rng(0)
+    core_tets = np.nonzero(np.isin(lm.tet_macro, core))[0]
+    n2 = np.unique(lm.tet_p2[core_tets].ravel())
+    n1 = np.unique(lm.tet_p1[core_tets].ravel())
+    s2 = np.unique(np.concatenate([rng.choice(n2, 300, replace=False), n2[lm.p2_keys[n2, 0] < 3][:100]]))
+    s1 = np.unique(np.concatenate([rng.choice(n1, 100, replace=False), n1[lm.p1_keys[n1, 0] < 3][:50]]))
+    yu_o, yp_o = sampled_rows(lm, True, eta_o, GAMMA_TALA, uo, po, s2, s1, bc)
+    M = lib_mesh(mac, L, True, BC_SHELL)
+    eta = lib_eta(M, L, C2)
+    yu, yp = hhg.stokes_apply(M, L, eta, GAMMA_TALA, lib_u(M, L, 2), lib_p(M, L, 3))
+    r2 = lookup_keys(M.canonical_keys(L, hhg.HHG_P2), lm.p2_keys[s2])
+    r1 = lookup_keys(M.canonical_keys(L, hhg.HHG_P1), lm.p1_keys[s1])
+    yu_c = canon(M, L, hhg.HHG_P2VEC, yu).reshape(-1, 3)[r2]
+    yp_c = canon(M, L, hhg.HHG_P1, yp)[r1]
+    assert rel_l2(yu_c, yu_o.reshape(-1, 3)[s2]) <= TOL_APPLY
+    assert rel_l2(yp_c, yp_o[s1]) <= TOL_APPLY
+
+
+def test_edge_cases():
+    # level 0 (one micro tet per macro), zero input, errors
+    mac = icoshell(3, 2)
+    M = lib_mesh(mac, 1, True, BC_SHELL)
+    lm, d, _ = oracle_case(mac, 0, True, BC_SHELL, C2, GAMMA_TALA)
+    eta = lib_eta(M, 0, C2)
+    uo = d.project(uniform_vec(lm.p2_keys, 2))
+    y = hhg.epsilon_apply(M, 0, eta, lib_u(M, 0, 2))
+    assert rel_l2(canon(M, 0, hhg.HHG_P2VEC, y), d.apply_A(uo)) <= TOL_APPLY
+    z = M.zeros(1, hhg.HHG_P2VEC)
+    assert torch.count_nonzero(hhg.epsilon_apply(M, 1, None, z)).item() == 0
+    with pytest.raises(hhg.HHGError, match="HHG_ELEVEL"):
+        hhg.epsilon_apply(M, 2, None, z)
+    with pytest.raises(hhg.HHGError, match="HHG_ELEVEL"):
+        hhg.p2_restrict(M, 0, z)
+    with pytest.raises(hhg.HHGError):
+        hhg.epsilon_apply(M, 1, None, z[:-1])
