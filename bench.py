@@ -253,7 +253,7 @@ def main():
     elem_ms = prof["apply_ms_sum"] / max(1, prof["apply_count"])
     achieved = flops_per_tet * n_tets / (elem_ms * 1e-3) / 1e12
     pk = peaks()
-    fp64_peak = pk.get("fp64_tflops") or FP64_PEAK_DERIVED
+    fp64_peak = pk.get("fp64_tflops") or FP64_PEAK_MEASURED
     result = {
         "metric": METRIC, "value": value, "unit": "GDoF/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -270,7 +270,9 @@ def main():
                      "kernel": "k_elem<blend,A,full> (fine level)", "elem_ms": elem_ms,
                      "flops_per_tet": flops_per_tet,
                      "peak_source": "MEASURED_PEAKS.json fp64_tflops" if pk.get("fp64_tflops") else
-                     "derived: 148 SM x 64 DFMA/clk x 2 x 1.965 GHz (DESIGN.md)"},
+                     "measured: tools/fp64_peak DFMA microbenchmark (profiles/r01_fp64_peak.json)",
+                     "hbm_gbs_algorithmic": (2 * n_dof + 240 * ((2 ** L + 1) * (2 ** L + 2) * (2 ** L + 3) // 6)) * 8
+                     / (elem_ms * 1e-3) / 1e9},
         "e2e": {"value": world * n_dof / (e2e_ms * 1e-3) / 1e9, "unit": "GDoF/s", "ms": e2e_ms,
                 "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes},
         "gpu_launches": kernels_per_cycle * args.steps,
@@ -291,8 +293,8 @@ def main():
 
 # algorithmic DP flops per micro tet of the A element kernel (cross-checked
 # against ncu smsp__sass_thread_inst_executed_op_d{fma,add,mul}_pred_on)
-FLOPS_PER_TET = 1300.0
-FP64_PEAK_DERIVED = 148 * 64 * 2 * 1.965e9 / 1e12
+FLOPS_PER_TET = 1530.0      # 532 DFMA + 233 DADD + 233 DMUL per tet (ncu, profiles/r01_ncu_elem_brick_L5_summary.txt)
+FP64_PEAK_MEASURED = 34.16  # tools/fp64_peak on this pool's B200 (profiles/r01_fp64_peak.json); DMMA 37.1 (r01_fp64_dfma_vs_dmma.json)
 TRAFFIC_PER_LAUNCH = None
 
 if __name__ == "__main__":

@@ -18,7 +18,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libhhgstokes.so")
+LIB_PATH = os.environ.get("HHG_LIB") or os.path.join(_HERE, "lib", "libhhgstokes.so")  # HHG_LIB: A/B builds
 
 HHG_P1, HHG_P2, HHG_P2VEC = 1, 2, 3
 HHG_BLEND_IDENTITY, HHG_BLEND_SHELL = 0, 1
@@ -142,7 +142,7 @@ class Mesh:
         return cls(macro.verts, macro.tets, macro.vtag, level_max, **kw)
 
     def __del__(self):
-        if getattr(self, "handle", None):
+        if getattr(self, "handle", None) and _lib is not None:
             _lib.hhg_mesh_destroy(self.handle)
             self.handle = None
 
@@ -313,7 +313,7 @@ class MG:
         self.handle = h
 
     def __del__(self):
-        if getattr(self, "handle", None):
+        if getattr(self, "handle", None) and _lib is not None:
             _lib.hhg_mg_destroy(self.handle)
             self.handle = None
 

@@ -57,6 +57,7 @@ constexpr int kLevelGeo = 6 * kTypeGeo + 2;  // + absdetF + pad
 
 struct Groups {           // replicated-node groups (interface and/or boundary nodes)
   int64_t n = 0;          // number of groups
+  int64_t nbc = 0;        // groups [0, nbc) carry a BC (sorted first)
   int64_t* ptr = nullptr; // [n+1] into copy
   int64_t* copy = nullptr;// scalar flat indices (macro*npts + idx)
   uint8_t* kind = nullptr;// BC kind per group (P2 only)
@@ -69,8 +70,8 @@ struct Level {
   int n1 = 0, n2 = 0;               // P1 / P2 lattice resolution
   int64_t npts1 = 0, npts2 = 0;     // per macro
   double* geo = nullptr;            // [n_macro][kLevelGeo]
-  int32_t* anchors[3] = {nullptr, nullptr, nullptr};  // s<=n-1, s<=n-2, s<=n-3, packed i|j<<10|k<<20
-  int64_t n_anchor[3] = {0, 0, 0};
+  int32_t* bricks = nullptr;        // 4x4x4-cube brick origins, packed i|j<<10|k<<20
+  int64_t n_bricks = 0;
   int32_t* rows1 = nullptr;         // packed (j | k<<16) for P1 rows
   int32_t* rows2 = nullptr;         // packed rows for P2
   int64_t nrows1 = 0, nrows2 = 0;

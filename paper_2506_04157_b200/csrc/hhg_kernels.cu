@@ -36,332 +36,6 @@ __constant__ int cEinv[6][9];
 
 __device__ __forceinline__ int64_t d_lidx(int i, int j, int k, int N) { return lidx(i, j, k, N); }
 
-// ------------------------------------------------------------------ element kernel
-template <bool BLEND, int MODE, bool FULL>
-__global__ void __launch_bounds__(128) k_elem(const MacroGeo* __restrict__ mgeo, const double* __restrict__ lgeo,
-                                              const int32_t* __restrict__ anc0, const int32_t* __restrict__ anc1,
-                                              const int32_t* __restrict__ anc2, int64_t na0, int64_t na1,
-                                              int64_t na2, int n1, int64_t npts1, int64_t npts2,
-                                              int64_t cstride, const double* __restrict__ eta,
-                                              const double* __restrict__ u, const double* __restrict__ p,
-                                              double* __restrict__ yu, double* __restrict__ yp, double gamma) {
-  const int t = blockIdx.z;
-  const int cls = (t == 0) ? 0 : (t == 5 ? 2 : 1);
-  const int32_t* anc = cls == 0 ? anc0 : (cls == 1 ? anc1 : anc2);
-  const int64_t na = cls == 0 ? na0 : (cls == 1 ? na1 : na2);
-  const int64_t aid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (aid >= na) return;
-  const int mac = blockIdx.y;
-  const int32_t pk = __ldg(anc + aid);
-  const int ai = pk & 1023, aj = (pk >> 10) & 1023, ak = pk >> 20;
-  const int n2 = 2 * n1;
-  const MacroGeo& g = mgeo[mac];
-  const double* G = lgeo + (int64_t)mac * kLevelGeo + t * kTypeGeo;
-  double JFi[9];
-#pragma unroll
-  for (int r = 0; r < 9; ++r) JFi[r] = __ldg(G + r);
-  const double absdetF = __ldg(lgeo + (int64_t)mac * kLevelGeo + 6 * kTypeGeo);
-  double nh[3] = {0, 0, 0}, cK = 1.0;
-  if (BLEND) {
-    nh[0] = g.nhat[0];
-    nh[1] = g.nhat[1];
-    nh[2] = g.nhat[2];
-    cK = g.cK;
-  }
-  // anchor position (unblended)
-  const double fa = (double)ai / n1, fb = (double)aj / n1, fc = (double)ak / n1;
-  double xa[3];
-#pragma unroll
-  for (int r = 0; r < 3; ++r) xa[r] = g.X0[r] + g.Jm[3 * r] * fa + g.Jm[3 * r + 1] * fb + g.Jm[3 * r + 2] * fc;
-
-  // node indices
-  int V[4][3];
-#pragma unroll
-  for (int v = 0; v < 4; ++v)
-#pragma unroll
-    for (int r = 0; r < 3; ++r) V[v][r] = cTV[t][v][r];
-  int64_t nid[10];
-  const int64_t mbase2 = (int64_t)mac * npts2;
-#pragma unroll
-  for (int v = 0; v < 4; ++v)
-    nid[v] = mbase2 + d_lidx(2 * (ai + V[v][0]), 2 * (aj + V[v][1]), 2 * (ak + V[v][2]), n2);
-  {
-    const int ep[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
-#pragma unroll
-    for (int e = 0; e < 6; ++e) {
-      const int a = ep[e][0], b = ep[e][1];
-      nid[4 + e] = mbase2 + d_lidx(2 * ai + V[a][0] + V[b][0], 2 * aj + V[a][1] + V[b][1], 2 * ak + V[a][2] + V[b][2], n2);
-    }
-  }
-  const int64_t mbase1 = (int64_t)mac * npts1;
-  int64_t pid[4];
-#pragma unroll
-  for (int v = 0; v < 4; ++v) pid[v] = mbase1 + d_lidx(ai + V[v][0], aj + V[v][1], ak + V[v][2], n1);
-
-  constexpr bool DO_A = (MODE & ELEM_A) != 0;
-  constexpr bool DO_BT = (MODE & ELEM_BT) != 0;
-  constexpr bool DO_DIV = (MODE & ELEM_DIV) != 0;
-  constexpr bool DO_DIAG = (MODE & ELEM_DIAG) != 0;
-  constexpr bool NEED_U = DO_A || DO_DIV;
-  constexpr bool NEED_ETA = DO_A || DO_DIAG;
-
-  double uu[10][3];
-  if (NEED_U) {
-#pragma unroll
-    for (int a = 0; a < 10; ++a)
-#pragma unroll
-      for (int c = 0; c < 3; ++c) uu[a][c] = __ldg(u + c * cstride + nid[a]);
-  }
-  double et[4] = {1.0, 1.0, 1.0, 1.0};
-  if (NEED_ETA && eta != nullptr) {
-#pragma unroll
-    for (int v = 0; v < 4; ++v) et[v] = __ldg(eta + pid[v]);
-  }
-  double pp[4] = {0, 0, 0, 0};
-  if (DO_BT) {
-#pragma unroll
-    for (int v = 0; v < 4; ++v) pp[v] = __ldg(p + pid[v]);
-  }
-  const double etaS = QB * (et[0] + et[1] + et[2] + et[3]);
-  const double pS = QB * (pp[0] + pp[1] + pp[2] + pp[3]);
-
-  // Sb[m][c] = 4 QB sum_{j != m} u_{mj}
-  double Sb[4][3];
-  if (NEED_U) {
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      Sb[0][c] = 4.0 * QB * (uu[4][c] + uu[5][c] + uu[6][c]);
-      Sb[1][c] = 4.0 * QB * (uu[4][c] + uu[7][c] + uu[8][c]);
-      Sb[2][c] = 4.0 * QB * (uu[5][c] + uu[7][c] + uu[9][c]);
-      Sb[3][c] = 4.0 * QB * (uu[6][c] + uu[8][c] + uu[9][c]);
-    }
-  }
-  double acc[10][3];
-  double Sbar[4][3];
-#pragma unroll
-  for (int a = 0; a < 10; ++a)
-#pragma unroll
-    for (int c = 0; c < 3; ++c) acc[a][c] = 0.0;
-#pragma unroll
-  for (int m = 0; m < 4; ++m)
-#pragma unroll
-    for (int c = 0; c < 3; ++c) Sbar[m][c] = 0.0;
-  double gq[4] = {0, 0, 0, 0}, gsum = 0.0;
-
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    double xq[3];
-#pragma unroll
-    for (int r = 0; r < 3; ++r) xq[r] = xa[r] + __ldg(G + 9 + 3 * q + r);
-    // blending at x_q: d = x/|x|, alpha = n.d, J_B^-1 = (I - d w^T)/(c alpha), w = n/alpha - d
-    double d[3] = {0, 0, 0}, wh[3] = {0, 0, 0}, ca = 1.0;
-    if (BLEND || DO_DIV) {
-      const double ri = rsqrt(xq[0] * xq[0] + xq[1] * xq[1] + xq[2] * xq[2]);
-      d[0] = xq[0] * ri;
-      d[1] = xq[1] * ri;
-      d[2] = xq[2] * ri;
-    }
-    if (BLEND) {
-      const double alpha = nh[0] * d[0] + nh[1] * d[1] + nh[2] * d[2];
-      const double ia = 1.0 / alpha;
-      wh[0] = nh[0] * ia - d[0];
-      wh[1] = nh[1] * ia - d[1];
-      wh[2] = nh[2] * ia - d[2];
-      ca = cK * alpha;
-    }
-    const double etaq = etaS + QAB * et[q];
-    // 2 eta w |det J_F| |det J_B| / (c alpha)^2 = 2 eta w |det J_F| c alpha
-    const double sA = 2.0 * etaq * WQ * absdetF * ca;
-
-    if (DO_DIAG) {
-      // physical gradients (times c alpha) of the 10 scalar basis functions at q
-#pragma unroll
-      for (int a = 0; a < 10; ++a) {
-        double gh[3];
-        if (a < 4) {
-          const double lam = (a == q) ? QA : QB;
-          const double f = 4.0 * lam - 1.0;
-          gh[0] = (a == 0) ? -f : (a == 1 ? f : 0.0);
-          gh[1] = (a == 0) ? -f : (a == 2 ? f : 0.0);
-          gh[2] = (a == 0) ? -f : (a == 3 ? f : 0.0);
-        } else {
-          const int ep[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
-          const int i0 = ep[a - 4][0], j0 = ep[a - 4][1];
-          const double li = (i0 == q) ? QA : QB, lj = (j0 == q) ? QA : QB;
-          // 4 (li grad lam_j + lj grad lam_i)
-#pragma unroll
-          for (int k = 0; k < 3; ++k) {
-            const double gi = (i0 == 0) ? -1.0 : (i0 == k + 1 ? 1.0 : 0.0);
-            const double gj = (j0 == 0) ? -1.0 : (j0 == k + 1 ? 1.0 : 0.0);
-            gh[k] = 4.0 * (li * gj + lj * gi);
-          }
-        }
-        double gx[3];
-#pragma unroll
-        for (int l = 0; l < 3; ++l) gx[l] = gh[0] * JFi[l] + gh[1] * JFi[3 + l] + gh[2] * JFi[6 + l];
-        if (BLEND) {
-          const double gd = gx[0] * d[0] + gx[1] * d[1] + gx[2] * d[2];
-          gx[0] -= gd * wh[0];
-          gx[1] -= gd * wh[1];
-          gx[2] -= gd * wh[2];
-        }
-        const double n2g = gx[0] * gx[0] + gx[1] * gx[1] + gx[2] * gx[2];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          const double gc2 = gx[c] * gx[c];
-          acc[a][c] += sA * (FULL ? (0.5 * (n2g + gc2) - gc2 * (1.0 / 3.0)) : 0.5 * (n2g + gc2));
-        }
-      }
-      continue;
-    }
-
-    double H[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
-    if (NEED_U) {
-      double gh[3][3];
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        double D[4];
-#pragma unroll
-        for (int m = 0; m < 4; ++m) {
-          const double Cmq = (m == q) ? 3.0 * uu[m][c] : 4.0 * uu[EI(m, q)][c] - uu[m][c];
-          D[m] = Sb[m][c] + QAB * Cmq;
-        }
-        gh[c][0] = D[1] - D[0];
-        gh[c][1] = D[2] - D[0];
-        gh[c][2] = D[3] - D[0];
-      }
-      // G = gh J_F^-1 ;  H = G - (G d) w^T
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-#pragma unroll
-        for (int l = 0; l < 3; ++l) H[c][l] = gh[c][0] * JFi[l] + gh[c][1] * JFi[3 + l] + gh[c][2] * JFi[6 + l];
-        if (BLEND) {
-          const double gd = H[c][0] * d[0] + H[c][1] * d[1] + H[c][2] * d[2];
-          H[c][0] -= gd * wh[0];
-          H[c][1] -= gd * wh[1];
-          H[c][2] -= gd * wh[2];
-        }
-      }
-    }
-    if (DO_DIV) {
-      // g_q = -W (div u + grad ln rho . u) with div u = tr(H)/(c alpha), grad ln rho = -gamma d
-      double uq[3];
-      const double phv = QB * (2.0 * QB - 1.0), phq = QA * (2.0 * QA - 1.0);
-      const double peq = 4.0 * QA * QB, pen = 4.0 * QB * QB;
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        double s = 0.0;
-#pragma unroll
-        for (int a = 0; a < 4; ++a) s += ((a == q) ? phq : phv) * uu[a][c];
-        const int ep[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
-#pragma unroll
-        for (int e = 0; e < 6; ++e) s += ((ep[e][0] == q || ep[e][1] == q) ? peq : pen) * uu[4 + e][c];
-        uq[c] = s;
-      }
-      const double W = WQ * absdetF * ca * ca * ca;
-      const double div = (H[0][0] + H[1][1] + H[2][2]) / ca;
-      const double gg = -W * (div - gamma * (d[0] * uq[0] + d[1] * uq[1] + d[2] * uq[2]));
-      gq[q] = gg;
-      gsum += gg;
-    }
-    if (DO_A || DO_BT) {
-      double S[3][3];
-      if (DO_A) {
-        const double tr3 = (H[0][0] + H[1][1] + H[2][2]) * (1.0 / 3.0);
-        if (FULL) {
-          S[0][0] = sA * (H[0][0] - tr3);
-          S[1][1] = sA * (H[1][1] - tr3);
-          S[2][2] = sA * (H[2][2] - tr3);
-        } else {
-          S[0][0] = sA * H[0][0];
-          S[1][1] = sA * H[1][1];
-          S[2][2] = sA * H[2][2];
-        }
-        S[0][1] = S[1][0] = 0.5 * sA * (H[0][1] + H[1][0]);
-        S[0][2] = S[2][0] = 0.5 * sA * (H[0][2] + H[2][0]);
-        S[1][2] = S[2][1] = 0.5 * sA * (H[1][2] + H[2][1]);
-      } else {
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-#pragma unroll
-          for (int l = 0; l < 3; ++l) S[c][l] = 0.0;
-      }
-      if (DO_BT) {
-        // B^T p: isotropic stress -p_q W I, scaled by 1/(c alpha)
-        const double pq = pS + QAB * pp[q];
-        const double wb = WQ * absdetF * ca * ca * pq;
-        S[0][0] -= wb;
-        S[1][1] -= wb;
-        S[2][2] -= wb;
-      }
-      // M = S - (S w) d^T ; R = M J_F^-T
-      double R[3][3];
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        double Mr[3] = {S[c][0], S[c][1], S[c][2]};
-        if (BLEND) {
-          const double sw = S[c][0] * wh[0] + S[c][1] * wh[1] + S[c][2] * wh[2];
-          Mr[0] -= sw * d[0];
-          Mr[1] -= sw * d[1];
-          Mr[2] -= sw * d[2];
-        }
-#pragma unroll
-        for (int k = 0; k < 3; ++k) R[c][k] = Mr[0] * JFi[3 * k] + Mr[1] * JFi[3 * k + 1] + Mr[2] * JFi[3 * k + 2];
-      }
-      // transpose of the barycentric gradient map
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        double Db[4];
-        Db[1] = R[c][0];
-        Db[2] = R[c][1];
-        Db[3] = R[c][2];
-        Db[0] = -(Db[1] + Db[2] + Db[3]);
-#pragma unroll
-        for (int m = 0; m < 4; ++m) {
-          Sbar[m][c] += Db[m];
-          if (m == q) {
-            acc[m][c] += 3.0 * QAB * Db[m];
-          } else {
-            acc[EI(m, q)][c] += 4.0 * QAB * Db[m];
-            acc[m][c] -= QAB * Db[m];
-          }
-        }
-      }
-    }
-  }
-  if (DO_A || DO_BT) {
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      acc[4][c] += 4.0 * QB * (Sbar[0][c] + Sbar[1][c]);
-      acc[5][c] += 4.0 * QB * (Sbar[0][c] + Sbar[2][c]);
-      acc[6][c] += 4.0 * QB * (Sbar[0][c] + Sbar[3][c]);
-      acc[7][c] += 4.0 * QB * (Sbar[1][c] + Sbar[2][c]);
-      acc[8][c] += 4.0 * QB * (Sbar[1][c] + Sbar[3][c]);
-      acc[9][c] += 4.0 * QB * (Sbar[2][c] + Sbar[3][c]);
-    }
-  }
-  if (DO_A || DO_BT || DO_DIAG) {
-#pragma unroll
-    for (int a = 0; a < 10; ++a)
-#pragma unroll
-      for (int c = 0; c < 3; ++c) atomicAdd(yu + c * cstride + nid[a], acc[a][c]);
-  }
-  if (DO_DIV) {
-#pragma unroll
-    for (int v = 0; v < 4; ++v) atomicAdd(yp + pid[v], QB * gsum + QAB * gq[v]);
-  }
-}
-
-template <bool BLEND, int MODE, bool FULL>
-static void elem_launch(const Mesh* m, const Level& L, const double* eta, double gamma, const double* u,
-                        const double* p, double* yu, double* yp, cudaStream_t s) {
-  const int64_t nm = macro_count(m);
-  dim3 grid((unsigned)((L.n_anchor[0] + 127) / 128), (unsigned)nm, 6);
-  k_elem<BLEND, MODE, FULL><<<grid, 128, 0, s>>>(m->dgeo, L.geo, L.anchors[0], L.anchors[1], L.anchors[2],
-                                                 L.n_anchor[0], L.n_anchor[1], L.n_anchor[2], L.n1, L.npts1,
-                                                 L.npts2, nm * L.npts2, eta, u, p, yu, yp, gamma);
-}
-
 static bool g_einv_ready = false;
 static int ensure_einv() {
   if (g_einv_ready) return HHG_OK;
@@ -382,32 +56,6 @@ static int ensure_einv() {
   }
   HHG_CUDA(cudaMemcpyToSymbol(cEinv, h, sizeof(h)));
   g_einv_ready = true;
-  return HHG_OK;
-}
-
-int launch_elem(const Mesh* m, const Level& L, int mode, int form, const double* eta, double gamma,
-                const double* u, const double* p, double* yu, double* yp, cudaStream_t s) {
-  const bool bl = m->blend == HHG_BLEND_SHELL;
-  const bool full = form == HHG_VISC_FULL;
-#define HHG_DISPATCH(MODE)                                                            \
-  if (bl) {                                                                           \
-    if (full) elem_launch<true, MODE, true>(m, L, eta, gamma, u, p, yu, yp, s);       \
-    else elem_launch<true, MODE, false>(m, L, eta, gamma, u, p, yu, yp, s);           \
-  } else {                                                                            \
-    if (full) elem_launch<false, MODE, true>(m, L, eta, gamma, u, p, yu, yp, s);      \
-    else elem_launch<false, MODE, false>(m, L, eta, gamma, u, p, yu, yp, s);          \
-  }
-  switch (mode) {
-    case ELEM_A: HHG_DISPATCH(ELEM_A); break;
-    case ELEM_BT: HHG_DISPATCH(ELEM_BT); break;
-    case ELEM_DIV: HHG_DISPATCH(ELEM_DIV); break;
-    case ELEM_A | ELEM_BT | ELEM_DIV: HHG_DISPATCH(ELEM_A | ELEM_BT | ELEM_DIV); break;
-    case ELEM_DIAG: HHG_DISPATCH(ELEM_DIAG); break;
-    default: return fail(HHG_EINVAL, "bad element mode");
-  }
-#undef HHG_DISPATCH
-  count_launch();
-  HHG_CUDA(cudaGetLastError());
   return HHG_OK;
 }
 
@@ -449,12 +97,14 @@ __global__ void k_fixup(int64_t ng, const int64_t* __restrict__ ptr, const int64
 int launch_fixup(const Mesh* m, const Level& L, int space, bool sum, bool bc, double* v, cudaStream_t s) {
   const int64_t nm = macro_count(m);
   if (space == HHG_P2VEC) {
-    if (L.g2.n == 0) return HHG_OK;
-    const unsigned nb = (unsigned)((L.g2.n + 255) / 256);
+    // BC-only passes visit just the groups carrying a BC (they are sorted first)
+    const int64_t ng = sum ? L.g2.n : (bc ? L.g2.nbc : 0);
+    if (ng == 0) return HHG_OK;
+    const unsigned nb = (unsigned)((ng + 255) / 256);
     if (bc)
-      k_fixup<3, true><<<nb, 256, 0, s>>>(L.g2.n, L.g2.ptr, L.g2.copy, L.g2.kind, L.g2.normal, nm * L.npts2, sum, v);
+      k_fixup<3, true><<<nb, 256, 0, s>>>(ng, L.g2.ptr, L.g2.copy, L.g2.kind, L.g2.normal, nm * L.npts2, sum, v);
     else
-      k_fixup<3, false><<<nb, 256, 0, s>>>(L.g2.n, L.g2.ptr, L.g2.copy, L.g2.kind, L.g2.normal, nm * L.npts2, sum, v);
+      k_fixup<3, false><<<nb, 256, 0, s>>>(ng, L.g2.ptr, L.g2.copy, L.g2.kind, L.g2.normal, nm * L.npts2, sum, v);
   } else if (space == HHG_P2) {
     if (L.g2.n == 0) return HHG_OK;
     const unsigned nb = (unsigned)((L.g2.n + 255) / 256);

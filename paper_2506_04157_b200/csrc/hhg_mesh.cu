@@ -61,7 +61,7 @@ void free_level(Level& L) {
     if (p) cudaFree(p);
   };
   f(L.geo);
-  for (int i = 0; i < 3; ++i) f(L.anchors[i]);
+  f(L.bricks);
   f(L.rows1);
   f(L.rows2);
   for (Groups* g : {&L.g1, &L.g2}) {
@@ -178,6 +178,8 @@ static int build_groups(const Mesh* m, const Prims& P, int N, bool with_bc, Grou
   std::vector<uint8_t> kind;
   std::vector<double> normal;
   own.assign((size_t)npts * m->local.size(), 1);
+  // two passes: groups carrying a BC first (so BC-only fixups touch just them), then the rest
+  for (int pass = 0; pass < 2; ++pass)
   for (auto& kv : P.macros) {
     const Key3& p = kv.first;
     int d = p[1] < 0 ? 0 : (p[2] < 0 ? 1 : 2);
@@ -191,6 +193,7 @@ static int build_groups(const Mesh* m, const Prims& P, int N, bool with_bc, Grou
       if (it != P.bc.end()) k = it->second;
     }
     if (loc.size() < 2 && k == HHG_BC_NONE) continue;
+    if ((pass == 0) != (k != HHG_BC_NONE)) continue;
     for_interior(d, N, [&](const int* w) {
       for (size_t c = 0; c < loc.size(); ++c) {
         int ijk[3];
@@ -211,6 +214,7 @@ static int build_groups(const Mesh* m, const Prims& P, int N, bool with_bc, Grou
     });
   }
   G.n = (int64_t)ptr.size() - 1;
+  G.nbc = with_bc ? (int64_t)std::count_if(kind.begin(), kind.end(), [](uint8_t k) { return k != HHG_BC_NONE; }) : 0;
   G.ncopy = (int64_t)copy.size();
   HHG_TRY(upload(&G.ptr, ptr));
   HHG_TRY(upload(&G.copy, copy));
@@ -271,15 +275,14 @@ int ensure_level(Mesh* m, int level) {
     G[6 * kTypeGeo] = g.absdet / ((double)n * n * n);
   }
   HHG_TRY(upload(&L.geo, geo));
-  // anchors
-  for (int cls = 0; cls < 3; ++cls) {
-    std::vector<int32_t> a;
-    int lim = n - 1 - cls;
-    for (int k = 0; k <= lim; ++k)
-      for (int j = 0; j + k <= lim; ++j)
-        for (int i = 0; i + j + k <= lim; ++i) a.push_back(i | (j << 10) | (k << 20));
-    L.n_anchor[cls] = (int64_t)a.size();
-    HHG_TRY(upload(&L.anchors[cls], a));
+  // bricks of 4x4x4 lattice cubes whose origin cube exists (i0+j0+k0 <= n-1)
+  {
+    std::vector<int32_t> b;
+    for (int k = 0; k <= n - 1; k += 4)
+      for (int j = 0; j + k <= n - 1; j += 4)
+        for (int i = 0; i + j + k <= n - 1; i += 4) b.push_back(i | (j << 10) | (k << 20));
+    L.n_bricks = (int64_t)b.size();
+    HHG_TRY(upload(&L.bricks, b));
   }
   // rows
   for (int sp = 0; sp < 2; ++sp) {
