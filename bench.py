@@ -75,6 +75,10 @@ class ClockSampler:
         time.sleep(0.25)
         self.proc.terminate()
         out, _ = self.proc.communicate(timeout=5)
+        raw = os.environ.get("HHG_CLOCKS_RAW")
+        if raw:
+            with open(raw, "a") as fh:
+                fh.write(out)
         for line in out.strip().splitlines():
             f = [x.strip() for x in line.split(",")]
             if len(f) >= 7:
