@@ -297,7 +297,7 @@ def main():
 
 # algorithmic DP flops per micro tet of the A element kernel (cross-checked
 # against ncu smsp__sass_thread_inst_executed_op_d{fma,add,mul}_pred_on)
-FLOPS_PER_TET = 1530.0      # 532 DFMA + 233 DADD + 233 DMUL per tet (ncu, profiles/r01_ncu_elem_brick_L5_summary.txt)
+FLOPS_PER_TET = 1098.0      # 352 DFMA + 228 DADD + 166 DMUL per tet, element kernel v5 (ncu, profiles/r01_ncu_elem_v5_L5_summary.txt)
 FP64_PEAK_MEASURED = 34.16  # tools/fp64_peak on this pool's B200 (profiles/r01_fp64_peak.json); DMMA 37.1 (r01_fp64_dfma_vs_dmma.json)
 TRAFFIC_PER_LAUNCH = None
 

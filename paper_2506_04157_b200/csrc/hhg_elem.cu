@@ -1,43 +1,46 @@
 // Element kernel of the hot path (sm_100a, fp64 DFMA pipe -- the operator is not a dense
-// contraction, so no tensor cores).
+// contraction, and B200's fp64 tensor path runs at the DFMA rate, so no tensor cores).
 //
 // Work decomposition ("brick"): the P1 lattice of a macro (resolution n = 2^L) is cut into
-// 4x4x4 blocks of lattice cubes; one CTA of 64 threads owns one block, one thread owns one cube
-// and evaluates the (up to) 6 micro tets of that cube (Bey/Freudenthal refinement):
-//   type 0 up {000,100,010,001}, 1-4 octahedron around diagonal 010-101, 5 down {011,101,110,111}.
-// Per tet: gather 30 velocity dofs (+4 eta, +4 p), evaluate the blending Jacobian at the 4
-// quadrature points on the fly, form 2 eta dev(eps(u)), -p I (B^T) and
-// -(div u + grad ln rho . u) (B+C), and scatter through the transpose of the barycentric
-// gradient map.  Outputs are accumulated in thread-private shared-memory slots (27 P2 nodes x 3
-// comps of the cube, + 8 P1 corners): no shared-memory atomics (sm_100a has no native fp64
-// ATOMS add).  After one __syncthreads the CTA gathers every node of the block footprint once:
-// nodes strictly inside the footprint get a plain store, footprint-border nodes one fp64 RED.
+// 4x4x4 blocks of lattice cubes; one CTA of 64 threads owns one block.  A cube holds up to 6
+// micro tets (Bey/Freudenthal refinement):
+//   type 0 up {000,100,010,001}, 1-4 octahedron around diagonal 010-101, 5 down {011,101,110,111};
+// a cube with anchor sum s has 6 tets if s <= n-3, 5 if s == n-2, 1 if s == n-1.
+//  * dense bricks (n - brick origin sum >= 5): one thread per cube, loop over its tets; outputs
+//    are accumulated in thread-private shared-memory slots (27 P2 nodes x 3 comps + 8 P1 corners
+//    of the cube; first touch stores, later touches add -- sm_100a has no native fp64 shared
+//    atomics), then each thread gathers the footprint nodes at doubled offsets {0,1}^3 of its cube
+//    (+ the brick's upper faces) from the <= 8 cubes containing them: plain store inside the brick
+//    footprint, one fp64 RED per footprint-border node.
+//  * sparse bricks (those cut by the macro's slanted face with <= 64 tets): one thread per tet,
+//    outputs go straight to global memory with fp64 REDs (the dense loop would run 6 iterations
+//    for 1 tet per thread on these bricks).
+//
+// Per tet (tet_body): gather 30 velocity dofs (+4 eta, +4 p), evaluate the blending map at the 4
+// quadrature points on the fly, and form 2 eta dev(eps(u)),
+// -p I (B^T) and -(div u + grad ln rho . u) (B+C).  Arithmetic layout:
+//   * reference gradients in barycentric form: D_m(q) = Dt_m + 4 x_m(q) (scaled by 1/(a-b)),
+//     Dt_m = (sqrt5-1) sum_j u_mj - u_m, x_m(q) = u_m if m == q else u_mq;
+//   * blending: with s = |x|^2, t = n.x, the physical gradient is grad_ref . K / (c alpha) with
+//     K = J_F^-1 - (J_F^-1 x) z^T, z = n/t - x/s, alpha = t/sqrt(s)  (rank-one closed form of
+//     J_B^-1, one rsqrt + one reciprocal per point, both MUFU-seeded + Newton);
+//   * the transposed map scatters R = S K^T through Sbar_m = sum_q Db_m(q) (vertex: -Sbar/4 +
+//     Db_m(m), edge: (sqrt5-1)/4 (Sbar_m + Sbar_j) + Db_m(j) + Db_j(m)), all constant factors
+//     folded into the per-point weight.
 #include "hhg_internal.h"
 
 namespace hhg {
 
 constexpr double EQA = 0.58541019662496845446;  // Q4 (5 + 3 sqrt 5)/20
 constexpr double EQB = 0.13819660112501051518;  // Q4 (5 - sqrt 5)/20
-constexpr double EQAB = EQA - EQB;
-constexpr double EWQ = 1.0 / 24.0;
+constexpr double EQAB = EQA - EQB;              // 1/sqrt 5
+constexpr double EWQ = 1.0 / 24.0;              // Q4 weight (reference volume 1/6, 4 points)
+constexpr double C_SB = 1.2360679774997896964;  // 4b/(a-b) = sqrt5 - 1
+constexpr double F_R = 4.0 * EQAB;              // prescale of R (folds 4(a-b) of the scatter)
+constexpr double C_V = -0.25;                   // (4b-1)/F_R
+constexpr double C_E = 0.30901699437494742410;  // 4b/F_R = (sqrt5-1)/4
 
-constexpr int kB = 4;          // cubes per brick edge
-constexpr int kBT = 64;        // threads per CTA (one per cube)
-constexpr int kFP = 2 * kB + 1;  // P2 footprint points per edge (9)
-constexpr int kFP1 = kB + 1;     // P1 footprint points per edge (5)
-
-__constant__ int eTV[6][4][3] = {
-    {{0, 0, 0}, {1, 0, 0}, {0, 1, 0}, {0, 0, 1}},
-    {{0, 1, 0}, {1, 0, 0}, {1, 0, 1}, {1, 1, 0}},
-    {{0, 0, 1}, {0, 1, 0}, {1, 0, 0}, {1, 0, 1}},
-    {{0, 1, 0}, {0, 1, 1}, {1, 0, 1}, {1, 1, 0}},
-    {{0, 0, 1}, {0, 1, 0}, {0, 1, 1}, {1, 0, 1}},
-    {{0, 1, 1}, {1, 0, 1}, {1, 1, 0}, {1, 1, 1}},
-};
-// cube-local P2 slot (a + 3b + 9c of the doubled offset) of each tet's 10 local nodes, and
-// cube-local P1 slot (a + 2b + 4c) of its 4 vertices; filled from eTV on the host side below.
-__constant__ int eSlot[6][10];
-__constant__ int ePSlot[6][4];
+constexpr int kBT = 64;  // threads per CTA; one CTA per brick of 4x4x4 lattice cubes
 
 // 32-bit lattice helpers (N <= 512 keeps (N+1)(N+2)(N+3) < 2^31)
 __device__ __forceinline__ int kbase32(int N, int k) {  // first index of plane k
@@ -49,13 +52,36 @@ __device__ __forceinline__ int rowstart32(int N, int j, int k) {  // index of (0
   return kbase32(N, k) + (j * (2 * m + 3 - j)) / 2;
 }
 
-#define EEI(m, j) (((m) == 0) ? (3 + (j)) : (((m) == 1) ? (((j) == 0) ? 4 : 5 + (j)) : (((m) == 2) ? (((j) == 0) ? 5 : ((j) == 1 ? 7 : 9)) : (((j) == 0) ? 6 : ((j) == 1 ? 8 : 9)))))
+// local edge index of edge (m, j), m != j (edges 01,02,03,12,13,23 -> 4..9)
+__host__ __device__ constexpr int EEI(int m, int j) {
+  return (m + j == 1) ? 4 : (m + j == 2) ? 5 : (m * j == 0) ? 6 : (m + j == 3) ? 7 : (m + j == 4) ? 8 : 9;
+}
 
-// One micro tet.  G: [JFinv(9) | qoff(4x3)] of the tet's type; xa: unblended anchor position.
-// acc[10][3]: velocity outputs (local P2 order v0..v3, e01..e23); gy[4]: P1 outputs.
-template <bool BLEND, int MODE, bool FULL>
-__device__ __forceinline__ void tet_body(const double* __restrict__ G, double absdetF, const double (&xa)[3],
-                                         const double (&nh)[3], double cK, double gamma, const double (&uu)[10][3],
+// fp64 reciprocal / reciprocal square root: MUFU seed (rcp/rsqrt.approx.ftz.f64) + Newton.
+// Arguments are positive normal numbers here (|x|^2 >= 0.3, n.x >= 0.5 on the shell).
+__device__ __forceinline__ double rcp_nr(double t) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(t));
+  double e = fma(-t, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-t, r, 1.0);
+  return fma(r, e, r);
+}
+__device__ __forceinline__ double rsqrt_nr(double s) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(s));
+  const double hs = 0.5 * s;
+  y = y * fma(-hs * y, y, 1.5);
+  y = y * fma(-hs * y, y, 1.5);
+  return y;
+}
+
+// Element outputs of one micro tet.  G: [JFinv(9) | qoff(4x3)] of the tet's type;
+// wdet = w |det J_F| of the level; xa: unblended anchor position.
+// acc[10][3]: velocity outputs (v0..v3, e01..e23); gy[4]: P1 outputs.
+template <bool BLEND, int MODE, bool FULL, class UA>
+__device__ __forceinline__ void tet_body(const double* G, double wdet, const double (&xa)[3],
+                                         const double (&nh)[3], double cK, double gamma, const UA& uu,
                                          const double (&et)[4], const double (&pp)[4], double (&acc)[10][3],
                                          double (&gy)[4]) {
   constexpr bool DO_A = (MODE & ELEM_A) != 0;
@@ -63,71 +89,121 @@ __device__ __forceinline__ void tet_body(const double* __restrict__ G, double ab
   constexpr bool DO_DIV = (MODE & ELEM_DIV) != 0;
   constexpr bool DO_DIAG = (MODE & ELEM_DIAG) != 0;
   constexpr bool NEED_U = DO_A || DO_DIV;
-  double JFi[9];
-#pragma unroll
-  for (int r = 0; r < 9; ++r) JFi[r] = __ldg(G + r);
+  constexpr bool SCATTER = DO_A || DO_BT;
+
   const double etaS = EQB * (et[0] + et[1] + et[2] + et[3]);
   const double pS = EQB * (pp[0] + pp[1] + pp[2] + pp[3]);
-  // D_m(lambda) = sum_j lambda_j C_mj, C_mm = 3u_m, C_mj = 4u_mj - u_m; at the Q4 point q:
-  // D_m(q) = Sb_m + (a-b) C_mq with Sb_m = 4 b sum_{j!=m} u_mj;  grad_xi u = D_k - D_0.
-  double Sb[4][3];
+  // per-macro constant factors of the point weights
+  const double cwA = (DO_DIAG ? 2.0 : 2.0 * F_R * EQAB) * wdet * cK;  // x eta_q alpha
+  const double cwB = F_R * wdet * cK * cK;                            // x alpha^2 p_q
+  const double cwD = wdet * cK * cK;                                  // x alpha^2 (div rows)
+
+  // Delta_k = Dt_k - Dt_0 (k = 1..3), Dt_m = C_SB sum_{j != m} u_mj - u_m
+  double Dl[3][3];
   if (NEED_U) {
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      Sb[0][c] = 4.0 * EQB * (uu[4][c] + uu[5][c] + uu[6][c]);
-      Sb[1][c] = 4.0 * EQB * (uu[4][c] + uu[7][c] + uu[8][c]);
-      Sb[2][c] = 4.0 * EQB * (uu[5][c] + uu[7][c] + uu[9][c]);
-      Sb[3][c] = 4.0 * EQB * (uu[6][c] + uu[8][c] + uu[9][c]);
+      const double d0 = fma(C_SB, uu(4, c) + uu(5, c) + uu(6, c), -uu(0, c));
+      const double d1 = fma(C_SB, uu(4, c) + uu(7, c) + uu(8, c), -uu(1, c));
+      const double d2 = fma(C_SB, uu(5, c) + uu(7, c) + uu(9, c), -uu(2, c));
+      const double d3 = fma(C_SB, uu(6, c) + uu(8, c) + uu(9, c), -uu(3, c));
+      Dl[0][c] = d1 - d0;
+      Dl[1][c] = d2 - d0;
+      Dl[2][c] = d3 - d0;
     }
   }
+  // u at the quadrature points (div rows): u_q = B0 + (phq-phv) u_q + (peq-pen) sum_{e ∋ q} u_e
+  constexpr double phv = EQB * (2.0 * EQB - 1.0), phq = EQA * (2.0 * EQA - 1.0);
+  constexpr double peq = 4.0 * EQA * EQB, pen = 4.0 * EQB * EQB;
+  double B0[3] = {0, 0, 0};
+  if (DO_DIV) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      B0[c] = phv * (uu(0, c) + uu(1, c) + uu(2, c) + uu(3, c)) +
+              pen * (uu(4, c) + uu(5, c) + uu(6, c) + uu(7, c) + uu(8, c) + uu(9, c));
+  }
   double Sbar[4][3];
-#pragma unroll
-  for (int a = 0; a < 10; ++a)
-#pragma unroll
-    for (int c = 0; c < 3; ++c) acc[a][c] = 0.0;
-#pragma unroll
-  for (int m = 0; m < 4; ++m)
-#pragma unroll
-    for (int c = 0; c < 3; ++c) Sbar[m][c] = 0.0;
   double gq[4] = {0, 0, 0, 0}, gsum = 0.0;
+  if (DO_DIAG) {
+#pragma unroll
+    for (int a = 0; a < 10; ++a)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) acc[a][c] = 0.0;
+  }
+
+  // ---- geometry of the 4 quadrature points first, written point-parallel (4 independent
+  // chains through the rsqrt/rcp Newton iterations): K_q = JFi - (JFi x_q) z_q^T,
+  // z_q = n/t_q - x_q/s_q, alpha_q = t_q/sqrt(s_q)  (rank-one J_B^-1)
+  double JFi[9];
+#pragma unroll
+  for (int r = 0; r < 9; ++r) JFi[r] = G[r];
+  double Kq[4][9], al[4] = {1.0, 1.0, 1.0, 1.0}, dq[4][3];
+  {
+    double xq[4][3], sq[4], yq[4], tq[4], rq[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int r = 0; r < 3; ++r) xq[q][r] = xa[r] + G[9 + 3 * q + r];
+    if (BLEND || DO_DIV) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) sq[q] = fma(xq[q][0], xq[q][0], fma(xq[q][1], xq[q][1], xq[q][2] * xq[q][2]));
+#pragma unroll
+      for (int q = 0; q < 4; ++q) yq[q] = rsqrt_nr(sq[q]);
+    }
+    if (DO_DIV) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int r = 0; r < 3; ++r) dq[q][r] = xq[q][r] * yq[q];
+    }
+    if (BLEND) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) tq[q] = fma(nh[0], xq[q][0], fma(nh[1], xq[q][1], nh[2] * xq[q][2]));
+#pragma unroll
+      for (int q = 0; q < 4; ++q) rq[q] = rcp_nr(tq[q]);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        al[q] = tq[q] * yq[q];
+        const double y2 = yq[q] * yq[q];
+        double z[3], v[3];
+#pragma unroll
+        for (int r = 0; r < 3; ++r) z[r] = fma(rq[q], nh[r], -xq[q][r] * y2);
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+          v[k] = fma(JFi[3 * k], xq[q][0], fma(JFi[3 * k + 1], xq[q][1], JFi[3 * k + 2] * xq[q][2]));
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+#pragma unroll
+          for (int l = 0; l < 3; ++l) Kq[q][3 * k + l] = fma(-v[k], z[l], JFi[3 * k + l]);
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int r = 0; r < 9; ++r) Kq[q][r] = JFi[r];
+    }
+  }
 
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    double xq[3];
-#pragma unroll
-    for (int r = 0; r < 3; ++r) xq[r] = xa[r] + __ldg(G + 9 + 3 * q + r);
-    // blending at x_q: d = x/|x|, alpha = n.d, J_B^-1 = (I - d w^T)/(c alpha), w = n/alpha - d
-    double d[3] = {0, 0, 0}, wh[3] = {0, 0, 0}, ca = 1.0;
-    if (BLEND || DO_DIV) {
-      const double ri = rsqrt(xq[0] * xq[0] + xq[1] * xq[1] + xq[2] * xq[2]);
-      d[0] = xq[0] * ri;
-      d[1] = xq[1] * ri;
-      d[2] = xq[2] * ri;
-    }
-    if (BLEND) {
-      const double alpha = nh[0] * d[0] + nh[1] * d[1] + nh[2] * d[2];
-      const double ia = 1.0 / alpha;
-      wh[0] = nh[0] * ia - d[0];
-      wh[1] = nh[1] * ia - d[1];
-      wh[2] = nh[2] * ia - d[2];
-      ca = cK * alpha;
-    }
-    const double etaq = etaS + EQAB * et[q];
-    // 2 eta w |det J_F| |det J_B| / (c alpha)^2 = 2 eta w |det J_F| c alpha
-    const double sA = 2.0 * etaq * EWQ * absdetF * ca;
+    const double* K = Kq[q];
+    const double alpha = al[q];
+    const double* d = dq[q];
+    const double etaq = fma(EQAB, et[q], etaS);
 
     if (DO_DIAG) {
+      // diag(A): sum_q 2 eta w|det J| [eps(phi_a e_c) : eps(phi_a e_c) - 1/3 (div)^2]
+      const double sA = cwA * etaq * alpha;
 #pragma unroll
       for (int a = 0; a < 10; ++a) {
         double gh[3];
         if (a < 4) {
-          const double lam = (a == q) ? EQA : EQB;
-          const double f = 4.0 * lam - 1.0;
+          const double f = 4.0 * ((a == q) ? EQA : EQB) - 1.0;
           gh[0] = (a == 0) ? -f : (a == 1 ? f : 0.0);
           gh[1] = (a == 0) ? -f : (a == 2 ? f : 0.0);
           gh[2] = (a == 0) ? -f : (a == 3 ? f : 0.0);
         } else {
-          const int ep[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
+          constexpr int ep[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
           const int i0 = ep[a - 4][0], j0 = ep[a - 4][1];
           const double li = (i0 == q) ? EQA : EQB, lj = (j0 == q) ? EQA : EQB;
 #pragma unroll
@@ -139,13 +215,7 @@ __device__ __forceinline__ void tet_body(const double* __restrict__ G, double ab
         }
         double gx[3];
 #pragma unroll
-        for (int l = 0; l < 3; ++l) gx[l] = gh[0] * JFi[l] + gh[1] * JFi[3 + l] + gh[2] * JFi[6 + l];
-        if (BLEND) {
-          const double gd = gx[0] * d[0] + gx[1] * d[1] + gx[2] * d[2];
-          gx[0] -= gd * wh[0];
-          gx[1] -= gd * wh[1];
-          gx[2] -= gd * wh[2];
-        }
+        for (int l = 0; l < 3; ++l) gx[l] = gh[0] * K[l] + gh[1] * K[3 + l] + gh[2] * K[6 + l];
         const double n2g = gx[0] * gx[0] + gx[1] * gx[1] + gx[2] * gx[2];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
@@ -156,183 +226,200 @@ __device__ __forceinline__ void tet_body(const double* __restrict__ G, double ab
       continue;
     }
 
-    double H[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+    // Ht = grad_ref(u)/(a-b) . K   (physical gradient = (a-b) Ht / (c alpha))
+    double H[3][3];
     if (NEED_U) {
-      double gh[3][3];
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        double D[4];
+        const double x0 = (q == 0) ? uu(0, c) : uu(EEI(0, q), c);
+        double gh[3];
 #pragma unroll
-        for (int m = 0; m < 4; ++m) {
-          const double Cmq = (m == q) ? 3.0 * uu[m][c] : 4.0 * uu[EEI(m, q)][c] - uu[m][c];
-          D[m] = Sb[m][c] + EQAB * Cmq;
+        for (int k = 0; k < 3; ++k) {
+          const double xk = (q == k + 1) ? uu(k + 1, c) : uu(EEI(k + 1, q), c);
+          gh[k] = fma(4.0, xk - x0, Dl[k][c]);
         }
-        gh[c][0] = D[1] - D[0];
-        gh[c][1] = D[2] - D[0];
-        gh[c][2] = D[3] - D[0];
-      }
-      // G = gh J_F^-1 ;  H = G - (G d) w^T   (grad_x u = H / (c alpha))
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-#pragma unroll
-        for (int l = 0; l < 3; ++l) H[c][l] = gh[c][0] * JFi[l] + gh[c][1] * JFi[3 + l] + gh[c][2] * JFi[6 + l];
-        if (BLEND) {
-          const double gd = H[c][0] * d[0] + H[c][1] * d[1] + H[c][2] * d[2];
-          H[c][0] -= gd * wh[0];
-          H[c][1] -= gd * wh[1];
-          H[c][2] -= gd * wh[2];
-        }
+        for (int l = 0; l < 3; ++l) H[c][l] = fma(gh[0], K[l], fma(gh[1], K[3 + l], gh[2] * K[6 + l]));
       }
     }
     if (DO_DIV) {
-      // g_q = -W (div u + grad ln rho . u),  div u = tr(H)/(c alpha),  grad ln rho = -gamma d
-      double uq[3];
-      const double phv = EQB * (2.0 * EQB - 1.0), phq = EQA * (2.0 * EQA - 1.0);
-      const double peq = 4.0 * EQA * EQB, pen = 4.0 * EQB * EQB;
+      // g_q = -w|det J_F| (c alpha)^2 [ (a-b) tr Ht - gamma c alpha d.u_q ]   (grad ln rho = -gamma d)
+      double du = 0.0;
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        double s = 0.0;
+        double es = 0.0;
 #pragma unroll
-        for (int a = 0; a < 4; ++a) s += ((a == q) ? phq : phv) * uu[a][c];
-        const int ep[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
-#pragma unroll
-        for (int e = 0; e < 6; ++e) s += ((ep[e][0] == q || ep[e][1] == q) ? peq : pen) * uu[4 + e][c];
-        uq[c] = s;
+        for (int m = 0; m < 4; ++m)
+          if (m != q) es += uu(EEI(m, q), c);
+        const double uqc = fma(peq - pen, es, fma(phq - phv, uu(q, c), B0[c]));
+        du = fma(d[c], uqc, du);
       }
-      const double W = EWQ * absdetF * ca * ca * ca;
-      const double div = (H[0][0] + H[1][1] + H[2][2]) / ca;
-      const double gg = -W * (div - gamma * (d[0] * uq[0] + d[1] * uq[1] + d[2] * uq[2]));
+      const double trH = H[0][0] + H[1][1] + H[2][2];
+      const double gg = -cwD * alpha * alpha * fma(EQAB, trH, -gamma * cK * alpha * du);
       gq[q] = gg;
       gsum += gg;
     }
-    if (DO_A || DO_BT) {
+    if (SCATTER) {
+      // S = F_R * (stress at q) * weight, symmetric
       double S[3][3];
       if (DO_A) {
-        const double tr3 = (H[0][0] + H[1][1] + H[2][2]) * (1.0 / 3.0);
+        const double sA = cwA * etaq * alpha;
         if (FULL) {
-          S[0][0] = sA * (H[0][0] - tr3);
-          S[1][1] = sA * (H[1][1] - tr3);
-          S[2][2] = sA * (H[2][2] - tr3);
+          const double m3 = sA * (1.0 / 3.0) * (H[0][0] + H[1][1] + H[2][2]);
+          S[0][0] = fma(sA, H[0][0], -m3);
+          S[1][1] = fma(sA, H[1][1], -m3);
+          S[2][2] = fma(sA, H[2][2], -m3);
         } else {
           S[0][0] = sA * H[0][0];
           S[1][1] = sA * H[1][1];
           S[2][2] = sA * H[2][2];
         }
-        S[0][1] = S[1][0] = 0.5 * sA * (H[0][1] + H[1][0]);
-        S[0][2] = S[2][0] = 0.5 * sA * (H[0][2] + H[2][0]);
-        S[1][2] = S[2][1] = 0.5 * sA * (H[1][2] + H[2][1]);
+        const double hs = 0.5 * sA;
+        S[0][1] = S[1][0] = hs * (H[0][1] + H[1][0]);
+        S[0][2] = S[2][0] = hs * (H[0][2] + H[2][0]);
+        S[1][2] = S[2][1] = hs * (H[1][2] + H[2][1]);
       } else {
 #pragma unroll
         for (int c = 0; c < 3; ++c)
 #pragma unroll
           for (int l = 0; l < 3; ++l) S[c][l] = 0.0;
       }
-      if (DO_BT) {
-        // B^T p: isotropic stress -p_q W I, scaled by 1/(c alpha)
-        const double pq = pS + EQAB * pp[q];
-        const double wb = EWQ * absdetF * ca * ca * pq;
+      if (DO_BT) {  // B^T p: isotropic stress -p_q W I / (c alpha)
+        const double wb = cwB * alpha * alpha * fma(EQAB, pp[q], pS);
         S[0][0] -= wb;
         S[1][1] -= wb;
         S[2][2] -= wb;
       }
-      // M = S - (S w) d^T ; R = M J_F^-T
-      double R[3][3];
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        double Mr[3] = {S[c][0], S[c][1], S[c][2]};
-        if (BLEND) {
-          const double sw = S[c][0] * wh[0] + S[c][1] * wh[1] + S[c][2] * wh[2];
-          Mr[0] -= sw * d[0];
-          Mr[1] -= sw * d[1];
-          Mr[2] -= sw * d[2];
-        }
-#pragma unroll
-        for (int k = 0; k < 3; ++k) R[c][k] = Mr[0] * JFi[3 * k] + Mr[1] * JFi[3 * k + 1] + Mr[2] * JFi[3 * k + 2];
-      }
-      // transpose of the barycentric gradient map
+      // R = S K^T ; Db_k = R[c][k-1], Db_0 = -(sum)
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         double Db[4];
-        Db[1] = R[c][0];
-        Db[2] = R[c][1];
-        Db[3] = R[c][2];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) Db[k + 1] = fma(S[c][0], K[3 * k], fma(S[c][1], K[3 * k + 1], S[c][2] * K[3 * k + 2]));
         Db[0] = -(Db[1] + Db[2] + Db[3]);
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
-          Sbar[m][c] += Db[m];
+          if (q == 0) Sbar[m][c] = Db[m];
+          else Sbar[m][c] += Db[m];
           if (m == q) {
-            acc[m][c] += 3.0 * EQAB * Db[m];
+            acc[m][c] = Db[m];
           } else {
-            acc[EEI(m, q)][c] += 4.0 * EQAB * Db[m];
-            acc[m][c] -= EQAB * Db[m];
+            if (q < m) acc[EEI(m, q)][c] = Db[m];  // edge (q,m), q < m: first contribution
+            else acc[EEI(m, q)][c] += Db[m];
           }
         }
       }
     }
   }
-  if (DO_A || DO_BT) {
+  if (SCATTER) {
+    constexpr int ep[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      acc[4][c] += 4.0 * EQB * (Sbar[0][c] + Sbar[1][c]);
-      acc[5][c] += 4.0 * EQB * (Sbar[0][c] + Sbar[2][c]);
-      acc[6][c] += 4.0 * EQB * (Sbar[0][c] + Sbar[3][c]);
-      acc[7][c] += 4.0 * EQB * (Sbar[1][c] + Sbar[2][c]);
-      acc[8][c] += 4.0 * EQB * (Sbar[1][c] + Sbar[3][c]);
-      acc[9][c] += 4.0 * EQB * (Sbar[2][c] + Sbar[3][c]);
+#pragma unroll
+      for (int m = 0; m < 4; ++m) acc[m][c] = fma(C_V, Sbar[m][c], acc[m][c]);
+#pragma unroll
+      for (int e = 0; e < 6; ++e) acc[4 + e][c] = fma(C_E, Sbar[ep[e][0]][c] + Sbar[ep[e][1]][c], acc[4 + e][c]);
+    }
+  }
+  if (DO_DIV) {
+#pragma unroll
+    for (int v = 0; v < 4; ++v) gy[v] = fma(EQB, gsum, EQAB * gq[v]);
+  }
+}
+
+// ---------------------------------------------------------------- tables (uploaded once)
+// Per tet type t and local node a: cube-local P2 slot sl = dx + 3dy + 9dz of the doubled offset,
+// packed load index (row (dy + 3dz) << 2 | dx), first-touch flags in type order 0..5 (the first
+// touch of a cube slot stores, later touches add), P1 corner slots; sparse-brick item lists.
+constexpr int kNS2 = 81;  // P2 slots per cube (27 nodes x 3)
+constexpr int kNS1 = 8;   // P1 slots per cube
+__constant__ int eSlot[6][10];
+__constant__ int eLd[6][10];
+__constant__ int ePSlot[6][4];
+__constant__ int eFirst[6];
+__constant__ int ePFirst[6];
+__device__ int eItems[5][64];  // delta = n - (i0+j0+k0) in 1..4: item = cube | type << 6
+__device__ int eNItems[5];
+
+constexpr int kGeoSm = 6 * kTypeGeo + 2;  // staged per-macro element geometry (doubles)
+
+// Array accessor for tet_body
+struct RegU {
+  const double (&u)[10][3];
+  __device__ __forceinline__ double operator()(int a, int c) const { return u[a][c]; }
+};
+
+template <int MODE>
+__device__ __forceinline__ void load_tet(int t, const int* rs2, const int* rs1, const double* __restrict__ um,
+                                         int64_t cstride, const double* __restrict__ em,
+                                         const double* __restrict__ pm, double (&uu)[10][3], double (&et)[4],
+                                         double (&pp)[4]) {
+  constexpr bool NEED_U = (MODE & (ELEM_A | ELEM_DIV)) != 0;
+  constexpr bool NEED_ETA = (MODE & (ELEM_A | ELEM_DIAG)) != 0;
+  constexpr bool NEED_P = (MODE & ELEM_BT) != 0;
+  if (NEED_U) {
+#pragma unroll
+    for (int a = 0; a < 10; ++a) {
+      const int pk = eLd[t][a];
+      const double* pa = um + rs2[(pk >> 2) * kBT] + (pk & 3);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) uu[a][c] = __ldg(pa + c * cstride);
     }
   }
 #pragma unroll
-  for (int v = 0; v < 4; ++v) gy[v] = EQB * gsum + EQAB * gq[v];
+  for (int v = 0; v < 4; ++v) {
+    const int ps = ePSlot[t][v];
+    const int ix = rs1[(ps >> 1) * kBT] + (ps & 1);
+    et[v] = (NEED_ETA && em != nullptr) ? __ldg(em + ix) : 1.0;
+    pp[v] = NEED_P ? __ldg(pm + ix) : 0.0;
+  }
 }
 
 template <bool BLEND, int MODE, bool FULL>
 #ifndef HHG_ELEM_MINB
 #define HHG_ELEM_MINB 4
 #endif
-__global__ void __launch_bounds__(kBT, HHG_ELEM_MINB) k_elem_brick(const MacroGeo* __restrict__ mgeo, const double* __restrict__ lgeo,
-                                                    const int32_t* __restrict__ bricks, int n1, int64_t npts1,
-                                                    int64_t npts2, int64_t cstride, const double* __restrict__ eta,
-                                                    const double* __restrict__ u, const double* __restrict__ p,
-                                                    double* __restrict__ yu, double* __restrict__ yp, double gamma) {
+__global__ void __launch_bounds__(kBT, HHG_ELEM_MINB)
+    k_elem_brick(const MacroGeo* __restrict__ mgeo, const double* __restrict__ lgeo, const int32_t* __restrict__ bricks,
+                 int n1, double inv_n1, int64_t npts1, int64_t npts2, int64_t cstride, const double* __restrict__ eta,
+                 const double* __restrict__ u, const double* __restrict__ p, double* __restrict__ yu,
+                 double* __restrict__ yp, double gamma) {
   constexpr bool DO_DIV = (MODE & ELEM_DIV) != 0;
   constexpr bool HAS_U_OUT = (MODE & (ELEM_A | ELEM_BT | ELEM_DIAG)) != 0;
-  constexpr bool NEED_U = (MODE & (ELEM_A | ELEM_DIV)) != 0;
-  constexpr bool NEED_ETA = (MODE & (ELEM_A | ELEM_DIAG)) != 0;
-  constexpr bool NEED_P = (MODE & ELEM_BT) != 0;
-  constexpr int NSU = HAS_U_OUT ? 81 : 0;
-  constexpr int NS = NSU + (DO_DIV ? 8 : 0);
-  extern __shared__ double sm[];  // [NS][kBT]
+  constexpr int NSU = HAS_U_OUT ? kNS2 : 0;
+  constexpr int NS = NSU + (DO_DIV ? kNS1 : 0);
+  extern __shared__ double sm[];  // [NS][kBT] cube slots | geometry [kGeoSm] | row starts int[13][kBT]
+  double* sgeo = sm + NS * kBT;
+  int* rs2 = reinterpret_cast<int*>(sgeo + kGeoSm) + threadIdx.x;  // [9][kBT]
+  int* rs1 = rs2 + 9 * kBT;                                         // [4][kBT]
 
   const int mac = blockIdx.y;
   const int32_t bpk = __ldg(bricks + blockIdx.x);
   const int i0 = bpk & 1023, j0 = (bpk >> 10) & 1023, k0 = bpk >> 20;
+  const int delta = n1 - (i0 + j0 + k0);
   const int tid = threadIdx.x;
-  const int ti = tid & 3, tj = (tid >> 2) & 3, tk = tid >> 4;
-  const int ai = i0 + ti, aj = j0 + tj, ak = k0 + tk;
-  const int s = ai + aj + ak;
   const int n2 = 2 * n1;
-#pragma unroll 1
-  for (int sl = 0; sl < NS; ++sl) sm[sl * kBT + tid] = 0.0;
 
-  if (s <= n1 - 1) {
-    const MacroGeo& g = mgeo[mac];
-    double nh[3] = {0, 0, 0}, cK = 1.0;
-    if (BLEND) {
-      nh[0] = g.nhat[0];
-      nh[1] = g.nhat[1];
-      nh[2] = g.nhat[2];
-      cK = g.cK;
-    }
-    const double fa = (double)ai / n1, fb = (double)aj / n1, fc = (double)ak / n1;
-    double xa[3];
+  const double* Gm = lgeo + (int64_t)mac * kLevelGeo;
+  for (int r = tid; r < kGeoSm; r += kBT) sgeo[r] = __ldg(Gm + r);
+  const MacroGeo& g = mgeo[mac];
+  double nh[3] = {0, 0, 0}, cK = 1.0;
+  if (BLEND) {
+    nh[0] = g.nhat[0];
+    nh[1] = g.nhat[1];
+    nh[2] = g.nhat[2];
+    cK = g.cK;
+  }
+  const double* um = u + (int64_t)mac * npts2;
+  const double* em = eta ? eta + (int64_t)mac * npts1 : nullptr;
+  const double* pm = p ? p + (int64_t)mac * npts1 : nullptr;
+  double* yum = yu + (int64_t)mac * npts2;
+  double* ypm = yp ? yp + (int64_t)mac * npts1 : nullptr;
+
+  auto cube_setup = [&](int ai, int aj, int ak, double (&xa)[3]) {
+    const double fa = ai * inv_n1, fb = aj * inv_n1, fc = ak * inv_n1;  // exact: n1 = 2^L
 #pragma unroll
     for (int r = 0; r < 3; ++r) xa[r] = g.X0[r] + g.Jm[3 * r] * fa + g.Jm[3 * r + 1] * fb + g.Jm[3 * r + 2] * fc;
-    const double* Gm = lgeo + (int64_t)mac * kLevelGeo;
-    const double absdetF = __ldg(Gm + 6 * kTypeGeo);
-    // per-cube row starts: P2 rows (2aj+b, 2ak+c), b,c in 0..2 ; P1 rows (aj+b, ak+c), b,c in 0..1
-    // (kept in per-thread shared-memory slots: the tet loop indexes them with runtime values)
-    int* rs2 = reinterpret_cast<int*>(sm + NS * kBT) + tid;  // stride kBT
-    int* rs1 = rs2 + 9 * kBT;
 #pragma unroll
     for (int c = 0; c < 3; ++c)
 #pragma unroll
@@ -341,102 +428,173 @@ __global__ void __launch_bounds__(kBT, HHG_ELEM_MINB) k_elem_brick(const MacroGe
     for (int c = 0; c < 2; ++c)
 #pragma unroll
       for (int b = 0; b < 2; ++b) rs1[(b + 2 * c) * kBT] = rowstart32(n1, aj + b, ak + c) + ai;
-    const double* um = u + (int64_t)mac * npts2;
-    const double* em = eta ? eta + (int64_t)mac * npts1 : nullptr;
-    const double* pm = p ? p + (int64_t)mac * npts1 : nullptr;
-    const int ntypes = (s <= n1 - 3) ? 6 : ((s <= n1 - 2) ? 5 : 1);
+  };
+  __syncthreads();
+  const double wdet = EWQ * sgeo[6 * kTypeGeo];
+
+  if (delta <= 4) {
+    // ---------------- sparse brick (<= 64 tets): one tet per thread, fp64 REDs to global memory
+    if (tid >= eNItems[delta]) return;
+    const int item = eItems[delta][tid];
+    const int cube = item & 63, t = item >> 6;
+    const int ai = i0 + (cube & 3), aj = j0 + ((cube >> 2) & 3), ak = k0 + (cube >> 4);
+    double xa[3];
+    cube_setup(ai, aj, ak, xa);
+    double uu[10][3], et[4], pp[4], acc[10][3], gy[4];
+    load_tet<MODE>(t, rs2, rs1, um, cstride, em, pm, uu, et, pp);
+    tet_body<BLEND, MODE, FULL>(sgeo + t * kTypeGeo, wdet, xa, nh, cK, gamma, RegU{uu}, et, pp, acc, gy);
+    if (HAS_U_OUT) {
+#pragma unroll
+      for (int a = 0; a < 10; ++a) {
+        const int pk = eLd[t][a];
+        double* pa = yum + rs2[(pk >> 2) * kBT] + (pk & 3);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) atomicAdd(pa + c * cstride, acc[a][c]);
+      }
+    }
+    if (DO_DIV) {
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int ps = ePSlot[t][v];
+        atomicAdd(ypm + rs1[(ps >> 1) * kBT] + (ps & 1), gy[v]);
+      }
+    }
+    return;
+  }
+
+  // ---------------- dense brick: one thread per cube, private shared-memory slots
+  const int ti = tid & 3, tj = (tid >> 2) & 3, tk = tid >> 4;
+  const int ai = i0 + ti, aj = j0 + tj, ak = k0 + tk;
+  const int s = ai + aj + ak;
+  const int ntypes = (s <= n1 - 3) ? 6 : ((s == n1 - 2) ? 5 : ((s == n1 - 1) ? 1 : 0));
+  if (ntypes < 6) {  // partial cube: the slots its tets never touch must read as zero in the gather
 #pragma unroll 1
-    for (int t = 0; t < ntypes; ++t) {  // s <= n-1: up only; s <= n-2: + octahedron (1-4); s <= n-3: + down
-      double uu[10][3];
-      if (NEED_U) {
-#pragma unroll
-        for (int a = 0; a < 10; ++a) {
-          const int sl = eSlot[t][a];  // doubled offset (sl%3, (sl/3)%3, sl/9) inside the cube
-          const int ix = rs2[(sl / 3) * kBT] + sl % 3;
-#pragma unroll
-          for (int c = 0; c < 3; ++c) uu[a][c] = __ldg(um + c * cstride + ix);
-        }
-      }
-      double et[4] = {1.0, 1.0, 1.0, 1.0}, pp[4] = {0, 0, 0, 0};
-      if ((NEED_ETA && eta != nullptr) || NEED_P) {
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          const int ps = ePSlot[t][v];  // (ps&1, (ps>>1)&1, ps>>2)
-          const int ix = rs1[(ps >> 1) * kBT] + (ps & 1);
-          if (NEED_ETA && eta != nullptr) et[v] = __ldg(em + ix);
-          if (NEED_P) pp[v] = __ldg(pm + ix);
-        }
-      }
-      double acc[10][3], gy[4];
-      tet_body<BLEND, MODE, FULL>(Gm + t * kTypeGeo, absdetF, xa, nh, cK, gamma, uu, et, pp, acc, gy);
+    for (int sl = 0; sl < NS; ++sl) sm[sl * kBT + tid] = 0.0;
+  }
+  if (ntypes > 0) {
+    double xa[3];
+    cube_setup(ai, aj, ak, xa);
+#pragma unroll 1
+    for (int t = 0; t < ntypes; ++t) {
+      double uu[10][3], et[4], pp[4], acc[10][3], gy[4];
+      load_tet<MODE>(t, rs2, rs1, um, cstride, em, pm, uu, et, pp);
+      tet_body<BLEND, MODE, FULL>(sgeo + t * kTypeGeo, wdet, xa, nh, cK, gamma, RegU{uu}, et, pp, acc, gy);
       if (HAS_U_OUT) {
+        const int first = eFirst[t];
 #pragma unroll
         for (int a = 0; a < 10; ++a) {
-          const int sl = eSlot[t][a];
+          double* sl = sm + 3 * eSlot[t][a] * kBT + tid;
+          if ((first >> a) & 1) {
 #pragma unroll
-          for (int c = 0; c < 3; ++c) sm[(3 * sl + c) * kBT + tid] += acc[a][c];
+            for (int c = 0; c < 3; ++c) sl[c * kBT] = acc[a][c];
+          } else {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) sl[c * kBT] += acc[a][c];
+          }
         }
       }
       if (DO_DIV) {
+        const int first = ePFirst[t];
 #pragma unroll
-        for (int v = 0; v < 4; ++v) sm[(NSU + ePSlot[t][v]) * kBT + tid] += gy[v];
+        for (int v = 0; v < 4; ++v) {
+          double* sl = sm + (NSU + ePSlot[t][v]) * kBT + tid;
+          if ((first >> v) & 1) *sl = gy[v];
+          else *sl += gy[v];
+        }
       }
     }
   }
   __syncthreads();
 
-  // gather the brick footprint: each node once (sum over the <= 8 cubes of the brick containing it)
-  if (HAS_U_OUT) {
-    const int64_t mbase2 = (int64_t)mac * npts2;
+  // gather.  Footprint point P = 2p + o (per dimension) of "position" p in [0,4]: round 0 takes the
+  // 64 positions p in [0,3]^3 (p = the thread's cube), round 1 the 61 positions on the upper faces
+  // (some p_d = 4; only o_d = 0 there).  Per dimension the point lies in cube p (slot o, if p <= 3)
+  // and, when o = 0, in cube p-1 (slot 2, if p >= 1).  Footprint-border points (P_d in {0, 8})
+  // are shared with other bricks: fp64 RED; all others get a plain store.
 #pragma unroll 1
-    for (int pt = tid; pt < kFP * kFP * kFP; pt += kBT) {
-      const int px = pt % kFP, py = (pt / kFP) % kFP, pz = pt / (kFP * kFP);
-      const int gx = 2 * i0 + px, gy_ = 2 * j0 + py, gz = 2 * k0 + pz;
-      if (gx + gy_ + gz > n2) continue;
-      const int lx0 = (px & 1) ? (px >> 1) : (px >> 1) - 1, lx1 = min(px >> 1, kB - 1);
-      const int ly0 = (py & 1) ? (py >> 1) : (py >> 1) - 1, ly1 = min(py >> 1, kB - 1);
-      const int lz0 = (pz & 1) ? (pz >> 1) : (pz >> 1) - 1, lz1 = min(pz >> 1, kB - 1);
-      double v[3] = {0.0, 0.0, 0.0};
-      for (int lz = max(lz0, 0); lz <= lz1; ++lz)
-        for (int ly = max(ly0, 0); ly <= ly1; ++ly)
-          for (int lx = max(lx0, 0); lx <= lx1; ++lx) {
-            const int sl = (px - 2 * lx) + 3 * (py - 2 * ly) + 9 * (pz - 2 * lz);
-            const int cube = lx + kB * ly + kB * kB * lz;
-#pragma unroll
-            for (int c = 0; c < 3; ++c) v[c] += sm[(3 * sl + c) * kBT + cube];
-          }
-      const int64_t idx = mbase2 + rowstart32(n2, gy_, gz) + gx;
-      const bool border = px == 0 || py == 0 || pz == 0 || px == kFP - 1 || py == kFP - 1 || pz == kFP - 1;
-      if (border) {
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-          if (v[c] != 0.0) atomicAdd(yu + c * cstride + idx, v[c]);
+  for (int round = 0; round < 2; ++round) {
+    int px = ti, py = tj, pz = tk;
+    if (round == 1) {
+      if (tid >= 61) break;
+      if (tid < 48) {  // faces
+        const int f = tid >> 4, a = tid & 3, b = (tid >> 2) & 3;
+        px = f == 0 ? 4 : a;
+        py = f == 1 ? 4 : (f == 0 ? a : b);
+        pz = f == 2 ? 4 : b;
+      } else if (tid < 60) {  // edges
+        const int e = (tid - 48) >> 2, c = (tid - 48) & 3;
+        px = e == 2 ? c : 4;
+        py = e == 1 ? c : 4;
+        pz = e == 0 ? c : 4;
       } else {
-#pragma unroll
-        for (int c = 0; c < 3; ++c) yu[c * cstride + idx] = v[c];
+        px = py = pz = 4;
       }
     }
-  }
-  if (DO_DIV) {
-    const int64_t mbase1 = (int64_t)mac * npts1;
-#pragma unroll 1
-    for (int pt = tid; pt < kFP1 * kFP1 * kFP1; pt += kBT) {
-      const int px = pt % kFP1, py = (pt / kFP1) % kFP1, pz = pt / (kFP1 * kFP1);
-      const int gx = i0 + px, gy_ = j0 + py, gz = k0 + pz;
-      if (gx + gy_ + gz > n1) continue;
-      double v = 0.0;
-      for (int lz = max(pz - 1, 0); lz <= min(pz, kB - 1); ++lz)
-        for (int ly = max(py - 1, 0); ly <= min(py, kB - 1); ++ly)
-          for (int lx = max(px - 1, 0); lx <= min(px, kB - 1); ++lx) {
-            const int sl = (px - lx) + 2 * (py - ly) + 4 * (pz - lz);
-            v += sm[(NSU + sl) * kBT + lx + kB * ly + kB * kB * lz];
+    if (HAS_U_OUT) {
+#pragma unroll
+      for (int oz = 0; oz < 2; ++oz) {
+#pragma unroll
+        for (int oy = 0; oy < 2; ++oy) {
+#pragma unroll
+          for (int ox = 0; ox < 2; ++ox) {
+            if ((ox && px == 4) || (oy && py == 4) || (oz && pz == 4)) continue;
+            const int gx = 2 * (i0 + px) + ox, gy_ = 2 * (j0 + py) + oy, gz = 2 * (k0 + pz) + oz;
+            if (gx + gy_ + gz > n2) continue;
+            double v[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+            for (int cz = 0; cz < 2; ++cz) {
+              if (cz && oz) continue;
+#pragma unroll
+              for (int cy = 0; cy < 2; ++cy) {
+                if (cy && oy) continue;
+#pragma unroll
+                for (int cx = 0; cx < 2; ++cx) {
+                  if (cx && ox) continue;
+                  const int qx = px - cx, qy = py - cy, qz = pz - cz;
+                  if (qx < 0 || qx > 3 || qy < 0 || qy > 3 || qz < 0 || qz > 3) continue;
+                  const int sl = (cx ? 2 : ox) + 3 * (cy ? 2 : oy) + 9 * (cz ? 2 : oz);
+                  const double* sp = sm + 3 * sl * kBT + qx + 4 * qy + 16 * qz;
+#pragma unroll
+                  for (int c = 0; c < 3; ++c) v[c] += sp[c * kBT];
+                }
+              }
+            }
+            double* dst = yum + rowstart32(n2, gy_, gz) + gx;
+            const bool border = (px == 0 && ox == 0) || (py == 0 && oy == 0) || (pz == 0 && oz == 0) || px == 4 ||
+                                py == 4 || pz == 4;
+            if (border) {
+#pragma unroll
+              for (int c = 0; c < 3; ++c)
+                if (v[c] != 0.0) atomicAdd(dst + c * cstride, v[c]);
+            } else {
+#pragma unroll
+              for (int c = 0; c < 3; ++c) dst[c * cstride] = v[c];
+            }
           }
-      const int64_t idx = mbase1 + rowstart32(n1, gy_, gz) + gx;
-      const bool border = px == 0 || py == 0 || pz == 0 || px == kFP1 - 1 || py == kFP1 - 1 || pz == kFP1 - 1;
-      if (border) {
-        if (v != 0.0) atomicAdd(yp + idx, v);
-      } else {
-        yp[idx] = v;
+        }
+      }
+    }
+    if (DO_DIV) {
+      const int gx = i0 + px, gy_ = j0 + py, gz = k0 + pz;
+      if (gx + gy_ + gz <= n1) {
+        double v = 0.0;
+#pragma unroll
+        for (int cz = 0; cz < 2; ++cz)
+#pragma unroll
+          for (int cy = 0; cy < 2; ++cy)
+#pragma unroll
+            for (int cx = 0; cx < 2; ++cx) {
+              const int qx = px - cx, qy = py - cy, qz = pz - cz;
+              if (qx < 0 || qx > 3 || qy < 0 || qy > 3 || qz < 0 || qz > 3) continue;
+              v += sm[(NSU + cx + 2 * cy + 4 * cz) * kBT + qx + 4 * qy + 16 * qz];
+            }
+        double* dst = ypm + rowstart32(n1, gy_, gz) + gx;
+        const bool border = px == 0 || py == 0 || pz == 0 || px == 4 || py == 4 || pz == 4;
+        if (border) {
+          if (v != 0.0) atomicAdd(dst, v);
+        } else {
+          *dst = v;
+        }
       }
     }
   }
@@ -450,19 +608,48 @@ static int ensure_slots() {
       {{0, 0, 1}, {0, 1, 0}, {1, 0, 0}, {1, 0, 1}}, {{0, 1, 0}, {0, 1, 1}, {1, 0, 1}, {1, 1, 0}},
       {{0, 0, 1}, {0, 1, 0}, {0, 1, 1}, {1, 0, 1}}, {{0, 1, 1}, {1, 0, 1}, {1, 1, 0}, {1, 1, 1}}};
   const int ep[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
-  int slot[6][10], pslot[6][4];
+  int slot[6][10], ld[6][10], pslot[6][4], first[6] = {0}, pfirst[6] = {0};
+  long long seen2 = 0;
+  int seen1 = 0;
   for (int t = 0; t < 6; ++t) {
+    int off[10][3];
     for (int v = 0; v < 4; ++v) {
-      slot[t][v] = 2 * TV[t][v][0] + 3 * 2 * TV[t][v][1] + 9 * 2 * TV[t][v][2];
+      for (int r = 0; r < 3; ++r) off[v][r] = 2 * TV[t][v][r];
       pslot[t][v] = TV[t][v][0] + 2 * TV[t][v][1] + 4 * TV[t][v][2];
     }
-    for (int e = 0; e < 6; ++e) {
-      const int a = ep[e][0], b = ep[e][1];
-      slot[t][4 + e] = (TV[t][a][0] + TV[t][b][0]) + 3 * (TV[t][a][1] + TV[t][b][1]) + 9 * (TV[t][a][2] + TV[t][b][2]);
+    for (int e = 0; e < 6; ++e)
+      for (int r = 0; r < 3; ++r) off[4 + e][r] = TV[t][ep[e][0]][r] + TV[t][ep[e][1]][r];
+    for (int a = 0; a < 10; ++a) {
+      slot[t][a] = off[a][0] + 3 * off[a][1] + 9 * off[a][2];
+      ld[t][a] = ((off[a][1] + 3 * off[a][2]) << 2) | off[a][0];
+      if (!((seen2 >> slot[t][a]) & 1)) {
+        first[t] |= 1 << a;
+        seen2 |= 1LL << slot[t][a];
+      }
     }
+    for (int v = 0; v < 4; ++v)
+      if (!((seen1 >> pslot[t][v]) & 1)) {
+        pfirst[t] |= 1 << v;
+        seen1 |= 1 << pslot[t][v];
+      }
   }
+  int items[5][64] = {{0}}, nitems[5] = {0};
+  for (int delta = 1; delta <= 4; ++delta)
+    for (int cube = 0; cube < 64; ++cube) {
+      const int ts = (cube & 3) + ((cube >> 2) & 3) + (cube >> 4);
+      const int nt = (ts <= delta - 3) ? 6 : (ts == delta - 2 ? 5 : (ts == delta - 1 ? 1 : 0));
+      for (int t = 0; t < nt; ++t) {
+        if (nitems[delta] >= 64) return fail(HHG_EINVAL, "sparse brick item table overflow");
+        items[delta][nitems[delta]++] = cube | (t << 6);
+      }
+    }
   HHG_CUDA(cudaMemcpyToSymbol(eSlot, slot, sizeof(slot)));
+  HHG_CUDA(cudaMemcpyToSymbol(eLd, ld, sizeof(ld)));
   HHG_CUDA(cudaMemcpyToSymbol(ePSlot, pslot, sizeof(pslot)));
+  HHG_CUDA(cudaMemcpyToSymbol(eFirst, first, sizeof(first)));
+  HHG_CUDA(cudaMemcpyToSymbol(ePFirst, pfirst, sizeof(pfirst)));
+  HHG_CUDA(cudaMemcpyToSymbol(eItems, items, sizeof(items)));
+  HHG_CUDA(cudaMemcpyToSymbol(eNItems, nitems, sizeof(nitems)));
   g_slots_ready = true;
   return HHG_OK;
 }
@@ -471,10 +658,18 @@ template <bool BLEND, int MODE, bool FULL>
 static void elem_launch(const Mesh* m, const Level& L, const double* eta, double gamma, const double* u,
                         const double* p, double* yu, double* yp, cudaStream_t s) {
   const int64_t nm = macro_count(m);
-  constexpr int NS = ((MODE & (ELEM_A | ELEM_BT | ELEM_DIAG)) ? 81 : 0) + ((MODE & ELEM_DIV) ? 8 : 0);
+  constexpr int NS = ((MODE & (ELEM_A | ELEM_BT | ELEM_DIAG)) ? kNS2 : 0) + ((MODE & ELEM_DIV) ? kNS1 : 0);
+  constexpr size_t smem = (NS * kBT + kGeoSm) * sizeof(double) + 13 * kBT * sizeof(int);
   dim3 grid((unsigned)L.n_bricks, (unsigned)nm);
-  k_elem_brick<BLEND, MODE, FULL><<<grid, kBT, NS * kBT * sizeof(double) + 13 * kBT * sizeof(int), s>>>(
-      m->dgeo, L.geo, L.bricks, L.n1, L.npts1, L.npts2, nm * L.npts2, eta, u, p, yu, yp, gamma);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_elem_brick<BLEND, MODE, FULL>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         (int)cudaSharedmemCarveoutMaxShared);
+    cudaFuncSetAttribute(k_elem_brick<BLEND, MODE, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  k_elem_brick<BLEND, MODE, FULL><<<grid, kBT, smem, s>>>(m->dgeo, L.geo, L.bricks, L.n1, 1.0 / L.n1, L.npts1,
+                                                          L.npts2, nm * L.npts2, eta, u, p, yu, yp, gamma);
 }
 
 int launch_elem(const Mesh* m, const Level& L, int mode, int form, const double* eta, double gamma,
