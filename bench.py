@@ -95,13 +95,23 @@ class ClockSampler:
                 "samples": len(rows)}
 
 
-def build_case(level, device):
-    """Library-side set-up of config 3 (mesh, eta per level, power start vectors, rhs)."""
+# weak scaling (BASELINE config 5): 240 macros per GPU -- shell(ntan, nrad) by GPU count
+SHELL_BY_GPUS = {1: (3, 2), 2: (3, 3), 4: (5, 2), 8: (5, 3)}
+
+
+def build_case(level, device, world=1, rank=0, comm=None):
+    """Library-side set-up of config 3 (mesh, eta per level, power start vectors, rhs).  world > 1:
+    shell with 240*world macros partitioned by recursive coordinate bisection, one part per rank."""
     import torch
     import paper_2506_04157_b200 as hhg
     from workload import icoshell, uniform_vec, viscosity
-    mac = icoshell(3, 2, 0.55, 1.0)
-    M = hhg.Mesh.from_macro(mac, level)
+    ntan, nrad = SHELL_BY_GPUS.get(world, (3, 2))
+    mac = icoshell(ntan, nrad, 0.55, 1.0)
+    if world > 1:
+        tr = hhg.partition_rcb(mac.verts, mac.tets, world, radial=True)
+        M = hhg.Mesh.from_macro(mac, level, tet_rank=tr, comm=comm)
+    else:
+        M = hhg.Mesh.from_macro(mac, level)
     M.blend_map(hhg.HHG_BLEND_SHELL)
     M.set_bc(hhg.HHG_BND_OUTER, hhg.HHG_BC_DIRICHLET0)
     M.set_bc(hhg.HHG_BND_INNER, hhg.HHG_BC_FREESLIP)
@@ -177,7 +187,8 @@ def main():
     import paper_2506_04157_b200 as hhg
 
     L = args.level
-    M, etas, v0, rhs, n_dof = build_case(L, local)
+    comm = hhg.Comm(rank, world, local) if world > 1 else None
+    M, etas, v0, rhs, n_dof = build_case(L, local, world, rank, comm)
     t0 = time.perf_counter()
     mg = hhg.MG(M, 1, L, etas, v0, pre=3, post=3, degree=3, power_iters=20, coarse_iters=50)
     setup_s = time.perf_counter() - t0
@@ -221,7 +232,7 @@ def main():
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    value = world * n_dof / (ms * 1e-3) / 1e9
+    value = n_dof / (ms * 1e-3) / 1e9          # n_dof: unique velocity dofs of the whole (partitioned) mesh
 
     # standalone fine-level epsilon_apply (BASELINE metric, first clause)
     y = M.zeros(L, hhg.HHG_P2VEC)
@@ -235,6 +246,10 @@ def main():
         a1.record(s)
     s.synchronize()
     apply_ms = a0.elapsed_time(a1) / args.apply_reps
+    if dist:
+        t = torch.tensor([apply_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        apply_ms = float(t.item())
 
     # end to end: pinned host rhs -> V-cycle -> host x, through vcycle_host
     rhs_h = rhs.cpu().pin_memory()
@@ -249,10 +264,14 @@ def main():
         h1.record(s)
     s.synchronize()
     e2e_ms = h0.elapsed_time(h1) / args.steps
+    if dist:
+        t = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
     nbytes = rhs.numel() * 8
 
     # roofline of the dominant kernel (fine-level element kernel, fp64 DFMA pipe)
-    n_tets = 240 * 8 ** L
+    n_tets = M.local_macros() * 8 ** L        # this rank's micro tets (the element kernel it times)
     flops_per_tet = float(os.environ.get("HHG_FLOPS_PER_TET", "0")) or FLOPS_PER_TET
     elem_ms = prof["apply_ms_sum"] / max(1, prof["apply_count"])
     achieved = flops_per_tet * n_tets / (elem_ms * 1e-3) / 1e12
@@ -262,9 +281,11 @@ def main():
         "metric": METRIC, "value": value, "unit": "GDoF/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"config3: V(3,3)-cycle, blended shell(3,2) level {L}->1, eta contrast 1e6 x30, "
+        "config": {"workload": f"config3: V(3,3)-cycle, blended shell{SHELL_BY_GPUS.get(world, (3, 2))} level {L}->1, "
+                               "eta contrast 1e6 x30, "
                                "Chebyshev deg 3, 50 PCG coarse its",
-                   "level": L, "velocity_dofs": n_dof, "micro_tets": n_tets, "parallelism": f"replicas{world}",
+                   "level": L, "velocity_dofs": n_dof, "macros": 240 * world,
+                   "micro_tets_per_gpu": n_tets, "parallelism": f"macro-partition x{world} (RCB), NCCL interface exchange" if world > 1 else "single GPU",
                    "l2": "inputs larger than L2 (rhs/x/work vectors 276 MB each at level 5)"},
         "apply": {"gdofs": n_dof / (apply_ms * 1e-3) / 1e9, "ms": apply_ms, "level": L,
                   "note": "epsilon_apply (memset + element kernel + interface sum/BC) standalone"},
@@ -275,9 +296,10 @@ def main():
                      "flops_per_tet": flops_per_tet,
                      "peak_source": "MEASURED_PEAKS.json fp64_tflops" if pk.get("fp64_tflops") else
                      "measured: tools/fp64_peak DFMA microbenchmark (profiles/r01_fp64_peak.json)",
-                     "hbm_gbs_algorithmic": (2 * n_dof + 240 * ((2 ** L + 1) * (2 ** L + 2) * (2 ** L + 3) // 6)) * 8
+                     "hbm_gbs_algorithmic": (2 * rhs.numel() + M.local_macros() * ((2 ** L + 1) * (2 ** L + 2)
+                                                                                    * (2 ** L + 3) // 6)) * 8
                      / (elem_ms * 1e-3) / 1e9},
-        "e2e": {"value": world * n_dof / (e2e_ms * 1e-3) / 1e9, "unit": "GDoF/s", "ms": e2e_ms,
+        "e2e": {"value": n_dof / (e2e_ms * 1e-3) / 1e9, "unit": "GDoF/s", "ms": e2e_ms,
                 "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes},
         "gpu_launches": kernels_per_cycle * args.steps,
         "clocks": clk.summary(),

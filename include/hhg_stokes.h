@@ -93,7 +93,8 @@ int hhg_comm_destroy(hhg_comm* comm);
  * library sorts each row ascending), vertex coordinates (n_vert x 3, host), vertex
  * tags (0 interior, 1 inner/CMB, 2 outer/surface; host; NULL = all 0), refinement
  * up to level_max (0..8).  tet_rank (host, n_tets, NULL = all local) assigns each
- * macro to a rank of comm; this process keeps the macros with tet_rank == its rank.
+ * macro to a rank of comm; this process keeps the macros with tet_rank == its rank
+ * (tet_rank with nonzero entries needs comm, else HHG_EINVAL: see hhg_mesh_create_part).
  * Errors: HHG_EINVAL (NULL, n < 1, level_max out of range, degenerate tet). */
 int hhg_mesh_create(const double* macro_xyz, int64_t n_vert, const int32_t* macro_tets, int64_t n_tets,
                     const int32_t* vertex_tag, int level_max, const int32_t* tet_rank, hhg_comm* comm,
@@ -101,6 +102,37 @@ int hhg_mesh_create(const double* macro_xyz, int64_t n_vert, const int32_t* macr
 int hhg_mesh_destroy(hhg_mesh* mesh);
 /* Number of macro tets stored by this process. */
 int hhg_mesh_local_macros(const hhg_mesh* mesh, int64_t* n);
+
+/* ------------------------------------------------------------------ partitioned meshes (multi-GPU)
+ * The path shards by macro tets (the paper's domain decomposition): each rank keeps
+ * the lattices of its macros; nodes on macro faces/edges/vertices shared with other ranks are
+ * summed by one exchange per operator (NCCL point-to-point over NVLink), dots by one allreduce.
+ * hhg_partition_rcb: recursive coordinate bisection of macro centroids into nparts (radial != 0:
+ *   centroids projected to the unit sphere, keeping radial macro columns on one rank) -> tet_rank
+ *   (host, n_tets).  Deterministic; equal part sizes up to rounding.
+ * hhg_mesh_create_part: rank `rank`'s view of a partition WITHOUT a communicator: interface sums
+ *   cover local copies only; the cross-rank part is done by the caller with hhg_halo_pack ->
+ *   (transport of the send buffers) -> hhg_interface_sum_remote.  hhg_mesh_create with a comm does
+ *   the same internally (pack, ncclSend/ncclRecv per neighbor, remote-sum kernel).
+ * Shared nodes with neighbor q are listed in canonical key order, so the receive buffer segment
+ * from q matches our send segment to q slot by slot.  Buffers: device, [slots][nc] fp64, nc = 3
+ *   (P2VEC) or 1 (P1), neighbor segments in ascending rank order (hhg_halo_info gives the ranks and
+ *   per-neighbor counts; host-only, no GPU needed).  hhg_halo_keys: HOST int64 [slots][10] node keys.
+ * Owner of a replicated node = its copy in the lowest global macro id: hhg_owned_count summed over
+ *   ranks equals hhg_canonical_len (host-only).  Errors: HHG_EINVAL (bad rank, NULL, bad space). */
+int hhg_partition_rcb(const double* macro_xyz, int64_t n_vert, const int32_t* macro_tets, int64_t n_tets,
+                      int nparts, int radial, int32_t* tet_rank);
+int hhg_mesh_create_part(const double* macro_xyz, int64_t n_vert, const int32_t* macro_tets, int64_t n_tets,
+                         const int32_t* vertex_tag, int level_max, const int32_t* tet_rank, int nranks, int rank,
+                         hhg_mesh** out);
+int hhg_mesh_rank(const hhg_mesh* mesh, int* rank, int* nranks);
+int hhg_halo_info(const hhg_mesh* mesh, int level, int space, int* n_nbr, int32_t* nbr_ranks, int64_t* counts);
+int hhg_halo_keys(const hhg_mesh* mesh, int level, int space, int64_t* keys_host);
+int hhg_owned_count(const hhg_mesh* mesh, int level, int space, int64_t* n_owned);
+int hhg_halo_pack(const hhg_mesh* mesh, int level, int space, const double* v, double* sendbuf,
+                  hhg_stream_t stream);
+int hhg_interface_sum_remote(const hhg_mesh* mesh, int level, int space, const double* recvbuf, double* v,
+                             hhg_stream_t stream);
 
 /* blend_map: HHG_BLEND_SHELL = origin-centred thick spherical
  * shell: per macro, B(x) = c_K x (n_K . x)/|x| with n_K the unit normal of the plane
@@ -158,6 +190,10 @@ int divT_apply(const hhg_mesh* mesh, int level, const double* p, double* y_u, in
 int stokes_apply(const hhg_mesh* mesh, int level, const double* eta_p1, double gamma, const double* u,
                  const double* p, double* y_u, double* y_p, hhg_stream_t stream);
 int hhg_diag(const hhg_mesh* mesh, int level, const double* eta_p1, double* diag, hhg_stream_t stream);
+/* epsilon_apply_partial: the element half of epsilon_apply only -- per-copy partial sums of
+ * A(eta) u, NO interface sum and NO BC (first phase of a split-phase exchange). */
+int epsilon_apply_partial(const hhg_mesh* mesh, int level, int form, const double* eta_p1, const double* u,
+                          double* y, hhg_stream_t stream);
 
 /* Inner product over UNIQUE dofs of two consistent vectors (each replicated node
  * counted once), allreduced over ranks; result written to out_dev (1 double). */

@@ -38,6 +38,8 @@ EXPORTS = [
     "stokes_apply", "hhg_diag", "hhg_dot", "p2_restrict", "p2_prolong", "chebyshev_smooth",
     "hhg_power_iteration", "hhg_mg_create", "hhg_mg_lambda", "vcycle", "vcycle_host", "hhg_mg_profile",
     "hhg_mg_profile_get", "hhg_mg_destroy", "hhg_launch_count",
+    "hhg_mesh_create_part", "hhg_partition_rcb", "hhg_mesh_rank", "hhg_halo_info", "hhg_halo_keys",
+    "hhg_owned_count", "hhg_halo_pack", "hhg_interface_sum_remote", "epsilon_apply_partial",
 ]
 
 
@@ -70,6 +72,11 @@ def _load():
         "hhg_mg_create": ([P, P, P, P, P], I), "hhg_mg_lambda": ([P, I, P], I), "vcycle": ([P, P, P, P], I),
         "vcycle_host": ([P, P, P, P], I), "hhg_mg_profile": ([P, I], I),
         "hhg_mg_profile_get": ([P, P, P, P, P], I), "hhg_mg_destroy": ([P], I),
+        "hhg_mesh_create_part": ([P, I64, P, I64, P, I, P, I, I, P], I),
+        "hhg_partition_rcb": ([P, I64, P, I64, I, I, P], I), "hhg_mesh_rank": ([P, P, P], I),
+        "hhg_halo_info": ([P, I, I, P, P, P], I), "hhg_halo_keys": ([P, I, I, P], I),
+        "hhg_owned_count": ([P, I, I, P], I), "hhg_halo_pack": ([P, I, I, P, P, P], I),
+        "hhg_interface_sum_remote": ([P, I, I, P, P, P], I), "epsilon_apply_partial": ([P, I, I, P, P, P, P], I),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -123,19 +130,108 @@ def launch_count(reset=False) -> int:
     return int(_lib.hhg_launch_count(1 if reset else 0))
 
 
-class Mesh:
-    """hhg_mesh_create + blend_map + hhg_set_bc (macro tets uniformly refined to level_max)."""
+class Comm:
+    """hhg_comm_create: the library's own NCCL communicator (one process per GPU); the unique id is
+    made on rank 0 and broadcast through the caller's torch.distributed process group."""
 
-    def __init__(self, verts, tets, vtag=None, level_max=4, tet_rank=None, comm=None):
+    def __init__(self, rank, world, device=0, group=None):
+        import torch
+        import torch.distributed as dist
+        idb = np.zeros(128, dtype=np.uint8)
+        if rank == 0:
+            _chk(_lib.hhg_comm_unique_id(_ptr(idb)))
+        t = torch.from_numpy(idb.astype(np.int64))
+        if dist.get_backend(group) == "nccl":
+            t = t.cuda()
+        dist.broadcast(t, 0, group=group)
+        idb = t.cpu().numpy().astype(np.uint8)
+        h = ctypes.c_void_p()
+        _chk(_lib.hhg_comm_create(_ptr(idb), int(world), int(rank), int(device), ctypes.byref(h)))
+        self.handle, self.rank, self.world = h, rank, world
+
+    def __del__(self):
+        if getattr(self, "handle", None) and _lib is not None:
+            _lib.hhg_comm_destroy(self.handle)
+            self.handle = None
+
+
+def partition_rcb(verts, tets, nparts, radial=True):
+    """hhg_partition_rcb: recursive coordinate bisection of macro centroids (projected to the unit
+    sphere when radial, keeping radial macro columns together) -> tet_rank (int32)."""
+    v = np.ascontiguousarray(verts, dtype=np.float64)
+    t = np.ascontiguousarray(tets, dtype=np.int32)
+    out = np.empty(t.shape[0], dtype=np.int32)
+    _chk(_lib.hhg_partition_rcb(_ptr(v), v.shape[0], _ptr(t), t.shape[0], int(nparts), 1 if radial else 0,
+                                _ptr(out)))
+    return out
+
+
+class Mesh:
+    """hhg_mesh_create + blend_map + hhg_set_bc (macro tets uniformly refined to level_max).
+    With comm (+ tet_rank) this process keeps its own macros and interface sums / dots run over NCCL;
+    ``Mesh.part`` builds rank `rank`'s view of a partition without a communicator (split-phase
+    exchange through halo_pack / interface_sum_remote, e.g. several partitions on one GPU)."""
+
+    def __init__(self, verts, tets, vtag=None, level_max=4, tet_rank=None, comm=None, part=None):
         v = np.ascontiguousarray(verts, dtype=np.float64)
         t = np.ascontiguousarray(tets, dtype=np.int32)
         g = None if vtag is None else np.ascontiguousarray(vtag, dtype=np.int32)
         r = None if tet_rank is None else np.ascontiguousarray(tet_rank, dtype=np.int32)
         h = ctypes.c_void_p()
-        _chk(_lib.hhg_mesh_create(_ptr(v), v.shape[0], _ptr(t), t.shape[0], _ptr(g), int(level_max), _ptr(r),
-                                  None if comm is None else comm.handle, ctypes.byref(h)))
+        if part is not None:
+            nranks, rank = part
+            _chk(_lib.hhg_mesh_create_part(_ptr(v), v.shape[0], _ptr(t), t.shape[0], _ptr(g), int(level_max), _ptr(r),
+                                           int(nranks), int(rank), ctypes.byref(h)))
+        else:
+            _chk(_lib.hhg_mesh_create(_ptr(v), v.shape[0], _ptr(t), t.shape[0], _ptr(g), int(level_max), _ptr(r),
+                                      None if comm is None else comm.handle, ctypes.byref(h)))
         self.handle = h
         self.level_max = level_max
+        self.comm = comm
+
+    @classmethod
+    def part(cls, macro, level_max, tet_rank, nranks, rank):
+        return cls(macro.verts, macro.tets, macro.vtag, level_max, tet_rank=tet_rank, part=(nranks, rank))
+
+    def rank(self):
+        r, n = ctypes.c_int(), ctypes.c_int()
+        _chk(_lib.hhg_mesh_rank(self.handle, ctypes.byref(r), ctypes.byref(n)))
+        return r.value, n.value
+
+    def halo_info(self, level, space):
+        """(neighbor ranks, shared-node counts) of the cross-rank interface (host-only)."""
+        n = ctypes.c_int()
+        _chk(_lib.hhg_halo_info(self.handle, level, space, ctypes.byref(n), None, None))
+        nb = np.empty(n.value, dtype=np.int32)
+        cnt = np.empty(n.value, dtype=np.int64)
+        _chk(_lib.hhg_halo_info(self.handle, level, space, ctypes.byref(n), _ptr(nb), _ptr(cnt)))
+        return nb, cnt
+
+    def halo_keys(self, level, space):
+        nb, cnt = self.halo_info(level, space)
+        keys = np.empty((int(cnt.sum()), 10), dtype=np.int64)
+        _chk(_lib.hhg_halo_keys(self.handle, level, space, _ptr(keys)))
+        return keys
+
+    def owned_count(self, level, space):
+        n = ctypes.c_int64()
+        _chk(_lib.hhg_owned_count(self.handle, level, space, ctypes.byref(n)))
+        return n.value
+
+    def halo_pack(self, level, space, v, sendbuf=None, stream=None):
+        import torch
+        nb, cnt = self.halo_info(level, space)
+        nc = 3 if space == HHG_P2VEC else 1
+        sendbuf = torch.zeros(max(1, int(cnt.sum()) * nc), dtype=torch.float64, device="cuda") \
+            if sendbuf is None else sendbuf
+        _chk(_lib.hhg_halo_pack(self.handle, level, space, _dev(v, self.vec_len(level, space)), _dev(sendbuf),
+                                _stream(stream)))
+        return sendbuf
+
+    def interface_sum_remote(self, level, space, recvbuf, v, stream=None):
+        _chk(_lib.hhg_interface_sum_remote(self.handle, level, space, _dev(recvbuf),
+                                           _dev(v, self.vec_len(level, space)), _stream(stream)))
+        return v
 
     @classmethod
     def from_macro(cls, macro, level_max, **kw):
@@ -176,7 +272,7 @@ class Mesh:
 
     def to_canonical(self, level, space, v, stream=None):
         import torch
-        out = torch.empty(self.canonical_len(level, space), dtype=torch.float64, device="cuda")
+        out = torch.zeros(self.canonical_len(level, space), dtype=torch.float64, device="cuda")
         _chk(_lib.hhg_to_canonical(self.handle, level, space, _dev(v, self.vec_len(level, space)), _dev(out),
                                    _stream(stream)))
         return out
@@ -215,6 +311,15 @@ def epsilon_apply(mesh, level, eta, u, y=None, form=HHG_VISC_FULL, stream=None):
     y = mesh.zeros(level, HHG_P2VEC) if y is None else y
     _chk(_lib.epsilon_apply(mesh.handle, level, form, _dev(eta, mesh.vec_len(level, HHG_P1), "eta"),
                             _dev(u, n, "u"), _dev(y, n, "y"), _stream(stream)))
+    return y
+
+
+def epsilon_apply_partial(mesh, level, eta, u, y=None, form=HHG_VISC_FULL, stream=None):
+    """Element contributions only (per-copy partial sums, no interface sum, no BC)."""
+    n = mesh.vec_len(level, HHG_P2VEC)
+    y = mesh.zeros(level, HHG_P2VEC) if y is None else y
+    _chk(_lib.epsilon_apply_partial(mesh.handle, level, form, _dev(eta, mesh.vec_len(level, HHG_P1), "eta"),
+                                    _dev(u, n, "u"), _dev(y, n, "y"), _stream(stream)))
     return y
 
 

@@ -2,6 +2,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <functional>
 
 #include "hhg_internal.h"
 
@@ -45,15 +46,17 @@ const char* hhg_version(void) {
 
 int64_t hhg_launch_count(int reset) { return launches(reset); }
 
-int hhg_mesh_create(const double* macro_xyz, int64_t n_vert, const int32_t* macro_tets, int64_t n_tets,
-                    const int32_t* vertex_tag, int level_max, const int32_t* tet_rank, hhg_comm* comm,
-                    hhg_mesh** out) {
+static int mesh_create_impl(const double* macro_xyz, int64_t n_vert, const int32_t* macro_tets, int64_t n_tets,
+                            const int32_t* vertex_tag, int level_max, const int32_t* tet_rank, int nranks, int rank,
+                            hhg_comm* comm, hhg_mesh** out) {
   CHECK_PTR(macro_xyz);
   CHECK_PTR(macro_tets);
   CHECK_PTR(out);
   *out = nullptr;
   if (n_vert < 4 || n_tets < 1) return fail(HHG_EINVAL, "need >= 4 vertices and >= 1 tet");
   if (level_max < 0 || level_max > 8) return fail(HHG_EINVAL, "level_max must be in [0, 8]");
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(HHG_EINVAL, "bad rank / nranks");
+  if (nranks > 1 && !tet_rank) return fail(HHG_EINVAL, "a partitioned mesh needs tet_rank");
   auto* m = new hhg_mesh();
   m->n_vert = n_vert;
   m->n_tets = n_tets;
@@ -72,16 +75,19 @@ int hhg_mesh_create(const double* macro_xyz, int64_t n_vert, const int32_t* macr
   }
   m->level_max = level_max;
   m->comm = comm;
-  if (comm) {
-    delete m;
-    return fail(HHG_EINVAL, "multi-GPU meshes are created through hhg_mesh_create_dist (not in this build)");
-  }
+  m->rank = rank;
+  m->nranks = nranks;
   m->tet_rank.assign(n_tets, 0);
   if (tet_rank) m->tet_rank.assign(tet_rank, tet_rank + n_tets);
-  for (int64_t t = 0; t < n_tets; ++t)
+  for (int64_t t = 0; t < n_tets; ++t) {
+    if (m->tet_rank[t] < 0 || m->tet_rank[t] >= nranks) {
+      delete m;
+      return fail(HHG_EINVAL, "tet_rank entry outside [0, nranks)");
+    }
     if (m->tet_rank[t] == m->rank) m->local.push_back(t);
+  }
   if (cudaGetDevice(&m->device) != cudaSuccess) {
-    m->device = -1;  // host-only use (keys, lengths) is still valid without a GPU
+    m->device = -1;  // host-only use (keys, lengths, plans) is still valid without a GPU
     cudaGetLastError();
   }
   m->levels.resize(level_max + 1);
@@ -92,6 +98,74 @@ int hhg_mesh_create(const double* macro_xyz, int64_t n_vert, const int32_t* macr
     return r;
   }
   *out = m;
+  return HHG_OK;
+}
+
+int hhg_mesh_create(const double* macro_xyz, int64_t n_vert, const int32_t* macro_tets, int64_t n_tets,
+                    const int32_t* vertex_tag, int level_max, const int32_t* tet_rank, hhg_comm* comm,
+                    hhg_mesh** out) {
+  const int nranks = comm ? comm->nranks : 1, rank = comm ? comm->rank : 0;
+  if (!comm && tet_rank) {
+    for (int64_t t = 0; t < n_tets; ++t)
+      if (tet_rank[t] != 0) return fail(HHG_EINVAL, "tet_rank without a communicator: use hhg_mesh_create_part");
+  }
+  return mesh_create_impl(macro_xyz, n_vert, macro_tets, n_tets, vertex_tag, level_max, tet_rank, nranks, rank, comm,
+                          out);
+}
+
+int hhg_mesh_create_part(const double* macro_xyz, int64_t n_vert, const int32_t* macro_tets, int64_t n_tets,
+                         const int32_t* vertex_tag, int level_max, const int32_t* tet_rank, int nranks, int rank,
+                         hhg_mesh** out) {
+  CHECK_PTR(tet_rank);
+  return mesh_create_impl(macro_xyz, n_vert, macro_tets, n_tets, vertex_tag, level_max, tet_rank, nranks, rank,
+                          nullptr, out);
+}
+
+int hhg_partition_rcb(const double* macro_xyz, int64_t n_vert, const int32_t* macro_tets, int64_t n_tets,
+                      int nparts, int radial, int32_t* tet_rank) {
+  CHECK_PTR(macro_xyz);
+  CHECK_PTR(macro_tets);
+  CHECK_PTR(tet_rank);
+  if (nparts < 1 || nparts > n_tets) return fail(HHG_EINVAL, "nparts must be in [1, n_tets]");
+  // macro centroids (radial != 0: projected to the unit sphere, so radial columns stay together)
+  std::vector<std::array<double, 3>> c(n_tets);
+  for (int64_t t = 0; t < n_tets; ++t) {
+    double x[3] = {0, 0, 0};
+    for (int a = 0; a < 4; ++a)
+      for (int r = 0; r < 3; ++r) x[r] += 0.25 * macro_xyz[3 * macro_tets[4 * t + a] + r];
+    if (radial) {
+      const double nr = std::sqrt(x[0] * x[0] + x[1] * x[1] + x[2] * x[2]);
+      for (int r = 0; r < 3; ++r) x[r] = nr > 0 ? x[r] / nr : 0.0;
+    }
+    c[t] = {x[0], x[1], x[2]};
+  }
+  std::vector<int64_t> idx(n_tets);
+  for (int64_t t = 0; t < n_tets; ++t) idx[t] = t;
+  // recursive bisection along the widest coordinate; part sizes proportional to part counts
+  std::function<void(int64_t, int64_t, int, int)> rec = [&](int64_t b, int64_t e, int p0, int np) {
+    if (np == 1) {
+      for (int64_t i = b; i < e; ++i) tet_rank[idx[i]] = p0;
+      return;
+    }
+    double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+    for (int64_t i = b; i < e; ++i)
+      for (int r = 0; r < 3; ++r) {
+        lo[r] = std::min(lo[r], c[idx[i]][r]);
+        hi[r] = std::max(hi[r], c[idx[i]][r]);
+      }
+    int ax = 0;
+    for (int r = 1; r < 3; ++r)
+      if (hi[r] - lo[r] > hi[ax] - lo[ax]) ax = r;
+    const int nl = np / 2;
+    const int64_t mid = b + (e - b) * nl / np;
+    std::stable_sort(idx.begin() + b, idx.begin() + e, [&](int64_t x, int64_t y) {
+      if (c[x][ax] != c[y][ax]) return c[x][ax] < c[y][ax];
+      return x < y;
+    });
+    rec(b, mid, p0, nl);
+    rec(mid, e, p0 + nl, np - nl);
+  };
+  rec(0, n_tets, 0, nparts);
   return HHG_OK;
 }
 
@@ -323,7 +397,6 @@ int p2_restrict(const hhg_mesh* mesh, int fine_level, const double* r_fine, doub
   const Level& Lf = m->levels[fine_level];
   const Level& Lc = m->levels[fine_level - 1];
   cudaStream_t s = (cudaStream_t)stream;
-  HHG_CUDA(cudaMemsetAsync(r_coarse, 0, 3 * macro_count(m) * Lc.npts2 * sizeof(double), s));
   HHG_TRY(launch_restrict(m, Lc, Lf, r_fine, r_coarse, s));
   return launch_fixup(m, Lc, HHG_P2VEC, true, true, r_coarse, s);
 }
@@ -341,6 +414,94 @@ int p2_prolong(const hhg_mesh* mesh, int coarse_level, const double* x_coarse, d
   const Level& Lf = m->levels[coarse_level + 1];
   HHG_TRY(launch_prolong(m, Lc, Lf, x_coarse, x_fine, s));
   return launch_fixup(m, Lf, HHG_P2VEC, false, true, x_fine, s);
+}
+
+
+// ------------------------------------------------------------------ partitioned meshes (multi-GPU)
+int hhg_mesh_rank(const hhg_mesh* mesh, int* rank, int* nranks) {
+  CHECK_PTR(mesh);
+  if (rank) *rank = mesh->rank;
+  if (nranks) *nranks = mesh->nranks;
+  return HHG_OK;
+}
+
+static int halo_host(const hhg_mesh* mesh, int level, int space, Halo& H, std::vector<uint8_t>* own_out) {
+  HHG_TRY(check_level(mesh, level));
+  if (space != HHG_P1 && space != HHG_P2 && space != HHG_P2VEC) return fail(HHG_EINVAL, "bad space");
+  std::vector<int64_t> ptr, copy, sg;
+  std::vector<uint8_t> kind, own;
+  std::vector<double> normal;
+  HHG_TRY(build_host_groups(mesh, level, space == HHG_P1 ? HHG_P1 : HHG_P2VEC, ptr, copy, kind, normal, own, H, sg));
+  if (own_out) own_out->swap(own);
+  return HHG_OK;
+}
+
+int hhg_halo_info(const hhg_mesh* mesh, int level, int space, int* n_nbr, int32_t* nbr_ranks, int64_t* counts) {
+  CHECK_PTR(n_nbr);
+  Halo H;
+  HHG_TRY(halo_host(mesh, level, space, H, nullptr));
+  *n_nbr = (int)H.nbr.size();
+  for (size_t i = 0; i < H.nbr.size(); ++i) {
+    if (nbr_ranks) nbr_ranks[i] = H.nbr[i];
+    if (counts) counts[i] = H.off[i + 1] - H.off[i];
+  }
+  return HHG_OK;
+}
+
+int hhg_halo_keys(const hhg_mesh* mesh, int level, int space, int64_t* keys_host) {
+  CHECK_PTR(keys_host);
+  Halo H;
+  HHG_TRY(halo_host(mesh, level, space, H, nullptr));
+  std::copy(H.keys.begin(), H.keys.end(), keys_host);
+  return HHG_OK;
+}
+
+int hhg_owned_count(const hhg_mesh* mesh, int level, int space, int64_t* n_owned) {
+  CHECK_PTR(n_owned);
+  Halo H;
+  std::vector<uint8_t> own;
+  HHG_TRY(halo_host(mesh, level, space, H, &own));
+  int64_t n = 0;
+  for (uint8_t o : own) n += o;
+  *n_owned = n;
+  return HHG_OK;
+}
+
+int hhg_halo_pack(const hhg_mesh* mesh, int level, int space, const double* v, double* sendbuf,
+                  hhg_stream_t stream) {
+  HHG_TRY(check_level(mesh, level));
+  CHECK_PTR(v);
+  CHECK_PTR(sendbuf);
+  if (space != HHG_P1 && space != HHG_P2VEC) return fail(HHG_EINVAL, "halo exchange: space must be P1 or P2VEC");
+  auto* m = const_cast<hhg_mesh*>(mesh);
+  HHG_TRY(ensure_level(m, level));
+  return launch_halo_pack(m, m->levels[level], space, v, sendbuf, (cudaStream_t)stream);
+}
+
+int hhg_interface_sum_remote(const hhg_mesh* mesh, int level, int space, const double* recvbuf, double* v,
+                             hhg_stream_t stream) {
+  HHG_TRY(check_level(mesh, level));
+  CHECK_PTR(v);
+  if (space != HHG_P1 && space != HHG_P2VEC) return fail(HHG_EINVAL, "halo exchange: space must be P1 or P2VEC");
+  auto* m = const_cast<hhg_mesh*>(mesh);
+  HHG_TRY(ensure_level(m, level));
+  const Level& L = m->levels[level];
+  if (!recvbuf && (space == HHG_P1 ? L.g1 : L.g2).halo.nslots > 0) return fail(HHG_EINVAL, "NULL recvbuf");
+  return launch_fixup_remote(m, L, space, space == HHG_P2VEC, recvbuf, v, (cudaStream_t)stream);
+}
+
+int epsilon_apply_partial(const hhg_mesh* mesh, int level, int form, const double* eta_p1, const double* u,
+                          double* y, hhg_stream_t stream) {
+  HHG_TRY(check_level(mesh, level));
+  CHECK_PTR(u);
+  CHECK_PTR(y);
+  if (form != HHG_VISC_FULL && form != HHG_VISC_EPS) return fail(HHG_EINVAL, "bad viscous form");
+  auto* m = const_cast<hhg_mesh*>(mesh);
+  HHG_TRY(ensure_level(m, level));
+  const Level& L = m->levels[level];
+  cudaStream_t s = (cudaStream_t)stream;
+  HHG_CUDA(cudaMemsetAsync(y, 0, 3 * macro_count(m) * L.npts2 * sizeof(double), s));
+  return launch_elem(m, L, ELEM_A, form, eta_p1, 0.0, u, nullptr, y, nullptr, s);
 }
 
 }  // extern "C"

@@ -55,6 +55,21 @@ struct MacroGeo {
 constexpr int kTypeGeo = 9 + 12;
 constexpr int kLevelGeo = 6 * kTypeGeo + 2;  // + absdetF + pad
 
+// Cross-rank part of the interface sum (multi-GPU, macro partition over ranks): the groups of
+// nodes shared with other ranks, one slot per (neighbor rank, shared node) in canonical node-key
+// order (identical on both sides, so no index exchange is needed).
+struct Halo {
+  std::vector<int> nbr;            // neighbor ranks, ascending
+  std::vector<int64_t> off;        // slot offset per neighbor (size nbr.size()+1)
+  int64_t nslots = 0;
+  std::vector<int64_t> keys;       // host [nslots][10] node keys (tests / diagnostics)
+  int64_t* slot_group = nullptr;   // device [nslots]: local group of each slot
+  int64_t* gs_ptr = nullptr;       // device [n_groups+1]: CSR group -> slots
+  int64_t* gs_idx = nullptr;       // device [nslots]
+  double* sbuf = nullptr;          // device [nslots][nc] local partial sums to send
+  double* rbuf = nullptr;          // device [nslots][nc] partial sums received
+};
+
 struct Groups {           // replicated-node groups (interface and/or boundary nodes)
   int64_t n = 0;          // number of groups
   int64_t nbc = 0;        // groups [0, nbc) carry a BC (sorted first)
@@ -63,6 +78,7 @@ struct Groups {           // replicated-node groups (interface and/or boundary n
   uint8_t* kind = nullptr;// BC kind per group (P2 only)
   double* normal = nullptr;// [n][3] (P2 only)
   int64_t ncopy = 0;
+  Halo halo;
 };
 
 struct Level {
@@ -119,6 +135,17 @@ int launch_elem(const Mesh* m, const Level& L, int mode, int form, const double*
                 const double* u, const double* p, double* yu, double* yp, cudaStream_t s);
 enum { ELEM_A = 1, ELEM_BT = 2, ELEM_DIV = 4, ELEM_DIAG = 8 };
 int launch_fixup(const Mesh* m, const Level& L, int space, bool sum, bool bc, double* v, cudaStream_t s);
+// split phases of a cross-rank interface sum: pack local partial sums of shared groups into
+// halo.sbuf; exchange (NCCL); final fixup adding halo.rbuf (launch_fixup does all three when the
+// mesh has a communicator)
+int launch_halo_pack(const Mesh* m, const Level& L, int space, const double* v, double* sbuf, cudaStream_t s);
+int launch_fixup_remote(const Mesh* m, const Level& L, int space, bool bc, const double* rbuf, double* v,
+                        cudaStream_t s);
+int comm_exchange(hhg_comm* c, const Halo& h, int nc, const double* sbuf, double* rbuf, cudaStream_t s);
+int comm_allreduce_sum(hhg_comm* c, double* buf, int64_t n, cudaStream_t s);
+int build_host_groups(const Mesh* m, int level, int space, std::vector<int64_t>& ptr, std::vector<int64_t>& copy,
+                      std::vector<uint8_t>& kind, std::vector<double>& normal, std::vector<uint8_t>& own,
+                      Halo& halo, std::vector<int64_t>& slot_group);
 int launch_dot(const Mesh* m, const Level& L, int space, const double* x, const double* y, double* out,
                cudaStream_t s);
 int launch_prolong(const Mesh* m, const Level& Lc, const Level& Lf, const double* xc, double* xf,
@@ -134,6 +161,10 @@ int launch_cheb0(int64_t n, const double* f, const double* t, const double* dinv
                  double* r, double* d, cudaStream_t s);  // r = f - t ; d = dinv r / theta
 int launch_chebk(int64_t n, const double* t, const double* dinv, double c1, double c2, double* x, double* r,
                  double* d, cudaStream_t s);            // x += d; r -= t; d = c1 d + c2 dinv r
+int launch_cheb_deg1(int64_t n, const double* f, const double* t, const double* dinv, double inv_theta, double* x,
+                     cudaStream_t s);                     // x += dinv (f - t) / theta  (t null: x = 0 first)
+int launch_chebk_last(int64_t n, const double* t, const double* dinv, double c1, double c2, const double* r,
+                      const double* d, double* x, cudaStream_t s);  // x += d + c1 d + c2 dinv (r - t)
 int launch_pcg_update(int64_t n, const double* scal, double* x, double* r, const double* p, const double* q,
                       const double* dinv, double* z, cudaStream_t s);
 int launch_scalar_ops(int op, double* scal, cudaStream_t s);
@@ -141,3 +172,9 @@ int launch_scalar_ops(int op, double* scal, cudaStream_t s);
 }  // namespace hhg
 
 struct hhg_mesh : public hhg::Mesh {};
+
+#include <nccl.h>
+struct hhg_comm {
+  ncclComm_t nccl = nullptr;
+  int nranks = 1, rank = 0, device = 0;
+};

@@ -17,47 +17,6 @@ namespace hhg {
 // Q4 rule (R6): barycentric (a,b,b,b) and permutations, weights 1/24.
 constexpr double QA = 0.58541019662496845446;  // (5 + 3 sqrt 5)/20
 constexpr double QB = 0.13819660112501051518;  // (5 - sqrt 5)/20
-constexpr double QAB = QA - QB;
-constexpr double WQ = 1.0 / 24.0;
-
-__constant__ int cTV[6][4][3] = {
-    {{0, 0, 0}, {1, 0, 0}, {0, 1, 0}, {0, 0, 1}},
-    {{0, 1, 0}, {1, 0, 0}, {1, 0, 1}, {1, 1, 0}},
-    {{0, 0, 1}, {0, 1, 0}, {1, 0, 0}, {1, 0, 1}},
-    {{0, 1, 0}, {0, 1, 1}, {1, 0, 1}, {1, 1, 0}},
-    {{0, 0, 1}, {0, 1, 0}, {0, 1, 1}, {1, 0, 1}},
-    {{0, 1, 1}, {1, 0, 1}, {1, 1, 0}, {1, 1, 1}},
-};
-// integer inverse of E_t (columns V1-V0, V2-V0, V3-V0), row-major, for the 6 types
-__constant__ int cEinv[6][9];
-
-// local P2 numbering: 0..3 vertices, 4..9 edges 01,02,03,12,13,23
-#define EI(m, j) (((m) == 0) ? (3 + (j)) : (((m) == 1) ? (((j) == 0) ? 4 : 5 + (j)) : (((m) == 2) ? (((j) == 0) ? 5 : ((j) == 1 ? 7 : 9)) : (((j) == 0) ? 6 : ((j) == 1 ? 8 : 9)))))
-
-__device__ __forceinline__ int64_t d_lidx(int i, int j, int k, int N) { return lidx(i, j, k, N); }
-
-static bool g_einv_ready = false;
-static int ensure_einv() {
-  if (g_einv_ready) return HHG_OK;
-  int h[6][9];
-  const int TV[6][4][3] = {
-      {{0, 0, 0}, {1, 0, 0}, {0, 1, 0}, {0, 0, 1}}, {{0, 1, 0}, {1, 0, 0}, {1, 0, 1}, {1, 1, 0}},
-      {{0, 0, 1}, {0, 1, 0}, {1, 0, 0}, {1, 0, 1}}, {{0, 1, 0}, {0, 1, 1}, {1, 0, 1}, {1, 1, 0}},
-      {{0, 0, 1}, {0, 1, 0}, {0, 1, 1}, {1, 0, 1}}, {{0, 1, 1}, {1, 0, 1}, {1, 1, 0}, {1, 1, 1}}};
-  for (int t = 0; t < 6; ++t) {
-    int E[9];
-    for (int r = 0; r < 3; ++r)
-      for (int c = 0; c < 3; ++c) E[3 * r + c] = TV[t][c + 1][r] - TV[t][0][r];
-    int det = E[0] * (E[4] * E[8] - E[5] * E[7]) - E[1] * (E[3] * E[8] - E[5] * E[6]) + E[2] * (E[3] * E[7] - E[4] * E[6]);
-    int adj[9] = {E[4] * E[8] - E[5] * E[7], E[2] * E[7] - E[1] * E[8], E[1] * E[5] - E[2] * E[4],
-                  E[5] * E[6] - E[3] * E[8], E[0] * E[8] - E[2] * E[6], E[2] * E[3] - E[0] * E[5],
-                  E[3] * E[7] - E[4] * E[6], E[1] * E[6] - E[0] * E[7], E[0] * E[4] - E[1] * E[3]};
-    for (int i = 0; i < 9; ++i) h[t][i] = adj[i] * det;  // det = +-1 -> inverse = adj/det = adj*det
-  }
-  HHG_CUDA(cudaMemcpyToSymbol(cEinv, h, sizeof(h)));
-  g_einv_ready = true;
-  return HHG_OK;
-}
 
 // ------------------------------------------------------------------ interface sum + BC
 template <int NC, bool BC>
@@ -94,7 +53,105 @@ __global__ void k_fixup(int64_t ng, const int64_t* __restrict__ ptr, const int64
     for (int c = 0; c < NC; ++c) v[c * cstride + copy[k]] = val[c];
 }
 
+// local partial sums of the groups shared with other ranks -> send buffer [slot][NC]
+template <int NC>
+__global__ void k_halo_pack(int64_t nslots, const int64_t* __restrict__ slot_group, const int64_t* __restrict__ ptr,
+                            const int64_t* __restrict__ copy, int64_t cstride, const double* __restrict__ v,
+                            double* __restrict__ sbuf) {
+  const int64_t sl = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (sl >= nslots) return;
+  const int64_t g = slot_group[sl], b = ptr[g], e = ptr[g + 1];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    double s = 0.0;
+    for (int64_t k = b; k < e; ++k) s += v[c * cstride + copy[k]];
+    sbuf[sl * NC + c] = s;
+  }
+}
+
+// interface sum including the partial sums received from other ranks, then BC, scattered to copies
+template <int NC, bool BC>
+__global__ void k_fixup_remote(int64_t ng, const int64_t* __restrict__ ptr, const int64_t* __restrict__ copy,
+                               const uint8_t* __restrict__ kind, const double* __restrict__ normal, int64_t cstride,
+                               const int64_t* __restrict__ gs_ptr, const int64_t* __restrict__ gs_idx,
+                               const double* __restrict__ rbuf, double* __restrict__ v) {
+  const int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gi >= ng) return;
+  const int64_t b = ptr[gi], e = ptr[gi + 1];
+  double val[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    double s = 0.0;
+    for (int64_t k = b; k < e; ++k) s += v[c * cstride + copy[k]];
+    for (int64_t k = gs_ptr[gi]; k < gs_ptr[gi + 1]; ++k) s += rbuf[gs_idx[k] * NC + c];
+    val[c] = s;
+  }
+  if (BC) {
+    const int kd = kind[gi];
+    if (kd == HHG_BC_DIRICHLET0) {
+#pragma unroll
+      for (int c = 0; c < NC; ++c) val[c] = 0.0;
+    } else if (kd == HHG_BC_FREESLIP && NC == 3) {
+      const double n0 = normal[3 * gi], n1 = normal[3 * gi + 1], n2 = normal[3 * gi + 2];
+      const double un = val[0] * n0 + val[1 % NC] * n1 + val[2 % NC] * n2;
+      val[0] -= un * n0;
+      val[1 % NC] -= un * n1;
+      val[2 % NC] -= un * n2;
+    }
+  }
+  for (int64_t k = b; k < e; ++k)
+#pragma unroll
+    for (int c = 0; c < NC; ++c) v[c * cstride + copy[k]] = val[c];
+}
+
+static const Groups& groups_of(const Level& L, int space) { return space == HHG_P1 ? L.g1 : L.g2; }
+
+int launch_halo_pack(const Mesh* m, const Level& L, int space, const double* v, double* sbuf, cudaStream_t s) {
+  const Groups& G = groups_of(L, space);
+  const Halo& H = G.halo;
+  if (H.nslots == 0) return HHG_OK;
+  const int64_t nm = macro_count(m);
+  const unsigned nb = (unsigned)((H.nslots + 255) / 256);
+  if (space == HHG_P2VEC)
+    k_halo_pack<3><<<nb, 256, 0, s>>>(H.nslots, H.slot_group, G.ptr, G.copy, nm * L.npts2, v, sbuf);
+  else
+    k_halo_pack<1><<<nb, 256, 0, s>>>(H.nslots, H.slot_group, G.ptr, G.copy, 0, v, sbuf);
+  count_launch();
+  HHG_CUDA(cudaGetLastError());
+  return HHG_OK;
+}
+
+int launch_fixup_remote(const Mesh* m, const Level& L, int space, bool bc, const double* rbuf, double* v,
+                        cudaStream_t s) {
+  const Groups& G = groups_of(L, space);
+  const Halo& H = G.halo;
+  if (G.n == 0) return HHG_OK;
+  const int64_t nm = macro_count(m);
+  const unsigned nb = (unsigned)((G.n + 255) / 256);
+  if (space == HHG_P2VEC) {
+    if (bc)
+      k_fixup_remote<3, true><<<nb, 256, 0, s>>>(G.n, G.ptr, G.copy, G.kind, G.normal, nm * L.npts2, H.gs_ptr,
+                                                 H.gs_idx, rbuf, v);
+    else
+      k_fixup_remote<3, false><<<nb, 256, 0, s>>>(G.n, G.ptr, G.copy, G.kind, G.normal, nm * L.npts2, H.gs_ptr,
+                                                  H.gs_idx, rbuf, v);
+  } else {
+    k_fixup_remote<1, false><<<nb, 256, 0, s>>>(G.n, G.ptr, G.copy, nullptr, nullptr, 0, H.gs_ptr, H.gs_idx, rbuf, v);
+  }
+  count_launch();
+  HHG_CUDA(cudaGetLastError());
+  return HHG_OK;
+}
+
 int launch_fixup(const Mesh* m, const Level& L, int space, bool sum, bool bc, double* v, cudaStream_t s) {
+  // multi-rank interface sum: pack shared partial sums, NCCL exchange, local + remote sum (+BC)
+  if (sum && m->comm && m->nranks > 1 && groups_of(L, space).halo.nslots > 0) {
+    const Halo& H = groups_of(L, space).halo;
+    const int nc = space == HHG_P2VEC ? 3 : 1;
+    HHG_TRY(launch_halo_pack(m, L, space, v, H.sbuf, s));
+    HHG_TRY(comm_exchange(m->comm, H, nc, H.sbuf, H.rbuf, s));
+    return launch_fixup_remote(m, L, space, bc && space == HHG_P2VEC, H.rbuf, v, s);
+  }
   const int64_t nm = macro_count(m);
   if (space == HHG_P2VEC) {
     // BC-only passes visit just the groups carrying a BC (they are sorted first)
@@ -168,6 +225,7 @@ int launch_dot(const Mesh* m, const Level& L, int space, const double* x, const 
   k_dot_final<<<1, 256, 0, s>>>(L.red, kRedBlocks, out);
   count_launch(2);
   HHG_CUDA(cudaGetLastError());
+  if (m->comm && m->nranks > 1) HHG_TRY(comm_allreduce_sum(m->comm, out, 1, s));
   return HHG_OK;
 }
 
@@ -187,102 +245,194 @@ __device__ __forceinline__ bool row_of(const int32_t* rows, int64_t nrows, int N
   return true;
 }
 
-// P2 prolongation: x_f += P x_c on every stored fine node (per macro, consistent copies)
-template <bool RESTRICT>
-__global__ void k_transfer(const int32_t* __restrict__ rowsf, int64_t nrowsf, int Nf, int64_t nptsf, int64_t nptsc,
-                           int64_t cstridef, int64_t cstridec, const uint8_t* __restrict__ ownf,
-                           const double* __restrict__ src, double* __restrict__ dst) {
+// ------------------------------------------------------------------ P2 transfers (stencil tables)
+// Prolongation = nodal interpolation of the coarse P2 function at the fine P2 nodes (DESIGN.md
+// R14); restriction = its transpose.  Both are gathers driven by host-built tables:
+//  * prolong: fine node F (fine P2 lattice index) lies in coarse cube F>>2 at offset o = F&3; the
+//    64 offset classes carry <= 10 (coarse node offset dC in [0,2]^3 from 2(F>>2), weight) pairs
+//    of the coarse tet containing the point (weights lambda(2 lambda - 1), 4 lambda_p lambda_q);
+//  * restrict: coarse node C gathers sum_F w(F,C) own(F) r(F) over the transposed stencil of its
+//    parity class (8 classes: coarse vertex or one of the 7 lattice edge directions), clipped to
+//    the macro's lattice.  No atomics; each output written once.
+constexpr int kPMax = 10, kRMax = 128;
+__constant__ int cPn[64];
+__constant__ int cPd[64][kPMax];      // dx + 3 dy + 9 dz
+__constant__ double cPw[64][kPMax];
+__device__ int cRn[8];
+__device__ int cRd[8][kRMax];         // (dx+8) | (dy+8) << 5 | (dz+8) << 10
+__device__ double cRw[8][kRMax];
+
+static bool g_tabs_ready = false;
+static int ensure_transfer_tabs() {
+  if (g_tabs_ready) return HHG_OK;
+  const int TV[6][4][3] = {
+      {{0, 0, 0}, {1, 0, 0}, {0, 1, 0}, {0, 0, 1}}, {{0, 1, 0}, {1, 0, 0}, {1, 0, 1}, {1, 1, 0}},
+      {{0, 0, 1}, {0, 1, 0}, {1, 0, 0}, {1, 0, 1}}, {{0, 1, 0}, {0, 1, 1}, {1, 0, 1}, {1, 1, 0}},
+      {{0, 0, 1}, {0, 1, 0}, {0, 1, 1}, {1, 0, 1}}, {{0, 1, 1}, {1, 0, 1}, {1, 1, 0}, {1, 1, 1}}};
+  const int ep[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
+  static int pn[64], pd[64][kPMax];
+  static double pw[64][kPMax];
+  for (int cls = 0; cls < 64; ++cls) {
+    const int o[3] = {cls & 3, (cls >> 2) & 3, cls >> 4};
+    pn[cls] = 0;
+    if (((o[0] | o[1] | o[2]) & 1) == 0) {
+      pd[cls][0] = o[0] / 2 + 3 * (o[1] / 2) + 9 * (o[2] / 2);
+      pw[cls][0] = 1.0;
+      pn[cls] = 1;
+      continue;
+    }
+    // coarse tet of the cube containing the point o/4 (Freudenthal split, sorted-coordinate rule)
+    const int S = o[0] + o[1] + o[2];
+    int t;
+    if (S <= 4) t = 0;
+    else if (S > 8) t = 5;
+    else {
+      const bool xy = o[0] + o[1] >= 4, yz = o[1] + o[2] >= 4;
+      t = xy ? (yz ? 3 : 1) : (yz ? 4 : 2);
+    }
+    // barycentric coordinates (exact multiples of 1/4): o = 4 V0 + sum_v b_v (V_v - V0)
+    double E[9];
+    for (int r = 0; r < 3; ++r)
+      for (int c = 0; c < 3; ++c) E[3 * r + c] = TV[t][c + 1][r] - TV[t][0][r];
+    const double det = E[0] * (E[4] * E[8] - E[5] * E[7]) - E[1] * (E[3] * E[8] - E[5] * E[6]) +
+                       E[2] * (E[3] * E[7] - E[4] * E[6]);
+    const double adj[9] = {E[4] * E[8] - E[5] * E[7], E[2] * E[7] - E[1] * E[8], E[1] * E[5] - E[2] * E[4],
+                           E[5] * E[6] - E[3] * E[8], E[0] * E[8] - E[2] * E[6], E[2] * E[3] - E[0] * E[5],
+                           E[3] * E[7] - E[4] * E[6], E[1] * E[6] - E[0] * E[7], E[0] * E[4] - E[1] * E[3]};
+    const double q[3] = {o[0] - 4.0 * TV[t][0][0], o[1] - 4.0 * TV[t][0][1], o[2] - 4.0 * TV[t][0][2]};
+    double lam[4];
+    for (int r = 0; r < 3; ++r) lam[r + 1] = 0.25 * (adj[3 * r] * q[0] + adj[3 * r + 1] * q[1] + adj[3 * r + 2] * q[2]) / det;
+    lam[0] = 1.0 - lam[1] - lam[2] - lam[3];
+    for (int v = 0; v < 4; ++v) {
+      const double w = lam[v] * (2.0 * lam[v] - 1.0);
+      if (w != 0.0) {
+        pd[cls][pn[cls]] = 2 * TV[t][v][0] + 3 * 2 * TV[t][v][1] + 9 * 2 * TV[t][v][2];
+        pw[cls][pn[cls]++] = w;
+      }
+    }
+    for (int e = 0; e < 6; ++e) {
+      const int p = ep[e][0], r = ep[e][1];
+      const double w = 4.0 * lam[p] * lam[r];
+      if (w != 0.0) {
+        pd[cls][pn[cls]] = (TV[t][p][0] + TV[t][r][0]) + 3 * (TV[t][p][1] + TV[t][r][1]) + 9 * (TV[t][p][2] + TV[t][r][2]);
+        pw[cls][pn[cls]++] = w;
+      }
+    }
+  }
+  // transpose: representative coarse node C = 8 + parity per dimension; scan fine nodes around 2C
+  static int rn[8], rd[8][kRMax];
+  static double rw[8][kRMax];
+  for (int pc = 0; pc < 8; ++pc) {
+    const int C[3] = {8 + (pc & 1), 8 + ((pc >> 1) & 1), 8 + (pc >> 2)};
+    rn[pc] = 0;
+    for (int dz = -8; dz <= 8; ++dz)
+      for (int dy = -8; dy <= 8; ++dy)
+        for (int dx = -8; dx <= 8; ++dx) {
+          const int F[3] = {2 * C[0] + dx, 2 * C[1] + dy, 2 * C[2] + dz};
+          const int cls = (F[0] & 3) + 4 * (F[1] & 3) + 16 * (F[2] & 3);
+          for (int e = 0; e < pn[cls]; ++e) {
+            const int d = pd[cls][e];
+            const int Cn[3] = {2 * (F[0] >> 2) + d % 3, 2 * (F[1] >> 2) + (d / 3) % 3, 2 * (F[2] >> 2) + d / 9};
+            if (Cn[0] == C[0] && Cn[1] == C[1] && Cn[2] == C[2]) {
+              if (rn[pc] >= kRMax) return fail(HHG_EINVAL, "restriction stencil table overflow");
+              rd[pc][rn[pc]] = (dx + 8) | ((dy + 8) << 5) | ((dz + 8) << 10);
+              rw[pc][rn[pc]++] = pw[cls][e];
+            }
+          }
+        }
+  }
+  HHG_CUDA(cudaMemcpyToSymbol(cPn, pn, sizeof(pn)));
+  HHG_CUDA(cudaMemcpyToSymbol(cPd, pd, sizeof(pd)));
+  HHG_CUDA(cudaMemcpyToSymbol(cPw, pw, sizeof(pw)));
+  HHG_CUDA(cudaMemcpyToSymbol(cRn, rn, sizeof(rn)));
+  HHG_CUDA(cudaMemcpyToSymbol(cRd, rd, sizeof(rd)));
+  HHG_CUDA(cudaMemcpyToSymbol(cRw, rw, sizeof(rw)));
+  g_tabs_ready = true;
+  return HHG_OK;
+}
+
+__device__ __forceinline__ int rowstart_i32(int N, int j, int k) {
+  const int M = N - k;
+  return ((N + 1) * (N + 2) * (N + 3) - (M + 1) * (M + 2) * (M + 3)) / 6 + (j * (2 * M + 3 - j)) / 2;
+}
+
+// x_f += P x_c on every stored fine node (per macro; consistent copies stay consistent)
+__global__ void k_prolong(const int32_t* __restrict__ rowsf, int64_t nrowsf, int Nf, int64_t nptsf, int64_t nptsc,
+                          int64_t cstridef, int64_t cstridec, const double* __restrict__ xc, double* __restrict__ xf) {
   RowCtx rc;
   if (!row_of(rowsf, nrowsf, Nf, rc)) return;
   const int mac = blockIdx.y;
   const int Nc = Nf / 2;
-  const int64_t fb = (int64_t)mac * nptsf + lidx(0, rc.j, rc.k, Nf);
-  const int64_t cb = (int64_t)mac * nptsc;
-  for (int i = threadIdx.x & 31; i < rc.len; i += 32) {
-    const int I = i, J = rc.j, K = rc.k;
-    const int64_t f = fb + i;
-    double w[10];
-    int64_t cid[10];
-    int nn;
-    if (((I | J | K) & 1) == 0) {
-      nn = 1;
-      w[0] = 1.0;
-      cid[0] = cb + lidx(I >> 1, J >> 1, K >> 1, Nc);
-    } else {
-      const int a0 = I >> 2, a1 = J >> 2, a2 = K >> 2;
-      const int F0 = I & 3, F1 = J & 3, F2 = K & 3;
-      const int S = F0 + F1 + F2;
-      int t;
-      if (S <= 4) t = 0;
-      else if (S > 8) t = 5;
-      else {
-        const bool xy = F0 + F1 >= 4, yz = F1 + F2 >= 4;
-        t = xy ? (yz ? 3 : 1) : (yz ? 4 : 2);
-      }
-      int V[4][3];
-#pragma unroll
-      for (int v = 0; v < 4; ++v)
-#pragma unroll
-        for (int r = 0; r < 3; ++r) V[v][r] = cTV[t][v][r];
-      const int q0 = F0 - 4 * V[0][0], q1 = F1 - 4 * V[0][1], q2 = F2 - 4 * V[0][2];
-      int b[4];
-      b[1] = cEinv[t][0] * q0 + cEinv[t][1] * q1 + cEinv[t][2] * q2;
-      b[2] = cEinv[t][3] * q0 + cEinv[t][4] * q1 + cEinv[t][5] * q2;
-      b[3] = cEinv[t][6] * q0 + cEinv[t][7] * q1 + cEinv[t][8] * q2;
-      b[0] = 4 - b[1] - b[2] - b[3];
-      double lam[4];
-#pragma unroll
-      for (int v = 0; v < 4; ++v) lam[v] = 0.25 * b[v];
-#pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        w[v] = lam[v] * (2.0 * lam[v] - 1.0);
-        cid[v] = cb + lidx(2 * (a0 + V[v][0]), 2 * (a1 + V[v][1]), 2 * (a2 + V[v][2]), Nc);
-      }
-      const int ep[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
-#pragma unroll
-      for (int e = 0; e < 6; ++e) {
-        const int p = ep[e][0], q = ep[e][1];
-        w[4 + e] = 4.0 * lam[p] * lam[q];
-        cid[4 + e] = cb + lidx(2 * a0 + V[p][0] + V[q][0], 2 * a1 + V[p][1] + V[q][1], 2 * a2 + V[p][2] + V[q][2], Nc);
-      }
-      nn = 10;
+  const int J = rc.j, K = rc.k;
+  double* fr = xf + (int64_t)mac * nptsf + rowstart_i32(Nf, J, K);
+  const double* cm = xc + (int64_t)mac * nptsc;
+  for (int I = threadIdx.x & 31; I < rc.len; I += 32) {
+    const int cls = (I & 3) + 4 * (J & 3) + 16 * (K & 3);
+    const int bx = 2 * (I >> 2), by = 2 * (J >> 2), bz = 2 * (K >> 2);
+    const int n = cPn[cls];
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    for (int e = 0; e < n; ++e) {
+      const int d = cPd[cls][e];
+      const int ci = rowstart_i32(Nc, by + (d / 3) % 3, bz + d / 9) + bx + d % 3;
+      const double w = cPw[cls][e];
+      s0 += w * __ldg(cm + ci);
+      s1 += w * __ldg(cm + cstridec + ci);
+      s2 += w * __ldg(cm + 2 * cstridec + ci);
     }
-    if (!RESTRICT) {
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        double s = 0.0;
-        for (int a = 0; a < nn; ++a) s += w[a] * src[c * cstridec + cid[a]];
-        dst[c * cstridef + f] += s;
-      }
-    } else {
-      if (!ownf[f]) continue;
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const double r = src[c * cstridef + f];
-        for (int a = 0; a < nn; ++a)
-          if (w[a] != 0.0) atomicAdd(dst + c * cstridec + cid[a], w[a] * r);
-      }
+    fr[I] += s0;
+    fr[cstridef + I] += s1;
+    fr[2 * cstridef + I] += s2;
+  }
+}
+
+// r_c = P^T r_f over owned fine copies (per macro), written (not accumulated) on every coarse node
+__global__ void k_restrict(const int32_t* __restrict__ rowsc, int64_t nrowsc, int Nc, int64_t nptsf, int64_t nptsc,
+                           int64_t cstridef, int64_t cstridec, const uint8_t* __restrict__ ownf,
+                           const double* __restrict__ rf, double* __restrict__ rc_out) {
+  RowCtx rc;
+  if (!row_of(rowsc, nrowsc, Nc, rc)) return;
+  const int mac = blockIdx.y;
+  const int Nf = 2 * Nc;
+  const int J = rc.j, K = rc.k;
+  const int64_t fb = (int64_t)mac * nptsf;
+  double* cr = rc_out + (int64_t)mac * nptsc + rowstart_i32(Nc, J, K);
+  for (int I = threadIdx.x & 31; I < rc.len; I += 32) {
+    const int pc = (I & 1) | ((J & 1) << 1) | ((K & 1) << 2);
+    const int n = cRn[pc];
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    for (int e = 0; e < n; ++e) {
+      const int d = cRd[pc][e];
+      const int fx = 2 * I + (d & 31) - 8, fy = 2 * J + ((d >> 5) & 31) - 8, fz = 2 * K + (d >> 10) - 8;
+      if (fx < 0 || fy < 0 || fz < 0 || fx + fy + fz > Nf) continue;
+      const int64_t fi = fb + rowstart_i32(Nf, fy, fz) + fx;
+      if (!ownf[fi]) continue;
+      const double w = cRw[pc][e];
+      s0 += w * __ldg(rf + fi);
+      s1 += w * __ldg(rf + cstridef + fi);
+      s2 += w * __ldg(rf + 2 * cstridef + fi);
     }
+    cr[I] = s0;
+    cr[cstridec + I] = s1;
+    cr[2 * cstridec + I] = s2;
   }
 }
 
 int launch_prolong(const Mesh* m, const Level& Lc, const Level& Lf, const double* xc, double* xf, cudaStream_t s) {
-  HHG_TRY(ensure_einv());
+  HHG_TRY(ensure_transfer_tabs());
   const int64_t nm = macro_count(m);
   dim3 grid((unsigned)((Lf.nrows2 + 7) / 8), (unsigned)nm);
-  k_transfer<false><<<grid, 256, 0, s>>>(Lf.rows2, Lf.nrows2, Lf.n2, Lf.npts2, Lc.npts2, nm * Lf.npts2,
-                                         nm * Lc.npts2, Lf.own2, xc, xf);
+  k_prolong<<<grid, 256, 0, s>>>(Lf.rows2, Lf.nrows2, Lf.n2, Lf.npts2, Lc.npts2, nm * Lf.npts2, nm * Lc.npts2, xc, xf);
   count_launch();
   HHG_CUDA(cudaGetLastError());
   return HHG_OK;
 }
 
 int launch_restrict(const Mesh* m, const Level& Lc, const Level& Lf, const double* rf, double* rc, cudaStream_t s) {
-  HHG_TRY(ensure_einv());
+  HHG_TRY(ensure_transfer_tabs());
   const int64_t nm = macro_count(m);
-  dim3 grid((unsigned)((Lf.nrows2 + 7) / 8), (unsigned)nm);
-  k_transfer<true><<<grid, 256, 0, s>>>(Lf.rows2, Lf.nrows2, Lf.n2, Lf.npts2, Lc.npts2, nm * Lf.npts2,
-                                        nm * Lc.npts2, Lf.own2, rf, rc);
+  dim3 grid((unsigned)((Lc.nrows2 + 7) / 8), (unsigned)nm);
+  k_restrict<<<grid, 256, 0, s>>>(Lc.rows2, Lc.nrows2, Lc.n2, Lf.npts2, Lc.npts2, nm * Lf.npts2, nm * Lc.npts2,
+                                  Lf.own2, rf, rc);
   count_launch();
   HHG_CUDA(cudaGetLastError());
   return HHG_OK;
@@ -359,12 +509,30 @@ static inline unsigned vgrid(int64_t n) {
 __global__ void k_axpby(int64_t n, double a, const double* __restrict__ x, double b, double* __restrict__ y) {
   GRID_STRIDE(i, n) y[i] = a * x[i] + b * y[i];
 }
+// first Chebyshev step: r = f - t (t = A x, or x = 0 when t == nullptr), d = D^-1 r / theta
 __global__ void k_cheb0(int64_t n, const double* __restrict__ f, const double* __restrict__ t,
                         const double* __restrict__ dinv, double it, double* __restrict__ r, double* __restrict__ d) {
   GRID_STRIDE(i, n) {
-    const double ri = f[i] - t[i];
+    const double ri = t ? f[i] - t[i] : f[i];
     r[i] = ri;
     d[i] = dinv[i] * ri * it;
+  }
+}
+// degree-1 sweep fused: x += D^-1 (f - t) / theta   (t == nullptr: x = 0 on entry)
+__global__ void k_cheb_deg1(int64_t n, const double* __restrict__ f, const double* __restrict__ t,
+                            const double* __restrict__ dinv, double it, double* __restrict__ x) {
+  GRID_STRIDE(i, n) {
+    const double ri = t ? f[i] - t[i] : f[i];
+    x[i] = (t ? x[i] : 0.0) + dinv[i] * ri * it;
+  }
+}
+// last Chebyshev step fused with the final update: x += d + (c1 d + c2 D^-1 (r - t)); r, d dead after
+__global__ void k_chebk_last(int64_t n, const double* __restrict__ t, const double* __restrict__ dinv, double c1,
+                             double c2, const double* __restrict__ r, const double* __restrict__ d,
+                             double* __restrict__ x) {
+  GRID_STRIDE(i, n) {
+    const double di = d[i];
+    x[i] += di + (c1 * di + c2 * dinv[i] * (r[i] - t[i]));
   }
 }
 __global__ void k_chebk(int64_t n, const double* __restrict__ t, const double* __restrict__ dinv, double c1, double c2,
@@ -387,6 +555,20 @@ int launch_axpby(int64_t n, double a, const double* x, double b, double* y, cuda
 int launch_cheb0(int64_t n, const double* f, const double* t, const double* dinv, double inv_theta, double* r,
                  double* d, cudaStream_t s) {
   k_cheb0<<<vgrid(n), 256, 0, s>>>(n, f, t, dinv, inv_theta, r, d);
+  count_launch();
+  HHG_CUDA(cudaGetLastError());
+  return HHG_OK;
+}
+int launch_cheb_deg1(int64_t n, const double* f, const double* t, const double* dinv, double inv_theta, double* x,
+                     cudaStream_t s) {
+  k_cheb_deg1<<<vgrid(n), 256, 0, s>>>(n, f, t, dinv, inv_theta, x);
+  count_launch();
+  HHG_CUDA(cudaGetLastError());
+  return HHG_OK;
+}
+int launch_chebk_last(int64_t n, const double* t, const double* dinv, double c1, double c2, const double* r,
+                      const double* d, double* x, cudaStream_t s) {
+  k_chebk_last<<<vgrid(n), 256, 0, s>>>(n, t, dinv, c1, c2, r, d, x);
   count_launch();
   HHG_CUDA(cudaGetLastError());
   return HHG_OK;

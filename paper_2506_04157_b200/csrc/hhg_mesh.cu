@@ -69,6 +69,11 @@ void free_level(Level& L) {
     f(g->copy);
     f(g->kind);
     f(g->normal);
+    f(g->halo.slot_group);
+    f(g->halo.gs_ptr);
+    f(g->halo.gs_idx);
+    f(g->halo.sbuf);
+    f(g->halo.rbuf);
     *g = Groups();
   }
   f(L.own1);
@@ -170,49 +175,123 @@ static int upload(T** dst, const std::vector<T>& src) {
   return HHG_OK;
 }
 
-static int build_groups(const Mesh* m, const Prims& P, int N, bool with_bc, Groups& G, std::vector<uint8_t>& own,
-                        int64_t npts) {
+// Replicated-node groups of one level/space (host): every node that lives on a macro primitive
+// held by several local macros, carries a BC, or is shared with another rank gets a group (its
+// local copies).  Owner of a node = its copy in the LOWEST GLOBAL macro id containing it (so the
+// owner masks of all ranks together count every node once).  Cross-rank slots: for each other
+// rank holding the primitive, one slot per interior node, in (primitive key, weight) order.
+static void host_groups(const Mesh* m, const Prims& P, int N, bool with_bc, int64_t npts,
+                        std::vector<int64_t>& ptr, std::vector<int64_t>& copy, std::vector<uint8_t>& kind,
+                        std::vector<double>& normal, std::vector<uint8_t>& own, Halo& halo,
+                        std::vector<int64_t>& slot_group) {
   std::vector<int64_t> gl_to_loc(m->n_tets, -1);
   for (size_t i = 0; i < m->local.size(); ++i) gl_to_loc[m->local[i]] = (int64_t)i;
-  std::vector<int64_t> ptr{0}, copy;
-  std::vector<uint8_t> kind;
-  std::vector<double> normal;
+  ptr.assign(1, 0);
+  copy.clear();
+  kind.clear();
+  normal.clear();
   own.assign((size_t)npts * m->local.size(), 1);
+  std::map<Key3, int64_t> gstart;
   // two passes: groups carrying a BC first (so BC-only fixups touch just them), then the rest
   for (int pass = 0; pass < 2; ++pass)
+    for (auto& kv : P.macros) {
+      const Key3& p = kv.first;
+      const int d = p[1] < 0 ? 0 : (p[2] < 0 ? 1 : 2);
+      std::vector<int64_t> loc;
+      bool remote = false;
+      for (int64_t t : kv.second) {
+        if (gl_to_loc[t] >= 0) loc.push_back(t);
+        else remote = true;
+      }
+      if (loc.empty()) continue;
+      int k = HHG_BC_NONE;
+      if (with_bc) {
+        auto it = P.bc.find(p);
+        if (it != P.bc.end()) k = it->second;
+      }
+      const int64_t owner = kv.second.front();  // macros listed in ascending global id
+      if (pass == 0)
+        for_interior(d, N, [&](const int* w) {  // owner masks (all replicated nodes, grouped or not)
+          for (size_t c = 0; c < loc.size(); ++c) {
+            int ijk[3];
+            local_ijk(&m->tets[4 * loc[c]], p.data(), w, d, ijk);
+            own[gl_to_loc[loc[c]] * npts + lidx(ijk[0], ijk[1], ijk[2], N)] = loc[c] == owner ? 1 : 0;
+          }
+        });
+      if (loc.size() < 2 && k == HHG_BC_NONE && !remote) continue;
+      if ((pass == 0) != (k != HHG_BC_NONE)) continue;
+      gstart[p] = (int64_t)ptr.size() - 1;
+      for_interior(d, N, [&](const int* w) {
+        for (size_t c = 0; c < loc.size(); ++c) {
+          int ijk[3];
+          local_ijk(&m->tets[4 * loc[c]], p.data(), w, d, ijk);
+          copy.push_back(gl_to_loc[loc[c]] * npts + lidx(ijk[0], ijk[1], ijk[2], N));
+        }
+        ptr.push_back((int64_t)copy.size());
+        if (with_bc) {
+          kind.push_back((uint8_t)k);
+          double x[3] = {0, 0, 0};
+          for (int r = 0; r <= d; ++r)
+            for (int c = 0; c < 3; ++c) x[c] += (double)w[r] / N * m->xyz[3 * p[r] + c];
+          double nr = std::sqrt(x[0] * x[0] + x[1] * x[1] + x[2] * x[2]);
+          for (int c = 0; c < 3; ++c) normal.push_back(nr > 0 ? x[c] / nr : 0.0);
+        }
+      });
+    }
+  // cross-rank slots, neighbor-major, then primitive-key / weight order
+  halo = Halo();
+  slot_group.clear();
+  std::map<int, std::vector<std::pair<int64_t, std::array<int64_t, 10>>>> per;
   for (auto& kv : P.macros) {
     const Key3& p = kv.first;
-    int d = p[1] < 0 ? 0 : (p[2] < 0 ? 1 : 2);
-    std::vector<int64_t> loc;
+    auto gs = gstart.find(p);
+    if (gs == gstart.end()) continue;
+    std::set<int> ranks;
     for (int64_t t : kv.second)
-      if (gl_to_loc[t] >= 0) loc.push_back(t);
-    if (loc.empty()) continue;
-    int k = HHG_BC_NONE;
-    if (with_bc) {
-      auto it = P.bc.find(p);
-      if (it != P.bc.end()) k = it->second;
-    }
-    if (loc.size() < 2 && k == HHG_BC_NONE) continue;
-    if ((pass == 0) != (k != HHG_BC_NONE)) continue;
+      if (m->tet_rank[t] != m->rank) ranks.insert(m->tet_rank[t]);
+    if (ranks.empty()) continue;
+    const int d = p[1] < 0 ? 0 : (p[2] < 0 ? 1 : 2);
+    int64_t i = 0;
     for_interior(d, N, [&](const int* w) {
-      for (size_t c = 0; c < loc.size(); ++c) {
-        int ijk[3];
-        local_ijk(&m->tets[4 * loc[c]], p.data(), w, d, ijk);
-        int64_t flat = gl_to_loc[loc[c]] * npts + lidx(ijk[0], ijk[1], ijk[2], N);
-        copy.push_back(flat);
-        if (c > 0) own[flat] = 0;
-      }
-      ptr.push_back((int64_t)copy.size());
-      if (with_bc) {
-        kind.push_back((uint8_t)k);
-        double x[3] = {0, 0, 0};
-        for (int r = 0; r <= d; ++r)
-          for (int c = 0; c < 3; ++c) x[c] += (double)w[r] / N * m->xyz[3 * p[r] + c];
-        double nr = std::sqrt(x[0] * x[0] + x[1] * x[1] + x[2] * x[2]);
-        for (int c = 0; c < 3; ++c) normal.push_back(nr > 0 ? x[c] / nr : 0.0);
-      }
+      std::array<int64_t, 10> key;
+      key[0] = d;
+      for (int c = 0; c < 4; ++c) key[1 + c] = c <= d ? p[c] : -1;
+      for (int c = 0; c < 4; ++c) key[5 + c] = c <= d ? w[c] : 0;
+      key[9] = N;
+      for (int q : ranks) per[q].push_back({gs->second + i, key});
+      ++i;
     });
   }
+  halo.off.push_back(0);
+  for (auto& kv : per) {
+    halo.nbr.push_back(kv.first);
+    for (auto& e : kv.second) {
+      slot_group.push_back(e.first);
+      halo.keys.insert(halo.keys.end(), e.second.begin(), e.second.end());
+    }
+    halo.off.push_back((int64_t)slot_group.size());
+  }
+  halo.nslots = (int64_t)slot_group.size();
+}
+
+int build_host_groups(const Mesh* m, int level, int space, std::vector<int64_t>& ptr, std::vector<int64_t>& copy,
+                      std::vector<uint8_t>& kind, std::vector<double>& normal, std::vector<uint8_t>& own,
+                      Halo& halo, std::vector<int64_t>& slot_group) {
+  Prims P;
+  build_prims(m, P);
+  const int n1 = 1 << level;
+  const bool p1 = space == HHG_P1;
+  const int N = p1 ? n1 : 2 * n1;
+  host_groups(m, P, N, !p1, npts3(N), ptr, copy, kind, normal, own, halo, slot_group);
+  return HHG_OK;
+}
+
+static int build_groups(const Mesh* m, const Prims& P, int N, bool with_bc, Groups& G, std::vector<uint8_t>& own,
+                        int64_t npts) {
+  std::vector<int64_t> ptr, copy, slot_group;
+  std::vector<uint8_t> kind;
+  std::vector<double> normal;
+  host_groups(m, P, N, with_bc, npts, ptr, copy, kind, normal, own, G.halo, slot_group);
   G.n = (int64_t)ptr.size() - 1;
   G.nbc = with_bc ? (int64_t)std::count_if(kind.begin(), kind.end(), [](uint8_t k) { return k != HHG_BC_NONE; }) : 0;
   G.ncopy = (int64_t)copy.size();
@@ -221,6 +300,22 @@ static int build_groups(const Mesh* m, const Prims& P, int N, bool with_bc, Grou
   if (with_bc) {
     HHG_TRY(upload(&G.kind, kind));
     HHG_TRY(upload(&G.normal, normal));
+  }
+  Halo& H = G.halo;
+  if (H.nslots > 0) {
+    // CSR group -> slots
+    std::vector<int64_t> gp(G.n + 1, 0), gi(H.nslots);
+    for (int64_t s = 0; s < H.nslots; ++s) ++gp[slot_group[s] + 1];
+    for (int64_t g = 0; g < G.n; ++g) gp[g + 1] += gp[g];
+    std::vector<int64_t> fill(gp.begin(), gp.end() - 1);
+    for (int64_t s = 0; s < H.nslots; ++s) gi[fill[slot_group[s]]++] = s;
+    HHG_TRY(upload(&H.slot_group, slot_group));
+    HHG_TRY(upload(&H.gs_ptr, gp));
+    HHG_TRY(upload(&H.gs_idx, gi));
+    const int nc = with_bc ? 3 : 1;
+    if (cudaMalloc(&H.sbuf, nc * H.nslots * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&H.rbuf, nc * H.nslots * sizeof(double)) != cudaSuccess)
+      return fail(HHG_ENOMEM, "cudaMalloc halo buffers");
   }
   return HHG_OK;
 }

@@ -130,6 +130,9 @@ static int mg_apply(hhg_mg* mg, int l, const double* u, double* y, cudaStream_t 
 }
 
 static int mg_cheb(hhg_mg* mg, int l, double* x, const double* f, bool x_is_zero, cudaStream_t s) {
+  // Chebyshev sweep of degree k on D^-1 A over [b/10, b] (R12).  Vector updates fused:
+  // the first step skips A x when x = 0, the last step folds "x += d" into the d-update and drops the
+  // dead r/d writes; the BC projection of that last d moves onto x (P_v M is linear, x consistent).
   auto& L = mg->lv[l];
   const Mesh* m = mg->mesh;
   const int64_t n = p2vec_len(m, l);
@@ -137,23 +140,29 @@ static int mg_cheb(hhg_mg* mg, int l, double* x, const double* f, bool x_is_zero
   const double theta = 0.5 * (b + a), delta = 0.5 * (b - a), sigma = theta / delta;
   double rho = 1.0 / sigma;
   const Level& LL = m->levels[l];
-  if (x_is_zero) {
-    HHG_CUDA(cudaMemsetAsync(L.t, 0, n * sizeof(double), s));
-  } else {
+  const double* t0 = nullptr;
+  if (!x_is_zero) {
     HHG_TRY(mg_apply(mg, l, x, L.t, s));
+    t0 = L.t;
   }
-  HHG_TRY(launch_cheb0(n, f, L.t, L.dinv, 1.0 / theta, L.r, L.d, s));
+  const int deg = mg->prm.degree;
+  if (deg == 1) {
+    HHG_TRY(launch_cheb_deg1(n, f, t0, L.dinv, 1.0 / theta, x, s));
+    return launch_fixup(m, LL, HHG_P2VEC, false, true, x, s);
+  }
+  HHG_TRY(launch_cheb0(n, f, t0, L.dinv, 1.0 / theta, L.r, L.d, s));
   HHG_TRY(launch_fixup(m, LL, HHG_P2VEC, false, true, L.d, s));
-  for (int k = 1; k <= mg->prm.degree; ++k) {
-    if (k < mg->prm.degree) {
-      HHG_TRY(mg_apply(mg, l, L.d, L.t, s));
-      const double rn = 1.0 / (2.0 * sigma - rho);
+  for (int k = 1; k < deg; ++k) {
+    HHG_TRY(mg_apply(mg, l, L.d, L.t, s));
+    const double rn = 1.0 / (2.0 * sigma - rho);
+    if (k < deg - 1) {
       HHG_TRY(launch_chebk(n, L.t, L.dinv, rn * rho, 2.0 * rn / delta, x, L.r, L.d, s));
       HHG_TRY(launch_fixup(m, LL, HHG_P2VEC, false, true, L.d, s));
-      rho = rn;
     } else {
-      HHG_TRY(launch_axpby(n, 1.0, L.d, 1.0, x, s));
+      HHG_TRY(launch_chebk_last(n, L.t, L.dinv, rn * rho, 2.0 * rn / delta, L.r, L.d, x, s));
+      HHG_TRY(launch_fixup(m, LL, HHG_P2VEC, false, true, x, s));
     }
+    rho = rn;
   }
   return HHG_OK;
 }

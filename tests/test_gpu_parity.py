@@ -115,6 +115,35 @@ def test_shell_transfers(shell_l2):
     assert rel_l2(canon(M, 1, hhg.HHG_P2VEC, rc), d1.project(P.T @ rf_o)) <= 1e-14
 
 
+@pytest.mark.parametrize("case", ["shell_L3_L4", "tet_L2_L3"])
+def test_transfers_larger_levels(case):
+    """P2 prolongation / restriction on lattices large enough for unclipped interior stencils
+    (coarse vertex stencils of 125 fine nodes), against the oracle's assembled P and P^T."""
+    from oracle.multigrid import p2_prolongation, vec_prolongation
+    from oracle.refine import build_level
+    from oracle.operators import Discretisation
+    if case == "shell_L3_L4":
+        mac, lf, blended, bc = icoshell(3, 2), 4, True, BC_SHELL
+    else:
+        mac, lf, blended, bc = reference_tet(), 3, False, BC_ALL
+    from tests.harness import oracle_bc
+    lmc = build_level(mac.verts, mac.tets, mac.vtag, lf - 1)
+    lmf = build_level(mac.verts, mac.tets, mac.vtag, lf)
+    dc = Discretisation(lmc, blended, None, 0.0, oracle_bc(bc), build=())
+    df = Discretisation(lmf, blended, None, 0.0, oracle_bc(bc), build=())
+    P = vec_prolongation(p2_prolongation(lmc, lmf))
+    M = lib_mesh(mac, lf, blended, bc)
+    xc_o = dc.project(uniform_vec(lmc.p2_keys, 21))
+    xf_o = df.project(uniform_vec(lmf.p2_keys, 22))
+    xc, xf = lib_u(M, lf - 1, 21), lib_u(M, lf, 22)
+    hhg.p2_prolong(M, lf - 1, xc, xf)
+    assert rel_l2(canon(M, lf, hhg.HHG_P2VEC, xf), xf_o + df.project(P @ xc_o)) <= 1e-14
+    rf = lib_u(M, lf, 23)
+    rc = hhg.p2_restrict(M, lf, rf)
+    rf_o = df.project(uniform_vec(lmf.p2_keys, 23))
+    assert rel_l2(canon(M, lf - 1, hhg.HHG_P2VEC, rc), dc.project(P.T @ rf_o)) <= 1e-14
+
+
 def test_power_iteration_and_chebyshev_level2(shell_l2):
     from oracle.multigrid import chebyshev, power_iteration
     mac, lm, d, eta_o, M = shell_l2
