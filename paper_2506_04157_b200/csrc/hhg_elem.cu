@@ -389,8 +389,14 @@ __global__ void __launch_bounds__(kBT, HHG_ELEM_MINB)
   constexpr int NSU = HAS_U_OUT ? kNS2 : 0;
   constexpr int NS = NSU + (DO_DIV ? kNS1 : 0);
   extern __shared__ double sm[];  // [NS][kBT] cube slots | geometry [kGeoSm] | row starts int[13][kBT]
+#ifdef HHG_GEO_GLOBAL
+  // per-macro geometry read through L1 (saves 1 KB of shared memory per CTA)
+  const double* sgeo = lgeo + (int64_t)blockIdx.y * kLevelGeo;
+  int* rs2 = reinterpret_cast<int*>(sm + NS * kBT) + threadIdx.x;  // [9][kBT]
+#else
   double* sgeo = sm + NS * kBT;
   int* rs2 = reinterpret_cast<int*>(sgeo + kGeoSm) + threadIdx.x;  // [9][kBT]
+#endif
   int* rs1 = rs2 + 9 * kBT;                                         // [4][kBT]
 
   const int mac = blockIdx.y;
@@ -401,7 +407,11 @@ __global__ void __launch_bounds__(kBT, HHG_ELEM_MINB)
   const int n2 = 2 * n1;
 
   const double* Gm = lgeo + (int64_t)mac * kLevelGeo;
+#ifndef HHG_GEO_GLOBAL
   for (int r = tid; r < kGeoSm; r += kBT) sgeo[r] = __ldg(Gm + r);
+#else
+  (void)Gm;
+#endif
   const MacroGeo& g = mgeo[mac];
   double nh[3] = {0, 0, 0}, cK = 1.0;
   if (BLEND) {
@@ -600,6 +610,248 @@ __global__ void __launch_bounds__(kBT, HHG_ELEM_MINB)
   }
 }
 
+// ================================================================ element kernel v6 ("footprint")
+// The brick's u footprint (9x9x9 doubled-lattice points x 3 comps) and P1 footprint (eta, p) are
+// staged in shared memory with cp.async; every tet reads its dofs with LDS at table offsets.
+// Outputs accumulate in a PER-WARP output footprint (warp w owns cube layers z = 2w, 2w+1, i.e.
+// points Z in [4w, 4w+4]) with plain load-add-store in 5 rounds separated by __syncwarp: in one
+// round all lanes (same tet type, different cubes) update the same local node index, hence
+// distinct points; the 6 edge midpoints of a tet have pairwise different parity classes (host-
+// checked), so they share one round, and the 4 vertices take one round each.  No atomics and no
+// per-cube slots.  After __syncthreads the CTA writes the footprint: plain stores inside, fp64 RED
+// on the footprint border (shared with neighbouring bricks), the two warps' Z = 4 planes summed.
+// Layout word(X,Y,Z) = xs(X) + kPY*Y + kPZ*Z, xs(X) = X/2 (even X) or 5 + X/2 (odd X): lanes
+// (x,y) of a half-warp then hit x + 20y + const -> 16 distinct 8-byte bank pairs.
+constexpr int kPY = 10, kPZ = 9 * kPY;     // row / plane pitch (words)
+constexpr int kFU = 9 * kPZ;               // u footprint words per component (810)
+constexpr int kFY = 5 * kPZ;               // per-warp output footprint words per component (450)
+constexpr int kF1 = 125, kF1Y = 75;        // P1 footprints: brick 5x5x5, per warp 5x5x3
+__host__ __device__ constexpr int xs(int X) { return (X & 1) ? 5 + (X >> 1) : (X >> 1); }
+__host__ __device__ constexpr int fword(int X, int Y, int Z) { return xs(X) + kPY * Y + kPZ * Z; }
+__constant__ int eOffU[6][10];  // footprint word offset of each local node from its cube's base word
+__constant__ int eOffP[6][4];   // P1 footprint offset of each vertex from the cube's P1 base
+
+struct FootU {
+  const double* b;  // su + cube base word
+  const int* off;   // eOffU[t]
+  __device__ __forceinline__ double operator()(int a, int c) const { return b[c * kFU + off[a]]; }
+};
+
+template <int MODE>
+__host__ __device__ constexpr int fp_smem_words() {
+  return ((MODE & (ELEM_A | ELEM_DIV)) ? 3 * kFU : 0) + ((MODE & (ELEM_A | ELEM_BT | ELEM_DIAG)) ? 2 * 3 * kFY : 0) +
+         kF1 + ((MODE & ELEM_BT) ? kF1 : 0) + ((MODE & ELEM_DIV) ? 2 * kF1Y : 0) + kGeoSm;
+}
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+template <bool BLEND, int MODE, bool FULL>
+#ifndef HHG_FP_MINB
+#define HHG_FP_MINB 5
+#endif
+__global__ void __launch_bounds__(kBT, HHG_FP_MINB)
+    k_elem_fp(const MacroGeo* __restrict__ mgeo, const double* __restrict__ lgeo, const int32_t* __restrict__ bricks,
+              int n1, double inv_n1, int64_t npts1, int64_t npts2, int64_t cstride, const double* __restrict__ eta,
+              const double* __restrict__ u, const double* __restrict__ p, double* __restrict__ yu,
+              double* __restrict__ yp, double gamma) {
+  constexpr bool DO_DIV = (MODE & ELEM_DIV) != 0;
+  constexpr bool NEED_U = (MODE & (ELEM_A | ELEM_DIV)) != 0;
+  constexpr bool NEED_P = (MODE & ELEM_BT) != 0;
+  constexpr bool HAS_U_OUT = (MODE & (ELEM_A | ELEM_BT | ELEM_DIAG)) != 0;
+  extern __shared__ double sm[];
+  double* su = sm;                                   // [3][kFU]
+  double* sy = su + (NEED_U ? 3 * kFU : 0);          // [2 warps][3][kFY]
+  double* se = sy + (HAS_U_OUT ? 6 * kFY : 0);       // [kF1]
+  double* sp = se + kF1;                             // [kF1]
+  double* syp = sp + (NEED_P ? kF1 : 0);             // [2 warps][kF1Y]
+  double* sgeo = syp + (DO_DIV ? 2 * kF1Y : 0);      // [kGeoSm]
+
+  const int mac = blockIdx.y;
+  const int32_t bpk = __ldg(bricks + blockIdx.x);
+  const int i0 = bpk & 1023, j0 = (bpk >> 10) & 1023, k0 = bpk >> 20;
+  const int delta = n1 - (i0 + j0 + k0);
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int n2 = 2 * n1;
+  const int64_t mb2 = (int64_t)mac * npts2, mb1 = (int64_t)mac * npts1;
+
+  // ---- stage: u footprint (cp.async), eta / p footprints, geometry; zero the output footprints
+  const double* Gm = lgeo + (int64_t)mac * kLevelGeo;
+  for (int r = tid; r < kGeoSm; r += kBT) sgeo[r] = __ldg(Gm + r);
+  if (NEED_U) {
+#pragma unroll 1
+    for (int L = tid; L < 729; L += kBT) {
+      const int X = L % 9, Y = (L / 9) % 9, Z = L / 81;
+      const int gx = 2 * i0 + X, gy = 2 * j0 + Y, gz = 2 * k0 + Z;
+      if (gx + gy + gz > n2) continue;
+      const double* src = u + mb2 + rowstart32(n2, gy, gz) + gx;
+      const int w = fword(X, Y, Z);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) cp_async8(su + c * kFU + w, src + c * cstride);
+    }
+  }
+  if (HAS_U_OUT)
+    for (int r = tid; r < 6 * kFY; r += kBT) sy[r] = 0.0;
+  if (DO_DIV)
+    for (int r = tid; r < 2 * kF1Y; r += kBT) syp[r] = 0.0;
+  for (int L = tid; L < kF1; L += kBT) {
+    const int X = L % 5, Y = (L / 5) % 5, Z = L / 25;
+    const int gx = i0 + X, gy = j0 + Y, gz = k0 + Z;
+    const bool in = gx + gy + gz <= n1;
+    const int64_t ix = mb1 + (in ? rowstart32(n1, gy, gz) + gx : 0);
+    se[L] = (eta != nullptr && in) ? __ldg(eta + ix) : 1.0;
+    if (NEED_P) sp[L] = in ? __ldg(p + ix) : 0.0;
+  }
+  const MacroGeo& g = mgeo[mac];
+  double nh[3] = {0, 0, 0}, cK = 1.0;
+  if (BLEND) {
+    nh[0] = g.nhat[0];
+    nh[1] = g.nhat[1];
+    nh[2] = g.nhat[2];
+    cK = g.cK;
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  const double wdet = EWQ * sgeo[6 * kTypeGeo];
+
+  auto anchor = [&](int x, int y, int z, double (&xa)[3]) {
+    const double fa = (i0 + x) * inv_n1, fb = (j0 + y) * inv_n1, fc = (k0 + z) * inv_n1;  // exact: n1 = 2^L
+#pragma unroll
+    for (int r = 0; r < 3; ++r) xa[r] = g.X0[r] + g.Jm[3 * r] * fa + g.Jm[3 * r + 1] * fb + g.Jm[3 * r + 2] * fc;
+  };
+
+  if (delta <= 4) {
+    // ---------------- sparse brick (<= 64 tets, mixed types per warp): one tet per thread, REDs
+    if (tid >= eNItems[delta]) return;
+    const int item = eItems[delta][tid];
+    const int cube = item & 63, t = item >> 6;
+    const int x = cube & 3, y = (cube >> 2) & 3, z = cube >> 4;
+    double xa[3];
+    anchor(x, y, z, xa);
+    const int cb2 = x + 2 * kPY * y + 2 * kPZ * z, cb1 = x + 5 * y + 25 * z;
+    double et[4], pp[4] = {0, 0, 0, 0}, acc[10][3], gy[4];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      et[v] = se[cb1 + eOffP[t][v]];
+      if (NEED_P) pp[v] = sp[cb1 + eOffP[t][v]];
+    }
+    tet_body<BLEND, MODE, FULL>(sgeo + t * kTypeGeo, wdet, xa, nh, cK, gamma, FootU{su + cb2, eOffU[t]}, et, pp,
+                                acc, gy);
+    if (HAS_U_OUT) {
+#pragma unroll
+      for (int a = 0; a < 10; ++a) {
+        const int o = eOffU[t][a];  // decode the footprint point of node a
+        const int Z = o / kPZ, Y = (o % kPZ) / kPY, xw = o % kPY;
+        const int X = xw >= 5 ? 2 * (xw - 5) + 1 : 2 * xw;
+        double* dst = yu + mb2 + rowstart32(n2, 2 * (j0 + y) + Y, 2 * (k0 + z) + Z) + 2 * (i0 + x) + X;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) atomicAdd(dst + c * cstride, acc[a][c]);
+      }
+    }
+    if (DO_DIV) {
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int o = eOffP[t][v];
+        const int X = o % 5, Y = (o / 5) % 5, Z = o / 25;
+        atomicAdd(yp + mb1 + rowstart32(n1, j0 + y + Y, k0 + z + Z) + i0 + x + X, gy[v]);
+      }
+    }
+    return;
+  }
+
+  // ---------------- dense brick: thread = cube, all lanes of a warp on the same tet type
+  const int x = tid & 3, y = (tid >> 2) & 3, z = tid >> 4;
+  const int s = i0 + j0 + k0 + x + y + z;
+  const int ntypes = (s <= n1 - 3) ? 6 : ((s == n1 - 2) ? 5 : ((s == n1 - 1) ? 1 : 0));
+  double xa[3];
+  anchor(x, y, z, xa);
+  const int cb2 = x + 2 * kPY * y + 2 * kPZ * z, cb1 = x + 5 * y + 25 * z;
+  double* yw = sy + warp * 3 * kFY + (x + 2 * kPY * y + 2 * kPZ * (z - 2 * warp));
+  double* ypw = syp + warp * kF1Y + (x + 5 * y + 25 * (z - 2 * warp));
+#pragma unroll 1
+  for (int t = 0; t < 6; ++t) {
+    const bool act = t < ntypes;
+    double acc[10][3], gy[4];
+    if (act) {
+      double et[4], pp[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        et[v] = se[cb1 + eOffP[t][v]];
+        if (NEED_P) pp[v] = sp[cb1 + eOffP[t][v]];
+      }
+      tet_body<BLEND, MODE, FULL>(sgeo + t * kTypeGeo, wdet, xa, nh, cK, gamma, FootU{su + cb2, eOffU[t]}, et, pp,
+                                  acc, gy);
+    }
+    const int* off = eOffU[t];
+    if (HAS_U_OUT) {
+      if (act) {  // round E: the 6 edge midpoints (pairwise different parity classes)
+        double old[6][3];
+#pragma unroll
+        for (int e = 0; e < 6; ++e)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) old[e][c] = yw[c * kFY + off[4 + e]];
+#pragma unroll
+        for (int e = 0; e < 6; ++e)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) yw[c * kFY + off[4 + e]] = old[e][c] + acc[4 + e][c];
+      }
+      __syncwarp();
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {  // rounds V0..V3: one vertex at a time (+ its P1 corner)
+      if (act) {
+        if (HAS_U_OUT) {
+#pragma unroll
+          for (int c = 0; c < 3; ++c) yw[c * kFY + off[a]] += acc[a][c];
+        }
+        if (DO_DIV) ypw[eOffP[t][a]] += gy[a];
+      }
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+
+  // ---- write the brick's output footprint
+  if (HAS_U_OUT) {
+#pragma unroll 1
+    for (int L = tid; L < 729; L += kBT) {
+      const int X = L % 9, Y = (L / 9) % 9, Z = L / 81;
+      const int gx = 2 * i0 + X, gy = 2 * j0 + Y, gz = 2 * k0 + Z;
+      if (gx + gy + gz > n2) continue;
+      const int wxy = xs(X) + kPY * Y;
+      double* dst = yu + mb2 + rowstart32(n2, gy, gz) + gx;
+      const bool border = X == 0 || Y == 0 || Z == 0 || X == 8 || Y == 8 || Z == 8;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        double v;
+        if (Z < 4) v = sy[c * kFY + wxy + kPZ * Z];
+        else if (Z > 4) v = sy[3 * kFY + c * kFY + wxy + kPZ * (Z - 4)];
+        else v = sy[c * kFY + wxy + kPZ * 4] + sy[3 * kFY + c * kFY + wxy];
+        if (!border) dst[c * cstride] = v;
+        else if (v != 0.0) atomicAdd(dst + c * cstride, v);
+      }
+    }
+  }
+  if (DO_DIV) {
+    for (int L = tid; L < kF1; L += kBT) {
+      const int X = L % 5, Y = (L / 5) % 5, Z = L / 25;
+      const int gx = i0 + X, gy = j0 + Y, gz = k0 + Z;
+      if (gx + gy + gz > n1) continue;
+      double v;
+      if (Z < 2) v = syp[X + 5 * Y + 25 * Z];
+      else if (Z > 2) v = syp[kF1Y + X + 5 * Y + 25 * (Z - 2)];
+      else v = syp[X + 5 * Y + 50] + syp[kF1Y + X + 5 * Y];
+      double* dst = yp + mb1 + rowstart32(n1, gy, gz) + gx;
+      const bool border = X == 0 || Y == 0 || Z == 0 || X == 4 || Y == 4 || Z == 4;
+      if (!border) *dst = v;
+      else if (v != 0.0) atomicAdd(dst, v);
+    }
+  }
+}
+
 static bool g_slots_ready = false;
 static int ensure_slots() {
   if (g_slots_ready) return HHG_OK;
@@ -643,6 +895,22 @@ static int ensure_slots() {
         items[delta][nitems[delta]++] = cube | (t << 6);
       }
     }
+  int offU[6][10], offP[6][4];
+  for (int t = 0; t < 6; ++t) {
+    int seen = 0;
+    for (int a = 0; a < 10; ++a) {
+      const int sl = slot[t][a];  // doubled offset (sl%3, (sl/3)%3, sl/9)
+      offU[t][a] = fword(sl % 3, (sl / 3) % 3, sl / 9);
+      if (a >= 4) {  // k_elem_fp's round E relies on distinct edge parity classes
+        const int par = (sl % 3) % 2 | (((sl / 3) % 3) % 2) << 1 | ((sl / 9) % 2) << 2;
+        if ((seen >> par) & 1) return fail(HHG_EINVAL, "edge parity classes collide");
+        seen |= 1 << par;
+      }
+    }
+    for (int v = 0; v < 4; ++v) offP[t][v] = TV[t][v][0] + 5 * TV[t][v][1] + 25 * TV[t][v][2];
+  }
+  HHG_CUDA(cudaMemcpyToSymbol(eOffU, offU, sizeof(offU)));
+  HHG_CUDA(cudaMemcpyToSymbol(eOffP, offP, sizeof(offP)));
   HHG_CUDA(cudaMemcpyToSymbol(eSlot, slot, sizeof(slot)));
   HHG_CUDA(cudaMemcpyToSymbol(eLd, ld, sizeof(ld)));
   HHG_CUDA(cudaMemcpyToSymbol(ePSlot, pslot, sizeof(pslot)));
@@ -658,8 +926,28 @@ template <bool BLEND, int MODE, bool FULL>
 static void elem_launch(const Mesh* m, const Level& L, const double* eta, double gamma, const double* u,
                         const double* p, double* yu, double* yp, cudaStream_t s) {
   const int64_t nm = macro_count(m);
+#ifndef HHG_ELEM_V5
+  {
+    constexpr size_t smem = fp_smem_words<MODE>() * sizeof(double);
+    dim3 grid((unsigned)L.n_bricks, (unsigned)nm);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_elem_fp<BLEND, MODE, FULL>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                           (int)cudaSharedmemCarveoutMaxShared);
+      cudaFuncSetAttribute(k_elem_fp<BLEND, MODE, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+    k_elem_fp<BLEND, MODE, FULL><<<grid, kBT, smem, s>>>(m->dgeo, L.geo, L.bricks, L.n1, 1.0 / L.n1, L.npts1,
+                                                         L.npts2, nm * L.npts2, eta, u, p, yu, yp, gamma);
+    return;
+  }
+#endif
   constexpr int NS = ((MODE & (ELEM_A | ELEM_BT | ELEM_DIAG)) ? kNS2 : 0) + ((MODE & ELEM_DIV) ? kNS1 : 0);
+#ifdef HHG_GEO_GLOBAL
+  constexpr size_t smem = (NS * kBT) * sizeof(double) + 13 * kBT * sizeof(int);
+#else
   constexpr size_t smem = (NS * kBT + kGeoSm) * sizeof(double) + 13 * kBT * sizeof(int);
+#endif
   dim3 grid((unsigned)L.n_bricks, (unsigned)nm);
   static bool attr = false;
   if (!attr) {

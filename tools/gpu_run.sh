@@ -7,7 +7,7 @@ done
 HHG_CLOCKS_RAW=gpurun_out/clocks_raw.csv timeout 600 python bench.py --no-cpu-baseline > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
 if [ "$1" = "ncu" ]; then
   python tools/one_apply.py --level 5 > gpurun_out/plain.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:k_elem_brick -s 1 -c 1 -o gpurun_out/prof_elem python tools/one_apply.py --level 5 > gpurun_out/ncu.log 2>&1
+  ncu --set full --clock-control none --import-source on -k regex:k_elem_ -s 1 -c 1 -o gpurun_out/prof_elem python tools/one_apply.py --level 5 > gpurun_out/ncu.log 2>&1
 fi
 if [ "$1" = "ll" ]; then
   python tools/one_vcycle.py --level 5 > gpurun_out/plain.log 2>&1 && \
