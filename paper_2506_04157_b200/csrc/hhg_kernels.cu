@@ -19,6 +19,59 @@ constexpr double QA = 0.58541019662496845446;  // (5 + 3 sqrt 5)/20
 constexpr double QB = 0.13819660112501051518;  // (5 - sqrt 5)/20
 
 // ------------------------------------------------------------------ interface sum + BC
+// Sum of the copies of group gi (copies gathered in chunks of 4 independent loads: macro vertices
+// have up to ~20 copies and a sequential dependent walk made coarse levels latency-bound).
+template <int NC>
+__device__ __forceinline__ void group_sum(int64_t b, int64_t e, const int64_t* __restrict__ copy, int64_t cstride,
+                                          const double* __restrict__ v, double (&val)[NC]) {
+  constexpr int CH = 4;
+#pragma unroll
+  for (int c = 0; c < NC; ++c) val[c] = 0.0;
+  for (int64_t k0 = b; k0 < e; k0 += CH) {
+    int64_t idx[CH];
+#pragma unroll
+    for (int j = 0; j < CH; ++j) idx[j] = (k0 + j < e) ? copy[k0 + j] : -1;
+    double x[CH][NC];
+#pragma unroll
+    for (int j = 0; j < CH; ++j)
+#pragma unroll
+      for (int c = 0; c < NC; ++c) x[j][c] = idx[j] >= 0 ? v[c * cstride + idx[j]] : 0.0;
+#pragma unroll
+    for (int j = 0; j < CH; ++j)
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+        if (idx[j] >= 0) val[c] += x[j][c];
+  }
+}
+template <int NC>
+__device__ __forceinline__ void group_store(int64_t b, int64_t e, const int64_t* __restrict__ copy, int64_t cstride,
+                                            const double (&val)[NC], double* __restrict__ v) {
+  constexpr int CH = 4;
+  for (int64_t k0 = b; k0 < e; k0 += CH) {
+    int64_t idx[CH];
+#pragma unroll
+    for (int j = 0; j < CH; ++j) idx[j] = (k0 + j < e) ? copy[k0 + j] : -1;
+#pragma unroll
+    for (int j = 0; j < CH; ++j)
+      if (idx[j] >= 0)
+#pragma unroll
+        for (int c = 0; c < NC; ++c) v[c * cstride + idx[j]] = val[c];
+  }
+}
+template <int NC>
+__device__ __forceinline__ void group_bc(int kd, const double* __restrict__ nrm, double (&val)[NC]) {
+  if (kd == HHG_BC_DIRICHLET0) {
+#pragma unroll
+    for (int c = 0; c < NC; ++c) val[c] = 0.0;
+  } else if (kd == HHG_BC_FREESLIP && NC == 3) {
+    const double n0 = nrm[0], n1 = nrm[1], n2 = nrm[2];
+    const double un = val[0] * n0 + val[1 % NC] * n1 + val[2 % NC] * n2;
+    val[0] -= un * n0;
+    val[1 % NC] -= un * n1;
+    val[2 % NC] -= un * n2;
+  }
+}
+
 template <int NC, bool BC>
 __global__ void k_fixup(int64_t ng, const int64_t* __restrict__ ptr, const int64_t* __restrict__ copy,
                         const uint8_t* __restrict__ kind, const double* __restrict__ normal, int64_t cstride,
@@ -27,30 +80,16 @@ __global__ void k_fixup(int64_t ng, const int64_t* __restrict__ ptr, const int64
   if (gi >= ng) return;
   const int64_t b = ptr[gi], e = ptr[gi + 1];
   double val[NC];
+  if (sum) {
+    group_sum<NC>(b, e, copy, cstride, v, val);
+  } else {
+    const int64_t i0 = copy[b];
 #pragma unroll
-  for (int c = 0; c < NC; ++c) {
-    double s = v[c * cstride + copy[b]];
-    if (sum)
-      for (int64_t k = b + 1; k < e; ++k) s += v[c * cstride + copy[k]];
-    val[c] = s;
+    for (int c = 0; c < NC; ++c) val[c] = v[c * cstride + i0];
   }
-  if (BC) {
-    const int kd = kind[gi];
-    if (kd == HHG_BC_DIRICHLET0) {
-#pragma unroll
-      for (int c = 0; c < NC; ++c) val[c] = 0.0;
-    } else if (kd == HHG_BC_FREESLIP && NC == 3) {
-      const double n0 = normal[3 * gi], n1 = normal[3 * gi + 1], n2 = normal[3 * gi + 2];
-      const double un = val[0] * n0 + val[1] * n1 + val[2 % NC] * n2;
-      val[0] -= un * n0;
-      val[1 % NC] -= un * n1;
-      val[2 % NC] -= un * n2;
-    }
-  }
+  if (BC) group_bc<NC>(kind[gi], normal + 3 * gi, val);
   if (!sum && !BC) return;
-  for (int64_t k = b; k < e; ++k)
-#pragma unroll
-    for (int c = 0; c < NC; ++c) v[c * cstride + copy[k]] = val[c];
+  group_store<NC>(b, e, copy, cstride, val, v);
 }
 
 // local partial sums of the groups shared with other ranks -> send buffer [slot][NC]
@@ -79,29 +118,12 @@ __global__ void k_fixup_remote(int64_t ng, const int64_t* __restrict__ ptr, cons
   if (gi >= ng) return;
   const int64_t b = ptr[gi], e = ptr[gi + 1];
   double val[NC];
+  group_sum<NC>(b, e, copy, cstride, v, val);
+  for (int64_t k = gs_ptr[gi]; k < gs_ptr[gi + 1]; ++k)
 #pragma unroll
-  for (int c = 0; c < NC; ++c) {
-    double s = 0.0;
-    for (int64_t k = b; k < e; ++k) s += v[c * cstride + copy[k]];
-    for (int64_t k = gs_ptr[gi]; k < gs_ptr[gi + 1]; ++k) s += rbuf[gs_idx[k] * NC + c];
-    val[c] = s;
-  }
-  if (BC) {
-    const int kd = kind[gi];
-    if (kd == HHG_BC_DIRICHLET0) {
-#pragma unroll
-      for (int c = 0; c < NC; ++c) val[c] = 0.0;
-    } else if (kd == HHG_BC_FREESLIP && NC == 3) {
-      const double n0 = normal[3 * gi], n1 = normal[3 * gi + 1], n2 = normal[3 * gi + 2];
-      const double un = val[0] * n0 + val[1 % NC] * n1 + val[2 % NC] * n2;
-      val[0] -= un * n0;
-      val[1 % NC] -= un * n1;
-      val[2 % NC] -= un * n2;
-    }
-  }
-  for (int64_t k = b; k < e; ++k)
-#pragma unroll
-    for (int c = 0; c < NC; ++c) v[c * cstride + copy[k]] = val[c];
+    for (int c = 0; c < NC; ++c) val[c] += rbuf[gs_idx[k] * NC + c];
+  if (BC) group_bc<NC>(kind[gi], normal + 3 * gi, val);
+  group_store<NC>(b, e, copy, cstride, val, v);
 }
 
 static const Groups& groups_of(const Level& L, int space) { return space == HHG_P1 ? L.g1 : L.g2; }
@@ -255,12 +277,12 @@ __device__ __forceinline__ bool row_of(const int32_t* rows, int64_t nrows, int N
 //    parity class (8 classes: coarse vertex or one of the 7 lattice edge directions), clipped to
 //    the macro's lattice.  No atomics; each output written once.
 constexpr int kPMax = 10, kRMax = 128;
-__constant__ int cPn[64];
-__constant__ int cPd[64][kPMax];      // dx + 3 dy + 9 dz
-__constant__ double cPw[64][kPMax];
-__device__ int cRn[8];
-__device__ int cRd[8][kRMax];         // (dx+8) | (dy+8) << 5 | (dz+8) << 10
-__device__ double cRw[8][kRMax];
+__device__ int gPn[64];
+__device__ int gPd[64][kPMax];        // dx + 3 dy + 9 dz
+__device__ double gPw[64][kPMax];
+__device__ int gRn[8];
+__device__ int gRd[8][kRMax];         // (dx+8) | (dy+8) << 5 | (dz+8) << 10
+__device__ double gRw[8][kRMax];
 
 static bool g_tabs_ready = false;
 static int ensure_transfer_tabs() {
@@ -341,12 +363,12 @@ static int ensure_transfer_tabs() {
           }
         }
   }
-  HHG_CUDA(cudaMemcpyToSymbol(cPn, pn, sizeof(pn)));
-  HHG_CUDA(cudaMemcpyToSymbol(cPd, pd, sizeof(pd)));
-  HHG_CUDA(cudaMemcpyToSymbol(cPw, pw, sizeof(pw)));
-  HHG_CUDA(cudaMemcpyToSymbol(cRn, rn, sizeof(rn)));
-  HHG_CUDA(cudaMemcpyToSymbol(cRd, rd, sizeof(rd)));
-  HHG_CUDA(cudaMemcpyToSymbol(cRw, rw, sizeof(rw)));
+  HHG_CUDA(cudaMemcpyToSymbol(gPn, pn, sizeof(pn)));
+  HHG_CUDA(cudaMemcpyToSymbol(gPd, pd, sizeof(pd)));
+  HHG_CUDA(cudaMemcpyToSymbol(gPw, pw, sizeof(pw)));
+  HHG_CUDA(cudaMemcpyToSymbol(gRn, rn, sizeof(rn)));
+  HHG_CUDA(cudaMemcpyToSymbol(gRd, rd, sizeof(rd)));
+  HHG_CUDA(cudaMemcpyToSymbol(gRw, rw, sizeof(rw)));
   g_tabs_ready = true;
   return HHG_OK;
 }
@@ -356,28 +378,35 @@ __device__ __forceinline__ int rowstart_i32(int N, int j, int k) {
   return ((N + 1) * (N + 2) * (N + 3) - (M + 1) * (M + 2) * (M + 3)) / 6 + (j * (2 * M + 3 - j)) / 2;
 }
 
-// x_f += P x_c on every stored fine node (per macro; consistent copies stay consistent)
+// x_f += P x_c on every stored fine node (per macro; consistent copies stay consistent).
+// Warp per fine row (J,K): the 9 coarse rows a stencil can touch are the same for the whole row,
+// so their starts are computed once per warp (shared memory); tables read through L1.
 __global__ void k_prolong(const int32_t* __restrict__ rowsf, int64_t nrowsf, int Nf, int64_t nptsf, int64_t nptsc,
                           int64_t cstridef, int64_t cstridec, const double* __restrict__ xc, double* __restrict__ xf) {
+  __shared__ int srs[8][9];
   RowCtx rc;
   if (!row_of(rowsf, nrowsf, Nf, rc)) return;
   const int mac = blockIdx.y;
   const int Nc = Nf / 2;
-  const int J = rc.j, K = rc.k;
+  const int J = rc.j, K = rc.k, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int by = 2 * (J >> 2), bz = 2 * (K >> 2);
+  if (lane < 9) srs[w][lane] = rowstart_i32(Nc, by + lane % 3, bz + lane / 3);
+  __syncwarp();
   double* fr = xf + (int64_t)mac * nptsf + rowstart_i32(Nf, J, K);
   const double* cm = xc + (int64_t)mac * nptsc;
-  for (int I = threadIdx.x & 31; I < rc.len; I += 32) {
-    const int cls = (I & 3) + 4 * (J & 3) + 16 * (K & 3);
-    const int bx = 2 * (I >> 2), by = 2 * (J >> 2), bz = 2 * (K >> 2);
-    const int n = cPn[cls];
+  const int cls0 = 4 * (J & 3) + 16 * (K & 3);
+  for (int I = lane; I < rc.len; I += 32) {
+    const int cls = (I & 3) + cls0;
+    const int bx = 2 * (I >> 2);
+    const int n = __ldg(gPn + cls);
     double s0 = 0.0, s1 = 0.0, s2 = 0.0;
     for (int e = 0; e < n; ++e) {
-      const int d = cPd[cls][e];
-      const int ci = rowstart_i32(Nc, by + (d / 3) % 3, bz + d / 9) + bx + d % 3;
-      const double w = cPw[cls][e];
-      s0 += w * __ldg(cm + ci);
-      s1 += w * __ldg(cm + cstridec + ci);
-      s2 += w * __ldg(cm + 2 * cstridec + ci);
+      const int d = __ldg(&gPd[cls][e]);
+      const int ci = srs[w][d / 3] + bx + d % 3;
+      const double wt = __ldg(&gPw[cls][e]);
+      s0 += wt * __ldg(cm + ci);
+      s1 += wt * __ldg(cm + cstridec + ci);
+      s2 += wt * __ldg(cm + 2 * cstridec + ci);
     }
     fr[I] += s0;
     fr[cstridef + I] += s1;
@@ -385,31 +414,45 @@ __global__ void k_prolong(const int32_t* __restrict__ rowsf, int64_t nrowsf, int
   }
 }
 
-// r_c = P^T r_f over owned fine copies (per macro), written (not accumulated) on every coarse node
+// r_c = P^T r_f over owned fine copies (per macro), written (not accumulated) on every coarse node.
+// Warp per coarse row (J,K): starts of the 17x17 fine rows (2J-8..2J+8, 2K-8..2K+8) the stencils
+// can touch are computed once per warp.
 __global__ void k_restrict(const int32_t* __restrict__ rowsc, int64_t nrowsc, int Nc, int64_t nptsf, int64_t nptsc,
                            int64_t cstridef, int64_t cstridec, const uint8_t* __restrict__ ownf,
                            const double* __restrict__ rf, double* __restrict__ rc_out) {
+  __shared__ int srs[8][289];
   RowCtx rc;
   if (!row_of(rowsc, nrowsc, Nc, rc)) return;
   const int mac = blockIdx.y;
   const int Nf = 2 * Nc;
-  const int J = rc.j, K = rc.k;
+  const int J = rc.j, K = rc.k, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int r = lane; r < 289; r += 32) {
+    const int fy = 2 * J + r % 17 - 8, fz = 2 * K + r / 17 - 8;
+    srs[w][r] = (fy >= 0 && fz >= 0 && fy + fz <= Nf) ? rowstart_i32(Nf, fy, fz) : -1;
+  }
+  __syncwarp();
   const int64_t fb = (int64_t)mac * nptsf;
+  const uint8_t* om = ownf + fb;
+  const double* rm = rf + fb;
   double* cr = rc_out + (int64_t)mac * nptsc + rowstart_i32(Nc, J, K);
-  for (int I = threadIdx.x & 31; I < rc.len; I += 32) {
-    const int pc = (I & 1) | ((J & 1) << 1) | ((K & 1) << 2);
-    const int n = cRn[pc];
+  const int pc0 = ((J & 1) << 1) | ((K & 1) << 2);
+  for (int I = lane; I < rc.len; I += 32) {
+    const int pc = (I & 1) | pc0;
+    const int n = __ldg(gRn + pc);
+    const int lim = Nf - 2 * J - 2 * K;  // fx + (fy - 2J) + (fz - 2K) <= lim
     double s0 = 0.0, s1 = 0.0, s2 = 0.0;
     for (int e = 0; e < n; ++e) {
-      const int d = cRd[pc][e];
-      const int fx = 2 * I + (d & 31) - 8, fy = 2 * J + ((d >> 5) & 31) - 8, fz = 2 * K + (d >> 10) - 8;
-      if (fx < 0 || fy < 0 || fz < 0 || fx + fy + fz > Nf) continue;
-      const int64_t fi = fb + rowstart_i32(Nf, fy, fz) + fx;
-      if (!ownf[fi]) continue;
-      const double w = cRw[pc][e];
-      s0 += w * __ldg(rf + fi);
-      s1 += w * __ldg(rf + cstridef + fi);
-      s2 += w * __ldg(rf + 2 * cstridef + fi);
+      const int d = __ldg(&gRd[pc][e]);
+      const int dx = (d & 31) - 8, dy = ((d >> 5) & 31) - 8, dz = (d >> 10) - 8;
+      const int fx = 2 * I + dx;
+      const int rs = srs[w][(dy + 8) + 17 * (dz + 8)];
+      if (fx < 0 || rs < 0 || fx + dy + dz > lim) continue;
+      const int fi = rs + fx;
+      if (!om[fi]) continue;
+      const double wt = __ldg(&gRw[pc][e]);
+      s0 += wt * __ldg(rm + fi);
+      s1 += wt * __ldg(rm + cstridef + fi);
+      s2 += wt * __ldg(rm + 2 * cstridef + fi);
     }
     cr[I] = s0;
     cr[cstridec + I] = s1;
