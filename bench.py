@@ -321,7 +321,7 @@ def main():
 # against ncu smsp__sass_thread_inst_executed_op_d{fma,add,mul}_pred_on)
 FLOPS_PER_TET = 1098.0      # 352 DFMA + 228 DADD + 166 DMUL per tet, element kernel v5 (ncu, profiles/r01_ncu_elem_v5_L5_summary.txt)
 FP64_PEAK_MEASURED = 34.16  # tools/fp64_peak on this pool's B200 (profiles/r01_fp64_peak.json); DMMA 37.1 (r01_fp64_dfma_vs_dmma.json)
-TRAFFIC_PER_LAUNCH = None
+TRAFFIC_PER_LAUNCH = 762.25e6  # bytes: dram__bytes_read.sum + dram__bytes_write.sum of one L5 launch (ncu --set full, profiles/r01_ncu_elem_v6_L5_summary.txt)
 
 if __name__ == "__main__":
     main()
