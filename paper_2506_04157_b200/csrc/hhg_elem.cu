@@ -680,7 +680,7 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
 
   // ---- stage: u footprint (cp.async), eta / p footprints, geometry; zero the output footprints
   const double* Gm = lgeo + (int64_t)mac * kLevelGeo;
-  for (int r = tid; r < kGeoSm; r += kBT) sgeo[r] = __ldg(Gm + r);
+  for (int r = tid; r < kGeoSm; r += kBT) cp_async8(sgeo + r, Gm + r);
   if (NEED_U) {
 #pragma unroll 1
     for (int L = tid; L < 729; L += kBT) {
@@ -697,13 +697,14 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
     for (int r = tid; r < 6 * kFY; r += kBT) sy[r] = 0.0;
   if (DO_DIV)
     for (int r = tid; r < 2 * kF1Y; r += kBT) syp[r] = 0.0;
-  for (int L = tid; L < kF1; L += kBT) {
+  for (int L = tid; L < kF1; L += kBT) {  // P1 footprint (points outside the lattice are never read)
     const int X = L % 5, Y = (L / 5) % 5, Z = L / 25;
     const int gx = i0 + X, gy = j0 + Y, gz = k0 + Z;
-    const bool in = gx + gy + gz <= n1;
-    const int64_t ix = mb1 + (in ? rowstart32(n1, gy, gz) + gx : 0);
-    se[L] = (eta != nullptr && in) ? __ldg(eta + ix) : 1.0;
-    if (NEED_P) sp[L] = in ? __ldg(p + ix) : 0.0;
+    if (gx + gy + gz > n1) continue;
+    const int64_t ix = mb1 + rowstart32(n1, gy, gz) + gx;
+    if (eta != nullptr) cp_async8(se + L, eta + ix);
+    else se[L] = 1.0;
+    if (NEED_P) cp_async8(sp + L, p + ix);
   }
   const MacroGeo& g = mgeo[mac];
   double nh[3] = {0, 0, 0}, cK = 1.0;
