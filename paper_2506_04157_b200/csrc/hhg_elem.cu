@@ -629,12 +629,15 @@ constexpr int kF1 = 125, kF1Y = 75;        // P1 footprints: brick 5x5x5, per wa
 __host__ __device__ constexpr int xs(int X) { return (X & 1) ? 5 + (X >> 1) : (X >> 1); }
 __host__ __device__ constexpr int fword(int X, int Y, int Z) { return xs(X) + kPY * Y + kPZ * Z; }
 __constant__ int eOffU[6][10];  // footprint word offset of each local node from its cube's base word
+__constant__ int eOffB[6][10];  // the same in bytes (LDS/STS [reg + uniform] addressing)
 __constant__ int eOffP[6][4];   // P1 footprint offset of each vertex from the cube's P1 base
 
 struct FootU {
-  const double* b;  // su + cube base word
-  const int* off;   // eOffU[t]
-  __device__ __forceinline__ double operator()(int a, int c) const { return b[c * kFU + off[a]]; }
+  const char* b;    // su + cube base word, as a byte address
+  const int* off;   // eOffB[t] (bytes)
+  __device__ __forceinline__ double operator()(int a, int c) const {
+    return *reinterpret_cast<const double*>(b + off[a] + c * (kFU * 8));
+  }
 };
 
 template <int MODE>
@@ -739,7 +742,7 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
       et[v] = se[cb1 + eOffP[t][v]];
       if (NEED_P) pp[v] = sp[cb1 + eOffP[t][v]];
     }
-    tet_body<BLEND, MODE, FULL>(sgeo + t * kTypeGeo, wdet, xa, nh, cK, gamma, FootU{su + cb2, eOffU[t]}, et, pp,
+    tet_body<BLEND, MODE, FULL>(sgeo + t * kTypeGeo, wdet, xa, nh, cK, gamma, FootU{reinterpret_cast<const char*>(su + cb2), eOffB[t]}, et, pp,
                                 acc, gy);
     if (HAS_U_OUT) {
 #pragma unroll
@@ -783,30 +786,35 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
         et[v] = se[cb1 + eOffP[t][v]];
         if (NEED_P) pp[v] = sp[cb1 + eOffP[t][v]];
       }
-      tet_body<BLEND, MODE, FULL>(sgeo + t * kTypeGeo, wdet, xa, nh, cK, gamma, FootU{su + cb2, eOffU[t]}, et, pp,
+      tet_body<BLEND, MODE, FULL>(sgeo + t * kTypeGeo, wdet, xa, nh, cK, gamma, FootU{reinterpret_cast<const char*>(su + cb2), eOffB[t]}, et, pp,
                                   acc, gy);
     }
-    const int* off = eOffU[t];
-    if (HAS_U_OUT) {
-      if (act) {  // round E: the 6 edge midpoints (pairwise different parity classes)
-        double old[6][3];
+    const int* off = eOffB[t];
+    char* ywb = reinterpret_cast<char*>(yw);
+    auto Y = [&](int a, int c) -> double& { return *reinterpret_cast<double*>(ywb + off[a] + c * (kFY * 8)); };
+    // round 0: the 6 edge midpoints (pairwise different parity classes, none even-even-even) and
+    // vertex 0 (parity 000) -- 7 nodes of pairwise different parity; rounds 1..3: one vertex each
+    if (act) {
+      if (HAS_U_OUT) {
+        double old[7][3];
 #pragma unroll
-        for (int e = 0; e < 6; ++e)
+        for (int e = 0; e < 7; ++e)
 #pragma unroll
-          for (int c = 0; c < 3; ++c) old[e][c] = yw[c * kFY + off[4 + e]];
+          for (int c = 0; c < 3; ++c) old[e][c] = Y(e < 6 ? 4 + e : 0, c);
 #pragma unroll
-        for (int e = 0; e < 6; ++e)
+        for (int e = 0; e < 7; ++e)
 #pragma unroll
-          for (int c = 0; c < 3; ++c) yw[c * kFY + off[4 + e]] = old[e][c] + acc[4 + e][c];
+          for (int c = 0; c < 3; ++c) Y(e < 6 ? 4 + e : 0, c) = old[e][c] + acc[e < 6 ? 4 + e : 0][c];
       }
-      __syncwarp();
+      if (DO_DIV) ypw[eOffP[t][0]] += gy[0];
     }
+    __syncwarp();
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {  // rounds V0..V3: one vertex at a time (+ its P1 corner)
+    for (int a = 1; a < 4; ++a) {
       if (act) {
         if (HAS_U_OUT) {
 #pragma unroll
-          for (int c = 0; c < 3; ++c) yw[c * kFY + off[a]] += acc[a][c];
+          for (int c = 0; c < 3; ++c) Y(a, c) += acc[a][c];
         }
         if (DO_DIV) ypw[eOffP[t][a]] += gy[a];
       }
@@ -911,6 +919,10 @@ static int ensure_slots() {
     for (int v = 0; v < 4; ++v) offP[t][v] = TV[t][v][0] + 5 * TV[t][v][1] + 25 * TV[t][v][2];
   }
   HHG_CUDA(cudaMemcpyToSymbol(eOffU, offU, sizeof(offU)));
+  int offB[6][10];
+  for (int t = 0; t < 6; ++t)
+    for (int a = 0; a < 10; ++a) offB[t][a] = 8 * offU[t][a];
+  HHG_CUDA(cudaMemcpyToSymbol(eOffB, offB, sizeof(offB)));
   HHG_CUDA(cudaMemcpyToSymbol(eOffP, offP, sizeof(offP)));
   HHG_CUDA(cudaMemcpyToSymbol(eSlot, slot, sizeof(slot)));
   HHG_CUDA(cudaMemcpyToSymbol(eLd, ld, sizeof(ld)));
