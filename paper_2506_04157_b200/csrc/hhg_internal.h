@@ -92,6 +92,7 @@ struct Level {
   int32_t* rows2 = nullptr;         // packed rows for P2
   int64_t nrows1 = 0, nrows2 = 0;
   Groups g1, g2;                    // P1 interface groups, P2 interface+BC groups
+  int32_t* bcn2 = nullptr;          // per stored P2 node: -1 none, -2 Dirichlet, g >= 0 free-slip group
   uint8_t* own1 = nullptr;          // owner mask per stored P1 node
   uint8_t* own2 = nullptr;          // owner mask per stored P2 node
   int64_t* canon1 = nullptr;        // canonical node index per stored node (lazy)
@@ -167,6 +168,23 @@ int launch_chebk_last(int64_t n, const double* t, const double* dinv, double c1,
                       const double* d, double* x, cudaStream_t s);  // x += d + c1 d + c2 dinv (r - t)
 int launch_pcg_update(int64_t n, const double* scal, double* x, double* r, const double* p, const double* q,
                       const double* dinv, double* z, cudaStream_t s);
+// node-major vector kernels with the BC projection (P_v M) of the updated direction fused in
+// (replaces a BC-only fixup pass); `L` supplies the per-node BC map and free-slip normals
+int launch_cheb0_bc(const Mesh* m, const Level& L, const double* f, const double* t, const double* dinv,
+                    double inv_theta, double* r, double* d, cudaStream_t s);
+int launch_chebk_bc(const Mesh* m, const Level& L, const double* t, const double* dinv, double c1, double c2, double* x,
+                    double* r, double* d, cudaStream_t s);
+int launch_chebk_last_bc(const Mesh* m, const Level& L, const double* t, const double* dinv, double c1, double c2,
+                         const double* r, const double* d, double* x, cudaStream_t s);
+int launch_cheb_deg1_bc(const Mesh* m, const Level& L, const double* f, const double* t, const double* dinv,
+                        double inv_theta, double* x, cudaStream_t s);
+// PCG with ping-pong r.z scalars: scal[0]/scal[2] alternate by iteration parity, scal[1] = p.q
+int launch_pcg_update_bc(const Mesh* m, const Level& L, int it, const double* scal, double* x, double* r,
+                         const double* p, const double* q, const double* dinv, double* z, cudaStream_t s);
+int launch_pcg_dir_zero(int64_t n, int it, const double* scal, const double* z, double* p, double* q_zero,
+                        cudaStream_t s);
+int launch_dot_fused(const Mesh* m, const Level& L, int space, const double* x, const double* y, double* out,
+                     cudaStream_t s);
 int launch_scalar_ops(int op, double* scal, cudaStream_t s);
 
 }  // namespace hhg

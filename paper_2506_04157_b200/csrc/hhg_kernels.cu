@@ -237,6 +237,64 @@ __global__ void k_dot_final(const double* __restrict__ part, int n, double* __re
   }
 }
 
+// one-launch dot: block partials + last-block (fixed-order) finalisation; counter lives in the
+// level's reduction scratch (reset by the last block, so graph replays stay valid)
+__global__ void k_dot_fused(int64_t nstored, int nc, int64_t cstride, const uint8_t* __restrict__ own,
+                            const double* __restrict__ x, const double* __restrict__ y, double* __restrict__ part,
+                            unsigned* __restrict__ counter, double* __restrict__ out) {
+  double s = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nstored; i += (int64_t)gridDim.x * blockDim.x) {
+    if (!own[i]) continue;
+    for (int c = 0; c < nc; ++c) s += x[c * cstride + i] * y[c * cstride + i];
+  }
+  __shared__ double sh[32];
+  __shared__ bool last;
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) {
+      part[blockIdx.x] = v;
+      __threadfence();
+      last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    }
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double t = 0.0;
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) t += ((volatile double*)part)[i];
+  t = warp_sum(t);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = t;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) {
+      *out = v;
+      *counter = 0u;
+    }
+  }
+}
+
+int launch_dot_fused(const Mesh* m, const Level& L, int space, const double* x, const double* y, double* out,
+                     cudaStream_t s) {
+  const int64_t nm = macro_count(m);
+  const bool p1 = space == HHG_P1;
+  const int64_t nst = nm * (p1 ? L.npts1 : L.npts2);
+  const int nc = space == HHG_P2VEC ? 3 : 1;
+  int64_t nb = (nst + 255) / 256;
+  nb = nb < 1 ? 1 : (nb > kRedBlocks ? kRedBlocks : nb);
+  k_dot_fused<<<(unsigned)nb, 256, 0, s>>>(nst, nc, nst, p1 ? L.own1 : L.own2, x, y, L.red,
+                                          reinterpret_cast<unsigned*>(L.red + kRedBlocks + 4), out);
+  count_launch();
+  HHG_CUDA(cudaGetLastError());
+  if (m->comm && m->nranks > 1) HHG_TRY(comm_allreduce_sum(m->comm, out, 1, s));
+  return HHG_OK;
+}
+
 int launch_dot(const Mesh* m, const Level& L, int space, const double* x, const double* y, double* out,
                cudaStream_t s) {
   const int64_t nm = macro_count(m);
@@ -619,6 +677,180 @@ int launch_chebk_last(int64_t n, const double* t, const double* dinv, double c1,
 int launch_chebk(int64_t n, const double* t, const double* dinv, double c1, double c2, double* x, double* r,
                  double* d, cudaStream_t s) {
   k_chebk<<<vgrid(n), 256, 0, s>>>(n, t, dinv, c1, c2, x, r, d);
+  count_launch();
+  HHG_CUDA(cudaGetLastError());
+  return HHG_OK;
+}
+
+// ---- node-major variants: i over stored P2 nodes, the 3 components at i, i+cs, i+2cs; the BC
+// projection P_v M of the new direction is applied per node (Dirichlet: 0; free slip: remove the
+// normal component with the node group's normal) -- identical to a BC-only interface pass on a
+// consistent vector.
+__device__ __forceinline__ void bc_project(int b, const double* __restrict__ nrm, double& v0, double& v1, double& v2) {
+  if (b == -1) return;
+  if (b == -2) {
+    v0 = v1 = v2 = 0.0;
+    return;
+  }
+  const double n0 = nrm[3 * b], n1 = nrm[3 * b + 1], n2 = nrm[3 * b + 2];
+  const double un = v0 * n0 + v1 * n1 + v2 * n2;
+  v0 -= un * n0;
+  v1 -= un * n1;
+  v2 -= un * n2;
+}
+__global__ void k_cheb0_bc(int64_t ns, int64_t cs, const double* __restrict__ f, const double* __restrict__ t,
+                           const double* __restrict__ dinv, double it, double* __restrict__ r, double* __restrict__ d,
+                           const int32_t* __restrict__ bcn, const double* __restrict__ nrm) {
+  GRID_STRIDE(i, ns) {
+    double dv[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const int64_t j = i + c * cs;
+      const double ri = t ? f[j] - t[j] : f[j];
+      r[j] = ri;
+      dv[c] = dinv[j] * ri * it;
+    }
+    bc_project(bcn[i], nrm, dv[0], dv[1], dv[2]);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) d[i + c * cs] = dv[c];
+  }
+}
+__global__ void k_cheb_deg1_bc(int64_t ns, int64_t cs, const double* __restrict__ f, const double* __restrict__ t,
+                               const double* __restrict__ dinv, double it, double* __restrict__ x,
+                               const int32_t* __restrict__ bcn, const double* __restrict__ nrm) {
+  GRID_STRIDE(i, ns) {
+    double dv[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const int64_t j = i + c * cs;
+      dv[c] = dinv[j] * (t ? f[j] - t[j] : f[j]) * it;
+    }
+    bc_project(bcn[i], nrm, dv[0], dv[1], dv[2]);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const int64_t j = i + c * cs;
+      x[j] = (t ? x[j] : 0.0) + dv[c];
+    }
+  }
+}
+__global__ void k_chebk_bc(int64_t ns, int64_t cs, const double* __restrict__ t, const double* __restrict__ dinv,
+                           double c1, double c2, double* __restrict__ x, double* __restrict__ r, double* __restrict__ d,
+                           const int32_t* __restrict__ bcn, const double* __restrict__ nrm) {
+  GRID_STRIDE(i, ns) {
+    double dv[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const int64_t j = i + c * cs;
+      const double di = d[j];
+      x[j] += di;
+      const double ri = r[j] - t[j];
+      r[j] = ri;
+      dv[c] = c1 * di + c2 * dinv[j] * ri;
+    }
+    bc_project(bcn[i], nrm, dv[0], dv[1], dv[2]);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) d[i + c * cs] = dv[c];
+  }
+}
+__global__ void k_chebk_last_bc(int64_t ns, int64_t cs, const double* __restrict__ t, const double* __restrict__ dinv,
+                                double c1, double c2, const double* __restrict__ r, const double* __restrict__ d,
+                                double* __restrict__ x, const int32_t* __restrict__ bcn,
+                                const double* __restrict__ nrm) {
+  GRID_STRIDE(i, ns) {
+    double dn[3], dold[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const int64_t j = i + c * cs;
+      dold[c] = d[j];
+      dn[c] = c1 * dold[c] + c2 * dinv[j] * (r[j] - t[j]);
+    }
+    bc_project(bcn[i], nrm, dn[0], dn[1], dn[2]);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) x[i + c * cs] += dold[c] + dn[c];
+  }
+}
+__global__ void k_pcg_update_bc(int64_t ns, int64_t cs, const double* __restrict__ rzp, const double* __restrict__ pqp,
+                                double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
+                                const double* __restrict__ q, const double* __restrict__ dinv, double* __restrict__ z,
+                                const int32_t* __restrict__ bcn, const double* __restrict__ nrm) {
+  const double rz = *rzp, pq = *pqp;
+  const double alpha = (rz > 1e-300 && pq != 0.0) ? rz / pq : 0.0;
+  GRID_STRIDE(i, ns) {
+    double zv[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const int64_t j = i + c * cs;
+      x[j] += alpha * p[j];
+      const double ri = r[j] - alpha * q[j];
+      r[j] = ri;
+      zv[c] = dinv[j] * ri;
+    }
+    bc_project(bcn[i], nrm, zv[0], zv[1], zv[2]);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) z[i + c * cs] = zv[c];
+  }
+}
+// p = z + beta p, beta = rz_new / rz_old (0 once converged to the zero-rhs guard); q = 0 for the
+// next operator application
+__global__ void k_pcg_dir_zero(int64_t n, const double* __restrict__ rzo, const double* __restrict__ rzn,
+                               const double* __restrict__ z, double* __restrict__ p, double* __restrict__ q) {
+  const double a = *rzo, b = *rzn;
+  const double beta = a > 1e-300 ? b / a : 0.0;
+  GRID_STRIDE(i, n) {
+    p[i] = z[i] + beta * p[i];
+    q[i] = 0.0;
+  }
+}
+
+static inline unsigned ngrid(int64_t ns) {
+  int64_t b = (ns + 255) / 256;
+  return (unsigned)(b < 148 * 8 ? (b < 1 ? 1 : b) : 148 * 8);
+}
+#define NODE_ARGS(m, L) (macro_count(m) * (L).npts2), (macro_count(m) * (L).npts2)
+int launch_cheb0_bc(const Mesh* m, const Level& L, const double* f, const double* t, const double* dinv,
+                    double inv_theta, double* r, double* d, cudaStream_t s) {
+  const int64_t ns = macro_count(m) * L.npts2;
+  k_cheb0_bc<<<ngrid(ns), 256, 0, s>>>(NODE_ARGS(m, L), f, t, dinv, inv_theta, r, d, L.bcn2, L.g2.normal);
+  count_launch();
+  HHG_CUDA(cudaGetLastError());
+  return HHG_OK;
+}
+int launch_cheb_deg1_bc(const Mesh* m, const Level& L, const double* f, const double* t, const double* dinv,
+                        double inv_theta, double* x, cudaStream_t s) {
+  const int64_t ns = macro_count(m) * L.npts2;
+  k_cheb_deg1_bc<<<ngrid(ns), 256, 0, s>>>(NODE_ARGS(m, L), f, t, dinv, inv_theta, x, L.bcn2, L.g2.normal);
+  count_launch();
+  HHG_CUDA(cudaGetLastError());
+  return HHG_OK;
+}
+int launch_chebk_bc(const Mesh* m, const Level& L, const double* t, const double* dinv, double c1, double c2, double* x,
+                    double* r, double* d, cudaStream_t s) {
+  const int64_t ns = macro_count(m) * L.npts2;
+  k_chebk_bc<<<ngrid(ns), 256, 0, s>>>(NODE_ARGS(m, L), t, dinv, c1, c2, x, r, d, L.bcn2, L.g2.normal);
+  count_launch();
+  HHG_CUDA(cudaGetLastError());
+  return HHG_OK;
+}
+int launch_chebk_last_bc(const Mesh* m, const Level& L, const double* t, const double* dinv, double c1, double c2,
+                         const double* r, const double* d, double* x, cudaStream_t s) {
+  const int64_t ns = macro_count(m) * L.npts2;
+  k_chebk_last_bc<<<ngrid(ns), 256, 0, s>>>(NODE_ARGS(m, L), t, dinv, c1, c2, r, d, x, L.bcn2, L.g2.normal);
+  count_launch();
+  HHG_CUDA(cudaGetLastError());
+  return HHG_OK;
+}
+int launch_pcg_update_bc(const Mesh* m, const Level& L, int it, const double* scal, double* x, double* r,
+                         const double* p, const double* q, const double* dinv, double* z, cudaStream_t s) {
+  const int64_t ns = macro_count(m) * L.npts2;
+  k_pcg_update_bc<<<ngrid(ns), 256, 0, s>>>(NODE_ARGS(m, L), scal + ((it & 1) ? 2 : 0), scal + 1, x, r, p, q, dinv,
+                                            z, L.bcn2, L.g2.normal);
+  count_launch();
+  HHG_CUDA(cudaGetLastError());
+  return HHG_OK;
+}
+int launch_pcg_dir_zero(int64_t n, int it, const double* scal, const double* z, double* p, double* q_zero,
+                        cudaStream_t s) {
+  k_pcg_dir_zero<<<vgrid(n), 256, 0, s>>>(n, scal + ((it & 1) ? 2 : 0), scal + ((it & 1) ? 0 : 2), z, p, q_zero);
   count_launch();
   HHG_CUDA(cudaGetLastError());
   return HHG_OK;

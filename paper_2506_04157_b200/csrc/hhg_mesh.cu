@@ -78,6 +78,7 @@ void free_level(Level& L) {
   }
   f(L.own1);
   f(L.own2);
+  f(L.bcn2);
   f(L.canon1);
   f(L.canon2);
   f(L.red);
@@ -287,11 +288,19 @@ int build_host_groups(const Mesh* m, int level, int space, std::vector<int64_t>&
 }
 
 static int build_groups(const Mesh* m, const Prims& P, int N, bool with_bc, Groups& G, std::vector<uint8_t>& own,
-                        int64_t npts) {
+                        int64_t npts, int32_t** bcn = nullptr) {
   std::vector<int64_t> ptr, copy, slot_group;
   std::vector<uint8_t> kind;
   std::vector<double> normal;
   host_groups(m, P, N, with_bc, npts, ptr, copy, kind, normal, own, G.halo, slot_group);
+  if (bcn) {  // per stored node BC map for the fused vector kernels
+    std::vector<int32_t> map((size_t)npts * m->local.size(), -1);
+    for (int64_t g = 0; g < (int64_t)kind.size(); ++g) {
+      if (kind[g] == HHG_BC_NONE) continue;
+      for (int64_t k = ptr[g]; k < ptr[g + 1]; ++k) map[copy[k]] = kind[g] == HHG_BC_DIRICHLET0 ? -2 : (int32_t)g;
+    }
+    HHG_TRY(upload(bcn, map));
+  }
   G.n = (int64_t)ptr.size() - 1;
   G.nbc = with_bc ? (int64_t)std::count_if(kind.begin(), kind.end(), [](uint8_t k) { return k != HHG_BC_NONE; }) : 0;
   G.ncopy = (int64_t)copy.size();
@@ -397,12 +406,13 @@ int ensure_level(Mesh* m, int level) {
   Prims P;
   build_prims(m, P);
   std::vector<uint8_t> own;
-  HHG_TRY(build_groups(m, P, L.n2, true, L.g2, own, L.npts2));
+  HHG_TRY(build_groups(m, P, L.n2, true, L.g2, own, L.npts2, &L.bcn2));
   HHG_TRY(upload(&L.own2, own));
   HHG_TRY(build_groups(m, P, L.n1, false, L.g1, own, L.npts1));
   HHG_TRY(upload(&L.own1, own));
   if (cudaMalloc(&L.red, (kRedBlocks + 8) * sizeof(double)) != cudaSuccess)
     return fail(HHG_ENOMEM, "cudaMalloc reduction scratch");
+  HHG_CUDA(cudaMemset(L.red, 0, (kRedBlocks + 8) * sizeof(double)));  // fused-dot counter starts at 0
   L.built = true;
   return HHG_OK;
 }

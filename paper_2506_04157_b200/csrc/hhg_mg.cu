@@ -106,7 +106,7 @@ struct hhg_mg {
   }
 };
 
-static int mg_apply(hhg_mg* mg, int l, const double* u, double* y, cudaStream_t s) {
+static int mg_apply(hhg_mg* mg, int l, const double* u, double* y, cudaStream_t s, bool y_zeroed = false) {
   const bool timed = mg->prof && l == mg->prm.l_max;
   if (timed) {
     if (mg->ev_used + 2 > mg->ev.size()) {
@@ -119,7 +119,7 @@ static int mg_apply(hhg_mg* mg, int l, const double* u, double* y, cudaStream_t 
   }
   // y = (M P_v) A u : zero, element kernel (timed alone when profiling), interface sum + BC
   const Level& L = mg->mesh->levels[l];
-  HHG_CUDA(cudaMemsetAsync(y, 0, p2vec_len(mg->mesh, l) * sizeof(double), s));
+  if (!y_zeroed) HHG_CUDA(cudaMemsetAsync(y, 0, p2vec_len(mg->mesh, l) * sizeof(double), s));
   if (timed) HHG_CUDA(cudaEventRecord(mg->ev[mg->ev_used], s));
   HHG_TRY(launch_elem(mg->mesh, L, ELEM_A, mg->prm.visc_form, mg->lv[l].eta, 0.0, u, nullptr, y, nullptr, s));
   if (timed) {
@@ -132,10 +132,10 @@ static int mg_apply(hhg_mg* mg, int l, const double* u, double* y, cudaStream_t 
 static int mg_cheb(hhg_mg* mg, int l, double* x, const double* f, bool x_is_zero, cudaStream_t s) {
   // Chebyshev sweep of degree k on D^-1 A over [b/10, b] (R12).  Vector updates fused:
   // the first step skips A x when x = 0, the last step folds "x += d" into the d-update and drops the
-  // dead r/d writes; the BC projection of that last d moves onto x (P_v M is linear, x consistent).
+  // dead r/d writes, and every direction update applies the BC projection P_v M per node (no
+  // separate BC pass).
   auto& L = mg->lv[l];
   const Mesh* m = mg->mesh;
-  const int64_t n = p2vec_len(m, l);
   const double b = mg->prm.cheb_hi_factor * L.lam, a = mg->prm.cheb_lo_ratio * b;
   const double theta = 0.5 * (b + a), delta = 0.5 * (b - a), sigma = theta / delta;
   double rho = 1.0 / sigma;
@@ -146,28 +146,22 @@ static int mg_cheb(hhg_mg* mg, int l, double* x, const double* f, bool x_is_zero
     t0 = L.t;
   }
   const int deg = mg->prm.degree;
-  if (deg == 1) {
-    HHG_TRY(launch_cheb_deg1(n, f, t0, L.dinv, 1.0 / theta, x, s));
-    return launch_fixup(m, LL, HHG_P2VEC, false, true, x, s);
-  }
-  HHG_TRY(launch_cheb0(n, f, t0, L.dinv, 1.0 / theta, L.r, L.d, s));
-  HHG_TRY(launch_fixup(m, LL, HHG_P2VEC, false, true, L.d, s));
+  if (deg == 1) return launch_cheb_deg1_bc(m, LL, f, t0, L.dinv, 1.0 / theta, x, s);
+  HHG_TRY(launch_cheb0_bc(m, LL, f, t0, L.dinv, 1.0 / theta, L.r, L.d, s));
   for (int k = 1; k < deg; ++k) {
     HHG_TRY(mg_apply(mg, l, L.d, L.t, s));
     const double rn = 1.0 / (2.0 * sigma - rho);
-    if (k < deg - 1) {
-      HHG_TRY(launch_chebk(n, L.t, L.dinv, rn * rho, 2.0 * rn / delta, x, L.r, L.d, s));
-      HHG_TRY(launch_fixup(m, LL, HHG_P2VEC, false, true, L.d, s));
-    } else {
-      HHG_TRY(launch_chebk_last(n, L.t, L.dinv, rn * rho, 2.0 * rn / delta, L.r, L.d, x, s));
-      HHG_TRY(launch_fixup(m, LL, HHG_P2VEC, false, true, x, s));
-    }
+    if (k < deg - 1) HHG_TRY(launch_chebk_bc(m, LL, L.t, L.dinv, rn * rho, 2.0 * rn / delta, x, L.r, L.d, s));
+    else HHG_TRY(launch_chebk_last_bc(m, LL, L.t, L.dinv, rn * rho, 2.0 * rn / delta, L.r, L.d, x, s));
     rho = rn;
   }
   return HHG_OK;
 }
 
 static int mg_pcg(hhg_mg* mg, int l, const double* f, double* x, cudaStream_t s) {
+  // Jacobi-PCG, exactly coarse_iters iterations from x = 0 (R15).  Scalars stay on the
+  // device (graph-capturable); r.z ping-pongs between scal[0] and scal[2]; p = z + beta p also
+  // zeroes q for the next operator application.
   auto& L = mg->lv[l];
   const Mesh* m = mg->mesh;
   const Level& LL = m->levels[l];
@@ -177,18 +171,16 @@ static int mg_pcg(hhg_mg* mg, int l, const double* f, double* x, cudaStream_t s)
   double* p = L.p;
   double* q = L.t;
   HHG_CUDA(cudaMemsetAsync(x, 0, n * sizeof(double), s));
-  HHG_CUDA(cudaMemcpyAsync(r, f, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  HHG_TRY(launch_cheb0(n, f, x, L.dinv, 1.0, r, z, s));  // r = f - 0, z = dinv r
-  HHG_TRY(launch_fixup(m, LL, HHG_P2VEC, false, true, z, s));
+  HHG_TRY(launch_cheb0_bc(m, LL, f, nullptr, L.dinv, 1.0, r, z, s));  // r = f, z = PM dinv r
   HHG_CUDA(cudaMemcpyAsync(p, z, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  HHG_TRY(launch_dot(m, LL, HHG_P2VEC, r, z, mg->scal + 0, s));
+  HHG_TRY(launch_dot_fused(m, LL, HHG_P2VEC, r, z, mg->scal + 0, s));
+  HHG_CUDA(cudaMemsetAsync(q, 0, n * sizeof(double), s));
   for (int it = 0; it < mg->prm.coarse_iters; ++it) {
-    HHG_TRY(mg_apply(mg, l, p, q, s));
-    HHG_TRY(launch_dot(m, LL, HHG_P2VEC, p, q, mg->scal + 1, s));
-    HHG_TRY(launch_pcg_update(n, mg->scal, x, r, p, q, L.dinv, z, s));
-    HHG_TRY(launch_fixup(m, LL, HHG_P2VEC, false, true, z, s));
-    HHG_TRY(launch_dot(m, LL, HHG_P2VEC, r, z, mg->scal + 2, s));
-    HHG_TRY(launch_pcg_dir(n, mg->scal, z, p, s));
+    HHG_TRY(mg_apply(mg, l, p, q, s, true));
+    HHG_TRY(launch_dot_fused(m, LL, HHG_P2VEC, p, q, mg->scal + 1, s));
+    HHG_TRY(launch_pcg_update_bc(m, LL, it, mg->scal, x, r, p, q, L.dinv, z, s));
+    HHG_TRY(launch_dot_fused(m, LL, HHG_P2VEC, r, z, mg->scal + ((it & 1) ? 0 : 2), s));
+    HHG_TRY(launch_pcg_dir_zero(n, it, mg->scal, z, p, q, s));
   }
   return HHG_OK;
 }
