@@ -453,18 +453,24 @@ __global__ void k_prolong(const int32_t* __restrict__ rowsf, int64_t nrowsf, int
   double* fr = xf + (int64_t)mac * nptsf + rowstart_i32(Nf, J, K);
   const double* cm = xc + (int64_t)mac * nptsc;
   const int cls0 = 4 * (J & 3) + 16 * (K & 3);
-  for (int I = lane; I < rc.len; I += 32) {
-    const int cls = (I & 3) + cls0;
+  // 4 passes over I mod 4 so that all lanes of a pass share one stencil class (no divergence)
+  for (int it = lane; it < 4 * ((rc.len + 3) / 4); it += 32) {
+    const int o = it / ((rc.len + 3) / 4), I = 4 * (it % ((rc.len + 3) / 4)) + o;
+    if (I >= rc.len) continue;
+    const int cls = o + cls0;
     const int bx = 2 * (I >> 2);
     const int n = __ldg(gPn + cls);
     double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-    for (int e = 0; e < n; ++e) {
-      const int d = __ldg(&gPd[cls][e]);
-      const int ci = srs[w][d / 3] + bx + d % 3;
-      const double wt = __ldg(&gPw[cls][e]);
-      s0 += wt * __ldg(cm + ci);
-      s1 += wt * __ldg(cm + cstridec + ci);
-      s2 += wt * __ldg(cm + 2 * cstridec + ci);
+#pragma unroll
+    for (int e = 0; e < kPMax; ++e) {  // fully unrolled, predicated: all gathers in flight at once
+      if (e < n) {
+        const int d = __ldg(&gPd[cls][e]);
+        const int ci = srs[w][d / 3] + bx + d % 3;
+        const double wt = __ldg(&gPw[cls][e]);
+        s0 += wt * __ldg(cm + ci);
+        s1 += wt * __ldg(cm + cstridec + ci);
+        s2 += wt * __ldg(cm + 2 * cstridec + ci);
+      }
     }
     fr[I] += s0;
     fr[cstridef + I] += s1;
@@ -494,20 +500,24 @@ __global__ void k_restrict(const int32_t* __restrict__ rowsc, int64_t nrowsc, in
   const double* rm = rf + fb;
   double* cr = rc_out + (int64_t)mac * nptsc + rowstart_i32(Nc, J, K);
   const int pc0 = ((J & 1) << 1) | ((K & 1) << 2);
-  for (int I = lane; I < rc.len; I += 32) {
-    const int pc = (I & 1) | pc0;
+  // 2 passes over I mod 2 so that all lanes of a pass share one stencil class (no divergence)
+  const int half = (rc.len + 1) / 2;
+  for (int it = lane; it < 2 * half; it += 32) {
+    const int ph = it / half, I = 2 * (it % half) + ph;
+    if (I >= rc.len) continue;
+    const int pc = ph | pc0;
     const int n = __ldg(gRn + pc);
     const int lim = Nf - 2 * J - 2 * K;  // fx + (fy - 2J) + (fz - 2K) <= lim
     double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-    for (int e = 0; e < n; ++e) {
+#pragma unroll 4
+    for (int e = 0; e < n; ++e) {  // branch-free body: out-of-lattice / non-owned entries get weight 0
       const int d = __ldg(&gRd[pc][e]);
       const int dx = (d & 31) - 8, dy = ((d >> 5) & 31) - 8, dz = (d >> 10) - 8;
       const int fx = 2 * I + dx;
       const int rs = srs[w][(dy + 8) + 17 * (dz + 8)];
-      if (fx < 0 || rs < 0 || fx + dy + dz > lim) continue;
-      const int fi = rs + fx;
-      if (!om[fi]) continue;
-      const double wt = __ldg(&gRw[pc][e]);
+      const bool in = fx >= 0 && rs >= 0 && fx + dy + dz <= lim;
+      const int fi = in ? rs + fx : 0;
+      const double wt = (in && om[fi]) ? __ldg(&gRw[pc][e]) : 0.0;
       s0 += wt * __ldg(rm + fi);
       s1 += wt * __ldg(rm + cstridef + fi);
       s2 += wt * __ldg(rm + 2 * cstridef + fi);

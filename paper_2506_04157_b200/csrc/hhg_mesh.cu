@@ -273,6 +273,38 @@ static void host_groups(const Mesh* m, const Prims& P, int N, bool with_bc, int6
     halo.off.push_back((int64_t)slot_group.size());
   }
   halo.nslots = (int64_t)slot_group.size();
+
+  // Memory locality of the interface-sum kernels: within the BC block [0, nbc) and the rest, order
+  // the groups by the flat index of their first copy (consecutive threads then walk each macro's
+  // boundary storage monotonically).  Slot -> group references are remapped.
+  const int64_t ng = (int64_t)ptr.size() - 1;
+  int64_t nbc = 0;
+  if (with_bc)
+    for (uint8_t k : kind) nbc += k != HHG_BC_NONE;
+  std::vector<int64_t> order(ng);
+  std::iota(order.begin(), order.end(), 0);
+  auto by_first = [&](int64_t a, int64_t b) { return copy[ptr[a]] < copy[ptr[b]]; };
+  std::stable_sort(order.begin(), order.begin() + nbc, by_first);
+  std::stable_sort(order.begin() + nbc, order.end(), by_first);
+  std::vector<int64_t> nptr(1, 0), ncopy, newid(ng);
+  std::vector<uint8_t> nkind;
+  std::vector<double> nnormal;
+  ncopy.reserve(copy.size());
+  for (int64_t gi = 0; gi < ng; ++gi) {
+    const int64_t g = order[gi];
+    newid[g] = gi;
+    for (int64_t k = ptr[g]; k < ptr[g + 1]; ++k) ncopy.push_back(copy[k]);
+    nptr.push_back((int64_t)ncopy.size());
+    if (with_bc) {
+      nkind.push_back(kind[g]);
+      for (int c = 0; c < 3; ++c) nnormal.push_back(normal[3 * g + c]);
+    }
+  }
+  ptr.swap(nptr);
+  copy.swap(ncopy);
+  kind.swap(nkind);
+  normal.swap(nnormal);
+  for (auto& g : slot_group) g = newid[g];
 }
 
 int build_host_groups(const Mesh* m, int level, int space, std::vector<int64_t>& ptr, std::vector<int64_t>& copy,
