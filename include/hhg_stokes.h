@@ -242,6 +242,12 @@ int hhg_mg_create(hhg_mesh* mesh, const hhg_mg_params* params, const double* con
 int hhg_mg_lambda(const hhg_mg* mg, int level, double* lambda_host);
 /* One V-cycle (fig:ASolverStructure) from x = 0: x = V(rhs). */
 int vcycle(hhg_mg* mg, const double* rhs, double* x, hhg_stream_t stream);
+/* hhg_ablock_cg (the A-block solver of the Uzawa preconditioners): CG preconditioned by one
+ * V-cycle (this hierarchy) per iteration, from x = 0, until |r|_2 <= tol |rhs|_2 (unique dofs) or
+ * max_iters.  rhs: consistent, BC-projected P2VEC on l_max; x overwritten.  Synchronises once per
+ * iteration (convergence check); iterations / final relative residual returned on the host. */
+int hhg_ablock_cg(hhg_mg* mg, const double* rhs, double* x, double tol, int max_iters, int* iters,
+                  double* rel_res, hhg_stream_t stream);
 /* Same with HOST (pinned or pageable) rhs / x: H2D copy, V-cycle, D2H copy on `stream`. */
 int vcycle_host(hhg_mg* mg, const double* rhs_host, double* x_host, hhg_stream_t stream);
 /* Kernel timing of the fine-level element kernel inside vcycle (CUDA events on the

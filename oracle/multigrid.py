@@ -166,3 +166,35 @@ class Hierarchy:
         for _ in range(self.post):
             x = chebyshev(self.Ac[l], self.dinv[l], self.Pm[l], f, x, self.degree, b)
         return x
+
+
+def ablock_cg(H: Hierarchy, f, tol=1e-2, max_iters=100):
+    """A-block solver: CG preconditioned by one V-cycle of H per iteration, from x = 0,
+    until |r|_2 <= tol |f|_2 or max_iters -> (x, iterations, relative residual)."""
+    A = H.Ac[H.lmax]
+    x = np.zeros_like(f)
+    r = f.copy()
+    r0 = float(np.linalg.norm(r))
+    if r0 == 0.0:
+        return x, 0, 0.0
+    z = H.vcycle(r)
+    p = z.copy()
+    rz = float(r @ z)
+    it, rel = 0, 1.0
+    while it < max_iters:
+        it += 1
+        q = A @ p
+        pq = float(p @ q)
+        alpha = rz / pq if pq != 0.0 else 0.0
+        x = x + alpha * p
+        r = r - alpha * q
+        rel = float(np.linalg.norm(r)) / r0
+        if rel <= tol:
+            break
+        z = H.vcycle(r)
+        rz_new = float(r @ z)
+        beta = rz_new / rz if rz != 0.0 else 0.0
+        p = z + beta * p
+        rz = rz_new
+    return x, it, rel
+

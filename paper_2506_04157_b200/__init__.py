@@ -40,6 +40,7 @@ EXPORTS = [
     "hhg_mg_profile_get", "hhg_mg_destroy", "hhg_launch_count",
     "hhg_mesh_create_part", "hhg_partition_rcb", "hhg_mesh_rank", "hhg_halo_info", "hhg_halo_keys",
     "hhg_owned_count", "hhg_halo_pack", "hhg_interface_sum_remote", "epsilon_apply_partial",
+    "hhg_ablock_cg",
 ]
 
 
@@ -77,6 +78,7 @@ def _load():
         "hhg_halo_info": ([P, I, I, P, P, P], I), "hhg_halo_keys": ([P, I, I, P], I),
         "hhg_owned_count": ([P, I, I, P], I), "hhg_halo_pack": ([P, I, I, P, P, P], I),
         "hhg_interface_sum_remote": ([P, I, I, P, P, P], I), "epsilon_apply_partial": ([P, I, I, P, P, P, P], I),
+        "hhg_ablock_cg": ([P, P, P, D, I, P, P, P], I),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -432,6 +434,15 @@ class MG:
         x = self.mesh.zeros(self.l_max, HHG_P2VEC) if x is None else x
         _chk(_lib.vcycle(self.handle, _dev(rhs, n, "rhs"), _dev(x, n, "x"), _stream(stream)))
         return x
+
+    def ablock_cg(self, rhs, x=None, tol=1e-2, max_iters=100, stream=None):
+        """A-block CG preconditioned by this V-cycle -> (x, iterations, relative residual)."""
+        n = self.mesh.vec_len(self.l_max, HHG_P2VEC)
+        x = self.mesh.zeros(self.l_max, HHG_P2VEC) if x is None else x
+        it, rel = ctypes.c_int(), ctypes.c_double()
+        _chk(_lib.hhg_ablock_cg(self.handle, _dev(rhs, n, "rhs"), _dev(x, n, "x"), float(tol), int(max_iters),
+                                ctypes.byref(it), ctypes.byref(rel), _stream(stream)))
+        return x, it.value, rel.value
 
     def vcycle_host(self, rhs_host, x_host, stream=None):
         _chk(_lib.vcycle_host(self.handle, _ptr(rhs_host), _ptr(x_host), _stream(stream)))

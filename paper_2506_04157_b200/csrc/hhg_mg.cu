@@ -88,6 +88,10 @@ struct hhg_mg {
   const double* g_rhs = nullptr;
   double* g_x = nullptr;
   cudaStream_t g_stream = nullptr;
+  // A-block CG (hhg_ablock_cg): fine-level work vectors + its own V-cycle graph (r -> z)
+  double *cg_r = nullptr, *cg_z = nullptr, *cg_p = nullptr, *cg_q = nullptr, *cg_s = nullptr;
+  cudaGraphExec_t cg_gexec = nullptr;
+  cudaStream_t cg_stream = nullptr;
   // profiling
   bool prof = false;
   std::vector<cudaEvent_t> ev;
@@ -102,6 +106,9 @@ struct hhg_mg {
     if (hbuf_rhs) cudaFree(hbuf_rhs);
     if (hbuf_x) cudaFree(hbuf_x);
     if (gexec) cudaGraphExecDestroy(gexec);
+    for (double* p : {cg_r, cg_z, cg_p, cg_q, cg_s})
+      if (p) cudaFree(p);
+    if (cg_gexec) cudaGraphExecDestroy(cg_gexec);
     for (auto e : ev) cudaEventDestroy(e);
   }
 };
@@ -310,6 +317,101 @@ int vcycle(hhg_mg* mg, const double* rhs, double* x, hhg_stream_t stream) {
   }
   HHG_CUDA(cudaGraphLaunch(mg->gexec, s));
   count_launch();
+  return HHG_OK;
+}
+
+// ---- A-block solver: CG preconditioned by one V-cycle per iteration, to a relative
+// residual tolerance tol_A.  x = 0 on entry; rhs consistent and BC-projected.
+__global__ void k_cg_step(int64_t n, const double* __restrict__ sc, double* __restrict__ x, double* __restrict__ r,
+                          const double* __restrict__ p, const double* __restrict__ q) {
+  const double alpha = sc[1] != 0.0 ? sc[0] / sc[1] : 0.0;  // sc[0] = r.z, sc[1] = p.q
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    x[i] += alpha * p[i];
+    r[i] -= alpha * q[i];
+  }
+}
+__global__ void k_cg_dir(int64_t n, double* __restrict__ sc, const double* __restrict__ z, double* __restrict__ p) {
+  const double beta = sc[0] != 0.0 ? sc[2] / sc[0] : 0.0;  // sc[2] = new r.z
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = z[i] + beta * p[i];
+}
+__global__ void k_cg_roll(double* sc) {
+  if (threadIdx.x == 0) sc[0] = sc[2];
+}
+
+static int cg_precond(hhg_mg* mg, cudaStream_t s) {  // z = V(r) with a cached graph
+  if (!mg->prm.use_graph || s == nullptr) return mg_cycle(mg, mg->prm.l_max, mg->cg_r, mg->cg_z, s);
+  if (!mg->cg_gexec || mg->cg_stream != s) {
+    if (mg->cg_gexec) cudaGraphExecDestroy(mg->cg_gexec);
+    mg->cg_gexec = nullptr;
+    cudaGraph_t g;
+    HHG_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    int r = mg_cycle(mg, mg->prm.l_max, mg->cg_r, mg->cg_z, s);
+    cudaError_t ce = cudaStreamEndCapture(s, &g);
+    if (r != HHG_OK) return r;
+    if (ce != cudaSuccess) return fail(HHG_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+    HHG_CUDA(cudaGraphInstantiate(&mg->cg_gexec, g, 0));
+    cudaGraphDestroy(g);
+    mg->cg_stream = s;
+  }
+  HHG_CUDA(cudaGraphLaunch(mg->cg_gexec, s));
+  count_launch();
+  return HHG_OK;
+}
+
+int hhg_ablock_cg(hhg_mg* mg, const double* rhs, double* x, double tol, int max_iters, int* iters_out,
+                  double* rel_res_out, hhg_stream_t stream) {
+  if (!mg || !rhs || !x) return fail(HHG_EINVAL, "hhg_ablock_cg: NULL argument");
+  if (!(tol > 0) || max_iters < 1) return fail(HHG_EINVAL, "hhg_ablock_cg: need tol > 0, max_iters >= 1");
+  for (int l = mg->prm.l_min + 1; l <= mg->prm.l_max; ++l)
+    if (!(mg->lv[l].lam > 0)) return fail(HHG_ENOTREADY, "hhg_ablock_cg: no spectrum estimate");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int l = mg->prm.l_max;
+  const Mesh* m = mg->mesh;
+  const Level& LL = m->levels[l];
+  const int64_t n = p2vec_len(m, l);
+  if (!mg->cg_r) {
+    for (double** p : {&mg->cg_r, &mg->cg_z, &mg->cg_p, &mg->cg_q})
+      if (cudaMalloc(p, n * sizeof(double)) != cudaSuccess) return fail(HHG_ENOMEM, "hhg_ablock_cg workspace");
+    if (cudaMalloc(&mg->cg_s, 8 * sizeof(double)) != cudaSuccess) return fail(HHG_ENOMEM, "hhg_ablock_cg scalars");
+  }
+  double* sc = mg->cg_s;  // [0] r.z  [1] p.q  [2] r.z new  [3] r.r  [4] r0.r0
+  HHG_CUDA(cudaMemsetAsync(x, 0, n * sizeof(double), s));
+  HHG_CUDA(cudaMemcpyAsync(mg->cg_r, rhs, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  HHG_TRY(launch_dot(m, LL, HHG_P2VEC, mg->cg_r, mg->cg_r, sc + 4, s));
+  double r00 = 0.0;
+  HHG_CUDA(cudaMemcpyAsync(&r00, sc + 4, sizeof(double), cudaMemcpyDeviceToHost, s));
+  HHG_CUDA(cudaStreamSynchronize(s));
+  const double r0 = std::sqrt(r00);
+  int it = 0;
+  double rel = r0 > 0 ? 1.0 : 0.0;
+  if (r0 > 0) {
+    HHG_TRY(cg_precond(mg, s));
+    HHG_CUDA(cudaMemcpyAsync(mg->cg_p, mg->cg_z, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    HHG_TRY(launch_dot(m, LL, HHG_P2VEC, mg->cg_r, mg->cg_z, sc + 0, s));
+    const unsigned nb = vg(n);
+    while (it < max_iters) {
+      ++it;
+      HHG_TRY(mg_apply(mg, l, mg->cg_p, mg->cg_q, s));
+      HHG_TRY(launch_dot(m, LL, HHG_P2VEC, mg->cg_p, mg->cg_q, sc + 1, s));
+      k_cg_step<<<nb, 256, 0, s>>>(n, sc, x, mg->cg_r, mg->cg_p, mg->cg_q);
+      count_launch();
+      HHG_TRY(launch_dot(m, LL, HHG_P2VEC, mg->cg_r, mg->cg_r, sc + 3, s));
+      double rr = 0.0;
+      HHG_CUDA(cudaMemcpyAsync(&rr, sc + 3, sizeof(double), cudaMemcpyDeviceToHost, s));
+      HHG_CUDA(cudaStreamSynchronize(s));
+      rel = std::sqrt(std::max(rr, 0.0)) / r0;
+      if (rel <= tol) break;
+      HHG_TRY(cg_precond(mg, s));
+      HHG_TRY(launch_dot(m, LL, HHG_P2VEC, mg->cg_r, mg->cg_z, sc + 2, s));
+      k_cg_dir<<<nb, 256, 0, s>>>(n, sc, mg->cg_z, mg->cg_p);
+      k_cg_roll<<<1, 32, 0, s>>>(sc);
+      count_launch(2);
+    }
+  }
+  HHG_CUDA(cudaGetLastError());
+  if (iters_out) *iters_out = it;
+  if (rel_res_out) *rel_res_out = rel;
   return HHG_OK;
 }
 

@@ -250,3 +250,37 @@ def test_edge_cases():
         hhg.p2_restrict(M, 0, z)
     with pytest.raises(hhg.HHGError):
         hhg.epsilon_apply(M, 1, None, z[:-1])
+
+
+@pytest.fixture(scope="module")
+def ablock_case():
+    from oracle.multigrid import Hierarchy
+    mac = icoshell(3, 2)
+    levels = (1, 2, 3)
+    discs, v0 = {}, {}
+    for L in levels:
+        lm, d, _ = oracle_case(mac, L, True, BC_SHELL, C2, 0.0, build=("A",))
+        discs[L], v0[L] = d, uniform_vec(lm.p2_keys, 6)
+    H = Hierarchy(discs, v0, pre=3, post=3, degree=3, power_iters=20, coarse_iters=50)
+    f_o = discs[3].project(uniform_vec(discs[3].lm.p2_keys, 4))
+    M = lib_mesh(mac, 3, True, BC_SHELL)
+    etas = {L: lib_eta(M, L, C2) for L in levels}
+    pv = {L: M.from_canonical(L, hhg.HHG_P2VEC, uniform_vec(M.canonical_keys(L, hhg.HHG_P2), 6)) for L in (2, 3)}
+    mg = hhg.MG(M, 1, 3, etas, pv, pre=3, post=3, degree=3, power_iters=20, coarse_iters=50)
+    return H, f_o, M, mg, etas
+
+
+@pytest.mark.parametrize("tol", [1e-2, 1e-6])
+def test_ablock_cg_vcycle_preconditioned(ablock_case, tol):
+    """A-block solver: V-cycle-preconditioned CG on the blended shell, levels 3 -> 1,
+    config-2 viscosity: same iteration count as the oracle, solution within 1e-9 relative."""
+    from oracle.multigrid import ablock_cg
+    H, f_o, M, mg, etas = ablock_case
+    x_o, it_o, rel_o = ablock_cg(H, f_o, tol=tol, max_iters=200)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        x, it, rel = mg.ablock_cg(lib_u(M, 3, 4), tol=tol, max_iters=200, stream=s)
+    s.synchronize()
+    assert it == it_o and rel <= tol
+    assert abs(rel - rel_o) <= 1e-6 * rel_o
+    assert rel_l2(canon(M, 3, hhg.HHG_P2VEC, x), x_o) <= TOL_VCYCLE

@@ -111,3 +111,24 @@ def test_vcycle_invariants(shell_hierarchy):
     import scipy.sparse.linalg as sla
     lmax = sla.eigsh(sp.diags(s) @ Af @ sp.diags(s), k=1, which="LA")[0][0]
     assert 0.85 * lmax < H.lam[2] < 1.1 * lmax
+
+
+def test_ablock_cg_converges_to_the_direct_solution(shell_hierarchy):
+    """CG preconditioned by the V-cycle reaches A^-1 f on the free dofs (direct sparse solve),
+    stops at the requested relative residual, and a looser tolerance needs fewer iterations."""
+    import scipy.sparse.linalg as sla
+    from oracle.multigrid import ablock_cg
+    discs, H = shell_hierarchy
+    d = discs[2]
+    f = d.project(uniform_vec(d.lm.p2_keys, 4))
+    A = H.Ac[2]
+    # Ac = (P_v M) A (P_v M) is singular on the constrained directions (Dirichlet dofs, CMB normals);
+    # adding I - P_v M there makes it invertible without touching the projected solution
+    Areg = (A + sp.identity(A.shape[0], format="csr") - d.Pm).tocsc()
+    x_direct = sla.spsolve(Areg, f)
+    x, it, rel = ablock_cg(H, f, tol=1e-12, max_iters=200)
+    assert rel <= 1e-12 and np.linalg.norm(f - A @ x) <= 1.01e-12 * np.linalg.norm(f)
+    assert np.linalg.norm(x - x_direct) <= 1e-9 * np.linalg.norm(x_direct)
+    x2, it2, rel2 = ablock_cg(H, f, tol=1e-2, max_iters=200)
+    assert rel2 <= 1e-2 and it2 < it
+    assert ablock_cg(H, 0 * f)[1] == 0
