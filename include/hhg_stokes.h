@@ -190,6 +190,13 @@ int divT_apply(const hhg_mesh* mesh, int level, const double* p, double* y_u, in
 int stokes_apply(const hhg_mesh* mesh, int level, const double* eta_p1, double gamma, const double* u,
                  const double* p, double* y_u, double* y_p, hhg_stream_t stream);
 int hhg_diag(const hhg_mesh* mesh, int level, const double* eta_p1, double* diag, hhg_stream_t stream);
+/* hhg_mass_apply: y = M_{1/eta} p, the P1 pressure mass matrix weighted by 1/eta (the Schur
+ * complement approximation S_M of eq:schurMass): M_vw = int (1/eta) psi_v psi_w with
+ * eta P1-interpolated at the quadrature points, blended geometry.  hhg_mass_diag: its diagonal.
+ * Both consistent (interface-summed) P1 vectors; eta_p1 NULL = 1 (plain pressure mass). */
+int hhg_mass_apply(const hhg_mesh* mesh, int level, const double* eta_p1, const double* p, double* y,
+                   hhg_stream_t stream);
+int hhg_mass_diag(const hhg_mesh* mesh, int level, const double* eta_p1, double* diag, hhg_stream_t stream);
 /* epsilon_apply_partial: the element half of epsilon_apply only -- per-copy partial sums of
  * A(eta) u, NO interface sum and NO BC (first phase of a split-phase exchange). */
 int epsilon_apply_partial(const hhg_mesh* mesh, int level, int form, const double* eta_p1, const double* u,

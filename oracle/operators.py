@@ -105,6 +105,14 @@ def element_C(W, xq, gamma):
     return -np.einsum("tq,qp,tqj->tpj", W, lam, vals)
 
 
+def element_M(W, eta_q):
+    """(T,4,4): pressure mass weighted by 1/eta, M_K[p,r] = sum_q W/eta_q lam_p lam_r
+    (Schur complement approximation M_{1/eta}, eq:schurMass)."""
+    xi, _ = fe.q4_rule()
+    lam = fe.p1_basis(xi)                                   # (Q,4)
+    return np.einsum("tq,qp,qr->tpr", W / eta_q, lam, lam)
+
+
 def p2vec_dofs(tet_p2: np.ndarray) -> np.ndarray:
     return (3 * tet_p2[:, :, None] + np.arange(3)[None, None, :]).reshape(tet_p2.shape[0], 30)
 
@@ -142,9 +150,15 @@ class Discretisation:
                 Ce = element_C(W, xq, gamma) if gamma != 0.0 else np.zeros((len(tets), 4, 30))
                 M = _coo(Ce, pd, vd, n1, 3 * n2)
                 mats["C"] = M if mats["C"] is None else mats["C"] + M
+            if "M" in build:
+                xi, _ = fe.q4_rule()
+                eta_q = eta_p1[pd] @ fe.p1_basis(xi).T
+                M = _coo(element_M(W, eta_q), pd, pd, n1, n1)
+                mats["M"] = M if mats["M"] is None else mats["M"] + M
         self.A = mats.get("A")
         self.B = mats.get("B")
         self.C = mats.get("C")
+        self.M = mats.get("M")
         # constraints
         self.bc = node_bc(lm.p2_keys, lm.macro_tets, lm.macro_vtag, bc_by_tag or {})
         self.Pm = constraint_matrix(lm.p2_xt, self.bc)

@@ -40,7 +40,7 @@ EXPORTS = [
     "hhg_mg_profile_get", "hhg_mg_destroy", "hhg_launch_count",
     "hhg_mesh_create_part", "hhg_partition_rcb", "hhg_mesh_rank", "hhg_halo_info", "hhg_halo_keys",
     "hhg_owned_count", "hhg_halo_pack", "hhg_interface_sum_remote", "epsilon_apply_partial",
-    "hhg_ablock_cg",
+    "hhg_ablock_cg", "hhg_mass_apply", "hhg_mass_diag",
 ]
 
 
@@ -79,6 +79,7 @@ def _load():
         "hhg_owned_count": ([P, I, I, P], I), "hhg_halo_pack": ([P, I, I, P, P, P], I),
         "hhg_interface_sum_remote": ([P, I, I, P, P, P], I), "epsilon_apply_partial": ([P, I, I, P, P, P, P], I),
         "hhg_ablock_cg": ([P, P, P, D, I, P, P, P], I),
+        "hhg_mass_apply": ([P, I, P, P, P, P], I), "hhg_mass_diag": ([P, I, P, P, P], I),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -323,6 +324,22 @@ def epsilon_apply_partial(mesh, level, eta, u, y=None, form=HHG_VISC_FULL, strea
     _chk(_lib.epsilon_apply_partial(mesh.handle, level, form, _dev(eta, mesh.vec_len(level, HHG_P1), "eta"),
                                     _dev(u, n, "u"), _dev(y, n, "y"), _stream(stream)))
     return y
+
+
+def hhg_mass_apply(mesh, level, eta, p, y=None, stream=None):
+    """y = M_{1/eta} p (eq:schurMass), consistent P1."""
+    n1 = mesh.vec_len(level, HHG_P1)
+    y = mesh.zeros(level, HHG_P1) if y is None else y
+    _chk(_lib.hhg_mass_apply(mesh.handle, level, _dev(eta, n1, "eta"), _dev(p, n1, "p"), _dev(y, n1, "y"),
+                             _stream(stream)))
+    return y
+
+
+def hhg_mass_diag(mesh, level, eta, out=None, stream=None):
+    n1 = mesh.vec_len(level, HHG_P1)
+    out = mesh.zeros(level, HHG_P1) if out is None else out
+    _chk(_lib.hhg_mass_diag(mesh.handle, level, _dev(eta, n1, "eta"), _dev(out, n1), _stream(stream)))
+    return out
 
 
 def div_apply(mesh, level, gamma, u, q=None, stream=None):

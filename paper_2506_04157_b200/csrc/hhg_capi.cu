@@ -302,7 +302,7 @@ int apply_op(const Mesh* m, int level, int mode, int form, const double* eta, do
   const Level& L = m->levels[level];
   const int64_t nm = macro_count(m);
   const bool has_u = (mode & (ELEM_A | ELEM_BT | ELEM_DIAG)) != 0;
-  const bool has_p = (mode & ELEM_DIV) != 0;
+  const bool has_p = elem_p_out(mode);
   if (has_u && !accumulate_u) HHG_CUDA(cudaMemsetAsync(yu, 0, 3 * nm * L.npts2 * sizeof(double), s));
   if (has_p) HHG_CUDA(cudaMemsetAsync(yp, 0, nm * L.npts1 * sizeof(double), s));
   if (has_u && accumulate_u) {
@@ -327,6 +327,25 @@ int epsilon_apply(const hhg_mesh* mesh, int level, int form, const double* eta_p
   auto* m = const_cast<hhg_mesh*>(mesh);
   HHG_TRY(ensure_level(m, level));
   return apply_op(m, level, ELEM_A, form, eta_p1, 0.0, u, nullptr, y, nullptr, false, (cudaStream_t)stream);
+}
+
+int hhg_mass_apply(const hhg_mesh* mesh, int level, const double* eta_p1, const double* p, double* y,
+                   hhg_stream_t stream) {
+  HHG_TRY(check_level(mesh, level));
+  CHECK_PTR(p);
+  CHECK_PTR(y);
+  auto* m = const_cast<hhg_mesh*>(mesh);
+  HHG_TRY(ensure_level(m, level));
+  return apply_op(m, level, ELEM_MASS, HHG_VISC_FULL, eta_p1, 0.0, nullptr, p, nullptr, y, false, (cudaStream_t)stream);
+}
+
+int hhg_mass_diag(const hhg_mesh* mesh, int level, const double* eta_p1, double* diag, hhg_stream_t stream) {
+  HHG_TRY(check_level(mesh, level));
+  CHECK_PTR(diag);
+  auto* m = const_cast<hhg_mesh*>(mesh);
+  HHG_TRY(ensure_level(m, level));
+  return apply_op(m, level, ELEM_MASSD, HHG_VISC_FULL, eta_p1, 0.0, nullptr, nullptr, nullptr, diag, false,
+                  (cudaStream_t)stream);
 }
 
 int div_apply(const hhg_mesh* mesh, int level, double gamma, const double* u, double* q, hhg_stream_t stream) {

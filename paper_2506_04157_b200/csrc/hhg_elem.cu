@@ -184,6 +184,27 @@ __device__ __forceinline__ void tet_body(const double* G, double wdet, const dou
     }
   }
 
+  if (MODE & (ELEM_MASS | ELEM_MASSD)) {
+    // pressure mass weighted by 1/eta (Schur approximation M_{1/eta}, eq:schurMass P:457-461):
+    // M_vw = sum_q w |det J_F| |det J_B| / eta_q  lambda_v(q) lambda_w(q),  |det J_B| = (c alpha)^3
+    double gs = 0.0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double cq = cK * al[q];
+      const double Wq = wdet * cq * cq * cq / fma(EQAB, et[q], etaS);
+      if (MODE & ELEM_MASS) {
+        gq[q] = Wq * fma(EQAB, pp[q], pS);
+        gs += gq[q];
+      } else {
+        gq[q] = Wq;
+        gs += Wq;
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < 4; ++v)
+      gy[v] = (MODE & ELEM_MASS) ? fma(EQB, gs, EQAB * gq[v]) : fma(EQB * EQB, gs, (EQA * EQA - EQB * EQB) * gq[v]);
+    return;
+  }
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const double* K = Kq[q];
@@ -643,7 +664,7 @@ struct FootU {
 template <int MODE>
 __host__ __device__ constexpr int fp_smem_words() {
   return ((MODE & (ELEM_A | ELEM_DIV)) ? 3 * kFU : 0) + ((MODE & (ELEM_A | ELEM_BT | ELEM_DIAG)) ? 2 * 3 * kFY : 0) +
-         kF1 + ((MODE & ELEM_BT) ? kF1 : 0) + ((MODE & ELEM_DIV) ? 2 * kF1Y : 0) + kGeoSm;
+         kF1 + ((MODE & (ELEM_BT | ELEM_MASS)) ? kF1 : 0) + (elem_p_out(MODE) ? 2 * kF1Y : 0) + kGeoSm;
 }
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
@@ -663,7 +684,8 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
               double* __restrict__ yp, double gamma) {
   constexpr bool DO_DIV = (MODE & ELEM_DIV) != 0;
   constexpr bool NEED_U = (MODE & (ELEM_A | ELEM_DIV)) != 0;
-  constexpr bool NEED_P = (MODE & ELEM_BT) != 0;
+  constexpr bool NEED_P = (MODE & (ELEM_BT | ELEM_MASS)) != 0;
+  constexpr bool HAS_P_OUT = elem_p_out(MODE);
   constexpr bool HAS_U_OUT = (MODE & (ELEM_A | ELEM_BT | ELEM_DIAG)) != 0;
   extern __shared__ double sm[];
   double* su = sm;                                   // [3][kFU]
@@ -671,7 +693,7 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
   double* se = sy + (HAS_U_OUT ? 6 * kFY : 0);       // [kF1]
   double* sp = se + kF1;                             // [kF1]
   double* syp = sp + (NEED_P ? kF1 : 0);             // [2 warps][kF1Y]
-  double* sgeo = syp + (DO_DIV ? 2 * kF1Y : 0);      // [kGeoSm]
+  double* sgeo = syp + (HAS_P_OUT ? 2 * kF1Y : 0);   // [kGeoSm]
 
   const int mac = blockIdx.y;
   const int32_t bpk = __ldg(bricks + blockIdx.x);
@@ -698,7 +720,7 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
   }
   if (HAS_U_OUT)
     for (int r = tid; r < 6 * kFY; r += kBT) sy[r] = 0.0;
-  if (DO_DIV)
+  if (HAS_P_OUT)
     for (int r = tid; r < 2 * kF1Y; r += kBT) syp[r] = 0.0;
   for (int L = tid; L < kF1; L += kBT) {  // P1 footprint (points outside the lattice are never read)
     const int X = L % 5, Y = (L / 5) % 5, Z = L / 25;
@@ -755,7 +777,7 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
         for (int c = 0; c < 3; ++c) atomicAdd(dst + c * cstride, acc[a][c]);
       }
     }
-    if (DO_DIV) {
+    if (HAS_P_OUT) {
 #pragma unroll
       for (int v = 0; v < 4; ++v) {
         const int o = eOffP[t][v];
@@ -806,7 +828,7 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
 #pragma unroll
           for (int c = 0; c < 3; ++c) Y(e < 6 ? 4 + e : 0, c) = old[e][c] + acc[e < 6 ? 4 + e : 0][c];
       }
-      if (DO_DIV) ypw[eOffP[t][0]] += gy[0];
+      if (HAS_P_OUT) ypw[eOffP[t][0]] += gy[0];
     }
     __syncwarp();
 #pragma unroll
@@ -816,7 +838,7 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
 #pragma unroll
           for (int c = 0; c < 3; ++c) Y(a, c) += acc[a][c];
         }
-        if (DO_DIV) ypw[eOffP[t][a]] += gy[a];
+        if (HAS_P_OUT) ypw[eOffP[t][a]] += gy[a];
       }
       __syncwarp();
     }
@@ -844,7 +866,7 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
       }
     }
   }
-  if (DO_DIV) {
+  if (HAS_P_OUT) {
     for (int L = tid; L < kF1; L += kBT) {
       const int X = L % 5, Y = (L / 5) % 5, Z = L / 25;
       const int gx = i0 + X, gy = j0 + Y, gz = k0 + Z;
@@ -939,7 +961,9 @@ template <bool BLEND, int MODE, bool FULL>
 static void elem_launch(const Mesh* m, const Level& L, const double* eta, double gamma, const double* u,
                         const double* p, double* yu, double* yp, cudaStream_t s) {
   const int64_t nm = macro_count(m);
-#ifndef HHG_ELEM_V5
+#ifdef HHG_ELEM_V5
+  if (MODE & (ELEM_MASS | ELEM_MASSD))
+#endif
   {
     constexpr size_t smem = fp_smem_words<MODE>() * sizeof(double);
     dim3 grid((unsigned)L.n_bricks, (unsigned)nm);
@@ -954,7 +978,6 @@ static void elem_launch(const Mesh* m, const Level& L, const double* eta, double
                                                          L.npts2, nm * L.npts2, eta, u, p, yu, yp, gamma);
     return;
   }
-#endif
   constexpr int NS = ((MODE & (ELEM_A | ELEM_BT | ELEM_DIAG)) ? kNS2 : 0) + ((MODE & ELEM_DIV) ? kNS1 : 0);
 #ifdef HHG_GEO_GLOBAL
   constexpr size_t smem = (NS * kBT) * sizeof(double) + 13 * kBT * sizeof(int);
@@ -992,6 +1015,8 @@ int launch_elem(const Mesh* m, const Level& L, int mode, int form, const double*
     case ELEM_DIV: HHG_DISPATCH(ELEM_DIV); break;
     case ELEM_A | ELEM_BT | ELEM_DIV: HHG_DISPATCH(ELEM_A | ELEM_BT | ELEM_DIV); break;
     case ELEM_DIAG: HHG_DISPATCH(ELEM_DIAG); break;
+    case ELEM_MASS: HHG_DISPATCH(ELEM_MASS); break;
+    case ELEM_MASSD: HHG_DISPATCH(ELEM_MASSD); break;
     default: return fail(HHG_EINVAL, "bad element mode");
   }
 #undef HHG_DISPATCH

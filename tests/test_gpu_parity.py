@@ -85,6 +85,20 @@ def test_shell_level2_stokes_apply(shell_l2):
     assert rel_l2(canon(M, 2, hhg.HHG_P2VEC, yt), d.apply_BT(po)) <= TOL_APPLY
 
 
+def test_pressure_mass_apply_and_diag(shell_l2):
+    """M_{1/eta} (eq:schurMass) apply and diagonal, blended shell L2, config-2 viscosity."""
+    from oracle.operators import Discretisation
+    from tests.harness import oracle_bc
+    mac, lm, d, eta_o, M = shell_l2
+    dm = Discretisation(lm, True, eta_o, 0.0, oracle_bc(BC_SHELL), build=("M",))
+    eta = lib_eta(M, 2, C2)
+    po = uniform_from_keys(lm.p1_keys, 3, 0)
+    y = hhg.hhg_mass_apply(M, 2, eta, lib_p(M, 2, 3))
+    assert rel_l2(canon(M, 2, hhg.HHG_P1, y), dm.M @ po) <= TOL_APPLY
+    dg = hhg.hhg_mass_diag(M, 2, eta)
+    assert rel_l2(canon(M, 2, hhg.HHG_P1, dg), dm.M.diagonal()) <= TOL_APPLY
+
+
 def test_shell_level2_diag_and_dot(shell_l2):
     mac, lm, d, eta_o, M = shell_l2
     eta = lib_eta(M, 2, C2)

@@ -181,3 +181,25 @@ def test_manufactured_solution_converges_at_order_3_in_L2():
         errs.append(math.sqrt(e2))
     rates = [math.log2(errs[i] / errs[i + 1]) for i in range(2)]
     assert rates[1] >= 2.8, (errs, rates)
+
+
+def test_pressure_mass_closed_forms():
+    """M_{1/eta} (eq:schurMass): with eta = 1, 1^T M 1 = |Omega| (reference tet: 1/6); element matrix
+    |K|/20 (1 + delta_pr) (degree-2 rule is exact for P1 x P1); scaling eta -> c eta gives M / c;
+    symmetric positive definite."""
+    import scipy.sparse.linalg as sla
+    from oracle.refine import build_level
+    from oracle.operators import Discretisation
+    from workload import reference_tet
+    m = reference_tet()
+    lm = build_level(m.verts, m.tets, m.vtag, 1)
+    d = Discretisation(lm, False, None, 0.0, {}, build=("M",))
+    one = np.ones(lm.n_p1)
+    assert abs(one @ d.M @ one - 1.0 / 6.0) < 1e-15
+    lm0 = build_level(m.verts, m.tets, m.vtag, 0)
+    M0 = Discretisation(lm0, False, None, 0.0, {}, build=("M",)).M.toarray()
+    assert np.abs(M0 - (1.0 / 6.0) / 20.0 * (np.ones((4, 4)) + np.eye(4))).max() < 1e-16
+    d3 = Discretisation(lm, False, 3.0 * np.ones(lm.n_p1), 0.0, {}, build=("M",))
+    assert abs(d3.M - d.M / 3.0).max() < 1e-17
+    assert abs(d.M - d.M.T).max() < 1e-18
+    assert sla.eigsh(d.M, k=1, which="SA")[0][0] > 0
