@@ -264,6 +264,31 @@ int hhg_mg_profile_get(hhg_mg* mg, double* apply_ms_sum, int64_t* apply_count, d
                        int64_t* cycle_count);
 int hhg_mg_destroy(hhg_mg* mg);
 
+/* ------------------------------------------------------------------ Stokes solve
+ * FGMRES (restarted every `restart` iterations) for the projected system
+ * P [[A, B^T], [B+C, 0]] P [u; p] = P [f; g] (P_p = pressure mean zero),
+ * right-preconditioned by the symmetric Uzawa block preconditioner (eq:SymmetricUzawaStep1,
+ * P:427-437, B -> B+C in the pressure update) with A^-1 = V-cycle-preconditioned CG to tol_A
+ * (hhg_ablock_cg on the hierarchy `mg`) and S^-1 = M_{1/eta}^-1 by Jacobi-CG to tol_mass
+ * (eq:schurMass).  The V-cycle BFBT Schur approximation (eq:schurV) is NOT built yet.
+ * Vectors: [u (P2VEC) | p (P1)] contiguous, device, on the hierarchy's finest level.  Stops at
+ * |r| <= tol |P rhs| (2-norm over unique dofs) or max_iters.  Synchronises (host Arnoldi). */
+typedef struct {
+  int restart, max_iters;      /* FGMRES restart length and iteration cap */
+  double tol;                  /* relative residual target of FGMRES */
+  double sigma, omega;         /* Uzawa scalings (Table 1: 1, 0.3) */
+  double tol_A;                /* A-block CG relative tolerance (Table 1: 1e-2) */
+  int ablock_max_iters;
+  double tol_mass;             /* M_{1/eta} CG relative tolerance (Table 1: 1e-10) */
+  int mass_max_iters;
+} hhg_stokes_params;
+typedef struct hhg_stokes hhg_stokes;
+int hhg_stokes_create(hhg_mg* mg, const double* eta_p1, double gamma, const hhg_stokes_params* params,
+                      hhg_stokes** out);
+int hhg_stokes_solve(hhg_stokes* solver, const double* rhs, double* x, int* iters, double* rel_res,
+                     hhg_stream_t stream);
+int hhg_stokes_destroy(hhg_stokes* solver);
+
 /* Number of kernels launched by the library on this thread since the last reset. */
 int64_t hhg_launch_count(int reset);
 

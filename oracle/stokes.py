@@ -1,0 +1,130 @@
+"""ORACLE (test infrastructure only): the preconditioned Stokes solve, step by step in the paper's
+order.
+
+  FGMRES (Saad 1993), right-preconditioned, restarted, modified Gram-Schmidt + Givens,
+  for the projected system P K P x = P b, K = [[A, B^T], [B + C, 0]] (eq:SaddlePointStructure,
+  P:284-287), P = diag(P_v M, P_p) with P_p = arithmetic mean zero.
+  Preconditioner: one symmetric Uzawa step from (0, 0) (eq:SymmetricUzawaStep1) with
+  B -> B + C in the pressure update:
+      u_hat = sigma A^-1 r_u ; p = -omega S^-1 (r_p - (B+C) u_hat) ; u = u_hat + sigma A^-1 (r_u - A u_hat - B^T p)
+  A^-1: CG preconditioned by the V-cycle to tol_A (multigrid.ablock_cg);
+  S^-1: M_{1/eta}^-1 by Jacobi-preconditioned CG to tol_mass (eq:schurMass).
+Readings (R17-R19): P_p applied to the rhs, to every operator output and to the
+preconditioned pressure; relative residual stopping; Table 1 defaults (sigma 1, omega 0.3,
+tol_A 1e-2, tol_mass 1e-10).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from .multigrid import Hierarchy, ablock_cg
+
+
+def mean0(p):
+    return p - p.mean()
+
+
+def mass_cg(M, r, tol=1e-10, max_iters=500):
+    """Jacobi-preconditioned CG on the SPD pressure mass from 0 to |r_k| <= tol |r|."""
+    dinv = 1.0 / M.diagonal()
+    z = np.zeros_like(r)
+    res = r.copy()
+    r0 = float(np.linalg.norm(res))
+    if not r0 > 0:
+        return z
+    s = dinv * res
+    p = s.copy()
+    rz = float(res @ s)
+    for _ in range(max_iters):
+        q = M @ p
+        pq = float(p @ q)
+        alpha = rz / pq if pq != 0.0 else 0.0
+        z = z + alpha * p
+        res = res - alpha * q
+        if float(np.linalg.norm(res)) <= tol * r0:
+            break
+        s = dinv * res
+        rzn = float(res @ s)
+        p = s + (rzn / rz) * p
+        rz = rzn
+    return z
+
+
+class StokesOracle:
+    def __init__(self, H: Hierarchy, disc, Mmass, sigma=1.0, omega=0.3, tol_A=1e-2, ablock_max_iters=200,
+                 tol_mass=1e-10, mass_max_iters=500):
+        self.H, self.d = H, disc
+        self.A = H.Ac[H.lmax]
+        self.Pm = disc.Pm
+        self.B, self.Bbar = disc.B, disc.B + disc.C
+        self.M = Mmass
+        self.sigma, self.omega, self.tol_A, self.ablock_max_iters = sigma, omega, tol_A, ablock_max_iters
+        self.tol_mass, self.mass_max_iters = tol_mass, mass_max_iters
+        self.n2 = self.A.shape[0]
+
+    def op(self, x):
+        """P K x."""
+        u, p = x[:self.n2], x[self.n2:]
+        yu = self.A @ u + self.Pm @ (self.B.T @ p)
+        yp = mean0(self.Bbar @ (self.Pm @ u))
+        return np.concatenate([yu, yp])
+
+    def prec(self, r):
+        ru, rp = r[:self.n2], r[self.n2:]
+        uh = self.sigma * ablock_cg(self.H, ru, self.tol_A, self.ablock_max_iters)[0]
+        tp = mean0(rp - self.Bbar @ (self.Pm @ uh))
+        p = mean0(-self.omega * mass_cg(self.M, tp, self.tol_mass, self.mass_max_iters))
+        tu = ru - (self.A @ uh + self.Pm @ (self.B.T @ p))
+        u = uh + self.sigma * ablock_cg(self.H, tu, self.tol_A, self.ablock_max_iters)[0]
+        return np.concatenate([u, p])
+
+    def solve(self, rhs, tol=1e-8, restart=30, max_iters=100):
+        """FGMRES from x = 0 -> (x, iterations, relative residual of the projected system)."""
+        b = np.concatenate([self.Pm @ rhs[:self.n2], mean0(rhs[self.n2:])])
+        bn = float(np.linalg.norm(b))
+        x = np.zeros_like(b)
+        total, rel = 0, 1.0 if bn > 0 else 0.0
+        while bn > 0 and total < max_iters and rel > tol:
+            r = b - self.op(x)
+            beta = float(np.linalg.norm(r))
+            rel = beta / bn
+            if rel <= tol:
+                break
+            m = restart
+            V, Z = [r / beta], []
+            H = np.zeros((m + 1, m))
+            cs, sn = np.zeros(m), np.zeros(m)
+            g = np.zeros(m + 1)
+            g[0] = beta
+            j = 0
+            while j < m and total < max_iters:
+                total += 1
+                Z.append(self.prec(V[j]))
+                w = self.op(Z[j])
+                for i in range(j + 1):                     # modified Gram-Schmidt
+                    H[i, j] = float(w @ V[i])
+                    w = w - H[i, j] * V[i]
+                hn = float(np.linalg.norm(w))
+                H[j + 1, j] = hn
+                V.append(w / hn if hn > 0 else w)
+                for i in range(j):                         # previous Givens rotations
+                    h0, h1 = H[i, j], H[i + 1, j]
+                    H[i, j], H[i + 1, j] = cs[i] * h0 + sn[i] * h1, -sn[i] * h0 + cs[i] * h1
+                h0, h1 = H[j, j], H[j + 1, j]
+                dd = float(np.hypot(h0, h1))
+                cs[j], sn[j] = (h0 / dd, h1 / dd) if dd > 0 else (1.0, 0.0)
+                H[j, j], H[j + 1, j] = dd, 0.0
+                g[j + 1] = -sn[j] * g[j]
+                g[j] = cs[j] * g[j]
+                rel = abs(g[j + 1]) / bn
+                j += 1
+                if rel <= tol or hn == 0.0:
+                    break
+            y = np.zeros(j)
+            for i in range(j - 1, -1, -1):
+                y[i] = (g[i] - H[i, i + 1:j] @ y[i + 1:j]) / H[i, i]
+            for i in range(j):
+                x = x + y[i] * Z[i]
+        if bn > 0:
+            rel = float(np.linalg.norm(b - self.op(x))) / bn
+        return x, total, rel

@@ -40,7 +40,8 @@ EXPORTS = [
     "hhg_mg_profile_get", "hhg_mg_destroy", "hhg_launch_count",
     "hhg_mesh_create_part", "hhg_partition_rcb", "hhg_mesh_rank", "hhg_halo_info", "hhg_halo_keys",
     "hhg_owned_count", "hhg_halo_pack", "hhg_interface_sum_remote", "epsilon_apply_partial",
-    "hhg_ablock_cg", "hhg_mass_apply", "hhg_mass_diag",
+    "hhg_ablock_cg", "hhg_mass_apply", "hhg_mass_diag", "hhg_stokes_create", "hhg_stokes_solve",
+    "hhg_stokes_destroy",
 ]
 
 
@@ -80,6 +81,8 @@ def _load():
         "hhg_interface_sum_remote": ([P, I, I, P, P, P], I), "epsilon_apply_partial": ([P, I, I, P, P, P, P], I),
         "hhg_ablock_cg": ([P, P, P, D, I, P, P, P], I),
         "hhg_mass_apply": ([P, I, P, P, P, P], I), "hhg_mass_diag": ([P, I, P, P, P], I),
+        "hhg_stokes_create": ([P, P, D, P, P], I), "hhg_stokes_solve": ([P, P, P, P, P, P], I),
+        "hhg_stokes_destroy": ([P], I),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -474,3 +477,40 @@ class MG:
         _chk(_lib.hhg_mg_profile_get(self.handle, ctypes.byref(a), ctypes.byref(na), ctypes.byref(c),
                                      ctypes.byref(nc)))
         return dict(apply_ms_sum=a.value, apply_count=na.value, cycle_ms_sum=c.value, cycle_count=nc.value)
+
+
+class _StokesParams(ctypes.Structure):
+    _fields_ = [("restart", ctypes.c_int), ("max_iters", ctypes.c_int), ("tol", ctypes.c_double),
+                ("sigma", ctypes.c_double), ("omega", ctypes.c_double), ("tol_A", ctypes.c_double),
+                ("ablock_max_iters", ctypes.c_int), ("tol_mass", ctypes.c_double), ("mass_max_iters", ctypes.c_int)]
+
+
+class StokesSolver:
+    """hhg_stokes_create / hhg_stokes_solve: FGMRES + symmetric Uzawa (A^-1: V-cycle CG, S^-1: M_{1/eta}
+    CG) on the finest level of `mg`.  Vectors are [u (P2VEC) | p (P1)] concatenated."""
+
+    def __init__(self, mg, eta, gamma, restart=30, max_iters=100, tol=1e-8, sigma=1.0, omega=0.3, tol_A=1e-2,
+                 ablock_max_iters=200, tol_mass=1e-10, mass_max_iters=500):
+        self.mg = mg
+        self._eta = eta
+        prm = _StokesParams(restart, max_iters, tol, sigma, omega, tol_A, ablock_max_iters, tol_mass, mass_max_iters)
+        h = ctypes.c_void_p()
+        _chk(_lib.hhg_stokes_create(mg.handle, _ptr(eta), float(gamma), ctypes.byref(prm), ctypes.byref(h)))
+        self.handle = h
+        L = mg.l_max
+        self.n2, self.n1 = mg.mesh.vec_len(L, HHG_P2VEC), mg.mesh.vec_len(L, HHG_P1)
+
+    def __del__(self):
+        if getattr(self, "handle", None) and _lib is not None:
+            _lib.hhg_stokes_destroy(self.handle)
+            self.handle = None
+
+    def solve(self, rhs, x=None, stream=None):
+        import torch
+        n = self.n2 + self.n1
+        x = torch.zeros(n, dtype=torch.float64, device="cuda") if x is None else x
+        it, rel = ctypes.c_int(), ctypes.c_double()
+        _chk(_lib.hhg_stokes_solve(self.handle, _dev(rhs, n, "rhs"), _dev(x, n, "x"), ctypes.byref(it),
+                                   ctypes.byref(rel), _stream(stream)))
+        return x, it.value, rel.value
+

@@ -187,6 +187,9 @@ int launch_pcg_dir_zero(int64_t n, int it, const double* scal, const double* z, 
 int launch_dot_fused(const Mesh* m, const Level& L, int space, const double* x, const double* y, double* out,
                      cudaStream_t s);
 int launch_scalar_ops(int op, double* scal, cudaStream_t s);
+int launch_fill(int64_t n, double v, double* y, cudaStream_t s);
+int launch_recip(int64_t n, double* y, cudaStream_t s);                          // y = 1 / y
+int launch_pcg_scale(int64_t n, const double* d, const double* x, double* y, cudaStream_t s);  // y = d x
 
 }  // namespace hhg
 

@@ -657,6 +657,29 @@ __global__ void k_chebk(int64_t n, const double* __restrict__ t, const double* _
   }
 }
 
+__global__ void k_fill(int64_t n, double v, double* __restrict__ y) { GRID_STRIDE(i, n) y[i] = v; }
+__global__ void k_recip(int64_t n, double* __restrict__ y) { GRID_STRIDE(i, n) y[i] = 1.0 / y[i]; }
+__global__ void k_scale(int64_t n, const double* __restrict__ d, const double* __restrict__ x, double* __restrict__ y) {
+  GRID_STRIDE(i, n) y[i] = d[i] * x[i];
+}
+int launch_fill(int64_t n, double v, double* y, cudaStream_t s) {
+  k_fill<<<vgrid(n), 256, 0, s>>>(n, v, y);
+  count_launch();
+  HHG_CUDA(cudaGetLastError());
+  return HHG_OK;
+}
+int launch_recip(int64_t n, double* y, cudaStream_t s) {
+  k_recip<<<vgrid(n), 256, 0, s>>>(n, y);
+  count_launch();
+  HHG_CUDA(cudaGetLastError());
+  return HHG_OK;
+}
+int launch_pcg_scale(int64_t n, const double* d, const double* x, double* y, cudaStream_t s) {
+  k_scale<<<vgrid(n), 256, 0, s>>>(n, d, x, y);
+  count_launch();
+  HHG_CUDA(cudaGetLastError());
+  return HHG_OK;
+}
 int launch_axpby(int64_t n, double a, const double* x, double b, double* y, cudaStream_t s) {
   k_axpby<<<vgrid(n), 256, 0, s>>>(n, a, x, b, y);
   count_launch();

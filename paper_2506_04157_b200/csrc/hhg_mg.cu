@@ -508,3 +508,265 @@ int hhg_power_iteration(const hhg_mesh* mesh, int level, const double* eta_p1, c
 }
 
 }  // extern "C"
+
+// ================================================================ Stokes solve (NEXT-1)
+// FGMRES right-preconditioned by the symmetric Uzawa block preconditioner
+// (eq:SymmetricUzawaStep1) with B replaced by B + C in the pressure update:
+//   u_hat = sigma A^-1 r_u ;  p = -omega S^-1 (r_p - (B+C) u_hat) ;  u = u_hat + sigma A^-1 (r_u - A u_hat - B^T p)
+// A^-1 = CG preconditioned by the V-cycle to tol_A (hhg_ablock_cg), S^-1 = M_{1/eta}^-1 by
+// Jacobi-CG to tol_M (eq:schurMass).  The pressure part of every Krylov vector, operator
+// output and preconditioner output is projected to arithmetic mean zero (P_p).
+// Block vectors are [u (P2VEC) | p (P1)] in one allocation.
+struct hhg_stokes {
+  hhg_mg* mg = nullptr;
+  hhg_mesh* mesh = nullptr;
+  int level = 0;
+  const double* eta = nullptr;
+  double gamma = 0.0;
+  hhg_stokes_params prm{};
+  int64_t n2 = 0, n1 = 0;
+  std::vector<double*> V, Z;
+  double *w = nullptr, *t = nullptr, *a = nullptr, *b = nullptr, *ones = nullptr, *mdinv = nullptr, *sc = nullptr;
+  double *mr = nullptr, *mz = nullptr, *mp = nullptr, *mq = nullptr;
+  double n_unique_p = 0.0;
+  ~hhg_stokes() {
+    for (double* p : V) cudaFree(p);
+    for (double* p : Z) cudaFree(p);
+    for (double* p : {w, t, a, b, ones, mdinv, sc, mr, mz, mp, mq})
+      if (p) cudaFree(p);
+  }
+};
+
+namespace {
+int st_dot(hhg_stokes* S, const double* x, const double* y, int what, double* out, cudaStream_t s) {
+  // what: 1 = velocity part, 2 = pressure part, 3 = both
+  const Mesh* m = S->mesh;
+  const Level& L = m->levels[S->level];
+  double h[2] = {0.0, 0.0};
+  if (what & 1) HHG_TRY(launch_dot(m, L, HHG_P2VEC, x, y, S->sc + 0, s));
+  if (what & 2) HHG_TRY(launch_dot(m, L, HHG_P1, x + S->n2, y + S->n2, S->sc + 1, s));
+  HHG_CUDA(cudaMemcpyAsync(h, S->sc, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  HHG_CUDA(cudaStreamSynchronize(s));
+  *out = ((what & 1) ? h[0] : 0.0) + ((what & 2) ? h[1] : 0.0);
+  HHG_CUDA(cudaMemsetAsync(S->sc, 0, 2 * sizeof(double), s));
+  return HHG_OK;
+}
+int st_mean0(hhg_stokes* S, double* p, cudaStream_t s) {  // P_p: arithmetic mean zero over unique nodes
+  const Level& L = S->mesh->levels[S->level];
+  HHG_TRY(launch_dot(S->mesh, L, HHG_P1, p, S->ones, S->sc + 2, s));
+  double sum = 0.0;
+  HHG_CUDA(cudaMemcpyAsync(&sum, S->sc + 2, sizeof(double), cudaMemcpyDeviceToHost, s));
+  HHG_CUDA(cudaStreamSynchronize(s));
+  return launch_axpby(S->n1, -sum / S->n_unique_p, S->ones, 1.0, p, s);
+}
+// y = P K x : [ (M P_v)(A u + B^T p) ; P_p (B + C) u ]
+int st_op(hhg_stokes* S, const double* x, double* y, cudaStream_t s) {
+  HHG_TRY(stokes_apply(S->mesh, S->level, S->eta, S->gamma, x, x + S->n2, y, y + S->n2, (hhg_stream_t)s));
+  return st_mean0(S, y + S->n2, s);
+}
+// z_p = M_{1/eta}^-1 r_p by Jacobi-CG from 0 to relative tolerance tol_M (mass SPD)
+int st_mass_solve(hhg_stokes* S, const double* rp, double* zp, cudaStream_t s) {
+  const int64_t n = S->n1;
+  HHG_CUDA(cudaMemsetAsync(zp, 0, n * sizeof(double), s));
+  HHG_CUDA(cudaMemcpyAsync(S->mr, rp, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  const Level& L = S->mesh->levels[S->level];
+  auto pdot = [&](const double* x, const double* y, double* out) -> int {
+    HHG_TRY(launch_dot(S->mesh, L, HHG_P1, x, y, S->sc + 3, s));
+    HHG_CUDA(cudaMemcpyAsync(out, S->sc + 3, sizeof(double), cudaMemcpyDeviceToHost, s));
+    HHG_CUDA(cudaStreamSynchronize(s));
+    return HHG_OK;
+  };
+  auto jac = [&](const double* r, double* z) { return launch_pcg_scale(n, S->mdinv, r, z, s); };
+  double r0 = 0.0;
+  HHG_TRY(pdot(S->mr, S->mr, &r0));
+  r0 = std::sqrt(r0);
+  if (!(r0 > 0)) return HHG_OK;
+  HHG_TRY(jac(S->mr, S->mz));
+  HHG_CUDA(cudaMemcpyAsync(S->mp, S->mz, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  double rz = 0.0;
+  HHG_TRY(pdot(S->mr, S->mz, &rz));
+  for (int it = 0; it < S->prm.mass_max_iters; ++it) {
+    HHG_TRY(hhg_mass_apply(S->mesh, S->level, S->eta, S->mp, S->mq, (hhg_stream_t)s));
+    double pq = 0.0;
+    HHG_TRY(pdot(S->mp, S->mq, &pq));
+    const double alpha = pq != 0.0 ? rz / pq : 0.0;
+    HHG_TRY(launch_axpby(n, alpha, S->mp, 1.0, zp, s));
+    HHG_TRY(launch_axpby(n, -alpha, S->mq, 1.0, S->mr, s));
+    double rr = 0.0;
+    HHG_TRY(pdot(S->mr, S->mr, &rr));
+    if (std::sqrt(std::max(rr, 0.0)) <= S->prm.tol_mass * r0) break;
+    HHG_TRY(jac(S->mr, S->mz));
+    double rzn = 0.0;
+    HHG_TRY(pdot(S->mr, S->mz, &rzn));
+    HHG_TRY(launch_axpby(n, 1.0, S->mz, rzn / rz, S->mp, s));  // p = z + beta p
+    rz = rzn;
+  }
+  return HHG_OK;
+}
+// z = Prec(r): one symmetric Uzawa step from (0, 0)
+int st_prec(hhg_stokes* S, const double* r, double* z, cudaStream_t s) {
+  const int64_t n2 = S->n2, n1 = S->n1;
+  const double sig = S->prm.sigma, om = S->prm.omega;
+  int it;
+  double rel;
+  // u_hat = sigma A^-1 r_u  (z_u holds u_hat)
+  HHG_TRY(hhg_ablock_cg(S->mg, r, z, S->prm.tol_A, S->prm.ablock_max_iters, &it, &rel, (hhg_stream_t)s));
+  HHG_TRY(launch_axpby(n2, 0.0, z, sig, z, s));
+  // t_p = r_p - (B + C) u_hat ; p = -omega S^-1 t_p ; P_p
+  HHG_TRY(div_apply(S->mesh, S->level, S->gamma, z, S->t + n2, (hhg_stream_t)s));
+  HHG_TRY(launch_axpby(n1, 1.0, r + n2, -1.0, S->t + n2, s));
+  HHG_TRY(st_mean0(S, S->t + n2, s));
+  HHG_TRY(st_mass_solve(S, S->t + n2, z + n2, s));
+  HHG_TRY(launch_axpby(n1, 0.0, z + n2, -om, z + n2, s));
+  HHG_TRY(st_mean0(S, z + n2, s));
+  // t_u = r_u - A u_hat - B^T p ; u = u_hat + sigma A^-1 t_u
+  HHG_TRY(stokes_apply(S->mesh, S->level, S->eta, S->gamma, z, z + n2, S->t, S->a + n2, (hhg_stream_t)s));
+  HHG_TRY(launch_axpby(n2, 1.0, r, -1.0, S->t, s));
+  HHG_TRY(hhg_ablock_cg(S->mg, S->t, S->a, S->prm.tol_A, S->prm.ablock_max_iters, &it, &rel, (hhg_stream_t)s));
+  return launch_axpby(n2, sig, S->a, 1.0, z, s);
+}
+}  // namespace
+
+extern "C" {
+
+int hhg_stokes_create(hhg_mg* mg, const double* eta_p1, double gamma, const hhg_stokes_params* prm,
+                      hhg_stokes** out) {
+  if (!mg || !prm || !out) return fail(HHG_EINVAL, "hhg_stokes_create: NULL argument");
+  if (prm->restart < 1 || prm->max_iters < 1 || !(prm->tol > 0) || !(prm->tol_A > 0) || !(prm->tol_mass > 0))
+    return fail(HHG_EINVAL, "hhg_stokes_create: bad parameters");
+  auto* S = new hhg_stokes();
+  S->mg = mg;
+  S->mesh = mg->mesh;
+  S->level = mg->prm.l_max;
+  S->eta = eta_p1;
+  S->gamma = gamma;
+  S->prm = *prm;
+  const Level& L = S->mesh->levels[S->level];
+  S->n2 = p2vec_len(S->mesh, S->level);
+  S->n1 = macro_count(S->mesh) * L.npts1;
+  const int64_t nb = S->n2 + S->n1;
+  auto alloc = [&](double** p, int64_t n) { return cudaMalloc(p, std::max<int64_t>(n, 1) * sizeof(double)) == cudaSuccess; };
+  bool ok = true;
+  S->V.resize(prm->restart + 1, nullptr);
+  S->Z.resize(prm->restart, nullptr);
+  for (auto& p : S->V) ok = ok && alloc(&p, nb);
+  for (auto& p : S->Z) ok = ok && alloc(&p, nb);
+  for (double** p : {&S->w, &S->t, &S->a, &S->b}) ok = ok && alloc(p, nb);
+  for (double** p : {&S->ones, &S->mdinv, &S->mr, &S->mz, &S->mp, &S->mq}) ok = ok && alloc(p, S->n1);
+  ok = ok && alloc(&S->sc, 8);
+  if (!ok) {
+    delete S;
+    return fail(HHG_ENOMEM, "hhg_stokes_create: workspace");
+  }
+  cudaStream_t s = nullptr;
+  int r = HHG_OK;
+  auto run = [&]() -> int {
+    HHG_CUDA(cudaMemset(S->sc, 0, 8 * sizeof(double)));
+    HHG_TRY(launch_fill(S->n1, 1.0, S->ones, s));
+    HHG_TRY(hhg_mass_diag(S->mesh, S->level, S->eta, S->mdinv, nullptr));
+    HHG_TRY(launch_recip(S->n1, S->mdinv, s));
+    HHG_TRY(launch_dot(S->mesh, L, HHG_P1, S->ones, S->ones, S->sc + 4, s));
+    HHG_CUDA(cudaMemcpy(&S->n_unique_p, S->sc + 4, sizeof(double), cudaMemcpyDeviceToHost));
+    return HHG_OK;
+  };
+  r = run();
+  if (r != HHG_OK) {
+    delete S;
+    return r;
+  }
+  *out = S;
+  return HHG_OK;
+}
+
+int hhg_stokes_destroy(hhg_stokes* S) {
+  delete S;
+  return HHG_OK;
+}
+
+int hhg_stokes_solve(hhg_stokes* S, const double* rhs, double* x, int* iters_out, double* rel_res_out,
+                     hhg_stream_t stream) {
+  if (!S || !rhs || !x) return fail(HHG_EINVAL, "hhg_stokes_solve: NULL argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t n2 = S->n2, n1 = S->n1, nb = n2 + n1;
+  const int m = S->prm.restart;
+  // b = P rhs
+  HHG_CUDA(cudaMemcpyAsync(S->b, rhs, nb * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  HHG_TRY(launch_fixup(S->mesh, S->mesh->levels[S->level], HHG_P2VEC, false, true, S->b, s));
+  HHG_TRY(st_mean0(S, S->b + n2, s));
+  double bn = 0.0;
+  HHG_TRY(st_dot(S, S->b, S->b, 3, &bn, s));
+  bn = std::sqrt(bn);
+  HHG_CUDA(cudaMemsetAsync(x, 0, nb * sizeof(double), s));
+  int total = 0;
+  double rel = bn > 0 ? 1.0 : 0.0;
+  std::vector<double> H((size_t)(m + 1) * m), cs(m), sn(m), g(m + 1), y(m);
+  while (bn > 0 && total < S->prm.max_iters && rel > S->prm.tol) {
+    // r = b - P K x
+    HHG_TRY(st_op(S, x, S->w, s));
+    HHG_TRY(launch_axpby(nb, 1.0, S->b, -1.0, S->w, s));
+    double beta = 0.0;
+    HHG_TRY(st_dot(S, S->w, S->w, 3, &beta, s));
+    beta = std::sqrt(beta);
+    rel = beta / bn;
+    if (rel <= S->prm.tol) break;
+    HHG_TRY(launch_axpby(nb, 1.0 / beta, S->w, 0.0, S->V[0], s));
+    std::fill(g.begin(), g.end(), 0.0);
+    g[0] = beta;
+    int j = 0;
+    for (; j < m && total < S->prm.max_iters; ++j) {
+      ++total;
+      HHG_TRY(st_prec(S, S->V[j], S->Z[j], s));
+      HHG_TRY(st_op(S, S->Z[j], S->w, s));
+      for (int i = 0; i <= j; ++i) {  // modified Gram-Schmidt
+        double h = 0.0;
+        HHG_TRY(st_dot(S, S->w, S->V[i], 3, &h, s));
+        H[(size_t)i * m + j] = h;
+        HHG_TRY(launch_axpby(nb, -h, S->V[i], 1.0, S->w, s));
+      }
+      double hn = 0.0;
+      HHG_TRY(st_dot(S, S->w, S->w, 3, &hn, s));
+      hn = std::sqrt(hn);
+      H[(size_t)(j + 1) * m + j] = hn;
+      if (hn > 0) HHG_TRY(launch_axpby(nb, 1.0 / hn, S->w, 0.0, S->V[j + 1], s));
+      for (int i = 0; i < j; ++i) {  // previous Givens rotations
+        const double h0 = H[(size_t)i * m + j], h1 = H[(size_t)(i + 1) * m + j];
+        H[(size_t)i * m + j] = cs[i] * h0 + sn[i] * h1;
+        H[(size_t)(i + 1) * m + j] = -sn[i] * h0 + cs[i] * h1;
+      }
+      const double h0 = H[(size_t)j * m + j], h1 = H[(size_t)(j + 1) * m + j];
+      const double d = std::hypot(h0, h1);
+      cs[j] = d > 0 ? h0 / d : 1.0;
+      sn[j] = d > 0 ? h1 / d : 0.0;
+      H[(size_t)j * m + j] = d;
+      H[(size_t)(j + 1) * m + j] = 0.0;
+      g[j + 1] = -sn[j] * g[j];
+      g[j] = cs[j] * g[j];
+      rel = std::fabs(g[j + 1]) / bn;
+      if (rel <= S->prm.tol || hn == 0.0) {
+        ++j;
+        break;
+      }
+    }
+    // x += Z y,  H(0:j,0:j) y = g(0:j)
+    for (int i = j - 1; i >= 0; --i) {
+      double acc = g[i];
+      for (int k = i + 1; k < j; ++k) acc -= H[(size_t)i * m + k] * y[k];
+      y[i] = acc / H[(size_t)i * m + i];
+    }
+    for (int i = 0; i < j; ++i) HHG_TRY(launch_axpby(nb, y[i], S->Z[i], 1.0, x, s));
+  }
+  // true residual of the projected system
+  if (bn > 0) {
+    HHG_TRY(st_op(S, x, S->w, s));
+    HHG_TRY(launch_axpby(nb, 1.0, S->b, -1.0, S->w, s));
+    double rr = 0.0;
+    HHG_TRY(st_dot(S, S->w, S->w, 3, &rr, s));
+    rel = std::sqrt(rr) / bn;
+  }
+  HHG_CUDA(cudaStreamSynchronize(s));
+  if (iters_out) *iters_out = total;
+  if (rel_res_out) *rel_res_out = rel;
+  return HHG_OK;
+}
+
+}  // extern "C"
