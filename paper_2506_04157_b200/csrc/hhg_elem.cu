@@ -28,6 +28,7 @@
 //     Db_m(m), edge: (sqrt5-1)/4 (Sbar_m + Sbar_j) + Db_m(j) + Db_j(m)), all constant factors
 //     folded into the per-point weight.
 #include "hhg_internal.h"
+#include "hhg_device.cuh"
 
 namespace hhg {
 
@@ -881,6 +882,232 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
       else if (v != 0.0) atomicAdd(dst, v);
     }
   }
+}
+
+static int ensure_slots();
+
+// ================================================================ persistent coarse solve
+// The 50-iteration Jacobi-PCG of the coarsest level (R15) as ONE kernel: one CTA per
+// macro (coarse levels n <= 4 are a single sparse brick per macro), a software grid barrier
+// between the phases of an iteration (all CTAs co-resident: #macros CTAs of 64 threads), device-
+// resident scalars recomputed identically by every CTA from per-macro partials in fixed order.
+// Per iteration: q = A p (element contributions of the CTA's macro summed in shared memory)
+// | interface sum + BC of q (groups strided over the grid) | p.q | x += a p, r -= a q,
+// z = P_v M D^-1 r, r.z | p = z + b p.  Single rank only (no NCCL inside a kernel).
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* vb = bar;
+    const unsigned gen = vb[1];
+    __threadfence();
+    if (atomicAdd(&bar[0], 1u) == nblocks - 1) {
+      bar[0] = 0;
+      __threadfence();
+      atomicAdd(&bar[1], 1u);
+    } else {
+      while (vb[1] == gen) {
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+__device__ __forceinline__ double block_sum64(double v, double* red) {  // 64-thread CTA, fixed order
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  return red[0] + red[1];
+}
+__device__ __forceinline__ double grid_total(const volatile double* part, int n) {
+  double t = 0.0;
+  for (int i = 0; i < n; ++i) t += part[i];
+  return t;
+}
+
+template <bool BLEND, bool FULL>
+__global__ void __launch_bounds__(kBT) k_coarse_pcg(
+    const MacroGeo* __restrict__ mgeo, const double* __restrict__ lgeo, int n1, double inv_n1, int64_t npts1,
+    int64_t npts2, int64_t cs, const double* __restrict__ eta, const double* __restrict__ dinv,
+    const int32_t* __restrict__ bcn, const uint8_t* __restrict__ own, int64_t ng, const int64_t* __restrict__ gptr,
+    const int64_t* __restrict__ gcopy, const uint8_t* __restrict__ gkind, const double* __restrict__ gnormal,
+    const double* __restrict__ f, double* x, double* r, double* z, double* p, double* q, double* part,
+    unsigned* bar, int iters) {
+  extern __shared__ double sy[];  // [3][npts2] element contributions of this macro
+  __shared__ double red[2];
+  const int mac = blockIdx.x, nb = gridDim.x, tid = threadIdx.x;
+  const int n2 = 2 * n1;
+  const int64_t mb2 = (int64_t)mac * npts2, mb1 = (int64_t)mac * npts1;
+  const int nloc = (int)npts2;
+  double* part1 = part;
+  double* part2 = part + nb;
+  // x = 0, r = f, z = P_v M D^-1 r, p = z ; r.z
+  double acc = 0.0;
+  for (int i = tid; i < nloc; i += kBT) {
+    const int64_t j = mb2 + i;
+    double zv[3], rv[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      x[j + c * cs] = 0.0;
+      rv[c] = f[j + c * cs];
+      r[j + c * cs] = rv[c];
+      zv[c] = dinv[j + c * cs] * rv[c];
+    }
+    bc_project(bcn[j], gnormal, zv[0], zv[1], zv[2]);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      z[j + c * cs] = zv[c];
+      p[j + c * cs] = zv[c];
+    }
+    if (own[j]) acc += rv[0] * zv[0] + rv[1] * zv[1] + rv[2] * zv[2];
+  }
+  acc = block_sum64(acc, red);
+  if (tid == 0) part2[mac] = acc;
+  grid_barrier(bar, nb);
+  double rz = grid_total(part2, nb);
+
+  const MacroGeo& g = mgeo[mac];
+  double nh[3] = {0, 0, 0}, cK = 1.0;
+  if (BLEND) {
+    nh[0] = g.nhat[0];
+    nh[1] = g.nhat[1];
+    nh[2] = g.nhat[2];
+    cK = g.cK;
+  }
+  const double* Gm = lgeo + (int64_t)mac * kLevelGeo;
+  const double wdet = EWQ * Gm[6 * kTypeGeo];
+  const int nit = eNItems[n1];
+  for (int it = 0; it < iters; ++it) {
+    // ---- q = A p on this macro (shared-memory accumulation), written to the macro's storage
+    for (int i = tid; i < 3 * nloc; i += kBT) sy[i] = 0.0;
+    __syncthreads();
+    for (int k = tid; k < nit; k += kBT) {
+      const int item = eItems[n1][k];
+      const int cube = item & 63, t = item >> 6;
+      const int ai = cube & 3, aj = (cube >> 2) & 3, ak = cube >> 4;
+      double xa[3];
+      const double fa = ai * inv_n1, fb = aj * inv_n1, fc = ak * inv_n1;
+#pragma unroll
+      for (int rr = 0; rr < 3; ++rr) xa[rr] = g.X0[rr] + g.Jm[3 * rr] * fa + g.Jm[3 * rr + 1] * fb + g.Jm[3 * rr + 2] * fc;
+      int ix[10];
+      double uu[10][3], et[4], pp[4] = {0, 0, 0, 0}, accv[10][3], gy[4];
+#pragma unroll
+      for (int a = 0; a < 10; ++a) {
+        const int sl = eSlot[t][a];
+        ix[a] = rowstart32(n2, 2 * aj + (sl / 3) % 3, 2 * ak + sl / 9) + 2 * ai + sl % 3;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) uu[a][c] = p[mb2 + ix[a] + c * cs];
+      }
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int ps = ePSlot[t][v];
+        et[v] = eta ? eta[mb1 + rowstart32(n1, aj + ((ps >> 1) & 1), ak + (ps >> 2)) + ai + (ps & 1)] : 1.0;
+      }
+      tet_body<BLEND, ELEM_A, FULL>(Gm + t * kTypeGeo, wdet, xa, nh, cK, 0.0, RegU{uu}, et, pp, accv, gy);
+#pragma unroll
+      for (int a = 0; a < 10; ++a)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) atomicAdd(&sy[c * nloc + ix[a]], accv[a][c]);
+    }
+    __syncthreads();
+    for (int i = tid; i < nloc; i += kBT)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) q[mb2 + i + c * cs] = sy[c * nloc + i];
+    grid_barrier(bar, nb);
+    // ---- interface sum + BC of q
+    for (int64_t gi = (int64_t)mac * kBT + tid; gi < ng; gi += (int64_t)nb * kBT) {
+      const int64_t b0 = gptr[gi], e0 = gptr[gi + 1];
+      double val[3];
+      group_sum<3>(b0, e0, gcopy, cs, q, val);
+      group_bc<3>(gkind[gi], gnormal + 3 * gi, val);
+      group_store<3>(b0, e0, gcopy, cs, val, q);
+    }
+    grid_barrier(bar, nb);
+    // ---- p.q
+    acc = 0.0;
+    for (int i = tid; i < nloc; i += kBT) {
+      const int64_t j = mb2 + i;
+      if (own[j]) acc += p[j] * q[j] + p[j + cs] * q[j + cs] + p[j + 2 * cs] * q[j + 2 * cs];
+    }
+    acc = block_sum64(acc, red);
+    if (tid == 0) part1[mac] = acc;
+    grid_barrier(bar, nb);
+    const double pq = grid_total(part1, nb);
+    const double alpha = (rz > 1e-300 && pq != 0.0) ? rz / pq : 0.0;
+    // ---- x += a p, r -= a q, z = P_v M D^-1 r ; r.z
+    acc = 0.0;
+    for (int i = tid; i < nloc; i += kBT) {
+      const int64_t j = mb2 + i;
+      double zv[3], rv[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const int64_t jc = j + c * cs;
+        x[jc] += alpha * p[jc];
+        rv[c] = r[jc] - alpha * q[jc];
+        r[jc] = rv[c];
+        zv[c] = dinv[jc] * rv[c];
+      }
+      bc_project(bcn[j], gnormal, zv[0], zv[1], zv[2]);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) z[j + c * cs] = zv[c];
+      if (own[j]) acc += rv[0] * zv[0] + rv[1] * zv[1] + rv[2] * zv[2];
+    }
+    acc = block_sum64(acc, red);
+    if (tid == 0) part2[mac] = acc;
+    grid_barrier(bar, nb);
+    const double rzn = grid_total(part2, nb);
+    const double beta = rz > 1e-300 ? rzn / rz : 0.0;
+    for (int i = tid; i < nloc; i += kBT)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const int64_t jc = mb2 + i + c * cs;
+        p[jc] = z[jc] + beta * p[jc];
+      }
+    rz = rz > 1e-300 ? rzn : rz;
+    __syncthreads();
+  }
+}
+
+// All CTAs of the persistent kernel must be co-resident (software grid barrier): true if the device
+// can hold one CTA per macro at once.
+bool coarse_pcg_fits(const Mesh* m, const Level& L) {
+  const int64_t nm = macro_count(m);
+  if (L.n1 > 4 || nm < 1) return false;
+  const size_t smem = 3 * L.npts2 * sizeof(double);
+  int per_sm = 0, nsm = 0, dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    return false;
+  const bool bl = m->blend == HHG_BLEND_SHELL;
+  cudaError_t e = bl ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_coarse_pcg<true, true>, kBT, smem)
+                     : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_coarse_pcg<false, true>, kBT, smem);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return (int64_t)per_sm * nsm >= nm;
+}
+
+int launch_coarse_pcg(const Mesh* m, const Level& L, const double* eta, const double* dinv, const double* f, double* x,
+                      double* r, double* z, double* p, double* q, double* part, unsigned* bar, int iters,
+                      cudaStream_t s) {
+  HHG_TRY(ensure_slots());
+  const int64_t nm = macro_count(m);
+  if (!coarse_pcg_fits(m, L)) return fail(HHG_EINVAL, "persistent coarse PCG: CTAs cannot all be co-resident");
+  const size_t smem = 3 * L.npts2 * sizeof(double);
+  const bool bl = m->blend == HHG_BLEND_SHELL;
+if (bl)
+    k_coarse_pcg<true, true><<<(unsigned)nm, kBT, smem, s>>>(m->dgeo, L.geo, L.n1, 1.0 / L.n1, L.npts1, L.npts2,
+                                                             nm * L.npts2, eta, dinv, L.bcn2, L.own2, L.g2.n, L.g2.ptr,
+                                                             L.g2.copy, L.g2.kind, L.g2.normal, f, x, r, z, p, q, part,
+                                                             bar, iters);
+  else
+    k_coarse_pcg<false, true><<<(unsigned)nm, kBT, smem, s>>>(m->dgeo, L.geo, L.n1, 1.0 / L.n1, L.npts1, L.npts2,
+                                                              nm * L.npts2, eta, dinv, L.bcn2, L.own2, L.g2.n, L.g2.ptr,
+                                                              L.g2.copy, L.g2.kind, L.g2.normal, f, x, r, z, p, q, part,
+                                                              bar, iters);
+  count_launch();
+  HHG_CUDA(cudaGetLastError());
+  return HHG_OK;
 }
 
 static bool g_slots_ready = false;

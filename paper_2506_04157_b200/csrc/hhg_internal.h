@@ -184,6 +184,11 @@ int launch_pcg_update_bc(const Mesh* m, const Level& L, int it, const double* sc
                          const double* p, const double* q, const double* dinv, double* z, cudaStream_t s);
 int launch_pcg_dir_zero(int64_t n, int it, const double* scal, const double* z, double* p, double* q_zero,
                         cudaStream_t s);
+// the coarsest level's Jacobi-PCG (all iterations) as one persistent kernel (single rank, n1 <= 4)
+bool coarse_pcg_fits(const Mesh* m, const Level& L);
+int launch_coarse_pcg(const Mesh* m, const Level& L, const double* eta, const double* dinv, const double* f, double* x,
+                      double* r, double* z, double* p, double* q, double* part, unsigned* bar, int iters,
+                      cudaStream_t s);
 int launch_dot_fused(const Mesh* m, const Level& L, int space, const double* x, const double* y, double* out,
                      cudaStream_t s);
 int launch_scalar_ops(int op, double* scal, cudaStream_t s);

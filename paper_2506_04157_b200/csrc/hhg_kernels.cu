@@ -11,6 +11,7 @@
 #include <cstdio>
 
 #include "hhg_internal.h"
+#include "hhg_device.cuh"
 
 namespace hhg {
 
@@ -19,59 +20,6 @@ constexpr double QA = 0.58541019662496845446;  // (5 + 3 sqrt 5)/20
 constexpr double QB = 0.13819660112501051518;  // (5 - sqrt 5)/20
 
 // ------------------------------------------------------------------ interface sum + BC
-// Sum of the copies of group gi (copies gathered in chunks of 4 independent loads: macro vertices
-// have up to ~20 copies and a sequential dependent walk made coarse levels latency-bound).
-template <int NC>
-__device__ __forceinline__ void group_sum(int64_t b, int64_t e, const int64_t* __restrict__ copy, int64_t cstride,
-                                          const double* __restrict__ v, double (&val)[NC]) {
-  constexpr int CH = 4;
-#pragma unroll
-  for (int c = 0; c < NC; ++c) val[c] = 0.0;
-  for (int64_t k0 = b; k0 < e; k0 += CH) {
-    int64_t idx[CH];
-#pragma unroll
-    for (int j = 0; j < CH; ++j) idx[j] = (k0 + j < e) ? copy[k0 + j] : -1;
-    double x[CH][NC];
-#pragma unroll
-    for (int j = 0; j < CH; ++j)
-#pragma unroll
-      for (int c = 0; c < NC; ++c) x[j][c] = idx[j] >= 0 ? v[c * cstride + idx[j]] : 0.0;
-#pragma unroll
-    for (int j = 0; j < CH; ++j)
-#pragma unroll
-      for (int c = 0; c < NC; ++c)
-        if (idx[j] >= 0) val[c] += x[j][c];
-  }
-}
-template <int NC>
-__device__ __forceinline__ void group_store(int64_t b, int64_t e, const int64_t* __restrict__ copy, int64_t cstride,
-                                            const double (&val)[NC], double* __restrict__ v) {
-  constexpr int CH = 4;
-  for (int64_t k0 = b; k0 < e; k0 += CH) {
-    int64_t idx[CH];
-#pragma unroll
-    for (int j = 0; j < CH; ++j) idx[j] = (k0 + j < e) ? copy[k0 + j] : -1;
-#pragma unroll
-    for (int j = 0; j < CH; ++j)
-      if (idx[j] >= 0)
-#pragma unroll
-        for (int c = 0; c < NC; ++c) v[c * cstride + idx[j]] = val[c];
-  }
-}
-template <int NC>
-__device__ __forceinline__ void group_bc(int kd, const double* __restrict__ nrm, double (&val)[NC]) {
-  if (kd == HHG_BC_DIRICHLET0) {
-#pragma unroll
-    for (int c = 0; c < NC; ++c) val[c] = 0.0;
-  } else if (kd == HHG_BC_FREESLIP && NC == 3) {
-    const double n0 = nrm[0], n1 = nrm[1], n2 = nrm[2];
-    const double un = val[0] * n0 + val[1 % NC] * n1 + val[2 % NC] * n2;
-    val[0] -= un * n0;
-    val[1 % NC] -= un * n1;
-    val[2 % NC] -= un * n2;
-  }
-}
-
 template <int NC, bool BC>
 __global__ void k_fixup(int64_t ng, const int64_t* __restrict__ ptr, const int64_t* __restrict__ copy,
                         const uint8_t* __restrict__ kind, const double* __restrict__ normal, int64_t cstride,
@@ -719,18 +667,6 @@ int launch_chebk(int64_t n, const double* t, const double* dinv, double c1, doub
 // projection P_v M of the new direction is applied per node (Dirichlet: 0; free slip: remove the
 // normal component with the node group's normal) -- identical to a BC-only interface pass on a
 // consistent vector.
-__device__ __forceinline__ void bc_project(int b, const double* __restrict__ nrm, double& v0, double& v1, double& v2) {
-  if (b == -1) return;
-  if (b == -2) {
-    v0 = v1 = v2 = 0.0;
-    return;
-  }
-  const double n0 = nrm[3 * b], n1 = nrm[3 * b + 1], n2 = nrm[3 * b + 2];
-  const double un = v0 * n0 + v1 * n1 + v2 * n2;
-  v0 -= un * n0;
-  v1 -= un * n1;
-  v2 -= un * n2;
-}
 __global__ void k_cheb0_bc(int64_t ns, int64_t cs, const double* __restrict__ f, const double* __restrict__ t,
                            const double* __restrict__ dinv, double it, double* __restrict__ r, double* __restrict__ d,
                            const int32_t* __restrict__ bcn, const double* __restrict__ nrm) {

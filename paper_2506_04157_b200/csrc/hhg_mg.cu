@@ -3,6 +3,7 @@
 // config 3; replaces the paper's AMG-CG of P:443), power-iteration spectrum estimate.
 // All scalars of the PCG stay on the device so the whole cycle can be captured in one CUDA graph.
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "hhg_internal.h"
@@ -82,6 +83,8 @@ struct hhg_mg {
   };
   std::vector<Lv> lv;
   double* scal = nullptr;    // device scalars
+  double* cpart = nullptr;   // persistent coarse PCG: per-macro partial sums [2][n_macro]
+  unsigned* cbar = nullptr;  // its grid barrier (count, generation)
   double* hbuf_rhs = nullptr;  // device staging for vcycle_host
   double* hbuf_x = nullptr;
   cudaGraphExec_t gexec = nullptr;
@@ -92,6 +95,10 @@ struct hhg_mg {
   double *cg_r = nullptr, *cg_z = nullptr, *cg_p = nullptr, *cg_q = nullptr, *cg_s = nullptr;
   cudaGraphExec_t cg_gexec = nullptr;
   cudaStream_t cg_stream = nullptr;
+  // HHG_PERSISTENT_COARSE=1: run the coarse PCG as one persistent kernel (k_coarse_pcg).  Off by
+  // default: measured 27.7 vs 26.4 ms per V(3,3) at L5 -- 200 software grid barriers per solve
+  // cost more than the ~300 launches they replace.
+  bool no_persistent = true;
   // profiling
   bool prof = false;
   std::vector<cudaEvent_t> ev;
@@ -103,6 +110,8 @@ struct hhg_mg {
       for (double* p : {L.x, L.f, L.r, L.d, L.t, L.dinv, L.p})
         if (p) cudaFree(p);
     if (scal) cudaFree(scal);
+    if (cpart) cudaFree(cpart);
+    if (cbar) cudaFree(cbar);
     if (hbuf_rhs) cudaFree(hbuf_rhs);
     if (hbuf_x) cudaFree(hbuf_x);
     if (gexec) cudaGraphExecDestroy(gexec);
@@ -177,6 +186,8 @@ static int mg_pcg(hhg_mg* mg, int l, const double* f, double* x, cudaStream_t s)
   double* z = L.d;
   double* p = L.p;
   double* q = L.t;
+  if (m->nranks == 1 && mg->prm.visc_form == HHG_VISC_FULL && !mg->no_persistent && coarse_pcg_fits(m, LL))
+    return launch_coarse_pcg(m, LL, L.eta, L.dinv, f, x, r, z, p, q, mg->cpart, mg->cbar, mg->prm.coarse_iters, s);
   HHG_CUDA(cudaMemsetAsync(x, 0, n * sizeof(double), s));
   HHG_TRY(launch_cheb0_bc(m, LL, f, nullptr, L.dinv, 1.0, r, z, s));  // r = f, z = PM dinv r
   HHG_CUDA(cudaMemcpyAsync(p, z, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
@@ -223,6 +234,10 @@ int hhg_mg_create(hhg_mesh* mesh, const hhg_mg_params* params, const double* con
     return fail(HHG_EINVAL, "hhg_mg_create: bad smoother parameters");
   auto* mg = new hhg_mg();
   mg->mesh = mesh;
+  {
+    const char* e = getenv("HHG_PERSISTENT_COARSE");
+    mg->no_persistent = !(e && e[0] == '1');
+  }
   mg->prm = P;
   mg->lv.resize(P.l_max + 1);
   auto bail = [&](int code) {
@@ -230,6 +245,9 @@ int hhg_mg_create(hhg_mesh* mesh, const hhg_mg_params* params, const double* con
     return code;
   };
   if (cudaMalloc(&mg->scal, 16 * sizeof(double)) != cudaSuccess) return bail(fail(HHG_ENOMEM, "scal"));
+  if (cudaMalloc(&mg->cpart, 2 * std::max<int64_t>(1, macro_count(mesh)) * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&mg->cbar, 2 * sizeof(unsigned)) != cudaSuccess || cudaMemset(mg->cbar, 0, 2 * sizeof(unsigned)) != cudaSuccess)
+    return bail(fail(HHG_ENOMEM, "coarse PCG scratch"));
   for (int l = P.l_min; l <= P.l_max; ++l) {
     int r = ensure_level(mesh, l);
     if (r != HHG_OK) return bail(r);
