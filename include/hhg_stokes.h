@@ -178,7 +178,7 @@ int hhg_interface_sum(const hhg_mesh* mesh, int level, int space, double* v, hhg
  * epsilon_apply: y = (M P_v) A(eta) u.  form HHG_VISC_FULL = the paper's A
  *   (P:277-278 with eta on both terms, R1); HHG_VISC_EPS = int 2 eta eps:eps.
  * div_apply:  q = (B + C) u, grad ln rho = -gamma x/|x|; gamma 0 -> B.
- * divT_apply: y_u = (M P_v) B^T p   (accumulate != 0: y_u += ...).
+ * divT_apply: y_u = (M P_v) B^T p   (accumulate != 0: y_u += ..., y_u consistent).
  * stokes_apply: y_u = (M P_v)(A u + B^T p), y_p = (B + C) u.
  * hhg_diag: diag(A(eta)) WITHOUT P_v, consistent, all dofs. */
 int epsilon_apply(const hhg_mesh* mesh, int level, int form, const double* eta_p1, const double* u,
@@ -270,7 +270,9 @@ int hhg_mg_destroy(hhg_mg* mg);
  * right-preconditioned by the symmetric Uzawa block preconditioner (eq:SymmetricUzawaStep1,
  * P:427-437, B -> B+C in the pressure update) with A^-1 = V-cycle-preconditioned CG to tol_A
  * (hhg_ablock_cg on the hierarchy `mg`) and S^-1 = M_{1/eta}^-1 by Jacobi-CG to tol_mass
- * (eq:schurMass).  The V-cycle BFBT Schur approximation (eq:schurV) is NOT built yet.
+ * (eq:schurMass) or S^-1 = the V-cycle BFBT of eq:schurV (A_C = the cheap
+ * hierarchy mg_cheap, e.g. V(1,1) with degree-1 Chebyshev; B A_C^-1 B^T inverted by CG
+ * preconditioned by M_{1/eta} to tol_vbfbt).
  * Vectors: [u (P2VEC) | p (P1)] contiguous, device, on the hierarchy's finest level.  Stops at
  * |r| <= tol |P rhs| (2-norm over unique dofs) or max_iters.  Synchronises (host Arnoldi). */
 typedef struct {
@@ -281,10 +283,13 @@ typedef struct {
   int ablock_max_iters;
   double tol_mass;             /* M_{1/eta} CG relative tolerance (Table 1: 1e-10) */
   int mass_max_iters;
+  int schur;                   /* 0: S = M_{1/eta} (eq:schurMass); 1: V-cycle BFBT (eq:schurV) */
+  double tol_vbfbt;            /* CG tolerance for B A_C^-1 B^T (Table 1: 1e-1), M_{1/eta}-preconditioned */
+  int vbfbt_max_iters;
 } hhg_stokes_params;
 typedef struct hhg_stokes hhg_stokes;
-int hhg_stokes_create(hhg_mg* mg, const double* eta_p1, double gamma, const hhg_stokes_params* params,
-                      hhg_stokes** out);
+int hhg_stokes_create(hhg_mg* mg, hhg_mg* mg_cheap /*NULL unless schur = 1*/, const double* eta_p1, double gamma,
+                      const hhg_stokes_params* params, hhg_stokes** out);
 int hhg_stokes_solve(hhg_stokes* solver, const double* rhs, double* x, int* iters, double* rel_res,
                      hhg_stream_t stream);
 int hhg_stokes_destroy(hhg_stokes* solver);

@@ -51,8 +51,14 @@ def mass_cg(M, r, tol=1e-10, max_iters=500):
 
 
 class StokesOracle:
+    """schur="mass": S^-1 = M_{1/eta}^-1 (eq:schurMass); schur="vbfbt": the V-cycle BFBT of eq:schurV
+    (P:483-489), S_V^-1 = (B A_C^-1 B^T)^-1 (B A_C^-1 A A_C^-1 B^T) (B A_C^-1 B^T)^-1 with A_C^-1 one
+    V-cycle of the cheap hierarchy HC and (B A_C^-1 B^T)^-1 by M_{1/eta}-preconditioned CG to tol_vbfbt."""
+
     def __init__(self, H: Hierarchy, disc, Mmass, sigma=1.0, omega=0.3, tol_A=1e-2, ablock_max_iters=200,
-                 tol_mass=1e-10, mass_max_iters=500):
+                 tol_mass=1e-10, mass_max_iters=500, schur="mass", HC: Hierarchy = None, tol_vbfbt=1e-1,
+                 vbfbt_max_iters=100):
+        self.schur, self.HC, self.tol_vbfbt, self.vbfbt_max_iters = schur, HC, tol_vbfbt, vbfbt_max_iters
         self.H, self.d = H, disc
         self.A = H.Ac[H.lmax]
         self.Pm = disc.Pm
@@ -69,11 +75,47 @@ class StokesOracle:
         yp = mean0(self.Bbar @ (self.Pm @ u))
         return np.concatenate([yu, yp])
 
+    def bacbt(self, y):
+        """P_p B A_C^-1 B^T y (B, not B + C: the Schur complement of the symmetric system)."""
+        return mean0(self.B @ (self.Pm @ self.HC.vcycle(self.Pm @ (self.B.T @ y))))
+
+    def bacbt_solve(self, t):
+        """CG for (B A_C^-1 B^T) y = t, preconditioned by M_{1/eta}^-1 (mass CG), to tol_vbfbt."""
+        y = np.zeros_like(t)
+        r = t.copy()
+        r0 = float(np.linalg.norm(r))
+        if not r0 > 0:
+            return y
+        z = mean0(mass_cg(self.M, r, self.tol_mass, self.mass_max_iters))
+        p = z.copy()
+        rz = float(r @ z)
+        for _ in range(self.vbfbt_max_iters):
+            q = self.bacbt(p)
+            pq = float(p @ q)
+            alpha = rz / pq if pq != 0.0 else 0.0
+            y = y + alpha * p
+            r = r - alpha * q
+            if float(np.linalg.norm(r)) <= self.tol_vbfbt * r0:
+                break
+            z = mean0(mass_cg(self.M, r, self.tol_mass, self.mass_max_iters))
+            rzn = float(r @ z)
+            p = z + (rzn / rz) * p
+            rz = rzn
+        return mean0(y)
+
+    def vbfbt(self, t):
+        y1 = self.bacbt_solve(t)
+        w = self.HC.vcycle(self.Pm @ (self.B.T @ y1))
+        w = self.HC.vcycle(self.A @ w)
+        y2 = mean0(self.B @ (self.Pm @ w))
+        return self.bacbt_solve(y2)
+
     def prec(self, r):
         ru, rp = r[:self.n2], r[self.n2:]
         uh = self.sigma * ablock_cg(self.H, ru, self.tol_A, self.ablock_max_iters)[0]
         tp = mean0(rp - self.Bbar @ (self.Pm @ uh))
-        p = mean0(-self.omega * mass_cg(self.M, tp, self.tol_mass, self.mass_max_iters))
+        sinv = self.vbfbt(tp) if self.schur == "vbfbt" else mass_cg(self.M, tp, self.tol_mass, self.mass_max_iters)
+        p = mean0(-self.omega * sinv)
         tu = ru - (self.A @ uh + self.Pm @ (self.B.T @ p))
         u = uh + self.sigma * ablock_cg(self.H, tu, self.tol_A, self.ablock_max_iters)[0]
         return np.concatenate([u, p])

@@ -81,7 +81,7 @@ def _load():
         "hhg_interface_sum_remote": ([P, I, I, P, P, P], I), "epsilon_apply_partial": ([P, I, I, P, P, P, P], I),
         "hhg_ablock_cg": ([P, P, P, D, I, P, P, P], I),
         "hhg_mass_apply": ([P, I, P, P, P, P], I), "hhg_mass_diag": ([P, I, P, P, P], I),
-        "hhg_stokes_create": ([P, P, D, P, P], I), "hhg_stokes_solve": ([P, P, P, P, P, P], I),
+        "hhg_stokes_create": ([P, P, P, D, P, P], I), "hhg_stokes_solve": ([P, P, P, P, P, P], I),
         "hhg_stokes_destroy": ([P], I),
     }
     for name, (args, res) in sig.items():
@@ -482,7 +482,8 @@ class MG:
 class _StokesParams(ctypes.Structure):
     _fields_ = [("restart", ctypes.c_int), ("max_iters", ctypes.c_int), ("tol", ctypes.c_double),
                 ("sigma", ctypes.c_double), ("omega", ctypes.c_double), ("tol_A", ctypes.c_double),
-                ("ablock_max_iters", ctypes.c_int), ("tol_mass", ctypes.c_double), ("mass_max_iters", ctypes.c_int)]
+                ("ablock_max_iters", ctypes.c_int), ("tol_mass", ctypes.c_double), ("mass_max_iters", ctypes.c_int),
+                ("schur", ctypes.c_int), ("tol_vbfbt", ctypes.c_double), ("vbfbt_max_iters", ctypes.c_int)]
 
 
 class StokesSolver:
@@ -490,12 +491,17 @@ class StokesSolver:
     CG) on the finest level of `mg`.  Vectors are [u (P2VEC) | p (P1)] concatenated."""
 
     def __init__(self, mg, eta, gamma, restart=30, max_iters=100, tol=1e-8, sigma=1.0, omega=0.3, tol_A=1e-2,
-                 ablock_max_iters=200, tol_mass=1e-10, mass_max_iters=500):
-        self.mg = mg
+                 ablock_max_iters=200, tol_mass=1e-10, mass_max_iters=500, schur="mass", mg_cheap=None,
+                 tol_vbfbt=1e-1, vbfbt_max_iters=100):
+        """schur: "mass" (S = M_{1/eta}, eq:schurMass) or "vbfbt" (eq:schurV; mg_cheap = the A_C hierarchy,
+        Table 1: V(1,1) with degree-1 Chebyshev)."""
+        self.mg, self.mg_cheap = mg, mg_cheap
         self._eta = eta
-        prm = _StokesParams(restart, max_iters, tol, sigma, omega, tol_A, ablock_max_iters, tol_mass, mass_max_iters)
+        prm = _StokesParams(restart, max_iters, tol, sigma, omega, tol_A, ablock_max_iters, tol_mass, mass_max_iters,
+                            1 if schur == "vbfbt" else 0, tol_vbfbt, vbfbt_max_iters)
         h = ctypes.c_void_p()
-        _chk(_lib.hhg_stokes_create(mg.handle, _ptr(eta), float(gamma), ctypes.byref(prm), ctypes.byref(h)))
+        _chk(_lib.hhg_stokes_create(mg.handle, None if mg_cheap is None else mg_cheap.handle, _ptr(eta), float(gamma),
+                                    ctypes.byref(prm), ctypes.byref(h)))
         self.handle = h
         L = mg.l_max
         self.n2, self.n1 = mg.mesh.vec_len(L, HHG_P2VEC), mg.mesh.vec_len(L, HHG_P1)

@@ -366,9 +366,13 @@ int divT_apply(const hhg_mesh* mesh, int level, const double* p, double* y_u, in
   HHG_TRY(ensure_level(m, level));
   cudaStream_t s = (cudaStream_t)stream;
   if (!accumulate) return apply_op(m, level, ELEM_BT, HHG_VISC_FULL, nullptr, 0.0, nullptr, p, y_u, nullptr, false, s);
-  // y_u += B^T p  (y_u consistent): compute into y_u after scaling non-owner copies away is
-  // not possible in place, so go through the interface-sum of the partial result only.
-  return fail(HHG_EINVAL, "divT_apply(accumulate=1) not supported in this build");
+  // y_u += (M P_v) B^T p: into the level's scratch vector (allocated on first use), then added
+  Level& L = m->levels[level];
+  const int64_t n = 3 * macro_count(m) * L.npts2;
+  if (!L.scratch_u && cudaMalloc(&L.scratch_u, n * sizeof(double)) != cudaSuccess)
+    return fail(HHG_ENOMEM, "divT_apply scratch");
+  HHG_TRY(apply_op(m, level, ELEM_BT, HHG_VISC_FULL, nullptr, 0.0, nullptr, p, L.scratch_u, nullptr, false, s));
+  return launch_axpby(n, 1.0, L.scratch_u, 1.0, y_u, s);
 }
 
 int stokes_apply(const hhg_mesh* mesh, int level, const double* eta_p1, double gamma, const double* u,

@@ -99,6 +99,7 @@ struct Level {
   int64_t* canon2 = nullptr;
   int64_t ncanon1 = 0, ncanon2 = 0;
   double* red = nullptr;            // reduction scratch [kRedBlocks + 8]
+  double* scratch_u = nullptr;      // P2VEC scratch (divT_apply accumulate), allocated on first use
   bool built = false;
 };
 

@@ -82,6 +82,7 @@ void free_level(Level& L) {
   f(L.canon1);
   f(L.canon2);
   f(L.red);
+  f(L.scratch_u);
   int lv = L.level;
   L = Level();
   L.level = lv;

@@ -537,6 +537,7 @@ int hhg_power_iteration(const hhg_mesh* mesh, int level, const double* eta_p1, c
 // Block vectors are [u (P2VEC) | p (P1)] in one allocation.
 struct hhg_stokes {
   hhg_mg* mg = nullptr;
+  hhg_mg* mgC = nullptr;     // cheap V-cycle A_C of the V-cycle BFBT (m_V = 1, deg_V = 1), may be NULL
   hhg_mesh* mesh = nullptr;
   int level = 0;
   const double* eta = nullptr;
@@ -546,11 +547,13 @@ struct hhg_stokes {
   std::vector<double*> V, Z;
   double *w = nullptr, *t = nullptr, *a = nullptr, *b = nullptr, *ones = nullptr, *mdinv = nullptr, *sc = nullptr;
   double *mr = nullptr, *mz = nullptr, *mp = nullptr, *mq = nullptr;
+  double *br = nullptr, *bz = nullptr, *bp = nullptr, *bq = nullptr, *bt = nullptr;  // BFBT CG (P1)
+  double *bu = nullptr, *bv = nullptr;                                                 // BFBT velocity temps
   double n_unique_p = 0.0;
   ~hhg_stokes() {
     for (double* p : V) cudaFree(p);
     for (double* p : Z) cudaFree(p);
-    for (double* p : {w, t, a, b, ones, mdinv, sc, mr, mz, mp, mq})
+    for (double* p : {w, t, a, b, ones, mdinv, sc, mr, mz, mp, mq, br, bz, bp, bq, bt, bu, bv})
       if (p) cudaFree(p);
   }
 };
@@ -621,6 +624,65 @@ int st_mass_solve(hhg_stokes* S, const double* rp, double* zp, cudaStream_t s) {
   }
   return HHG_OK;
 }
+// w = P_p B A_C^-1 B^T y  (A_C^-1 = one cheap V-cycle, eq:schurV)
+int st_bacbt(hhg_stokes* S, const double* y, double* w, cudaStream_t s) {
+  HHG_TRY(divT_apply(S->mesh, S->level, y, S->bu, 0, (hhg_stream_t)s));
+  HHG_TRY(vcycle(S->mgC, S->bu, S->bv, (hhg_stream_t)s));
+  HHG_TRY(div_apply(S->mesh, S->level, 0.0, S->bv, w, (hhg_stream_t)s));
+  return st_mean0(S, w, s);
+}
+// y = (B A_C^-1 B^T)^-1 t by CG preconditioned by M_{1/eta} (mass CG to tol_mass), to tol_vbfbt
+int st_bacbt_solve(hhg_stokes* S, const double* t, double* y, cudaStream_t s) {
+  const int64_t n = S->n1;
+  const Level& L = S->mesh->levels[S->level];
+  auto pdot = [&](const double* x, const double* v, double* out) -> int {
+    HHG_TRY(launch_dot(S->mesh, L, HHG_P1, x, v, S->sc + 5, s));
+    HHG_CUDA(cudaMemcpyAsync(out, S->sc + 5, sizeof(double), cudaMemcpyDeviceToHost, s));
+    HHG_CUDA(cudaStreamSynchronize(s));
+    return HHG_OK;
+  };
+  HHG_CUDA(cudaMemsetAsync(y, 0, n * sizeof(double), s));
+  HHG_CUDA(cudaMemcpyAsync(S->br, t, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  double r0 = 0.0;
+  HHG_TRY(pdot(S->br, S->br, &r0));
+  r0 = std::sqrt(r0);
+  if (!(r0 > 0)) return HHG_OK;
+  HHG_TRY(st_mass_solve(S, S->br, S->bz, s));
+  HHG_TRY(st_mean0(S, S->bz, s));
+  HHG_CUDA(cudaMemcpyAsync(S->bp, S->bz, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  double rz = 0.0;
+  HHG_TRY(pdot(S->br, S->bz, &rz));
+  for (int it = 0; it < S->prm.vbfbt_max_iters; ++it) {
+    HHG_TRY(st_bacbt(S, S->bp, S->bq, s));
+    double pq = 0.0;
+    HHG_TRY(pdot(S->bp, S->bq, &pq));
+    const double alpha = pq != 0.0 ? rz / pq : 0.0;
+    HHG_TRY(launch_axpby(n, alpha, S->bp, 1.0, y, s));
+    HHG_TRY(launch_axpby(n, -alpha, S->bq, 1.0, S->br, s));
+    double rr = 0.0;
+    HHG_TRY(pdot(S->br, S->br, &rr));
+    if (std::sqrt(std::max(rr, 0.0)) <= S->prm.tol_vbfbt * r0) break;
+    HHG_TRY(st_mass_solve(S, S->br, S->bz, s));
+    HHG_TRY(st_mean0(S, S->bz, s));
+    double rzn = 0.0;
+    HHG_TRY(pdot(S->br, S->bz, &rzn));
+    HHG_TRY(launch_axpby(n, 1.0, S->bz, rzn / rz, S->bp, s));
+    rz = rzn;
+  }
+  return st_mean0(S, y, s);
+}
+// z_p = S_V^-1 t (eq:schurV): (B A_C^-1 B^T)^-1 (B A_C^-1 A A_C^-1 B^T) (B A_C^-1 B^T)^-1 t
+int st_vbfbt(hhg_stokes* S, const double* t, double* z, cudaStream_t s) {
+  HHG_TRY(st_bacbt_solve(S, t, S->bt, s));
+  HHG_TRY(divT_apply(S->mesh, S->level, S->bt, S->bu, 0, (hhg_stream_t)s));
+  HHG_TRY(vcycle(S->mgC, S->bu, S->bv, (hhg_stream_t)s));
+  HHG_TRY(epsilon_apply(S->mesh, S->level, HHG_VISC_FULL, S->eta, S->bv, S->bu, (hhg_stream_t)s));
+  HHG_TRY(vcycle(S->mgC, S->bu, S->bv, (hhg_stream_t)s));
+  HHG_TRY(div_apply(S->mesh, S->level, 0.0, S->bv, S->bt, (hhg_stream_t)s));
+  HHG_TRY(st_mean0(S, S->bt, s));
+  return st_bacbt_solve(S, S->bt, z, s);
+}
+
 // z = Prec(r): one symmetric Uzawa step from (0, 0)
 int st_prec(hhg_stokes* S, const double* r, double* z, cudaStream_t s) {
   const int64_t n2 = S->n2, n1 = S->n1;
@@ -634,7 +696,8 @@ int st_prec(hhg_stokes* S, const double* r, double* z, cudaStream_t s) {
   HHG_TRY(div_apply(S->mesh, S->level, S->gamma, z, S->t + n2, (hhg_stream_t)s));
   HHG_TRY(launch_axpby(n1, 1.0, r + n2, -1.0, S->t + n2, s));
   HHG_TRY(st_mean0(S, S->t + n2, s));
-  HHG_TRY(st_mass_solve(S, S->t + n2, z + n2, s));
+  if (S->prm.schur == 1) HHG_TRY(st_vbfbt(S, S->t + n2, z + n2, s));
+  else HHG_TRY(st_mass_solve(S, S->t + n2, z + n2, s));
   HHG_TRY(launch_axpby(n1, 0.0, z + n2, -om, z + n2, s));
   HHG_TRY(st_mean0(S, z + n2, s));
   // t_u = r_u - A u_hat - B^T p ; u = u_hat + sigma A^-1 t_u
@@ -647,13 +710,18 @@ int st_prec(hhg_stokes* S, const double* r, double* z, cudaStream_t s) {
 
 extern "C" {
 
-int hhg_stokes_create(hhg_mg* mg, const double* eta_p1, double gamma, const hhg_stokes_params* prm,
+int hhg_stokes_create(hhg_mg* mg, hhg_mg* mg_cheap, const double* eta_p1, double gamma, const hhg_stokes_params* prm,
                       hhg_stokes** out) {
   if (!mg || !prm || !out) return fail(HHG_EINVAL, "hhg_stokes_create: NULL argument");
   if (prm->restart < 1 || prm->max_iters < 1 || !(prm->tol > 0) || !(prm->tol_A > 0) || !(prm->tol_mass > 0))
     return fail(HHG_EINVAL, "hhg_stokes_create: bad parameters");
+  if (prm->schur != 0 && prm->schur != 1) return fail(HHG_EINVAL, "hhg_stokes_create: schur must be 0 (mass) or 1 (V-BFBT)");
+  if (prm->schur == 1 && (!mg_cheap || mg_cheap->mesh != mg->mesh || mg_cheap->prm.l_max != mg->prm.l_max ||
+                          !(prm->tol_vbfbt > 0) || prm->vbfbt_max_iters < 1))
+    return fail(HHG_EINVAL, "hhg_stokes_create: V-BFBT needs a cheap hierarchy on the same mesh/levels and tol_vbfbt");
   auto* S = new hhg_stokes();
   S->mg = mg;
+  S->mgC = mg_cheap;
   S->mesh = mg->mesh;
   S->level = mg->prm.l_max;
   S->eta = eta_p1;
@@ -670,7 +738,9 @@ int hhg_stokes_create(hhg_mg* mg, const double* eta_p1, double gamma, const hhg_
   for (auto& p : S->V) ok = ok && alloc(&p, nb);
   for (auto& p : S->Z) ok = ok && alloc(&p, nb);
   for (double** p : {&S->w, &S->t, &S->a, &S->b}) ok = ok && alloc(p, nb);
-  for (double** p : {&S->ones, &S->mdinv, &S->mr, &S->mz, &S->mp, &S->mq}) ok = ok && alloc(p, S->n1);
+  for (double** p : {&S->ones, &S->mdinv, &S->mr, &S->mz, &S->mp, &S->mq, &S->br, &S->bz, &S->bp, &S->bq, &S->bt})
+    ok = ok && alloc(p, S->n1);
+  for (double** p : {&S->bu, &S->bv}) ok = ok && alloc(p, S->n2);
   ok = ok && alloc(&S->sc, 8);
   if (!ok) {
     delete S;

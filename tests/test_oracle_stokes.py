@@ -57,3 +57,21 @@ def test_fgmres_uzawa_recovers_a_manufactured_solution(tet_case):
     # a loose tolerance stops earlier and still meets it
     x2, it2, rel2 = S.solve(rhs, tol=1e-3, restart=40, max_iters=200)
     assert rel2 <= 1e-3 and it2 < it
+
+
+def test_fgmres_uzawa_vbfbt_recovers_a_manufactured_solution(tet_case):
+    """Same manufactured solve with the V-cycle BFBT Schur approximation (eq:schurV, A_C = V(1,1) with
+    degree-1 Chebyshev, B A_C^-1 B^T by M_{1/eta}-preconditioned CG to 0.1)."""
+    discs, H = tet_case
+    d = discs[2]
+    v0 = {L: uniform_vec(discs[L].lm.p2_keys, 6) for L in (1, 2)}
+    HC = Hierarchy(discs, v0, pre=1, post=1, degree=1)
+    S = StokesOracle(H, d, d.M, tol_A=1e-2, schur="vbfbt", HC=HC, tol_vbfbt=1e-1)
+    n2 = 3 * d.lm.n_p2
+    xs = np.concatenate([d.project(uniform_vec(d.lm.p2_keys, 2)), uniform_from_keys(d.lm.p1_keys, 3, 0)])
+    xs[n2:] -= xs[n2:].mean()
+    rhs = S.op(xs)
+    x, it, rel = S.solve(rhs, tol=1e-10, restart=60, max_iters=200)
+    assert rel <= 1e-10
+    assert np.linalg.norm(x[:n2] - xs[:n2]) <= 1e-8 * np.linalg.norm(xs[:n2])
+    assert np.linalg.norm(S.op(x - xs)) <= 1e-9 * np.linalg.norm(rhs)
