@@ -197,6 +197,10 @@ int hhg_diag(const hhg_mesh* mesh, int level, const double* eta_p1, double* diag
 int hhg_mass_apply(const hhg_mesh* mesh, int level, const double* eta_p1, const double* p, double* y,
                    hhg_stream_t stream);
 int hhg_mass_diag(const hhg_mesh* mesh, int level, const double* eta_p1, double* diag, hhg_stream_t stream);
+/* hhg_buoyancy_load: f = (M P_v) b, b_i = int (T - 1/2) (x/|x|) . phi_i  -- the buoyancy right-hand
+ * side of config 4 (P:282 with rho' = -alpha (T - 1/2), alpha = 1, gravity g = -x/|x|; DESIGN.md
+ * R21).  T_p1: consistent P1 temperature at the level's vertices; f: P2VEC, consistent. */
+int hhg_buoyancy_load(const hhg_mesh* mesh, int level, const double* T_p1, double* f, hhg_stream_t stream);
 /* epsilon_apply_partial: the element half of epsilon_apply only -- per-copy partial sums of
  * A(eta) u, NO interface sum and NO BC (first phase of a split-phase exchange). */
 int epsilon_apply_partial(const hhg_mesh* mesh, int level, int form, const double* eta_p1, const double* u,

@@ -192,6 +192,25 @@ class Discretisation:
         return m
 
 
+def buoyancy_load(lm: LevelMesh, blended: bool, T_p1, chunk=20000) -> np.ndarray:
+    """Config-4 buoyancy right-hand side (P:282 with rho' = -alpha (T - 1/2), alpha = 1, g = -x/|x|;
+    DESIGN.md R21): b_(a,c) = sum_K sum_q w_q |det J| (T_q - 1/2) (x_q/|x_q|)_c phi_a(xi_q), T the P1
+    interpolant of the nodal temperature.  Unconstrained (apply Pm for the constrained rhs)."""
+    xi, _ = fe.q4_rule()
+    lam = fe.p1_basis(xi)
+    phi = fe.p2_basis(xi)                                   # (Q,10)
+    bp = macro_blend(lm) if blended else None
+    b = np.zeros(3 * lm.n_p2)
+    for s in range(0, lm.n_tets, chunk):
+        tets = np.arange(s, min(s + chunk, lm.n_tets))
+        W, _, xq = quad_geometry(lm, tets, blended, bp)
+        Tq = np.asarray(T_p1)[lm.tet_p1[tets]] @ lam.T      # (T,Q)
+        dq = xq / np.linalg.norm(xq, axis=2, keepdims=True)
+        Be = np.einsum("tq,qa,tqc->tac", W * (Tq - 0.5), phi, dq).reshape(len(tets), 30)
+        np.add.at(b, p2vec_dofs(lm.tet_p2[tets]).ravel(), Be.ravel())
+    return b
+
+
 def node_coords(lm: LevelMesh, space: str, blended: bool) -> np.ndarray:
     """Physical (blended) coordinates of the canonical nodes: B(x~) evaluated with the blending
     parameters of one macro containing the node (B is C^0 across macros)."""

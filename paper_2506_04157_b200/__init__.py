@@ -41,7 +41,7 @@ EXPORTS = [
     "hhg_mesh_create_part", "hhg_partition_rcb", "hhg_mesh_rank", "hhg_halo_info", "hhg_halo_keys",
     "hhg_owned_count", "hhg_halo_pack", "hhg_interface_sum_remote", "epsilon_apply_partial",
     "hhg_ablock_cg", "hhg_mass_apply", "hhg_mass_diag", "hhg_stokes_create", "hhg_stokes_solve",
-    "hhg_stokes_destroy",
+    "hhg_stokes_destroy", "hhg_buoyancy_load",
 ]
 
 
@@ -82,7 +82,7 @@ def _load():
         "hhg_ablock_cg": ([P, P, P, D, I, P, P, P], I),
         "hhg_mass_apply": ([P, I, P, P, P, P], I), "hhg_mass_diag": ([P, I, P, P, P], I),
         "hhg_stokes_create": ([P, P, P, D, P, P], I), "hhg_stokes_solve": ([P, P, P, P, P, P], I),
-        "hhg_stokes_destroy": ([P], I),
+        "hhg_stokes_destroy": ([P], I), "hhg_buoyancy_load": ([P, I, P, P, P], I),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -336,6 +336,14 @@ def hhg_mass_apply(mesh, level, eta, p, y=None, stream=None):
     _chk(_lib.hhg_mass_apply(mesh.handle, level, _dev(eta, n1, "eta"), _dev(p, n1, "p"), _dev(y, n1, "y"),
                              _stream(stream)))
     return y
+
+
+def hhg_buoyancy_load(mesh, level, T, f=None, stream=None):
+    """f = (M P_v) int (T - 1/2)(x/|x|) . phi  (config-4 buoyancy rhs), T a consistent P1 temperature."""
+    f = mesh.zeros(level, HHG_P2VEC) if f is None else f
+    _chk(_lib.hhg_buoyancy_load(mesh.handle, level, _dev(T, mesh.vec_len(level, HHG_P1), "T"),
+                                _dev(f, mesh.vec_len(level, HHG_P2VEC), "f"), _stream(stream)))
+    return f
 
 
 def hhg_mass_diag(mesh, level, eta, out=None, stream=None):

@@ -301,7 +301,7 @@ int apply_op(const Mesh* m, int level, int mode, int form, const double* eta, do
              const double* p, double* yu, double* yp, bool accumulate_u, cudaStream_t s) {
   const Level& L = m->levels[level];
   const int64_t nm = macro_count(m);
-  const bool has_u = (mode & (ELEM_A | ELEM_BT | ELEM_DIAG)) != 0;
+  const bool has_u = elem_u_out(mode);
   const bool has_p = elem_p_out(mode);
   if (has_u && !accumulate_u) HHG_CUDA(cudaMemsetAsync(yu, 0, 3 * nm * L.npts2 * sizeof(double), s));
   if (has_p) HHG_CUDA(cudaMemsetAsync(yp, 0, nm * L.npts1 * sizeof(double), s));
@@ -337,6 +337,15 @@ int hhg_mass_apply(const hhg_mesh* mesh, int level, const double* eta_p1, const 
   auto* m = const_cast<hhg_mesh*>(mesh);
   HHG_TRY(ensure_level(m, level));
   return apply_op(m, level, ELEM_MASS, HHG_VISC_FULL, eta_p1, 0.0, nullptr, p, nullptr, y, false, (cudaStream_t)stream);
+}
+
+int hhg_buoyancy_load(const hhg_mesh* mesh, int level, const double* T_p1, double* f, hhg_stream_t stream) {
+  HHG_TRY(check_level(mesh, level));
+  CHECK_PTR(T_p1);
+  CHECK_PTR(f);
+  auto* m = const_cast<hhg_mesh*>(mesh);
+  HHG_TRY(ensure_level(m, level));
+  return apply_op(m, level, ELEM_LOAD, HHG_VISC_FULL, nullptr, 0.0, nullptr, T_p1, f, nullptr, false, (cudaStream_t)stream);
 }
 
 int hhg_mass_diag(const hhg_mesh* mesh, int level, const double* eta_p1, double* diag, hhg_stream_t stream) {

@@ -185,6 +185,37 @@ __device__ __forceinline__ void tet_body(const double* G, double wdet, const dou
     }
   }
 
+  if (MODE & ELEM_LOAD) {
+    // buoyancy load (P:282 with rho' = -alpha (T - 1/2), alpha = 1, g = -x/|x|; R21):
+    // f_a,c = sum_q w |det J_F| |det J_B| (T_q - 1/2) (x_q/|x_q|)_c phi_a(q), T P1-interpolated (pp)
+#pragma unroll
+    for (int a = 0; a < 10; ++a)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) acc[a][c] = 0.0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      double xq[3];
+#pragma unroll
+      for (int r = 0; r < 3; ++r) xq[r] = xa[r] + G[9 + 3 * q + r];
+      const double ri = rsqrt_nr(fma(xq[0], xq[0], fma(xq[1], xq[1], xq[2] * xq[2])));
+      const double cq = cK * al[q];
+      const double sq = wdet * cq * cq * cq * (fma(EQAB, pp[q], pS) - 0.5) * ri;
+      constexpr double phv = EQB * (2.0 * EQB - 1.0), phq = EQA * (2.0 * EQA - 1.0);
+      constexpr double peq = 4.0 * EQA * EQB, pen = 4.0 * EQB * EQB;
+#pragma unroll
+      for (int a = 0; a < 10; ++a) {
+        double phi;
+        if (a < 4) phi = (a == q) ? phq : phv;
+        else {
+          constexpr int ep[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
+          phi = (ep[a - 4][0] == q || ep[a - 4][1] == q) ? peq : pen;
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) acc[a][c] = fma(sq * phi, xq[c], acc[a][c]);
+      }
+    }
+    return;
+  }
   if (MODE & (ELEM_MASS | ELEM_MASSD)) {
     // pressure mass weighted by 1/eta (Schur approximation M_{1/eta}, eq:schurMass P:457-461):
     // M_vw = sum_q w |det J_F| |det J_B| / eta_q  lambda_v(q) lambda_w(q),  |det J_B| = (c alpha)^3
@@ -378,7 +409,7 @@ __device__ __forceinline__ void load_tet(int t, const int* rs2, const int* rs1, 
                                          double (&pp)[4]) {
   constexpr bool NEED_U = (MODE & (ELEM_A | ELEM_DIV)) != 0;
   constexpr bool NEED_ETA = (MODE & (ELEM_A | ELEM_DIAG)) != 0;
-  constexpr bool NEED_P = (MODE & ELEM_BT) != 0;
+  constexpr bool NEED_P = (MODE & (ELEM_BT | ELEM_LOAD)) != 0;
   if (NEED_U) {
 #pragma unroll
     for (int a = 0; a < 10; ++a) {
@@ -407,7 +438,7 @@ __global__ void __launch_bounds__(kBT, HHG_ELEM_MINB)
                  const double* __restrict__ u, const double* __restrict__ p, double* __restrict__ yu,
                  double* __restrict__ yp, double gamma) {
   constexpr bool DO_DIV = (MODE & ELEM_DIV) != 0;
-  constexpr bool HAS_U_OUT = (MODE & (ELEM_A | ELEM_BT | ELEM_DIAG)) != 0;
+  constexpr bool HAS_U_OUT = elem_u_out(MODE);
   constexpr int NSU = HAS_U_OUT ? kNS2 : 0;
   constexpr int NS = NSU + (DO_DIV ? kNS1 : 0);
   extern __shared__ double sm[];  // [NS][kBT] cube slots | geometry [kGeoSm] | row starts int[13][kBT]
@@ -664,8 +695,8 @@ struct FootU {
 
 template <int MODE>
 __host__ __device__ constexpr int fp_smem_words() {
-  return ((MODE & (ELEM_A | ELEM_DIV)) ? 3 * kFU : 0) + ((MODE & (ELEM_A | ELEM_BT | ELEM_DIAG)) ? 2 * 3 * kFY : 0) +
-         kF1 + ((MODE & (ELEM_BT | ELEM_MASS)) ? kF1 : 0) + (elem_p_out(MODE) ? 2 * kF1Y : 0) + kGeoSm;
+  return ((MODE & (ELEM_A | ELEM_DIV)) ? 3 * kFU : 0) + (elem_u_out(MODE) ? 2 * 3 * kFY : 0) +
+         kF1 + ((MODE & (ELEM_BT | ELEM_MASS | ELEM_LOAD)) ? kF1 : 0) + (elem_p_out(MODE) ? 2 * kF1Y : 0) + kGeoSm;
 }
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
@@ -685,9 +716,9 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
               double* __restrict__ yp, double gamma) {
   constexpr bool DO_DIV = (MODE & ELEM_DIV) != 0;
   constexpr bool NEED_U = (MODE & (ELEM_A | ELEM_DIV)) != 0;
-  constexpr bool NEED_P = (MODE & (ELEM_BT | ELEM_MASS)) != 0;
+  constexpr bool NEED_P = (MODE & (ELEM_BT | ELEM_MASS | ELEM_LOAD)) != 0;
   constexpr bool HAS_P_OUT = elem_p_out(MODE);
-  constexpr bool HAS_U_OUT = (MODE & (ELEM_A | ELEM_BT | ELEM_DIAG)) != 0;
+  constexpr bool HAS_U_OUT = elem_u_out(MODE);
   extern __shared__ double sm[];
   double* su = sm;                                   // [3][kFU]
   double* sy = su + (NEED_U ? 3 * kFU : 0);          // [2 warps][3][kFY]
@@ -1189,7 +1220,7 @@ static void elem_launch(const Mesh* m, const Level& L, const double* eta, double
                         const double* p, double* yu, double* yp, cudaStream_t s) {
   const int64_t nm = macro_count(m);
 #ifdef HHG_ELEM_V5
-  if (MODE & (ELEM_MASS | ELEM_MASSD))
+  if (MODE & (ELEM_MASS | ELEM_MASSD | ELEM_LOAD))
 #endif
   {
     constexpr size_t smem = fp_smem_words<MODE>() * sizeof(double);
@@ -1205,7 +1236,7 @@ static void elem_launch(const Mesh* m, const Level& L, const double* eta, double
                                                          L.npts2, nm * L.npts2, eta, u, p, yu, yp, gamma);
     return;
   }
-  constexpr int NS = ((MODE & (ELEM_A | ELEM_BT | ELEM_DIAG)) ? kNS2 : 0) + ((MODE & ELEM_DIV) ? kNS1 : 0);
+  constexpr int NS = (elem_u_out(MODE) ? kNS2 : 0) + ((MODE & ELEM_DIV) ? kNS1 : 0);
 #ifdef HHG_GEO_GLOBAL
   constexpr size_t smem = (NS * kBT) * sizeof(double) + 13 * kBT * sizeof(int);
 #else
@@ -1244,6 +1275,7 @@ int launch_elem(const Mesh* m, const Level& L, int mode, int form, const double*
     case ELEM_DIAG: HHG_DISPATCH(ELEM_DIAG); break;
     case ELEM_MASS: HHG_DISPATCH(ELEM_MASS); break;
     case ELEM_MASSD: HHG_DISPATCH(ELEM_MASSD); break;
+    case ELEM_LOAD: HHG_DISPATCH(ELEM_LOAD); break;
     default: return fail(HHG_EINVAL, "bad element mode");
   }
 #undef HHG_DISPATCH

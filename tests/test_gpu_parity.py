@@ -99,6 +99,21 @@ def test_pressure_mass_apply_and_diag(shell_l2):
     assert rel_l2(canon(M, 2, hhg.HHG_P1, dg), dm.M.diagonal()) <= TOL_APPLY
 
 
+def test_buoyancy_load(shell_l2):
+    """Config-4 buoyancy rhs (M P_v) int (T - 1/2)(x/|x|).phi on the blended shell L2, T = the
+    workload temperature at the P1 nodes."""
+    from oracle.operators import buoyancy_load, node_coords
+    from workload import temperature
+    from tests.harness import lib_coords_canonical
+    mac, lm, d, eta_o, M = shell_l2
+    T_o = temperature(node_coords(lm, "P1", True), lm.p1_keys)
+    f_o = d.project(buoyancy_load(lm, True, T_o))
+    keys = M.canonical_keys(2, hhg.HHG_P1)
+    T = M.from_canonical(2, hhg.HHG_P1, temperature(lib_coords_canonical(M, 2, hhg.HHG_P1), keys))
+    f = hhg.hhg_buoyancy_load(M, 2, T)
+    assert rel_l2(canon(M, 2, hhg.HHG_P2VEC, f), f_o) <= TOL_APPLY
+
+
 def test_shell_level2_diag_and_dot(shell_l2):
     mac, lm, d, eta_o, M = shell_l2
     eta = lib_eta(M, 2, C2)

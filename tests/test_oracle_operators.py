@@ -203,3 +203,28 @@ def test_pressure_mass_closed_forms():
     assert abs(d3.M - d.M / 3.0).max() < 1e-17
     assert abs(d.M - d.M.T).max() < 1e-18
     assert sla.eigsh(d.M, k=1, which="SA")[0][0] > 0
+
+
+def test_buoyancy_load_closed_forms():
+    """Config-4 buoyancy load: linear in (T - 1/2); T = 1/2 gives 0; a uniform T = 3/2 gives
+    b . e = int (x/|x|) . e over the domain for the constant field e (partition of unity of P2),
+    which for the blended shell and e = e_z vanishes by symmetry and for the radial test field
+    v = x (nodal interpolation) equals int |x| = pi (r1^4 - r0^4) up to the quadrature error."""
+    from oracle.refine import build_level
+    from oracle.operators import buoyancy_load, node_coords
+    from workload import icoshell
+    m = icoshell(3, 2)
+    lm = build_level(m.verts, m.tets, m.vtag, 2)
+    half = np.full(lm.n_p1, 0.5)
+    assert np.abs(buoyancy_load(lm, True, half)).max() == 0.0
+    b = buoyancy_load(lm, True, np.full(lm.n_p1, 1.5))
+    ez = np.zeros(3 * lm.n_p2)
+    ez[2::3] = 1.0
+    x2 = node_coords(lm, "P2", True).ravel()
+    radial = b @ x2
+    assert abs(radial - np.pi * (1.0 - 0.55 ** 4)) < 1e-4 * np.pi
+    assert abs(b @ ez) < 1e-5 * radial          # zero for the exact shell; discretisation-level here
+    rng = np.random.default_rng(0)
+    T1, T2 = rng.uniform(0, 1, lm.n_p1), rng.uniform(0, 1, lm.n_p1)
+    lin = buoyancy_load(lm, True, 2 * T1 - T2)
+    assert np.abs(lin - (2 * buoyancy_load(lm, True, T1) - buoyancy_load(lm, True, T2) - buoyancy_load(lm, True, half))).max() < 1e-14
