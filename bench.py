@@ -99,7 +99,7 @@ class ClockSampler:
 SHELL_BY_GPUS = {1: (3, 2), 2: (3, 3), 4: (5, 2), 8: (5, 3)}
 
 
-def build_case(level, device, world=1, rank=0, comm=None):
+def build_case(level, device, world=1, rank=0, comm=None, contrast=1e6, jump=30.0):
     """Library-side set-up of config 3 (mesh, eta per level, power start vectors, rhs).  world > 1:
     shell with 240*world macros partitioned by recursive coordinate bisection, one part per rank."""
     import torch
@@ -120,7 +120,7 @@ def build_case(level, device, world=1, rank=0, comm=None):
         keys1 = M.canonical_keys(L, hhg.HHG_P1)
         xyz = M.node_coords(L, hhg.HHG_P1)
         xc = torch.stack([M.to_canonical(L, hhg.HHG_P1, xyz[:, c].contiguous()) for c in range(3)], 1)
-        etas[L] = M.from_canonical(L, hhg.HHG_P1, viscosity(xc.cpu().numpy(), keys1, 1e6, 30.0))
+        etas[L] = M.from_canonical(L, hhg.HHG_P1, viscosity(xc.cpu().numpy(), keys1, contrast, jump))
         if L > 1:
             v0[L] = M.from_canonical(L, hhg.HHG_P2VEC, uniform_vec(M.canonical_keys(L, hhg.HHG_P2), 6))
     keysL = M.canonical_keys(level, hhg.HHG_P2)

@@ -1,0 +1,51 @@
+"""Config-4-style preconditioned Stokes solve on ONE GPU (the paper's config 4 is L6 on 8 GPUs):
+blended shell(3,2) at --level, contrast 1e6 x 30 viscosity, TALA compressibility, buoyancy rhs from
+the workload temperature, FGMRES + symmetric Uzawa with the V-cycle BFBT (or mass) Schur
+approximation, Table-1 parameters (sigma 1, omega 0.3, tol_A 1e-2, tol_V 1e-1, tol_mass 1e-10,
+V(3,3)/V(1,1) hierarchies with Chebyshev degree 2/1) and BASELINE's relative reduction 1e-8.
+Prints one JSON line (time, iterations, residual)."""
+import argparse, json, os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_2506_04157_b200 as hhg
+from bench import build_case, GAMMA
+from workload import temperature
+ap = argparse.ArgumentParser()
+ap.add_argument("--level", type=int, default=4)
+ap.add_argument("--schur", default="vbfbt", choices=["vbfbt", "mass"])
+ap.add_argument("--tol", type=float, default=1e-8)
+ap.add_argument("--max-iters", type=int, default=60)
+ap.add_argument("--restart", type=int, default=30)
+ap.add_argument("--deg", type=int, default=2, help="Chebyshev degree of the A-block V-cycle (Table 1: 2)")
+ap.add_argument("--contrast", type=float, default=1e6)
+ap.add_argument("--jump", type=float, default=30.0)
+a = ap.parse_args()
+L = a.level
+M, etas, v0, _, n_dof = build_case(L, 0, contrast=a.contrast, jump=a.jump)
+t0 = time.perf_counter()
+mg = hhg.MG(M, 1, L, etas, v0, pre=3, post=3, degree=a.deg)
+v0c = {l: v.clone() for l, v in build_case(L, 0, contrast=a.contrast, jump=a.jump)[2].items()} if a.schur == "vbfbt" else None
+mgc = hhg.MG(M, 1, L, etas, v0c, pre=1, post=1, degree=1) if a.schur == "vbfbt" else None
+keys = M.canonical_keys(L, hhg.HHG_P1)
+xyz = M.node_coords(L, hhg.HHG_P1)
+xc = torch.stack([M.to_canonical(L, hhg.HHG_P1, xyz[:, c].contiguous()) for c in range(3)], 1)
+T = M.from_canonical(L, hhg.HHG_P1, temperature(xc.cpu().numpy(), keys))
+f = hhg.hhg_buoyancy_load(M, L, T)
+rhs = torch.cat([f, M.zeros(L, hhg.HHG_P1)])
+S = hhg.StokesSolver(mg, etas[L], GAMMA, restart=a.restart, max_iters=a.max_iters, tol=a.tol, schur=a.schur,
+                     mg_cheap=mgc)
+torch.cuda.synchronize()
+setup = time.perf_counter() - t0
+s = torch.cuda.Stream()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+with torch.cuda.stream(s):
+    e0.record(s)
+    x, it, rel = S.solve(rhs, stream=s)
+    e1.record(s)
+s.synchronize()
+ms = e0.elapsed_time(e1)
+n_p = M.canonical_len(L, hhg.HHG_P1)
+x2, ita, rela = mg.ablock_cg(f, tol=1e-2, max_iters=200)
+print(json.dumps({"what": "stokes_solve", "ablock_cg_iters_tol1e-2": ita, "ablock_rel": rela, "level": L, "schur": a.schur, "velocity_dofs": n_dof, "pressure_dofs": n_p,
+                  "fgmres_iters": it, "rel_res": rel, "tol": a.tol, "solve_s": ms / 1e3, "setup_s": setup,
+                  "viscosity": f"contrast {a.contrast:g} x {a.jump:g} jump", "rhs": "buoyancy (T - 1/2) x/|x|, g = 0"}))
