@@ -100,6 +100,16 @@ int hhg_mesh_create(const double* macro_xyz, int64_t n_vert, const int32_t* macr
                     const int32_t* vertex_tag, int level_max, const int32_t* tet_rank, hhg_comm* comm,
                     hhg_mesh** out);
 int hhg_mesh_destroy(hhg_mesh* mesh);
+/* The thick spherical shell macro mesh shell(ntan, nrad) (R4): each icosahedron
+ * face split into (ntan-1)^2 flat triangles normalised to the sphere, nrad spheres between r_min
+ * and r_max, every layer prism split into 3 tets (sorted-id staircase rule); 60 (ntan-1)^2 (nrad-1)
+ * macro tets (shell(3,2) = the paper's 240 macros).  Vertex tags 1 (r_min, CMB) / 2 (r_max,
+ * surface) / 0.  hhg_icoshell_macro returns the arrays (host; pass NULL arrays to query sizes);
+ * hhg_mesh_create_icoshell builds the mesh directly.  HHG_EINVAL for ntan < 2, nrad < 2, bad radii. */
+int hhg_icoshell_macro(int ntan, int nrad, double r_min, double r_max, double* verts, int32_t* tets, int32_t* vtag,
+                       int64_t* n_vert, int64_t* n_tets);
+int hhg_mesh_create_icoshell(int ntan, int nrad, double r_min, double r_max, int level_max, const int32_t* tet_rank,
+                             hhg_comm* comm, hhg_mesh** out);
 /* Number of macro tets stored by this process. */
 int hhg_mesh_local_macros(const hhg_mesh* mesh, int64_t* n);
 

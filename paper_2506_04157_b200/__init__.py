@@ -41,7 +41,7 @@ EXPORTS = [
     "hhg_mesh_create_part", "hhg_partition_rcb", "hhg_mesh_rank", "hhg_halo_info", "hhg_halo_keys",
     "hhg_owned_count", "hhg_halo_pack", "hhg_interface_sum_remote", "epsilon_apply_partial",
     "hhg_ablock_cg", "hhg_mass_apply", "hhg_mass_diag", "hhg_stokes_create", "hhg_stokes_solve",
-    "hhg_stokes_destroy", "hhg_buoyancy_load",
+    "hhg_stokes_destroy", "hhg_buoyancy_load", "hhg_icoshell_macro", "hhg_mesh_create_icoshell",
 ]
 
 
@@ -83,6 +83,8 @@ def _load():
         "hhg_mass_apply": ([P, I, P, P, P, P], I), "hhg_mass_diag": ([P, I, P, P, P], I),
         "hhg_stokes_create": ([P, P, P, D, P, P], I), "hhg_stokes_solve": ([P, P, P, P, P, P], I),
         "hhg_stokes_destroy": ([P], I), "hhg_buoyancy_load": ([P, I, P, P, P], I),
+        "hhg_icoshell_macro": ([I, I, D, D, P, P, P, P, P], I),
+        "hhg_mesh_create_icoshell": ([I, I, D, D, I, P, P, P], I),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -159,6 +161,18 @@ class Comm:
         if getattr(self, "handle", None) and _lib is not None:
             _lib.hhg_comm_destroy(self.handle)
             self.handle = None
+
+
+def icoshell_macro(ntan, nrad, r_min=0.55, r_max=1.0):
+    """hhg_icoshell_macro: (verts (V,3), tets (T,4) int32, vtag (V,) int32) of shell(ntan, nrad)."""
+    nv, nt = ctypes.c_int64(), ctypes.c_int64()
+    _chk(_lib.hhg_icoshell_macro(int(ntan), int(nrad), float(r_min), float(r_max), None, None, None,
+                                 ctypes.byref(nv), ctypes.byref(nt)))
+    v = np.empty((nv.value, 3), dtype=np.float64)
+    t = np.empty((nt.value, 4), dtype=np.int32)
+    g = np.empty(nv.value, dtype=np.int32)
+    _chk(_lib.hhg_icoshell_macro(int(ntan), int(nrad), float(r_min), float(r_max), _ptr(v), _ptr(t), _ptr(g), None, None))
+    return v, t, g
 
 
 def partition_rcb(verts, tets, nparts, radial=True):

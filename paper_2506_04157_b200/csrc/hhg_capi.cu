@@ -537,3 +537,127 @@ int epsilon_apply_partial(const hhg_mesh* mesh, int level, int form, const doubl
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------ icosahedral shell generator
+// shell(ntan, nrad) (R4): each icosahedron face split into (ntan-1)^2 flat
+// triangles (vertices normalised to the unit sphere, numbered by their sorted (vertex, weight)
+// keys), nrad spheres r_l = r_min + l (r_max - r_min)/(nrad-1), every layer prism split into 3 tets
+// by the sorted-id staircase rule (p_i,q_i,r_i,r_o), (p_i,q_i,q_o,r_o), (p_i,p_o,q_o,r_o).
+namespace {
+int icoshell_build(int ntan, int nrad, double r_min, double r_max, std::vector<double>& verts,
+                   std::vector<int32_t>& tets, std::vector<int32_t>& vtag) {
+  if (ntan < 2 || nrad < 2 || !(0.0 < r_min && r_min < r_max)) return fail(HHG_EINVAL, "icoshell: need ntan>=2, nrad>=2, 0<r_min<r_max");
+  const double phi = (1.0 + std::sqrt(5.0)) / 2.0;
+  std::vector<std::array<double, 3>> ico;
+  for (double s1 : {-1.0, 1.0})
+    for (double s2 : {-1.0, 1.0}) {
+      ico.push_back({0.0, s1, s2 * phi});
+      ico.push_back({s1, s2 * phi, 0.0});
+      ico.push_back({s2 * phi, 0.0, s1});
+    }
+  const int n = (int)ico.size();
+  auto dist = [&](int a, int b) {
+    double s = 0;
+    for (int c = 0; c < 3; ++c) s += (ico[a][c] - ico[b][c]) * (ico[a][c] - ico[b][c]);
+    return std::sqrt(s);
+  };
+  auto adj = [&](int a, int b) { return std::fabs(dist(a, b) - 2.0) < 1e-9; };
+  std::vector<std::array<int, 3>> faces;
+  for (int a = 0; a < n; ++a)
+    for (int b = a + 1; b < n; ++b) {
+      if (!adj(a, b)) continue;
+      for (int c = b + 1; c < n; ++c)
+        if (adj(a, c) && adj(b, c)) faces.push_back({a, b, c});
+    }
+  if (faces.size() != 20) return fail(HHG_EINVAL, "icoshell: icosahedron face search failed");
+  const int m = ntan - 1;
+  using Key = std::vector<std::pair<int, int>>;
+  std::map<Key, int> key_to_id;
+  std::vector<std::array<double, 3>> pts;
+  std::vector<std::map<std::pair<int, int>, int>> grids;
+  for (auto& f : faces) {
+    std::map<std::pair<int, int>, int> grid;
+    for (int i = 0; i <= m; ++i)
+      for (int j = 0; j <= m - i; ++j) {
+        const int wa = m - i - j, wb = i, wc = j;
+        Key key;
+        for (auto vw : {std::make_pair(f[0], wa), std::make_pair(f[1], wb), std::make_pair(f[2], wc)})
+          if (vw.second > 0) key.push_back(vw);
+        std::sort(key.begin(), key.end());
+        auto it = key_to_id.find(key);
+        if (it == key_to_id.end()) {
+          it = key_to_id.emplace(key, (int)pts.size()).first;
+          std::array<double, 3> p;
+          for (int c = 0; c < 3; ++c) p[c] = (wa * ico[f[0]][c] + wb * ico[f[1]][c] + wc * ico[f[2]][c]) / m;
+          const double nr = std::sqrt(p[0] * p[0] + p[1] * p[1] + p[2] * p[2]);
+          for (int c = 0; c < 3; ++c) p[c] /= nr;
+          pts.push_back(p);
+        }
+        grid[{i, j}] = it->second;
+      }
+    grids.push_back(grid);
+  }
+  std::vector<int> remap(pts.size());
+  {
+    int k = 0;
+    for (auto& kv : key_to_id) remap[kv.second] = k++;  // std::map iterates in sorted key order
+  }
+  const int ns = (int)pts.size();
+  std::vector<std::array<int, 3>> tris;
+  for (auto& grid : grids)
+    for (int i = 0; i < m; ++i)
+      for (int j = 0; j < m - i; ++j) {
+        tris.push_back({remap[grid[{i, j}]], remap[grid[{i + 1, j}]], remap[grid[{i, j + 1}]]});
+        if (i + j < m - 1) tris.push_back({remap[grid[{i + 1, j}]], remap[grid[{i, j + 1}]], remap[grid[{i + 1, j + 1}]]});
+      }
+  verts.assign((size_t)ns * nrad * 3, 0.0);
+  vtag.assign((size_t)ns * nrad, 0);
+  for (int l = 0; l < nrad; ++l) {
+    const double r = r_min + l * (r_max - r_min) / (nrad - 1);
+    for (int old = 0; old < ns; ++old)
+      for (int c = 0; c < 3; ++c) verts[3 * ((size_t)l * ns + remap[old]) + c] = r * pts[old][c];
+  }
+  for (int v = 0; v < ns; ++v) {
+    vtag[v] = 1;                                  // inner sphere (CMB)
+    vtag[(size_t)(nrad - 1) * ns + v] = 2;        // outer sphere (surface)
+  }
+  tets.clear();
+  for (int l = 0; l < nrad - 1; ++l)
+    for (auto& tri : tris) {
+      std::array<int, 3> s = tri;
+      std::sort(s.begin(), s.end());
+      const int pi = l * ns + s[0], qi = l * ns + s[1], ri = l * ns + s[2];
+      const int po = pi + ns, qo = qi + ns, ro = ri + ns;
+      for (std::array<int, 4> t : {std::array<int, 4>{pi, qi, ri, ro}, std::array<int, 4>{pi, qi, qo, ro},
+                                   std::array<int, 4>{pi, po, qo, ro}}) {
+        std::sort(t.begin(), t.end());
+        tets.insert(tets.end(), t.begin(), t.end());
+      }
+    }
+  return HHG_OK;
+}
+}  // namespace
+
+extern "C" {
+int hhg_icoshell_macro(int ntan, int nrad, double r_min, double r_max, double* verts, int32_t* tets,
+                       int32_t* vtag, int64_t* n_vert, int64_t* n_tets) {
+  std::vector<double> v;
+  std::vector<int32_t> t, g;
+  HHG_TRY(icoshell_build(ntan, nrad, r_min, r_max, v, t, g));
+  if (n_vert) *n_vert = (int64_t)g.size();
+  if (n_tets) *n_tets = (int64_t)t.size() / 4;
+  if (verts) std::copy(v.begin(), v.end(), verts);
+  if (tets) std::copy(t.begin(), t.end(), tets);
+  if (vtag) std::copy(g.begin(), g.end(), vtag);
+  return HHG_OK;
+}
+
+int hhg_mesh_create_icoshell(int ntan, int nrad, double r_min, double r_max, int level_max, const int32_t* tet_rank,
+                             hhg_comm* comm, hhg_mesh** out) {
+  std::vector<double> v;
+  std::vector<int32_t> t, g;
+  HHG_TRY(icoshell_build(ntan, nrad, r_min, r_max, v, t, g));
+  return hhg_mesh_create(v.data(), (int64_t)g.size(), t.data(), (int64_t)t.size() / 4, g.data(), level_max, tet_rank,
+                         comm, out);
+}
+}  // extern "C"

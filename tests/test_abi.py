@@ -68,3 +68,19 @@ def test_argument_errors():
         M.blend_map(hhg.HHG_BLEND_SHELL)      # reference tet has a vertex at the origin
     with pytest.raises(hhg.HHGError, match="HHG_EINVAL"):
         M.set_bc(5, hhg.HHG_BC_DIRICHLET0)
+
+
+@pytest.mark.parametrize("ntan,nrad", [(2, 2), (3, 2), (5, 3)])
+def test_library_icoshell_generator_matches_workload(ntan, nrad):
+    """hhg_icoshell_macro (the library's shell generator) reproduces the workload's shell(ntan, nrad):
+    identical numbering, tets and tags, coordinates to 1e-15; 60 (ntan-1)^2 (nrad-1) macros."""
+    import numpy as np
+    import paper_2506_04157_b200 as hhg
+    from workload import icoshell
+    v, t, g = hhg.icoshell_macro(ntan, nrad, 0.55, 1.0)
+    w = icoshell(ntan, nrad, 0.55, 1.0)
+    assert t.shape[0] == 60 * (ntan - 1) ** 2 * (nrad - 1)
+    assert np.array_equal(t, w.tets) and np.array_equal(g, w.vtag)
+    assert np.abs(v - w.verts).max() <= 1e-15
+    with pytest.raises(hhg.HHGError):
+        hhg.icoshell_macro(1, 2)
