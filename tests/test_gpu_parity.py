@@ -356,3 +356,58 @@ def test_stokes_fgmres_uzawa_solve(eta_cj, tol, max_iters, schur):
         assert rel <= tol and rel_o <= tol
     assert it == it_o and abs(rel - rel_o) <= 1e-6 * rel_o
     assert rel_l2(xc, x_o) <= 1e-8, rel_l2(xc, x_o)
+
+
+@pytest.mark.slow
+def test_config3_full_size_sampled_rows_and_vcycle_properties():
+    """BASELINE config 3 at full size (shell(3,2), L5, contrast 1e6 x 30), in the bench's launch
+    configuration: epsilon_apply rows against the oracle computed one by one on sampled nodes
+    (macro faces/edges/vertices included), and properties of the graph-launched V(3,3)-cycle that
+    hold at any size: V(0) = 0 exactly, V(2f) = 2 V(f) (every step is homogeneous of degree 1; the
+    only deviation is the order of fp64 REDs on brick borders, hence 1e-12 rather than bitwise),
+    graph replays agree to 1e-12, the result satisfies the constraints (P_v M x = x)."""
+    from oracle.refine import build_level, node_bc
+    from oracle.operators import node_coords, sampled_rows, constraint_matrix
+    from oracle.multigrid import lookup_keys
+    from workload import viscosity
+    from bench import build_case
+    mac = icoshell(3, 2)
+    L = 5
+    core = [5, 120]
+    core_verts = set(mac.tets[core].ravel().tolist())
+    star = [t for t in range(mac.n_tets) if core_verts & set(mac.tets[t].tolist())]
+    lm = build_level(mac.verts, mac.tets, mac.vtag, L, macro_subset=star)
+    bc = node_bc(lm.p2_keys, lm.macro_tets, lm.macro_vtag, {2: 1, 1: 2})
+    C3 = (1e6, 30.0)
+    eta_o = viscosity(node_coords(lm, "P1", True), lm.p1_keys, *C3)
+    uo = constraint_matrix(lm.p2_xt, bc) @ uniform_vec(lm.p2_keys, 2)
+    rng = np.random.default_rng(1)
+    core_tets = np.nonzero(np.isin(lm.tet_macro, core))[0]
+    n2 = np.unique(lm.tet_p2[core_tets].ravel())
+    s2 = np.unique(np.concatenate([rng.choice(n2, 300, replace=False), n2[lm.p2_keys[n2, 0] < 3][:100]]))
+    yu_o, _ = sampled_rows(lm, True, eta_o, 0.0, uo, np.zeros(lm.n_p1), s2, np.zeros(0, dtype=np.int64), bc)
+    M, etas, v0, rhs, n_dof = build_case(L, 0)
+    y = hhg.epsilon_apply(M, L, etas[L], lib_u(M, L, 2))
+    r2 = lookup_keys(M.canonical_keys(L, hhg.HHG_P2), lm.p2_keys[s2])
+    yc = canon(M, L, hhg.HHG_P2VEC, y).reshape(-1, 3)[r2]
+    assert rel_l2(yc, yu_o.reshape(-1, 3)[s2]) <= TOL_APPLY
+    mg = hhg.MG(M, 1, L, etas, v0, pre=3, post=3, degree=3, power_iters=20, coarse_iters=50)
+    s = torch.cuda.Stream()
+    x = M.zeros(L, hhg.HHG_P2VEC)
+    x0 = M.zeros(L, hhg.HHG_P2VEC)
+    with torch.cuda.stream(s):
+        mg.vcycle(rhs, x, stream=s)
+        xa = x.clone()
+        mg.vcycle(rhs, x, stream=s)           # graph replay
+        xb = x.clone()
+        r2x = (2.0 * rhs).contiguous()
+        x2 = M.zeros(L, hhg.HHG_P2VEC)
+        mg.vcycle(r2x, x2, stream=s)
+        mg.vcycle(M.zeros(L, hhg.HHG_P2VEC), x0, stream=s)
+    s.synchronize()
+    nx = float(xa.norm())
+    assert float((xa - xb).norm()) <= 1e-12 * nx
+    assert float((x2 - 2.0 * xa).norm()) <= 1e-12 * 2.0 * nx
+    assert torch.count_nonzero(x0).item() == 0
+    assert float((M.apply_bc(L, xa.clone()) - xa).norm()) <= 1e-14 * nx
+    assert torch.isfinite(xa).all()
