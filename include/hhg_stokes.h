@@ -252,6 +252,8 @@ typedef struct {
   double cheb_lo_ratio;      /* 0.1  (a = b/10)           */
   int visc_form;             /* HHG_VISC_FULL */
   int use_graph;             /* capture the V-cycle in a CUDA graph */
+  int l_eta;                 /* levels <= l_eta evaluate eta at the quadrature points (NEXT-2; -1: none) */
+  double qeta_lnC, qeta_jump, qeta_rjump;  /* eta_q = exp(lnC (1/2 - T_q)) (jump if r_q < rjump else 1) */
 } hhg_mg_params;
 
 /* hhg_mg_create: builds per-level workspaces, diag(A) and D^-1, and lambda_hat per
@@ -260,6 +262,19 @@ typedef struct {
  * stay alive while the hierarchy is used.  Synchronises. */
 int hhg_mg_create(hhg_mesh* mesh, const hhg_mg_params* params, const double* const* eta_per_level,
                   double* const* power_v0, hhg_mg** out);
+/* hhg_mg_create_qeta: as hhg_mg_create, and on levels l <= params->l_eta the A operator (apply,
+ * diag, lambda) evaluates the viscosity at the quadrature points from the P2 temperature
+ * T2_per_level[l] (consistent P2 vectors, kept alive by the caller): the two-tier viscosity of
+ * P:451-453 (the paper's order-6 exp surrogate is a CPU-vectorisation device; the fp64 exp is used). */
+int hhg_mg_create_qeta(hhg_mesh* mesh, const hhg_mg_params* params, const double* const* eta_per_level,
+                       const double* const* T2_per_level, double* const* power_v0, hhg_mg** out);
+/* epsilon_apply_qeta / hhg_diag_qeta: A(eta) u and diag(A) with eta evaluated at the quadrature
+ * points: eta_q = exp(lnC (1/2 - T_q)) * (jump if |x_q| < r_jump else 1), T_q the P2 interpolant of
+ * T_p2 (NEXT-2 tier).  Results consistent; apply BC-masked (M P_v), diag without P_v. */
+int epsilon_apply_qeta(const hhg_mesh* mesh, int level, const double* T_p2, double lnC, double jump, double r_jump,
+                       const double* u, double* y, hhg_stream_t stream);
+int hhg_diag_qeta(const hhg_mesh* mesh, int level, const double* T_p2, double lnC, double jump, double r_jump,
+                  double* diag, hhg_stream_t stream);
 int hhg_mg_lambda(const hhg_mg* mg, int level, double* lambda_host);
 /* One V-cycle (fig:ASolverStructure) from x = 0: x = V(rhs). */
 int vcycle(hhg_mg* mg, const double* rhs, double* x, hhg_stream_t stream);

@@ -121,7 +121,10 @@ class Discretisation:
     """Assembled operators of one level.  eta_p1: nodal P1 viscosity (canonical order) or None (=1)."""
 
     def __init__(self, lm: LevelMesh, blended: bool, eta_p1=None, gamma=0.0,
-                 bc_by_tag=None, form=FORM_FULL, chunk=20000, build=("A", "B", "C")):
+                 bc_by_tag=None, form=FORM_FULL, chunk=20000, build=("A", "B", "C"), T_p2=None, qeta=None):
+        """T_p2 + qeta = (lnC, jump, r_jump): A uses eta at the quadrature points,
+        eta_q = exp(lnC (1/2 - T_q)) (jump if |x_q| < r_jump else 1), T_q = P2 interpolant of the nodal
+        temperature (the quadrature-point tier of P:451-453, R22); else the P1 eta."""
         self.lm = lm
         self.blended = blended
         self.blend_params = macro_blend(lm) if blended else None
@@ -138,7 +141,13 @@ class Discretisation:
             pd = lm.tet_p1[tets]
             if "A" in build:
                 xi, _ = fe.q4_rule()
-                eta_q = eta_p1[pd] @ fe.p1_basis(xi).T       # (T,Q) P1 interpolation
+                if T_p2 is not None:
+                    lnC, jump, r_jump = qeta
+                    Tq = np.asarray(T_p2)[lm.tet_p2[tets]] @ fe.p2_basis(xi).T     # (T,Q)
+                    rq = np.linalg.norm(xq, axis=2)
+                    eta_q = np.exp(lnC * (0.5 - Tq)) * np.where(rq < r_jump, jump, 1.0)
+                else:
+                    eta_q = eta_p1[pd] @ fe.p1_basis(xi).T   # (T,Q) P1 interpolation
                 Ae = element_A(W, grads, eta_q, form)
                 M = _coo(Ae, vd, vd, 3 * n2, 3 * n2)
                 mats["A"] = M if mats["A"] is None else mats["A"] + M

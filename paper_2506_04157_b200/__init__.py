@@ -42,6 +42,7 @@ EXPORTS = [
     "hhg_owned_count", "hhg_halo_pack", "hhg_interface_sum_remote", "epsilon_apply_partial",
     "hhg_ablock_cg", "hhg_mass_apply", "hhg_mass_diag", "hhg_stokes_create", "hhg_stokes_solve",
     "hhg_stokes_destroy", "hhg_buoyancy_load", "hhg_icoshell_macro", "hhg_mesh_create_icoshell",
+    "hhg_mg_create_qeta", "epsilon_apply_qeta", "hhg_diag_qeta",
 ]
 
 
@@ -85,6 +86,8 @@ def _load():
         "hhg_stokes_destroy": ([P], I), "hhg_buoyancy_load": ([P, I, P, P, P], I),
         "hhg_icoshell_macro": ([I, I, D, D, P, P, P, P, P], I),
         "hhg_mesh_create_icoshell": ([I, I, D, D, I, P, P, P], I),
+        "hhg_mg_create_qeta": ([P, P, P, P, P, P], I), "epsilon_apply_qeta": ([P, I, P, D, D, D, P, P, P], I),
+        "hhg_diag_qeta": ([P, I, P, D, D, D, P, P], I),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -367,6 +370,23 @@ def hhg_mass_diag(mesh, level, eta, out=None, stream=None):
     return out
 
 
+def epsilon_apply_qeta(mesh, level, T2, qeta, u, y=None, stream=None):
+    """y = (M P_v) A(eta) u with eta_q = exp(lnC (1/2 - T_q)) (jump if r_q < r_jump else 1) at the
+    quadrature points, T_q the P2 interpolant of T2 (NEXT-2 tier); qeta = (lnC, jump, r_jump)."""
+    n = mesh.vec_len(level, HHG_P2VEC)
+    y = mesh.zeros(level, HHG_P2VEC) if y is None else y
+    _chk(_lib.epsilon_apply_qeta(mesh.handle, level, _dev(T2, mesh.vec_len(level, HHG_P2), "T2"), *[float(v) for v in qeta],
+                                 _dev(u, n, "u"), _dev(y, n, "y"), _stream(stream)))
+    return y
+
+
+def hhg_diag_qeta(mesh, level, T2, qeta, out=None, stream=None):
+    out = mesh.zeros(level, HHG_P2VEC) if out is None else out
+    _chk(_lib.hhg_diag_qeta(mesh.handle, level, _dev(T2, mesh.vec_len(level, HHG_P2), "T2"), *[float(v) for v in qeta],
+                            _dev(out, mesh.vec_len(level, HHG_P2VEC)), _stream(stream)))
+    return out
+
+
 def div_apply(mesh, level, gamma, u, q=None, stream=None):
     q = mesh.zeros(level, HHG_P1) if q is None else q
     _chk(_lib.div_apply(mesh.handle, level, float(gamma), _dev(u, mesh.vec_len(level, HHG_P2VEC), "u"),
@@ -440,25 +460,34 @@ class _MGParams(ctypes.Structure):
     _fields_ = [("l_min", ctypes.c_int), ("l_max", ctypes.c_int), ("pre", ctypes.c_int), ("post", ctypes.c_int),
                 ("degree", ctypes.c_int), ("power_iters", ctypes.c_int), ("coarse_iters", ctypes.c_int),
                 ("cheb_hi_factor", ctypes.c_double), ("cheb_lo_ratio", ctypes.c_double),
-                ("visc_form", ctypes.c_int), ("use_graph", ctypes.c_int)]
+                ("visc_form", ctypes.c_int), ("use_graph", ctypes.c_int), ("l_eta", ctypes.c_int),
+                ("qeta_lnC", ctypes.c_double), ("qeta_jump", ctypes.c_double), ("qeta_rjump", ctypes.c_double)]
 
 
 class MG:
     """hhg_mg_create: per-level D^-1 and lambda_hat; vcycle() applies one V-cycle."""
 
     def __init__(self, mesh, l_min, l_max, eta_per_level, power_v0, pre=3, post=3, degree=3, power_iters=20,
-                 coarse_iters=50, hi=1.1, lo=0.1, form=HHG_VISC_FULL, use_graph=True):
+                 coarse_iters=50, hi=1.1, lo=0.1, form=HHG_VISC_FULL, use_graph=True, T2_per_level=None, l_eta=-1,
+                 qeta=(0.0, 1.0, 0.0)):
+        """T2_per_level / l_eta / qeta = (lnC, jump, r_jump): on levels <= l_eta the viscosity is evaluated
+        at the quadrature points from the P2 temperature (NEXT-2 tier)."""
         self.mesh = mesh
         self.l_min, self.l_max = l_min, l_max
         prm = _MGParams(l_min, l_max, pre, post, degree, power_iters, coarse_iters, hi, lo, form,
-                        1 if use_graph else 0)
+                        1 if use_graph else 0, int(l_eta), *[float(v) for v in qeta])
         self._eta = dict(eta_per_level)
         self._v0 = dict(power_v0)
+        self._T2 = dict(T2_per_level or {})
         L = l_max + 1
         etas = (ctypes.c_void_p * L)(*[_ptr(self._eta.get(l)) for l in range(L)])
         v0s = (ctypes.c_void_p * L)(*[_ptr(self._v0.get(l)) for l in range(L)])
         h = ctypes.c_void_p()
-        _chk(_lib.hhg_mg_create(mesh.handle, ctypes.byref(prm), etas, v0s, ctypes.byref(h)))
+        if T2_per_level:
+            t2 = (ctypes.c_void_p * L)(*[_ptr(self._T2.get(l)) for l in range(L)])
+            _chk(_lib.hhg_mg_create_qeta(mesh.handle, ctypes.byref(prm), etas, t2, v0s, ctypes.byref(h)))
+        else:
+            _chk(_lib.hhg_mg_create(mesh.handle, ctypes.byref(prm), etas, v0s, ctypes.byref(h)))
         self.handle = h
 
     def __del__(self):

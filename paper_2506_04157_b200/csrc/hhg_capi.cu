@@ -329,6 +329,35 @@ int epsilon_apply(const hhg_mesh* mesh, int level, int form, const double* eta_p
   return apply_op(m, level, ELEM_A, form, eta_p1, 0.0, u, nullptr, y, nullptr, false, (cudaStream_t)stream);
 }
 
+int epsilon_apply_qeta(const hhg_mesh* mesh, int level, const double* T_p2, double lnC, double jump, double r_jump,
+                       const double* u, double* y, hhg_stream_t stream) {
+  HHG_TRY(check_level(mesh, level));
+  CHECK_PTR(T_p2);
+  CHECK_PTR(u);
+  CHECK_PTR(y);
+  auto* m = const_cast<hhg_mesh*>(mesh);
+  HHG_TRY(ensure_level(m, level));
+  const Level& L = m->levels[level];
+  cudaStream_t s = (cudaStream_t)stream;
+  HHG_CUDA(cudaMemsetAsync(y, 0, 3 * macro_count(m) * L.npts2 * sizeof(double), s));
+  HHG_TRY(launch_elem_qeta(m, L, ELEM_A, T_p2, lnC, jump, r_jump, u, y, s));
+  return launch_fixup(m, L, HHG_P2VEC, true, true, y, s);
+}
+
+int hhg_diag_qeta(const hhg_mesh* mesh, int level, const double* T_p2, double lnC, double jump, double r_jump,
+                  double* diag, hhg_stream_t stream) {
+  HHG_TRY(check_level(mesh, level));
+  CHECK_PTR(T_p2);
+  CHECK_PTR(diag);
+  auto* m = const_cast<hhg_mesh*>(mesh);
+  HHG_TRY(ensure_level(m, level));
+  const Level& L = m->levels[level];
+  cudaStream_t s = (cudaStream_t)stream;
+  HHG_CUDA(cudaMemsetAsync(diag, 0, 3 * macro_count(m) * L.npts2 * sizeof(double), s));
+  HHG_TRY(launch_elem_qeta(m, L, ELEM_DIAG, T_p2, lnC, jump, r_jump, nullptr, diag, s));
+  return launch_fixup(m, L, HHG_P2VEC, true, false, diag, s);
+}
+
 int hhg_mass_apply(const hhg_mesh* mesh, int level, const double* eta_p1, const double* p, double* y,
                    hhg_stream_t stream) {
   HHG_TRY(check_level(mesh, level));

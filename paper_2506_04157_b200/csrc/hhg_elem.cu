@@ -80,11 +80,20 @@ __device__ __forceinline__ double rsqrt_nr(double s) {
 // Element outputs of one micro tet.  G: [JFinv(9) | qoff(4x3)] of the tet's type;
 // wdet = w |det J_F| of the level; xa: unblended anchor position.
 // acc[10][3]: velocity outputs (v0..v3, e01..e23); gy[4]: P1 outputs.
-template <bool BLEND, int MODE, bool FULL, class UA>
+// Quadrature-point viscosity tier (NEXT-2): eta_q = exp(lnC (1/2 - T_q)) * (jump if
+// r_q < r_jump else 1) with T_q the P2 interpolant of the nodal temperature (R22).
+struct EtaQ {
+  double lnC, jump, r_jump;
+};
+struct NoT {
+  __device__ __forceinline__ double operator()(int) const { return 0.0; }
+};
+
+template <bool BLEND, int MODE, bool FULL, class UA, bool ETAQ = false, class TA = NoT>
 __device__ __forceinline__ void tet_body(const double* G, double wdet, const double (&xa)[3],
                                          const double (&nh)[3], double cK, double gamma, const UA& uu,
                                          const double (&et)[4], const double (&pp)[4], double (&acc)[10][3],
-                                         double (&gy)[4]) {
+                                         double (&gy)[4], const TA& tt = TA{}, EtaQ eq = EtaQ{0.0, 1.0, 0.0}) {
   constexpr bool DO_A = (MODE & ELEM_A) != 0;
   constexpr bool DO_BT = (MODE & ELEM_BT) != 0;
   constexpr bool DO_DIV = (MODE & ELEM_DIV) != 0;
@@ -138,13 +147,33 @@ __device__ __forceinline__ void tet_body(const double* G, double wdet, const dou
   double JFi[9];
 #pragma unroll
   for (int r = 0; r < 9; ++r) JFi[r] = G[r];
-  double Kq[4][9], al[4] = {1.0, 1.0, 1.0, 1.0}, dq[4][3];
+  double Kq[4][9], al[4] = {1.0, 1.0, 1.0, 1.0}, dq[4][3], etv[4] = {1.0, 1.0, 1.0, 1.0};
   {
     double xq[4][3], sq[4], yq[4], tq[4], rq[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q)
 #pragma unroll
       for (int r = 0; r < 3; ++r) xq[q][r] = xa[r] + G[9 + 3 * q + r];
+    if (ETAQ) {
+      constexpr double phv = EQB * (2.0 * EQB - 1.0), phq = EQA * (2.0 * EQA - 1.0);
+      constexpr double peq = 4.0 * EQA * EQB, pen = 4.0 * EQB * EQB;
+      double tv[10];
+#pragma unroll
+      for (int a = 0; a < 10; ++a) tv[a] = tt(a);
+      const double sv = phv * (tv[0] + tv[1] + tv[2] + tv[3]) + pen * (tv[4] + tv[5] + tv[6] + tv[7] + tv[8] + tv[9]);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        double es = 0.0;
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+          if (m != q) es += tv[EEI(m, q)];
+        const double Tq = fma(peq - pen, es, fma(phq - phv, tv[q], sv));
+        const double s2 = fma(xq[q][0], xq[q][0], fma(xq[q][1], xq[q][1], xq[q][2] * xq[q][2]));
+        // radius of the blended point: |B(x)| = c (n.x)
+        const double rr = BLEND ? cK * fma(nh[0], xq[q][0], fma(nh[1], xq[q][1], nh[2] * xq[q][2])) : sqrt(s2);
+        etv[q] = exp(eq.lnC * (0.5 - Tq)) * (rr < eq.r_jump ? eq.jump : 1.0);
+      }
+    }
     if (BLEND || DO_DIV) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) sq[q] = fma(xq[q][0], xq[q][0], fma(xq[q][1], xq[q][1], xq[q][2] * xq[q][2]));
@@ -242,7 +271,7 @@ __device__ __forceinline__ void tet_body(const double* G, double wdet, const dou
     const double* K = Kq[q];
     const double alpha = al[q];
     const double* d = dq[q];
-    const double etaq = fma(EQAB, et[q], etaS);
+    const double etaq = ETAQ ? etv[q] : fma(EQAB, et[q], etaS);
 
     if (DO_DIAG) {
       // diag(A): sum_q 2 eta w|det J| [eps(phi_a e_c) : eps(phi_a e_c) - 1/3 (div)^2]
@@ -693,10 +722,17 @@ struct FootU {
   }
 };
 
-template <int MODE>
+struct FootT {  // scalar P2 footprint (temperature) for the quadrature-point viscosity tier
+  const char* b;
+  const int* off;
+  __device__ __forceinline__ double operator()(int a) const { return *reinterpret_cast<const double*>(b + off[a]); }
+};
+
+template <int MODE, bool ETAQ = false>
 __host__ __device__ constexpr int fp_smem_words() {
   return ((MODE & (ELEM_A | ELEM_DIV)) ? 3 * kFU : 0) + (elem_u_out(MODE) ? 2 * 3 * kFY : 0) +
-         kF1 + ((MODE & (ELEM_BT | ELEM_MASS | ELEM_LOAD)) ? kF1 : 0) + (elem_p_out(MODE) ? 2 * kF1Y : 0) + kGeoSm;
+         kF1 + ((MODE & (ELEM_BT | ELEM_MASS | ELEM_LOAD)) ? kF1 : 0) + (elem_p_out(MODE) ? 2 * kF1Y : 0) + kGeoSm +
+         (ETAQ ? kFU : 0);
 }
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
@@ -705,7 +741,7 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-template <bool BLEND, int MODE, bool FULL>
+template <bool BLEND, int MODE, bool FULL, bool ETAQ = false>
 #ifndef HHG_FP_MINB
 #define HHG_FP_MINB 5
 #endif
@@ -713,7 +749,8 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
     k_elem_fp(const MacroGeo* __restrict__ mgeo, const double* __restrict__ lgeo, const int32_t* __restrict__ bricks,
               int n1, double inv_n1, int64_t npts1, int64_t npts2, int64_t cstride, const double* __restrict__ eta,
               const double* __restrict__ u, const double* __restrict__ p, double* __restrict__ yu,
-              double* __restrict__ yp, double gamma) {
+              double* __restrict__ yp, double gamma, const double* __restrict__ T2 = nullptr,
+              EtaQ eq = EtaQ{0.0, 1.0, 0.0}) {
   constexpr bool DO_DIV = (MODE & ELEM_DIV) != 0;
   constexpr bool NEED_U = (MODE & (ELEM_A | ELEM_DIV)) != 0;
   constexpr bool NEED_P = (MODE & (ELEM_BT | ELEM_MASS | ELEM_LOAD)) != 0;
@@ -726,6 +763,7 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
   double* sp = se + kF1;                             // [kF1]
   double* syp = sp + (NEED_P ? kF1 : 0);             // [2 warps][kF1Y]
   double* sgeo = syp + (HAS_P_OUT ? 2 * kF1Y : 0);   // [kGeoSm]
+  double* stt = sgeo + kGeoSm;                       // [kFU] temperature footprint (ETAQ)
 
   const int mac = blockIdx.y;
   const int32_t bpk = __ldg(bricks + blockIdx.x);
@@ -748,6 +786,15 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
       const int w = fword(X, Y, Z);
 #pragma unroll
       for (int c = 0; c < 3; ++c) cp_async8(su + c * kFU + w, src + c * cstride);
+    }
+  }
+  if (ETAQ) {
+#pragma unroll 1
+    for (int L = tid; L < 729; L += kBT) {
+      const int X = L % 9, Y = (L / 9) % 9, Z = L / 81;
+      const int gx = 2 * i0 + X, gy = 2 * j0 + Y, gz = 2 * k0 + Z;
+      if (gx + gy + gz > n2) continue;
+      cp_async8(stt + fword(X, Y, Z), T2 + mb2 + rowstart32(n2, gy, gz) + gx);
     }
   }
   if (HAS_U_OUT)
@@ -796,8 +843,9 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
       et[v] = se[cb1 + eOffP[t][v]];
       if (NEED_P) pp[v] = sp[cb1 + eOffP[t][v]];
     }
-    tet_body<BLEND, MODE, FULL>(sgeo + t * kTypeGeo, wdet, xa, nh, cK, gamma, FootU{reinterpret_cast<const char*>(su + cb2), eOffB[t]}, et, pp,
-                                acc, gy);
+    tet_body<BLEND, MODE, FULL, FootU, ETAQ, FootT>(sgeo + t * kTypeGeo, wdet, xa, nh, cK, gamma,
+                                                    FootU{reinterpret_cast<const char*>(su + cb2), eOffB[t]}, et, pp,
+                                                    acc, gy, FootT{reinterpret_cast<const char*>(stt + cb2), eOffB[t]}, eq);
     if (HAS_U_OUT) {
 #pragma unroll
       for (int a = 0; a < 10; ++a) {
@@ -840,8 +888,9 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
         et[v] = se[cb1 + eOffP[t][v]];
         if (NEED_P) pp[v] = sp[cb1 + eOffP[t][v]];
       }
-      tet_body<BLEND, MODE, FULL>(sgeo + t * kTypeGeo, wdet, xa, nh, cK, gamma, FootU{reinterpret_cast<const char*>(su + cb2), eOffB[t]}, et, pp,
-                                  acc, gy);
+      tet_body<BLEND, MODE, FULL, FootU, ETAQ, FootT>(sgeo + t * kTypeGeo, wdet, xa, nh, cK, gamma,
+                                                      FootU{reinterpret_cast<const char*>(su + cb2), eOffB[t]}, et, pp,
+                                                      acc, gy, FootT{reinterpret_cast<const char*>(stt + cb2), eOffB[t]}, eq);
     }
     const int* off = eOffB[t];
     char* ywb = reinterpret_cast<char*>(yw);
@@ -1252,6 +1301,44 @@ static void elem_launch(const Mesh* m, const Level& L, const double* eta, double
   }
   k_elem_brick<BLEND, MODE, FULL><<<grid, kBT, smem, s>>>(m->dgeo, L.geo, L.bricks, L.n1, 1.0 / L.n1, L.npts1,
                                                           L.npts2, nm * L.npts2, eta, u, p, yu, yp, gamma);
+}
+
+template <bool BLEND, int MODE>
+static void elem_launch_qeta(const Mesh* m, const Level& L, const double* T2, EtaQ eq, const double* u, double* yu,
+                             cudaStream_t s) {
+  const int64_t nm = macro_count(m);
+  constexpr size_t smem = fp_smem_words<MODE, true>() * sizeof(double);
+  dim3 grid((unsigned)L.n_bricks, (unsigned)nm);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_elem_fp<BLEND, MODE, true, true>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         (int)cudaSharedmemCarveoutMaxShared);
+    cudaFuncSetAttribute(k_elem_fp<BLEND, MODE, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  k_elem_fp<BLEND, MODE, true, true><<<grid, kBT, smem, s>>>(m->dgeo, L.geo, L.bricks, L.n1, 1.0 / L.n1, L.npts1, L.npts2,
+                                                             nm * L.npts2, nullptr, u, nullptr, yu, nullptr, 0.0, T2, eq);
+}
+
+// A (mode ELEM_A) or diag(A) (ELEM_DIAG) with the viscosity evaluated at the quadrature points from the
+// P2 temperature T2 (NEXT-2 tier); full form only
+int launch_elem_qeta(const Mesh* m, const Level& L, int mode, const double* T2, double lnC, double jump, double r_jump,
+                     const double* u, double* yu, cudaStream_t s) {
+  HHG_TRY(ensure_slots());
+  const EtaQ eq{lnC, jump, r_jump};
+  const bool bl = m->blend == HHG_BLEND_SHELL;
+  if (mode == ELEM_A) {
+    if (bl) elem_launch_qeta<true, ELEM_A>(m, L, T2, eq, u, yu, s);
+    else elem_launch_qeta<false, ELEM_A>(m, L, T2, eq, u, yu, s);
+  } else if (mode == ELEM_DIAG) {
+    if (bl) elem_launch_qeta<true, ELEM_DIAG>(m, L, T2, eq, u, yu, s);
+    else elem_launch_qeta<false, ELEM_DIAG>(m, L, T2, eq, u, yu, s);
+  } else {
+    return fail(HHG_EINVAL, "quadrature-point viscosity: mode must be A or diag");
+  }
+  count_launch();
+  HHG_CUDA(cudaGetLastError());
+  return HHG_OK;
 }
 
 int launch_elem(const Mesh* m, const Level& L, int mode, int form, const double* eta, double gamma,

@@ -135,6 +135,8 @@ int64_t macro_count(const Mesh* m);
 // ---------------------------------------------------------------- kernel launchers (hhg_kernels.cu)
 int launch_elem(const Mesh* m, const Level& L, int mode, int form, const double* eta, double gamma,
                 const double* u, const double* p, double* yu, double* yp, cudaStream_t s);
+int launch_elem_qeta(const Mesh* m, const Level& L, int mode, const double* T2, double lnC, double jump, double r_jump,
+                     const double* u, double* yu, cudaStream_t s);
 enum { ELEM_A = 1, ELEM_BT = 2, ELEM_DIV = 4, ELEM_DIAG = 8, ELEM_MASS = 16, ELEM_MASSD = 32, ELEM_LOAD = 64 };
 constexpr bool elem_p_out(int mode) { return (mode & (ELEM_DIV | ELEM_MASS | ELEM_MASSD)) != 0; }
 constexpr bool elem_u_out(int mode) { return (mode & (ELEM_A | ELEM_BT | ELEM_DIAG | ELEM_LOAD)) != 0; }

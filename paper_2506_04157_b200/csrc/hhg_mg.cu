@@ -79,6 +79,7 @@ struct hhg_mg {
   struct Lv {
     double *x = nullptr, *f = nullptr, *r = nullptr, *d = nullptr, *t = nullptr, *dinv = nullptr, *p = nullptr;
     const double* eta = nullptr;
+    const double* T2 = nullptr;   // P2 temperature: quadrature-point viscosity on this level (l <= l_eta)
     double lam = 0.0;
   };
   std::vector<Lv> lv;
@@ -137,7 +138,11 @@ static int mg_apply(hhg_mg* mg, int l, const double* u, double* y, cudaStream_t 
   const Level& L = mg->mesh->levels[l];
   if (!y_zeroed) HHG_CUDA(cudaMemsetAsync(y, 0, p2vec_len(mg->mesh, l) * sizeof(double), s));
   if (timed) HHG_CUDA(cudaEventRecord(mg->ev[mg->ev_used], s));
-  HHG_TRY(launch_elem(mg->mesh, L, ELEM_A, mg->prm.visc_form, mg->lv[l].eta, 0.0, u, nullptr, y, nullptr, s));
+  if (mg->lv[l].T2)
+    HHG_TRY(launch_elem_qeta(mg->mesh, L, ELEM_A, mg->lv[l].T2, mg->prm.qeta_lnC, mg->prm.qeta_jump, mg->prm.qeta_rjump,
+                             u, y, s));
+  else
+    HHG_TRY(launch_elem(mg->mesh, L, ELEM_A, mg->prm.visc_form, mg->lv[l].eta, 0.0, u, nullptr, y, nullptr, s));
   if (timed) {
     HHG_CUDA(cudaEventRecord(mg->ev[mg->ev_used + 1], s));
     mg->ev_used += 2;
@@ -186,7 +191,7 @@ static int mg_pcg(hhg_mg* mg, int l, const double* f, double* x, cudaStream_t s)
   double* z = L.d;
   double* p = L.p;
   double* q = L.t;
-  if (m->nranks == 1 && mg->prm.visc_form == HHG_VISC_FULL && !mg->no_persistent && coarse_pcg_fits(m, LL))
+  if (m->nranks == 1 && mg->prm.visc_form == HHG_VISC_FULL && !mg->no_persistent && !L.T2 && coarse_pcg_fits(m, LL))
     return launch_coarse_pcg(m, LL, L.eta, L.dinv, f, x, r, z, p, q, mg->cpart, mg->cbar, mg->prm.coarse_iters, s);
   HHG_CUDA(cudaMemsetAsync(x, 0, n * sizeof(double), s));
   HHG_TRY(launch_cheb0_bc(m, LL, f, nullptr, L.dinv, 1.0, r, z, s));  // r = f, z = PM dinv r
@@ -222,10 +227,40 @@ static int mg_cycle(hhg_mg* mg, int l, const double* f, double* x, cudaStream_t 
   return HHG_OK;
 }
 
+// power iteration of hhg_power_iteration with the hierarchy's own operator (quadrature-point
+// viscosity levels): w = P_v M D^-1 A v, lambda = |w|, v = w / lambda
+static int mg_power(hhg_mg* mg, int l, double* v0, double* lam) {
+  auto& L = mg->lv[l];
+  const Mesh* m = mg->mesh;
+  const Level& LL = m->levels[l];
+  const int64_t n = p2vec_len(m, l);
+  cudaStream_t s = nullptr;
+  HHG_TRY(launch_fixup(m, LL, HHG_P2VEC, false, true, v0, s));
+  for (int it = 0; it < mg->prm.power_iters; ++it) {
+    HHG_TRY(mg_apply(mg, l, v0, L.t, s));
+    k_scale_dinv<<<vg(n), 256, 0, s>>>(n, L.t, L.dinv, L.t);
+    count_launch();
+    HHG_TRY(launch_fixup(m, LL, HHG_P2VEC, false, true, L.t, s));
+    HHG_TRY(launch_dot(m, LL, HHG_P2VEC, L.t, L.t, mg->scal + 8, s));
+    k_normalize<<<vg(n), 256, 0, s>>>(n, mg->scal + 8, L.t, v0);
+    count_launch();
+  }
+  double h = 0;
+  HHG_CUDA(cudaMemcpy(&h, mg->scal + 8, sizeof(double), cudaMemcpyDeviceToHost));
+  if (!(h > 0) || !std::isfinite(h)) return fail(HHG_EZEROOP, "power iteration on a zero operator");
+  *lam = std::sqrt(h);
+  return HHG_OK;
+}
+
 extern "C" {
 
 int hhg_mg_create(hhg_mesh* mesh, const hhg_mg_params* params, const double* const* eta_per_level,
                   double* const* power_v0, hhg_mg** out) {
+  return hhg_mg_create_qeta(mesh, params, eta_per_level, nullptr, power_v0, out);
+}
+
+int hhg_mg_create_qeta(hhg_mesh* mesh, const hhg_mg_params* params, const double* const* eta_per_level,
+                       const double* const* T2_per_level, double* const* power_v0, hhg_mg** out) {
   if (!mesh || !params || !out) return fail(HHG_EINVAL, "hhg_mg_create: NULL argument");
   const hhg_mg_params& P = *params;
   if (P.l_min < 0 || P.l_max > mesh->level_max || P.l_min > P.l_max)
@@ -254,17 +289,26 @@ int hhg_mg_create(hhg_mesh* mesh, const hhg_mg_params* params, const double* con
     const int64_t n = p2vec_len(mesh, l);
     auto& L = mg->lv[l];
     L.eta = eta_per_level ? eta_per_level[l] : nullptr;
+    if (T2_per_level && l <= P.l_eta) {
+      if (!T2_per_level[l]) return bail(fail(HHG_EINVAL, "hhg_mg_create_qeta: T2_per_level[l] missing"));
+      if (P.visc_form != HHG_VISC_FULL) return bail(fail(HHG_EINVAL, "hhg_mg_create_qeta: full form only"));
+      L.T2 = T2_per_level[l];
+    }
     for (double** p : {&L.x, &L.f, &L.r, &L.d, &L.t, &L.dinv})
       if (cudaMalloc(p, n * sizeof(double)) != cudaSuccess) return bail(fail(HHG_ENOMEM, "mg vectors"));
     if (l == P.l_min && cudaMalloc(&L.p, n * sizeof(double)) != cudaSuccess) return bail(fail(HHG_ENOMEM, "mg p"));
     // diag(A) without P_v -> D^-1
-    r = apply_op(mesh, l, ELEM_DIAG, P.visc_form, L.eta, 0.0, nullptr, nullptr, L.t, nullptr, false, 0);
+    if (L.T2)
+      r = hhg_diag_qeta(mesh, l, L.T2, P.qeta_lnC, P.qeta_jump, P.qeta_rjump, L.t, nullptr);
+    else
+      r = apply_op(mesh, l, ELEM_DIAG, P.visc_form, L.eta, 0.0, nullptr, nullptr, L.t, nullptr, false, 0);
     if (r != HHG_OK) return bail(r);
     k_recip<<<vg(n), 256>>>(n, L.t, L.dinv);
     count_launch();
     if (l > P.l_min) {
       if (!power_v0 || !power_v0[l]) return bail(fail(HHG_EINVAL, "hhg_mg_create: power_v0[l] missing"));
-      r = hhg_power_iteration(mesh, l, L.eta, L.dinv, P.power_iters, power_v0[l], &L.lam, nullptr);
+      r = L.T2 ? mg_power(mg, l, power_v0[l], &L.lam)
+               : hhg_power_iteration(mesh, l, L.eta, L.dinv, P.power_iters, power_v0[l], &L.lam, nullptr);
       if (r != HHG_OK) return bail(r);
     }
   }

@@ -114,6 +114,68 @@ def test_buoyancy_load(shell_l2):
     assert rel_l2(canon(M, 2, hhg.HHG_P2VEC, f), f_o) <= TOL_APPLY
 
 
+def _temperature_p2(M, L):
+    from workload import temperature
+    from tests.harness import lib_coords_canonical
+    keys = M.canonical_keys(L, hhg.HHG_P2)
+    return M.from_canonical(L, hhg.HHG_P2, temperature(lib_coords_canonical(M, L, hhg.HHG_P2), keys))
+
+
+def test_quadrature_point_viscosity_apply_and_diag(shell_l2):
+    """NEXT-2 tier: A and diag(A) with eta evaluated at the quadrature points from the P2 temperature
+    (config-3 viscosity law: contrast 1e6, jump 30 below r = 0.9), blended shell L2."""
+    from oracle.operators import Discretisation, node_coords
+    from workload import temperature
+    from tests.harness import oracle_bc
+    mac, lm, d, eta_o, M = shell_l2
+    qeta = (np.log(1e6), 30.0, 0.9)
+    T_o = temperature(node_coords(lm, "P2", True), lm.p2_keys)
+    dq = Discretisation(lm, True, None, 0.0, oracle_bc(BC_SHELL), build=("A",), T_p2=T_o, qeta=qeta)
+    uo = dq.project(uniform_vec(lm.p2_keys, 2))
+    T2 = _temperature_p2(M, 2)
+    y = hhg.epsilon_apply_qeta(M, 2, T2, qeta, lib_u(M, 2, 2))
+    assert rel_l2(canon(M, 2, hhg.HHG_P2VEC, y), dq.apply_A(uo)) <= TOL_APPLY
+    dg = hhg.hhg_diag_qeta(M, 2, T2, qeta)
+    assert rel_l2(canon(M, 2, hhg.HHG_P2VEC, dg), dq.diagA()) <= TOL_APPLY
+
+
+def test_vcycle_with_quadrature_point_viscosity_levels():
+    """Config-3 V(3,3) on shell levels 3 -> 1 with the quadrature-point viscosity on levels <= 2
+    (l_eta = 2): one V-cycle against the oracle hierarchy built the same way."""
+    from oracle.multigrid import Hierarchy
+    from oracle.operators import Discretisation, node_coords
+    from oracle.refine import build_level
+    from workload import temperature, viscosity
+    from tests.harness import oracle_bc
+    mac = icoshell(3, 2)
+    qeta = (np.log(1e6), 30.0, 0.9)
+    discs, v0 = {}, {}
+    for L in (1, 2, 3):
+        lm = build_level(mac.verts, mac.tets, mac.vtag, L)
+        if L <= 2:
+            T_o = temperature(node_coords(lm, "P2", True), lm.p2_keys)
+            discs[L] = Discretisation(lm, True, None, 0.0, oracle_bc(BC_SHELL), build=("A",), T_p2=T_o, qeta=qeta)
+        else:
+            eta = viscosity(node_coords(lm, "P1", True), lm.p1_keys, 1e6, 30.0)
+            discs[L] = Discretisation(lm, True, eta, 0.0, oracle_bc(BC_SHELL), build=("A",))
+        v0[L] = uniform_vec(lm.p2_keys, 6)
+    H = Hierarchy(discs, v0, pre=3, post=3, degree=3, power_iters=20, coarse_iters=50)
+    f_o = discs[3].project(uniform_vec(discs[3].lm.p2_keys, 4))
+    x_o = H.vcycle(f_o)
+    M = lib_mesh(mac, 3, True, BC_SHELL)
+    etas = {L: lib_eta(M, L, (1e6, 30.0)) for L in (1, 2, 3)}
+    T2s = {L: _temperature_p2(M, L) for L in (1, 2)}
+    pv = {L: M.from_canonical(L, hhg.HHG_P2VEC, uniform_vec(M.canonical_keys(L, hhg.HHG_P2), 6)) for L in (2, 3)}
+    mg = hhg.MG(M, 1, 3, etas, pv, T2_per_level=T2s, l_eta=2, qeta=qeta)
+    for L in (2, 3):
+        assert abs(mg.lam(L) - H.lam[L]) <= 1e-12 * H.lam[L]
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        x = mg.vcycle(lib_u(M, 3, 4), stream=s)
+    s.synchronize()
+    assert rel_l2(canon(M, 3, hhg.HHG_P2VEC, x), x_o) <= TOL_VCYCLE
+
+
 def test_shell_level2_diag_and_dot(shell_l2):
     mac, lm, d, eta_o, M = shell_l2
     eta = lib_eta(M, 2, C2)

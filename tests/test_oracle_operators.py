@@ -228,3 +228,22 @@ def test_buoyancy_load_closed_forms():
     T1, T2 = rng.uniform(0, 1, lm.n_p1), rng.uniform(0, 1, lm.n_p1)
     lin = buoyancy_load(lm, True, 2 * T1 - T2)
     assert np.abs(lin - (2 * buoyancy_load(lm, True, T1) - buoyancy_load(lm, True, T2) - buoyancy_load(lm, True, half))).max() < 1e-14
+
+
+def test_quadrature_point_viscosity_tier_special_cases():
+    """NEXT-2 tier: with a constant temperature T = t0 and no jump the quadrature-point
+    viscosity is the constant exp(lnC (1/2 - t0)), so A equals the P1-eta operator with that constant;
+    a jump radius beyond the domain multiplies A by the jump factor."""
+    from oracle.refine import build_level
+    from oracle.operators import Discretisation
+    from workload import icoshell
+    m = icoshell(3, 2)
+    lm = build_level(m.verts, m.tets, m.vtag, 1)
+    lnC, t0 = np.log(1e4), 0.3
+    T = np.full(lm.n_p2, t0)
+    dq = Discretisation(lm, True, None, 0.0, {}, build=("A",), T_p2=T, qeta=(lnC, 1.0, 0.0))
+    e = np.exp(lnC * (0.5 - t0))
+    dp = Discretisation(lm, True, np.full(lm.n_p1, e), 0.0, {}, build=("A",))
+    assert abs(dq.A - dp.A).max() <= 1e-13 * abs(dp.A).max()
+    dj = Discretisation(lm, True, None, 0.0, {}, build=("A",), T_p2=T, qeta=(lnC, 30.0, 2.0))
+    assert abs(dj.A - 30.0 * dq.A).max() <= 1e-13 * abs(dj.A).max()
