@@ -19,13 +19,23 @@ ap.add_argument("--restart", type=int, default=30)
 ap.add_argument("--deg", type=int, default=2, help="Chebyshev degree of the A-block V-cycle (Table 1: 2)")
 ap.add_argument("--contrast", type=float, default=1e6)
 ap.add_argument("--jump", type=float, default=30.0)
+ap.add_argument("--l-eta", type=int, default=-1, help="levels <= l_eta use quadrature-point viscosity (NEXT-2)")
 a = ap.parse_args()
 L = a.level
 M, etas, v0, _, n_dof = build_case(L, 0, contrast=a.contrast, jump=a.jump)
+def temp_p2(l):
+    keys2 = M.canonical_keys(l, hhg.HHG_P2)
+    xyz2 = M.node_coords(l, hhg.HHG_P2)
+    xc2 = torch.stack([M.to_canonical(l, hhg.HHG_P2, xyz2[:, c].contiguous()) for c in range(3)], 1)
+    return M.from_canonical(l, hhg.HHG_P2, temperature(xc2.cpu().numpy(), keys2))
+import math
+T2s = {l: temp_p2(l) for l in range(1, a.l_eta + 1)} if a.l_eta >= 1 else None
+qeta = (math.log(a.contrast), a.jump, 0.9)
 t0 = time.perf_counter()
-mg = hhg.MG(M, 1, L, etas, v0, pre=3, post=3, degree=a.deg)
+mg = hhg.MG(M, 1, L, etas, v0, pre=3, post=3, degree=a.deg, T2_per_level=T2s, l_eta=a.l_eta, qeta=qeta)
 v0c = {l: v.clone() for l, v in build_case(L, 0, contrast=a.contrast, jump=a.jump)[2].items()} if a.schur == "vbfbt" else None
-mgc = hhg.MG(M, 1, L, etas, v0c, pre=1, post=1, degree=1) if a.schur == "vbfbt" else None
+mgc = hhg.MG(M, 1, L, etas, v0c, pre=1, post=1, degree=1, T2_per_level=T2s, l_eta=a.l_eta, qeta=qeta) \
+    if a.schur == "vbfbt" else None
 keys = M.canonical_keys(L, hhg.HHG_P1)
 xyz = M.node_coords(L, hhg.HHG_P1)
 xc = torch.stack([M.to_canonical(L, hhg.HHG_P1, xyz[:, c].contiguous()) for c in range(3)], 1)
@@ -46,6 +56,6 @@ s.synchronize()
 ms = e0.elapsed_time(e1)
 n_p = M.canonical_len(L, hhg.HHG_P1)
 x2, ita, rela = mg.ablock_cg(f, tol=1e-2, max_iters=200)
-print(json.dumps({"what": "stokes_solve", "ablock_cg_iters_tol1e-2": ita, "ablock_rel": rela, "level": L, "schur": a.schur, "velocity_dofs": n_dof, "pressure_dofs": n_p,
+print(json.dumps({"what": "stokes_solve", "l_eta": a.l_eta, "ablock_cg_iters_tol1e-2": ita, "ablock_rel": rela, "level": L, "schur": a.schur, "velocity_dofs": n_dof, "pressure_dofs": n_p,
                   "fgmres_iters": it, "rel_res": rel, "tol": a.tol, "solve_s": ms / 1e3, "setup_s": setup,
                   "viscosity": f"contrast {a.contrast:g} x {a.jump:g} jump", "rhs": "buoyancy (T - 1/2) x/|x|, g = 0"}))
