@@ -315,6 +315,7 @@ typedef struct {
   int schur;                   /* 0: S = M_{1/eta} (eq:schurMass); 1: V-cycle BFBT (eq:schurV) */
   double tol_vbfbt;            /* CG tolerance for B A_C^-1 B^T (Table 1: 1e-1), M_{1/eta}-preconditioned */
   int vbfbt_max_iters;
+  int uzawa;                   /* 0 symmetric (default), 1 inexact, 2 adjoint inexact */
 } hhg_stokes_params;
 typedef struct hhg_stokes hhg_stokes;
 int hhg_stokes_create(hhg_mg* mg, hhg_mg* mg_cheap /*NULL unless schur = 1*/, const double* eta_p1, double gamma,

@@ -57,8 +57,9 @@ class StokesOracle:
 
     def __init__(self, H: Hierarchy, disc, Mmass, sigma=1.0, omega=0.3, tol_A=1e-2, ablock_max_iters=200,
                  tol_mass=1e-10, mass_max_iters=500, schur="mass", HC: Hierarchy = None, tol_vbfbt=1e-1,
-                 vbfbt_max_iters=100):
+                 vbfbt_max_iters=100, uzawa="symmetric"):
         self.schur, self.HC, self.tol_vbfbt, self.vbfbt_max_iters = schur, HC, tol_vbfbt, vbfbt_max_iters
+        self.uzawa = uzawa
         self.H, self.d = H, disc
         self.A = H.Ac[H.lmax]
         self.Pm = disc.Pm
@@ -110,12 +111,23 @@ class StokesOracle:
         y2 = mean0(self.B @ (self.Pm @ w))
         return self.bacbt_solve(y2)
 
+    def schur_step(self, t):
+        sinv = self.vbfbt(t) if self.schur == "vbfbt" else mass_cg(self.M, t, self.tol_mass, self.mass_max_iters)
+        return mean0(-self.omega * sinv)
+
     def prec(self, r):
+        """One Uzawa step from (0, 0): symmetric (eq:SymmetricUzawaStep1), inexact
+        (eq:InexactUzawaStep1) or adjoint inexact (eq:AdjointInexactUzawaStep1)."""
         ru, rp = r[:self.n2], r[self.n2:]
+        if self.uzawa == "adjoint":
+            p = self.schur_step(mean0(rp))
+            u = self.sigma * ablock_cg(self.H, ru - self.Pm @ (self.B.T @ p), self.tol_A, self.ablock_max_iters)[0]
+            return np.concatenate([u, p])
         uh = self.sigma * ablock_cg(self.H, ru, self.tol_A, self.ablock_max_iters)[0]
         tp = mean0(rp - self.Bbar @ (self.Pm @ uh))
-        sinv = self.vbfbt(tp) if self.schur == "vbfbt" else mass_cg(self.M, tp, self.tol_mass, self.mass_max_iters)
-        p = mean0(-self.omega * sinv)
+        p = self.schur_step(tp)
+        if self.uzawa == "inexact":
+            return np.concatenate([uh, p])
         tu = ru - (self.A @ uh + self.Pm @ (self.B.T @ p))
         u = uh + self.sigma * ablock_cg(self.H, tu, self.tol_A, self.ablock_max_iters)[0]
         return np.concatenate([u, p])

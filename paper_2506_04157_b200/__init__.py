@@ -534,7 +534,8 @@ class _StokesParams(ctypes.Structure):
     _fields_ = [("restart", ctypes.c_int), ("max_iters", ctypes.c_int), ("tol", ctypes.c_double),
                 ("sigma", ctypes.c_double), ("omega", ctypes.c_double), ("tol_A", ctypes.c_double),
                 ("ablock_max_iters", ctypes.c_int), ("tol_mass", ctypes.c_double), ("mass_max_iters", ctypes.c_int),
-                ("schur", ctypes.c_int), ("tol_vbfbt", ctypes.c_double), ("vbfbt_max_iters", ctypes.c_int)]
+                ("schur", ctypes.c_int), ("tol_vbfbt", ctypes.c_double), ("vbfbt_max_iters", ctypes.c_int),
+                ("uzawa", ctypes.c_int)]
 
 
 class StokesSolver:
@@ -543,13 +544,14 @@ class StokesSolver:
 
     def __init__(self, mg, eta, gamma, restart=30, max_iters=100, tol=1e-8, sigma=1.0, omega=0.3, tol_A=1e-2,
                  ablock_max_iters=200, tol_mass=1e-10, mass_max_iters=500, schur="mass", mg_cheap=None,
-                 tol_vbfbt=1e-1, vbfbt_max_iters=100):
+                 tol_vbfbt=1e-1, vbfbt_max_iters=100, uzawa="symmetric"):
         """schur: "mass" (S = M_{1/eta}, eq:schurMass) or "vbfbt" (eq:schurV; mg_cheap = the A_C hierarchy,
         Table 1: V(1,1) with degree-1 Chebyshev)."""
         self.mg, self.mg_cheap = mg, mg_cheap
         self._eta = eta
         prm = _StokesParams(restart, max_iters, tol, sigma, omega, tol_A, ablock_max_iters, tol_mass, mass_max_iters,
-                            1 if schur == "vbfbt" else 0, tol_vbfbt, vbfbt_max_iters)
+                            1 if schur == "vbfbt" else 0, tol_vbfbt, vbfbt_max_iters,
+                            {"symmetric": 0, "inexact": 1, "adjoint": 2}[uzawa])
         h = ctypes.c_void_p()
         _chk(_lib.hhg_stokes_create(mg.handle, None if mg_cheap is None else mg_cheap.handle, _ptr(eta), float(gamma),
                                     ctypes.byref(prm), ctypes.byref(h)))

@@ -728,11 +728,30 @@ int st_vbfbt(hhg_stokes* S, const double* t, double* z, cudaStream_t s) {
 }
 
 // z = Prec(r): one symmetric Uzawa step from (0, 0)
+int st_schur(hhg_stokes* S, const double* t, double* z, cudaStream_t s) {  // z = -omega S^-1 t, mean zero
+  if (S->prm.schur == 1) HHG_TRY(st_vbfbt(S, t, z, s));
+  else HHG_TRY(st_mass_solve(S, t, z, s));
+  HHG_TRY(launch_axpby(S->n1, 0.0, z, -S->prm.omega, z, s));
+  return st_mean0(S, z, s);
+}
+// z = Prec(r): one Uzawa step from (0, 0) -- symmetric (eq:SymmetricUzawaStep1, default), inexact
+// (eq:InexactUzawaStep1) or adjoint inexact (eq:AdjointInexactUzawaStep1), B -> B + C in the
+// pressure update
 int st_prec(hhg_stokes* S, const double* r, double* z, cudaStream_t s) {
   const int64_t n2 = S->n2, n1 = S->n1;
-  const double sig = S->prm.sigma, om = S->prm.omega;
+  const double sig = S->prm.sigma;
   int it;
   double rel;
+  if (S->prm.uzawa == 2) {
+    // adjoint: p = -omega S^-1 (r_p - (B+C) 0) ; u = sigma A^-1 (r_u - B^T p)
+    HHG_CUDA(cudaMemcpyAsync(S->t + n2, r + n2, n1 * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    HHG_TRY(st_mean0(S, S->t + n2, s));
+    HHG_TRY(st_schur(S, S->t + n2, z + n2, s));
+    HHG_TRY(divT_apply(S->mesh, S->level, z + n2, S->t, 0, (hhg_stream_t)s));
+    HHG_TRY(launch_axpby(n2, 1.0, r, -1.0, S->t, s));
+    HHG_TRY(hhg_ablock_cg(S->mg, S->t, z, S->prm.tol_A, S->prm.ablock_max_iters, &it, &rel, (hhg_stream_t)s));
+    return launch_axpby(n2, 0.0, z, sig, z, s);
+  }
   // u_hat = sigma A^-1 r_u  (z_u holds u_hat)
   HHG_TRY(hhg_ablock_cg(S->mg, r, z, S->prm.tol_A, S->prm.ablock_max_iters, &it, &rel, (hhg_stream_t)s));
   HHG_TRY(launch_axpby(n2, 0.0, z, sig, z, s));
@@ -740,10 +759,8 @@ int st_prec(hhg_stokes* S, const double* r, double* z, cudaStream_t s) {
   HHG_TRY(div_apply(S->mesh, S->level, S->gamma, z, S->t + n2, (hhg_stream_t)s));
   HHG_TRY(launch_axpby(n1, 1.0, r + n2, -1.0, S->t + n2, s));
   HHG_TRY(st_mean0(S, S->t + n2, s));
-  if (S->prm.schur == 1) HHG_TRY(st_vbfbt(S, S->t + n2, z + n2, s));
-  else HHG_TRY(st_mass_solve(S, S->t + n2, z + n2, s));
-  HHG_TRY(launch_axpby(n1, 0.0, z + n2, -om, z + n2, s));
-  HHG_TRY(st_mean0(S, z + n2, s));
+  HHG_TRY(st_schur(S, S->t + n2, z + n2, s));
+  if (S->prm.uzawa == 1) return HHG_OK;  // inexact: (u_hat, p)
   // t_u = r_u - A u_hat - B^T p ; u = u_hat + sigma A^-1 t_u
   HHG_TRY(stokes_apply(S->mesh, S->level, S->eta, S->gamma, z, z + n2, S->t, S->a + n2, (hhg_stream_t)s));
   HHG_TRY(launch_axpby(n2, 1.0, r, -1.0, S->t, s));
@@ -760,6 +777,7 @@ int hhg_stokes_create(hhg_mg* mg, hhg_mg* mg_cheap, const double* eta_p1, double
   if (prm->restart < 1 || prm->max_iters < 1 || !(prm->tol > 0) || !(prm->tol_A > 0) || !(prm->tol_mass > 0))
     return fail(HHG_EINVAL, "hhg_stokes_create: bad parameters");
   if (prm->schur != 0 && prm->schur != 1) return fail(HHG_EINVAL, "hhg_stokes_create: schur must be 0 (mass) or 1 (V-BFBT)");
+  if (prm->uzawa < 0 || prm->uzawa > 2) return fail(HHG_EINVAL, "hhg_stokes_create: uzawa must be 0, 1 or 2");
   if (prm->schur == 1 && (!mg_cheap || mg_cheap->mesh != mg->mesh || mg_cheap->prm.l_max != mg->prm.l_max ||
                           !(prm->tol_vbfbt > 0) || prm->vbfbt_max_iters < 1))
     return fail(HHG_EINVAL, "hhg_stokes_create: V-BFBT needs a cheap hierarchy on the same mesh/levels and tol_vbfbt");

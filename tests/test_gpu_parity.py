@@ -377,9 +377,12 @@ def test_ablock_cg_vcycle_preconditioned(ablock_case, tol):
     assert rel_l2(canon(M, 3, hhg.HHG_P2VEC, x), x_o) <= TOL_VCYCLE
 
 
-@pytest.mark.parametrize("eta_cj,tol,max_iters,schur", [(None, 1e-6, 80, "mass"), (C2, 1e-6, 20, "mass"),
-                                                        (None, 1e-6, 60, "vbfbt")])
-def test_stokes_fgmres_uzawa_solve(eta_cj, tol, max_iters, schur):
+@pytest.mark.parametrize("eta_cj,tol,max_iters,schur,uzawa", [(None, 1e-6, 80, "mass", "symmetric"),
+                                                              (C2, 1e-6, 20, "mass", "symmetric"),
+                                                              (None, 1e-6, 60, "vbfbt", "symmetric"),
+                                                              (None, 1e-6, 80, "mass", "inexact"),
+                                                              (None, 1e-6, 80, "mass", "adjoint")])
+def test_stokes_fgmres_uzawa_solve(eta_cj, tol, max_iters, schur, uzawa):
     """NEXT-1 Stokes solve: FGMRES + symmetric Uzawa (A^-1: V-cycle CG to 1e-2, S^-1: M_{1/eta} CG to
     1e-10), blended shell levels 2 -> 1, TALA compressibility.  Isoviscous: converges to 1e-6 in
     the same number of iterations as the oracle.  Config-2 viscosity (contrast 1e5, where the mass
@@ -395,7 +398,7 @@ def test_stokes_fgmres_uzawa_solve(eta_cj, tol, max_iters, schur):
     H = Hierarchy(discs, v0, pre=3, post=3, degree=3, power_iters=20, coarse_iters=50)
     HC = Hierarchy(discs, v0, pre=1, post=1, degree=1, power_iters=20, coarse_iters=50) if schur == "vbfbt" else None
     d = discs[2]
-    S_o = StokesOracle(H, d, d.M, sigma=1.0, omega=0.3, tol_A=1e-2, schur=schur, HC=HC)
+    S_o = StokesOracle(H, d, d.M, sigma=1.0, omega=0.3, tol_A=1e-2, schur=schur, HC=HC, uzawa=uzawa)
     rhs_o = np.concatenate([uniform_vec(d.lm.p2_keys, 2), uniform_from_keys(d.lm.p1_keys, 3, 0)])
     x_o, it_o, rel_o = S_o.solve(rhs_o, tol=tol, restart=max_iters, max_iters=max_iters)
     M = lib_mesh(mac, 2, True, BC_SHELL)
@@ -405,7 +408,7 @@ def test_stokes_fgmres_uzawa_solve(eta_cj, tol, max_iters, schur):
     pvc = {2: M.from_canonical(2, hhg.HHG_P2VEC, uniform_vec(M.canonical_keys(2, hhg.HHG_P2), 6))}  # fresh start
     mgc = hhg.MG(M, 1, 2, etas, pvc, pre=1, post=1, degree=1, power_iters=20, coarse_iters=50) if schur == "vbfbt" else None
     S = hhg.StokesSolver(mg, etas[2], GAMMA_TALA, restart=max_iters, max_iters=max_iters, tol=tol, sigma=1.0,
-                         omega=0.3, tol_A=1e-2, schur=schur, mg_cheap=mgc)
+                         omega=0.3, tol_A=1e-2, schur=schur, mg_cheap=mgc, uzawa=uzawa)
     ru = M.from_canonical(2, hhg.HHG_P2VEC, uniform_vec(M.canonical_keys(2, hhg.HHG_P2), 2))
     rhs = torch.cat([ru, lib_p(M, 2, 3)])
     s = torch.cuda.Stream()

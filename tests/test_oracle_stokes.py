@@ -75,3 +75,20 @@ def test_fgmres_uzawa_vbfbt_recovers_a_manufactured_solution(tet_case):
     assert rel <= 1e-10
     assert np.linalg.norm(x[:n2] - xs[:n2]) <= 1e-8 * np.linalg.norm(xs[:n2])
     assert np.linalg.norm(S.op(x - xs)) <= 1e-9 * np.linalg.norm(rhs)
+
+
+@pytest.mark.parametrize("uzawa", ["inexact", "adjoint"])
+def test_uzawa_variants_recover_a_manufactured_solution(tet_case, uzawa):
+    """Inexact (eq:InexactUzawaStep1) and adjoint inexact (eq:AdjointInexactUzawaStep1) Uzawa as
+    FGMRES preconditioners also reach the manufactured velocity."""
+    discs, H = tet_case
+    d = discs[2]
+    S = StokesOracle(H, d, d.M, tol_A=1e-2, uzawa=uzawa)
+    n2 = 3 * d.lm.n_p2
+    xs = np.concatenate([d.project(uniform_vec(d.lm.p2_keys, 2)), uniform_from_keys(d.lm.p1_keys, 3, 0)])
+    xs[n2:] -= xs[n2:].mean()
+    rhs = S.op(xs)
+    x, it, rel = S.solve(rhs, tol=1e-10, restart=80, max_iters=200)
+    assert rel <= 1e-10
+    assert np.linalg.norm(x[:n2] - xs[:n2]) <= 1e-7 * np.linalg.norm(xs[:n2])  # residual 1e-10 x conditioning
+
