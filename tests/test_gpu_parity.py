@@ -476,3 +476,29 @@ def test_config3_full_size_sampled_rows_and_vcycle_properties():
     assert torch.count_nonzero(x0).item() == 0
     assert float((M.apply_bc(L, xa.clone()) - xa).norm()) <= 1e-14 * nx
     assert torch.isfinite(xa).all()
+
+
+@pytest.mark.slow
+def test_maximum_size_level7_apply_properties():
+    """Config 5's largest single-GPU size: shell(3,2) at L7 (2.02e9 velocity dofs, 503 M micro tets).
+    Properties that hold at any size: rigid translations are in the kernel of the blended A (their
+    gradient vanishes exactly at every quadrature point), A is linear (A(2u) = 2 A(u) to rounding of
+    the RED order) and the unconstrained apply of a seeded field is finite."""
+    mac = icoshell(3, 2)
+    L = 7
+    M = hhg.Mesh.from_macro(mac, L)
+    M.blend_map(hhg.HHG_BLEND_SHELL)
+    n = M.vec_len(L, hhg.HHG_P2VEC)
+    assert n >= 3 * 240 * 2862209   # 3 components x 240 macros x P2 nodes per macro at L7
+    u = torch.zeros(n, dtype=torch.float64, device="cuda")
+    u[: n // 3] = 1.0                       # translation e_x on every copy
+    y = hhg.epsilon_apply(M, L, None, u)
+    assert float(y.abs().max()) <= 1e-9
+    del y, u
+    g = torch.Generator(device="cuda").manual_seed(7)
+    v = torch.rand(n, dtype=torch.float64, device="cuda", generator=g)
+    M.interface_sum(L, hhg.HHG_P2VEC, v)   # consistent copies
+    y1 = hhg.epsilon_apply(M, L, None, v)
+    y2 = hhg.epsilon_apply(M, L, None, (2.0 * v).contiguous())
+    assert torch.isfinite(y1).all()
+    assert float((y2 - 2.0 * y1).norm()) <= 1e-12 * float(y2.norm())
