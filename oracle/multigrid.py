@@ -59,6 +59,28 @@ def p2_prolongation(coarse: LevelMesh, fine: LevelMesh) -> sp.csr_matrix:
     return P
 
 
+def p1_prolongation(coarse: LevelMesh, fine: LevelMesh) -> sp.csr_matrix:
+    """Scalar P1 prolongation P[f, c] = lam_c^coarse(x_f): nodal (linear) interpolation of the coarse
+    P1 function at the fine P1 nodes (nested P1 spaces; the K_{1/sqrt(eta)} multigrid of P:470)."""
+    nc = 2 ** coarse.level
+    beta = np.array([(a, b, c, 2 - a - b - c) for a in range(3) for b in range(3 - a)
+                     for c in range(3 - a - b)], dtype=np.int64)       # (10,4) over coarse-tet vertices
+    lam = beta.astype(np.float64) / 2.0                                # barycentric coordinates
+    T = coarse.n_tets
+    w = np.einsum("pv,tvm->tpm", beta, coarse.tet_w)                  # fine-node weights at res 2 nc
+    mids = coarse.macro_tets[coarse.tet_macro]
+    keys = keys_from_weights(w.reshape(-1, 4), 2 * nc, np.repeat(mids, 10, axis=0))
+    frow = lookup_keys(fine.p1_keys, keys).reshape(T, 10)
+    rows = np.broadcast_to(frow[:, :, None], (T, 10, 4)).ravel()
+    cols = np.broadcast_to(coarse.tet_p1[:, None, :], (T, 10, 4)).ravel()
+    vals = np.broadcast_to(lam[None], (T, 10, 4)).ravel()
+    keep = vals > 0
+    rc = np.stack([rows[keep], cols[keep]], axis=1)
+    rc_u, first = np.unique(rc, axis=0, return_index=True)
+    return sp.coo_matrix((vals[keep][first], (rc_u[:, 0], rc_u[:, 1])),
+                         shape=(fine.n_p1, coarse.n_p1)).tocsr()
+
+
 def vec_prolongation(Ps: sp.csr_matrix) -> sp.csr_matrix:
     """Componentwise (node-major, xyz interleaved) version of the scalar prolongation."""
     return sp.kron(Ps, sp.identity(3), format="csr")

@@ -15,6 +15,11 @@ Definitions followed:
   free-slip projection P_v at CMB nodes, u <- u - (u.n) n (P:331-340);
   the constrained operator is (M P_v) A (P_v M).  diag(A) WITHOUT P_v.
 
+Weighted-BFBT pieces (eq:schurWBFBT and the a_l / a_r variant):
+  K_ij = int omega grad(lam_j) . grad(lam_i),  omega = 1/sqrt(eta_a)  (P1, Neumann: no constraints)
+  VM_(a,c),(b,d) = delta_cd int sqrt(eta_a) phi_a phi_b                (P2 vector mass)
+  eta_a = a^2 eta on D_eta (micro tets with a vertex on the surface, the outer boundary), else eta.
+
 The element matrices are computed one quadrature point at a time from these
 formulas (numpy) and summed into scipy CSR matrices (assembly = the plain
 definition of the matrix-free apply).
@@ -35,9 +40,9 @@ def macro_blend(lm: LevelMesh):
     return fe.shell_blend_params(lm.macro_verts[lm.macro_tets])
 
 
-def quad_geometry(lm: LevelMesh, tets: np.ndarray, blended: bool, blend_params=None):
+def quad_geometry(lm: LevelMesh, tets: np.ndarray, blended: bool, blend_params=None, p1_grads=False):
     """For the micro tets `tets`: per quadrature point the weight w_q |det J|, the physical
-    P2 gradients (T,Q,10,3), the blended point x_q (T,Q,3)."""
+    P2 gradients (T,Q,10,3), the blended point x_q (T,Q,3) [, the physical P1 gradients (T,Q,4,3)]."""
     xi, w = fe.q4_rule()
     X = lm.X[tets]                                          # (T,4,3)
     JF = np.stack([X[:, 1] - X[:, 0], X[:, 2] - X[:, 0], X[:, 3] - X[:, 0]], axis=2)  # columns
@@ -45,6 +50,8 @@ def quad_geometry(lm: LevelMesh, tets: np.ndarray, blended: bool, blend_params=N
     T, Q = len(tets), len(w)
     W = np.empty((T, Q))
     grads = np.empty((T, Q, 10, 3))
+    g1 = np.empty((T, Q, 4, 3))
+    DL = np.array([[-1.0, -1.0, -1.0], [1.0, 0.0, 0.0], [0.0, 1.0, 0.0], [0.0, 0.0, 1.0]])
     xq_all = np.empty((T, Q, 3))
     if blended:
         nhat_m, c_m = blend_params
@@ -63,6 +70,9 @@ def quad_geometry(lm: LevelMesh, tets: np.ndarray, blended: bool, blend_params=N
         W[:, q] = w[q] * np.abs(np.linalg.det(J))
         # grad_x phi (row) = grad_xi phi (row) J^-1
         grads[:, q] = np.einsum("am,tmd->tad", G[q], Jinv)
+        g1[:, q] = np.einsum("am,tmd->tad", DL, Jinv)
+    if p1_grads:
+        return W, grads, xq_all, g1
     return W, grads, xq_all
 
 
@@ -113,6 +123,26 @@ def element_M(W, eta_q):
     return np.einsum("tq,qp,qr->tpr", W / eta_q, lam, lam)
 
 
+def element_K(W, g1, omega_q):
+    """(T,4,4): K_K[p,r] = sum_q W omega_q grad lam_p . grad lam_r (P1 Laplacian weighted by omega)."""
+    return np.einsum("tq,tqpd,tqrd->tpr", W * omega_q, g1, g1)
+
+
+def element_VM(W, omega_q):
+    """(T,30,30): vector mass weighted by omega, VM[(a,c),(b,d)] = delta_cd sum_q W omega_q phi_a phi_b."""
+    xi, _ = fe.q4_rule()
+    phi = fe.p2_basis(xi)                                   # (Q,10)
+    Ms = np.einsum("tq,qa,qb->tab", W * omega_q, phi, phi)  # (T,10,10)
+    return np.einsum("tab,cd->tacbd", Ms, np.eye(3)).reshape(W.shape[0], 30, 30)
+
+
+def surface_tets(lm: LevelMesh, outer_tag=2) -> np.ndarray:
+    """D_eta of P:474-478: micro tets with at least one vertex on the surface (boundary faces tagged
+    `outer_tag`), by node keys (a node is on the surface iff its primitive lies in such a face)."""
+    on = node_bc(lm.p1_keys, lm.macro_tets, lm.macro_vtag, {outer_tag: BC_DIRICHLET}) != 0
+    return on[lm.tet_p1].any(axis=1)
+
+
 def p2vec_dofs(tet_p2: np.ndarray) -> np.ndarray:
     return (3 * tet_p2[:, :, None] + np.arange(3)[None, None, :]).reshape(tet_p2.shape[0], 30)
 
@@ -121,10 +151,12 @@ class Discretisation:
     """Assembled operators of one level.  eta_p1: nodal P1 viscosity (canonical order) or None (=1)."""
 
     def __init__(self, lm: LevelMesh, blended: bool, eta_p1=None, gamma=0.0,
-                 bc_by_tag=None, form=FORM_FULL, chunk=20000, build=("A", "B", "C"), T_p2=None, qeta=None):
+                 bc_by_tag=None, form=FORM_FULL, chunk=20000, build=("A", "B", "C"), T_p2=None, qeta=None,
+                 surf_a=1.0):
         """T_p2 + qeta = (lnC, jump, r_jump): A uses eta at the quadrature points,
         eta_q = exp(lnC (1/2 - T_q)) (jump if |x_q| < r_jump else 1), T_q = P2 interpolant of the nodal
-        temperature (the quadrature-point tier of P:451-453, R22); else the P1 eta."""
+        temperature (the quadrature-point tier of P:451-453, R22); else the P1 eta.
+        build "K" / "VM": the w-BFBT operators with eta_a = surf_a^2 eta on D_eta."""
         self.lm = lm
         self.blended = blended
         self.blend_params = macro_blend(lm) if blended else None
@@ -134,9 +166,10 @@ class Discretisation:
         eta_p1 = np.ones(n1) if eta_p1 is None else np.asarray(eta_p1, dtype=np.float64)
         self.eta_p1 = eta_p1
         mats = {k: None for k in build}
+        dsurf = surface_tets(lm) if ("K" in build or "VM" in build) else None
         for s in range(0, lm.n_tets, chunk):
             tets = np.arange(s, min(s + chunk, lm.n_tets))
-            W, grads, xq = quad_geometry(lm, tets, blended, self.blend_params)
+            W, grads, xq, g1 = quad_geometry(lm, tets, blended, self.blend_params, p1_grads=True)
             vd = p2vec_dofs(lm.tet_p2[tets])
             pd = lm.tet_p1[tets]
             if "A" in build:
@@ -164,10 +197,21 @@ class Discretisation:
                 eta_q = eta_p1[pd] @ fe.p1_basis(xi).T
                 M = _coo(element_M(W, eta_q), pd, pd, n1, n1)
                 mats["M"] = M if mats["M"] is None else mats["M"] + M
+            if "K" in build or "VM" in build:
+                xi, _ = fe.q4_rule()
+                eta_a = (eta_p1[pd] @ fe.p1_basis(xi).T) * np.where(dsurf[tets], surf_a ** 2, 1.0)[:, None]
+                if "K" in build:
+                    M = _coo(element_K(W, g1, 1.0 / np.sqrt(eta_a)), pd, pd, n1, n1)
+                    mats["K"] = M if mats["K"] is None else mats["K"] + M
+                if "VM" in build:
+                    M = _coo(element_VM(W, np.sqrt(eta_a)), vd, vd, 3 * n2, 3 * n2)
+                    mats["VM"] = M if mats["VM"] is None else mats["VM"] + M
         self.A = mats.get("A")
         self.B = mats.get("B")
         self.C = mats.get("C")
         self.M = mats.get("M")
+        self.K = mats.get("K")
+        self.VM = mats.get("VM")
         # constraints
         self.bc = node_bc(lm.p2_keys, lm.macro_tets, lm.macro_vtag, bc_by_tag or {})
         self.Pm = constraint_matrix(lm.p2_xt, self.bc)

@@ -9,6 +9,10 @@ order.
       u_hat = sigma A^-1 r_u ; p = -omega S^-1 (r_p - (B+C) u_hat) ; u = u_hat + sigma A^-1 (r_u - A u_hat - B^T p)
   A^-1: CG preconditioned by the V-cycle to tol_A (P:441, multigrid.ablock_cg);
   S^-1: M_{1/eta}^-1 by Jacobi-preconditioned CG to tol_mass (eq:schurMass).
+  schur="wbfbt": the weighted BFBT with the a_l / a_r surface scaling (eq:schurWBFBT),
+      S_w^-1 = K_l^-1 (B VM_l^-1 A VM_r^-1 B^T) K_r^-1,
+  K = K_{1/sqrt(eta_a)} (Neumann, solved exactly on the mean-zero space), VM = M_{sqrt(eta_a)} (solved
+  exactly on the constrained velocity space) -- the library solves both iteratively to tolerance.
 Readings (R17-R19): P_p applied to the rhs, to every operator output and to the
 preconditioned pressure; relative residual stopping; Table 1 defaults (sigma 1, omega 0.3,
 tol_A 1e-2, tol_mass 1e-10).
@@ -22,6 +26,35 @@ from .multigrid import Hierarchy, ablock_cg
 
 def mean0(p):
     return p - p.mean()
+
+
+_LU = {}
+
+
+def _lu(key, refs, build):
+    """Sparse LU factorisation, computed once per (matrix, system) and reused for every solve.  The
+    cache holds the matrices themselves so that their ids (the key) cannot be recycled."""
+    import scipy.sparse.linalg as spla
+    if key not in _LU:
+        _LU[key] = (refs, spla.splu(build()))
+    return _LU[key][1]
+
+
+def neumann_solve(K, t):
+    """y with K y = t and sum(y) = 0 (t must sum to zero): the augmented system [[K, e], [e^T, 0]]."""
+    import scipy.sparse as sp
+    n = K.shape[0]
+    e = sp.csr_matrix(np.ones((n, 1)))
+    lu = _lu(("K", id(K)), (K,), lambda: sp.bmat([[K, e], [e.T, None]], format="csc"))
+    return lu.solve(np.concatenate([t, [0.0]]))[:n]
+
+
+def constrained_solve(VM, Pm, v):
+    """x = (P VM P)^-1 P v on the constrained velocity space (regularised by I - P)."""
+    import scipy.sparse as sp
+    n = VM.shape[0]
+    lu = _lu(("VM", id(VM), id(Pm)), (VM, Pm), lambda: (Pm @ VM @ Pm + (sp.identity(n) - Pm)).tocsc())
+    return Pm @ lu.solve(Pm @ v)
 
 
 def mass_cg(M, r, tol=1e-10, max_iters=500):
@@ -57,7 +90,9 @@ class StokesOracle:
 
     def __init__(self, H: Hierarchy, disc, Mmass, sigma=1.0, omega=0.3, tol_A=1e-2, ablock_max_iters=200,
                  tol_mass=1e-10, mass_max_iters=500, schur="mass", HC: Hierarchy = None, tol_vbfbt=1e-1,
-                 vbfbt_max_iters=100, uzawa="symmetric"):
+                 vbfbt_max_iters=100, uzawa="symmetric", wbfbt_ops=None):
+        """wbfbt_ops = (K_l, K_r, VM_l, VM_r) for schur="wbfbt"."""
+        self.wb = wbfbt_ops
         self.schur, self.HC, self.tol_vbfbt, self.vbfbt_max_iters = schur, HC, tol_vbfbt, vbfbt_max_iters
         self.uzawa = uzawa
         self.H, self.d = H, disc
@@ -111,8 +146,21 @@ class StokesOracle:
         y2 = mean0(self.B @ (self.Pm @ w))
         return self.bacbt_solve(y2)
 
+    def wbfbt(self, t):
+        """S_w^-1 t = K_l^-1 (B VM_l^-1 A VM_r^-1 B^T) K_r^-1 t."""
+        Kl, Kr, VMl, VMr = self.wb
+        y = neumann_solve(Kr, mean0(t))
+        w = constrained_solve(VMr, self.Pm, self.Pm @ (self.B.T @ y))
+        w = constrained_solve(VMl, self.Pm, self.A @ w)
+        return neumann_solve(Kl, mean0(self.B @ (self.Pm @ w)))
+
     def schur_step(self, t):
-        sinv = self.vbfbt(t) if self.schur == "vbfbt" else mass_cg(self.M, t, self.tol_mass, self.mass_max_iters)
+        if self.schur == "vbfbt":
+            sinv = self.vbfbt(t)
+        elif self.schur == "wbfbt":
+            sinv = self.wbfbt(t)
+        else:
+            sinv = mass_cg(self.M, t, self.tol_mass, self.mass_max_iters)
         return mean0(-self.omega * sinv)
 
     def prec(self, r):
