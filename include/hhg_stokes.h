@@ -316,6 +316,13 @@ typedef struct {
   double tol_vbfbt;            /* CG tolerance for B A_C^-1 B^T (Table 1: 1e-1), M_{1/eta}-preconditioned */
   int vbfbt_max_iters;
   int uzawa;                   /* 0 symmetric (default), 1 inexact, 2 adjoint inexact */
+  /* schur = 2: weighted BFBT (eq:schurWBFBT with the a_l / a_r surface scaling) */
+  double a_l, a_r;             /* eta_l = a_l^2 eta, eta_r = a_r^2 eta on D_eta (1, 1: plain w-BFBT) */
+  double tol_wbfbt;            /* K_{1/sqrt(eta)} GMG-CG: relative tolerance ... */
+  double tol_wbfbt_abs;        /* ... or absolute residual 2-norm, whichever is met first */
+  int wbfbt_max_iters;
+  double tol_vmass;            /* M_{sqrt(eta)} Jacobi-CG relative tolerance (reading R24) */
+  int vmass_max_iters;
 } hhg_stokes_params;
 typedef struct hhg_stokes hhg_stokes;
 int hhg_stokes_create(hhg_mg* mg, hhg_mg* mg_cheap /*NULL unless schur = 1*/, const double* eta_p1, double gamma,
@@ -323,6 +330,42 @@ int hhg_stokes_create(hhg_mg* mg, hhg_mg* mg_cheap /*NULL unless schur = 1*/, co
 int hhg_stokes_solve(hhg_stokes* solver, const double* rhs, double* x, int* iters, double* rel_res,
                      hhg_stream_t stream);
 int hhg_stokes_destroy(hhg_stokes* solver);
+/* z = S^-1 t for the solver's Schur approximation (schur 0: M_{1/eta}^-1, 1: S_V^-1, 2: S_w^-1), without
+ * the -omega of the Uzawa step; t: P1 on the finest level, projected to mean zero first; z mean zero.
+ * Synchronises (inner CG stopping tests). */
+int hhg_stokes_schur_apply(hhg_stokes* solver, const double* t, double* z, hhg_stream_t stream);
+
+/* ------------------------------------------------------------------ weighted BFBT pieces (NEXT-3)
+ * eq:schurWBFBT: S_w^-1 ~ K_{1/sqrt(eta_l)}^-1 (B M_{sqrt(eta_l)}^-1 A M_{sqrt(eta_r)}^-1 B^T)
+ * K_{1/sqrt(eta_r)}^-1 with eta_a = a^2 eta on D_eta = the micro tets with a vertex on the outer sphere
+ * (the radius of the HHG_BND_OUTER-tagged macro vertices; a != 1 needs a shell-blended mesh -> HHG_EINVAL).
+ * hhg_kp1_apply: y = K_{1/sqrt(eta_a)} p, the P1 Laplacian weighted by 1/sqrt(eta_a) (P1 eta interpolated
+ *   at the quadrature points), Neumann (no constraints); p consistent P1, y consistent P1 (overwritten).
+ * hhg_kp1_diag: its diagonal.  hhg_vmass_apply: y = (P_v M) M_{sqrt(eta_a)} u, the P2 vector mass weighted
+ *   by sqrt(eta_a) (u consistent, BC-projected P2VEC); hhg_vmass_diag: its diagonal (no P_v, like diag A).
+ * eta_p1 NULL means eta = 1.  Asynchronous on `stream`. */
+int hhg_kp1_apply(const hhg_mesh* mesh, int level, const double* eta_p1, double a, const double* p, double* y,
+                  hhg_stream_t stream);
+int hhg_kp1_diag(const hhg_mesh* mesh, int level, const double* eta_p1, double a, double* diag, hhg_stream_t stream);
+int hhg_vmass_apply(const hhg_mesh* mesh, int level, const double* eta_p1, double a, const double* u, double* y,
+                    hhg_stream_t stream);
+int hhg_vmass_diag(const hhg_mesh* mesh, int level, const double* eta_p1, double a, double* diag,
+                   hhg_stream_t stream);
+/* P1 transfers of the K multigrid: x_fine += P x_coarse (linear interpolation; consistent in, consistent
+ * out); r_coarse = P^T r_fine over unique fine nodes, then the coarse interface sum (overwritten). */
+int p1_prolong(const hhg_mesh* mesh, int coarse_level, const double* x_coarse, double* x_fine, hhg_stream_t stream);
+int p1_restrict(const hhg_mesh* mesh, int fine_level, const double* r_fine, double* r_coarse, hhg_stream_t stream);
+/* K_{1/sqrt(eta_a)}^-1 by CG preconditioned by a P1 GMG V-cycle ("a CG solver preconditioned by a
+ * GMG approach"): Chebyshev(D^-1 K) smoothing, P1 transfers, coarse Jacobi-PCG, the smoother / level /
+ * power-iteration settings of `params`; eta_per_level[l] P1 eta on level l (NULL entries: 1).
+ * hhg_kmg_solve: from x = 0, rhs projected to mean zero, until |r| <= tol |r0| or |r| <= tol_abs or
+ * max_iters; x mean zero.  Synchronises once per iteration. */
+typedef struct hhg_kmg hhg_kmg;
+int hhg_kmg_create(hhg_mesh* mesh, const hhg_mg_params* params, const double* const* eta_per_level, double a,
+                   hhg_kmg** out);
+int hhg_kmg_solve(hhg_kmg* kmg, const double* rhs, double* x, double tol, double tol_abs, int max_iters, int* iters,
+                  double* rel_res, hhg_stream_t stream);
+int hhg_kmg_destroy(hhg_kmg* kmg);
 
 /* Number of kernels launched by the library on this thread since the last reset. */
 int64_t hhg_launch_count(int reset);

@@ -43,6 +43,8 @@ EXPORTS = [
     "hhg_ablock_cg", "hhg_mass_apply", "hhg_mass_diag", "hhg_stokes_create", "hhg_stokes_solve",
     "hhg_stokes_destroy", "hhg_buoyancy_load", "hhg_icoshell_macro", "hhg_mesh_create_icoshell",
     "hhg_mg_create_qeta", "epsilon_apply_qeta", "hhg_diag_qeta",
+    "hhg_stokes_schur_apply", "hhg_kp1_apply", "hhg_kp1_diag", "hhg_vmass_apply", "hhg_vmass_diag",
+    "p1_prolong", "p1_restrict", "hhg_kmg_create", "hhg_kmg_solve", "hhg_kmg_destroy",
 ]
 
 
@@ -88,6 +90,12 @@ def _load():
         "hhg_mesh_create_icoshell": ([I, I, D, D, I, P, P, P], I),
         "hhg_mg_create_qeta": ([P, P, P, P, P, P], I), "epsilon_apply_qeta": ([P, I, P, D, D, D, P, P, P], I),
         "hhg_diag_qeta": ([P, I, P, D, D, D, P, P], I),
+        "hhg_stokes_schur_apply": ([P, P, P, P], I),
+        "hhg_kp1_apply": ([P, I, P, D, P, P, P], I), "hhg_kp1_diag": ([P, I, P, D, P, P], I),
+        "hhg_vmass_apply": ([P, I, P, D, P, P, P], I), "hhg_vmass_diag": ([P, I, P, D, P, P], I),
+        "p1_prolong": ([P, I, P, P, P], I), "p1_restrict": ([P, I, P, P, P], I),
+        "hhg_kmg_create": ([P, P, P, D, P], I), "hhg_kmg_solve": ([P, P, P, D, D, I, P, P, P], I),
+        "hhg_kmg_destroy": ([P], I),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -370,6 +378,53 @@ def hhg_mass_diag(mesh, level, eta, out=None, stream=None):
     return out
 
 
+def hhg_kp1_apply(mesh, level, eta, a, p, y=None, stream=None):
+    """y = K_{1/sqrt(eta_a)} p: P1 Laplacian weighted by 1/sqrt(eta_a), eta_a = a^2 eta on D_eta (w-BFBT)."""
+    n1 = mesh.vec_len(level, HHG_P1)
+    y = mesh.zeros(level, HHG_P1) if y is None else y
+    _chk(_lib.hhg_kp1_apply(mesh.handle, level, _dev(eta, n1, "eta"), float(a), _dev(p, n1, "p"), _dev(y, n1, "y"),
+                            _stream(stream)))
+    return y
+
+
+def hhg_kp1_diag(mesh, level, eta, a, out=None, stream=None):
+    n1 = mesh.vec_len(level, HHG_P1)
+    out = mesh.zeros(level, HHG_P1) if out is None else out
+    _chk(_lib.hhg_kp1_diag(mesh.handle, level, _dev(eta, n1, "eta"), float(a), _dev(out, n1), _stream(stream)))
+    return out
+
+
+def hhg_vmass_apply(mesh, level, eta, a, u, y=None, stream=None):
+    """y = (M P_v) M_{sqrt(eta_a)} u: P2 vector mass weighted by sqrt(eta_a) (w-BFBT)."""
+    n = mesh.vec_len(level, HHG_P2VEC)
+    y = mesh.zeros(level, HHG_P2VEC) if y is None else y
+    _chk(_lib.hhg_vmass_apply(mesh.handle, level, _dev(eta, mesh.vec_len(level, HHG_P1), "eta"), float(a),
+                              _dev(u, n, "u"), _dev(y, n, "y"), _stream(stream)))
+    return y
+
+
+def hhg_vmass_diag(mesh, level, eta, a, out=None, stream=None):
+    n = mesh.vec_len(level, HHG_P2VEC)
+    out = mesh.zeros(level, HHG_P2VEC) if out is None else out
+    _chk(_lib.hhg_vmass_diag(mesh.handle, level, _dev(eta, mesh.vec_len(level, HHG_P1), "eta"), float(a),
+                             _dev(out, n), _stream(stream)))
+    return out
+
+
+def p1_prolong(mesh, coarse_level, x_coarse, x_fine, stream=None):
+    """x_fine += P x_coarse (P1 linear interpolation)."""
+    _chk(_lib.p1_prolong(mesh.handle, coarse_level, _dev(x_coarse, mesh.vec_len(coarse_level, HHG_P1)),
+                         _dev(x_fine, mesh.vec_len(coarse_level + 1, HHG_P1)), _stream(stream)))
+    return x_fine
+
+
+def p1_restrict(mesh, fine_level, r_fine, r_coarse=None, stream=None):
+    r_coarse = mesh.zeros(fine_level - 1, HHG_P1) if r_coarse is None else r_coarse
+    _chk(_lib.p1_restrict(mesh.handle, fine_level, _dev(r_fine, mesh.vec_len(fine_level, HHG_P1)),
+                          _dev(r_coarse, mesh.vec_len(fine_level - 1, HHG_P1)), _stream(stream)))
+    return r_coarse
+
+
 def epsilon_apply_qeta(mesh, level, T2, qeta, u, y=None, stream=None):
     """y = (M P_v) A(eta) u with eta_q = exp(lnC (1/2 - T_q)) (jump if r_q < r_jump else 1) at the
     quadrature points, T_q the P2 interpolant of T2 (NEXT-2 tier); qeta = (lnC, jump, r_jump)."""
@@ -530,12 +585,43 @@ class MG:
         return dict(apply_ms_sum=a.value, apply_count=na.value, cycle_ms_sum=c.value, cycle_count=nc.value)
 
 
+class KMG:
+    """hhg_kmg_create: GMG-preconditioned CG for K_{1/sqrt(eta_a)} (the w-BFBT Poisson solve)."""
+
+    def __init__(self, mesh, l_min, l_max, eta_per_level, a=1.0, pre=3, post=3, degree=3, power_iters=20,
+                 coarse_iters=50, hi=1.1, lo=0.1):
+        self.mesh, self.l_min, self.l_max = mesh, l_min, l_max
+        prm = _MGParams(l_min, l_max, pre, post, degree, power_iters, coarse_iters, hi, lo, HHG_VISC_FULL, 0, -1,
+                        0.0, 1.0, 0.0)
+        self._eta = dict(eta_per_level or {})
+        L = l_max + 1
+        etas = (ctypes.c_void_p * L)(*[_ptr(self._eta.get(l)) for l in range(L)])
+        h = ctypes.c_void_p()
+        _chk(_lib.hhg_kmg_create(mesh.handle, ctypes.byref(prm), etas, float(a), ctypes.byref(h)))
+        self.handle = h
+
+    def __del__(self):
+        if getattr(self, "handle", None) and _lib is not None:
+            _lib.hhg_kmg_destroy(self.handle)
+            self.handle = None
+
+    def solve(self, rhs, x=None, tol=1e-8, tol_abs=0.0, max_iters=100, stream=None):
+        n = self.mesh.vec_len(self.l_max, HHG_P1)
+        x = self.mesh.zeros(self.l_max, HHG_P1) if x is None else x
+        it, rel = ctypes.c_int(), ctypes.c_double()
+        _chk(_lib.hhg_kmg_solve(self.handle, _dev(rhs, n, "rhs"), _dev(x, n, "x"), float(tol), float(tol_abs),
+                                int(max_iters), ctypes.byref(it), ctypes.byref(rel), _stream(stream)))
+        return x, it.value, rel.value
+
+
 class _StokesParams(ctypes.Structure):
     _fields_ = [("restart", ctypes.c_int), ("max_iters", ctypes.c_int), ("tol", ctypes.c_double),
                 ("sigma", ctypes.c_double), ("omega", ctypes.c_double), ("tol_A", ctypes.c_double),
                 ("ablock_max_iters", ctypes.c_int), ("tol_mass", ctypes.c_double), ("mass_max_iters", ctypes.c_int),
                 ("schur", ctypes.c_int), ("tol_vbfbt", ctypes.c_double), ("vbfbt_max_iters", ctypes.c_int),
-                ("uzawa", ctypes.c_int)]
+                ("uzawa", ctypes.c_int), ("a_l", ctypes.c_double), ("a_r", ctypes.c_double),
+                ("tol_wbfbt", ctypes.c_double), ("tol_wbfbt_abs", ctypes.c_double), ("wbfbt_max_iters", ctypes.c_int),
+                ("tol_vmass", ctypes.c_double), ("vmass_max_iters", ctypes.c_int)]
 
 
 class StokesSolver:
@@ -544,14 +630,17 @@ class StokesSolver:
 
     def __init__(self, mg, eta, gamma, restart=30, max_iters=100, tol=1e-8, sigma=1.0, omega=0.3, tol_A=1e-2,
                  ablock_max_iters=200, tol_mass=1e-10, mass_max_iters=500, schur="mass", mg_cheap=None,
-                 tol_vbfbt=1e-1, vbfbt_max_iters=100, uzawa="symmetric"):
-        """schur: "mass" (S = M_{1/eta}, eq:schurMass) or "vbfbt" (eq:schurV; mg_cheap = the A_C hierarchy,
-        Table 1: V(1,1) with degree-1 Chebyshev)."""
+                 tol_vbfbt=1e-1, vbfbt_max_iters=100, uzawa="symmetric", a_l=1.0, a_r=1.0, tol_wbfbt=1e-1,
+                 tol_wbfbt_abs=0.0, wbfbt_max_iters=100, tol_vmass=1e-6, vmass_max_iters=200):
+        """schur: "mass" (S = M_{1/eta}, eq:schurMass), "vbfbt" (eq:schurV; mg_cheap = the A_C hierarchy,
+        Table 1: V(1,1) with degree-1 Chebyshev) or "wbfbt" (eq:schurWBFBT with the a_l / a_r scaling;
+        K_{1/sqrt(eta)} by GMG-CG to tol_wbfbt / tol_wbfbt_abs, M_{sqrt(eta)} by Jacobi-CG to tol_vmass)."""
         self.mg, self.mg_cheap = mg, mg_cheap
         self._eta = eta
         prm = _StokesParams(restart, max_iters, tol, sigma, omega, tol_A, ablock_max_iters, tol_mass, mass_max_iters,
-                            1 if schur == "vbfbt" else 0, tol_vbfbt, vbfbt_max_iters,
-                            {"symmetric": 0, "inexact": 1, "adjoint": 2}[uzawa])
+                            {"mass": 0, "vbfbt": 1, "wbfbt": 2}[schur], tol_vbfbt, vbfbt_max_iters,
+                            {"symmetric": 0, "inexact": 1, "adjoint": 2}[uzawa], a_l, a_r, tol_wbfbt, tol_wbfbt_abs,
+                            wbfbt_max_iters, tol_vmass, vmass_max_iters)
         h = ctypes.c_void_p()
         _chk(_lib.hhg_stokes_create(mg.handle, None if mg_cheap is None else mg_cheap.handle, _ptr(eta), float(gamma),
                                     ctypes.byref(prm), ctypes.byref(h)))
@@ -563,6 +652,12 @@ class StokesSolver:
         if getattr(self, "handle", None) and _lib is not None:
             _lib.hhg_stokes_destroy(self.handle)
             self.handle = None
+
+    def schur_apply(self, t, z=None, stream=None):
+        """z = S^-1 t of the solver's Schur approximation (no -omega), mean zero."""
+        z = self.mg.mesh.zeros(self.mg.l_max, HHG_P1) if z is None else z
+        _chk(_lib.hhg_stokes_schur_apply(self.handle, _dev(t, self.n1, "t"), _dev(z, self.n1, "z"), _stream(stream)))
+        return z
 
     def solve(self, rhs, x=None, stream=None):
         import torch

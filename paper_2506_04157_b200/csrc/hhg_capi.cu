@@ -314,6 +314,27 @@ int apply_op(const Mesh* m, int level, int mode, int form, const double* eta, do
   if (has_p) HHG_TRY(launch_fixup(m, L, HHG_P1, true, false, yp, s));
   return HHG_OK;
 }
+
+// radius of the outer boundary sphere (D_eta of the w-BFBT scaling): max |x| over outer-tagged vertices
+static double r_outer(const Mesh* m) {
+  double r = 0.0;
+  for (int64_t v = 0; v < m->n_vert; ++v)
+    if (m->vtag[v] == HHG_BND_OUTER)
+      r = std::max(r, std::sqrt(m->xyz[3 * v] * m->xyz[3 * v] + m->xyz[3 * v + 1] * m->xyz[3 * v + 1] +
+                                m->xyz[3 * v + 2] * m->xyz[3 * v + 2]));
+  return r > 0.0 ? r : 1e300;
+}
+
+// w-BFBT operators: element kernel + interface sum (+ P_v M for the vector mass apply)
+int surf_op(const Mesh* m, int level, int mode, const double* eta, double a, const double* in, double* out,
+            cudaStream_t s) {
+  const Level& L = m->levels[level];
+  const int64_t nm = macro_count(m);
+  const bool vec = (mode & (ELEM_VMASS | ELEM_VMASSD)) != 0;
+  HHG_CUDA(cudaMemsetAsync(out, 0, (vec ? 3 * nm * L.npts2 : nm * L.npts1) * sizeof(double), s));
+  HHG_TRY(launch_elem_surf(m, L, mode, eta, a, r_outer(m), in, out, s));
+  return launch_fixup(m, L, vec ? HHG_P2VEC : HHG_P1, true, mode == ELEM_VMASS, out, s);
+}
 }  // namespace hhg
 
 extern "C" {
@@ -384,6 +405,69 @@ int hhg_mass_diag(const hhg_mesh* mesh, int level, const double* eta_p1, double*
   HHG_TRY(ensure_level(m, level));
   return apply_op(m, level, ELEM_MASSD, HHG_VISC_FULL, eta_p1, 0.0, nullptr, nullptr, nullptr, diag, false,
                   (cudaStream_t)stream);
+}
+
+int hhg_kp1_apply(const hhg_mesh* mesh, int level, const double* eta_p1, double a, const double* p, double* y,
+                  hhg_stream_t stream) {
+  HHG_TRY(check_level(mesh, level));
+  CHECK_PTR(p);
+  CHECK_PTR(y);
+  auto* m = const_cast<hhg_mesh*>(mesh);
+  HHG_TRY(ensure_level(m, level));
+  return surf_op(m, level, ELEM_KP1, eta_p1, a, p, y, (cudaStream_t)stream);
+}
+
+int hhg_kp1_diag(const hhg_mesh* mesh, int level, const double* eta_p1, double a, double* diag, hhg_stream_t stream) {
+  HHG_TRY(check_level(mesh, level));
+  CHECK_PTR(diag);
+  auto* m = const_cast<hhg_mesh*>(mesh);
+  HHG_TRY(ensure_level(m, level));
+  return surf_op(m, level, ELEM_KP1D, eta_p1, a, nullptr, diag, (cudaStream_t)stream);
+}
+
+int hhg_vmass_apply(const hhg_mesh* mesh, int level, const double* eta_p1, double a, const double* u, double* y,
+                    hhg_stream_t stream) {
+  HHG_TRY(check_level(mesh, level));
+  CHECK_PTR(u);
+  CHECK_PTR(y);
+  auto* m = const_cast<hhg_mesh*>(mesh);
+  HHG_TRY(ensure_level(m, level));
+  return surf_op(m, level, ELEM_VMASS, eta_p1, a, u, y, (cudaStream_t)stream);
+}
+
+int hhg_vmass_diag(const hhg_mesh* mesh, int level, const double* eta_p1, double a, double* diag,
+                   hhg_stream_t stream) {
+  HHG_TRY(check_level(mesh, level));
+  CHECK_PTR(diag);
+  auto* m = const_cast<hhg_mesh*>(mesh);
+  HHG_TRY(ensure_level(m, level));
+  return surf_op(m, level, ELEM_VMASSD, eta_p1, a, nullptr, diag, (cudaStream_t)stream);
+}
+
+int p1_prolong(const hhg_mesh* mesh, int coarse_level, const double* x_coarse, double* x_fine, hhg_stream_t stream) {
+  HHG_TRY(check_level(mesh, coarse_level));
+  if (coarse_level + 1 > mesh->level_max) return fail(HHG_ELEVEL, "p1_prolong: coarse_level must be < level_max");
+  CHECK_PTR(x_coarse);
+  CHECK_PTR(x_fine);
+  auto* m = const_cast<hhg_mesh*>(mesh);
+  HHG_TRY(ensure_level(m, coarse_level));
+  HHG_TRY(ensure_level(m, coarse_level + 1));
+  return launch_p1_prolong(m, m->levels[coarse_level], m->levels[coarse_level + 1], x_coarse, x_fine,
+                           (cudaStream_t)stream);
+}
+
+int p1_restrict(const hhg_mesh* mesh, int fine_level, const double* r_fine, double* r_coarse, hhg_stream_t stream) {
+  HHG_TRY(check_level(mesh, fine_level));
+  if (fine_level < 1) return fail(HHG_ELEVEL, "p1_restrict: fine_level must be >= 1");
+  CHECK_PTR(r_fine);
+  CHECK_PTR(r_coarse);
+  auto* m = const_cast<hhg_mesh*>(mesh);
+  HHG_TRY(ensure_level(m, fine_level));
+  HHG_TRY(ensure_level(m, fine_level - 1));
+  const Level& Lc = m->levels[fine_level - 1];
+  cudaStream_t s = (cudaStream_t)stream;
+  HHG_TRY(launch_p1_restrict(m, Lc, m->levels[fine_level], r_fine, r_coarse, s));
+  return launch_fixup(m, Lc, HHG_P1, true, false, r_coarse, s);
 }
 
 int div_apply(const hhg_mesh* mesh, int level, double gamma, const double* u, double* q, hhg_stream_t stream) {

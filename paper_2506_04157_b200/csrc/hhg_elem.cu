@@ -148,6 +148,7 @@ __device__ __forceinline__ void tet_body(const double* G, double wdet, const dou
 #pragma unroll
   for (int r = 0; r < 9; ++r) JFi[r] = G[r];
   double Kq[4][9], al[4] = {1.0, 1.0, 1.0, 1.0}, dq[4][3], etv[4] = {1.0, 1.0, 1.0, 1.0};
+  double sfac = 1.0;  // w-BFBT modes: a on D_eta (gamma carries a, eq.r_jump the outer radius)
   {
     double xq[4][3], sq[4], yq[4], tq[4], rq[4];
 #pragma unroll
@@ -191,6 +192,13 @@ __device__ __forceinline__ void tet_body(const double* G, double wdet, const dou
       for (int q = 0; q < 4; ++q) tq[q] = fma(nh[0], xq[q][0], fma(nh[1], xq[q][1], nh[2] * xq[q][2]));
 #pragma unroll
       for (int q = 0; q < 4; ++q) rq[q] = rcp_nr(tq[q]);
+      if ((MODE & ELEM_SURF) && gamma != 1.0) {
+        // D_eta: a vertex on the outer sphere.  Vertex m from its quadrature point,
+        // x_q(m) = EQAB x_m + EQB sum_v x_v, and the blended radius |B(x)| = c (n.x) is linear in x.
+        const double ts = EQB * (tq[0] + tq[1] + tq[2] + tq[3]);
+        const double tmax = fmax(fmax(tq[0], tq[1]), fmax(tq[2], tq[3]));
+        if (cK * (tmax - ts) * (1.0 / EQAB) >= eq.r_jump * (1.0 - 1e-9)) sfac = gamma;
+      }
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         al[q] = tq[q] * yq[q];
@@ -241,6 +249,84 @@ __device__ __forceinline__ void tet_body(const double* G, double wdet, const dou
         }
 #pragma unroll
         for (int c = 0; c < 3; ++c) acc[a][c] = fma(sq * phi, xq[c], acc[a][c]);
+      }
+    }
+    return;
+  }
+  if (MODE & (ELEM_KP1 | ELEM_KP1D)) {
+    // K_{1/sqrt(eta_a)} (w-BFBT Poisson replacement of B M^-1 B^T):
+    // K_vw = sum_q w |det J| omega_q grad lam_v . grad lam_w,  omega = 1/sqrt(eta_a),
+    // grad lam_{k+1} = row k of K_q / (c alpha_q)  =>  weight w |det J_F| c alpha_q omega_q
+#pragma unroll
+    for (int v = 0; v < 4; ++v) gy[v] = 0.0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double* K = Kq[q];
+      const double Wq = wdet * cK * al[q] / (sfac * sqrt(fma(EQAB, et[q], etaS)));
+      const double R0[3] = {K[0], K[1], K[2]}, R1[3] = {K[3], K[4], K[5]}, R2[3] = {K[6], K[7], K[8]};
+      if (MODE & ELEM_KP1) {
+        double G[3];
+#pragma unroll
+        for (int r = 0; r < 3; ++r) G[r] = (pp[1] - pp[0]) * R0[r] + (pp[2] - pp[0]) * R1[r] + (pp[3] - pp[0]) * R2[r];
+        const double d1 = R0[0] * G[0] + R0[1] * G[1] + R0[2] * G[2];
+        const double d2 = R1[0] * G[0] + R1[1] * G[1] + R1[2] * G[2];
+        const double d3 = R2[0] * G[0] + R2[1] * G[1] + R2[2] * G[2];
+        gy[1] += Wq * d1;
+        gy[2] += Wq * d2;
+        gy[3] += Wq * d3;
+        gy[0] -= Wq * (d1 + d2 + d3);
+      } else {
+        double S0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+          const double t0 = R0[r] + R1[r] + R2[r];
+          S0 += t0 * t0;
+          s1 += R0[r] * R0[r];
+          s2 += R1[r] * R1[r];
+          s3 += R2[r] * R2[r];
+        }
+        gy[0] += Wq * S0;
+        gy[1] += Wq * s1;
+        gy[2] += Wq * s2;
+        gy[3] += Wq * s3;
+      }
+    }
+    return;
+  }
+  if (MODE & (ELEM_VMASS | ELEM_VMASSD)) {
+    // vector mass M_{sqrt(eta_a)}: y_(a,c) = sum_q w |det J| sqrt(eta_a,q) phi_a(q) u_c(q)
+    constexpr double phv = EQB * (2.0 * EQB - 1.0), phq = EQA * (2.0 * EQA - 1.0);
+    constexpr double peq = 4.0 * EQA * EQB, pen = 4.0 * EQB * EQB;
+    constexpr int ep[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
+#pragma unroll
+    for (int a = 0; a < 10; ++a)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) acc[a][c] = 0.0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double cq = cK * al[q];
+      const double Wq = wdet * cq * cq * cq * sfac * sqrt(fma(EQAB, et[q], etaS));
+      double phi[10];
+#pragma unroll
+      for (int a = 0; a < 10; ++a)
+        phi[a] = a < 4 ? ((a == q) ? phq : phv) : ((ep[a - 4][0] == q || ep[a - 4][1] == q) ? peq : pen);
+      if (MODE & ELEM_VMASS) {
+        double uq[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+        for (int a = 0; a < 10; ++a)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) uq[c] = fma(phi[a], uu(a, c), uq[c]);
+#pragma unroll
+        for (int a = 0; a < 10; ++a)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) acc[a][c] = fma(Wq * phi[a], uq[c], acc[a][c]);
+      } else {
+#pragma unroll
+        for (int a = 0; a < 10; ++a) {
+          const double d = Wq * phi[a] * phi[a];
+#pragma unroll
+          for (int c = 0; c < 3; ++c) acc[a][c] += d;
+        }
       }
     }
     return;
@@ -730,8 +816,8 @@ struct FootT {  // scalar P2 footprint (temperature) for the quadrature-point vi
 
 template <int MODE, bool ETAQ = false>
 __host__ __device__ constexpr int fp_smem_words() {
-  return ((MODE & (ELEM_A | ELEM_DIV)) ? 3 * kFU : 0) + (elem_u_out(MODE) ? 2 * 3 * kFY : 0) +
-         kF1 + ((MODE & (ELEM_BT | ELEM_MASS | ELEM_LOAD)) ? kF1 : 0) + (elem_p_out(MODE) ? 2 * kF1Y : 0) + kGeoSm +
+  return (elem_need_u(MODE) ? 3 * kFU : 0) + (elem_u_out(MODE) ? 2 * 3 * kFY : 0) +
+         kF1 + (elem_need_p(MODE) ? kF1 : 0) + (elem_p_out(MODE) ? 2 * kF1Y : 0) + kGeoSm +
          (ETAQ ? kFU : 0);
 }
 
@@ -752,8 +838,8 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
               double* __restrict__ yp, double gamma, const double* __restrict__ T2 = nullptr,
               EtaQ eq = EtaQ{0.0, 1.0, 0.0}) {
   constexpr bool DO_DIV = (MODE & ELEM_DIV) != 0;
-  constexpr bool NEED_U = (MODE & (ELEM_A | ELEM_DIV)) != 0;
-  constexpr bool NEED_P = (MODE & (ELEM_BT | ELEM_MASS | ELEM_LOAD)) != 0;
+  constexpr bool NEED_U = elem_need_u(MODE);
+  constexpr bool NEED_P = elem_need_p(MODE);
   constexpr bool HAS_P_OUT = elem_p_out(MODE);
   constexpr bool HAS_U_OUT = elem_u_out(MODE);
   extern __shared__ double sm[];
@@ -1269,7 +1355,7 @@ static void elem_launch(const Mesh* m, const Level& L, const double* eta, double
                         const double* p, double* yu, double* yp, cudaStream_t s) {
   const int64_t nm = macro_count(m);
 #ifdef HHG_ELEM_V5
-  if (MODE & (ELEM_MASS | ELEM_MASSD | ELEM_LOAD))
+  if (MODE & (ELEM_MASS | ELEM_MASSD | ELEM_LOAD | ELEM_SURF))
 #endif
   {
     constexpr size_t smem = fp_smem_words<MODE>() * sizeof(double);
@@ -1285,6 +1371,7 @@ static void elem_launch(const Mesh* m, const Level& L, const double* eta, double
                                                          L.npts2, nm * L.npts2, eta, u, p, yu, yp, gamma);
     return;
   }
+#ifdef HHG_ELEM_V5
   constexpr int NS = (elem_u_out(MODE) ? kNS2 : 0) + ((MODE & ELEM_DIV) ? kNS1 : 0);
 #ifdef HHG_GEO_GLOBAL
   constexpr size_t smem = (NS * kBT) * sizeof(double) + 13 * kBT * sizeof(int);
@@ -1301,6 +1388,48 @@ static void elem_launch(const Mesh* m, const Level& L, const double* eta, double
   }
   k_elem_brick<BLEND, MODE, FULL><<<grid, kBT, smem, s>>>(m->dgeo, L.geo, L.bricks, L.n1, 1.0 / L.n1, L.npts1,
                                                           L.npts2, nm * L.npts2, eta, u, p, yu, yp, gamma);
+#endif
+}
+
+// w-BFBT operators: same brick kernel, a in the gamma slot, the outer radius in eq.r_jump
+template <bool BLEND, int MODE>
+static void elem_launch_surf(const Mesh* m, const Level& L, const double* eta, double a, double r_outer,
+                             const double* u, const double* p, double* yu, double* yp, cudaStream_t s) {
+  const int64_t nm = macro_count(m);
+  constexpr size_t smem = fp_smem_words<MODE>() * sizeof(double);
+  dim3 grid((unsigned)L.n_bricks, (unsigned)nm);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_elem_fp<BLEND, MODE, true>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         (int)cudaSharedmemCarveoutMaxShared);
+    cudaFuncSetAttribute(k_elem_fp<BLEND, MODE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  k_elem_fp<BLEND, MODE, true><<<grid, kBT, smem, s>>>(m->dgeo, L.geo, L.bricks, L.n1, 1.0 / L.n1, L.npts1, L.npts2,
+                                                       nm * L.npts2, eta, u, p, yu, yp, a, nullptr,
+                                                       EtaQ{0.0, 1.0, r_outer});
+}
+
+int launch_elem_surf(const Mesh* m, const Level& L, int mode, const double* eta, double a, double r_outer,
+                     const double* in, double* out, cudaStream_t s) {
+  HHG_TRY(ensure_slots());
+  const bool bl = m->blend == HHG_BLEND_SHELL;
+  if (a != 1.0 && !bl) return fail(HHG_EINVAL, "w-BFBT surface scaling a != 1 needs a shell-blended mesh");
+  if (!(a > 0.0)) return fail(HHG_EINVAL, "w-BFBT surface scaling a must be > 0");
+#define HHG_SURF(MODE, U, P, YU, YP)                                                   \
+  if (bl) elem_launch_surf<true, MODE>(m, L, eta, a, r_outer, U, P, YU, YP, s);        \
+  else elem_launch_surf<false, MODE>(m, L, eta, a, r_outer, U, P, YU, YP, s);
+  switch (mode) {
+    case ELEM_KP1: HHG_SURF(ELEM_KP1, nullptr, in, nullptr, out); break;
+    case ELEM_KP1D: HHG_SURF(ELEM_KP1D, nullptr, nullptr, nullptr, out); break;
+    case ELEM_VMASS: HHG_SURF(ELEM_VMASS, in, nullptr, out, nullptr); break;
+    case ELEM_VMASSD: HHG_SURF(ELEM_VMASSD, nullptr, nullptr, out, nullptr); break;
+    default: return fail(HHG_EINVAL, "bad w-BFBT element mode");
+  }
+#undef HHG_SURF
+  count_launch();
+  HHG_CUDA(cudaGetLastError());
+  return HHG_OK;
 }
 
 template <bool BLEND, int MODE>

@@ -135,11 +135,26 @@ int64_t macro_count(const Mesh* m);
 // ---------------------------------------------------------------- kernel launchers (hhg_kernels.cu)
 int launch_elem(const Mesh* m, const Level& L, int mode, int form, const double* eta, double gamma,
                 const double* u, const double* p, double* yu, double* yp, cudaStream_t s);
+// w-BFBT operators (eq:schurWBFBT): K_{1/sqrt(eta_a)} (ELEM_KP1/KP1D, P1 -> P1) and the vector
+// mass M_{sqrt(eta_a)} (ELEM_VMASS/VMASSD, P2VEC -> P2VEC), eta_a = a^2 eta on micro tets touching the
+// sphere of radius r_outer (D_eta), a != 1 only on shell-blended meshes
+int launch_elem_surf(const Mesh* m, const Level& L, int mode, const double* eta, double a, double r_outer,
+                     const double* in, double* out, cudaStream_t s);
+int surf_op(const Mesh* m, int level, int mode, const double* eta, double a, const double* in, double* out,
+            cudaStream_t s);  // element kernel + interface sum (+ P_v M for ELEM_VMASS)
+int launch_p1_prolong(const Mesh* m, const Level& Lc, const Level& Lf, const double* xc, double* xf, cudaStream_t s);
+int launch_p1_restrict(const Mesh* m, const Level& Lc, const Level& Lf, const double* rf, double* rc, cudaStream_t s);
 int launch_elem_qeta(const Mesh* m, const Level& L, int mode, const double* T2, double lnC, double jump, double r_jump,
                      const double* u, double* yu, cudaStream_t s);
-enum { ELEM_A = 1, ELEM_BT = 2, ELEM_DIV = 4, ELEM_DIAG = 8, ELEM_MASS = 16, ELEM_MASSD = 32, ELEM_LOAD = 64 };
-constexpr bool elem_p_out(int mode) { return (mode & (ELEM_DIV | ELEM_MASS | ELEM_MASSD)) != 0; }
-constexpr bool elem_u_out(int mode) { return (mode & (ELEM_A | ELEM_BT | ELEM_DIAG | ELEM_LOAD)) != 0; }
+enum { ELEM_A = 1, ELEM_BT = 2, ELEM_DIV = 4, ELEM_DIAG = 8, ELEM_MASS = 16, ELEM_MASSD = 32, ELEM_LOAD = 64,
+       ELEM_KP1 = 128, ELEM_KP1D = 256, ELEM_VMASS = 512, ELEM_VMASSD = 1024 };
+constexpr int ELEM_SURF = ELEM_KP1 | ELEM_KP1D | ELEM_VMASS | ELEM_VMASSD;  // w-BFBT operators (eta_a scaling)
+constexpr bool elem_p_out(int mode) { return (mode & (ELEM_DIV | ELEM_MASS | ELEM_MASSD | ELEM_KP1 | ELEM_KP1D)) != 0; }
+constexpr bool elem_u_out(int mode) {
+  return (mode & (ELEM_A | ELEM_BT | ELEM_DIAG | ELEM_LOAD | ELEM_VMASS | ELEM_VMASSD)) != 0;
+}
+constexpr bool elem_need_u(int mode) { return (mode & (ELEM_A | ELEM_DIV | ELEM_VMASS)) != 0; }
+constexpr bool elem_need_p(int mode) { return (mode & (ELEM_BT | ELEM_MASS | ELEM_LOAD | ELEM_KP1)) != 0; }
 int launch_fixup(const Mesh* m, const Level& L, int space, bool sum, bool bc, double* v, cudaStream_t s);
 // split phases of a cross-rank interface sum: pack local partial sums of shared groups into
 // halo.sbuf; exchange (NCCL); final fixup adding halo.rbuf (launch_fixup does all three when the

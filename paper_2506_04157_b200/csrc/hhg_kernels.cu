@@ -497,6 +497,90 @@ int launch_restrict(const Mesh* m, const Level& Lc, const Level& Lf, const doubl
   return HHG_OK;
 }
 
+// ------------------------------------------------------------------ P1 transfers (w-BFBT K multigrid)
+// Nested P1 spaces: a fine node F (res 2 Nc) with odd-coordinate pattern o != 0 is the midpoint of the
+// coarse lattice edge F -/+ d(o) (the 7 edge directions of the Freudenthal split); linear interpolation
+// x_f(F) = 1/2 (x_c((F - d)/2) + x_c((F + d)/2)), x_f(2C) = x_c(C).  Restriction = the transpose over
+// owned fine copies, then the interface sum of the coarse copies.
+__device__ __forceinline__ void p1_dir(int o, int& dx, int& dy, int& dz) {
+  // o = ox | oy << 1 | oz << 2  ->  d with |d_r| = o_r: (1,-1,0), (1,0,-1), (0,1,-1), (1,-1,1) for pairs/triple
+  dx = o & 1;
+  dy = (o >> 1) & 1;
+  dz = (o >> 2) & 1;
+  if (dx && dy) dy = -1;
+  else if (dz && (dx || dy)) dz = -1;
+  if (o == 7) dz = 1;
+}
+
+__global__ void k_p1_prolong(const int32_t* __restrict__ rowsf, int64_t nrowsf, int Nf, int64_t nptsf, int64_t nptsc,
+                             const double* __restrict__ xc, double* __restrict__ xf) {
+  RowCtx rc;
+  if (!row_of(rowsf, nrowsf, Nf, rc)) return;
+  const int mac = blockIdx.y, Nc = Nf / 2, lane = threadIdx.x & 31;
+  const double* cm = xc + (int64_t)mac * nptsc;
+  double* fr = xf + (int64_t)mac * nptsf + rowstart_i32(Nf, rc.j, rc.k);
+  for (int I = lane; I < rc.len; I += 32) {
+    const int o = (I & 1) | ((rc.j & 1) << 1) | ((rc.k & 1) << 2);
+    if (o == 0) {
+      fr[I] += __ldg(cm + rowstart_i32(Nc, rc.j >> 1, rc.k >> 1) + (I >> 1));
+      continue;
+    }
+    int dx, dy, dz;
+    p1_dir(o, dx, dy, dz);
+    const int a = rowstart_i32(Nc, (rc.j - dy) >> 1, (rc.k - dz) >> 1) + ((I - dx) >> 1);
+    const int b = rowstart_i32(Nc, (rc.j + dy) >> 1, (rc.k + dz) >> 1) + ((I + dx) >> 1);
+    fr[I] += 0.5 * (__ldg(cm + a) + __ldg(cm + b));
+  }
+}
+
+__global__ void k_p1_restrict(const int32_t* __restrict__ rowsc, int64_t nrowsc, int Nc, int64_t nptsf, int64_t nptsc,
+                              const uint8_t* __restrict__ ownf, const double* __restrict__ rf, double* __restrict__ rc_out) {
+  RowCtx rc;
+  if (!row_of(rowsc, nrowsc, Nc, rc)) return;
+  const int mac = blockIdx.y, Nf = 2 * Nc, lane = threadIdx.x & 31;
+  const int64_t fb = (int64_t)mac * nptsf;
+  const uint8_t* om = ownf + fb;
+  const double* rm = rf + fb;
+  double* cr = rc_out + (int64_t)mac * nptsc + rowstart_i32(Nc, rc.j, rc.k);
+  const int FY = 2 * rc.j, FZ = 2 * rc.k;
+  for (int I = lane; I < rc.len; I += 32) {
+    const int FX = 2 * I;
+    int c = rowstart_i32(Nf, FY, FZ) + FX;
+    double s = om[c] ? rm[c] : 0.0;
+#pragma unroll
+    for (int o = 1; o < 8; ++o) {
+      int dx, dy, dz;
+      p1_dir(o, dx, dy, dz);
+#pragma unroll
+      for (int sg = -1; sg <= 1; sg += 2) {
+        const int x = FX + sg * dx, y = FY + sg * dy, z = FZ + sg * dz;
+        if (x < 0 || y < 0 || z < 0 || x + y + z > Nf) continue;
+        c = rowstart_i32(Nf, y, z) + x;
+        if (om[c]) s += 0.5 * rm[c];
+      }
+    }
+    cr[I] = s;
+  }
+}
+
+int launch_p1_prolong(const Mesh* m, const Level& Lc, const Level& Lf, const double* xc, double* xf, cudaStream_t s) {
+  const int64_t nm = macro_count(m);
+  dim3 grid((unsigned)((Lf.nrows1 + 7) / 8), (unsigned)nm);
+  k_p1_prolong<<<grid, 256, 0, s>>>(Lf.rows1, Lf.nrows1, Lf.n1, Lf.npts1, Lc.npts1, xc, xf);
+  count_launch();
+  HHG_CUDA(cudaGetLastError());
+  return HHG_OK;
+}
+
+int launch_p1_restrict(const Mesh* m, const Level& Lc, const Level& Lf, const double* rf, double* rc, cudaStream_t s) {
+  const int64_t nm = macro_count(m);
+  dim3 grid((unsigned)((Lc.nrows1 + 7) / 8), (unsigned)nm);
+  k_p1_restrict<<<grid, 256, 0, s>>>(Lc.rows1, Lc.nrows1, Lc.n1, Lf.npts1, Lc.npts1, Lf.own1, rf, rc);
+  count_launch();
+  HHG_CUDA(cudaGetLastError());
+  return HHG_OK;
+}
+
 // ------------------------------------------------------------------ coordinates
 __global__ void k_coords(const MacroGeo* __restrict__ mgeo, const int32_t* __restrict__ rows, int64_t nrows, int N,
                          int64_t npts, bool blend, double* __restrict__ xyz) {

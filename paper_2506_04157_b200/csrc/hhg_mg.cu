@@ -2,8 +2,10 @@
 // inverse diagonal, P2 transfers with projections, coarse Jacobi-PCG (BASELINE
 // config 3; replaces the paper's AMG-CG of P:443), power-iteration spectrum estimate.
 // All scalars of the PCG stay on the device so the whole cycle can be captured in one CUDA graph.
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <functional>
 #include <vector>
 
 #include "hhg_internal.h"
@@ -571,6 +573,278 @@ int hhg_power_iteration(const hhg_mesh* mesh, int level, const double* eta_p1, c
 
 }  // extern "C"
 
+// ================================================================ K_{1/sqrt(eta)} multigrid (w-BFBT, NEXT-3)
+// The Poisson replacement of (B M_{sqrt(eta)}^-1 B^T)^-1 in eq:schurWBFBT: "an inverse viscosity scaled
+// Poisson problem with Neumann boundary conditions ... CG solver preconditioned by a GMG approach"
+// (P:470).  P1 levels l_min..l_max, Chebyshev(D^-1 K) smoothing as for A (R12), P1 linear
+// transfers, coarse Jacobi-PCG (fixed iteration count, device scalars).  No constraints; the constant
+// kernel is handled by projecting the outer CG's vectors to mean zero.
+namespace {
+__global__ void k_hash_fill(int64_t n, uint64_t seed, double* __restrict__ v) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t z = (uint64_t)i + seed + 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    v[i] = (double)(z >> 11) * 0x1.0p-53 - 0.5;
+  }
+}
+// PCG step with ping-pong r.z scalars (scal[0] / scal[2] by iteration parity, scal[1] = p.q), no BC
+__global__ void k_pcg_update_pp(int64_t n, int it, const double* __restrict__ scal, double* __restrict__ x,
+                                double* __restrict__ r, const double* __restrict__ p, const double* __restrict__ q,
+                                const double* __restrict__ dinv, double* __restrict__ z) {
+  const double rz = scal[(it & 1) ? 2 : 0], pq = scal[1];
+  const double alpha = (rz > 1e-300 && pq != 0.0) ? rz / pq : 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    x[i] += alpha * p[i];
+    const double ri = r[i] - alpha * q[i];
+    r[i] = ri;
+    z[i] = dinv[i] * ri;
+  }
+}
+__global__ void k_shift(int64_t n, const double* __restrict__ sum, double inv_count, double* __restrict__ v) {
+  const double m = *sum * inv_count;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    v[i] -= m;
+}
+}  // namespace
+
+struct hhg_kmg {
+  hhg_mesh* mesh = nullptr;
+  hhg_mg_params prm{};
+  double a = 1.0;
+  struct Lv {
+    double *x = nullptr, *f = nullptr, *r = nullptr, *d = nullptr, *t = nullptr, *dinv = nullptr, *p = nullptr;
+    double* ones = nullptr;
+    const double* eta = nullptr;
+    double lam = 0.0, inv_count = 0.0;  // 1 / number of unique nodes
+  };
+  std::vector<Lv> lv;
+  double* scal = nullptr;
+  double *cr = nullptr, *cz = nullptr, *cp = nullptr, *cq = nullptr;  // outer CG (finest level)
+  ~hhg_kmg() {
+    for (auto& L : lv)
+      for (double* p : {L.x, L.f, L.r, L.d, L.t, L.dinv, L.p, L.ones})
+        if (p) cudaFree(p);
+    for (double* p : {scal, cr, cz, cp, cq})
+      if (p) cudaFree(p);
+  }
+};
+
+namespace {
+int64_t p1_len(const Mesh* m, int l) { return macro_count(m) * m->levels[l].npts1; }
+int km_apply(hhg_kmg* K, int l, const double* u, double* y, cudaStream_t s) {
+  return surf_op(K->mesh, l, ELEM_KP1, K->lv[l].eta, K->a, u, y, s);
+}
+int km_mean0(hhg_kmg* K, int l, double* v, cudaStream_t s) {  // v -= mean over unique nodes (no sync)
+  const Mesh* m = K->mesh;
+  HHG_TRY(launch_dot_fused(m, m->levels[l], HHG_P1, v, K->lv[l].ones, K->scal + 6, s));
+  const int64_t n = p1_len(m, l);
+  k_shift<<<vg(n), 256, 0, s>>>(n, K->scal + 6, K->lv[l].inv_count, v);
+  count_launch();
+  return HHG_OK;
+}
+int km_cheb(hhg_kmg* K, int l, double* x, const double* f, bool x_is_zero, cudaStream_t s) {
+  auto& L = K->lv[l];
+  const int64_t n = p1_len(K->mesh, l);
+  const double b = K->prm.cheb_hi_factor * L.lam, a = K->prm.cheb_lo_ratio * b;
+  const double theta = 0.5 * (b + a), delta = 0.5 * (b - a), sigma = theta / delta;
+  double rho = 1.0 / sigma;
+  const double* t0 = nullptr;
+  if (!x_is_zero) {
+    HHG_TRY(km_apply(K, l, x, L.t, s));
+    t0 = L.t;
+  }
+  if (K->prm.degree == 1) return launch_cheb_deg1(n, f, t0, L.dinv, 1.0 / theta, x, s);
+  HHG_TRY(launch_cheb0(n, f, t0, L.dinv, 1.0 / theta, L.r, L.d, s));
+  for (int k = 1; k < K->prm.degree; ++k) {
+    HHG_TRY(km_apply(K, l, L.d, L.t, s));
+    const double rn = 1.0 / (2.0 * sigma - rho);
+    if (k < K->prm.degree - 1) HHG_TRY(launch_chebk(n, L.t, L.dinv, rn * rho, 2.0 * rn / delta, x, L.r, L.d, s));
+    else HHG_TRY(launch_chebk_last(n, L.t, L.dinv, rn * rho, 2.0 * rn / delta, L.r, L.d, x, s));
+    rho = rn;
+  }
+  return HHG_OK;
+}
+int km_pcg(hhg_kmg* K, int l, const double* f, double* x, cudaStream_t s) {
+  auto& L = K->lv[l];
+  const Mesh* m = K->mesh;
+  const Level& LL = m->levels[l];
+  const int64_t n = p1_len(m, l);
+  HHG_CUDA(cudaMemsetAsync(x, 0, n * sizeof(double), s));
+  HHG_TRY(launch_cheb0(n, f, nullptr, L.dinv, 1.0, L.r, L.d, s));  // r = f, z = D^-1 r
+  HHG_TRY(km_mean0(K, l, L.r, s));                                  // consistent singular system
+  HHG_TRY(launch_pcg_scale(n, L.dinv, L.r, L.d, s));
+  HHG_CUDA(cudaMemcpyAsync(L.p, L.d, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  HHG_TRY(launch_dot_fused(m, LL, HHG_P1, L.r, L.d, K->scal + 0, s));
+  for (int it = 0; it < K->prm.coarse_iters; ++it) {
+    HHG_TRY(km_apply(K, l, L.p, L.t, s));
+    HHG_TRY(launch_dot_fused(m, LL, HHG_P1, L.p, L.t, K->scal + 1, s));
+    k_pcg_update_pp<<<vg(n), 256, 0, s>>>(n, it, K->scal, x, L.r, L.p, L.t, L.dinv, L.d);
+    count_launch();
+    HHG_TRY(launch_dot_fused(m, LL, HHG_P1, L.r, L.d, K->scal + ((it & 1) ? 0 : 2), s));
+    HHG_TRY(launch_pcg_dir_zero(n, it, K->scal, L.d, L.p, L.t, s));
+  }
+  return HHG_OK;
+}
+int km_cycle(hhg_kmg* K, int l, const double* f, double* x, cudaStream_t s) {
+  if (l == K->prm.l_min) return km_pcg(K, l, f, x, s);
+  auto& L = K->lv[l];
+  const int64_t n = p1_len(K->mesh, l);
+  HHG_CUDA(cudaMemsetAsync(x, 0, n * sizeof(double), s));
+  for (int i = 0; i < K->prm.pre; ++i) HHG_TRY(km_cheb(K, l, x, f, i == 0, s));
+  HHG_TRY(km_apply(K, l, x, L.t, s));
+  k_sub<<<vg(n), 256, 0, s>>>(n, f, L.t, L.r);
+  count_launch();
+  auto& C = K->lv[l - 1];
+  HHG_TRY(p1_restrict(K->mesh, l, L.r, C.f, (hhg_stream_t)s));
+  HHG_TRY(km_cycle(K, l - 1, C.f, C.x, s));
+  HHG_TRY(p1_prolong(K->mesh, l - 1, C.x, x, (hhg_stream_t)s));
+  for (int i = 0; i < K->prm.post; ++i) HHG_TRY(km_cheb(K, l, x, f, false, s));
+  return HHG_OK;
+}
+int km_power(hhg_kmg* K, int l) {  // lambda_max(D^-1 K) from a hashed consistent start vector
+  auto& L = K->lv[l];
+  const Mesh* m = K->mesh;
+  const Level& LL = m->levels[l];
+  const int64_t n = p1_len(m, l);
+  cudaStream_t s = nullptr;
+  k_hash_fill<<<vg(n), 256, 0, s>>>(n, 0x5eedull + (uint64_t)l, L.x);
+  count_launch();
+  HHG_TRY(launch_fixup(m, LL, HHG_P1, true, false, L.x, s));
+  for (int it = 0; it < K->prm.power_iters; ++it) {
+    HHG_TRY(km_apply(K, l, L.x, L.t, s));
+    k_scale_dinv<<<vg(n), 256, 0, s>>>(n, L.t, L.dinv, L.t);
+    HHG_TRY(launch_dot(m, LL, HHG_P1, L.t, L.t, K->scal + 8, s));
+    k_normalize<<<vg(n), 256, 0, s>>>(n, K->scal + 8, L.t, L.x);
+    count_launch(2);
+  }
+  double h = 0;
+  HHG_CUDA(cudaMemcpy(&h, K->scal + 8, sizeof(double), cudaMemcpyDeviceToHost));
+  if (!(h > 0) || !std::isfinite(h)) return fail(HHG_EZEROOP, "K power iteration on a zero operator");
+  L.lam = std::sqrt(h);
+  return HHG_OK;
+}
+// CG with device scalars and one host sync per iteration; op / prec write their outputs; proj (may
+// be empty) projects a vector in place (mean zero, or nothing)
+int dev_pcg(const Mesh* m, const Level& LL, int space, int64_t n, const std::function<int(const double*, double*)>& op,
+            const std::function<int(const double*, double*)>& prec, const std::function<int(double*)>& proj,
+            const double* rhs, double* x, double tol, double tol_abs, int max_iters, double* r, double* z, double* p,
+            double* q, double* sc, cudaStream_t s, int* iters_out, double* rel_out) {
+  HHG_CUDA(cudaMemsetAsync(x, 0, n * sizeof(double), s));
+  HHG_CUDA(cudaMemcpyAsync(r, rhs, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  if (proj) HHG_TRY(proj(r));
+  HHG_TRY(launch_dot(m, LL, space, r, r, sc + 3, s));
+  double r0 = 0.0;
+  HHG_CUDA(cudaMemcpyAsync(&r0, sc + 3, sizeof(double), cudaMemcpyDeviceToHost, s));
+  HHG_CUDA(cudaStreamSynchronize(s));
+  r0 = std::sqrt(std::max(r0, 0.0));
+  int it = 0;
+  double rel = r0 > 0 ? 1.0 : 0.0;
+  if (r0 > 0 && r0 > tol_abs) {
+    HHG_TRY(prec(r, z));
+    if (proj) HHG_TRY(proj(z));
+    HHG_CUDA(cudaMemcpyAsync(p, z, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    HHG_TRY(launch_dot(m, LL, space, r, z, sc + 0, s));
+    const unsigned nb = vg(n);
+    while (it < max_iters) {
+      ++it;
+      HHG_TRY(op(p, q));
+      HHG_TRY(launch_dot(m, LL, space, p, q, sc + 1, s));
+      k_cg_step<<<nb, 256, 0, s>>>(n, sc, x, r, p, q);
+      count_launch();
+      HHG_TRY(launch_dot(m, LL, space, r, r, sc + 3, s));
+      double rr = 0.0;
+      HHG_CUDA(cudaMemcpyAsync(&rr, sc + 3, sizeof(double), cudaMemcpyDeviceToHost, s));
+      HHG_CUDA(cudaStreamSynchronize(s));
+      const double rn = std::sqrt(std::max(rr, 0.0));
+      rel = rn / r0;
+      if (rel <= tol || rn <= tol_abs) break;
+      HHG_TRY(prec(r, z));
+      if (proj) HHG_TRY(proj(z));
+      HHG_TRY(launch_dot(m, LL, space, r, z, sc + 2, s));
+      k_cg_dir<<<nb, 256, 0, s>>>(n, sc, z, p);
+      k_cg_roll<<<1, 32, 0, s>>>(sc);
+      count_launch(2);
+    }
+  }
+  if (proj) HHG_TRY(proj(x));
+  if (iters_out) *iters_out = it;
+  if (rel_out) *rel_out = rel;
+  return HHG_OK;
+}
+}  // namespace
+
+extern "C" {
+int hhg_kmg_create(hhg_mesh* mesh, const hhg_mg_params* params, const double* const* eta_per_level, double a,
+                   hhg_kmg** out) {
+  if (!mesh || !params || !out) return fail(HHG_EINVAL, "hhg_kmg_create: NULL argument");
+  const hhg_mg_params& P = *params;
+  if (P.l_min < 0 || P.l_max > mesh->level_max || P.l_min > P.l_max)
+    return fail(HHG_ELEVEL, "hhg_kmg_create: need 0 <= l_min <= l_max <= level_max");
+  if (P.degree < 1 || P.pre < 0 || P.post < 0 || P.coarse_iters < 0 || P.power_iters < 1 || !(a > 0))
+    return fail(HHG_EINVAL, "hhg_kmg_create: bad parameters");
+  if (a != 1.0 && mesh->blend != HHG_BLEND_SHELL)
+    return fail(HHG_EINVAL, "hhg_kmg_create: surface scaling a != 1 needs a shell-blended mesh");
+  auto* K = new hhg_kmg();
+  K->mesh = mesh;
+  K->prm = P;
+  K->a = a;
+  K->lv.resize(P.l_max + 1);
+  auto bail = [&](int code) {
+    delete K;
+    return code;
+  };
+  if (cudaMalloc(&K->scal, 16 * sizeof(double)) != cudaSuccess || cudaMemset(K->scal, 0, 16 * sizeof(double)) != cudaSuccess)
+    return bail(fail(HHG_ENOMEM, "kmg scal"));
+  const int64_t nf = p1_len(mesh, P.l_max);
+  for (double** p : {&K->cr, &K->cz, &K->cp, &K->cq})
+    if (cudaMalloc(p, std::max<int64_t>(nf, 1) * sizeof(double)) != cudaSuccess) return bail(fail(HHG_ENOMEM, "kmg cg"));
+  for (int l = P.l_min; l <= P.l_max; ++l) {
+    int r = ensure_level(mesh, l);
+    if (r != HHG_OK) return bail(r);
+    const int64_t n = p1_len(mesh, l);
+    auto& L = K->lv[l];
+    L.eta = eta_per_level ? eta_per_level[l] : nullptr;
+    for (double** p : {&L.x, &L.f, &L.r, &L.d, &L.t, &L.dinv, &L.p, &L.ones})
+      if (cudaMalloc(p, std::max<int64_t>(n, 1) * sizeof(double)) != cudaSuccess) return bail(fail(HHG_ENOMEM, "kmg vectors"));
+    r = launch_fill(n, 1.0, L.ones, nullptr);
+    if (r == HHG_OK) r = launch_dot(mesh, mesh->levels[l], HHG_P1, L.ones, L.ones, K->scal + 9, nullptr);
+    double cnt = 0.0;
+    if (r == HHG_OK && cudaMemcpy(&cnt, K->scal + 9, sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess)
+      r = fail(HHG_ECUDA, "kmg count");
+    if (r != HHG_OK) return bail(r);
+    L.inv_count = 1.0 / cnt;
+    r = surf_op(mesh, l, ELEM_KP1D, L.eta, a, nullptr, L.t, nullptr);
+    if (r != HHG_OK) return bail(r);
+    k_recip<<<vg(n), 256>>>(n, L.t, L.dinv);
+    count_launch();
+    if (l > P.l_min && (r = km_power(K, l)) != HHG_OK) return bail(r);
+  }
+  if (cudaDeviceSynchronize() != cudaSuccess) return bail(fail(HHG_ECUDA, "hhg_kmg_create: sync failed"));
+  *out = K;
+  return HHG_OK;
+}
+
+int hhg_kmg_solve(hhg_kmg* K, const double* rhs, double* x, double tol, double tol_abs, int max_iters, int* iters,
+                  double* rel_res, hhg_stream_t stream) {
+  if (!K || !rhs || !x) return fail(HHG_EINVAL, "hhg_kmg_solve: NULL argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int lf = K->prm.l_max;
+  const Mesh* m = K->mesh;
+  auto op = [&](const double* u, double* y) { return km_apply(K, lf, u, y, s); };
+  auto prec = [&](const double* r, double* z) { return km_cycle(K, lf, r, z, s); };
+  auto proj = [&](double* v) { return km_mean0(K, lf, v, s); };
+  return dev_pcg(m, m->levels[lf], HHG_P1, p1_len(m, lf), op, prec, proj, rhs, x, tol, tol_abs, max_iters, K->cr,
+                 K->cz, K->cp, K->cq, K->scal + 10, s, iters, rel_res);
+}
+
+int hhg_kmg_destroy(hhg_kmg* K) {
+  delete K;
+  return HHG_OK;
+}
+}  // extern "C"
+
 // ================================================================ Stokes solve (NEXT-1)
 // FGMRES right-preconditioned by the symmetric Uzawa block preconditioner
 // (eq:SymmetricUzawaStep1) with B replaced by B + C in the pressure update:
@@ -593,12 +867,18 @@ struct hhg_stokes {
   double *mr = nullptr, *mz = nullptr, *mp = nullptr, *mq = nullptr;
   double *br = nullptr, *bz = nullptr, *bp = nullptr, *bq = nullptr, *bt = nullptr;  // BFBT CG (P1)
   double *bu = nullptr, *bv = nullptr;                                                 // BFBT velocity temps
+  // w-BFBT (schur = 2): K_{1/sqrt(eta_l)}, K_{1/sqrt(eta_r)} hierarchies (kr == kl when a_l == a_r),
+  // inverse diagonals of M_{sqrt(eta_l)}, M_{sqrt(eta_r)} and the vector-mass CG vectors
+  hhg_kmg *kl = nullptr, *kr = nullptr;
+  double *vdl = nullptr, *vdr = nullptr, *vr = nullptr, *vz = nullptr, *vp = nullptr, *vq = nullptr;
   double n_unique_p = 0.0;
   ~hhg_stokes() {
     for (double* p : V) cudaFree(p);
     for (double* p : Z) cudaFree(p);
-    for (double* p : {w, t, a, b, ones, mdinv, sc, mr, mz, mp, mq, br, bz, bp, bq, bt, bu, bv})
+    for (double* p : {w, t, a, b, ones, mdinv, sc, mr, mz, mp, mq, br, bz, bp, bq, bt, bu, bv, vdl, vdr, vr, vz, vp, vq})
       if (p) cudaFree(p);
+    if (kr && kr != kl) delete kr;
+    if (kl) delete kl;
   }
 };
 
@@ -727,10 +1007,44 @@ int st_vbfbt(hhg_stokes* S, const double* t, double* z, cudaStream_t s) {
   return st_bacbt_solve(S, S->bt, z, s);
 }
 
+// x = M_{sqrt(eta_a)}^-1 v on the constrained velocity space: Jacobi-CG (D^-1 then P_v M) to tol_vmass
+int st_vmass_solve(hhg_stokes* S, double a, const double* vdinv, const double* v, double* x, cudaStream_t s) {
+  const Mesh* m = S->mesh;
+  const Level& L = m->levels[S->level];
+  auto op = [&](const double* u, double* y) { return hhg_vmass_apply(S->mesh, S->level, S->eta, a, u, y, (hhg_stream_t)s); };
+  auto prec = [&](const double* r, double* z) {
+    HHG_TRY(launch_pcg_scale(S->n2, vdinv, r, z, s));
+    return launch_fixup(m, L, HHG_P2VEC, false, true, z, s);
+  };
+  int it;
+  double rel;
+  return dev_pcg(m, L, HHG_P2VEC, S->n2, op, prec, std::function<int(double*)>(), v, x, S->prm.tol_vmass, 0.0,
+                 S->prm.vmass_max_iters, S->vr, S->vz, S->vp, S->vq, S->sc, s, &it, &rel);
+}
+// z = S_w^-1 t (eq:schurWBFBT with a_l / a_r):
+//   K_{1/sqrt(eta_l)}^-1 B M_{sqrt(eta_l)}^-1 A M_{sqrt(eta_r)}^-1 B^T K_{1/sqrt(eta_r)}^-1 t
+int st_wbfbt(hhg_stokes* S, const double* t, double* z, cudaStream_t s) {
+  int it;
+  double rel;
+  const auto& P = S->prm;
+  HHG_TRY(hhg_kmg_solve(S->kr, t, S->bt, P.tol_wbfbt, P.tol_wbfbt_abs, P.wbfbt_max_iters, &it, &rel, (hhg_stream_t)s));
+  HHG_TRY(divT_apply(S->mesh, S->level, S->bt, S->bu, 0, (hhg_stream_t)s));
+  HHG_TRY(st_vmass_solve(S, P.a_r, S->vdr, S->bu, S->bv, s));
+  HHG_TRY(epsilon_apply(S->mesh, S->level, HHG_VISC_FULL, S->eta, S->bv, S->bu, (hhg_stream_t)s));
+  HHG_TRY(st_vmass_solve(S, P.a_l, S->vdl, S->bu, S->bv, s));
+  HHG_TRY(div_apply(S->mesh, S->level, 0.0, S->bv, S->bt, (hhg_stream_t)s));
+  HHG_TRY(st_mean0(S, S->bt, s));
+  return hhg_kmg_solve(S->kl, S->bt, z, P.tol_wbfbt, P.tol_wbfbt_abs, P.wbfbt_max_iters, &it, &rel, (hhg_stream_t)s);
+}
+
+int st_schur_inv(hhg_stokes* S, const double* t, double* z, cudaStream_t s) {  // z = S^-1 t
+  if (S->prm.schur == 1) return st_vbfbt(S, t, z, s);
+  if (S->prm.schur == 2) return st_wbfbt(S, t, z, s);
+  return st_mass_solve(S, t, z, s);
+}
 // z = Prec(r): one symmetric Uzawa step from (0, 0)
 int st_schur(hhg_stokes* S, const double* t, double* z, cudaStream_t s) {  // z = -omega S^-1 t, mean zero
-  if (S->prm.schur == 1) HHG_TRY(st_vbfbt(S, t, z, s));
-  else HHG_TRY(st_mass_solve(S, t, z, s));
+  HHG_TRY(st_schur_inv(S, t, z, s));
   HHG_TRY(launch_axpby(S->n1, 0.0, z, -S->prm.omega, z, s));
   return st_mean0(S, z, s);
 }
@@ -776,7 +1090,11 @@ int hhg_stokes_create(hhg_mg* mg, hhg_mg* mg_cheap, const double* eta_p1, double
   if (!mg || !prm || !out) return fail(HHG_EINVAL, "hhg_stokes_create: NULL argument");
   if (prm->restart < 1 || prm->max_iters < 1 || !(prm->tol > 0) || !(prm->tol_A > 0) || !(prm->tol_mass > 0))
     return fail(HHG_EINVAL, "hhg_stokes_create: bad parameters");
-  if (prm->schur != 0 && prm->schur != 1) return fail(HHG_EINVAL, "hhg_stokes_create: schur must be 0 (mass) or 1 (V-BFBT)");
+  if (prm->schur < 0 || prm->schur > 2)
+    return fail(HHG_EINVAL, "hhg_stokes_create: schur must be 0 (mass), 1 (V-BFBT) or 2 (w-BFBT)");
+  if (prm->schur == 2 && (!(prm->a_l > 0) || !(prm->a_r > 0) || !(prm->tol_wbfbt > 0 || prm->tol_wbfbt_abs > 0) ||
+                          prm->wbfbt_max_iters < 1 || !(prm->tol_vmass > 0) || prm->vmass_max_iters < 1))
+    return fail(HHG_EINVAL, "hhg_stokes_create: w-BFBT needs a_l, a_r > 0, a K tolerance, tol_vmass and iteration caps");
   if (prm->uzawa < 0 || prm->uzawa > 2) return fail(HHG_EINVAL, "hhg_stokes_create: uzawa must be 0, 1 or 2");
   if (prm->schur == 1 && (!mg_cheap || mg_cheap->mesh != mg->mesh || mg_cheap->prm.l_max != mg->prm.l_max ||
                           !(prm->tol_vbfbt > 0) || prm->vbfbt_max_iters < 1))
@@ -803,6 +1121,8 @@ int hhg_stokes_create(hhg_mg* mg, hhg_mg* mg_cheap, const double* eta_p1, double
   for (double** p : {&S->ones, &S->mdinv, &S->mr, &S->mz, &S->mp, &S->mq, &S->br, &S->bz, &S->bp, &S->bq, &S->bt})
     ok = ok && alloc(p, S->n1);
   for (double** p : {&S->bu, &S->bv}) ok = ok && alloc(p, S->n2);
+  if (prm->schur == 2)
+    for (double** p : {&S->vdl, &S->vdr, &S->vr, &S->vz, &S->vp, &S->vq}) ok = ok && alloc(p, S->n2);
   ok = ok && alloc(&S->sc, 8);
   if (!ok) {
     delete S;
@@ -817,6 +1137,18 @@ int hhg_stokes_create(hhg_mg* mg, hhg_mg* mg_cheap, const double* eta_p1, double
     HHG_TRY(launch_recip(S->n1, S->mdinv, s));
     HHG_TRY(launch_dot(S->mesh, L, HHG_P1, S->ones, S->ones, S->sc + 4, s));
     HHG_CUDA(cudaMemcpy(&S->n_unique_p, S->sc + 4, sizeof(double), cudaMemcpyDeviceToHost));
+    if (prm->schur == 2) {
+      std::vector<const double*> etas(mg->prm.l_max + 1, nullptr);
+      for (int l = mg->prm.l_min; l <= mg->prm.l_max; ++l) etas[l] = mg->lv[l].eta;
+      HHG_TRY(hhg_kmg_create(S->mesh, &mg->prm, etas.data(), prm->a_l, &S->kl));
+      if (prm->a_r == prm->a_l) S->kr = S->kl;
+      else HHG_TRY(hhg_kmg_create(S->mesh, &mg->prm, etas.data(), prm->a_r, &S->kr));
+      HHG_TRY(hhg_vmass_diag(S->mesh, S->level, S->eta, prm->a_l, S->vdl, nullptr));
+      HHG_TRY(launch_recip(S->n2, S->vdl, s));
+      HHG_TRY(hhg_vmass_diag(S->mesh, S->level, S->eta, prm->a_r, S->vdr, nullptr));
+      HHG_TRY(launch_recip(S->n2, S->vdr, s));
+      HHG_CUDA(cudaDeviceSynchronize());
+    }
     return HHG_OK;
   };
   r = run();
@@ -825,6 +1157,17 @@ int hhg_stokes_create(hhg_mg* mg, hhg_mg* mg_cheap, const double* eta_p1, double
     return r;
   }
   *out = S;
+  return HHG_OK;
+}
+
+int hhg_stokes_schur_apply(hhg_stokes* S, const double* t, double* z, hhg_stream_t stream) {
+  if (!S || !t || !z) return fail(HHG_EINVAL, "hhg_stokes_schur_apply: NULL argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  HHG_CUDA(cudaMemcpyAsync(S->t + S->n2, t, S->n1 * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  HHG_TRY(st_mean0(S, S->t + S->n2, s));
+  HHG_TRY(st_schur_inv(S, S->t + S->n2, z, s));
+  HHG_TRY(st_mean0(S, z, s));
+  HHG_CUDA(cudaStreamSynchronize(s));
   return HHG_OK;
 }
 

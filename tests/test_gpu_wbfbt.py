@@ -1,0 +1,156 @@
+"""GPU parity of the weighted-BFBT pieces (eq:schurWBFBT with the a_l / a_r
+surface scaling) against the oracle: K_{1/sqrt(eta_a)} apply and diagonal, the vector mass
+M_{sqrt(eta_a)} apply and diagonal, the P1 transfers, the GMG-preconditioned K solve, the w-BFBT Schur
+apply and the FGMRES/Uzawa Stokes solve with it.  Blended shell(3,2), config-2 viscosity."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2506_04157_b200 as hhg  # noqa: E402
+from tests.harness import BC_SHELL, canon, lib_eta, lib_mesh, lib_p, oracle_bc, oracle_case, rel_l2  # noqa: E402
+from workload import icoshell, uniform_vec, uniform_from_keys, GAMMA_TALA  # noqa: E402
+
+TOL_APPLY = 1e-11
+C2 = (1e4, 10.0)
+
+
+@pytest.fixture(scope="module")
+def shell():
+    return icoshell(3, 2)
+
+
+@pytest.mark.parametrize("a", [1.0, 3.0])
+def test_kp1_apply_and_diag(shell, a):
+    from oracle.operators import Discretisation
+    L = 2
+    lm, d0, eta_o = oracle_case(shell, L, True, BC_SHELL, C2, build=())
+    d = Discretisation(lm, True, eta_o, 0.0, oracle_bc(BC_SHELL), build=("K",), surf_a=a)
+    M = lib_mesh(shell, L, True, BC_SHELL)
+    eta = lib_eta(M, L, C2)
+    p = lib_p(M, L, 3)
+    y = hhg.hhg_kp1_apply(M, L, eta, a, p)
+    p_o = uniform_from_keys(lm.p1_keys, 3, 0)
+    assert rel_l2(canon(M, L, hhg.HHG_P1, y), d.K @ p_o) <= TOL_APPLY
+    dg = hhg.hhg_kp1_diag(M, L, eta, a)
+    assert rel_l2(canon(M, L, hhg.HHG_P1, dg), d.K.diagonal()) <= TOL_APPLY
+
+
+@pytest.mark.parametrize("a", [1.0, 2.0])
+def test_vmass_apply_and_diag(shell, a):
+    from oracle.operators import Discretisation
+    L = 2
+    lm, d0, eta_o = oracle_case(shell, L, True, BC_SHELL, C2, build=())
+    d = Discretisation(lm, True, eta_o, 0.0, oracle_bc(BC_SHELL), build=("VM",), surf_a=a)
+    M = lib_mesh(shell, L, True, BC_SHELL)
+    eta = lib_eta(M, L, C2)
+    u_o = d.Pm @ uniform_vec(lm.p2_keys, 2)
+    u = M.from_canonical(L, hhg.HHG_P2VEC, u_o)
+    y = hhg.hhg_vmass_apply(M, L, eta, a, u)
+    assert rel_l2(canon(M, L, hhg.HHG_P2VEC, y), d.Pm @ (d.VM @ u_o)) <= TOL_APPLY
+    dg = hhg.hhg_vmass_diag(M, L, eta, a)
+    assert rel_l2(canon(M, L, hhg.HHG_P2VEC, dg), d.VM.diagonal()) <= TOL_APPLY
+
+
+@pytest.mark.parametrize("lc", [1, 2, 3])
+def test_p1_transfers(shell, lc):
+    """x_f += P x_c and r_c = P^T r_f against the oracle's P1 prolongation (exact arithmetic: weights 1, 1/2)."""
+    from oracle.multigrid import p1_prolongation
+    from oracle.refine import build_level
+    lo = build_level(shell.verts, shell.tets, shell.vtag, lc)
+    lf = build_level(shell.verts, shell.tets, shell.vtag, lc + 1)
+    P = p1_prolongation(lo, lf)
+    M = lib_mesh(shell, lc + 1, True, BC_SHELL)
+    xc_o = uniform_from_keys(lo.p1_keys, 7, 0)
+    rf_o = uniform_from_keys(lf.p1_keys, 8, 0)
+    xc = M.from_canonical(lc, hhg.HHG_P1, xc_o)
+    xf = M.zeros(lc + 1, hhg.HHG_P1)
+    hhg.p1_prolong(M, lc, xc, xf)
+    assert np.abs(canon(M, lc + 1, hhg.HHG_P1, xf) - P @ xc_o).max() <= 1e-15
+    rc = hhg.p1_restrict(M, lc + 1, M.from_canonical(lc + 1, hhg.HHG_P1, rf_o))
+    assert rel_l2(canon(M, lc, hhg.HHG_P1, rc), P.T @ rf_o) <= 1e-14
+
+
+@pytest.mark.parametrize("a,L", [(1.0, 2), (3.0, 2), (1.0, 3)])
+def test_kmg_solve_matches_direct_neumann_solve(shell, a, L):
+    """K_{1/sqrt(eta_a)}^-1 by GMG-preconditioned CG to 1e-12 equals the oracle's direct mean-zero solve;
+    the iteration count stays small and level-robust (multigrid, not plain CG)."""
+    from oracle.operators import Discretisation
+    from oracle.stokes import neumann_solve
+    lm, _, eta_o = oracle_case(shell, L, True, BC_SHELL, C2, build=())
+    d = Discretisation(lm, True, eta_o, 0.0, oracle_bc(BC_SHELL), build=("K",), surf_a=a)
+    t_o = uniform_from_keys(lm.p1_keys, 3, 0)
+    t_o -= t_o.mean()
+    y_o = neumann_solve(d.K, t_o)
+    M = lib_mesh(shell, L, True, BC_SHELL)
+    etas = {l: lib_eta(M, l, C2) for l in range(1, L + 1)}
+    K = hhg.KMG(M, 1, L, etas, a=a)
+    y, it, rel = K.solve(lib_p(M, L, 3), tol=1e-12, max_iters=100)
+    assert rel <= 1e-12 and it <= 25, (it, rel)
+    assert rel_l2(canon(M, L, hhg.HHG_P1, y), y_o) <= 1e-9
+
+
+def _stokes_case(shell, eta_cj, build_extra=("K", "VM"), a=(1.0, 1.0)):
+    from oracle.multigrid import Hierarchy
+    from oracle.operators import Discretisation
+    discs, v0 = {}, {}
+    for L in (1, 2):
+        lm, d, eta_o = oracle_case(shell, L, True, BC_SHELL, eta_cj, GAMMA_TALA,
+                                   build=("A", "B", "C", "M") if L == 2 else ("A",))
+        discs[L], v0[L] = d, uniform_vec(lm.p2_keys, 6)
+    H = Hierarchy(discs, v0, pre=3, post=3, degree=3, power_iters=20, coarse_iters=50)
+    d = discs[2]
+    dl = Discretisation(d.lm, True, d.eta_p1, 0.0, oracle_bc(BC_SHELL), build=build_extra, surf_a=a[0])
+    dr = dl if a[1] == a[0] else Discretisation(d.lm, True, d.eta_p1, 0.0, oracle_bc(BC_SHELL), build=build_extra,
+                                                surf_a=a[1])
+    M = lib_mesh(shell, 2, True, BC_SHELL)
+    etas = {L: lib_eta(M, L, eta_cj) for L in (1, 2)}
+    pv = {2: M.from_canonical(2, hhg.HHG_P2VEC, uniform_vec(M.canonical_keys(2, hhg.HHG_P2), 6))}
+    mg = hhg.MG(M, 1, 2, etas, pv, pre=3, post=3, degree=3, power_iters=20, coarse_iters=50)
+    return H, d, (dl.K, dr.K, dl.VM, dr.VM), M, etas, mg
+
+
+@pytest.mark.parametrize("a", [(1.0, 1.0), (2.0, 0.5)])
+def test_wbfbt_schur_apply(shell, a):
+    """S_w^-1 t with tight inner tolerances equals the oracle's S_w^-1 with exact inner solves."""
+    from oracle.stokes import StokesOracle
+    H, d, ops, M, etas, mg = _stokes_case(shell, C2, a=a)
+    S_o = StokesOracle(H, d, d.M, schur="wbfbt", wbfbt_ops=ops)
+    t_o = uniform_from_keys(d.lm.p1_keys, 3, 0)
+    z_o = S_o.wbfbt(t_o - t_o.mean())
+    S = hhg.StokesSolver(mg, etas[2], GAMMA_TALA, schur="wbfbt", a_l=a[0], a_r=a[1], tol_wbfbt=1e-13,
+                         wbfbt_max_iters=200, tol_vmass=1e-14, vmass_max_iters=2000)
+    z = S.schur_apply(lib_p(M, 2, 3))
+    assert rel_l2(canon(M, 2, hhg.HHG_P1, z), z_o) <= 1e-8
+
+
+def test_stokes_fgmres_wbfbt_solve(shell):
+    """FGMRES + symmetric Uzawa with S_w (tight inner solves): same iteration count and residual history as
+    the oracle with exact inner solves; solution within 1e-8."""
+    from oracle.stokes import StokesOracle
+    H, d, ops, M, etas, mg = _stokes_case(shell, C2)
+    S_o = StokesOracle(H, d, d.M, sigma=1.0, omega=0.3, tol_A=1e-2, schur="wbfbt", wbfbt_ops=ops)
+    rhs_o = np.concatenate([uniform_vec(d.lm.p2_keys, 2), uniform_from_keys(d.lm.p1_keys, 3, 0)])
+    x_o, it_o, rel_o = S_o.solve(rhs_o, tol=1e-6, restart=60, max_iters=60)
+    S = hhg.StokesSolver(mg, etas[2], GAMMA_TALA, restart=60, max_iters=60, tol=1e-6, sigma=1.0, omega=0.3,
+                         tol_A=1e-2, schur="wbfbt", tol_wbfbt=1e-13, wbfbt_max_iters=200, tol_vmass=1e-14,
+                         vmass_max_iters=2000)
+    ru = M.from_canonical(2, hhg.HHG_P2VEC, uniform_vec(M.canonical_keys(2, hhg.HHG_P2), 2))
+    rhs = torch.cat([ru, lib_p(M, 2, 3)])
+    x, it, rel = S.solve(rhs)
+    n2 = M.vec_len(2, hhg.HHG_P2VEC)
+    xc = np.concatenate([canon(M, 2, hhg.HHG_P2VEC, x[:n2].contiguous()), canon(M, 2, hhg.HHG_P1, x[n2:].contiguous())])
+    assert it == it_o and abs(rel - rel_o) <= 1e-6 * rel_o
+    assert rel_l2(xc, x_o) <= 1e-8, rel_l2(xc, x_o)
+
+
+def test_wbfbt_rejects_surface_scaling_without_blending(shell):
+    M = lib_mesh(shell, 1, False, BC_SHELL)
+    p = lib_p(M, 1, 3)
+    with pytest.raises(hhg.HHGError):
+        hhg.hhg_kp1_apply(M, 1, None, 2.0, p)
+    hhg.hhg_kp1_apply(M, 1, None, 1.0, p)
