@@ -630,11 +630,12 @@ class StokesSolver:
 
     def __init__(self, mg, eta, gamma, restart=30, max_iters=100, tol=1e-8, sigma=1.0, omega=0.3, tol_A=1e-2,
                  ablock_max_iters=200, tol_mass=1e-10, mass_max_iters=500, schur="mass", mg_cheap=None,
-                 tol_vbfbt=1e-1, vbfbt_max_iters=100, uzawa="symmetric", a_l=1.0, a_r=1.0, tol_wbfbt=1e-1,
-                 tol_wbfbt_abs=0.0, wbfbt_max_iters=100, tol_vmass=1e-6, vmass_max_iters=200):
+                 tol_vbfbt=1e-1, vbfbt_max_iters=100, uzawa="symmetric", a_l=1.0, a_r=1.0, tol_wbfbt=1e-10,
+                 tol_wbfbt_abs=1e-10, wbfbt_max_iters=100, tol_vmass=1e-4, vmass_max_iters=500):
         """schur: "mass" (S = M_{1/eta}, eq:schurMass), "vbfbt" (eq:schurV; mg_cheap = the A_C hierarchy,
         Table 1: V(1,1) with degree-1 Chebyshev) or "wbfbt" (eq:schurWBFBT with the a_l / a_r scaling;
-        K_{1/sqrt(eta)} by GMG-CG to tol_wbfbt / tol_wbfbt_abs, M_{sqrt(eta)} by Jacobi-CG to tol_vmass)."""
+        K_{1/sqrt(eta)} by GMG-CG to tol_wbfbt / tol_wbfbt_abs, M_{sqrt(eta)} by Jacobi-CG to tol_vmass;
+        defaults from Table 1: 1e-10, 1e-4, a_l = a_r = 1)."""
         self.mg, self.mg_cheap = mg, mg_cheap
         self._eta = eta
         prm = _StokesParams(restart, max_iters, tol, sigma, omega, tol_A, ablock_max_iters, tol_mass, mass_max_iters,

@@ -12,7 +12,12 @@ from bench import build_case, GAMMA
 from workload import temperature
 ap = argparse.ArgumentParser()
 ap.add_argument("--level", type=int, default=4)
-ap.add_argument("--schur", default="vbfbt", choices=["vbfbt", "mass"])
+ap.add_argument("--schur", default="vbfbt", choices=["vbfbt", "mass", "wbfbt"])
+ap.add_argument("--omega", type=float, default=0.3, help="Uzawa pressure scaling (Table 1: 0.3; P:685: 0.0125 for w-BFBT)")
+ap.add_argument("--a-l", type=float, default=1.0)
+ap.add_argument("--a-r", type=float, default=1.0)
+ap.add_argument("--uzawa", default="symmetric", choices=["symmetric", "inexact", "adjoint"])
+ap.add_argument("--tol-A", type=float, default=1e-2)
 ap.add_argument("--tol", type=float, default=1e-8)
 ap.add_argument("--max-iters", type=int, default=60)
 ap.add_argument("--restart", type=int, default=30)
@@ -43,7 +48,7 @@ T = M.from_canonical(L, hhg.HHG_P1, temperature(xc.cpu().numpy(), keys))
 f = hhg.hhg_buoyancy_load(M, L, T)
 rhs = torch.cat([f, M.zeros(L, hhg.HHG_P1)])
 S = hhg.StokesSolver(mg, etas[L], GAMMA, restart=a.restart, max_iters=a.max_iters, tol=a.tol, schur=a.schur,
-                     mg_cheap=mgc)
+                     mg_cheap=mgc, omega=a.omega, a_l=a.a_l, a_r=a.a_r, uzawa=a.uzawa, tol_A=a.tol_A)
 torch.cuda.synchronize()
 setup = time.perf_counter() - t0
 s = torch.cuda.Stream()
@@ -56,6 +61,6 @@ s.synchronize()
 ms = e0.elapsed_time(e1)
 n_p = M.canonical_len(L, hhg.HHG_P1)
 x2, ita, rela = mg.ablock_cg(f, tol=1e-2, max_iters=200)
-print(json.dumps({"what": "stokes_solve", "l_eta": a.l_eta, "ablock_cg_iters_tol1e-2": ita, "ablock_rel": rela, "level": L, "schur": a.schur, "velocity_dofs": n_dof, "pressure_dofs": n_p,
+print(json.dumps({"what": "stokes_solve", "l_eta": a.l_eta, "ablock_cg_iters_tol1e-2": ita, "ablock_rel": rela, "level": L, "schur": a.schur, "omega": a.omega, "a_l": a.a_l, "a_r": a.a_r, "uzawa": a.uzawa, "tol_A": a.tol_A, "velocity_dofs": n_dof, "pressure_dofs": n_p,
                   "fgmres_iters": it, "rel_res": rel, "tol": a.tol, "solve_s": ms / 1e3, "setup_s": setup,
                   "viscosity": f"contrast {a.contrast:g} x {a.jump:g} jump", "rhs": "buoyancy (T - 1/2) x/|x|, g = 0"}))
