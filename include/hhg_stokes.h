@@ -367,6 +367,30 @@ int hhg_kmg_solve(hhg_kmg* kmg, const double* rhs, double* x, double tol, double
                   double* rel_res, hhg_stream_t stream);
 int hhg_kmg_destroy(hhg_kmg* kmg);
 
+/* ------------------------------------------------------------------ temperature operator (NEXT-4, part)
+ * eq:WeakTemp without the MMOC advection step: for P2 scalar T and test w
+ *   L(T, w) = s int T w + tau [ int (u . grad T) w + int kappa grad T . grad(w / rho) - int beta T (u . g) w ]
+ * with rho = exp(gamma (1 - |x|)) (grad ln rho = -gamma x/|x|), g = -x/|x|, u a P2VEC velocity;
+ *   P(T, w) = s int T w + tau int (kappa / rho) grad T . grad w   (the symmetric mass + diffusion part).
+ * s = s^{n+1} of the BDF2 step, tau = tau^{n+1}, kappa = k/(Pe C_p), beta = Di alpha / C_p. */
+typedef struct {
+  double s, tau, kappa, beta, gamma;
+} hhg_temp_params;
+/* y = L T (which 0), P T (1) or diag(P) (2, T ignored); unconstrained, interface-summed, overwritten.
+ * u: consistent P2VEC (which 0 only), T / y: consistent P2 scalars on `level`. */
+int hhg_temp_apply(const hhg_mesh* mesh, int level, const hhg_temp_params* prm, const double* u, const double* T,
+                   double* y, int which, hhg_stream_t stream);
+/* The temperature solve of P:548: FGMRES (restarted, right-preconditioned by CG on P with the inverse
+ * diagonal, to tol_cg) for L T = b at interior nodes with T fixed on the boundary nodes that carry a
+ * velocity BC (surface and CMB for the shell).  T: in = Dirichlet values on those nodes (interior entries
+ * ignored), out = solution.  Stops at |r| <= tol |r0| or |r| <= tol_abs (2-norm over unique interior
+ * nodes) or max_iters.  Workspace allocated in create.  Synchronises (host Arnoldi). */
+typedef struct hhg_temp_solver hhg_temp_solver;
+int hhg_temp_solver_create(hhg_mesh* mesh, int level, const hhg_temp_params* prm, int restart, hhg_temp_solver** out);
+int hhg_temp_solve(hhg_temp_solver* S, const double* u, const double* b, double* T, double tol, double tol_abs,
+                   int max_iters, double tol_cg, int cg_max_iters, int* iters, double* rel_res, hhg_stream_t stream);
+int hhg_temp_solver_destroy(hhg_temp_solver* S);
+
 /* Number of kernels launched by the library on this thread since the last reset. */
 int64_t hhg_launch_count(int reset);
 

@@ -45,6 +45,7 @@ EXPORTS = [
     "hhg_mg_create_qeta", "epsilon_apply_qeta", "hhg_diag_qeta",
     "hhg_stokes_schur_apply", "hhg_kp1_apply", "hhg_kp1_diag", "hhg_vmass_apply", "hhg_vmass_diag",
     "p1_prolong", "p1_restrict", "hhg_kmg_create", "hhg_kmg_solve", "hhg_kmg_destroy",
+    "hhg_temp_apply", "hhg_temp_solver_create", "hhg_temp_solve", "hhg_temp_solver_destroy",
 ]
 
 
@@ -96,6 +97,8 @@ def _load():
         "p1_prolong": ([P, I, P, P, P], I), "p1_restrict": ([P, I, P, P, P], I),
         "hhg_kmg_create": ([P, P, P, D, P], I), "hhg_kmg_solve": ([P, P, P, D, D, I, P, P, P], I),
         "hhg_kmg_destroy": ([P], I),
+        "hhg_temp_apply": ([P, I, P, P, P, P, I, P], I), "hhg_temp_solver_create": ([P, I, P, I, P], I),
+        "hhg_temp_solve": ([P, P, P, P, D, D, I, D, I, P, P, P], I), "hhg_temp_solver_destroy": ([P], I),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -612,6 +615,46 @@ class KMG:
         _chk(_lib.hhg_kmg_solve(self.handle, _dev(rhs, n, "rhs"), _dev(x, n, "x"), float(tol), float(tol_abs),
                                 int(max_iters), ctypes.byref(it), ctypes.byref(rel), _stream(stream)))
         return x, it.value, rel.value
+
+
+class _TempParams(ctypes.Structure):
+    _fields_ = [("s", ctypes.c_double), ("tau", ctypes.c_double), ("kappa", ctypes.c_double),
+                ("beta", ctypes.c_double), ("gamma", ctypes.c_double)]
+
+
+def hhg_temp_apply(mesh, level, prm, u, T, y=None, which=0, stream=None):
+    """y = L T (which 0), P T (1) or diag P (2) of eq:WeakTemp; prm = dict(s, tau, kappa, beta, gamma)."""
+    n = mesh.vec_len(level, HHG_P2)
+    y = mesh.zeros(level, HHG_P2) if y is None else y
+    p = _TempParams(**{k: float(v) for k, v in prm.items()})
+    _chk(_lib.hhg_temp_apply(mesh.handle, level, ctypes.byref(p), _dev(u, mesh.vec_len(level, HHG_P2VEC), "u"),
+                             _dev(T, n, "T"), _dev(y, n, "y"), int(which), _stream(stream)))
+    return y
+
+
+class TempSolver:
+    """hhg_temp_solver_*: FGMRES preconditioned by CG on the mass + diffusion part."""
+
+    def __init__(self, mesh, level, prm, restart=30):
+        self.mesh, self.level = mesh, level
+        p = _TempParams(**{k: float(v) for k, v in prm.items()})
+        h = ctypes.c_void_p()
+        _chk(_lib.hhg_temp_solver_create(mesh.handle, level, ctypes.byref(p), int(restart), ctypes.byref(h)))
+        self.handle = h
+
+    def __del__(self):
+        if getattr(self, "handle", None) and _lib is not None:
+            _lib.hhg_temp_solver_destroy(self.handle)
+            self.handle = None
+
+    def solve(self, u, b, T, tol=1e-10, tol_abs=0.0, max_iters=100, tol_cg=1e-13, cg_max_iters=2000, stream=None):
+        """T: in = Dirichlet values on the boundary nodes, out = solution -> (T, iterations, rel. residual)."""
+        n = self.mesh.vec_len(self.level, HHG_P2)
+        it, rel = ctypes.c_int(), ctypes.c_double()
+        _chk(_lib.hhg_temp_solve(self.handle, _dev(u, self.mesh.vec_len(self.level, HHG_P2VEC), "u"), _dev(b, n, "b"),
+                                 _dev(T, n, "T"), float(tol), float(tol_abs), int(max_iters), float(tol_cg),
+                                 int(cg_max_iters), ctypes.byref(it), ctypes.byref(rel), _stream(stream)))
+        return T, it.value, rel.value
 
 
 class _StokesParams(ctypes.Structure):

@@ -142,6 +142,10 @@ int launch_elem_surf(const Mesh* m, const Level& L, int mode, const double* eta,
                      const double* in, double* out, cudaStream_t s);
 int surf_op(const Mesh* m, int level, int mode, const double* eta, double a, const double* in, double* out,
             cudaStream_t s);  // element kernel + interface sum (+ P_v M for ELEM_VMASS)
+// temperature operator of eq:WeakTemp (hhg_temp.cu): mode 0 y += L T, 1 y += P T, 2 y += diag P
+typedef hhg_temp_params TempCoef;
+int launch_temp(const Mesh* m, const Level& L, int mode, TempCoef cf, const double* u, const double* T, double* y,
+                cudaStream_t s);
 int launch_p1_prolong(const Mesh* m, const Level& Lc, const Level& Lf, const double* xc, double* xf, cudaStream_t s);
 int launch_p1_restrict(const Mesh* m, const Level& Lc, const Level& Lf, const double* rf, double* rc, cudaStream_t s);
 int launch_elem_qeta(const Mesh* m, const Level& L, int mode, const double* T2, double lnC, double jump, double r_jump,

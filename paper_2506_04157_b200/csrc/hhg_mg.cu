@@ -1263,3 +1263,221 @@ int hhg_stokes_solve(hhg_stokes* S, const double* rhs, double* x, int* iters_out
 }
 
 }  // extern "C"
+
+// ================================================================ temperature solve (NEXT-4, part)
+// "an FGMRES outer loop preconditioned by a CG solver solving the symmetric, positive
+// semidefinite mass and diffusion part of the left-hand-side"; Dirichlet values on the surface and
+// the CMB.  Unknown delta = T - T_D lives on the interior nodes (bcn2 == -1); every Krylov vector and
+// operator output is masked to them (the boundary rows of the constrained system are the identity
+// with a zero right-hand side, so they stay zero).
+namespace {
+__global__ void k_mask(int64_t n, const int32_t* __restrict__ bcn, int keep_boundary, const double* __restrict__ in,
+                       double* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const bool bnd = bcn[i] != -1;
+    out[i] = (bnd == (keep_boundary != 0)) ? in[i] : 0.0;
+  }
+}
+int temp_apply_raw(const Mesh* m, int level, const hhg_temp_params& prm, const double* u, const double* T, double* y,
+                   int which, cudaStream_t s) {
+  const Level& L = m->levels[level];
+  HHG_CUDA(cudaMemsetAsync(y, 0, macro_count(m) * L.npts2 * sizeof(double), s));
+  HHG_TRY(launch_temp(m, L, which, prm, u, T, y, s));
+  return launch_fixup(m, L, HHG_P2, true, false, y, s);
+}
+// restarted right-preconditioned FGMRES (MGS + Givens), host Hessenberg, device vectors
+int fgmres(int64_t n, int m, int max_iters, double tol, double tol_abs,
+           const std::function<int(const double*, double*)>& op, const std::function<int(const double*, double*)>& prec,
+           const std::function<int(const double*, const double*, double*)>& dot, std::vector<double*>& V,
+           std::vector<double*>& Z, double* w, const double* b, double* x, cudaStream_t s, int* iters_out,
+           double* rel_out) {
+  double bn = 0.0;
+  HHG_TRY(dot(b, b, &bn));
+  bn = std::sqrt(bn);
+  HHG_CUDA(cudaMemsetAsync(x, 0, n * sizeof(double), s));
+  int total = 0;
+  double rel = bn > 0 ? 1.0 : 0.0;
+  std::vector<double> H((size_t)(m + 1) * m), cs(m), sn(m), g(m + 1), y(m);
+  while (bn > 0 && total < max_iters && rel > tol && rel * bn > tol_abs) {
+    HHG_TRY(op(x, w));
+    HHG_TRY(launch_axpby(n, 1.0, b, -1.0, w, s));
+    double beta = 0.0;
+    HHG_TRY(dot(w, w, &beta));
+    beta = std::sqrt(beta);
+    rel = beta / bn;
+    if (rel <= tol || beta <= tol_abs) break;
+    HHG_TRY(launch_axpby(n, 1.0 / beta, w, 0.0, V[0], s));
+    std::fill(g.begin(), g.end(), 0.0);
+    g[0] = beta;
+    int j = 0;
+    for (; j < m && total < max_iters; ++j) {
+      ++total;
+      HHG_TRY(prec(V[j], Z[j]));
+      HHG_TRY(op(Z[j], w));
+      for (int i = 0; i <= j; ++i) {
+        double h = 0.0;
+        HHG_TRY(dot(w, V[i], &h));
+        H[(size_t)i * m + j] = h;
+        HHG_TRY(launch_axpby(n, -h, V[i], 1.0, w, s));
+      }
+      double hn = 0.0;
+      HHG_TRY(dot(w, w, &hn));
+      hn = std::sqrt(hn);
+      H[(size_t)(j + 1) * m + j] = hn;
+      if (hn > 0) HHG_TRY(launch_axpby(n, 1.0 / hn, w, 0.0, V[j + 1], s));
+      for (int i = 0; i < j; ++i) {
+        const double h0 = H[(size_t)i * m + j], h1 = H[(size_t)(i + 1) * m + j];
+        H[(size_t)i * m + j] = cs[i] * h0 + sn[i] * h1;
+        H[(size_t)(i + 1) * m + j] = -sn[i] * h0 + cs[i] * h1;
+      }
+      const double h0 = H[(size_t)j * m + j], h1 = H[(size_t)(j + 1) * m + j];
+      const double d = std::hypot(h0, h1);
+      cs[j] = d > 0 ? h0 / d : 1.0;
+      sn[j] = d > 0 ? h1 / d : 0.0;
+      H[(size_t)j * m + j] = d;
+      H[(size_t)(j + 1) * m + j] = 0.0;
+      g[j + 1] = -sn[j] * g[j];
+      g[j] = cs[j] * g[j];
+      rel = std::fabs(g[j + 1]) / bn;
+      if (rel <= tol || rel * bn <= tol_abs || hn == 0.0) {
+        ++j;
+        break;
+      }
+    }
+    for (int i = j - 1; i >= 0; --i) {
+      double acc = g[i];
+      for (int k = i + 1; k < j; ++k) acc -= H[(size_t)i * m + k] * y[k];
+      y[i] = acc / H[(size_t)i * m + i];
+    }
+    for (int i = 0; i < j; ++i) HHG_TRY(launch_axpby(n, y[i], Z[i], 1.0, x, s));
+  }
+  if (bn > 0) {  // true residual
+    HHG_TRY(op(x, w));
+    HHG_TRY(launch_axpby(n, 1.0, b, -1.0, w, s));
+    double rr = 0.0;
+    HHG_TRY(dot(w, w, &rr));
+    rel = std::sqrt(rr) / bn;
+  }
+  if (iters_out) *iters_out = total;
+  if (rel_out) *rel_out = rel;
+  return HHG_OK;
+}
+}  // namespace
+
+struct hhg_temp_solver {
+  hhg_mesh* mesh = nullptr;
+  int level = 0, restart = 0;
+  hhg_temp_params prm{};
+  int64_t n = 0;
+  std::vector<double*> V, Z;
+  double *w = nullptr, *td = nullptr, *bp = nullptr, *dl = nullptr, *dinv = nullptr, *t1 = nullptr;
+  double *cr = nullptr, *cz = nullptr, *cp = nullptr, *cq = nullptr, *sc = nullptr;
+  ~hhg_temp_solver() {
+    for (double* p : V) cudaFree(p);
+    for (double* p : Z) cudaFree(p);
+    for (double* p : {w, td, bp, dl, dinv, t1, cr, cz, cp, cq, sc})
+      if (p) cudaFree(p);
+  }
+};
+
+extern "C" {
+int hhg_temp_apply(const hhg_mesh* mesh, int level, const hhg_temp_params* prm, const double* u, const double* T,
+                   double* y, int which, hhg_stream_t stream) {
+  if (!mesh || !prm || !y || (which != 2 && !T) || (which == 0 && !u)) return fail(HHG_EINVAL, "hhg_temp_apply: NULL argument");
+  if (which < 0 || which > 2) return fail(HHG_EINVAL, "hhg_temp_apply: which must be 0, 1 or 2");
+  if (level < 0 || level > mesh->level_max) return fail(HHG_ELEVEL, "hhg_temp_apply: bad level");
+  auto* m = const_cast<hhg_mesh*>(mesh);
+  HHG_TRY(ensure_level(m, level));
+  return temp_apply_raw(m, level, *prm, u, T, y, which, (cudaStream_t)stream);
+}
+
+int hhg_temp_solver_create(hhg_mesh* mesh, int level, const hhg_temp_params* prm, int restart, hhg_temp_solver** out) {
+  if (!mesh || !prm || !out) return fail(HHG_EINVAL, "hhg_temp_solver_create: NULL argument");
+  if (level < 0 || level > mesh->level_max) return fail(HHG_ELEVEL, "hhg_temp_solver_create: bad level");
+  if (restart < 1) return fail(HHG_EINVAL, "hhg_temp_solver_create: restart >= 1");
+  HHG_TRY(ensure_level(mesh, level));
+  auto* S = new hhg_temp_solver();
+  S->mesh = mesh;
+  S->level = level;
+  S->prm = *prm;
+  S->restart = restart;
+  S->n = macro_count(mesh) * mesh->levels[level].npts2;
+  auto alloc = [&](double** p) { return cudaMalloc(p, std::max<int64_t>(S->n, 1) * sizeof(double)) == cudaSuccess; };
+  bool ok = true;
+  S->V.resize(restart + 1, nullptr);
+  S->Z.resize(restart, nullptr);
+  for (auto& p : S->V) ok = ok && alloc(&p);
+  for (auto& p : S->Z) ok = ok && alloc(&p);
+  for (double** p : {&S->w, &S->td, &S->bp, &S->dl, &S->dinv, &S->t1, &S->cr, &S->cz, &S->cp, &S->cq}) ok = ok && alloc(p);
+  ok = ok && cudaMalloc(&S->sc, 16 * sizeof(double)) == cudaSuccess;
+  if (!ok) {
+    delete S;
+    return fail(HHG_ENOMEM, "hhg_temp_solver_create: workspace");
+  }
+  int r = temp_apply_raw(mesh, level, S->prm, nullptr, nullptr, S->dinv, 2, nullptr);
+  if (r == HHG_OK) r = launch_recip(S->n, S->dinv, nullptr);
+  if (r == HHG_OK && cudaDeviceSynchronize() != cudaSuccess) r = fail(HHG_ECUDA, "hhg_temp_solver_create: sync");
+  if (r != HHG_OK) {
+    delete S;
+    return r;
+  }
+  *out = S;
+  return HHG_OK;
+}
+
+int hhg_temp_solve(hhg_temp_solver* S, const double* u, const double* b, double* T, double tol, double tol_abs,
+                   int max_iters, double tol_cg, int cg_max_iters, int* iters, double* rel_res, hhg_stream_t stream) {
+  if (!S || !u || !b || !T) return fail(HHG_EINVAL, "hhg_temp_solve: NULL argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  const Mesh* m = S->mesh;
+  const Level& L = m->levels[S->level];
+  const int64_t n = S->n;
+  const unsigned nb = vg(n);
+  auto mask = [&](const double* in, double* out, int keep_bnd) -> int {
+    k_mask<<<nb, 256, 0, s>>>(n, L.bcn2, keep_bnd, in, out);
+    count_launch();
+    return HHG_OK;
+  };
+  auto dot = [&](const double* x, const double* y, double* out) -> int {
+    HHG_TRY(launch_dot(m, L, HHG_P2, x, y, S->sc + 8, s));
+    HHG_CUDA(cudaMemcpyAsync(out, S->sc + 8, sizeof(double), cudaMemcpyDeviceToHost, s));
+    HHG_CUDA(cudaStreamSynchronize(s));
+    return HHG_OK;
+  };
+  auto opL = [&](const double* x, double* y) -> int {
+    HHG_TRY(temp_apply_raw(m, S->level, S->prm, u, x, y, 0, s));
+    return mask(y, y, 0);
+  };
+  auto opP = [&](const double* x, double* y) -> int {
+    HHG_TRY(temp_apply_raw(m, S->level, S->prm, nullptr, x, y, 1, s));
+    return mask(y, y, 0);
+  };
+  auto jac = [&](const double* r, double* z) -> int {
+    HHG_TRY(launch_pcg_scale(n, S->dinv, r, z, s));
+    return mask(z, z, 0);
+  };
+  auto prec = [&](const double* r, double* z) -> int {
+    int it;
+    double rel;
+    return dev_pcg(m, L, HHG_P2, n, opP, jac, std::function<int(double*)>(), r, z, tol_cg, 0.0, cg_max_iters, S->cr,
+                   S->cz, S->cp, S->cq, S->sc, s, &it, &rel);
+  };
+  // T_D on the boundary, b' = mask_int(b - L T_D)
+  HHG_TRY(mask(T, S->td, 1));
+  HHG_TRY(temp_apply_raw(m, S->level, S->prm, u, S->td, S->t1, 0, s));
+  HHG_TRY(launch_axpby(n, 1.0, b, -1.0, S->t1, s));
+  HHG_TRY(mask(S->t1, S->bp, 0));
+  HHG_TRY(fgmres(n, S->restart, max_iters, tol, tol_abs, opL, prec, dot, S->V, S->Z, S->w, S->bp, S->dl, s, iters,
+                 rel_res));
+  // T = T_D + delta
+  HHG_CUDA(cudaMemcpyAsync(T, S->td, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  HHG_TRY(launch_axpby(n, 1.0, S->dl, 1.0, T, s));
+  HHG_CUDA(cudaStreamSynchronize(s));
+  return HHG_OK;
+}
+
+int hhg_temp_solver_destroy(hhg_temp_solver* S) {
+  delete S;
+  return HHG_OK;
+}
+}  // extern "C"
