@@ -897,56 +897,29 @@ int st_dot(hhg_stokes* S, const double* x, const double* y, int what, double* ou
   return HHG_OK;
 }
 int st_mean0(hhg_stokes* S, double* p, cudaStream_t s) {  // P_p: arithmetic mean zero over unique nodes
+  // device-only: fused owner-masked sum, then p -= sum / n_unique read on the device (no host sync)
   const Level& L = S->mesh->levels[S->level];
-  HHG_TRY(launch_dot(S->mesh, L, HHG_P1, p, S->ones, S->sc + 2, s));
-  double sum = 0.0;
-  HHG_CUDA(cudaMemcpyAsync(&sum, S->sc + 2, sizeof(double), cudaMemcpyDeviceToHost, s));
-  HHG_CUDA(cudaStreamSynchronize(s));
-  return launch_axpby(S->n1, -sum / S->n_unique_p, S->ones, 1.0, p, s);
+  HHG_TRY(launch_dot_fused(S->mesh, L, HHG_P1, p, S->ones, S->sc + 2, s));
+  k_shift<<<vg(S->n1), 256, 0, s>>>(S->n1, S->sc + 2, 1.0 / S->n_unique_p, p);
+  count_launch();
+  return HHG_OK;
 }
 // y = P K x : [ (M P_v)(A u + B^T p) ; P_p (B + C) u ]
 int st_op(hhg_stokes* S, const double* x, double* y, cudaStream_t s) {
   HHG_TRY(stokes_apply(S->mesh, S->level, S->eta, S->gamma, x, x + S->n2, y, y + S->n2, (hhg_stream_t)s));
   return st_mean0(S, y + S->n2, s);
 }
-// z_p = M_{1/eta}^-1 r_p by Jacobi-CG from 0 to relative tolerance tol_M (mass SPD)
+// z_p = M_{1/eta}^-1 r_p by Jacobi-CG from 0 to relative tolerance tol_M (mass SPD); device scalars,
+// one host sync per iteration (dev_pcg), scalar slots sc[8..11]
 int st_mass_solve(hhg_stokes* S, const double* rp, double* zp, cudaStream_t s) {
-  const int64_t n = S->n1;
-  HHG_CUDA(cudaMemsetAsync(zp, 0, n * sizeof(double), s));
-  HHG_CUDA(cudaMemcpyAsync(S->mr, rp, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  const Level& L = S->mesh->levels[S->level];
-  auto pdot = [&](const double* x, const double* y, double* out) -> int {
-    HHG_TRY(launch_dot(S->mesh, L, HHG_P1, x, y, S->sc + 3, s));
-    HHG_CUDA(cudaMemcpyAsync(out, S->sc + 3, sizeof(double), cudaMemcpyDeviceToHost, s));
-    HHG_CUDA(cudaStreamSynchronize(s));
-    return HHG_OK;
-  };
-  auto jac = [&](const double* r, double* z) { return launch_pcg_scale(n, S->mdinv, r, z, s); };
-  double r0 = 0.0;
-  HHG_TRY(pdot(S->mr, S->mr, &r0));
-  r0 = std::sqrt(r0);
-  if (!(r0 > 0)) return HHG_OK;
-  HHG_TRY(jac(S->mr, S->mz));
-  HHG_CUDA(cudaMemcpyAsync(S->mp, S->mz, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  double rz = 0.0;
-  HHG_TRY(pdot(S->mr, S->mz, &rz));
-  for (int it = 0; it < S->prm.mass_max_iters; ++it) {
-    HHG_TRY(hhg_mass_apply(S->mesh, S->level, S->eta, S->mp, S->mq, (hhg_stream_t)s));
-    double pq = 0.0;
-    HHG_TRY(pdot(S->mp, S->mq, &pq));
-    const double alpha = pq != 0.0 ? rz / pq : 0.0;
-    HHG_TRY(launch_axpby(n, alpha, S->mp, 1.0, zp, s));
-    HHG_TRY(launch_axpby(n, -alpha, S->mq, 1.0, S->mr, s));
-    double rr = 0.0;
-    HHG_TRY(pdot(S->mr, S->mr, &rr));
-    if (std::sqrt(std::max(rr, 0.0)) <= S->prm.tol_mass * r0) break;
-    HHG_TRY(jac(S->mr, S->mz));
-    double rzn = 0.0;
-    HHG_TRY(pdot(S->mr, S->mz, &rzn));
-    HHG_TRY(launch_axpby(n, 1.0, S->mz, rzn / rz, S->mp, s));  // p = z + beta p
-    rz = rzn;
-  }
-  return HHG_OK;
+  const Mesh* m = S->mesh;
+  const Level& L = m->levels[S->level];
+  auto op = [&](const double* x, double* y) -> int { return hhg_mass_apply(S->mesh, S->level, S->eta, x, y, (hhg_stream_t)s); };
+  auto jac = [&](const double* r, double* z) -> int { return launch_pcg_scale(S->n1, S->mdinv, r, z, s); };
+  int it;
+  double rel;
+  return dev_pcg(m, L, HHG_P1, S->n1, op, jac, std::function<int(double*)>(), rp, zp, S->prm.tol_mass, 0.0,
+                 S->prm.mass_max_iters, S->mr, S->mz, S->mp, S->mq, S->sc + 8, s, &it, &rel);
 }
 // w = P_p B A_C^-1 B^T y  (A_C^-1 = one cheap V-cycle, eq:schurV)
 int st_bacbt(hhg_stokes* S, const double* y, double* w, cudaStream_t s) {
@@ -955,45 +928,18 @@ int st_bacbt(hhg_stokes* S, const double* y, double* w, cudaStream_t s) {
   HHG_TRY(div_apply(S->mesh, S->level, 0.0, S->bv, w, (hhg_stream_t)s));
   return st_mean0(S, w, s);
 }
-// y = (B A_C^-1 B^T)^-1 t by CG preconditioned by M_{1/eta} (mass CG to tol_mass), to tol_vbfbt
+// y = (B A_C^-1 B^T)^-1 t by CG preconditioned by M_{1/eta} (mass CG to tol_mass), to tol_vbfbt;
+// mean-zero projections of r, z and y (P_p); scalar slots sc[12..15]
 int st_bacbt_solve(hhg_stokes* S, const double* t, double* y, cudaStream_t s) {
-  const int64_t n = S->n1;
-  const Level& L = S->mesh->levels[S->level];
-  auto pdot = [&](const double* x, const double* v, double* out) -> int {
-    HHG_TRY(launch_dot(S->mesh, L, HHG_P1, x, v, S->sc + 5, s));
-    HHG_CUDA(cudaMemcpyAsync(out, S->sc + 5, sizeof(double), cudaMemcpyDeviceToHost, s));
-    HHG_CUDA(cudaStreamSynchronize(s));
-    return HHG_OK;
-  };
-  HHG_CUDA(cudaMemsetAsync(y, 0, n * sizeof(double), s));
-  HHG_CUDA(cudaMemcpyAsync(S->br, t, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  double r0 = 0.0;
-  HHG_TRY(pdot(S->br, S->br, &r0));
-  r0 = std::sqrt(r0);
-  if (!(r0 > 0)) return HHG_OK;
-  HHG_TRY(st_mass_solve(S, S->br, S->bz, s));
-  HHG_TRY(st_mean0(S, S->bz, s));
-  HHG_CUDA(cudaMemcpyAsync(S->bp, S->bz, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  double rz = 0.0;
-  HHG_TRY(pdot(S->br, S->bz, &rz));
-  for (int it = 0; it < S->prm.vbfbt_max_iters; ++it) {
-    HHG_TRY(st_bacbt(S, S->bp, S->bq, s));
-    double pq = 0.0;
-    HHG_TRY(pdot(S->bp, S->bq, &pq));
-    const double alpha = pq != 0.0 ? rz / pq : 0.0;
-    HHG_TRY(launch_axpby(n, alpha, S->bp, 1.0, y, s));
-    HHG_TRY(launch_axpby(n, -alpha, S->bq, 1.0, S->br, s));
-    double rr = 0.0;
-    HHG_TRY(pdot(S->br, S->br, &rr));
-    if (std::sqrt(std::max(rr, 0.0)) <= S->prm.tol_vbfbt * r0) break;
-    HHG_TRY(st_mass_solve(S, S->br, S->bz, s));
-    HHG_TRY(st_mean0(S, S->bz, s));
-    double rzn = 0.0;
-    HHG_TRY(pdot(S->br, S->bz, &rzn));
-    HHG_TRY(launch_axpby(n, 1.0, S->bz, rzn / rz, S->bp, s));
-    rz = rzn;
-  }
-  return st_mean0(S, y, s);
+  const Mesh* m = S->mesh;
+  const Level& L = m->levels[S->level];
+  auto op = [&](const double* x, double* w) -> int { return st_bacbt(S, x, w, s); };
+  auto prec = [&](const double* r, double* z) -> int { return st_mass_solve(S, r, z, s); };
+  auto proj = [&](double* v) -> int { return st_mean0(S, v, s); };
+  int it;
+  double rel;
+  return dev_pcg(m, L, HHG_P1, S->n1, op, prec, proj, t, y, S->prm.tol_vbfbt, 0.0, S->prm.vbfbt_max_iters, S->br,
+                 S->bz, S->bp, S->bq, S->sc + 12, s, &it, &rel);
 }
 // z_p = S_V^-1 t (eq:schurV): (B A_C^-1 B^T)^-1 (B A_C^-1 A A_C^-1 B^T) (B A_C^-1 B^T)^-1 t
 int st_vbfbt(hhg_stokes* S, const double* t, double* z, cudaStream_t s) {
@@ -1019,7 +965,7 @@ int st_vmass_solve(hhg_stokes* S, double a, const double* vdinv, const double* v
   int it;
   double rel;
   return dev_pcg(m, L, HHG_P2VEC, S->n2, op, prec, std::function<int(double*)>(), v, x, S->prm.tol_vmass, 0.0,
-                 S->prm.vmass_max_iters, S->vr, S->vz, S->vp, S->vq, S->sc, s, &it, &rel);
+                 S->prm.vmass_max_iters, S->vr, S->vz, S->vp, S->vq, S->sc + 16, s, &it, &rel);
 }
 // z = S_w^-1 t (eq:schurWBFBT with a_l / a_r):
 //   K_{1/sqrt(eta_l)}^-1 B M_{sqrt(eta_l)}^-1 A M_{sqrt(eta_r)}^-1 B^T K_{1/sqrt(eta_r)}^-1 t
@@ -1123,7 +1069,7 @@ int hhg_stokes_create(hhg_mg* mg, hhg_mg* mg_cheap, const double* eta_p1, double
   for (double** p : {&S->bu, &S->bv}) ok = ok && alloc(p, S->n2);
   if (prm->schur == 2)
     for (double** p : {&S->vdl, &S->vdr, &S->vr, &S->vz, &S->vp, &S->vq}) ok = ok && alloc(p, S->n2);
-  ok = ok && alloc(&S->sc, 8);
+  ok = ok && alloc(&S->sc, 32);
   if (!ok) {
     delete S;
     return fail(HHG_ENOMEM, "hhg_stokes_create: workspace");
@@ -1131,7 +1077,7 @@ int hhg_stokes_create(hhg_mg* mg, hhg_mg* mg_cheap, const double* eta_p1, double
   cudaStream_t s = nullptr;
   int r = HHG_OK;
   auto run = [&]() -> int {
-    HHG_CUDA(cudaMemset(S->sc, 0, 8 * sizeof(double)));
+    HHG_CUDA(cudaMemset(S->sc, 0, 32 * sizeof(double)));
     HHG_TRY(launch_fill(S->n1, 1.0, S->ones, s));
     HHG_TRY(hhg_mass_diag(S->mesh, S->level, S->eta, S->mdinv, nullptr));
     HHG_TRY(launch_recip(S->n1, S->mdinv, s));
