@@ -390,6 +390,13 @@ int hhg_temp_solver_create(hhg_mesh* mesh, int level, const hhg_temp_params* prm
 int hhg_temp_solve(hhg_temp_solver* S, const double* u, const double* b, double* T, double tol, double tol_abs,
                    int max_iters, double tol_cg, int cg_max_iters, int* iters, double* rel_res, hhg_stream_t stream);
 int hhg_temp_solver_destroy(hhg_temp_solver* S);
+/* MMOC step: T_hat(x) = T(X(x)) at every P2 node x, X = RK4 back-tracking over tau along
+ * u(y, th) = (1 - th) u_new(y) + th u_old(y) (linear in time between t^{n+1} and t^n); fields evaluated
+ * at located points (inverse blending, macro, lattice cube, micro tet, P2 basis); points leaving the
+ * shell are moved radially onto it.  T, T_hat: consistent P2 scalars; u_*: consistent P2VEC.
+ * Synchronises; HHG_EINVAL if a point cannot be located (non-shell meshes: a point left the domain). */
+int hhg_mmoc(const hhg_mesh* mesh, int level, const double* T, const double* u_new, const double* u_old, double tau,
+             double* T_hat, hhg_stream_t stream);
 
 /* Number of kernels launched by the library on this thread since the last reset. */
 int64_t hhg_launch_count(int reset);

@@ -45,7 +45,7 @@ EXPORTS = [
     "hhg_mg_create_qeta", "epsilon_apply_qeta", "hhg_diag_qeta",
     "hhg_stokes_schur_apply", "hhg_kp1_apply", "hhg_kp1_diag", "hhg_vmass_apply", "hhg_vmass_diag",
     "p1_prolong", "p1_restrict", "hhg_kmg_create", "hhg_kmg_solve", "hhg_kmg_destroy",
-    "hhg_temp_apply", "hhg_temp_solver_create", "hhg_temp_solve", "hhg_temp_solver_destroy",
+    "hhg_temp_apply", "hhg_temp_solver_create", "hhg_temp_solve", "hhg_temp_solver_destroy", "hhg_mmoc",
 ]
 
 
@@ -99,6 +99,7 @@ def _load():
         "hhg_kmg_destroy": ([P], I),
         "hhg_temp_apply": ([P, I, P, P, P, P, I, P], I), "hhg_temp_solver_create": ([P, I, P, I, P], I),
         "hhg_temp_solve": ([P, P, P, P, D, D, I, D, I, P, P, P], I), "hhg_temp_solver_destroy": ([P], I),
+        "hhg_mmoc": ([P, I, P, P, P, D, P, P], I),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -630,6 +631,16 @@ def hhg_temp_apply(mesh, level, prm, u, T, y=None, which=0, stream=None):
     _chk(_lib.hhg_temp_apply(mesh.handle, level, ctypes.byref(p), _dev(u, mesh.vec_len(level, HHG_P2VEC), "u"),
                              _dev(T, n, "T"), _dev(y, n, "y"), int(which), _stream(stream)))
     return y
+
+
+def hhg_mmoc(mesh, level, T, u_new, u_old, tau, T_hat=None, stream=None):
+    """T_hat = T at the RK4 back-tracked positions of the P2 nodes (MMOC)."""
+    n = mesh.vec_len(level, HHG_P2)
+    nv = mesh.vec_len(level, HHG_P2VEC)
+    T_hat = mesh.zeros(level, HHG_P2) if T_hat is None else T_hat
+    _chk(_lib.hhg_mmoc(mesh.handle, level, _dev(T, n, "T"), _dev(u_new, nv, "u_new"), _dev(u_old, nv, "u_old"),
+                       float(tau), _dev(T_hat, n, "T_hat"), _stream(stream)))
+    return T_hat
 
 
 class TempSolver:

@@ -146,6 +146,8 @@ int surf_op(const Mesh* m, int level, int mode, const double* eta, double a, con
 typedef hhg_temp_params TempCoef;
 int launch_temp(const Mesh* m, const Level& L, int mode, TempCoef cf, const double* u, const double* T, double* y,
                 cudaStream_t s);
+int launch_mmoc(const Mesh* m, const Level& L, double rmin, double rmax, double tau, const double* T, const double* un,
+                const double* uo, double* out, int* fail_flag, cudaStream_t s);
 int launch_p1_prolong(const Mesh* m, const Level& Lc, const Level& Lf, const double* xc, double* xf, cudaStream_t s);
 int launch_p1_restrict(const Mesh* m, const Level& Lc, const Level& Lf, const double* rf, double* rc, cudaStream_t s);
 int launch_elem_qeta(const Mesh* m, const Level& L, int mode, const double* T2, double lnC, double jump, double r_jump,

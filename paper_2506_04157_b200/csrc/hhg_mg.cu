@@ -1422,6 +1422,33 @@ int hhg_temp_solve(hhg_temp_solver* S, const double* u, const double* b, double*
   return HHG_OK;
 }
 
+int hhg_mmoc(const hhg_mesh* mesh, int level, const double* T, const double* u_new, const double* u_old, double tau,
+             double* T_hat, hhg_stream_t stream) {
+  if (!mesh || !T || !u_new || !u_old || !T_hat) return fail(HHG_EINVAL, "hhg_mmoc: NULL argument");
+  if (level < 0 || level > mesh->level_max) return fail(HHG_ELEVEL, "hhg_mmoc: bad level");
+  auto* m = const_cast<hhg_mesh*>(mesh);
+  HHG_TRY(ensure_level(m, level));
+  const Level& L = m->levels[level];
+  cudaStream_t s = (cudaStream_t)stream;
+  double rmin = 1e300, rmax = 0.0;
+  for (int64_t v = 0; v < m->n_vert; ++v) {
+    const double r = std::sqrt(m->xyz[3 * v] * m->xyz[3 * v] + m->xyz[3 * v + 1] * m->xyz[3 * v + 1] +
+                               m->xyz[3 * v + 2] * m->xyz[3 * v + 2]);
+    rmin = std::min(rmin, r);
+    rmax = std::max(rmax, r);
+  }
+  int* flag = reinterpret_cast<int*>(L.red + kRedBlocks + 6);
+  HHG_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), s));
+  HHG_CUDA(cudaMemsetAsync(T_hat, 0, macro_count(m) * L.npts2 * sizeof(double), s));
+  HHG_TRY(launch_mmoc(m, L, rmin, rmax, tau, T, u_new, u_old, T_hat, flag, s));
+  HHG_TRY(launch_fixup(m, L, HHG_P2, true, false, T_hat, s));  // owner values to every copy
+  int h = 0;
+  HHG_CUDA(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+  HHG_CUDA(cudaStreamSynchronize(s));
+  if (h) return fail(HHG_EINVAL, "hhg_mmoc: a back-tracked point could not be located in the mesh");
+  return HHG_OK;
+}
+
 int hhg_temp_solver_destroy(hhg_temp_solver* S) {
   delete S;
   return HHG_OK;

@@ -142,6 +142,215 @@ __global__ void k_temp(const MacroGeo* __restrict__ mgeo, int n1, int64_t npts2,
 }
 }  // namespace
 
+// ------------------------------------------------------------------ MMOC
+// Per owned stored P2 node: RK4 back-tracking along u(y, th) = (1 - th) u_new(y) + th u_old(y),
+// X = x - tau/6 (k1 + 2 k2 + 2 k3 + k4), T_hat = T(X).  A physical point is located by inverse blending
+// (directions are kept: x = |y| / (c n.y^) y^), the macro's barycentric coordinates (own macro of the
+// previous stage first, then all macros), the lattice cube and the one of its 6 tets (valid for the
+// cube's anchor sum) with the largest minimum barycentric coordinate; points outside the shell are
+// moved radially onto it (R28).
+namespace {
+__constant__ double kTinv[6][9];  // per tet type: inverse of [V1-V0 | V2-V0 | V3-V0] (unit-cube offsets)
+
+struct Loc {
+  int mac, t, ci, cj, ck;
+  double mu[4];
+};
+
+__device__ bool locate(const MacroGeo* __restrict__ mg, int nm, int n1, bool blend, const double (&y)[3], int hint,
+                       double tol, Loc& L) {
+  const double ry = sqrt(y[0] * y[0] + y[1] * y[1] + y[2] * y[2]);
+  const double d[3] = {y[0] / ry, y[1] / ry, y[2] / ry};
+  for (int a = 0; a <= nm; ++a) {
+    const int m = a == 0 ? hint : (a - 1 < hint ? a - 1 : a);
+    if (m >= nm) break;
+    const MacroGeo& g = mg[m];
+    double x[3];
+    if (blend) {
+      const double den = g.cK * (g.nhat[0] * d[0] + g.nhat[1] * d[1] + g.nhat[2] * d[2]);
+      if (!(den > 0.0)) continue;
+      for (int r = 0; r < 3; ++r) x[r] = ry / den * d[r];
+    } else {
+      for (int r = 0; r < 3; ++r) x[r] = y[r];
+    }
+    double lam[3];
+    for (int r = 0; r < 3; ++r)
+      lam[r] = g.Jminv[3 * r] * (x[0] - g.X0[0]) + g.Jminv[3 * r + 1] * (x[1] - g.X0[1]) + g.Jminv[3 * r + 2] * (x[2] - g.X0[2]);
+    if (fmin(fmin(lam[0], lam[1]), lam[2]) < -tol || lam[0] + lam[1] + lam[2] > 1.0 + tol) continue;
+    double xi[3];
+    int c[3];
+    for (int r = 0; r < 3; ++r) {
+      xi[r] = n1 * lam[r];
+      c[r] = min(max((int)floor(xi[r]), 0), n1 - 1);
+    }
+    while (c[0] + c[1] + c[2] > n1 - 1) {  // far-face points: step back along a coordinate with f ~ 0
+      int r = 0;
+      double best = 2.0;
+      for (int q = 0; q < 3; ++q)
+        if (c[q] > 0 && xi[q] - c[q] < best) best = xi[q] - c[q], r = q;
+      --c[r];
+    }
+    const int sc = c[0] + c[1] + c[2];
+    const double f[3] = {xi[0] - c[0], xi[1] - c[1], xi[2] - c[2]};
+    double bestmin = -1e300;
+    for (int t = 0; t < 6; ++t) {
+      if ((t >= 1 && t <= 4 && sc > n1 - 2) || (t == 5 && sc > n1 - 3)) continue;
+      double o[3];
+      for (int r = 0; r < 3; ++r) o[r] = f[r] - kTV[t][0][r];
+      double mu[4];
+      for (int r = 0; r < 3; ++r) mu[r + 1] = kTinv[t][3 * r] * o[0] + kTinv[t][3 * r + 1] * o[1] + kTinv[t][3 * r + 2] * o[2];
+      mu[0] = 1.0 - mu[1] - mu[2] - mu[3];
+      const double mn = fmin(fmin(mu[0], mu[1]), fmin(mu[2], mu[3]));
+      if (mn > bestmin) {
+        bestmin = mn;
+        L.t = t;
+        for (int v = 0; v < 4; ++v) L.mu[v] = mu[v];
+      }
+    }
+    L.mac = m;
+    L.ci = c[0];
+    L.cj = c[1];
+    L.ck = c[2];
+    return true;
+  }
+  return false;
+}
+
+// P2 basis of the located tet and the stored indices of its 10 nodes
+__device__ void p2_eval_setup(const Loc& L, int n1, double (&ph)[10], int (&idx)[10]) {
+  const int n2 = 2 * n1;
+  for (int v = 0; v < 4; ++v) {
+    ph[v] = L.mu[v] * (2.0 * L.mu[v] - 1.0);
+    idx[v] = rs32(n2, 2 * (L.cj + kTV[L.t][v][1]), 2 * (L.ck + kTV[L.t][v][2])) + 2 * (L.ci + kTV[L.t][v][0]);
+  }
+  for (int e = 0; e < 6; ++e) {
+    const int a = kEP[e][0], b = kEP[e][1];
+    ph[4 + e] = 4.0 * L.mu[a] * L.mu[b];
+    idx[4 + e] = rs32(n2, 2 * L.cj + kTV[L.t][a][1] + kTV[L.t][b][1], 2 * L.ck + kTV[L.t][a][2] + kTV[L.t][b][2]) +
+                 2 * L.ci + kTV[L.t][a][0] + kTV[L.t][b][0];
+  }
+}
+
+__device__ __forceinline__ void clamp_r(double (&y)[3], bool blend, double rmin, double rmax) {
+  if (!blend) return;
+  const double r = sqrt(y[0] * y[0] + y[1] * y[1] + y[2] * y[2]);
+  const double s = r > rmax ? rmax / r : (r < rmin ? rmin / r : 1.0);
+  for (int q = 0; q < 3; ++q) y[q] *= s;
+}
+
+__global__ void k_mmoc(const MacroGeo* __restrict__ mg, int nm, const int32_t* __restrict__ rows, int64_t nrows, int n1,
+                       int64_t npts2, const uint8_t* __restrict__ own, bool blend, double rmin, double rmax, double tau,
+                       const double* __restrict__ T, const double* __restrict__ un, const double* __restrict__ uo,
+                       double* __restrict__ out, int* __restrict__ fail_flag) {
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= nrows) return;
+  const int n2 = 2 * n1;
+  const int j = rows[row] & 0xffff, k = rows[row] >> 16, len = n2 - j - k + 1;
+  const int mac = blockIdx.y;
+  const int64_t cs = (int64_t)nm * npts2;
+  const MacroGeo& g = mg[mac];
+  for (int i = threadIdx.x & 31; i < len; i += 32) {
+    const int64_t node = (int64_t)mac * npts2 + rs32(n2, j, k) + i;
+    if (!own[node]) continue;
+    double x[3];
+    const double a = (double)i / n2, b = (double)j / n2, c = (double)k / n2;
+    for (int r = 0; r < 3; ++r) x[r] = g.X0[r] + g.Jm[3 * r] * a + g.Jm[3 * r + 1] * b + g.Jm[3 * r + 2] * c;
+    if (blend) {
+      const double rr = sqrt(x[0] * x[0] + x[1] * x[1] + x[2] * x[2]);
+      const double fct = g.cK * (g.nhat[0] * x[0] + g.nhat[1] * x[1] + g.nhat[2] * x[2]) / rr;
+      for (int r = 0; r < 3; ++r) x[r] *= fct;
+    }
+    int hint = mac;
+    bool ok = true;
+    auto vel = [&](const double (&p)[3], double th, double (&v)[3]) {
+      double y[3] = {p[0], p[1], p[2]};
+      clamp_r(y, blend, rmin, rmax);
+      Loc L;
+      if (!locate(mg, nm, n1, blend, y, hint, 1e-12, L) && !locate(mg, nm, n1, blend, y, hint, 1e-9, L)) {
+        ok = false;
+        v[0] = v[1] = v[2] = 0.0;
+        return;
+      }
+      hint = L.mac;
+      double ph[10];
+      int id[10];
+      p2_eval_setup(L, n1, ph, id);
+      const int64_t mb = (int64_t)L.mac * npts2;
+      for (int q = 0; q < 3; ++q) {
+        double sn = 0.0, so = 0.0;
+        for (int e = 0; e < 10; ++e) {
+          sn += ph[e] * un[q * cs + mb + id[e]];
+          so += ph[e] * uo[q * cs + mb + id[e]];
+        }
+        v[q] = (1.0 - th) * sn + th * so;
+      }
+    };
+    double k1[3], k2[3], k3[3], k4[3], p[3];
+    vel(x, 0.0, k1);
+    for (int q = 0; q < 3; ++q) p[q] = x[q] - 0.5 * tau * k1[q];
+    vel(p, 0.5, k2);
+    for (int q = 0; q < 3; ++q) p[q] = x[q] - 0.5 * tau * k2[q];
+    vel(p, 0.5, k3);
+    for (int q = 0; q < 3; ++q) p[q] = x[q] - tau * k3[q];
+    vel(p, 1.0, k4);
+    for (int q = 0; q < 3; ++q) p[q] = x[q] - tau / 6.0 * (k1[q] + 2.0 * k2[q] + 2.0 * k3[q] + k4[q]);
+    clamp_r(p, blend, rmin, rmax);
+    Loc L;
+    double val = 0.0;
+    if (locate(mg, nm, n1, blend, p, hint, 1e-12, L) || locate(mg, nm, n1, blend, p, hint, 1e-9, L)) {
+      double ph[10];
+      int id[10];
+      p2_eval_setup(L, n1, ph, id);
+      const int64_t mb = (int64_t)L.mac * npts2;
+      for (int e = 0; e < 10; ++e) val += ph[e] * T[mb + id[e]];
+    } else {
+      ok = false;
+    }
+    out[node] = val;
+    if (!ok) atomicOr(fail_flag, 1);
+  }
+}
+}  // namespace
+
+int launch_mmoc(const Mesh* m, const Level& L, double rmin, double rmax, double tau, const double* T, const double* un,
+                const double* uo, double* out, int* fail_flag, cudaStream_t s) {
+  static bool tinv_ready = false;
+  if (!tinv_ready) {
+    const int TV[6][4][3] = {
+        {{0, 0, 0}, {1, 0, 0}, {0, 1, 0}, {0, 0, 1}}, {{0, 1, 0}, {1, 0, 0}, {1, 0, 1}, {1, 1, 0}},
+        {{0, 0, 1}, {0, 1, 0}, {1, 0, 0}, {1, 0, 1}}, {{0, 1, 0}, {0, 1, 1}, {1, 0, 1}, {1, 1, 0}},
+        {{0, 0, 1}, {0, 1, 0}, {0, 1, 1}, {1, 0, 1}}, {{0, 1, 1}, {1, 0, 1}, {1, 1, 0}, {1, 1, 1}}};
+    double inv[6][9];
+    for (int t = 0; t < 6; ++t) {
+      double E[3][3];
+      for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) E[r][c] = TV[t][c + 1][r] - TV[t][0][r];
+      const double det = E[0][0] * (E[1][1] * E[2][2] - E[1][2] * E[2][1]) - E[0][1] * (E[1][0] * E[2][2] - E[1][2] * E[2][0]) +
+                         E[0][2] * (E[1][0] * E[2][1] - E[1][1] * E[2][0]);
+      inv[t][0] = (E[1][1] * E[2][2] - E[1][2] * E[2][1]) / det;
+      inv[t][1] = (E[0][2] * E[2][1] - E[0][1] * E[2][2]) / det;
+      inv[t][2] = (E[0][1] * E[1][2] - E[0][2] * E[1][1]) / det;
+      inv[t][3] = (E[1][2] * E[2][0] - E[1][0] * E[2][2]) / det;
+      inv[t][4] = (E[0][0] * E[2][2] - E[0][2] * E[2][0]) / det;
+      inv[t][5] = (E[0][2] * E[1][0] - E[0][0] * E[1][2]) / det;
+      inv[t][6] = (E[1][0] * E[2][1] - E[1][1] * E[2][0]) / det;
+      inv[t][7] = (E[0][1] * E[2][0] - E[0][0] * E[2][1]) / det;
+      inv[t][8] = (E[0][0] * E[1][1] - E[0][1] * E[1][0]) / det;
+    }
+    HHG_CUDA(cudaMemcpyToSymbol(kTinv, inv, sizeof(inv)));
+    tinv_ready = true;
+  }
+  HHG_TRY(ensure_device_geo(const_cast<Mesh*>(m)));
+  const int64_t nm = macro_count(m);
+  if (nm == 0) return HHG_OK;
+  dim3 grid((unsigned)((L.nrows2 + 7) / 8), (unsigned)nm);
+  k_mmoc<<<grid, 256, 0, s>>>(m->dgeo, (int)nm, L.rows2, L.nrows2, L.n1, L.npts2, L.own2, m->blend == HHG_BLEND_SHELL,
+                              rmin, rmax, tau, T, un, uo, out, fail_flag);
+  count_launch();
+  HHG_CUDA(cudaGetLastError());
+  return HHG_OK;
+}
+
 int launch_temp(const Mesh* m, const Level& L, int mode, TempCoef cf, const double* u, const double* T, double* y,
                 cudaStream_t s) {
   const int64_t nm = macro_count(m);

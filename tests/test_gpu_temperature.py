@@ -57,3 +57,26 @@ def test_temperature_solve_matches_direct_solve():
     T, it, rel = S.solve(u, b, T, tol=1e-12, max_iters=100)
     assert rel <= 1e-12 and it < 30, (it, rel)
     assert rel_l2(canon(M, L, hhg.HHG_P2, T), T_ref) <= 1e-9
+
+
+@pytest.mark.parametrize("L,scale", [(1, 0.3), (2, 0.3)])
+def test_mmoc_matches_oracle(L, scale):
+    """MMOC on the blended shell: seeded u_new, u_old (displacements ~ a micro-tet size),
+    seeded T; every P2 node against the oracle's RK4 back-tracking with brute-force point location."""
+    from oracle.mmoc import mmoc
+    lm, M, u_o, u = _case(L)
+    keys = M.canonical_keys(L, hhg.HHG_P2)
+    un_o = scale * uniform_vec(lm.p2_keys, 2)
+    uo_o = scale * uniform_vec(lm.p2_keys, 5)
+    T_o = uniform_from_keys(lm.p2_keys, 3, 0)
+    tau = 0.1
+    ref = mmoc(lm, True, T_o, un_o, uo_o, tau)
+    un = M.from_canonical(L, hhg.HHG_P2VEC, scale * uniform_vec(keys, 2))
+    uo = M.from_canonical(L, hhg.HHG_P2VEC, scale * uniform_vec(keys, 5))
+    T = M.from_canonical(L, hhg.HHG_P2, uniform_from_keys(keys, 3, 0))
+    Th = hhg.hhg_mmoc(M, L, T, un, uo, tau)
+    got = canon(M, L, hhg.HHG_P2, Th)
+    assert np.abs(got - ref).max() <= 1e-11 * np.abs(ref).max()
+    z = torch.zeros_like(un)
+    assert torch.equal(hhg.hhg_mmoc(M, L, T, z, z, tau), T) or \
+        float((hhg.hhg_mmoc(M, L, T, z, z, tau) - T).abs().max()) <= 1e-14
