@@ -24,10 +24,16 @@ for _ in range(10):
     hhg.hhg_temp_apply(M, L, PRM, u, T, y)
 e1.record(); torch.cuda.synchronize()
 apply_ms = e0.elapsed_time(e1) / 10
+uo = M.from_canonical(L, hhg.HHG_P2VEC, 100.0 * uniform_vec(keys, 5))
+Th = hhg.hhg_mmoc(M, L, T, u, uo, a.tau)
+torch.cuda.synchronize(); e0.record()
+hhg.hhg_mmoc(M, L, T, u, uo, a.tau, Th)
+e1.record(); torch.cuda.synchronize()
+mmoc_ms = e0.elapsed_time(e1)
 S = hhg.TempSolver(M, L, PRM, restart=50)
 torch.cuda.synchronize(); e0.record()
 T, it, rel = S.solve(u, b, T, tol=1e-10, max_iters=100, tol_cg=1e-12)
 e1.record(); torch.cuda.synchronize()
 print(json.dumps({"what": "temperature", "level": L, "p2_nodes": M.canonical_len(L, hhg.HHG_P2), "micro_tets": 240 * 8 ** L,
-                  "apply_ms": apply_ms, "solve_ms": e0.elapsed_time(e1), "fgmres_iters": it, "rel_res": rel, "prm": PRM,
+                  "apply_ms": apply_ms, "mmoc_ms": mmoc_ms, "solve_ms": e0.elapsed_time(e1), "fgmres_iters": it, "rel_res": rel, "prm": PRM,
                   "u": "100 x seeded uniform P2 velocity"}))
