@@ -394,7 +394,8 @@ int hhg_temp_solver_destroy(hhg_temp_solver* S);
  * u(y, th) = (1 - th) u_new(y) + th u_old(y) (linear in time between t^{n+1} and t^n); fields evaluated
  * at located points (inverse blending, macro, lattice cube, micro tet, P2 basis); points leaving the
  * shell are moved radially onto it.  T, T_hat: consistent P2 scalars; u_*: consistent P2VEC.
- * Synchronises; HHG_EINVAL if a point cannot be located (non-shell meshes: a point left the domain). */
+ * Synchronises; HHG_EINVAL if a point cannot be located (non-shell meshes: a point left the domain) or the
+ * mesh is partitioned over several ranks (particles would need the neighbours' macros). */
 int hhg_mmoc(const hhg_mesh* mesh, int level, const double* T, const double* u_new, const double* u_old, double tau,
              double* T_hat, hhg_stream_t stream);
 

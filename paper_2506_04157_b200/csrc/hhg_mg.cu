@@ -1426,6 +1426,8 @@ int hhg_mmoc(const hhg_mesh* mesh, int level, const double* T, const double* u_n
              double* T_hat, hhg_stream_t stream) {
   if (!mesh || !T || !u_new || !u_old || !T_hat) return fail(HHG_EINVAL, "hhg_mmoc: NULL argument");
   if (level < 0 || level > mesh->level_max) return fail(HHG_ELEVEL, "hhg_mmoc: bad level");
+  if (mesh->nranks > 1)  // particles may leave the rank's macros: would need a macro halo (not built)
+    return fail(HHG_EINVAL, "hhg_mmoc: single-rank meshes only");
   auto* m = const_cast<hhg_mesh*>(mesh);
   HHG_TRY(ensure_level(m, level));
   const Level& L = m->levels[level];
