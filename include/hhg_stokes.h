@@ -286,6 +286,12 @@ int hhg_ablock_cg(hhg_mg* mg, const double* rhs, double* x, double tol, int max_
                   double* rel_res, hhg_stream_t stream);
 /* Same with HOST (pinned or pageable) rhs / x: H2D copy, V-cycle, D2H copy on `stream`. */
 int vcycle_host(hhg_mg* mg, const double* rhs_host, double* x_host, hhg_stream_t stream);
+/* nsteps V-cycles on HOST buffers, pipelined: step k's H2D copy, V-cycle and D2H copy each run on their own
+ * stream so that the H2D of step k+1 and the D2H of step k-1 overlap V-cycle k (two device staging
+ * pairs, event-ordered reuse).  rhs_host[k] / x_host[k]: pinned host pointers (repeats allowed).
+ * Asynchronous: `stream` is complete once every x_host[k] is written. */
+int vcycle_host_batch(hhg_mg* mg, const double* const* rhs_host, double* const* x_host, int nsteps,
+                      hhg_stream_t stream);
 /* Kernel timing of the fine-level element kernel inside vcycle (CUDA events on the
  * launching stream; disables graph capture while on).  get: sum of ms and count. */
 int hhg_mg_profile(hhg_mg* mg, int enable);

@@ -46,6 +46,7 @@ EXPORTS = [
     "hhg_stokes_schur_apply", "hhg_kp1_apply", "hhg_kp1_diag", "hhg_vmass_apply", "hhg_vmass_diag",
     "p1_prolong", "p1_restrict", "hhg_kmg_create", "hhg_kmg_solve", "hhg_kmg_destroy",
     "hhg_temp_apply", "hhg_temp_solver_create", "hhg_temp_solve", "hhg_temp_solver_destroy", "hhg_mmoc",
+    "vcycle_host_batch",
 ]
 
 
@@ -100,6 +101,7 @@ def _load():
         "hhg_temp_apply": ([P, I, P, P, P, P, I, P], I), "hhg_temp_solver_create": ([P, I, P, I, P], I),
         "hhg_temp_solve": ([P, P, P, P, D, D, I, D, I, P, P, P], I), "hhg_temp_solver_destroy": ([P], I),
         "hhg_mmoc": ([P, I, P, P, P, D, P, P], I),
+        "vcycle_host_batch": ([P, P, P, I, P], I),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -577,6 +579,21 @@ class MG:
     def vcycle_host(self, rhs_host, x_host, stream=None):
         _chk(_lib.vcycle_host(self.handle, _ptr(rhs_host), _ptr(x_host), _stream(stream)))
         return x_host
+
+    def vcycle_host_batch(self, rhs_hosts, x_hosts, stream=None):
+        """One V-cycle per (rhs_hosts[k] -> x_hosts[k]) pair of pinned host tensors, with the copies of
+        neighbouring steps overlapped with the compute (asynchronous on `stream`)."""
+        k = len(rhs_hosts)
+        assert len(x_hosts) == k
+        n = self.mesh.vec_len(self.l_max, HHG_P2VEC)
+        for t in list(rhs_hosts) + list(x_hosts):
+            if not (t.is_pinned() and t.dtype.is_floating_point and t.numel() == n and t.is_contiguous()):
+                raise HHGError("vcycle_host_batch: need pinned contiguous float64 host tensors of the level's length")
+        self._batch_keep = (list(rhs_hosts), list(x_hosts))
+        rh = (ctypes.c_void_p * k)(*[t.data_ptr() for t in rhs_hosts])
+        xh = (ctypes.c_void_p * k)(*[t.data_ptr() for t in x_hosts])
+        _chk(_lib.vcycle_host_batch(self.handle, rh, xh, k, _stream(stream)))
+        return x_hosts
 
     def profile(self, enable=True):
         _chk(_lib.hhg_mg_profile(self.handle, 1 if enable else 0))

@@ -98,6 +98,13 @@ struct hhg_mg {
   double *cg_r = nullptr, *cg_z = nullptr, *cg_p = nullptr, *cg_q = nullptr, *cg_s = nullptr;
   cudaGraphExec_t cg_gexec = nullptr;
   cudaStream_t cg_stream = nullptr;
+  // vcycle_host_batch: double-buffered staging, copy streams, per-buffer graphs and events
+  double *st_in[2] = {nullptr, nullptr}, *st_out[2] = {nullptr, nullptr};
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  cudaEvent_t ev_in_ready[2] = {}, ev_in_free[2] = {}, ev_out_ready[2] = {}, ev_out_free[2] = {}, ev_start = nullptr,
+              ev_done = nullptr;
+  cudaGraphExec_t pipe_gexec[2] = {nullptr, nullptr};
+  cudaStream_t pipe_stream = nullptr;
   // HHG_PERSISTENT_COARSE=1: run the coarse PCG as one persistent kernel (k_coarse_pcg).  Off by
   // default: measured 27.7 vs 26.4 ms per V(3,3) at L5 -- 200 software grid barriers per solve
   // cost more than the ~300 launches they replace.
@@ -121,6 +128,17 @@ struct hhg_mg {
     for (double* p : {cg_r, cg_z, cg_p, cg_q, cg_s})
       if (p) cudaFree(p);
     if (cg_gexec) cudaGraphExecDestroy(cg_gexec);
+    for (int b = 0; b < 2; ++b) {
+      if (st_in[b]) cudaFree(st_in[b]);
+      if (st_out[b]) cudaFree(st_out[b]);
+      if (pipe_gexec[b]) cudaGraphExecDestroy(pipe_gexec[b]);
+      for (cudaEvent_t e : {ev_in_ready[b], ev_in_free[b], ev_out_ready[b], ev_out_free[b]})
+        if (e) cudaEventDestroy(e);
+    }
+    if (ev_start) cudaEventDestroy(ev_start);
+    if (ev_done) cudaEventDestroy(ev_done);
+    if (s_h2d) cudaStreamDestroy(s_h2d);
+    if (s_d2h) cudaStreamDestroy(s_d2h);
     for (auto e : ev) cudaEventDestroy(e);
   }
 };
@@ -490,6 +508,75 @@ int vcycle_host(hhg_mg* mg, const double* rhs_host, double* x_host, hhg_stream_t
   HHG_CUDA(cudaMemcpyAsync(mg->hbuf_rhs, rhs_host, n * sizeof(double), cudaMemcpyHostToDevice, s));
   HHG_TRY(vcycle(mg, mg->hbuf_rhs, mg->hbuf_x, stream));
   HHG_CUDA(cudaMemcpyAsync(x_host, mg->hbuf_x, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  return HHG_OK;
+}
+
+// nsteps V-cycles on host buffers with the copies hidden behind the compute: H2D of step k+1 (copy
+// stream) and D2H of step k-1 (second copy stream) overlap V-cycle k; two device staging pairs
+// alternate, each with its own captured graph; events order reuse of a buffer pair.
+int vcycle_host_batch(hhg_mg* mg, const double* const* rhs_host, double* const* x_host, int nsteps,
+                      hhg_stream_t stream) {
+  if (!mg || !rhs_host || !x_host || nsteps < 0) return fail(HHG_EINVAL, "vcycle_host_batch: bad argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t n = p2vec_len(mg->mesh, mg->prm.l_max);
+  const size_t nb = n * sizeof(double);
+  if (!mg->st_in[0]) {
+    for (int b = 0; b < 2; ++b) {
+      if (cudaMalloc(&mg->st_in[b], nb) != cudaSuccess || cudaMalloc(&mg->st_out[b], nb) != cudaSuccess)
+        return fail(HHG_ENOMEM, "vcycle_host_batch: staging");
+      for (cudaEvent_t* e : {&mg->ev_in_ready[b], &mg->ev_in_free[b], &mg->ev_out_ready[b], &mg->ev_out_free[b]})
+        HHG_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    }
+    HHG_CUDA(cudaEventCreateWithFlags(&mg->ev_start, cudaEventDisableTiming));
+    HHG_CUDA(cudaEventCreateWithFlags(&mg->ev_done, cudaEventDisableTiming));
+    HHG_CUDA(cudaStreamCreateWithFlags(&mg->s_h2d, cudaStreamNonBlocking));
+    HHG_CUDA(cudaStreamCreateWithFlags(&mg->s_d2h, cudaStreamNonBlocking));
+  }
+  for (int l = mg->prm.l_min + 1; l <= mg->prm.l_max; ++l)
+    if (!(mg->lv[l].lam > 0)) return fail(HHG_ENOTREADY, "vcycle_host_batch: no spectrum estimate");
+  const bool use_graph = mg->prm.use_graph && s != nullptr && !mg->prof;
+  if (use_graph && mg->pipe_stream != s) {
+    for (int b = 0; b < 2; ++b) {
+      if (mg->pipe_gexec[b]) cudaGraphExecDestroy(mg->pipe_gexec[b]);
+      mg->pipe_gexec[b] = nullptr;
+      cudaGraph_t g;
+      HHG_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+      int r = mg_cycle(mg, mg->prm.l_max, mg->st_in[b], mg->st_out[b], s);
+      cudaError_t ce = cudaStreamEndCapture(s, &g);
+      if (r != HHG_OK) return r;
+      if (ce != cudaSuccess) return fail(HHG_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+      HHG_CUDA(cudaGraphInstantiate(&mg->pipe_gexec[b], g, 0));
+      cudaGraphDestroy(g);
+    }
+    mg->pipe_stream = s;
+  }
+  if (nsteps == 0) return HHG_OK;
+  HHG_CUDA(cudaEventRecord(mg->ev_start, s));
+  HHG_CUDA(cudaStreamWaitEvent(mg->s_h2d, mg->ev_start, 0));
+  HHG_CUDA(cudaStreamWaitEvent(mg->s_d2h, mg->ev_start, 0));
+  auto h2d = [&](int k) -> int {
+    const int b = k & 1;
+    if (k >= 2) HHG_CUDA(cudaStreamWaitEvent(mg->s_h2d, mg->ev_in_free[b], 0));
+    HHG_CUDA(cudaMemcpyAsync(mg->st_in[b], rhs_host[k], nb, cudaMemcpyHostToDevice, mg->s_h2d));
+    HHG_CUDA(cudaEventRecord(mg->ev_in_ready[b], mg->s_h2d));
+    return HHG_OK;
+  };
+  HHG_TRY(h2d(0));
+  for (int k = 0; k < nsteps; ++k) {
+    const int b = k & 1;
+    HHG_CUDA(cudaStreamWaitEvent(s, mg->ev_in_ready[b], 0));
+    if (k >= 2) HHG_CUDA(cudaStreamWaitEvent(s, mg->ev_out_free[b], 0));
+    if (use_graph) HHG_CUDA(cudaGraphLaunch(mg->pipe_gexec[b], s));
+    else HHG_TRY(mg_cycle(mg, mg->prm.l_max, mg->st_in[b], mg->st_out[b], s));
+    HHG_CUDA(cudaEventRecord(mg->ev_in_free[b], s));
+    HHG_CUDA(cudaEventRecord(mg->ev_out_ready[b], s));
+    if (k + 1 < nsteps) HHG_TRY(h2d(k + 1));
+    HHG_CUDA(cudaStreamWaitEvent(mg->s_d2h, mg->ev_out_ready[b], 0));
+    HHG_CUDA(cudaMemcpyAsync(x_host[k], mg->st_out[b], nb, cudaMemcpyDeviceToHost, mg->s_d2h));
+    HHG_CUDA(cudaEventRecord(mg->ev_out_free[b], mg->s_d2h));
+  }
+  HHG_CUDA(cudaEventRecord(mg->ev_done, mg->s_d2h));
+  HHG_CUDA(cudaStreamWaitEvent(s, mg->ev_done, 0));
   return HHG_OK;
 }
 

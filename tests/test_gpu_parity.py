@@ -502,3 +502,19 @@ def test_maximum_size_level7_apply_properties():
     y2 = hhg.epsilon_apply(M, L, None, (2.0 * v).contiguous())
     assert torch.isfinite(y1).all()
     assert float((y2 - 2.0 * y1).norm()) <= 1e-12 * float(y2.norm())
+
+
+def test_vcycle_host_batch_matches_device_vcycle(ablock_case):
+    """The pipelined host-buffer path (H2D of step k+1 / D2H of step k-1 overlapping V-cycle k) returns,
+    for every step, the V-cycle of that step's rhs (tolerance: fp64 RED order on brick borders)."""
+    H, f_o, M, mg, etas = ablock_case
+    rhs = [lib_u(M, 3, seed) for seed in (4, 7, 8)]
+    ref = [mg.vcycle(r).cpu() for r in rhs]
+    rh = [r.cpu().pin_memory() for r in rhs]
+    xh = [torch.empty_like(rh[0]).pin_memory() for _ in rhs]
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        mg.vcycle_host_batch(rh + rh[:1], xh + [torch.empty_like(rh[0]).pin_memory()], stream=s)
+    s.synchronize()
+    for a, b in zip(xh, ref):
+        assert float((a - b).norm()) <= 1e-12 * float(b.norm())
