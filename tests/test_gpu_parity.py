@@ -518,3 +518,14 @@ def test_vcycle_host_batch_matches_device_vcycle(ablock_case):
     s.synchronize()
     for a, b in zip(xh, ref):
         assert float((a - b).norm()) <= 1e-12 * float(b.norm())
+
+
+def test_divT_apply_accumulate():
+    """divT_apply(accumulate=1): y_u += (M P_v) B^T p against the oracle on top of a consistent y_u."""
+    mac = icoshell(3, 2)
+    lm, d, _ = oracle_case(mac, 2, True, BC_SHELL, None, 0.0, build=("B",))
+    M = lib_mesh(mac, 2, True, BC_SHELL)
+    y0 = lib_u(M, 2, 4)
+    y = hhg.divT_apply(M, 2, lib_p(M, 2, 3), y0.clone(), accumulate=True)
+    ref = d.Pm @ uniform_vec(lm.p2_keys, 4) + d.apply_BT(uniform_from_keys(lm.p1_keys, 3, 0))
+    assert rel_l2(canon(M, 2, hhg.HHG_P2VEC, y), ref) <= TOL_APPLY
