@@ -138,7 +138,19 @@ def _dev(t, n=None, name="tensor"):
         raise HHGError(f"{name}: need a contiguous float64 CUDA tensor")
     if n is not None and t.numel() != n:
         raise HHGError(f"{name}: length {t.numel()} != expected {n}")
+    if t.numel() == 0:       # empty vector (a rank without macros): any valid device address, never read
+        return _empty_device_ptr()
     return t.data_ptr()
+
+
+_EMPTY = []
+
+
+def _empty_device_ptr():
+    import torch
+    if not _EMPTY:
+        _EMPTY.append(torch.zeros(1, dtype=torch.float64, device="cuda"))
+    return _EMPTY[0].data_ptr()
 
 
 def _stream(stream=None):

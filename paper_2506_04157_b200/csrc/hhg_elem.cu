@@ -1412,6 +1412,7 @@ static void elem_launch_surf(const Mesh* m, const Level& L, const double* eta, d
 
 int launch_elem_surf(const Mesh* m, const Level& L, int mode, const double* eta, double a, double r_outer,
                      const double* in, double* out, cudaStream_t s) {
+  if (macro_count(m) == 0) return HHG_OK;  // a rank without macros (empty partition)
   HHG_TRY(ensure_slots());
   const bool bl = m->blend == HHG_BLEND_SHELL;
   if (a != 1.0 && !bl) return fail(HHG_EINVAL, "w-BFBT surface scaling a != 1 needs a shell-blended mesh");
@@ -1453,6 +1454,7 @@ static void elem_launch_qeta(const Mesh* m, const Level& L, const double* T2, Et
 // P2 temperature T2 (NEXT-2 tier); full form only
 int launch_elem_qeta(const Mesh* m, const Level& L, int mode, const double* T2, double lnC, double jump, double r_jump,
                      const double* u, double* yu, cudaStream_t s) {
+  if (macro_count(m) == 0) return HHG_OK;  // a rank without macros (empty partition)
   HHG_TRY(ensure_slots());
   const EtaQ eq{lnC, jump, r_jump};
   const bool bl = m->blend == HHG_BLEND_SHELL;
@@ -1472,6 +1474,7 @@ int launch_elem_qeta(const Mesh* m, const Level& L, int mode, const double* T2, 
 
 int launch_elem(const Mesh* m, const Level& L, int mode, int form, const double* eta, double gamma,
                 const double* u, const double* p, double* yu, double* yp, cudaStream_t s) {
+  if (macro_count(m) == 0) return HHG_OK;  // a rank without macros (empty partition)
   HHG_TRY(ensure_slots());
   const bool bl = m->blend == HHG_BLEND_SHELL;
   const bool full = form == HHG_VISC_FULL;

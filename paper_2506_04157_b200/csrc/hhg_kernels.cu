@@ -477,6 +477,7 @@ __global__ void k_restrict(const int32_t* __restrict__ rowsc, int64_t nrowsc, in
 }
 
 int launch_prolong(const Mesh* m, const Level& Lc, const Level& Lf, const double* xc, double* xf, cudaStream_t s) {
+  if (macro_count(m) == 0) return HHG_OK;
   HHG_TRY(ensure_transfer_tabs());
   const int64_t nm = macro_count(m);
   dim3 grid((unsigned)((Lf.nrows2 + 7) / 8), (unsigned)nm);
@@ -487,6 +488,7 @@ int launch_prolong(const Mesh* m, const Level& Lc, const Level& Lf, const double
 }
 
 int launch_restrict(const Mesh* m, const Level& Lc, const Level& Lf, const double* rf, double* rc, cudaStream_t s) {
+  if (macro_count(m) == 0) return HHG_OK;
   HHG_TRY(ensure_transfer_tabs());
   const int64_t nm = macro_count(m);
   dim3 grid((unsigned)((Lc.nrows2 + 7) / 8), (unsigned)nm);
@@ -564,6 +566,7 @@ __global__ void k_p1_restrict(const int32_t* __restrict__ rowsc, int64_t nrowsc,
 }
 
 int launch_p1_prolong(const Mesh* m, const Level& Lc, const Level& Lf, const double* xc, double* xf, cudaStream_t s) {
+  if (macro_count(m) == 0) return HHG_OK;
   const int64_t nm = macro_count(m);
   dim3 grid((unsigned)((Lf.nrows1 + 7) / 8), (unsigned)nm);
   k_p1_prolong<<<grid, 256, 0, s>>>(Lf.rows1, Lf.nrows1, Lf.n1, Lf.npts1, Lc.npts1, xc, xf);
@@ -573,6 +576,7 @@ int launch_p1_prolong(const Mesh* m, const Level& Lc, const Level& Lf, const dou
 }
 
 int launch_p1_restrict(const Mesh* m, const Level& Lc, const Level& Lf, const double* rf, double* rc, cudaStream_t s) {
+  if (macro_count(m) == 0) return HHG_OK;
   const int64_t nm = macro_count(m);
   dim3 grid((unsigned)((Lc.nrows1 + 7) / 8), (unsigned)nm);
   k_p1_restrict<<<grid, 256, 0, s>>>(Lc.rows1, Lc.nrows1, Lc.n1, Lf.npts1, Lc.npts1, Lf.own1, rf, rc);
@@ -609,6 +613,7 @@ __global__ void k_coords(const MacroGeo* __restrict__ mgeo, const int32_t* __res
 }
 
 int launch_coords(const Mesh* m, const Level& L, int space, double* xyz, cudaStream_t s) {
+  if (macro_count(m) == 0) return HHG_OK;
   const int64_t nm = macro_count(m);
   const bool p1 = space == HHG_P1;
   const int64_t nrows = p1 ? L.nrows1 : L.nrows2;

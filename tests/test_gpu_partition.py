@@ -74,3 +74,29 @@ def test_partitioned_apply_matches_global(nparts, level):
         uu = P.from_canonical(level, hhg.HHG_P2VEC, u_c)
         tot += float(hhg.hhg_dot(P, level, hhg.HHG_P2VEC, uu, uu).item())
     assert abs(tot - ref) <= 1e-13 * abs(ref)
+
+
+def test_rank_without_macros_is_a_no_op():
+    """Degenerate partition: every macro on rank 0, rank 1 empty.  The empty rank's vectors have length 0,
+    its applies, interface sums and dots are no-ops (0 for the dot), it has no halo neighbours, and rank 0
+    alone reproduces the global operator."""
+    mac = icoshell(3, 2)
+    level = 2
+    tr = np.zeros(len(mac.tets), np.int32)
+    E = _part_mesh(mac, level, tr, 2, 1)
+    assert E.local_macros() == 0 and E.vec_len(level, hhg.HHG_P2VEC) == 0
+    u = E.zeros(level, hhg.HHG_P2VEC)
+    y = hhg.epsilon_apply_partial(E, level, E.zeros(level, hhg.HHG_P1), u)
+    assert y.numel() == 0
+    nb, cnt = E.halo_info(level, hhg.HHG_P2VEC)
+    assert len(nb) == 0
+    assert float(hhg.hhg_dot(E, level, hhg.HHG_P2VEC, u, u).item()) == 0.0
+    F = _part_mesh(mac, level, tr, 2, 0)
+    M = lib_mesh(mac, level, True, BC_SHELL)
+    eta = lib_eta(M, level, C2)
+    uu = lib_u(M, level, 2)
+    ref = M.to_canonical(level, hhg.HHG_P2VEC, hhg.epsilon_apply(M, level, eta, uu))
+    e = F.from_canonical(level, hhg.HHG_P1, M.to_canonical(level, hhg.HHG_P1, eta))
+    v = F.from_canonical(level, hhg.HHG_P2VEC, M.to_canonical(level, hhg.HHG_P2VEC, uu))
+    got = F.to_canonical(level, hhg.HHG_P2VEC, hhg.epsilon_apply(F, level, e, v))
+    assert rel_l2(got.cpu().numpy(), ref.cpu().numpy()) <= 1e-14
