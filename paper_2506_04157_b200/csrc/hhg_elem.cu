@@ -6,15 +6,17 @@
 // micro tets (Bey/Freudenthal refinement):
 //   type 0 up {000,100,010,001}, 1-4 octahedron around diagonal 010-101, 5 down {011,101,110,111};
 // a cube with anchor sum s has 6 tets if s <= n-3, 5 if s == n-2, 1 if s == n-1.
-//  * dense bricks (n - brick origin sum >= 5): one thread per cube, loop over its tets; outputs
-//    are accumulated in thread-private shared-memory slots (27 P2 nodes x 3 comps + 8 P1 corners
-//    of the cube; first touch stores, later touches add -- sm_100a has no native fp64 shared
-//    atomics), then each thread gathers the footprint nodes at doubled offsets {0,1}^3 of its cube
-//    (+ the brick's upper faces) from the <= 8 cubes containing them: plain store inside the brick
-//    footprint, one fp64 RED per footprint-border node.
+//  * k_elem_fp (v6): the brick's 9x9x9-point P2 footprint of u (and eta / p on the 5x5x5 P1
+//    footprint, and the macro's element geometry) is staged in shared memory with cp.async; one
+//    thread per cube loops over its tets, all lanes of a warp on the same type; element outputs are
+//    added into a per-warp output footprint in 4 conflict-free rounds (the 6 edge midpoints of a tet
+//    have pairwise different parity classes, the 4 vertices take one round each; sm_100a has no
+//    native fp64 shared atomics), then the CTA writes the footprint: plain stores inside, one fp64
+//    RED per footprint-border point (shared with neighbouring bricks).
 //  * sparse bricks (those cut by the macro's slanted face with <= 64 tets): one thread per tet,
 //    outputs go straight to global memory with fp64 REDs (the dense loop would run 6 iterations
 //    for 1 tet per thread on these bricks).
+//  History (v1 thread-per-tet, v2 private slots, v5 slot gather): DESIGN.md §6.
 //
 // Per tet (tet_body): gather 30 velocity dofs (+4 eta, +4 p), evaluate the blending map at the 4
 // quadrature points on the fly, and form 2 eta dev(eps(u)),
@@ -516,267 +518,6 @@ struct RegU {
   const double (&u)[10][3];
   __device__ __forceinline__ double operator()(int a, int c) const { return u[a][c]; }
 };
-
-template <int MODE>
-__device__ __forceinline__ void load_tet(int t, const int* rs2, const int* rs1, const double* __restrict__ um,
-                                         int64_t cstride, const double* __restrict__ em,
-                                         const double* __restrict__ pm, double (&uu)[10][3], double (&et)[4],
-                                         double (&pp)[4]) {
-  constexpr bool NEED_U = (MODE & (ELEM_A | ELEM_DIV)) != 0;
-  constexpr bool NEED_ETA = (MODE & (ELEM_A | ELEM_DIAG)) != 0;
-  constexpr bool NEED_P = (MODE & (ELEM_BT | ELEM_LOAD)) != 0;
-  if (NEED_U) {
-#pragma unroll
-    for (int a = 0; a < 10; ++a) {
-      const int pk = eLd[t][a];
-      const double* pa = um + rs2[(pk >> 2) * kBT] + (pk & 3);
-#pragma unroll
-      for (int c = 0; c < 3; ++c) uu[a][c] = __ldg(pa + c * cstride);
-    }
-  }
-#pragma unroll
-  for (int v = 0; v < 4; ++v) {
-    const int ps = ePSlot[t][v];
-    const int ix = rs1[(ps >> 1) * kBT] + (ps & 1);
-    et[v] = (NEED_ETA && em != nullptr) ? __ldg(em + ix) : 1.0;
-    pp[v] = NEED_P ? __ldg(pm + ix) : 0.0;
-  }
-}
-
-template <bool BLEND, int MODE, bool FULL>
-#ifndef HHG_ELEM_MINB
-#define HHG_ELEM_MINB 4
-#endif
-__global__ void __launch_bounds__(kBT, HHG_ELEM_MINB)
-    k_elem_brick(const MacroGeo* __restrict__ mgeo, const double* __restrict__ lgeo, const int32_t* __restrict__ bricks,
-                 int n1, double inv_n1, int64_t npts1, int64_t npts2, int64_t cstride, const double* __restrict__ eta,
-                 const double* __restrict__ u, const double* __restrict__ p, double* __restrict__ yu,
-                 double* __restrict__ yp, double gamma) {
-  constexpr bool DO_DIV = (MODE & ELEM_DIV) != 0;
-  constexpr bool HAS_U_OUT = elem_u_out(MODE);
-  constexpr int NSU = HAS_U_OUT ? kNS2 : 0;
-  constexpr int NS = NSU + (DO_DIV ? kNS1 : 0);
-  extern __shared__ double sm[];  // [NS][kBT] cube slots | geometry [kGeoSm] | row starts int[13][kBT]
-#ifdef HHG_GEO_GLOBAL
-  // per-macro geometry read through L1 (saves 1 KB of shared memory per CTA)
-  const double* sgeo = lgeo + (int64_t)blockIdx.y * kLevelGeo;
-  int* rs2 = reinterpret_cast<int*>(sm + NS * kBT) + threadIdx.x;  // [9][kBT]
-#else
-  double* sgeo = sm + NS * kBT;
-  int* rs2 = reinterpret_cast<int*>(sgeo + kGeoSm) + threadIdx.x;  // [9][kBT]
-#endif
-  int* rs1 = rs2 + 9 * kBT;                                         // [4][kBT]
-
-  const int mac = blockIdx.y;
-  const int32_t bpk = __ldg(bricks + blockIdx.x);
-  const int i0 = bpk & 1023, j0 = (bpk >> 10) & 1023, k0 = bpk >> 20;
-  const int delta = n1 - (i0 + j0 + k0);
-  const int tid = threadIdx.x;
-  const int n2 = 2 * n1;
-
-  const double* Gm = lgeo + (int64_t)mac * kLevelGeo;
-#ifndef HHG_GEO_GLOBAL
-  for (int r = tid; r < kGeoSm; r += kBT) sgeo[r] = __ldg(Gm + r);
-#else
-  (void)Gm;
-#endif
-  const MacroGeo& g = mgeo[mac];
-  double nh[3] = {0, 0, 0}, cK = 1.0;
-  if (BLEND) {
-    nh[0] = g.nhat[0];
-    nh[1] = g.nhat[1];
-    nh[2] = g.nhat[2];
-    cK = g.cK;
-  }
-  const double* um = u + (int64_t)mac * npts2;
-  const double* em = eta ? eta + (int64_t)mac * npts1 : nullptr;
-  const double* pm = p ? p + (int64_t)mac * npts1 : nullptr;
-  double* yum = yu + (int64_t)mac * npts2;
-  double* ypm = yp ? yp + (int64_t)mac * npts1 : nullptr;
-
-  auto cube_setup = [&](int ai, int aj, int ak, double (&xa)[3]) {
-    const double fa = ai * inv_n1, fb = aj * inv_n1, fc = ak * inv_n1;  // exact: n1 = 2^L
-#pragma unroll
-    for (int r = 0; r < 3; ++r) xa[r] = g.X0[r] + g.Jm[3 * r] * fa + g.Jm[3 * r + 1] * fb + g.Jm[3 * r + 2] * fc;
-#pragma unroll
-    for (int c = 0; c < 3; ++c)
-#pragma unroll
-      for (int b = 0; b < 3; ++b) rs2[(b + 3 * c) * kBT] = rowstart32(n2, 2 * aj + b, 2 * ak + c) + 2 * ai;
-#pragma unroll
-    for (int c = 0; c < 2; ++c)
-#pragma unroll
-      for (int b = 0; b < 2; ++b) rs1[(b + 2 * c) * kBT] = rowstart32(n1, aj + b, ak + c) + ai;
-  };
-  __syncthreads();
-  const double wdet = EWQ * sgeo[6 * kTypeGeo];
-
-  if (delta <= 4) {
-    // ---------------- sparse brick (<= 64 tets): one tet per thread, fp64 REDs to global memory
-    if (tid >= eNItems[delta]) return;
-    const int item = eItems[delta][tid];
-    const int cube = item & 63, t = item >> 6;
-    const int ai = i0 + (cube & 3), aj = j0 + ((cube >> 2) & 3), ak = k0 + (cube >> 4);
-    double xa[3];
-    cube_setup(ai, aj, ak, xa);
-    double uu[10][3], et[4], pp[4], acc[10][3], gy[4];
-    load_tet<MODE>(t, rs2, rs1, um, cstride, em, pm, uu, et, pp);
-    tet_body<BLEND, MODE, FULL>(sgeo + t * kTypeGeo, wdet, xa, nh, cK, gamma, RegU{uu}, et, pp, acc, gy);
-    if (HAS_U_OUT) {
-#pragma unroll
-      for (int a = 0; a < 10; ++a) {
-        const int pk = eLd[t][a];
-        double* pa = yum + rs2[(pk >> 2) * kBT] + (pk & 3);
-#pragma unroll
-        for (int c = 0; c < 3; ++c) atomicAdd(pa + c * cstride, acc[a][c]);
-      }
-    }
-    if (DO_DIV) {
-#pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        const int ps = ePSlot[t][v];
-        atomicAdd(ypm + rs1[(ps >> 1) * kBT] + (ps & 1), gy[v]);
-      }
-    }
-    return;
-  }
-
-  // ---------------- dense brick: one thread per cube, private shared-memory slots
-  const int ti = tid & 3, tj = (tid >> 2) & 3, tk = tid >> 4;
-  const int ai = i0 + ti, aj = j0 + tj, ak = k0 + tk;
-  const int s = ai + aj + ak;
-  const int ntypes = (s <= n1 - 3) ? 6 : ((s == n1 - 2) ? 5 : ((s == n1 - 1) ? 1 : 0));
-  if (ntypes < 6) {  // partial cube: the slots its tets never touch must read as zero in the gather
-#pragma unroll 1
-    for (int sl = 0; sl < NS; ++sl) sm[sl * kBT + tid] = 0.0;
-  }
-  if (ntypes > 0) {
-    double xa[3];
-    cube_setup(ai, aj, ak, xa);
-#pragma unroll 1
-    for (int t = 0; t < ntypes; ++t) {
-      double uu[10][3], et[4], pp[4], acc[10][3], gy[4];
-      load_tet<MODE>(t, rs2, rs1, um, cstride, em, pm, uu, et, pp);
-      tet_body<BLEND, MODE, FULL>(sgeo + t * kTypeGeo, wdet, xa, nh, cK, gamma, RegU{uu}, et, pp, acc, gy);
-      if (HAS_U_OUT) {
-        const int first = eFirst[t];
-#pragma unroll
-        for (int a = 0; a < 10; ++a) {
-          double* sl = sm + 3 * eSlot[t][a] * kBT + tid;
-          if ((first >> a) & 1) {
-#pragma unroll
-            for (int c = 0; c < 3; ++c) sl[c * kBT] = acc[a][c];
-          } else {
-#pragma unroll
-            for (int c = 0; c < 3; ++c) sl[c * kBT] += acc[a][c];
-          }
-        }
-      }
-      if (DO_DIV) {
-        const int first = ePFirst[t];
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          double* sl = sm + (NSU + ePSlot[t][v]) * kBT + tid;
-          if ((first >> v) & 1) *sl = gy[v];
-          else *sl += gy[v];
-        }
-      }
-    }
-  }
-  __syncthreads();
-
-  // gather.  Footprint point P = 2p + o (per dimension) of "position" p in [0,4]: round 0 takes the
-  // 64 positions p in [0,3]^3 (p = the thread's cube), round 1 the 61 positions on the upper faces
-  // (some p_d = 4; only o_d = 0 there).  Per dimension the point lies in cube p (slot o, if p <= 3)
-  // and, when o = 0, in cube p-1 (slot 2, if p >= 1).  Footprint-border points (P_d in {0, 8})
-  // are shared with other bricks: fp64 RED; all others get a plain store.
-#pragma unroll 1
-  for (int round = 0; round < 2; ++round) {
-    int px = ti, py = tj, pz = tk;
-    if (round == 1) {
-      if (tid >= 61) break;
-      if (tid < 48) {  // faces
-        const int f = tid >> 4, a = tid & 3, b = (tid >> 2) & 3;
-        px = f == 0 ? 4 : a;
-        py = f == 1 ? 4 : (f == 0 ? a : b);
-        pz = f == 2 ? 4 : b;
-      } else if (tid < 60) {  // edges
-        const int e = (tid - 48) >> 2, c = (tid - 48) & 3;
-        px = e == 2 ? c : 4;
-        py = e == 1 ? c : 4;
-        pz = e == 0 ? c : 4;
-      } else {
-        px = py = pz = 4;
-      }
-    }
-    if (HAS_U_OUT) {
-#pragma unroll
-      for (int oz = 0; oz < 2; ++oz) {
-#pragma unroll
-        for (int oy = 0; oy < 2; ++oy) {
-#pragma unroll
-          for (int ox = 0; ox < 2; ++ox) {
-            if ((ox && px == 4) || (oy && py == 4) || (oz && pz == 4)) continue;
-            const int gx = 2 * (i0 + px) + ox, gy_ = 2 * (j0 + py) + oy, gz = 2 * (k0 + pz) + oz;
-            if (gx + gy_ + gz > n2) continue;
-            double v[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-            for (int cz = 0; cz < 2; ++cz) {
-              if (cz && oz) continue;
-#pragma unroll
-              for (int cy = 0; cy < 2; ++cy) {
-                if (cy && oy) continue;
-#pragma unroll
-                for (int cx = 0; cx < 2; ++cx) {
-                  if (cx && ox) continue;
-                  const int qx = px - cx, qy = py - cy, qz = pz - cz;
-                  if (qx < 0 || qx > 3 || qy < 0 || qy > 3 || qz < 0 || qz > 3) continue;
-                  const int sl = (cx ? 2 : ox) + 3 * (cy ? 2 : oy) + 9 * (cz ? 2 : oz);
-                  const double* sp = sm + 3 * sl * kBT + qx + 4 * qy + 16 * qz;
-#pragma unroll
-                  for (int c = 0; c < 3; ++c) v[c] += sp[c * kBT];
-                }
-              }
-            }
-            double* dst = yum + rowstart32(n2, gy_, gz) + gx;
-            const bool border = (px == 0 && ox == 0) || (py == 0 && oy == 0) || (pz == 0 && oz == 0) || px == 4 ||
-                                py == 4 || pz == 4;
-            if (border) {
-#pragma unroll
-              for (int c = 0; c < 3; ++c)
-                if (v[c] != 0.0) atomicAdd(dst + c * cstride, v[c]);
-            } else {
-#pragma unroll
-              for (int c = 0; c < 3; ++c) dst[c * cstride] = v[c];
-            }
-          }
-        }
-      }
-    }
-    if (DO_DIV) {
-      const int gx = i0 + px, gy_ = j0 + py, gz = k0 + pz;
-      if (gx + gy_ + gz <= n1) {
-        double v = 0.0;
-#pragma unroll
-        for (int cz = 0; cz < 2; ++cz)
-#pragma unroll
-          for (int cy = 0; cy < 2; ++cy)
-#pragma unroll
-            for (int cx = 0; cx < 2; ++cx) {
-              const int qx = px - cx, qy = py - cy, qz = pz - cz;
-              if (qx < 0 || qx > 3 || qy < 0 || qy > 3 || qz < 0 || qz > 3) continue;
-              v += sm[(NSU + cx + 2 * cy + 4 * cz) * kBT + qx + 4 * qy + 16 * qz];
-            }
-        double* dst = ypm + rowstart32(n1, gy_, gz) + gx;
-        const bool border = px == 0 || py == 0 || pz == 0 || px == 4 || py == 4 || pz == 4;
-        if (border) {
-          if (v != 0.0) atomicAdd(dst, v);
-        } else {
-          *dst = v;
-        }
-      }
-    }
-  }
-}
 
 // ================================================================ element kernel v6 ("footprint")
 // The brick's u footprint (9x9x9 doubled-lattice points x 3 comps) and P1 footprint (eta, p) are
@@ -1354,41 +1095,17 @@ template <bool BLEND, int MODE, bool FULL>
 static void elem_launch(const Mesh* m, const Level& L, const double* eta, double gamma, const double* u,
                         const double* p, double* yu, double* yp, cudaStream_t s) {
   const int64_t nm = macro_count(m);
-#ifdef HHG_ELEM_V5
-  if (MODE & (ELEM_MASS | ELEM_MASSD | ELEM_LOAD | ELEM_SURF))
-#endif
-  {
-    constexpr size_t smem = fp_smem_words<MODE>() * sizeof(double);
-    dim3 grid((unsigned)L.n_bricks, (unsigned)nm);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_elem_fp<BLEND, MODE, FULL>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                           (int)cudaSharedmemCarveoutMaxShared);
-      cudaFuncSetAttribute(k_elem_fp<BLEND, MODE, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr = true;
-    }
-    k_elem_fp<BLEND, MODE, FULL><<<grid, kBT, smem, s>>>(m->dgeo, L.geo, L.bricks, L.n1, 1.0 / L.n1, L.npts1,
-                                                         L.npts2, nm * L.npts2, eta, u, p, yu, yp, gamma);
-    return;
-  }
-#ifdef HHG_ELEM_V5
-  constexpr int NS = (elem_u_out(MODE) ? kNS2 : 0) + ((MODE & ELEM_DIV) ? kNS1 : 0);
-#ifdef HHG_GEO_GLOBAL
-  constexpr size_t smem = (NS * kBT) * sizeof(double) + 13 * kBT * sizeof(int);
-#else
-  constexpr size_t smem = (NS * kBT + kGeoSm) * sizeof(double) + 13 * kBT * sizeof(int);
-#endif
+  constexpr size_t smem = fp_smem_words<MODE>() * sizeof(double);
   dim3 grid((unsigned)L.n_bricks, (unsigned)nm);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_elem_brick<BLEND, MODE, FULL>, cudaFuncAttributePreferredSharedMemoryCarveout,
+    cudaFuncSetAttribute(k_elem_fp<BLEND, MODE, FULL>, cudaFuncAttributePreferredSharedMemoryCarveout,
                          (int)cudaSharedmemCarveoutMaxShared);
-    cudaFuncSetAttribute(k_elem_brick<BLEND, MODE, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_elem_fp<BLEND, MODE, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  k_elem_brick<BLEND, MODE, FULL><<<grid, kBT, smem, s>>>(m->dgeo, L.geo, L.bricks, L.n1, 1.0 / L.n1, L.npts1,
-                                                          L.npts2, nm * L.npts2, eta, u, p, yu, yp, gamma);
-#endif
+  k_elem_fp<BLEND, MODE, FULL><<<grid, kBT, smem, s>>>(m->dgeo, L.geo, L.bricks, L.n1, 1.0 / L.n1, L.npts1, L.npts2,
+                                                       nm * L.npts2, eta, u, p, yu, yp, gamma);
 }
 
 // w-BFBT operators: same brick kernel, a in the gamma slot, the outer radius in eq.r_jump
