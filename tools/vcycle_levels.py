@@ -30,7 +30,9 @@ for L in a.levels:
                 v0[l] = torch.rand(M.vec_len(l, hhg.HHG_P2VEC), dtype=torch.float64, device="cuda", generator=g)
                 M.interface_sum(l, hhg.HHG_P2VEC, v0[l])
         mg = hhg.MG(M, 1, L, etas, v0, pre=3, post=3, degree=3, power_iters=20, coarse_iters=50)
+        mg._v0 = {}                 # the start vectors are only needed by the power iterations in create
         del v0
+        torch.cuda.empty_cache()
         rhs = torch.rand(M.vec_len(L, hhg.HHG_P2VEC), dtype=torch.float64, device="cuda", generator=g)
         M.interface_sum(L, hhg.HHG_P2VEC, rhs)
         rhs = M.apply_bc(L, rhs)
