@@ -16,7 +16,14 @@ from the paper (arxiv 2506.04157, /root/reference/PAPER.md, cited "P:<line>"):
                     free-slip projection P_v; diag(A) without P_v
   * multigrid.py -- P2 nodal-interpolation prolongation and its transpose,
                     Chebyshev smoother, power iteration, Jacobi-PCG coarse solve
-                    and the V-cycle of fig:ASolverStructure
+                    and the V-cycle of fig:ASolverStructure; P1 linear
+                    prolongation (w-BFBT K multigrid); the A-block CG
+  * stokes.py    -- FGMRES + Uzawa block preconditioners with the mass,
+                    V-cycle BFBT and weighted BFBT Schur approximations
+  * temperature.py -- the eq:WeakTemp operator, its symmetric part and the
+                    Dirichlet solve
+  * mmoc.py      -- RK4 particle back-tracking with brute-force point location
+                    (P:500-512)
 
 Every function cites the passage it follows.  Readings of silent/garbled
 passages are listed in DESIGN.md ("Readings").  All floating point is fp64.
