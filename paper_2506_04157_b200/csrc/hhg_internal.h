@@ -205,7 +205,6 @@ int launch_chebk_last_bc(const Mesh* m, const Level& L, const double* t, const d
 int launch_cheb_deg1_bc(const Mesh* m, const Level& L, const double* f, const double* t, const double* dinv,
                         double inv_theta, double* x, cudaStream_t s);
 // PCG with ping-pong r.z scalars: scal[0]/scal[2] alternate by iteration parity, scal[1] = p.q
-// (also writes the new r.z over owned nodes into the other ping-pong slot, all-reduced over ranks)
 int launch_pcg_update_bc(const Mesh* m, const Level& L, int it, const double* scal, double* x, double* r,
                          const double* p, const double* q, const double* dinv, double* z, cudaStream_t s);
 int launch_pcg_dir_zero(int64_t n, int it, const double* scal, const double* z, double* p, double* q_zero,

@@ -827,63 +827,25 @@ __global__ void k_chebk_last_bc(int64_t ns, int64_t cs, const double* __restrict
     for (int c = 0; c < 3; ++c) x[i + c * cs] += dold[c] + dn[c];
   }
 }
-// ... and, fused (rz_out != nullptr), the new r.z over owned nodes: block partials + last-block
-// fixed-order finalisation (as k_dot_fused; grid <= kRedBlocks)
 __global__ void k_pcg_update_bc(int64_t ns, int64_t cs, const double* __restrict__ rzp, const double* __restrict__ pqp,
                                 double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
                                 const double* __restrict__ q, const double* __restrict__ dinv, double* __restrict__ z,
-                                const int32_t* __restrict__ bcn, const double* __restrict__ nrm,
-                                const uint8_t* __restrict__ own, double* __restrict__ part,
-                                unsigned* __restrict__ counter, double* __restrict__ rz_out) {
+                                const int32_t* __restrict__ bcn, const double* __restrict__ nrm) {
   const double rz = *rzp, pq = *pqp;
   const double alpha = (rz > 1e-300 && pq != 0.0) ? rz / pq : 0.0;
-  double acc = 0.0;
   GRID_STRIDE(i, ns) {
-    double zv[3], rv[3];
+    double zv[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       const int64_t j = i + c * cs;
       x[j] += alpha * p[j];
       const double ri = r[j] - alpha * q[j];
       r[j] = ri;
-      rv[c] = ri;
       zv[c] = dinv[j] * ri;
     }
     bc_project(bcn[i], nrm, zv[0], zv[1], zv[2]);
 #pragma unroll
     for (int c = 0; c < 3; ++c) z[i + c * cs] = zv[c];
-    if (rz_out && own[i]) acc += rv[0] * zv[0] + rv[1] * zv[1] + rv[2] * zv[2];
-  }
-  if (!rz_out) return;
-  __shared__ double sh[32];
-  __shared__ bool last;
-  acc = warp_sum(acc);
-  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    double v = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
-    v = warp_sum(v);
-    if (threadIdx.x == 0) {
-      part[blockIdx.x] = v;
-      __threadfence();
-      last = atomicAdd(counter, 1u) == gridDim.x - 1;
-    }
-  }
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  double t = 0.0;
-  for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) t += ((volatile double*)part)[i];
-  t = warp_sum(t);
-  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = t;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    double v = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
-    v = warp_sum(v);
-    if (threadIdx.x == 0) {
-      *rz_out = v;
-      *counter = 0u;
-    }
   }
 }
 // p = z + beta p, beta = rz_new / rz_old (0 once converged to the zero-rhs guard); q = 0 for the
@@ -938,17 +900,10 @@ int launch_chebk_last_bc(const Mesh* m, const Level& L, const double* t, const d
 int launch_pcg_update_bc(const Mesh* m, const Level& L, int it, const double* scal, double* x, double* r,
                          const double* p, const double* q, const double* dinv, double* z, cudaStream_t s) {
   const int64_t ns = macro_count(m) * L.npts2;
-  // fused new r.z into the other ping-pong slot (the coarse PCG's dot, one launch fewer per iteration)
-  unsigned nb = ngrid(ns);
-  nb = nb > (unsigned)kRedBlocks ? (unsigned)kRedBlocks : nb;
-  k_pcg_update_bc<<<nb, 256, 0, s>>>(NODE_ARGS(m, L), scal + ((it & 1) ? 2 : 0), scal + 1, x, r, p, q, dinv, z,
-                                     L.bcn2, L.g2.normal, L.own2, L.red,
-                                     reinterpret_cast<unsigned*>(L.red + kRedBlocks + 4),
-                                     const_cast<double*>(scal) + ((it & 1) ? 0 : 2));
+  k_pcg_update_bc<<<ngrid(ns), 256, 0, s>>>(NODE_ARGS(m, L), scal + ((it & 1) ? 2 : 0), scal + 1, x, r, p, q, dinv,
+                                            z, L.bcn2, L.g2.normal);
   count_launch();
   HHG_CUDA(cudaGetLastError());
-  if (m->comm && m->nranks > 1)
-    HHG_TRY(comm_allreduce_sum(m->comm, const_cast<double*>(scal) + ((it & 1) ? 0 : 2), 1, s));
   return HHG_OK;
 }
 int launch_pcg_dir_zero(int64_t n, int it, const double* scal, const double* z, double* p, double* q_zero,

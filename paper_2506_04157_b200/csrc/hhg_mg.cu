@@ -221,7 +221,8 @@ static int mg_pcg(hhg_mg* mg, int l, const double* f, double* x, cudaStream_t s)
   for (int it = 0; it < mg->prm.coarse_iters; ++it) {
     HHG_TRY(mg_apply(mg, l, p, q, s, true));
     HHG_TRY(launch_dot_fused(m, LL, HHG_P2VEC, p, q, mg->scal + 1, s));
-    HHG_TRY(launch_pcg_update_bc(m, LL, it, mg->scal, x, r, p, q, L.dinv, z, s));  // + the new r.z
+    HHG_TRY(launch_pcg_update_bc(m, LL, it, mg->scal, x, r, p, q, L.dinv, z, s));
+    HHG_TRY(launch_dot_fused(m, LL, HHG_P2VEC, r, z, mg->scal + ((it & 1) ? 0 : 2), s));
     HHG_TRY(launch_pcg_dir_zero(n, it, mg->scal, z, p, q, s));
   }
   return HHG_OK;
