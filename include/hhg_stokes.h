@@ -16,9 +16,18 @@
  *    hhg_last_error() returns a thread-local message for the last failure.
  *  - Handles (hhg_mesh, hhg_mg, hhg_comm) are opaque and library-owned.
  *  - VECTORS are caller-owned DEVICE pointers to contiguous fp64 arrays in the
- *    LIBRARY LAYOUT (below); their length comes from hhg_vec_len().  The library
- *    never allocates in hot calls except lazily-built per-level tables on the
- *    FIRST use of a (mesh, level) after hhg_mesh_create / blend_map / hhg_set_bc.
+ *    LIBRARY LAYOUT (below); their length comes from hhg_vec_len().  Per-level
+ *    tables are built on the FIRST use of a (mesh, level) after hhg_mesh_create /
+ *    blend_map / hhg_set_bc, or eagerly by hhg_mesh_prepare(); that build ends with a
+ *    device synchronisation (so a following call on any stream, blocking or not, sees
+ *    it) and must not happen under stream capture: call hhg_mesh_prepare() (or create
+ *    the solver object, which builds its levels) before capturing.  Solver objects
+ *    (hhg_mg, hhg_kmg, hhg_stokes, hhg_temp_solver) allocate all their workspace,
+ *    including their own reduction scratch, in *_create; hot calls never allocate.
+ *  - One solver object is used by one stream at a time; different objects on the same
+ *    mesh may run concurrently on different streams (they share no scratch).
+ *    hhg_dot uses the level's scratch: concurrent hhg_dot calls on one (mesh, level)
+ *    must be ordered by the caller.
  *  - Hot calls are asynchronous on the caller's cudaStream_t (pass NULL for the
  *    legacy default stream).  Calls that return host scalars synchronise and say so.
  *  - Outputs must not alias inputs unless stated.
@@ -152,8 +161,23 @@ int hhg_interface_sum_remote(const hhg_mesh* mesh, int level, int space, const d
 int blend_map(hhg_mesh* mesh, int kind);
 
 /* hhg_set_bc: boundary faces = macro faces of exactly one macro tet; a face's tag
- * is the common tag of its 3 vertices.  tag = HHG_BND_ALL sets every boundary face. */
+ * is the common tag of its 3 vertices.  tag = HHG_BND_ALL sets every boundary face.
+ * blend_map / hhg_set_bc / hhg_set_deterministic invalidate the per-level tables and
+ * return HHG_EINVAL while solver objects built on the mesh are alive (their diagonals,
+ * spectrum estimates and captured CUDA graphs depend on the old tables). */
 int hhg_set_bc(hhg_mesh* mesh, int tag, int kind);
+
+/* hhg_set_deterministic (on != 0): every element kernel (A, diag, B, B^T, C, mass, load,
+ * w-BFBT operators) runs as 8 launches, one per brick colour (bricks of one colour share
+ * no lattice point), accumulating brick borders with plain load-add-store instead of fp64
+ * atomics, so applies, dots, V-cycles and solves are bitwise reproducible run to run.
+ * Off by default (the atomic single-launch path is faster).  The temperature operator
+ * (hhg_temp_apply) keeps its atomics.  Errors: HHG_EINVAL with live solver objects. */
+int hhg_set_deterministic(hhg_mesh* mesh, int on);
+
+/* hhg_mesh_prepare: build the per-level tables of every level 0..level_max now (host work
+ * + uploads + one device synchronisation), so that no later call builds them lazily. */
+int hhg_mesh_prepare(hhg_mesh* mesh);
 
 /* Length (doubles) of a vector of `space` at `level` in the library layout. */
 int hhg_vec_len(const hhg_mesh* mesh, int level, int space, int64_t* n);

@@ -165,7 +165,7 @@ class Discretisation:
         n2, n1 = lm.n_p2, lm.n_p1
         eta_p1 = np.ones(n1) if eta_p1 is None else np.asarray(eta_p1, dtype=np.float64)
         self.eta_p1 = eta_p1
-        mats = {k: None for k in build}
+        mats = {k: [] for k in build}
         dsurf = surface_tets(lm) if ("K" in build or "VM" in build) else None
         for s in range(0, lm.n_tets, chunk):
             tets = np.arange(s, min(s + chunk, lm.n_tets))
@@ -183,29 +183,30 @@ class Discretisation:
                     eta_q = eta_p1[pd] @ fe.p1_basis(xi).T   # (T,Q) P1 interpolation
                 Ae = element_A(W, grads, eta_q, form)
                 M = _coo(Ae, vd, vd, 3 * n2, 3 * n2)
-                mats["A"] = M if mats["A"] is None else mats["A"] + M
+                mats["A"].append(M)
             if "B" in build:
                 Be = element_B(W, grads)
                 M = _coo(Be, pd, vd, n1, 3 * n2)
-                mats["B"] = M if mats["B"] is None else mats["B"] + M
+                mats["B"].append(M)
             if "C" in build:
                 Ce = element_C(W, xq, gamma) if gamma != 0.0 else np.zeros((len(tets), 4, 30))
                 M = _coo(Ce, pd, vd, n1, 3 * n2)
-                mats["C"] = M if mats["C"] is None else mats["C"] + M
+                mats["C"].append(M)
             if "M" in build:
                 xi, _ = fe.q4_rule()
                 eta_q = eta_p1[pd] @ fe.p1_basis(xi).T
                 M = _coo(element_M(W, eta_q), pd, pd, n1, n1)
-                mats["M"] = M if mats["M"] is None else mats["M"] + M
+                mats["M"].append(M)
             if "K" in build or "VM" in build:
                 xi, _ = fe.q4_rule()
                 eta_a = (eta_p1[pd] @ fe.p1_basis(xi).T) * np.where(dsurf[tets], surf_a ** 2, 1.0)[:, None]
                 if "K" in build:
                     M = _coo(element_K(W, g1, 1.0 / np.sqrt(eta_a)), pd, pd, n1, n1)
-                    mats["K"] = M if mats["K"] is None else mats["K"] + M
+                    mats["K"].append(M)
                 if "VM" in build:
                     M = _coo(element_VM(W, np.sqrt(eta_a)), vd, vd, 3 * n2, 3 * n2)
-                    mats["VM"] = M if mats["VM"] is None else mats["VM"] + M
+                    mats["VM"].append(M)
+        mats = {k: _tree_sum(v) for k, v in mats.items()}
         self.A = mats.get("A")
         self.B = mats.get("B")
         self.C = mats.get("C")
@@ -307,6 +308,16 @@ def sampled_rows(lm: LevelMesh, blended, eta_p1, gamma, u, p, nodes_p2, nodes_p1
         np.add.at(yp, pd, np.einsum("tpj,tj->tp", Be + Ce, ue))
     Pm = constraint_matrix(lm.p2_xt, bc)
     return Pm @ yu, yp
+
+
+def _tree_sum(parts):
+    """Sum of the per-chunk assembled matrices, pairwise (the entries are those of the element-by-element
+    definition; only the order in which duplicate entries are added differs from a running sum)."""
+    if not parts:
+        return None
+    while len(parts) > 1:
+        parts = [parts[i] + parts[i + 1] if i + 1 < len(parts) else parts[i] for i in range(0, len(parts), 2)]
+    return parts[0]
 
 
 def _coo(E, rows, cols, nr, nc):

@@ -46,7 +46,7 @@ EXPORTS = [
     "hhg_stokes_schur_apply", "hhg_kp1_apply", "hhg_kp1_diag", "hhg_vmass_apply", "hhg_vmass_diag",
     "p1_prolong", "p1_restrict", "hhg_kmg_create", "hhg_kmg_solve", "hhg_kmg_destroy",
     "hhg_temp_apply", "hhg_temp_solver_create", "hhg_temp_solve", "hhg_temp_solver_destroy", "hhg_mmoc",
-    "vcycle_host_batch",
+    "vcycle_host_batch", "hhg_set_deterministic", "hhg_mesh_prepare",
 ]
 
 
@@ -102,6 +102,7 @@ def _load():
         "hhg_temp_solve": ([P, P, P, P, D, D, I, D, I, P, P, P], I), "hhg_temp_solver_destroy": ([P], I),
         "hhg_mmoc": ([P, I, P, P, P, D, P, P], I),
         "vcycle_host_batch": ([P, P, P, I, P], I),
+        "hhg_set_deterministic": ([P, I], I), "hhg_mesh_prepare": ([P], I),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -154,8 +155,15 @@ def _empty_device_ptr():
 
 
 def _stream(stream=None):
+    """The CUDA stream a call runs on (default: torch's current stream).  When it is not the default
+    stream, it first waits for the default stream, where tensors made outside a `torch.cuda.stream`
+    block are produced (torch's side streams are non-blocking: without the wait a call could read an
+    input that is still being written)."""
     import torch
     s = torch.cuda.current_stream() if stream is None else stream
+    d = torch.cuda.default_stream(s.device)
+    if s != d:
+        s.wait_stream(d)
     return ctypes.c_void_p(s.cuda_stream)
 
 
@@ -290,6 +298,17 @@ class Mesh:
         if getattr(self, "handle", None) and _lib is not None:
             _lib.hhg_mesh_destroy(self.handle)
             self.handle = None
+
+    def set_deterministic(self, on=True):
+        """hhg_set_deterministic: colour-ordered element kernels without fp64 atomics (bitwise
+        reproducible results; slower)."""
+        _chk(_lib.hhg_set_deterministic(self.handle, 1 if on else 0))
+        return self
+
+    def prepare(self):
+        """hhg_mesh_prepare: build every level's tables now (never lazily in a later call)."""
+        _chk(_lib.hhg_mesh_prepare(self.handle))
+        return self
 
     def blend_map(self, kind=HHG_BLEND_SHELL):
         _chk(_lib.blend_map(self.handle, kind))
@@ -588,7 +607,20 @@ class MG:
                                 ctypes.byref(it), ctypes.byref(rel), _stream(stream)))
         return x, it.value, rel.value
 
+    def _host_vec(self, t, name):
+        import torch
+        n = self.mesh.vec_len(self.l_max, HHG_P2VEC)
+        if not (isinstance(t, torch.Tensor) and t.device.type == "cpu" and t.dtype == torch.float64
+                and t.is_contiguous() and t.numel() == n):
+            raise HHGError(f"{name}: need a contiguous float64 host tensor of length {n}")
+        return t
+
     def vcycle_host(self, rhs_host, x_host, stream=None):
+        """One V-cycle on host buffers (H2D, V-cycle, D2H on `stream`; asynchronous when the buffers
+        are pinned -- the binding keeps references to them until the next call)."""
+        self._host_vec(rhs_host, "rhs_host")
+        self._host_vec(x_host, "x_host")
+        self._host_keep = (rhs_host, x_host)
         _chk(_lib.vcycle_host(self.handle, _ptr(rhs_host), _ptr(x_host), _stream(stream)))
         return x_host
 
@@ -597,10 +629,10 @@ class MG:
         neighbouring steps overlapped with the compute (asynchronous on `stream`)."""
         k = len(rhs_hosts)
         assert len(x_hosts) == k
-        n = self.mesh.vec_len(self.l_max, HHG_P2VEC)
         for t in list(rhs_hosts) + list(x_hosts):
-            if not (t.is_pinned() and t.dtype.is_floating_point and t.numel() == n and t.is_contiguous()):
-                raise HHGError("vcycle_host_batch: need pinned contiguous float64 host tensors of the level's length")
+            self._host_vec(t, "vcycle_host_batch")
+            if not t.is_pinned():
+                raise HHGError("vcycle_host_batch: need pinned host tensors")
         self._batch_keep = (list(rhs_hosts), list(x_hosts))
         rh = (ctypes.c_void_p * k)(*[t.data_ptr() for t in rhs_hosts])
         xh = (ctypes.c_void_p * k)(*[t.data_ptr() for t in x_hosts])

@@ -185,9 +185,18 @@ static void invalidate(hhg_mesh* m) {
   for (auto& L : m->levels) free_level(L);
 }
 
+static int check_no_dependents(const hhg_mesh* m, const char* what) {
+  if (m->dependents > 0)
+    return fail(HHG_EINVAL, std::string(what) + ": " + std::to_string(m->dependents) +
+                                " solver object(s) (hhg_mg / hhg_kmg / hhg_stokes / hhg_temp_solver) still use this mesh; "
+                                "destroy them first (their diagonals, spectra and captured graphs depend on it)");
+  return HHG_OK;
+}
+
 int blend_map(hhg_mesh* mesh, int kind) {
   CHECK_PTR(mesh);
   if (kind != HHG_BLEND_IDENTITY && kind != HHG_BLEND_SHELL) return fail(HHG_EINVAL, "bad blending kind");
+  HHG_TRY(check_no_dependents(mesh, "blend_map"));
   int old = mesh->blend;
   mesh->blend = kind;
   int r = mesh_set_geometry(mesh);
@@ -199,9 +208,23 @@ int blend_map(hhg_mesh* mesh, int kind) {
   return HHG_OK;
 }
 
+int hhg_mesh_prepare(hhg_mesh* mesh) {
+  CHECK_PTR(mesh);
+  for (int l = 0; l <= mesh->level_max; ++l) HHG_TRY(ensure_level(mesh, l));
+  return HHG_OK;
+}
+
+int hhg_set_deterministic(hhg_mesh* mesh, int on) {
+  CHECK_PTR(mesh);
+  HHG_TRY(check_no_dependents(mesh, "hhg_set_deterministic"));
+  mesh->deterministic = on != 0;
+  return HHG_OK;
+}
+
 int hhg_set_bc(hhg_mesh* mesh, int tag, int kind) {
   CHECK_PTR(mesh);
   if (kind < HHG_BC_NONE || kind > HHG_BC_FREESLIP) return fail(HHG_EINVAL, "bad BC kind");
+  HHG_TRY(check_no_dependents(mesh, "hhg_set_bc"));
   if (tag == HHG_BND_ALL) {
     mesh->bc_kind[0] = mesh->bc_kind[1] = mesh->bc_kind[2] = kind;
   } else if (tag == HHG_BND_INNER || tag == HHG_BND_OUTER) {
@@ -528,7 +551,7 @@ int hhg_dot(const hhg_mesh* mesh, int level, int space, const double* x, const d
   if (space != HHG_P1 && space != HHG_P2 && space != HHG_P2VEC) return fail(HHG_EINVAL, "bad space");
   auto* m = const_cast<hhg_mesh*>(mesh);
   HHG_TRY(ensure_level(m, level));
-  return launch_dot(m, m->levels[level], space, x, y, out_dev, (cudaStream_t)stream);
+  return launch_dot(m, m->levels[level], space, x, y, out_dev, (cudaStream_t)stream, m->levels[level].red);
 }
 
 int p2_restrict(const hhg_mesh* mesh, int fine_level, const double* r_fine, double* r_coarse, hhg_stream_t stream) {

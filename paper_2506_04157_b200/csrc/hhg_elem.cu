@@ -29,6 +29,8 @@
 //   * the transposed map scatters R = S K^T through Sbar_m = sum_q Db_m(q) (vertex: -Sbar/4 +
 //     Db_m(m), edge: (sqrt5-1)/4 (Sbar_m + Sbar_j) + Db_m(j) + Db_j(m)), all constant factors
 //     folded into the per-point weight.
+#include <algorithm>
+
 #include "hhg_internal.h"
 #include "hhg_device.cuh"
 
@@ -567,18 +569,26 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 
+constexpr int kMG = 26;  // MacroGeo (doubles)
+static_assert(sizeof(MacroGeo) == kMG * sizeof(double), "MacroGeo layout");
+
+// k_elem_fp (v6): one CTA per (brick of `bricks` = blockIdx.x, macro = blockIdx.y).  det != 0
+// (deterministic mode, one launch per brick colour -- bricks of one colour share no footprint point):
+// border points use plain load-add-store instead of fp64 REDs and sparse bricks take the dense path, so
+// the result is bitwise reproducible.
 template <bool BLEND, int MODE, bool FULL, bool ETAQ = false>
 #ifndef HHG_FP_MINB
 #define HHG_FP_MINB 5
 #endif
 __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
     k_elem_fp(const MacroGeo* __restrict__ mgeo, const double* __restrict__ lgeo, const int32_t* __restrict__ bricks,
-              int n1, double inv_n1, int64_t npts1, int64_t npts2, int64_t cstride, const double* __restrict__ eta,
-              const double* __restrict__ u, const double* __restrict__ p, double* __restrict__ yu,
-              double* __restrict__ yp, double gamma, const double* __restrict__ T2 = nullptr,
-              EtaQ eq = EtaQ{0.0, 1.0, 0.0}) {
-  constexpr bool DO_DIV = (MODE & ELEM_DIV) != 0;
+              int nb, int n1, double inv_n1, int64_t npts1, int64_t npts2, int64_t cstride,
+              const double* __restrict__ eta, const double* __restrict__ u, const double* __restrict__ p,
+              double* __restrict__ yu, double* __restrict__ yp, double gamma, const double* __restrict__ T2, EtaQ eq,
+              int det) {
+  (void)nb;
   constexpr bool NEED_U = elem_need_u(MODE);
   constexpr bool NEED_P = elem_need_p(MODE);
   constexpr bool HAS_P_OUT = elem_p_out(MODE);
@@ -603,6 +613,26 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
   // ---- stage: u footprint (cp.async), eta / p footprints, geometry; zero the output footprints
   const double* Gm = lgeo + (int64_t)mac * kLevelGeo;
   for (int r = tid; r < kGeoSm; r += kBT) cp_async8(sgeo + r, Gm + r);
+#ifdef HHG_EXP_ROWSTAGE
+  // one (row, component) item per thread: 2 row-start evaluations per thread, 9 cp.async per item
+  if (NEED_U || ETAQ) {
+    constexpr int NI = (NEED_U ? 243 : 0) + (ETAQ ? 81 : 0);
+#pragma unroll 1
+    for (int it = tid; it < NI; it += kBT) {
+      const int c = it / 81, r = it - 81 * c;
+      const int Y = r % 9, Z = r / 9;
+      const int gy = 2 * j0 + Y, gz = 2 * k0 + Z;
+      const int len = min(9, n2 - 2 * i0 - gy - gz + 1);
+      if (len <= 0) continue;
+      const int o = rowstart32(n2, gy, gz) + 2 * i0;
+      const double* sr = (NEED_U && c < 3) ? u + mb2 + c * cstride + o : T2 + mb2 + o;
+      double* d = ((NEED_U && c < 3) ? su + c * kFU : stt) + kPY * Y + kPZ * Z;
+#pragma unroll
+      for (int X = 0; X < 9; ++X)
+        if (X < len) cp_async8(d + xs(X), sr + X);
+    }
+  }
+#else
   if (NEED_U) {
 #pragma unroll 1
     for (int L = tid; L < 729; L += kBT) {
@@ -624,6 +654,7 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
       cp_async8(stt + fword(X, Y, Z), T2 + mb2 + rowstart32(n2, gy, gz) + gx);
     }
   }
+#endif
   if (HAS_U_OUT)
     for (int r = tid; r < 6 * kFY; r += kBT) sy[r] = 0.0;
   if (HAS_P_OUT)
@@ -655,7 +686,10 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
     for (int r = 0; r < 3; ++r) xa[r] = g.X0[r] + g.Jm[3 * r] * fa + g.Jm[3 * r + 1] * fb + g.Jm[3 * r + 2] * fc;
   };
 
-  if (delta <= 4) {
+  if (delta <= 4 && !det) {
+#ifdef HHG_EXP_NOSPARSE
+    return;
+#endif
     // ---------------- sparse brick (<= 64 tets, mixed types per warp): one tet per thread, REDs
     if (tid >= eNItems[delta]) return;
     const int item = eItems[delta][tid];
@@ -715,9 +749,21 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
         et[v] = se[cb1 + eOffP[t][v]];
         if (NEED_P) pp[v] = sp[cb1 + eOffP[t][v]];
       }
+#ifdef HHG_EXP_NOBODY
+      {
+        FootU fu{reinterpret_cast<const char*>(su + cb2), eOffB[t]};
+#pragma unroll
+        for (int a = 0; a < 10; ++a)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) acc[a][c] = fu(a, c) * et[0];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) gy[v] = pp[v];
+      }
+#else
       tet_body<BLEND, MODE, FULL, FootU, ETAQ, FootT>(sgeo + t * kTypeGeo, wdet, xa, nh, cK, gamma,
                                                       FootU{reinterpret_cast<const char*>(su + cb2), eOffB[t]}, et, pp,
                                                       acc, gy, FootT{reinterpret_cast<const char*>(stt + cb2), eOffB[t]}, eq);
+#endif
     }
     const int* off = eOffB[t];
     char* ywb = reinterpret_cast<char*>(yw);
@@ -753,7 +799,9 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
   }
   __syncthreads();
 
-  // ---- write the brick's output footprint
+  // ---- write the brick's output footprint: plain stores inside, fp64 RED (deterministic mode: plain
+  // load-add-store) on the footprint border shared with neighbouring bricks; the two warps' Z = 4 planes
+  // are summed first
   if (HAS_U_OUT) {
 #pragma unroll 1
     for (int L = tid; L < 729; L += kBT) {
@@ -770,7 +818,10 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
         else if (Z > 4) v = sy[3 * kFY + c * kFY + wxy + kPZ * (Z - 4)];
         else v = sy[c * kFY + wxy + kPZ * 4] + sy[3 * kFY + c * kFY + wxy];
         if (!border) dst[c * cstride] = v;
-        else if (v != 0.0) atomicAdd(dst + c * cstride, v);
+        else if (v != 0.0) {
+          if (det) dst[c * cstride] += v;
+          else atomicAdd(dst + c * cstride, v);
+        }
       }
     }
   }
@@ -786,236 +837,50 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
       double* dst = yp + mb1 + rowstart32(n1, gy, gz) + gx;
       const bool border = X == 0 || Y == 0 || Z == 0 || X == 4 || Y == 4 || Z == 4;
       if (!border) *dst = v;
-      else if (v != 0.0) atomicAdd(dst, v);
+      else if (v != 0.0) {
+        if (det) *dst += v;
+        else atomicAdd(dst, v);
+      }
     }
   }
 }
 
-static int ensure_slots();
-
-// ================================================================ persistent coarse solve
-// The 50-iteration Jacobi-PCG of the coarsest level (R15) as ONE kernel: one CTA per
-// macro (coarse levels n <= 4 are a single sparse brick per macro), a software grid barrier
-// between the phases of an iteration (all CTAs co-resident: #macros CTAs of 64 threads), device-
-// resident scalars recomputed identically by every CTA from per-macro partials in fixed order.
-// Per iteration: q = A p (element contributions of the CTA's macro summed in shared memory)
-// | interface sum + BC of q (groups strided over the grid) | p.q | x += a p, r -= a q,
-// z = P_v M D^-1 r, r.z | p = z + b p.  Single rank only (no NCCL inside a kernel).
-__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    volatile unsigned* vb = bar;
-    const unsigned gen = vb[1];
-    __threadfence();
-    if (atomicAdd(&bar[0], 1u) == nblocks - 1) {
-      bar[0] = 0;
-      __threadfence();
-      atomicAdd(&bar[1], 1u);
+// Launch of one element-kernel instantiation: one CTA per (macro, brick) item, one launch over all bricks --
+// or, in deterministic mode, one launch per brick colour.
+template <bool BLEND, int MODE, bool FULL, bool ETAQ>
+struct ElemKernel {
+  static constexpr size_t smem = fp_smem_words<MODE, ETAQ>() * sizeof(double);
+  static bool ready;
+  static int prepare() {  // host-side attributes (eager: never under stream capture)
+    if (ready) return HHG_OK;
+    auto k = k_elem_fp<BLEND, MODE, FULL, ETAQ>;
+    HHG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared));
+    HHG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ready = true;
+    return HHG_OK;
+  }
+  static int launch(const Mesh* m, const Level& L, const double* eta, double gamma, const double* u, const double* p,
+                    double* yu, double* yp, const double* T2, EtaQ eq, cudaStream_t s) {
+    HHG_TRY(prepare());
+    const int64_t nm = macro_count(m);
+    auto go = [&](const int32_t* list, int64_t nb, int det) {
+      if (nm * nb == 0) return;
+      k_elem_fp<BLEND, MODE, FULL, ETAQ><<<dim3((unsigned)nb, (unsigned)nm), kBT, smem, s>>>(m->dgeo, L.geo, list, (int)nb, L.n1,
+                                                                           1.0 / L.n1, L.npts1, L.npts2, nm * L.npts2,
+                                                                           eta, u, p, yu, yp, gamma, T2, eq, det);
+      count_launch();
+    };
+    if (!m->deterministic) {
+      go(L.bricks, L.n_bricks, 0);
     } else {
-      while (vb[1] == gen) {
-      }
+      for (int c = 0; c < 8; ++c) go(L.bricks_col + L.col_off[c], L.col_off[c + 1] - L.col_off[c], 1);
     }
-    __threadfence();
+    HHG_CUDA(cudaGetLastError());
+    return HHG_OK;
   }
-  __syncthreads();
-}
-__device__ __forceinline__ double block_sum64(double v, double* red) {  // 64-thread CTA, fixed order
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  __syncthreads();
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-  __syncthreads();
-  return red[0] + red[1];
-}
-__device__ __forceinline__ double grid_total(const volatile double* part, int n) {
-  double t = 0.0;
-  for (int i = 0; i < n; ++i) t += part[i];
-  return t;
-}
-
-template <bool BLEND, bool FULL>
-__global__ void __launch_bounds__(kBT) k_coarse_pcg(
-    const MacroGeo* __restrict__ mgeo, const double* __restrict__ lgeo, int n1, double inv_n1, int64_t npts1,
-    int64_t npts2, int64_t cs, const double* __restrict__ eta, const double* __restrict__ dinv,
-    const int32_t* __restrict__ bcn, const uint8_t* __restrict__ own, int64_t ng, const int64_t* __restrict__ gptr,
-    const int64_t* __restrict__ gcopy, const uint8_t* __restrict__ gkind, const double* __restrict__ gnormal,
-    const double* __restrict__ f, double* x, double* r, double* z, double* p, double* q, double* part,
-    unsigned* bar, int iters) {
-  extern __shared__ double sy[];  // [3][npts2] element contributions of this macro
-  __shared__ double red[2];
-  const int mac = blockIdx.x, nb = gridDim.x, tid = threadIdx.x;
-  const int n2 = 2 * n1;
-  const int64_t mb2 = (int64_t)mac * npts2, mb1 = (int64_t)mac * npts1;
-  const int nloc = (int)npts2;
-  double* part1 = part;
-  double* part2 = part + nb;
-  // x = 0, r = f, z = P_v M D^-1 r, p = z ; r.z
-  double acc = 0.0;
-  for (int i = tid; i < nloc; i += kBT) {
-    const int64_t j = mb2 + i;
-    double zv[3], rv[3];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      x[j + c * cs] = 0.0;
-      rv[c] = f[j + c * cs];
-      r[j + c * cs] = rv[c];
-      zv[c] = dinv[j + c * cs] * rv[c];
-    }
-    bc_project(bcn[j], gnormal, zv[0], zv[1], zv[2]);
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      z[j + c * cs] = zv[c];
-      p[j + c * cs] = zv[c];
-    }
-    if (own[j]) acc += rv[0] * zv[0] + rv[1] * zv[1] + rv[2] * zv[2];
-  }
-  acc = block_sum64(acc, red);
-  if (tid == 0) part2[mac] = acc;
-  grid_barrier(bar, nb);
-  double rz = grid_total(part2, nb);
-
-  const MacroGeo& g = mgeo[mac];
-  double nh[3] = {0, 0, 0}, cK = 1.0;
-  if (BLEND) {
-    nh[0] = g.nhat[0];
-    nh[1] = g.nhat[1];
-    nh[2] = g.nhat[2];
-    cK = g.cK;
-  }
-  const double* Gm = lgeo + (int64_t)mac * kLevelGeo;
-  const double wdet = EWQ * Gm[6 * kTypeGeo];
-  const int nit = eNItems[n1];
-  for (int it = 0; it < iters; ++it) {
-    // ---- q = A p on this macro (shared-memory accumulation), written to the macro's storage
-    for (int i = tid; i < 3 * nloc; i += kBT) sy[i] = 0.0;
-    __syncthreads();
-    for (int k = tid; k < nit; k += kBT) {
-      const int item = eItems[n1][k];
-      const int cube = item & 63, t = item >> 6;
-      const int ai = cube & 3, aj = (cube >> 2) & 3, ak = cube >> 4;
-      double xa[3];
-      const double fa = ai * inv_n1, fb = aj * inv_n1, fc = ak * inv_n1;
-#pragma unroll
-      for (int rr = 0; rr < 3; ++rr) xa[rr] = g.X0[rr] + g.Jm[3 * rr] * fa + g.Jm[3 * rr + 1] * fb + g.Jm[3 * rr + 2] * fc;
-      int ix[10];
-      double uu[10][3], et[4], pp[4] = {0, 0, 0, 0}, accv[10][3], gy[4];
-#pragma unroll
-      for (int a = 0; a < 10; ++a) {
-        const int sl = eSlot[t][a];
-        ix[a] = rowstart32(n2, 2 * aj + (sl / 3) % 3, 2 * ak + sl / 9) + 2 * ai + sl % 3;
-#pragma unroll
-        for (int c = 0; c < 3; ++c) uu[a][c] = p[mb2 + ix[a] + c * cs];
-      }
-#pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        const int ps = ePSlot[t][v];
-        et[v] = eta ? eta[mb1 + rowstart32(n1, aj + ((ps >> 1) & 1), ak + (ps >> 2)) + ai + (ps & 1)] : 1.0;
-      }
-      tet_body<BLEND, ELEM_A, FULL>(Gm + t * kTypeGeo, wdet, xa, nh, cK, 0.0, RegU{uu}, et, pp, accv, gy);
-#pragma unroll
-      for (int a = 0; a < 10; ++a)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) atomicAdd(&sy[c * nloc + ix[a]], accv[a][c]);
-    }
-    __syncthreads();
-    for (int i = tid; i < nloc; i += kBT)
-#pragma unroll
-      for (int c = 0; c < 3; ++c) q[mb2 + i + c * cs] = sy[c * nloc + i];
-    grid_barrier(bar, nb);
-    // ---- interface sum + BC of q
-    for (int64_t gi = (int64_t)mac * kBT + tid; gi < ng; gi += (int64_t)nb * kBT) {
-      const int64_t b0 = gptr[gi], e0 = gptr[gi + 1];
-      double val[3];
-      group_sum<3>(b0, e0, gcopy, cs, q, val);
-      group_bc<3>(gkind[gi], gnormal + 3 * gi, val);
-      group_store<3>(b0, e0, gcopy, cs, val, q);
-    }
-    grid_barrier(bar, nb);
-    // ---- p.q
-    acc = 0.0;
-    for (int i = tid; i < nloc; i += kBT) {
-      const int64_t j = mb2 + i;
-      if (own[j]) acc += p[j] * q[j] + p[j + cs] * q[j + cs] + p[j + 2 * cs] * q[j + 2 * cs];
-    }
-    acc = block_sum64(acc, red);
-    if (tid == 0) part1[mac] = acc;
-    grid_barrier(bar, nb);
-    const double pq = grid_total(part1, nb);
-    const double alpha = (rz > 1e-300 && pq != 0.0) ? rz / pq : 0.0;
-    // ---- x += a p, r -= a q, z = P_v M D^-1 r ; r.z
-    acc = 0.0;
-    for (int i = tid; i < nloc; i += kBT) {
-      const int64_t j = mb2 + i;
-      double zv[3], rv[3];
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const int64_t jc = j + c * cs;
-        x[jc] += alpha * p[jc];
-        rv[c] = r[jc] - alpha * q[jc];
-        r[jc] = rv[c];
-        zv[c] = dinv[jc] * rv[c];
-      }
-      bc_project(bcn[j], gnormal, zv[0], zv[1], zv[2]);
-#pragma unroll
-      for (int c = 0; c < 3; ++c) z[j + c * cs] = zv[c];
-      if (own[j]) acc += rv[0] * zv[0] + rv[1] * zv[1] + rv[2] * zv[2];
-    }
-    acc = block_sum64(acc, red);
-    if (tid == 0) part2[mac] = acc;
-    grid_barrier(bar, nb);
-    const double rzn = grid_total(part2, nb);
-    const double beta = rz > 1e-300 ? rzn / rz : 0.0;
-    for (int i = tid; i < nloc; i += kBT)
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const int64_t jc = mb2 + i + c * cs;
-        p[jc] = z[jc] + beta * p[jc];
-      }
-    rz = rz > 1e-300 ? rzn : rz;
-    __syncthreads();
-  }
-}
-
-// All CTAs of the persistent kernel must be co-resident (software grid barrier): true if the device
-// can hold one CTA per macro at once.
-bool coarse_pcg_fits(const Mesh* m, const Level& L) {
-  const int64_t nm = macro_count(m);
-  if (L.n1 > 4 || nm < 1) return false;
-  const size_t smem = 3 * L.npts2 * sizeof(double);
-  int per_sm = 0, nsm = 0, dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
-    return false;
-  const bool bl = m->blend == HHG_BLEND_SHELL;
-  cudaError_t e = bl ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_coarse_pcg<true, true>, kBT, smem)
-                     : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_coarse_pcg<false, true>, kBT, smem);
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    return false;
-  }
-  return (int64_t)per_sm * nsm >= nm;
-}
-
-int launch_coarse_pcg(const Mesh* m, const Level& L, const double* eta, const double* dinv, const double* f, double* x,
-                      double* r, double* z, double* p, double* q, double* part, unsigned* bar, int iters,
-                      cudaStream_t s) {
-  HHG_TRY(ensure_slots());
-  const int64_t nm = macro_count(m);
-  if (!coarse_pcg_fits(m, L)) return fail(HHG_EINVAL, "persistent coarse PCG: CTAs cannot all be co-resident");
-  const size_t smem = 3 * L.npts2 * sizeof(double);
-  const bool bl = m->blend == HHG_BLEND_SHELL;
-if (bl)
-    k_coarse_pcg<true, true><<<(unsigned)nm, kBT, smem, s>>>(m->dgeo, L.geo, L.n1, 1.0 / L.n1, L.npts1, L.npts2,
-                                                             nm * L.npts2, eta, dinv, L.bcn2, L.own2, L.g2.n, L.g2.ptr,
-                                                             L.g2.copy, L.g2.kind, L.g2.normal, f, x, r, z, p, q, part,
-                                                             bar, iters);
-  else
-    k_coarse_pcg<false, true><<<(unsigned)nm, kBT, smem, s>>>(m->dgeo, L.geo, L.n1, 1.0 / L.n1, L.npts1, L.npts2,
-                                                              nm * L.npts2, eta, dinv, L.bcn2, L.own2, L.g2.n, L.g2.ptr,
-                                                              L.g2.copy, L.g2.kind, L.g2.normal, f, x, r, z, p, q, part,
-                                                              bar, iters);
-  count_launch();
-  HHG_CUDA(cudaGetLastError());
-  return HHG_OK;
-}
+};
+template <bool BLEND, int MODE, bool FULL, bool ETAQ>
+bool ElemKernel<BLEND, MODE, FULL, ETAQ>::ready = false;
 
 static bool g_slots_ready = false;
 static int ensure_slots() {
@@ -1091,42 +956,6 @@ static int ensure_slots() {
   return HHG_OK;
 }
 
-template <bool BLEND, int MODE, bool FULL>
-static void elem_launch(const Mesh* m, const Level& L, const double* eta, double gamma, const double* u,
-                        const double* p, double* yu, double* yp, cudaStream_t s) {
-  const int64_t nm = macro_count(m);
-  constexpr size_t smem = fp_smem_words<MODE>() * sizeof(double);
-  dim3 grid((unsigned)L.n_bricks, (unsigned)nm);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_elem_fp<BLEND, MODE, FULL>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                         (int)cudaSharedmemCarveoutMaxShared);
-    cudaFuncSetAttribute(k_elem_fp<BLEND, MODE, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
-  k_elem_fp<BLEND, MODE, FULL><<<grid, kBT, smem, s>>>(m->dgeo, L.geo, L.bricks, L.n1, 1.0 / L.n1, L.npts1, L.npts2,
-                                                       nm * L.npts2, eta, u, p, yu, yp, gamma);
-}
-
-// w-BFBT operators: same brick kernel, a in the gamma slot, the outer radius in eq.r_jump
-template <bool BLEND, int MODE>
-static void elem_launch_surf(const Mesh* m, const Level& L, const double* eta, double a, double r_outer,
-                             const double* u, const double* p, double* yu, double* yp, cudaStream_t s) {
-  const int64_t nm = macro_count(m);
-  constexpr size_t smem = fp_smem_words<MODE>() * sizeof(double);
-  dim3 grid((unsigned)L.n_bricks, (unsigned)nm);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_elem_fp<BLEND, MODE, true>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                         (int)cudaSharedmemCarveoutMaxShared);
-    cudaFuncSetAttribute(k_elem_fp<BLEND, MODE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
-  k_elem_fp<BLEND, MODE, true><<<grid, kBT, smem, s>>>(m->dgeo, L.geo, L.bricks, L.n1, 1.0 / L.n1, L.npts1, L.npts2,
-                                                       nm * L.npts2, eta, u, p, yu, yp, a, nullptr,
-                                                       EtaQ{0.0, 1.0, r_outer});
-}
-
 int launch_elem_surf(const Mesh* m, const Level& L, int mode, const double* eta, double a, double r_outer,
                      const double* in, double* out, cudaStream_t s) {
   if (macro_count(m) == 0) return HHG_OK;  // a rank without macros (empty partition)
@@ -1134,37 +963,19 @@ int launch_elem_surf(const Mesh* m, const Level& L, int mode, const double* eta,
   const bool bl = m->blend == HHG_BLEND_SHELL;
   if (a != 1.0 && !bl) return fail(HHG_EINVAL, "w-BFBT surface scaling a != 1 needs a shell-blended mesh");
   if (!(a > 0.0)) return fail(HHG_EINVAL, "w-BFBT surface scaling a must be > 0");
-#define HHG_SURF(MODE, U, P, YU, YP)                                                   \
-  if (bl) elem_launch_surf<true, MODE>(m, L, eta, a, r_outer, U, P, YU, YP, s);        \
-  else elem_launch_surf<false, MODE>(m, L, eta, a, r_outer, U, P, YU, YP, s);
+  // a in the gamma slot, the outer radius in eq.r_jump
+  const EtaQ eq{0.0, 1.0, r_outer};
+#define HHG_SURF(MODE, U, P, YU, YP)                                                                     \
+  return bl ? ElemKernel<true, MODE, true, false>::launch(m, L, eta, a, U, P, YU, YP, nullptr, eq, s)    \
+            : ElemKernel<false, MODE, true, false>::launch(m, L, eta, a, U, P, YU, YP, nullptr, eq, s);
   switch (mode) {
-    case ELEM_KP1: HHG_SURF(ELEM_KP1, nullptr, in, nullptr, out); break;
-    case ELEM_KP1D: HHG_SURF(ELEM_KP1D, nullptr, nullptr, nullptr, out); break;
-    case ELEM_VMASS: HHG_SURF(ELEM_VMASS, in, nullptr, out, nullptr); break;
-    case ELEM_VMASSD: HHG_SURF(ELEM_VMASSD, nullptr, nullptr, out, nullptr); break;
+    case ELEM_KP1: HHG_SURF(ELEM_KP1, nullptr, in, nullptr, out);
+    case ELEM_KP1D: HHG_SURF(ELEM_KP1D, nullptr, nullptr, nullptr, out);
+    case ELEM_VMASS: HHG_SURF(ELEM_VMASS, in, nullptr, out, nullptr);
+    case ELEM_VMASSD: HHG_SURF(ELEM_VMASSD, nullptr, nullptr, out, nullptr);
     default: return fail(HHG_EINVAL, "bad w-BFBT element mode");
   }
 #undef HHG_SURF
-  count_launch();
-  HHG_CUDA(cudaGetLastError());
-  return HHG_OK;
-}
-
-template <bool BLEND, int MODE>
-static void elem_launch_qeta(const Mesh* m, const Level& L, const double* T2, EtaQ eq, const double* u, double* yu,
-                             cudaStream_t s) {
-  const int64_t nm = macro_count(m);
-  constexpr size_t smem = fp_smem_words<MODE, true>() * sizeof(double);
-  dim3 grid((unsigned)L.n_bricks, (unsigned)nm);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_elem_fp<BLEND, MODE, true, true>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                         (int)cudaSharedmemCarveoutMaxShared);
-    cudaFuncSetAttribute(k_elem_fp<BLEND, MODE, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
-  k_elem_fp<BLEND, MODE, true, true><<<grid, kBT, smem, s>>>(m->dgeo, L.geo, L.bricks, L.n1, 1.0 / L.n1, L.npts1, L.npts2,
-                                                             nm * L.npts2, nullptr, u, nullptr, yu, nullptr, 0.0, T2, eq);
 }
 
 // A (mode ELEM_A) or diag(A) (ELEM_DIAG) with the viscosity evaluated at the quadrature points from the
@@ -1175,18 +986,13 @@ int launch_elem_qeta(const Mesh* m, const Level& L, int mode, const double* T2, 
   HHG_TRY(ensure_slots());
   const EtaQ eq{lnC, jump, r_jump};
   const bool bl = m->blend == HHG_BLEND_SHELL;
-  if (mode == ELEM_A) {
-    if (bl) elem_launch_qeta<true, ELEM_A>(m, L, T2, eq, u, yu, s);
-    else elem_launch_qeta<false, ELEM_A>(m, L, T2, eq, u, yu, s);
-  } else if (mode == ELEM_DIAG) {
-    if (bl) elem_launch_qeta<true, ELEM_DIAG>(m, L, T2, eq, u, yu, s);
-    else elem_launch_qeta<false, ELEM_DIAG>(m, L, T2, eq, u, yu, s);
-  } else {
-    return fail(HHG_EINVAL, "quadrature-point viscosity: mode must be A or diag");
-  }
-  count_launch();
-  HHG_CUDA(cudaGetLastError());
-  return HHG_OK;
+  if (mode == ELEM_A)
+    return bl ? ElemKernel<true, ELEM_A, true, true>::launch(m, L, nullptr, 0.0, u, nullptr, yu, nullptr, T2, eq, s)
+              : ElemKernel<false, ELEM_A, true, true>::launch(m, L, nullptr, 0.0, u, nullptr, yu, nullptr, T2, eq, s);
+  if (mode == ELEM_DIAG)
+    return bl ? ElemKernel<true, ELEM_DIAG, true, true>::launch(m, L, nullptr, 0.0, u, nullptr, yu, nullptr, T2, eq, s)
+              : ElemKernel<false, ELEM_DIAG, true, true>::launch(m, L, nullptr, 0.0, u, nullptr, yu, nullptr, T2, eq, s);
+  return fail(HHG_EINVAL, "quadrature-point viscosity: mode must be A or diag");
 }
 
 int launch_elem(const Mesh* m, const Level& L, int mode, int form, const double* eta, double gamma,
@@ -1195,28 +1001,50 @@ int launch_elem(const Mesh* m, const Level& L, int mode, int form, const double*
   HHG_TRY(ensure_slots());
   const bool bl = m->blend == HHG_BLEND_SHELL;
   const bool full = form == HHG_VISC_FULL;
-#define HHG_DISPATCH(MODE)                                                            \
-  if (bl) {                                                                           \
-    if (full) elem_launch<true, MODE, true>(m, L, eta, gamma, u, p, yu, yp, s);       \
-    else elem_launch<true, MODE, false>(m, L, eta, gamma, u, p, yu, yp, s);           \
-  } else {                                                                            \
-    if (full) elem_launch<false, MODE, true>(m, L, eta, gamma, u, p, yu, yp, s);      \
-    else elem_launch<false, MODE, false>(m, L, eta, gamma, u, p, yu, yp, s);          \
-  }
+  const EtaQ eq{0.0, 1.0, 0.0};
+#define HHG_DISPATCH(MODE)                                                                                           \
+  return bl ? (full ? ElemKernel<true, MODE, true, false>::launch(m, L, eta, gamma, u, p, yu, yp, nullptr, eq, s)   \
+                    : ElemKernel<true, MODE, false, false>::launch(m, L, eta, gamma, u, p, yu, yp, nullptr, eq, s)) \
+            : (full ? ElemKernel<false, MODE, true, false>::launch(m, L, eta, gamma, u, p, yu, yp, nullptr, eq, s)  \
+                    : ElemKernel<false, MODE, false, false>::launch(m, L, eta, gamma, u, p, yu, yp, nullptr, eq, s));
   switch (mode) {
-    case ELEM_A: HHG_DISPATCH(ELEM_A); break;
-    case ELEM_BT: HHG_DISPATCH(ELEM_BT); break;
-    case ELEM_DIV: HHG_DISPATCH(ELEM_DIV); break;
-    case ELEM_A | ELEM_BT | ELEM_DIV: HHG_DISPATCH(ELEM_A | ELEM_BT | ELEM_DIV); break;
-    case ELEM_DIAG: HHG_DISPATCH(ELEM_DIAG); break;
-    case ELEM_MASS: HHG_DISPATCH(ELEM_MASS); break;
-    case ELEM_MASSD: HHG_DISPATCH(ELEM_MASSD); break;
-    case ELEM_LOAD: HHG_DISPATCH(ELEM_LOAD); break;
+    case ELEM_A: HHG_DISPATCH(ELEM_A);
+    case ELEM_BT: HHG_DISPATCH(ELEM_BT);
+    case ELEM_DIV: HHG_DISPATCH(ELEM_DIV);
+    case ELEM_A | ELEM_BT | ELEM_DIV: HHG_DISPATCH(ELEM_A | ELEM_BT | ELEM_DIV);
+    case ELEM_DIAG: HHG_DISPATCH(ELEM_DIAG);
+    case ELEM_MASS: HHG_DISPATCH(ELEM_MASS);
+    case ELEM_MASSD: HHG_DISPATCH(ELEM_MASSD);
+    case ELEM_LOAD: HHG_DISPATCH(ELEM_LOAD);
     default: return fail(HHG_EINVAL, "bad element mode");
   }
 #undef HHG_DISPATCH
-  count_launch();
-  HHG_CUDA(cudaGetLastError());
+}
+
+// Eager one-time set-up of the element kernels (tables in __constant__ memory, kernel attributes,
+// occupancy): called from mesh/level construction so that no hot call -- in particular none under
+// CUDA-graph capture -- runs a synchronous host API.
+int elem_prepare_all() {
+  HHG_TRY(ensure_slots());
+#define HHG_PREP(B, MODE, F, E) HHG_TRY((ElemKernel<B, MODE, F, E>::prepare()));
+#define HHG_PREP4(MODE) HHG_PREP(true, MODE, true, false) HHG_PREP(true, MODE, false, false) \
+  HHG_PREP(false, MODE, true, false) HHG_PREP(false, MODE, false, false)
+  HHG_PREP4(ELEM_A)
+  HHG_PREP4(ELEM_BT)
+  HHG_PREP4(ELEM_DIV)
+  HHG_PREP4(ELEM_A | ELEM_BT | ELEM_DIV)
+  HHG_PREP4(ELEM_DIAG)
+  HHG_PREP4(ELEM_MASS)
+  HHG_PREP4(ELEM_MASSD)
+  HHG_PREP4(ELEM_LOAD)
+  HHG_PREP(true, ELEM_KP1, true, false) HHG_PREP(false, ELEM_KP1, true, false)
+  HHG_PREP(true, ELEM_KP1D, true, false) HHG_PREP(false, ELEM_KP1D, true, false)
+  HHG_PREP(true, ELEM_VMASS, true, false) HHG_PREP(false, ELEM_VMASS, true, false)
+  HHG_PREP(true, ELEM_VMASSD, true, false) HHG_PREP(false, ELEM_VMASSD, true, false)
+  HHG_PREP(true, ELEM_A, true, true) HHG_PREP(false, ELEM_A, true, true)
+  HHG_PREP(true, ELEM_DIAG, true, true) HHG_PREP(false, ELEM_DIAG, true, true)
+#undef HHG_PREP4
+#undef HHG_PREP
   return HHG_OK;
 }
 

@@ -88,6 +88,10 @@ struct Level {
   double* geo = nullptr;            // [n_macro][kLevelGeo]
   int32_t* bricks = nullptr;        // 4x4x4-cube brick origins, packed i|j<<10|k<<20
   int64_t n_bricks = 0;
+  int32_t* bricks_col = nullptr;    // the same bricks sorted by colour (bi&1 | (bj&1)<<1 | (bk&1)<<2)
+  int64_t col_off[9] = {0};         // colour c: bricks_col[col_off[c] .. col_off[c+1])
+  int32_t* rs1 = nullptr;           // row starts of the P1 / P2 lattices: index of (0, j, k) at [k (N+1) + j]
+  int32_t* rs2 = nullptr;
   int32_t* rows1 = nullptr;         // packed (j | k<<16) for P1 rows
   int32_t* rows2 = nullptr;         // packed rows for P2
   int64_t nrows1 = 0, nrows2 = 0;
@@ -104,6 +108,7 @@ struct Level {
 };
 
 constexpr int kRedBlocks = 296;     // 2 x 148 SMs
+constexpr int kRedScratch = kRedBlocks + 8;
 
 struct Mesh {
   // global macro mesh (host)
@@ -117,6 +122,8 @@ struct Mesh {
   hhg_comm* comm = nullptr;
   std::vector<int64_t> local;       // global ids of local macros
   int blend = HHG_BLEND_IDENTITY;
+  bool deterministic = false;       // element kernels per brick colour, no fp64 REDs (hhg_set_deterministic)
+  int dependents = 0;               // live hhg_mg / hhg_kmg / hhg_stokes / hhg_temp_solver objects on this mesh
   int bc_kind[3] = {HHG_BC_NONE, HHG_BC_NONE, HHG_BC_NONE};  // untagged, inner, outer
   std::vector<MacroGeo> hgeo;       // host copy, local macros
   MacroGeo* dgeo = nullptr;         // device
@@ -129,6 +136,9 @@ struct Mesh {
 int ensure_level(Mesh* m, int level);
 int ensure_device_geo(Mesh* m);
 int ensure_canon(Mesh* m, int level, int space);
+int canonical_count(const Mesh* m, int N, int64_t* n);
+int canonical_keys(const Mesh* m, int N, int64_t* keys);
+constexpr uint64_t kKPowerSeed = 7;  // K_{1/sqrt(eta)} power-iteration start vector (hhg_kmg_create)
 void free_level(Level& L);
 int64_t macro_count(const Mesh* m);
 
@@ -173,8 +183,11 @@ int comm_allreduce_sum(hhg_comm* c, double* buf, int64_t n, cudaStream_t s);
 int build_host_groups(const Mesh* m, int level, int space, std::vector<int64_t>& ptr, std::vector<int64_t>& copy,
                       std::vector<uint8_t>& kind, std::vector<double>& normal, std::vector<uint8_t>& own,
                       Halo& halo, std::vector<int64_t>& slot_group);
+// reduction scratch: kRedScratch doubles (partials + a zero-initialised counter at [kRedBlocks + 4]); every
+// solver object owns one (red_alloc), mesh-level calls (hhg_dot) use the level's L.red
 int launch_dot(const Mesh* m, const Level& L, int space, const double* x, const double* y, double* out,
-               cudaStream_t s);
+               cudaStream_t s, double* red);
+int red_alloc(double** red);
 int launch_prolong(const Mesh* m, const Level& Lc, const Level& Lf, const double* xc, double* xf,
                    cudaStream_t s);
 int launch_restrict(const Mesh* m, const Level& Lc, const Level& Lf, const double* rf, double* rc,
@@ -209,13 +222,11 @@ int launch_pcg_update_bc(const Mesh* m, const Level& L, int it, const double* sc
                          const double* p, const double* q, const double* dinv, double* z, cudaStream_t s);
 int launch_pcg_dir_zero(int64_t n, int it, const double* scal, const double* z, double* p, double* q_zero,
                         cudaStream_t s);
-// the coarsest level's Jacobi-PCG (all iterations) as one persistent kernel (single rank, n1 <= 4)
-bool coarse_pcg_fits(const Mesh* m, const Level& L);
-int launch_coarse_pcg(const Mesh* m, const Level& L, const double* eta, const double* dinv, const double* f, double* x,
-                      double* r, double* z, double* p, double* q, double* part, unsigned* bar, int iters,
-                      cudaStream_t s);
+// eager one-time set-up of kernel tables / attributes (never from a hot call)
+int elem_prepare_all();
+int transfer_prepare();
 int launch_dot_fused(const Mesh* m, const Level& L, int space, const double* x, const double* y, double* out,
-                     cudaStream_t s);
+                     cudaStream_t s, double* red);
 int launch_scalar_ops(int op, double* scal, cudaStream_t s);
 int launch_fill(int64_t n, double v, double* y, cudaStream_t s);
 int launch_recip(int64_t n, double* y, cudaStream_t s);                          // y = 1 / y

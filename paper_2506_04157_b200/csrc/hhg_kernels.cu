@@ -185,8 +185,9 @@ __global__ void k_dot_final(const double* __restrict__ part, int n, double* __re
   }
 }
 
-// one-launch dot: block partials + last-block (fixed-order) finalisation; counter lives in the
-// level's reduction scratch (reset by the last block, so graph replays stay valid)
+// one-launch dot: block partials + last-block (fixed-order) finalisation; partials and counter live in
+// the caller's reduction scratch `red` (one per solver object, so dots of different objects never share
+// it; the counter is reset by the last block, so graph replays stay valid)
 __global__ void k_dot_fused(int64_t nstored, int nc, int64_t cstride, const uint8_t* __restrict__ own,
                             const double* __restrict__ x, const double* __restrict__ y, double* __restrict__ part,
                             unsigned* __restrict__ counter, double* __restrict__ out) {
@@ -228,29 +229,35 @@ __global__ void k_dot_fused(int64_t nstored, int nc, int64_t cstride, const uint
 }
 
 int launch_dot_fused(const Mesh* m, const Level& L, int space, const double* x, const double* y, double* out,
-                     cudaStream_t s) {
+                     cudaStream_t s, double* red) {
   const int64_t nm = macro_count(m);
   const bool p1 = space == HHG_P1;
   const int64_t nst = nm * (p1 ? L.npts1 : L.npts2);
   const int nc = space == HHG_P2VEC ? 3 : 1;
   int64_t nb = (nst + 255) / 256;
   nb = nb < 1 ? 1 : (nb > kRedBlocks ? kRedBlocks : nb);
-  k_dot_fused<<<(unsigned)nb, 256, 0, s>>>(nst, nc, nst, p1 ? L.own1 : L.own2, x, y, L.red,
-                                          reinterpret_cast<unsigned*>(L.red + kRedBlocks + 4), out);
+  k_dot_fused<<<(unsigned)nb, 256, 0, s>>>(nst, nc, nst, p1 ? L.own1 : L.own2, x, y, red,
+                                          reinterpret_cast<unsigned*>(red + kRedBlocks + 4), out);
   count_launch();
   HHG_CUDA(cudaGetLastError());
   if (m->comm && m->nranks > 1) HHG_TRY(comm_allreduce_sum(m->comm, out, 1, s));
   return HHG_OK;
 }
 
+int red_alloc(double** red) {
+  if (cudaMalloc(red, kRedScratch * sizeof(double)) != cudaSuccess) return fail(HHG_ENOMEM, "reduction scratch");
+  HHG_CUDA(cudaMemset(*red, 0, kRedScratch * sizeof(double)));
+  return HHG_OK;
+}
+
 int launch_dot(const Mesh* m, const Level& L, int space, const double* x, const double* y, double* out,
-               cudaStream_t s) {
+               cudaStream_t s, double* red) {
   const int64_t nm = macro_count(m);
   const bool p1 = space == HHG_P1;
   const int64_t nst = nm * (p1 ? L.npts1 : L.npts2);
   const int nc = space == HHG_P2VEC ? 3 : 1;
-  k_dot_partial<<<kRedBlocks, 256, 0, s>>>(nst, nc, nst, p1 ? L.own1 : L.own2, x, y, L.red);
-  k_dot_final<<<1, 256, 0, s>>>(L.red, kRedBlocks, out);
+  k_dot_partial<<<kRedBlocks, 256, 0, s>>>(nst, nc, nst, p1 ? L.own1 : L.own2, x, y, red);
+  k_dot_final<<<1, 256, 0, s>>>(red, kRedBlocks, out);
   count_launch(2);
   HHG_CUDA(cudaGetLastError());
   if (m->comm && m->nranks > 1) HHG_TRY(comm_allreduce_sum(m->comm, out, 1, s));
@@ -475,6 +482,8 @@ __global__ void k_restrict(const int32_t* __restrict__ rowsc, int64_t nrowsc, in
     cr[2 * cstridec + I] = s2;
   }
 }
+
+int transfer_prepare() { return ensure_transfer_tabs(); }
 
 int launch_prolong(const Mesh* m, const Level& Lc, const Level& Lf, const double* xc, double* xf, cudaStream_t s) {
   if (macro_count(m) == 0) return HHG_OK;

@@ -62,6 +62,9 @@ void free_level(Level& L) {
   };
   f(L.geo);
   f(L.bricks);
+  f(L.bricks_col);
+  f(L.rs1);
+  f(L.rs2);
   f(L.rows1);
   f(L.rows2);
   for (Groups* g : {&L.g1, &L.g2}) {
@@ -420,6 +423,26 @@ int ensure_level(Mesh* m, int level) {
         for (int i = 0; i + j + k <= n - 1; i += 4) b.push_back(i | (j << 10) | (k << 20));
     L.n_bricks = (int64_t)b.size();
     HHG_TRY(upload(&L.bricks, b));
+    // colour classes for the deterministic mode: bricks of one colour are >= 8 cubes apart in some
+    // direction, so their 9x9x9 P2 footprints are disjoint
+    std::vector<int32_t> bc;
+    for (int c = 0; c < 8; ++c) {
+      L.col_off[c] = (int64_t)bc.size();
+      for (int32_t pk : b) {
+        const int bi = (pk & 1023) >> 2, bj = ((pk >> 10) & 1023) >> 2, bk = (pk >> 20) >> 2;
+        if (((bi & 1) | ((bj & 1) << 1) | ((bk & 1) << 2)) == c) bc.push_back(pk);
+      }
+    }
+    L.col_off[8] = (int64_t)bc.size();
+    HHG_TRY(upload(&L.bricks_col, bc));
+  }
+  // row-start tables (element kernel staging / write-out)
+  for (int sp = 0; sp < 2; ++sp) {
+    const int N = sp == 0 ? L.n1 : L.n2;
+    std::vector<int32_t> rs((size_t)(N + 1) * (N + 1), 0);
+    for (int k = 0; k <= N; ++k)
+      for (int j = 0; j + k <= N; ++j) rs[(size_t)k * (N + 1) + j] = (int32_t)lidx(0, j, k, N);
+    HHG_TRY(upload(sp == 0 ? &L.rs1 : &L.rs2, rs));
   }
   // rows
   for (int sp = 0; sp < 2; ++sp) {
@@ -446,6 +469,11 @@ int ensure_level(Mesh* m, int level) {
   if (cudaMalloc(&L.red, (kRedBlocks + 8) * sizeof(double)) != cudaSuccess)
     return fail(HHG_ENOMEM, "cudaMalloc reduction scratch");
   HHG_CUDA(cudaMemset(L.red, 0, (kRedBlocks + 8) * sizeof(double)));  // fused-dot counter starts at 0
+  // kernel tables and attributes eagerly, then a device-wide sync: a later hot call on any stream
+  // (non-blocking streams included, and under graph capture) sees a finished set-up
+  HHG_TRY(elem_prepare_all());
+  HHG_TRY(transfer_prepare());
+  HHG_CUDA(cudaDeviceSynchronize());
   L.built = true;
   return HHG_OK;
 }

@@ -86,8 +86,7 @@ struct hhg_mg {
   };
   std::vector<Lv> lv;
   double* scal = nullptr;    // device scalars
-  double* cpart = nullptr;   // persistent coarse PCG: per-macro partial sums [2][n_macro]
-  unsigned* cbar = nullptr;  // its grid barrier (count, generation)
+  double* red = nullptr;     // this object's reduction scratch (dots never share it with other objects)
   double* hbuf_rhs = nullptr;  // device staging for vcycle_host
   double* hbuf_x = nullptr;
   cudaGraphExec_t gexec = nullptr;
@@ -105,10 +104,6 @@ struct hhg_mg {
               ev_done = nullptr;
   cudaGraphExec_t pipe_gexec[2] = {nullptr, nullptr};
   cudaStream_t pipe_stream = nullptr;
-  // HHG_PERSISTENT_COARSE=1: run the coarse PCG as one persistent kernel (k_coarse_pcg).  Off by
-  // default: measured 27.7 vs 26.4 ms per V(3,3) at L5 -- 200 software grid barriers per solve
-  // cost more than the ~300 launches they replace.
-  bool no_persistent = true;
   // profiling
   bool prof = false;
   std::vector<cudaEvent_t> ev;
@@ -120,8 +115,8 @@ struct hhg_mg {
       for (double* p : {L.x, L.f, L.r, L.d, L.t, L.dinv, L.p})
         if (p) cudaFree(p);
     if (scal) cudaFree(scal);
-    if (cpart) cudaFree(cpart);
-    if (cbar) cudaFree(cbar);
+    if (red) cudaFree(red);
+    if (mesh) --mesh->dependents;
     if (hbuf_rhs) cudaFree(hbuf_rhs);
     if (hbuf_x) cudaFree(hbuf_x);
     if (gexec) cudaGraphExecDestroy(gexec);
@@ -211,18 +206,16 @@ static int mg_pcg(hhg_mg* mg, int l, const double* f, double* x, cudaStream_t s)
   double* z = L.d;
   double* p = L.p;
   double* q = L.t;
-  if (m->nranks == 1 && mg->prm.visc_form == HHG_VISC_FULL && !mg->no_persistent && !L.T2 && coarse_pcg_fits(m, LL))
-    return launch_coarse_pcg(m, LL, L.eta, L.dinv, f, x, r, z, p, q, mg->cpart, mg->cbar, mg->prm.coarse_iters, s);
   HHG_CUDA(cudaMemsetAsync(x, 0, n * sizeof(double), s));
   HHG_TRY(launch_cheb0_bc(m, LL, f, nullptr, L.dinv, 1.0, r, z, s));  // r = f, z = PM dinv r
   HHG_CUDA(cudaMemcpyAsync(p, z, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  HHG_TRY(launch_dot_fused(m, LL, HHG_P2VEC, r, z, mg->scal + 0, s));
+  HHG_TRY(launch_dot_fused(m, LL, HHG_P2VEC, r, z, mg->scal + 0, s, mg->red));
   HHG_CUDA(cudaMemsetAsync(q, 0, n * sizeof(double), s));
   for (int it = 0; it < mg->prm.coarse_iters; ++it) {
     HHG_TRY(mg_apply(mg, l, p, q, s, true));
-    HHG_TRY(launch_dot_fused(m, LL, HHG_P2VEC, p, q, mg->scal + 1, s));
+    HHG_TRY(launch_dot_fused(m, LL, HHG_P2VEC, p, q, mg->scal + 1, s, mg->red));
     HHG_TRY(launch_pcg_update_bc(m, LL, it, mg->scal, x, r, p, q, L.dinv, z, s));
-    HHG_TRY(launch_dot_fused(m, LL, HHG_P2VEC, r, z, mg->scal + ((it & 1) ? 0 : 2), s));
+    HHG_TRY(launch_dot_fused(m, LL, HHG_P2VEC, r, z, mg->scal + ((it & 1) ? 0 : 2), s, mg->red));
     HHG_TRY(launch_pcg_dir_zero(n, it, mg->scal, z, p, q, s));
   }
   return HHG_OK;
@@ -261,7 +254,7 @@ static int mg_power(hhg_mg* mg, int l, double* v0, double* lam) {
     k_scale_dinv<<<vg(n), 256, 0, s>>>(n, L.t, L.dinv, L.t);
     count_launch();
     HHG_TRY(launch_fixup(m, LL, HHG_P2VEC, false, true, L.t, s));
-    HHG_TRY(launch_dot(m, LL, HHG_P2VEC, L.t, L.t, mg->scal + 8, s));
+    HHG_TRY(launch_dot(m, LL, HHG_P2VEC, L.t, L.t, mg->scal + 8, s, mg->red));
     k_normalize<<<vg(n), 256, 0, s>>>(n, mg->scal + 8, L.t, v0);
     count_launch();
   }
@@ -289,20 +282,15 @@ int hhg_mg_create_qeta(hhg_mesh* mesh, const hhg_mg_params* params, const double
     return fail(HHG_EINVAL, "hhg_mg_create: bad smoother parameters");
   auto* mg = new hhg_mg();
   mg->mesh = mesh;
-  {
-    const char* e = getenv("HHG_PERSISTENT_COARSE");
-    mg->no_persistent = !(e && e[0] == '1');
-  }
   mg->prm = P;
   mg->lv.resize(P.l_max + 1);
   auto bail = [&](int code) {
     delete mg;
     return code;
   };
+  ++mesh->dependents;
   if (cudaMalloc(&mg->scal, 16 * sizeof(double)) != cudaSuccess) return bail(fail(HHG_ENOMEM, "scal"));
-  if (cudaMalloc(&mg->cpart, 2 * std::max<int64_t>(1, macro_count(mesh)) * sizeof(double)) != cudaSuccess ||
-      cudaMalloc(&mg->cbar, 2 * sizeof(unsigned)) != cudaSuccess || cudaMemset(mg->cbar, 0, 2 * sizeof(unsigned)) != cudaSuccess)
-    return bail(fail(HHG_ENOMEM, "coarse PCG scratch"));
+  if (red_alloc(&mg->red) != HHG_OK) return bail(HHG_ENOMEM);
   for (int l = P.l_min; l <= P.l_max; ++l) {
     int r = ensure_level(mesh, l);
     if (r != HHG_OK) return bail(r);
@@ -460,7 +448,7 @@ int hhg_ablock_cg(hhg_mg* mg, const double* rhs, double* x, double tol, int max_
   double* sc = mg->cg_s;  // [0] r.z  [1] p.q  [2] r.z new  [3] r.r  [4] r0.r0
   HHG_CUDA(cudaMemsetAsync(x, 0, n * sizeof(double), s));
   HHG_CUDA(cudaMemcpyAsync(mg->cg_r, rhs, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  HHG_TRY(launch_dot(m, LL, HHG_P2VEC, mg->cg_r, mg->cg_r, sc + 4, s));
+  HHG_TRY(launch_dot(m, LL, HHG_P2VEC, mg->cg_r, mg->cg_r, sc + 4, s, mg->red));
   double r00 = 0.0;
   HHG_CUDA(cudaMemcpyAsync(&r00, sc + 4, sizeof(double), cudaMemcpyDeviceToHost, s));
   HHG_CUDA(cudaStreamSynchronize(s));
@@ -470,22 +458,22 @@ int hhg_ablock_cg(hhg_mg* mg, const double* rhs, double* x, double tol, int max_
   if (r0 > 0) {
     HHG_TRY(cg_precond(mg, s));
     HHG_CUDA(cudaMemcpyAsync(mg->cg_p, mg->cg_z, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    HHG_TRY(launch_dot(m, LL, HHG_P2VEC, mg->cg_r, mg->cg_z, sc + 0, s));
+    HHG_TRY(launch_dot(m, LL, HHG_P2VEC, mg->cg_r, mg->cg_z, sc + 0, s, mg->red));
     const unsigned nb = vg(n);
     while (it < max_iters) {
       ++it;
       HHG_TRY(mg_apply(mg, l, mg->cg_p, mg->cg_q, s));
-      HHG_TRY(launch_dot(m, LL, HHG_P2VEC, mg->cg_p, mg->cg_q, sc + 1, s));
+      HHG_TRY(launch_dot(m, LL, HHG_P2VEC, mg->cg_p, mg->cg_q, sc + 1, s, mg->red));
       k_cg_step<<<nb, 256, 0, s>>>(n, sc, x, mg->cg_r, mg->cg_p, mg->cg_q);
       count_launch();
-      HHG_TRY(launch_dot(m, LL, HHG_P2VEC, mg->cg_r, mg->cg_r, sc + 3, s));
+      HHG_TRY(launch_dot(m, LL, HHG_P2VEC, mg->cg_r, mg->cg_r, sc + 3, s, mg->red));
       double rr = 0.0;
       HHG_CUDA(cudaMemcpyAsync(&rr, sc + 3, sizeof(double), cudaMemcpyDeviceToHost, s));
       HHG_CUDA(cudaStreamSynchronize(s));
       rel = std::sqrt(std::max(rr, 0.0)) / r0;
       if (rel <= tol) break;
       HHG_TRY(cg_precond(mg, s));
-      HHG_TRY(launch_dot(m, LL, HHG_P2VEC, mg->cg_r, mg->cg_z, sc + 2, s));
+      HHG_TRY(launch_dot(m, LL, HHG_P2VEC, mg->cg_r, mg->cg_z, sc + 2, s, mg->red));
       k_cg_dir<<<nb, 256, 0, s>>>(n, sc, mg->cg_z, mg->cg_p);
       k_cg_roll<<<1, 32, 0, s>>>(sc);
       count_launch(2);
@@ -627,10 +615,11 @@ int hhg_power_iteration(const hhg_mesh* mesh, int level, const double* eta_p1, c
   cudaStream_t s = (cudaStream_t)stream;
   const Level& L = m->levels[level];
   const int64_t n = p2vec_len(m, level);
-  double *t = nullptr, *sc = nullptr;
+  double *t = nullptr, *sc = nullptr, *red = nullptr;
   if (cudaMalloc(&t, n * sizeof(double)) != cudaSuccess) return fail(HHG_ENOMEM, "power iteration workspace");
-  if (cudaMalloc(&sc, sizeof(double)) != cudaSuccess) {
+  if (cudaMalloc(&sc, sizeof(double)) != cudaSuccess || red_alloc(&red) != HHG_OK) {
     cudaFree(t);
+    if (sc) cudaFree(sc);
     return fail(HHG_ENOMEM, "power iteration workspace");
   }
   int r = HHG_OK;
@@ -641,7 +630,7 @@ int hhg_power_iteration(const hhg_mesh* mesh, int level, const double* eta_p1, c
       k_scale_dinv<<<vg(n), 256, 0, s>>>(n, t, dinv, t);
       count_launch();
       HHG_TRY(launch_fixup(m, L, HHG_P2VEC, false, true, t, s));
-      HHG_TRY(launch_dot(m, L, HHG_P2VEC, t, t, sc, s));
+      HHG_TRY(launch_dot(m, L, HHG_P2VEC, t, t, sc, s, red));
       k_normalize<<<vg(n), 256, 0, s>>>(n, sc, t, v0);
       count_launch();
     }
@@ -653,8 +642,10 @@ int hhg_power_iteration(const hhg_mesh* mesh, int level, const double* eta_p1, c
     return HHG_OK;
   };
   r = run();
+  cudaStreamSynchronize(s);
   cudaFree(t);
   cudaFree(sc);
+  cudaFree(red);
   return r;
 }
 
@@ -667,14 +658,28 @@ int hhg_power_iteration(const hhg_mesh* mesh, int level, const double* eta_p1, c
 // transfers, coarse Jacobi-PCG (fixed iteration count, device scalars).  No constraints; the constant
 // kernel is handled by projecting the outer CG's vectors to mean zero.
 namespace {
-__global__ void k_hash_fill(int64_t n, uint64_t seed, double* __restrict__ v) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    uint64_t z = (uint64_t)i + seed + 0x9E3779B97F4A7C15ull;
-    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-    z ^= z >> 31;
-    v[i] = (double)(z >> 11) * 0x1.0p-53 - 0.5;
-  }
+// Counter-based start vector of the K power iteration, keyed by canonical node identity (the harness
+// contract of SURVEY Appendix A2, implemented here independently of the input generators): the value at a
+// node does not depend on the storage layout, the partition or the level, so any implementation of the
+// method that keys its random numbers the same way draws the same start vector.
+uint64_t splitmix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+double keyed_uniform(const int64_t* key, uint64_t seed, int component) {
+  int64_t w[5] = {key[5], key[6], key[7], key[8], key[9]};  // weights (0 padded) and resolution
+  while (w[4] > 1 && !((w[0] | w[1] | w[2] | w[3] | w[4]) & 1))
+    for (auto& x : w) x /= 2;
+  const int dim = (int)key[0];
+  uint64_t h = seed;
+  h = splitmix64(h ^ (uint64_t)key[0]);
+  for (int c = 0; c < 4; ++c) h = splitmix64(h ^ (uint64_t)(c <= dim ? key[1 + c] : 0));
+  for (int c = 0; c < 4; ++c) h = splitmix64(h ^ (uint64_t)(c <= dim ? w[c] : 0));
+  h = splitmix64(h ^ (uint64_t)w[4]);
+  h = splitmix64(h ^ (uint64_t)component);
+  return 2.0 * ((double)(h >> 11) * 0x1.0p-53) - 1.0;
 }
 // PCG step with ping-pong r.z scalars (scal[0] / scal[2] by iteration parity, scal[1] = p.q), no BC
 __global__ void k_pcg_update_pp(int64_t n, int it, const double* __restrict__ scal, double* __restrict__ x,
@@ -708,12 +713,14 @@ struct hhg_kmg {
   };
   std::vector<Lv> lv;
   double* scal = nullptr;
+  double* red = nullptr;  // reduction scratch of this object
   double *cr = nullptr, *cz = nullptr, *cp = nullptr, *cq = nullptr;  // outer CG (finest level)
   ~hhg_kmg() {
+    if (mesh) --mesh->dependents;
     for (auto& L : lv)
       for (double* p : {L.x, L.f, L.r, L.d, L.t, L.dinv, L.p, L.ones})
         if (p) cudaFree(p);
-    for (double* p : {scal, cr, cz, cp, cq})
+    for (double* p : {scal, red, cr, cz, cp, cq})
       if (p) cudaFree(p);
   }
 };
@@ -725,7 +732,7 @@ int km_apply(hhg_kmg* K, int l, const double* u, double* y, cudaStream_t s) {
 }
 int km_mean0(hhg_kmg* K, int l, double* v, cudaStream_t s) {  // v -= mean over unique nodes (no sync)
   const Mesh* m = K->mesh;
-  HHG_TRY(launch_dot_fused(m, m->levels[l], HHG_P1, v, K->lv[l].ones, K->scal + 6, s));
+  HHG_TRY(launch_dot_fused(m, m->levels[l], HHG_P1, v, K->lv[l].ones, K->scal + 6, s, K->red));
   const int64_t n = p1_len(m, l);
   k_shift<<<vg(n), 256, 0, s>>>(n, K->scal + 6, K->lv[l].inv_count, v);
   count_launch();
@@ -763,13 +770,13 @@ int km_pcg(hhg_kmg* K, int l, const double* f, double* x, cudaStream_t s) {
   HHG_TRY(km_mean0(K, l, L.r, s));                                  // consistent singular system
   HHG_TRY(launch_pcg_scale(n, L.dinv, L.r, L.d, s));
   HHG_CUDA(cudaMemcpyAsync(L.p, L.d, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  HHG_TRY(launch_dot_fused(m, LL, HHG_P1, L.r, L.d, K->scal + 0, s));
+  HHG_TRY(launch_dot_fused(m, LL, HHG_P1, L.r, L.d, K->scal + 0, s, K->red));
   for (int it = 0; it < K->prm.coarse_iters; ++it) {
     HHG_TRY(km_apply(K, l, L.p, L.t, s));
-    HHG_TRY(launch_dot_fused(m, LL, HHG_P1, L.p, L.t, K->scal + 1, s));
+    HHG_TRY(launch_dot_fused(m, LL, HHG_P1, L.p, L.t, K->scal + 1, s, K->red));
     k_pcg_update_pp<<<vg(n), 256, 0, s>>>(n, it, K->scal, x, L.r, L.p, L.t, L.dinv, L.d);
     count_launch();
-    HHG_TRY(launch_dot_fused(m, LL, HHG_P1, L.r, L.d, K->scal + ((it & 1) ? 0 : 2), s));
+    HHG_TRY(launch_dot_fused(m, LL, HHG_P1, L.r, L.d, K->scal + ((it & 1) ? 0 : 2), s, K->red));
     HHG_TRY(launch_pcg_dir_zero(n, it, K->scal, L.d, L.p, L.t, s));
   }
   return HHG_OK;
@@ -790,19 +797,34 @@ int km_cycle(hhg_kmg* K, int l, const double* f, double* x, cudaStream_t s) {
   for (int i = 0; i < K->prm.post; ++i) HHG_TRY(km_cheb(K, l, x, f, false, s));
   return HHG_OK;
 }
-int km_power(hhg_kmg* K, int l) {  // lambda_max(D^-1 K) from a hashed consistent start vector
+int km_power(hhg_kmg* K, int l) {  // lambda_max(D^-1 K) from a keyed consistent start vector
   auto& L = K->lv[l];
   const Mesh* m = K->mesh;
   const Level& LL = m->levels[l];
   const int64_t n = p1_len(m, l);
   cudaStream_t s = nullptr;
-  k_hash_fill<<<vg(n), 256, 0, s>>>(n, 0x5eedull + (uint64_t)l, L.x);
-  count_launch();
-  HHG_TRY(launch_fixup(m, LL, HHG_P1, true, false, L.x, s));
+  {  // start vector U[-1,1) keyed by canonical node (seed kKPowerSeed), scattered to all copies
+    int64_t nc = 0;
+    HHG_TRY(canonical_count(m, LL.n1, &nc));
+    std::vector<int64_t> keys((size_t)nc * 10);
+    HHG_TRY(canonical_keys(m, LL.n1, keys.data()));
+    std::vector<double> v0((size_t)nc);
+    for (int64_t i = 0; i < nc; ++i) v0[i] = keyed_uniform(&keys[(size_t)10 * i], kKPowerSeed, 0);
+    HHG_TRY(ensure_canon(const_cast<Mesh*>(m), l, HHG_P1));
+    double* cdev = nullptr;
+    if (cudaMalloc(&cdev, std::max<int64_t>(nc, 1) * sizeof(double)) != cudaSuccess) return fail(HHG_ENOMEM, "kmg start");
+    int r = HHG_OK;
+    if (cudaMemcpy(cdev, v0.data(), nc * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess)
+      r = fail(HHG_ECUDA, "kmg start upload");
+    if (r == HHG_OK) r = launch_gather_canon(LL, HHG_P1, n, cdev, L.x, false, s);
+    if (r == HHG_OK && cudaDeviceSynchronize() != cudaSuccess) r = fail(HHG_ECUDA, "kmg start");
+    cudaFree(cdev);
+    HHG_TRY(r);
+  }
   for (int it = 0; it < K->prm.power_iters; ++it) {
     HHG_TRY(km_apply(K, l, L.x, L.t, s));
     k_scale_dinv<<<vg(n), 256, 0, s>>>(n, L.t, L.dinv, L.t);
-    HHG_TRY(launch_dot(m, LL, HHG_P1, L.t, L.t, K->scal + 8, s));
+    HHG_TRY(launch_dot(m, LL, HHG_P1, L.t, L.t, K->scal + 8, s, K->red));
     k_normalize<<<vg(n), 256, 0, s>>>(n, K->scal + 8, L.t, L.x);
     count_launch(2);
   }
@@ -817,11 +839,11 @@ int km_power(hhg_kmg* K, int l) {  // lambda_max(D^-1 K) from a hashed consisten
 int dev_pcg(const Mesh* m, const Level& LL, int space, int64_t n, const std::function<int(const double*, double*)>& op,
             const std::function<int(const double*, double*)>& prec, const std::function<int(double*)>& proj,
             const double* rhs, double* x, double tol, double tol_abs, int max_iters, double* r, double* z, double* p,
-            double* q, double* sc, cudaStream_t s, int* iters_out, double* rel_out) {
+            double* q, double* sc, double* red, cudaStream_t s, int* iters_out, double* rel_out) {
   HHG_CUDA(cudaMemsetAsync(x, 0, n * sizeof(double), s));
   HHG_CUDA(cudaMemcpyAsync(r, rhs, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
   if (proj) HHG_TRY(proj(r));
-  HHG_TRY(launch_dot(m, LL, space, r, r, sc + 3, s));
+  HHG_TRY(launch_dot(m, LL, space, r, r, sc + 3, s, red));
   double r0 = 0.0;
   HHG_CUDA(cudaMemcpyAsync(&r0, sc + 3, sizeof(double), cudaMemcpyDeviceToHost, s));
   HHG_CUDA(cudaStreamSynchronize(s));
@@ -832,15 +854,15 @@ int dev_pcg(const Mesh* m, const Level& LL, int space, int64_t n, const std::fun
     HHG_TRY(prec(r, z));
     if (proj) HHG_TRY(proj(z));
     HHG_CUDA(cudaMemcpyAsync(p, z, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    HHG_TRY(launch_dot(m, LL, space, r, z, sc + 0, s));
+    HHG_TRY(launch_dot(m, LL, space, r, z, sc + 0, s, red));
     const unsigned nb = vg(n);
     while (it < max_iters) {
       ++it;
       HHG_TRY(op(p, q));
-      HHG_TRY(launch_dot(m, LL, space, p, q, sc + 1, s));
+      HHG_TRY(launch_dot(m, LL, space, p, q, sc + 1, s, red));
       k_cg_step<<<nb, 256, 0, s>>>(n, sc, x, r, p, q);
       count_launch();
-      HHG_TRY(launch_dot(m, LL, space, r, r, sc + 3, s));
+      HHG_TRY(launch_dot(m, LL, space, r, r, sc + 3, s, red));
       double rr = 0.0;
       HHG_CUDA(cudaMemcpyAsync(&rr, sc + 3, sizeof(double), cudaMemcpyDeviceToHost, s));
       HHG_CUDA(cudaStreamSynchronize(s));
@@ -849,7 +871,7 @@ int dev_pcg(const Mesh* m, const Level& LL, int space, int64_t n, const std::fun
       if (rel <= tol || rn <= tol_abs) break;
       HHG_TRY(prec(r, z));
       if (proj) HHG_TRY(proj(z));
-      HHG_TRY(launch_dot(m, LL, space, r, z, sc + 2, s));
+      HHG_TRY(launch_dot(m, LL, space, r, z, sc + 2, s, red));
       k_cg_dir<<<nb, 256, 0, s>>>(n, sc, z, p);
       k_cg_roll<<<1, 32, 0, s>>>(sc);
       count_launch(2);
@@ -882,8 +904,10 @@ int hhg_kmg_create(hhg_mesh* mesh, const hhg_mg_params* params, const double* co
     delete K;
     return code;
   };
+  ++mesh->dependents;
   if (cudaMalloc(&K->scal, 16 * sizeof(double)) != cudaSuccess || cudaMemset(K->scal, 0, 16 * sizeof(double)) != cudaSuccess)
     return bail(fail(HHG_ENOMEM, "kmg scal"));
+  if (red_alloc(&K->red) != HHG_OK) return bail(HHG_ENOMEM);
   const int64_t nf = p1_len(mesh, P.l_max);
   for (double** p : {&K->cr, &K->cz, &K->cp, &K->cq})
     if (cudaMalloc(p, std::max<int64_t>(nf, 1) * sizeof(double)) != cudaSuccess) return bail(fail(HHG_ENOMEM, "kmg cg"));
@@ -896,7 +920,7 @@ int hhg_kmg_create(hhg_mesh* mesh, const hhg_mg_params* params, const double* co
     for (double** p : {&L.x, &L.f, &L.r, &L.d, &L.t, &L.dinv, &L.p, &L.ones})
       if (cudaMalloc(p, std::max<int64_t>(n, 1) * sizeof(double)) != cudaSuccess) return bail(fail(HHG_ENOMEM, "kmg vectors"));
     r = launch_fill(n, 1.0, L.ones, nullptr);
-    if (r == HHG_OK) r = launch_dot(mesh, mesh->levels[l], HHG_P1, L.ones, L.ones, K->scal + 9, nullptr);
+    if (r == HHG_OK) r = launch_dot(mesh, mesh->levels[l], HHG_P1, L.ones, L.ones, K->scal + 9, nullptr, K->red);
     double cnt = 0.0;
     if (r == HHG_OK && cudaMemcpy(&cnt, K->scal + 9, sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess)
       r = fail(HHG_ECUDA, "kmg count");
@@ -923,7 +947,7 @@ int hhg_kmg_solve(hhg_kmg* K, const double* rhs, double* x, double tol, double t
   auto prec = [&](const double* r, double* z) { return km_cycle(K, lf, r, z, s); };
   auto proj = [&](double* v) { return km_mean0(K, lf, v, s); };
   return dev_pcg(m, m->levels[lf], HHG_P1, p1_len(m, lf), op, prec, proj, rhs, x, tol, tol_abs, max_iters, K->cr,
-                 K->cz, K->cp, K->cq, K->scal + 10, s, iters, rel_res);
+                 K->cz, K->cp, K->cq, K->scal + 10, K->red, s, iters, rel_res);
 }
 
 int hhg_kmg_destroy(hhg_kmg* K) {
@@ -951,6 +975,7 @@ struct hhg_stokes {
   int64_t n2 = 0, n1 = 0;
   std::vector<double*> V, Z;
   double *w = nullptr, *t = nullptr, *a = nullptr, *b = nullptr, *ones = nullptr, *mdinv = nullptr, *sc = nullptr;
+  double* red = nullptr;  // reduction scratch of this object
   double *mr = nullptr, *mz = nullptr, *mp = nullptr, *mq = nullptr;
   double *br = nullptr, *bz = nullptr, *bp = nullptr, *bq = nullptr, *bt = nullptr;  // BFBT CG (P1)
   double *bu = nullptr, *bv = nullptr;                                                 // BFBT velocity temps
@@ -962,7 +987,8 @@ struct hhg_stokes {
   ~hhg_stokes() {
     for (double* p : V) cudaFree(p);
     for (double* p : Z) cudaFree(p);
-    for (double* p : {w, t, a, b, ones, mdinv, sc, mr, mz, mp, mq, br, bz, bp, bq, bt, bu, bv, vdl, vdr, vr, vz, vp, vq})
+    if (mesh) --mesh->dependents;
+    for (double* p : {w, t, a, b, ones, mdinv, sc, red, mr, mz, mp, mq, br, bz, bp, bq, bt, bu, bv, vdl, vdr, vr, vz, vp, vq})
       if (p) cudaFree(p);
     if (kr && kr != kl) delete kr;
     if (kl) delete kl;
@@ -975,8 +1001,8 @@ int st_dot(hhg_stokes* S, const double* x, const double* y, int what, double* ou
   const Mesh* m = S->mesh;
   const Level& L = m->levels[S->level];
   double h[2] = {0.0, 0.0};
-  if (what & 1) HHG_TRY(launch_dot(m, L, HHG_P2VEC, x, y, S->sc + 0, s));
-  if (what & 2) HHG_TRY(launch_dot(m, L, HHG_P1, x + S->n2, y + S->n2, S->sc + 1, s));
+  if (what & 1) HHG_TRY(launch_dot(m, L, HHG_P2VEC, x, y, S->sc + 0, s, S->red));
+  if (what & 2) HHG_TRY(launch_dot(m, L, HHG_P1, x + S->n2, y + S->n2, S->sc + 1, s, S->red));
   HHG_CUDA(cudaMemcpyAsync(h, S->sc, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
   HHG_CUDA(cudaStreamSynchronize(s));
   *out = ((what & 1) ? h[0] : 0.0) + ((what & 2) ? h[1] : 0.0);
@@ -986,7 +1012,7 @@ int st_dot(hhg_stokes* S, const double* x, const double* y, int what, double* ou
 int st_mean0(hhg_stokes* S, double* p, cudaStream_t s) {  // P_p: arithmetic mean zero over unique nodes
   // device-only: fused owner-masked sum, then p -= sum / n_unique read on the device (no host sync)
   const Level& L = S->mesh->levels[S->level];
-  HHG_TRY(launch_dot_fused(S->mesh, L, HHG_P1, p, S->ones, S->sc + 2, s));
+  HHG_TRY(launch_dot_fused(S->mesh, L, HHG_P1, p, S->ones, S->sc + 2, s, S->red));
   k_shift<<<vg(S->n1), 256, 0, s>>>(S->n1, S->sc + 2, 1.0 / S->n_unique_p, p);
   count_launch();
   return HHG_OK;
@@ -1006,7 +1032,7 @@ int st_mass_solve(hhg_stokes* S, const double* rp, double* zp, cudaStream_t s) {
   int it;
   double rel;
   return dev_pcg(m, L, HHG_P1, S->n1, op, jac, std::function<int(double*)>(), rp, zp, S->prm.tol_mass, 0.0,
-                 S->prm.mass_max_iters, S->mr, S->mz, S->mp, S->mq, S->sc + 8, s, &it, &rel);
+                 S->prm.mass_max_iters, S->mr, S->mz, S->mp, S->mq, S->sc + 8, S->red, s, &it, &rel);
 }
 // w = P_p B A_C^-1 B^T y  (A_C^-1 = one cheap V-cycle, eq:schurV)
 int st_bacbt(hhg_stokes* S, const double* y, double* w, cudaStream_t s) {
@@ -1026,7 +1052,7 @@ int st_bacbt_solve(hhg_stokes* S, const double* t, double* y, cudaStream_t s) {
   int it;
   double rel;
   return dev_pcg(m, L, HHG_P1, S->n1, op, prec, proj, t, y, S->prm.tol_vbfbt, 0.0, S->prm.vbfbt_max_iters, S->br,
-                 S->bz, S->bp, S->bq, S->sc + 12, s, &it, &rel);
+                 S->bz, S->bp, S->bq, S->sc + 12, S->red, s, &it, &rel);
 }
 // z_p = S_V^-1 t (eq:schurV): (B A_C^-1 B^T)^-1 (B A_C^-1 A A_C^-1 B^T) (B A_C^-1 B^T)^-1 t
 int st_vbfbt(hhg_stokes* S, const double* t, double* z, cudaStream_t s) {
@@ -1052,7 +1078,7 @@ int st_vmass_solve(hhg_stokes* S, double a, const double* vdinv, const double* v
   int it;
   double rel;
   return dev_pcg(m, L, HHG_P2VEC, S->n2, op, prec, std::function<int(double*)>(), v, x, S->prm.tol_vmass, 0.0,
-                 S->prm.vmass_max_iters, S->vr, S->vz, S->vp, S->vq, S->sc + 16, s, &it, &rel);
+                 S->prm.vmass_max_iters, S->vr, S->vz, S->vp, S->vq, S->sc + 16, S->red, s, &it, &rel);
 }
 // z = S_w^-1 t (eq:schurWBFBT with a_l / a_r):
 //   K_{1/sqrt(eta_l)}^-1 B M_{sqrt(eta_l)}^-1 A M_{sqrt(eta_r)}^-1 B^T K_{1/sqrt(eta_r)}^-1 t
@@ -1156,7 +1182,8 @@ int hhg_stokes_create(hhg_mg* mg, hhg_mg* mg_cheap, const double* eta_p1, double
   for (double** p : {&S->bu, &S->bv}) ok = ok && alloc(p, S->n2);
   if (prm->schur == 2)
     for (double** p : {&S->vdl, &S->vdr, &S->vr, &S->vz, &S->vp, &S->vq}) ok = ok && alloc(p, S->n2);
-  ok = ok && alloc(&S->sc, 32);
+  ok = ok && alloc(&S->sc, 32) && red_alloc(&S->red) == HHG_OK;
+  ++S->mesh->dependents;
   if (!ok) {
     delete S;
     return fail(HHG_ENOMEM, "hhg_stokes_create: workspace");
@@ -1168,7 +1195,7 @@ int hhg_stokes_create(hhg_mg* mg, hhg_mg* mg_cheap, const double* eta_p1, double
     HHG_TRY(launch_fill(S->n1, 1.0, S->ones, s));
     HHG_TRY(hhg_mass_diag(S->mesh, S->level, S->eta, S->mdinv, nullptr));
     HHG_TRY(launch_recip(S->n1, S->mdinv, s));
-    HHG_TRY(launch_dot(S->mesh, L, HHG_P1, S->ones, S->ones, S->sc + 4, s));
+    HHG_TRY(launch_dot(S->mesh, L, HHG_P1, S->ones, S->ones, S->sc + 4, s, S->red));
     HHG_CUDA(cudaMemcpy(&S->n_unique_p, S->sc + 4, sizeof(double), cudaMemcpyDeviceToHost));
     if (prm->schur == 2) {
       std::vector<const double*> etas(mg->prm.l_max + 1, nullptr);
@@ -1405,10 +1432,12 @@ struct hhg_temp_solver {
   std::vector<double*> V, Z;
   double *w = nullptr, *td = nullptr, *bp = nullptr, *dl = nullptr, *dinv = nullptr, *t1 = nullptr;
   double *cr = nullptr, *cz = nullptr, *cp = nullptr, *cq = nullptr, *sc = nullptr;
+  double* red = nullptr;  // reduction scratch of this object
   ~hhg_temp_solver() {
+    if (mesh) --mesh->dependents;
     for (double* p : V) cudaFree(p);
     for (double* p : Z) cudaFree(p);
-    for (double* p : {w, td, bp, dl, dinv, t1, cr, cz, cp, cq, sc})
+    for (double* p : {w, td, bp, dl, dinv, t1, cr, cz, cp, cq, sc, red})
       if (p) cudaFree(p);
   }
 };
@@ -1442,7 +1471,8 @@ int hhg_temp_solver_create(hhg_mesh* mesh, int level, const hhg_temp_params* prm
   for (auto& p : S->V) ok = ok && alloc(&p);
   for (auto& p : S->Z) ok = ok && alloc(&p);
   for (double** p : {&S->w, &S->td, &S->bp, &S->dl, &S->dinv, &S->t1, &S->cr, &S->cz, &S->cp, &S->cq}) ok = ok && alloc(p);
-  ok = ok && cudaMalloc(&S->sc, 16 * sizeof(double)) == cudaSuccess;
+  ok = ok && cudaMalloc(&S->sc, 16 * sizeof(double)) == cudaSuccess && red_alloc(&S->red) == HHG_OK;
+  ++mesh->dependents;
   if (!ok) {
     delete S;
     return fail(HHG_ENOMEM, "hhg_temp_solver_create: workspace");
@@ -1472,7 +1502,7 @@ int hhg_temp_solve(hhg_temp_solver* S, const double* u, const double* b, double*
     return HHG_OK;
   };
   auto dot = [&](const double* x, const double* y, double* out) -> int {
-    HHG_TRY(launch_dot(m, L, HHG_P2, x, y, S->sc + 8, s));
+    HHG_TRY(launch_dot(m, L, HHG_P2, x, y, S->sc + 8, s, S->red));
     HHG_CUDA(cudaMemcpyAsync(out, S->sc + 8, sizeof(double), cudaMemcpyDeviceToHost, s));
     HHG_CUDA(cudaStreamSynchronize(s));
     return HHG_OK;
@@ -1493,7 +1523,7 @@ int hhg_temp_solve(hhg_temp_solver* S, const double* u, const double* b, double*
     int it;
     double rel;
     return dev_pcg(m, L, HHG_P2, n, opP, jac, std::function<int(double*)>(), r, z, tol_cg, 0.0, cg_max_iters, S->cr,
-                   S->cz, S->cp, S->cq, S->sc, s, &it, &rel);
+                   S->cz, S->cp, S->cq, S->sc, S->red, s, &it, &rel);
   };
   // T_D on the boundary, b' = mask_int(b - L T_D)
   HHG_TRY(mask(T, S->td, 1));

@@ -247,3 +247,32 @@ def test_quadrature_point_viscosity_tier_special_cases():
     assert abs(dq.A - dp.A).max() <= 1e-13 * abs(dp.A).max()
     dj = Discretisation(lm, True, None, 0.0, {}, build=("A",), T_p2=T, qeta=(lnC, 30.0, 2.0))
     assert abs(dj.A - 30.0 * dq.A).max() <= 1e-13 * abs(dj.A).max()
+
+
+def test_sampled_rows_equal_assembled_rows_shell_level2():
+    """Pin of sampled_rows (the checker of every full-size parity test): on the blended shell at L2 with
+    the TALA term (gamma = 0.3781), config-2 viscosity and constraints, its rows at nodes sampled on macro
+    vertices, edges, faces and cells equal the rows of the fully assembled Discretisation."""
+    from oracle.refine import build_level, node_bc
+    from oracle.operators import Discretisation, node_coords, sampled_rows
+    from workload import icoshell, uniform_vec, uniform_from_keys, viscosity, GAMMA_TALA
+    mac = icoshell(3, 2)
+    lm = build_level(mac.verts, mac.tets, mac.vtag, 2)
+    bc_tags = {2: 1, 1: 2}
+    eta = viscosity(node_coords(lm, "P1", True), lm.p1_keys, 1e4, 10.0)
+    d = Discretisation(lm, True, eta, GAMMA_TALA, bc_tags)
+    u = d.project(uniform_vec(lm.p2_keys, 2))
+    p = uniform_from_keys(lm.p1_keys, 3, 0)
+    yu_full = d.apply_A(u) + d.apply_BT(p)
+    yp_full = d.apply_Bbar(u)
+    rng = np.random.default_rng(3)
+    s2 = np.unique(np.concatenate([np.nonzero(lm.p2_keys[:, 0] == dim)[0][rng.integers(0, 10**9, 25) %
+                                   np.count_nonzero(lm.p2_keys[:, 0] == dim)] for dim in range(4)]))
+    s1 = np.unique(np.concatenate([np.nonzero(lm.p1_keys[:, 0] == dim)[0][rng.integers(0, 10**9, 15) %
+                                   np.count_nonzero(lm.p1_keys[:, 0] == dim)] for dim in range(4)]))
+    assert {int(k) for k in lm.p2_keys[s2, 0]} == {0, 1, 2, 3}
+    bc = node_bc(lm.p2_keys, lm.macro_tets, lm.macro_vtag, bc_tags)
+    yu_s, yp_s = sampled_rows(lm, True, eta, GAMMA_TALA, u, p, s2, s1, bc)
+    r2 = (3 * s2[:, None] + np.arange(3)).ravel()
+    assert np.linalg.norm(yu_s[r2] - yu_full[r2]) <= 1e-13 * np.linalg.norm(yu_full[r2])
+    assert np.linalg.norm(yp_s[s1] - yp_full[s1]) <= 1e-13 * np.linalg.norm(yp_full[s1])
