@@ -11,8 +11,10 @@ order.
   S^-1: M_{1/eta}^-1 by Jacobi-preconditioned CG to tol_mass (eq:schurMass).
   schur="wbfbt": the weighted BFBT with the a_l / a_r surface scaling (eq:schurWBFBT),
       S_w^-1 = K_l^-1 (B VM_l^-1 A VM_r^-1 B^T) K_r^-1,
-  K = K_{1/sqrt(eta_a)} (Neumann, solved exactly on the mean-zero space), VM = M_{sqrt(eta_a)} (solved
-  exactly on the constrained velocity space) -- the library solves both iteratively to tolerance.
+  K = K_{1/sqrt(eta_a)} (Neumann, mean-zero space), VM = M_{sqrt(eta_a)} (constrained velocity space),
+  either solved exactly (direct factorisations: pins of the approximation itself) or -- wbfbt_iter --
+  iteratively as the method prescribes (oracle/kmg.py: GMG-preconditioned CG for K to tol_wBFBT,
+  Jacobi CG for VM to tol_VM, Table 1; readings R23, R24).
 Readings (R17-R19): P_p applied to the rhs, to every operator output and to the
 preconditioned pressure; relative residual stopping; Table 1 defaults (sigma 1, omega 0.3,
 tol_A 1e-2, tol_mass 1e-10).
@@ -90,9 +92,12 @@ class StokesOracle:
 
     def __init__(self, H: Hierarchy, disc, Mmass, sigma=1.0, omega=0.3, tol_A=1e-2, ablock_max_iters=200,
                  tol_mass=1e-10, mass_max_iters=500, schur="mass", HC: Hierarchy = None, tol_vbfbt=1e-1,
-                 vbfbt_max_iters=100, uzawa="symmetric", wbfbt_ops=None):
-        """wbfbt_ops = (K_l, K_r, VM_l, VM_r) for schur="wbfbt"."""
+                 vbfbt_max_iters=100, uzawa="symmetric", wbfbt_ops=None, wbfbt_iter=None):
+        """wbfbt_ops = (K_l, K_r, VM_l, VM_r) for schur="wbfbt" (direct inner solves); wbfbt_iter = dict(Kl, Kr
+        (oracle.kmg.KHierarchy), VMl, VMr, tol_wbfbt, tol_wbfbt_abs, wbfbt_max_iters, tol_vmass,
+        vmass_max_iters) for the iterative inner solves of the method."""
         self.wb = wbfbt_ops
+        self.wbi = wbfbt_iter
         self.schur, self.HC, self.tol_vbfbt, self.vbfbt_max_iters = schur, HC, tol_vbfbt, vbfbt_max_iters
         self.uzawa = uzawa
         self.H, self.d = H, disc
@@ -148,6 +153,14 @@ class StokesOracle:
 
     def wbfbt(self, t):
         """S_w^-1 t = K_l^-1 (B VM_l^-1 A VM_r^-1 B^T) K_r^-1 t."""
+        if self.wbi is not None:
+            from .kmg import vmass_solve
+            w = self.wbi
+            y = w["Kr"].solve(mean0(t), w["tol_wbfbt"], w["tol_wbfbt_abs"], w["wbfbt_max_iters"])[0]
+            v = vmass_solve(w["VMr"], self.Pm, self.Pm @ (self.B.T @ y), w["tol_vmass"], w["vmass_max_iters"])[0]
+            v = vmass_solve(w["VMl"], self.Pm, self.A @ v, w["tol_vmass"], w["vmass_max_iters"])[0]
+            return w["Kl"].solve(mean0(self.B @ (self.Pm @ v)), w["tol_wbfbt"], w["tol_wbfbt_abs"],
+                                 w["wbfbt_max_iters"])[0]
         Kl, Kr, VMl, VMr = self.wb
         y = neumann_solve(Kr, mean0(t))
         w = constrained_solve(VMr, self.Pm, self.Pm @ (self.B.T @ y))

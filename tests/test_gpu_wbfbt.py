@@ -128,6 +128,87 @@ def test_wbfbt_schur_apply(shell, a):
     assert rel_l2(canon(M, 2, hhg.HHG_P1, z), z_o) <= 1e-8
 
 
+def _khier(discs, a, pre=3, post=3, degree=3):
+    """Oracle K_{1/sqrt(eta_a)} GMG hierarchy on the A hierarchy's levels (reading R23)."""
+    from oracle.kmg import KHierarchy, K_POWER_SEED
+    from oracle.operators import Discretisation
+    Ks, lms, v0 = {}, {}, {}
+    for L, d in discs.items():
+        dk = Discretisation(d.lm, True, d.eta_p1, 0.0, oracle_bc(BC_SHELL), build=("K",), surf_a=a)
+        Ks[L], lms[L], v0[L] = dk.K, d.lm, uniform_from_keys(d.lm.p1_keys, K_POWER_SEED, 0)
+    return KHierarchy(Ks, lms, v0, pre=pre, post=post, degree=degree, power_iters=20, coarse_iters=50)
+
+
+@pytest.mark.parametrize("a,L", [(1.0, 2), (3.0, 3)])
+def test_kmg_solve_matches_oracle_gmg_cg(shell, a, L):
+    """The library's K solve runs the method's algorithm (reading R23) step by step: the oracle's
+    GMG-preconditioned CG (same hierarchy, smoother, keyed power start, coarse PCG, tolerances) takes the
+    same number of iterations and returns the same solution (<= 1e-9)."""
+    discs = {}
+    for l in range(1, L + 1):
+        lm, d, _ = oracle_case(shell, l, True, BC_SHELL, C2, build=())
+        discs[l] = d
+    KH = _khier(discs, a)
+    t_o = uniform_from_keys(discs[L].lm.p1_keys, 3, 0)
+    y_o, it_o, rel_o = KH.solve(t_o, 1e-8, 0.0, 100)
+    M = lib_mesh(shell, L, True, BC_SHELL)
+    etas = {l: lib_eta(M, l, C2) for l in range(1, L + 1)}
+    K = hhg.KMG(M, 1, L, etas, a=a)
+    y, it, rel = K.solve(lib_p(M, L, 3), tol=1e-8, max_iters=100)
+    assert it == it_o and abs(rel - rel_o) <= 1e-6 * rel_o, (it, it_o, rel, rel_o)
+    assert rel_l2(canon(M, L, hhg.HHG_P1, y), y_o) <= 1e-9
+
+
+TABLE1_WBFBT = dict(tol_wbfbt=1e-10, tol_wbfbt_abs=1e-10, wbfbt_max_iters=100, tol_vmass=1e-4, vmass_max_iters=500)
+
+
+def _oracle_wbfbt_iter(H, discs, d, a):
+    from oracle.operators import Discretisation
+    KL = _khier(discs, a[0])
+    KR = KL if a[1] == a[0] else _khier(discs, a[1])
+    vml = Discretisation(d.lm, True, d.eta_p1, 0.0, oracle_bc(BC_SHELL), build=("VM",), surf_a=a[0]).VM
+    vmr = vml if a[1] == a[0] else Discretisation(d.lm, True, d.eta_p1, 0.0, oracle_bc(BC_SHELL), build=("VM",),
+                                                  surf_a=a[1]).VM
+    return dict(Kl=KL, Kr=KR, VMl=vml, VMr=vmr, **TABLE1_WBFBT)
+
+
+@pytest.mark.parametrize("a", [(1.0, 1.0), (2.0, 0.5)])
+def test_wbfbt_schur_apply_table1_tolerances(shell, a):
+    """S_w^-1 t with the paper's inner tolerances (Table 1: tol_wBFBT = 1e-10, tol_VM = 1e-4) against the
+    oracle running the same iterative inner solves: <= 1e-8."""
+    from oracle.multigrid import Hierarchy
+    from oracle.stokes import StokesOracle
+    H, d, ops, M, etas, mg = _stokes_case(shell, C2, a=a)
+    discs = {1: oracle_case(shell, 1, True, BC_SHELL, C2, build=())[1], 2: d}
+    S_o = StokesOracle(H, d, d.M, schur="wbfbt", wbfbt_iter=_oracle_wbfbt_iter(H, discs, d, a))
+    t_o = uniform_from_keys(d.lm.p1_keys, 3, 0)
+    z_o = S_o.wbfbt(t_o - t_o.mean())
+    S = hhg.StokesSolver(mg, etas[2], GAMMA_TALA, schur="wbfbt", a_l=a[0], a_r=a[1], **TABLE1_WBFBT)
+    z = S.schur_apply(lib_p(M, 2, 3))
+    assert rel_l2(canon(M, 2, hhg.HHG_P1, z), z_o) <= 1e-8
+
+
+def test_stokes_fgmres_wbfbt_solve_table1(shell):
+    """FGMRES + symmetric Uzawa with S_w and the paper's inner tolerances, against the oracle running the
+    same iterative inner solves: same iteration count and residual history, solutions <= 1e-8."""
+    from oracle.stokes import StokesOracle
+    H, d, ops, M, etas, mg = _stokes_case(shell, C2)
+    discs = {1: oracle_case(shell, 1, True, BC_SHELL, C2, build=())[1], 2: d}
+    S_o = StokesOracle(H, d, d.M, sigma=1.0, omega=0.3, tol_A=1e-2, schur="wbfbt",
+                       wbfbt_iter=_oracle_wbfbt_iter(H, discs, d, (1.0, 1.0)))
+    rhs_o = np.concatenate([uniform_vec(d.lm.p2_keys, 2), uniform_from_keys(d.lm.p1_keys, 3, 0)])
+    x_o, it_o, rel_o = S_o.solve(rhs_o, tol=1e-6, restart=60, max_iters=60)
+    S = hhg.StokesSolver(mg, etas[2], GAMMA_TALA, restart=60, max_iters=60, tol=1e-6, sigma=1.0, omega=0.3,
+                         tol_A=1e-2, schur="wbfbt", **TABLE1_WBFBT)
+    ru = M.from_canonical(2, hhg.HHG_P2VEC, uniform_vec(M.canonical_keys(2, hhg.HHG_P2), 2))
+    rhs = torch.cat([ru, lib_p(M, 2, 3)])
+    x, it, rel = S.solve(rhs)
+    n2 = M.vec_len(2, hhg.HHG_P2VEC)
+    xc = np.concatenate([canon(M, 2, hhg.HHG_P2VEC, x[:n2].contiguous()), canon(M, 2, hhg.HHG_P1, x[n2:].contiguous())])
+    assert it == it_o and abs(rel - rel_o) <= 1e-6 * rel_o, (it, it_o, rel, rel_o)
+    assert rel_l2(xc, x_o) <= 1e-8, rel_l2(xc, x_o)
+
+
 def test_stokes_fgmres_wbfbt_solve(shell):
     """FGMRES + symmetric Uzawa with S_w (tight inner solves): same iteration count and residual history as
     the oracle with exact inner solves.  The library's inner K / M solves stop at 1e-13 / 1e-14 while the

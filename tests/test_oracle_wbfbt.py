@@ -166,3 +166,51 @@ def test_fgmres_wbfbt_recovers_a_manufactured_solution(shell_case, a):
     x, it, rel = S.solve(rhs, tol=1e-9, restart=60, max_iters=200)
     assert rel <= 1e-9
     assert np.linalg.norm(x[:n2] - xs[:n2]) <= 1e-7 * np.linalg.norm(xs[:n2])
+
+
+def _k_levels(a, levels=(1, 2)):
+    from workload import viscosity
+    from oracle.operators import node_coords
+    m = icoshell(3, 2)
+    out = {}
+    for L in levels:
+        lm = build_level(m.verts, m.tets, m.vtag, L)
+        eta = viscosity(node_coords(lm, "P1", True), lm.p1_keys, 1e4, 10.0)
+        out[L] = (lm, Discretisation(lm, True, eta, 0.0, {2: BC_DIRICHLET, 1: 2}, build=("K", "VM"), surf_a=a))
+    return out
+
+
+@pytest.mark.parametrize("a", [1.0, 3.0])
+def test_kmg_cg_converges_to_the_direct_neumann_solution(a):
+    """oracle.kmg (reading R23) pinned to the direct mean-zero solve: the GMG-preconditioned CG driven to
+    1e-13 reproduces neumann_solve to 1e-10, in few (level-robust multigrid) iterations; the power
+    iteration's lambda_hat lies within 5% below the dense lambda_max(D^-1 K) of the finest level."""
+    from oracle.kmg import KHierarchy, K_POWER_SEED, mean0
+    lv = _k_levels(a)
+    KH = KHierarchy({L: d.K for L, (lm, d) in lv.items()}, {L: lm for L, (lm, d) in lv.items()},
+                    {L: uniform_from_keys(lm.p1_keys, K_POWER_SEED, 0) for L, (lm, d) in lv.items()})
+    lm, d = lv[2]
+    t = mean0(uniform_from_keys(lm.p1_keys, 3, 0))
+    y, it, rel = KH.solve(t, 1e-13, 0.0, 100)
+    y_d = neumann_solve(d.K, t)
+    assert rel <= 1e-13 and it <= 30
+    assert np.linalg.norm(y - y_d) <= 1e-10 * np.linalg.norm(y_d)
+    Kd = d.K.toarray()
+    dinv = 1.0 / np.diag(Kd)
+    lmax = float(np.max(np.real(np.linalg.eigvals(dinv[:, None] * Kd))))
+    assert 0.95 * lmax <= KH.lam[2] <= lmax * (1 + 1e-12)
+
+
+def test_vmass_cg_converges_to_the_direct_constrained_solution():
+    """oracle.kmg.vmass_solve (reading R24) pinned to the direct constrained solve at tight tolerance."""
+    from oracle.kmg import vmass_solve
+    from oracle.stokes import constrained_solve
+    lm, d = _k_levels(2.0, levels=(1,))[1]
+    from oracle.refine import node_bc
+    from oracle.operators import constraint_matrix
+    Pm = constraint_matrix(lm.p2_xt, node_bc(lm.p2_keys, lm.macro_tets, lm.macro_vtag, {2: BC_DIRICHLET, 1: 2}))
+    v = Pm @ uniform_vec(lm.p2_keys, 5)
+    x, it, rel = vmass_solve(d.VM, Pm, v, 1e-14, 2000)
+    x_d = constrained_solve(d.VM, Pm, v)
+    assert rel <= 1e-14
+    assert np.linalg.norm(x - x_d) <= 1e-9 * np.linalg.norm(x_d)
