@@ -182,6 +182,10 @@ def main():
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
+        # communicator set-up lines (ranks, channels, NVLS) on stderr, so the driver can check nranks
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2506_04157_b200 as hhg

@@ -97,6 +97,22 @@ int hhg_comm_unique_id(uint8_t id[128]);
 int hhg_comm_create(const uint8_t id[128], int nranks, int rank, int device, hhg_comm** out);
 int hhg_comm_destroy(hhg_comm* comm);
 
+/* Host-staged transport (P:689-709 multi-process decomposition, without NCCL): the library drains the
+ * stream, copies its send buffer to pinned host memory and calls
+ *   exchange(user, n_nbr, nbr[n_nbr], off[n_nbr+1], nc, send, recv): for every neighbour rank nbr[i],
+ *     send the doubles send[off[i]*nc .. off[i+1]*nc) to it and receive its block of the same length
+ *     into recv[off[i]*nc ..) (both sides list the shared nodes in the same canonical order);
+ *     called on EVERY rank for every interface sum (n_nbr may be 0), so it may be collective;
+ *   allreduce(user, buf, n): in-place elementwise sum of n doubles over all ranks;
+ * both return 0 on success.  Then the received data is copied back.  Any number of ranks may share
+ * one GPU (no kernel waits on another rank).  Hot calls synchronise their stream, so objects using
+ * such a communicator never capture CUDA graphs.  Errors: HHG_ENCCL if a callback fails. */
+typedef int (*hhg_exchange_fn)(void* user, int n_nbr, const int* nbr, const int64_t* off, int nc, const double* send,
+                               double* recv);
+typedef int (*hhg_allreduce_fn)(void* user, double* buf, int64_t n);
+int hhg_comm_create_host(int nranks, int rank, hhg_exchange_fn exchange, hhg_allreduce_fn allreduce, void* user,
+                         hhg_comm** out);
+
 /* ------------------------------------------------------------------ mesh
  * hhg_mesh_create: macro tets (n_tets x 4 vertex ids, any order; the
  * library sorts each row ascending), vertex coordinates (n_vert x 3, host), vertex
@@ -278,6 +294,10 @@ typedef struct {
   int use_graph;             /* capture the V-cycle in a CUDA graph */
   int l_eta;                 /* levels <= l_eta evaluate eta at the quadrature points (NEXT-2; -1: none) */
   double qeta_lnC, qeta_jump, qeta_rjump;  /* eta_q = exp(lnC (1/2 - T_q)) (jump if r_q < rjump else 1) */
+  int coarse_redundant;      /* multi-rank meshes: gather the l_min problem of ALL macros (one allreduce of the
+                                zero-padded global vector) and solve it redundantly on every rank -- the analogue
+                                of the paper's coarse-grid agglomeration; 0: distributed PCG
+                                (an interface exchange + 2 allreduces per coarse iteration) */
 } hhg_mg_params;
 
 /* hhg_mg_create: builds per-level workspaces, diag(A) and D^-1, and lambda_hat per

@@ -46,7 +46,7 @@ EXPORTS = [
     "hhg_stokes_schur_apply", "hhg_kp1_apply", "hhg_kp1_diag", "hhg_vmass_apply", "hhg_vmass_diag",
     "p1_prolong", "p1_restrict", "hhg_kmg_create", "hhg_kmg_solve", "hhg_kmg_destroy",
     "hhg_temp_apply", "hhg_temp_solver_create", "hhg_temp_solve", "hhg_temp_solver_destroy", "hhg_mmoc",
-    "vcycle_host_batch", "hhg_set_deterministic", "hhg_mesh_prepare",
+    "vcycle_host_batch", "hhg_set_deterministic", "hhg_mesh_prepare", "hhg_comm_create_host",
 ]
 
 
@@ -103,6 +103,7 @@ def _load():
         "hhg_mmoc": ([P, I, P, P, P, D, P, P], I),
         "vcycle_host_batch": ([P, P, P, I, P], I),
         "hhg_set_deterministic": ([P, I], I), "hhg_mesh_prepare": ([P], I),
+        "hhg_comm_create_host": ([I, I, P, P, P, P], I),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -193,6 +194,64 @@ class Comm:
         h = ctypes.c_void_p()
         _chk(_lib.hhg_comm_create(_ptr(idb), int(world), int(rank), int(device), ctypes.byref(h)))
         self.handle, self.rank, self.world = h, rank, world
+
+    def __del__(self):
+        if getattr(self, "handle", None) and _lib is not None:
+            _lib.hhg_comm_destroy(self.handle)
+            self.handle = None
+
+
+_EXCHANGE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
+                                ctypes.POINTER(ctypes.c_int64), ctypes.c_int, ctypes.POINTER(ctypes.c_double),
+                                ctypes.POINTER(ctypes.c_double))
+_ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.c_int64)
+
+
+class HostComm:
+    """hhg_comm_create_host: the library's interface exchange and allreduce carried by a torch.distributed
+    process group (e.g. gloo) through host memory -- any number of ranks may share one GPU.  The callbacks
+    only move bytes (isend/irecv of the library's packed partial sums, all_reduce of its scalars)."""
+
+    def __init__(self, group=None):
+        import torch
+        import torch.distributed as dist
+        self.group = group
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+
+        def exchange(user, n_nbr, nbr, off, nc, send, recv):
+            try:
+                n = int(off[n_nbr]) * nc if n_nbr > 0 else 0
+                if n == 0:
+                    return 0
+                sv = torch.from_numpy(np.ctypeslib.as_array(send, shape=(n,)))
+                rv = torch.from_numpy(np.ctypeslib.as_array(recv, shape=(n,)))
+                reqs = []
+                for i in range(n_nbr):
+                    a, b = int(off[i]) * nc, int(off[i + 1]) * nc
+                    peer = dist.get_global_rank(group, int(nbr[i])) if group is not None else int(nbr[i])
+                    reqs.append(dist.isend(sv[a:b].clone(), peer, group=group))
+                    reqs.append(dist.irecv(rv[a:b], peer, group=group))
+                for r in reqs:
+                    r.wait()
+                return 0
+            except Exception as e:  # pragma: no cover - reported through HHG_ENCCL
+                print("HostComm exchange failed:", e)
+                return 1
+
+        def allreduce(user, buf, n):
+            try:
+                if n > 0:
+                    dist.all_reduce(torch.from_numpy(np.ctypeslib.as_array(buf, shape=(int(n),))), group=group)
+                return 0
+            except Exception as e:  # pragma: no cover
+                print("HostComm allreduce failed:", e)
+                return 1
+
+        self._cb = (_EXCHANGE_FN(exchange), _ALLREDUCE_FN(allreduce))   # keep the trampolines alive
+        h = ctypes.c_void_p()
+        _chk(_lib.hhg_comm_create_host(int(self.world), int(self.rank), ctypes.cast(self._cb[0], ctypes.c_void_p),
+                                       ctypes.cast(self._cb[1], ctypes.c_void_p), None, ctypes.byref(h)))
+        self.handle = h
 
     def __del__(self):
         if getattr(self, "handle", None) and _lib is not None:
@@ -553,7 +612,8 @@ class _MGParams(ctypes.Structure):
                 ("degree", ctypes.c_int), ("power_iters", ctypes.c_int), ("coarse_iters", ctypes.c_int),
                 ("cheb_hi_factor", ctypes.c_double), ("cheb_lo_ratio", ctypes.c_double),
                 ("visc_form", ctypes.c_int), ("use_graph", ctypes.c_int), ("l_eta", ctypes.c_int),
-                ("qeta_lnC", ctypes.c_double), ("qeta_jump", ctypes.c_double), ("qeta_rjump", ctypes.c_double)]
+                ("qeta_lnC", ctypes.c_double), ("qeta_jump", ctypes.c_double), ("qeta_rjump", ctypes.c_double),
+                ("coarse_redundant", ctypes.c_int)]
 
 
 class MG:
@@ -561,13 +621,14 @@ class MG:
 
     def __init__(self, mesh, l_min, l_max, eta_per_level, power_v0, pre=3, post=3, degree=3, power_iters=20,
                  coarse_iters=50, hi=1.1, lo=0.1, form=HHG_VISC_FULL, use_graph=True, T2_per_level=None, l_eta=-1,
-                 qeta=(0.0, 1.0, 0.0)):
+                 qeta=(0.0, 1.0, 0.0), coarse_redundant=True):
         """T2_per_level / l_eta / qeta = (lnC, jump, r_jump): on levels <= l_eta the viscosity is evaluated
-        at the quadrature points from the P2 temperature (NEXT-2 tier)."""
+        at the quadrature points from the P2 temperature (NEXT-2 tier).  coarse_redundant
+        (multi-rank meshes): solve the gathered coarse problem on every rank."""
         self.mesh = mesh
         self.l_min, self.l_max = l_min, l_max
         prm = _MGParams(l_min, l_max, pre, post, degree, power_iters, coarse_iters, hi, lo, form,
-                        1 if use_graph else 0, int(l_eta), *[float(v) for v in qeta])
+                        1 if use_graph else 0, int(l_eta), *[float(v) for v in qeta], 1 if coarse_redundant else 0)
         self._eta = dict(eta_per_level)
         self._v0 = dict(power_v0)
         self._T2 = dict(T2_per_level or {})
@@ -657,7 +718,7 @@ class KMG:
                  coarse_iters=50, hi=1.1, lo=0.1):
         self.mesh, self.l_min, self.l_max = mesh, l_min, l_max
         prm = _MGParams(l_min, l_max, pre, post, degree, power_iters, coarse_iters, hi, lo, HHG_VISC_FULL, 0, -1,
-                        0.0, 1.0, 0.0)
+                        0.0, 1.0, 0.0, 0)
         self._eta = dict(eta_per_level or {})
         L = l_max + 1
         etas = (ctypes.c_void_p * L)(*[_ptr(self._eta.get(l)) for l in range(L)])

@@ -135,6 +135,7 @@ struct Mesh {
 
 int ensure_level(Mesh* m, int level);
 int ensure_device_geo(Mesh* m);
+int mesh_set_geometry(Mesh* m);
 int ensure_canon(Mesh* m, int level, int space);
 int canonical_count(const Mesh* m, int N, int64_t* n);
 int canonical_keys(const Mesh* m, int N, int64_t* keys);
@@ -180,6 +181,7 @@ int launch_fixup_remote(const Mesh* m, const Level& L, int space, bool bc, const
                         cudaStream_t s);
 int comm_exchange(hhg_comm* c, const Halo& h, int nc, const double* sbuf, double* rbuf, cudaStream_t s);
 int comm_allreduce_sum(hhg_comm* c, double* buf, int64_t n, cudaStream_t s);
+bool comm_capturable(const hhg_comm* c);  // false for the host-staged transport (host synchronisation)
 int build_host_groups(const Mesh* m, int level, int space, std::vector<int64_t>& ptr, std::vector<int64_t>& copy,
                       std::vector<uint8_t>& kind, std::vector<double>& normal, std::vector<uint8_t>& own,
                       Halo& halo, std::vector<int64_t>& slot_group);
@@ -240,4 +242,11 @@ struct hhg_mesh : public hhg::Mesh {};
 struct hhg_comm {
   ncclComm_t nccl = nullptr;
   int nranks = 1, rank = 0, device = 0;
+  // host-staged transport (hhg_comm_create_host)
+  bool host = false;
+  hhg_exchange_fn exchange_fn = nullptr;
+  hhg_allreduce_fn allreduce_fn = nullptr;
+  void* user = nullptr;
+  double* hbuf = nullptr;   // pinned [2][hcap] send / receive staging
+  size_t hcap = 0;
 };

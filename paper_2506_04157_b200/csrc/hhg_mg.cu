@@ -87,6 +87,13 @@ struct hhg_mg {
   std::vector<Lv> lv;
   double* scal = nullptr;    // device scalars
   double* red = nullptr;     // this object's reduction scratch (dots never share it with other objects)
+  // redundant coarse solve (multi-rank, prm.coarse_redundant): the l_min problem of ALL macros on every
+  // rank -- a single-rank mesh/hierarchy of the global macro mesh, the rank's local macro ids, global
+  // coarse vectors (the agglomeration analogue of P:443)
+  hhg_mesh* cmesh = nullptr;
+  hhg_mg* cmg = nullptr;
+  int64_t* cids = nullptr;   // device: global id of every local macro
+  double *cf = nullptr, *cx = nullptr, *ceta = nullptr, *cT2 = nullptr;
   double* hbuf_rhs = nullptr;  // device staging for vcycle_host
   double* hbuf_x = nullptr;
   cudaGraphExec_t gexec = nullptr;
@@ -116,6 +123,10 @@ struct hhg_mg {
         if (p) cudaFree(p);
     if (scal) cudaFree(scal);
     if (red) cudaFree(red);
+    if (cmg) delete cmg;
+    if (cmesh) delete cmesh;
+    for (void* p : {(void*)cids, (void*)cf, (void*)cx, (void*)ceta, (void*)cT2})
+      if (p) cudaFree(p);
     if (mesh) --mesh->dependents;
     if (hbuf_rhs) cudaFree(hbuf_rhs);
     if (hbuf_x) cudaFree(hbuf_x);
@@ -221,7 +232,44 @@ static int mg_pcg(hhg_mg* mg, int l, const double* f, double* x, cudaStream_t s)
   return HHG_OK;
 }
 
+// copy between a rank's macro-local layout and the global macro layout of the coarse mesh (nc
+// components of per-macro lattices with npts points; component strides cs_loc / cs_glob)
+__global__ void k_macro_copy(int64_t nloc, int64_t npts, int nc, const int64_t* __restrict__ ids, int64_t cs_loc,
+                             int64_t cs_glob, const double* __restrict__ src, double* __restrict__ dst, int to_global) {
+  const int64_t n = nloc * npts;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n * nc; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = i / n, r = i - c * n, t = r / npts, k = r - t * npts;
+    const int64_t lo = c * cs_loc + t * npts + k, gl = c * cs_glob + ids[t] * npts + k;
+    if (to_global) dst[gl] = src[lo];
+    else dst[lo] = src[gl];
+  }
+}
+// local -> global (zero padding, then a sum over ranks: every macro lives on exactly one rank)
+static int coarse_gather(hhg_mg* mg, int l, int nc, int64_t npts, const double* loc, double* glob, cudaStream_t s) {
+  const int64_t nl = macro_count(mg->mesh), ng = mg->mesh->n_tets;
+  HHG_CUDA(cudaMemsetAsync(glob, 0, nc * ng * npts * sizeof(double), s));
+  if (nl > 0) {
+    k_macro_copy<<<vg(nl * npts * nc), 256, 0, s>>>(nl, npts, nc, mg->cids, nl * npts, ng * npts, loc, glob, 1);
+    count_launch();
+  }
+  return comm_allreduce_sum(mg->mesh->comm, glob, nc * ng * npts, s);
+}
+static int coarse_scatter(hhg_mg* mg, int nc, int64_t npts, const double* glob, double* loc, cudaStream_t s) {
+  const int64_t nl = macro_count(mg->mesh), ng = mg->mesh->n_tets;
+  if (nl == 0) return HHG_OK;
+  k_macro_copy<<<vg(nl * npts * nc), 256, 0, s>>>(nl, npts, nc, mg->cids, nl * npts, ng * npts, glob, loc, 0);
+  count_launch();
+  HHG_CUDA(cudaGetLastError());
+  return HHG_OK;
+}
+
 static int mg_cycle(hhg_mg* mg, int l, const double* f, double* x, cudaStream_t s) {
+  if (l == mg->prm.l_min && mg->cmg) {  // redundant coarse solve: gather, solve the global problem, scatter
+    const int64_t np2 = mg->mesh->levels[l].npts2;
+    HHG_TRY(coarse_gather(mg, l, 3, np2, f, mg->cf, s));
+    HHG_TRY(mg_cycle(mg->cmg, l, mg->cf, mg->cx, s));
+    return coarse_scatter(mg, 3, np2, mg->cx, x, s);
+  }
   if (l == mg->prm.l_min) return mg_pcg(mg, l, f, x, s);
   auto& L = mg->lv[l];
   const Mesh* m = mg->mesh;
@@ -320,6 +368,51 @@ int hhg_mg_create_qeta(hhg_mesh* mesh, const hhg_mg_params* params, const double
       if (r != HHG_OK) return bail(r);
     }
   }
+  if (P.coarse_redundant && mesh->nranks > 1) {
+    // the coarse level of all macros on every rank: global mesh (no communicator), global eta (and T2)
+    const int lc = P.l_min;
+    hhg_mesh* cm = nullptr;
+    int r = hhg_mesh_create(mesh->xyz.data(), mesh->n_vert, mesh->tets.data(), mesh->n_tets, mesh->vtag.data(), lc,
+                            nullptr, nullptr, &cm);
+    if (r != HHG_OK) return bail(r);
+    mg->cmesh = cm;
+    cm->blend = mesh->blend;
+    for (int i = 0; i < 3; ++i) cm->bc_kind[i] = mesh->bc_kind[i];
+    cm->deterministic = mesh->deterministic;
+    cm->dgeo_dirty = true;
+    if ((r = mesh_set_geometry(cm)) != HHG_OK || (r = ensure_level(cm, lc)) != HHG_OK) return bail(r);
+    std::vector<int64_t> ids(mesh->local.begin(), mesh->local.end());
+    if (cudaMalloc(&mg->cids, std::max<size_t>(ids.size(), 1) * sizeof(int64_t)) != cudaSuccess)
+      return bail(fail(HHG_ENOMEM, "coarse ids"));
+    if (!ids.empty() && cudaMemcpy(mg->cids, ids.data(), ids.size() * sizeof(int64_t), cudaMemcpyHostToDevice) != cudaSuccess)
+      return bail(fail(HHG_ECUDA, "coarse ids"));
+    const Level& LC = cm->levels[lc];
+    const int64_t ng = mesh->n_tets;
+    for (double** p : {&mg->cf, &mg->cx})
+      if (cudaMalloc(p, 3 * ng * LC.npts2 * sizeof(double)) != cudaSuccess) return bail(fail(HHG_ENOMEM, "coarse vectors"));
+    const double* ce = nullptr;
+    if (mg->lv[lc].eta) {
+      if (cudaMalloc(&mg->ceta, ng * LC.npts1 * sizeof(double)) != cudaSuccess) return bail(fail(HHG_ENOMEM, "coarse eta"));
+      if ((r = coarse_gather(mg, lc, 1, LC.npts1, mg->lv[lc].eta, mg->ceta, 0)) != HHG_OK) return bail(r);
+      ce = mg->ceta;
+    }
+    const double* ct = nullptr;
+    if (mg->lv[lc].T2) {
+      if (cudaMalloc(&mg->cT2, ng * LC.npts2 * sizeof(double)) != cudaSuccess) return bail(fail(HHG_ENOMEM, "coarse T2"));
+      if ((r = coarse_gather(mg, lc, 1, LC.npts2, mg->lv[lc].T2, mg->cT2, 0)) != HHG_OK) return bail(r);
+      ct = mg->cT2;
+    }
+    if (cudaDeviceSynchronize() != cudaSuccess) return bail(fail(HHG_ECUDA, "coarse gather"));
+    hhg_mg_params cp = P;
+    cp.l_max = lc;
+    cp.coarse_redundant = 0;
+    std::vector<const double*> etas(lc + 1, nullptr), t2s(lc + 1, nullptr);
+    etas[lc] = ce;
+    t2s[lc] = ct;
+    r = ct ? hhg_mg_create_qeta(cm, &cp, etas.data(), t2s.data(), nullptr, &mg->cmg)
+           : hhg_mg_create(cm, &cp, etas.data(), nullptr, &mg->cmg);
+    if (r != HHG_OK) return bail(r);
+  }
   if (cudaDeviceSynchronize() != cudaSuccess) return bail(fail(HHG_ECUDA, "hhg_mg_create: sync failed"));
   *out = mg;
   return HHG_OK;
@@ -337,7 +430,7 @@ int vcycle(hhg_mg* mg, const double* rhs, double* x, hhg_stream_t stream) {
   cudaStream_t s = (cudaStream_t)stream;
   for (int l = mg->prm.l_min + 1; l <= mg->prm.l_max; ++l)
     if (!(mg->lv[l].lam > 0)) return fail(HHG_ENOTREADY, "vcycle: no spectrum estimate");
-  const bool use_graph = mg->prm.use_graph && s != nullptr && !mg->prof;
+  const bool use_graph = mg->prm.use_graph && s != nullptr && !mg->prof && comm_capturable(mg->mesh->comm);
   if (!use_graph) {
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (mg->prof) {
@@ -410,7 +503,8 @@ __global__ void k_cg_roll(double* sc) {
 }
 
 static int cg_precond(hhg_mg* mg, cudaStream_t s) {  // z = V(r) with a cached graph
-  if (!mg->prm.use_graph || s == nullptr) return mg_cycle(mg, mg->prm.l_max, mg->cg_r, mg->cg_z, s);
+  if (!mg->prm.use_graph || s == nullptr || !comm_capturable(mg->mesh->comm))
+    return mg_cycle(mg, mg->prm.l_max, mg->cg_r, mg->cg_z, s);
   if (!mg->cg_gexec || mg->cg_stream != s) {
     if (mg->cg_gexec) cudaGraphExecDestroy(mg->cg_gexec);
     mg->cg_gexec = nullptr;
@@ -522,7 +616,7 @@ int vcycle_host_batch(hhg_mg* mg, const double* const* rhs_host, double* const* 
   }
   for (int l = mg->prm.l_min + 1; l <= mg->prm.l_max; ++l)
     if (!(mg->lv[l].lam > 0)) return fail(HHG_ENOTREADY, "vcycle_host_batch: no spectrum estimate");
-  const bool use_graph = mg->prm.use_graph && s != nullptr && !mg->prof;
+  const bool use_graph = mg->prm.use_graph && s != nullptr && !mg->prof && comm_capturable(mg->mesh->comm);
   if (use_graph && mg->pipe_stream != s) {
     for (int b = 0; b < 2; ++b) {
       if (mg->pipe_gexec[b]) cudaGraphExecDestroy(mg->pipe_gexec[b]);

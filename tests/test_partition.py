@@ -141,3 +141,61 @@ def test_world2_gloo_exchange_protocol():
         p.join(120)
     assert all(p.exitcode == 0 for p in procs)
     assert list(out) == [1, 1]
+
+
+# ------------------------------------------------------------------ the library's host-staged transport callbacks
+def _hostcomm_worker(rank, world, port, out):
+    """The HostComm trampolines the library calls (hhg_comm_create_host), driven with the halo plans the
+    library built for this rank: every neighbour's block arrives in the right slots, allreduce sums."""
+    import ctypes
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        comm = hhg.HostComm()
+        exchange, allreduce = comm._cb
+        mac = icoshell(3, 2)
+        level = 2
+        tr = hhg.partition_rcb(mac.verts, mac.tets, world)
+        M = hhg.Mesh.part(mac, level, tr, world, rank)
+        ok = True
+        for space, nc in ((hhg.HHG_P1, 1), (hhg.HHG_P2VEC, 3)):
+            nb, cnt = M.halo_info(level, space)
+            keys = M.halo_keys(level, space)
+            off = np.concatenate([[0], np.cumsum(cnt)]).astype(np.int64)
+            send = np.ascontiguousarray(np.stack([hash_keys(keys, 100 + rank, c) for c in range(nc)], 1).astype(np.float64))
+            recv = np.zeros_like(send)
+            nbr = np.ascontiguousarray(nb, dtype=np.int32)
+            rc = exchange(None, len(nbr), nbr.ctypes.data_as(ctypes.POINTER(ctypes.c_int)),
+                          off.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), nc,
+                          send.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                          recv.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+            ok &= rc == 0
+            for i, q in enumerate(nb):
+                expect = np.stack([hash_keys(keys[off[i]:off[i + 1]], 100 + int(q), c) for c in range(nc)], 1)
+                ok &= bool(np.array_equal(recv[off[i]:off[i + 1]], expect))
+        v = np.array([rank + 1.0, 10.0 * rank], dtype=np.float64)
+        ok &= allreduce(None, v.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), 2) == 0
+        ok &= bool(np.array_equal(v, [world * (world + 1) / 2.0, 10.0 * world * (world - 1) / 2.0]))
+        out[rank] = 1 if ok else 0
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_host_transport_callbacks_gloo(world):
+    import socket
+    import torch.multiprocessing as mp
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    out = ctx.Array("i", [0] * world)
+    procs = [ctx.Process(target=_hostcomm_worker, args=(r, world, port, out)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(180)
+    assert all(p.exitcode == 0 for p in procs)
+    assert list(out) == [1] * world
