@@ -655,6 +655,28 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
     }
   }
 #endif
+#ifdef HHG_EXP_PF
+  // warm L2 for the brick whose CTA is dispatched after this one's wave (CTA index + resident CTAs):
+  // its cp.async staging then hits L2 instead of DRAM
+  if (NEED_U) {
+    const unsigned nbx = gridDim.x, b2 = blockIdx.y * nbx + blockIdx.x + HHG_EXP_PF;
+    if (b2 < nbx * gridDim.y) {
+      const int mac2 = b2 / nbx;
+      const int32_t bp2 = __ldg(bricks + (b2 - mac2 * nbx));
+      const int a2 = bp2 & 1023, c2 = (bp2 >> 10) & 1023, d2 = bp2 >> 20;
+      const double* ub2 = u + (int64_t)mac2 * npts2;
+      for (int it = tid; it < 243; it += kBT) {
+        const int c = it / 81, r = it - 81 * c;
+        const int gy = 2 * c2 + r % 9, gz = 2 * d2 + r / 9;
+        const int len = min(9, n2 - 2 * a2 - gy - gz + 1);
+        if (len <= 0) continue;
+        const double* rp = ub2 + c * cstride + rowstart32(n2, gy, gz) + 2 * a2;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(rp));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(rp + len - 1));
+      }
+    }
+  }
+#endif
   if (HAS_U_OUT)
     for (int r = tid; r < 6 * kFY; r += kBT) sy[r] = 0.0;
   if (HAS_P_OUT)

@@ -37,12 +37,15 @@ def _run(M, redundant):
     import paper_2506_04157_b200 as hhg
     from tests.harness import canon
     levels = tuple(range(1, L + 1))
-    etas, pv, rhs = _case(M, levels)
+    etas, pv0, rhs = _case(M, levels)
+    pv0 = {l: v.clone() for l, v in pv0.items()}
     y = hhg.epsilon_apply(M, L, etas[L], rhs)
     dot = float(hhg.hhg_dot(M, L, hhg.HHG_P2VEC, rhs, y).item())
     out = {"apply": canon(M, L, hhg.HHG_P2VEC, y), "dot": dot,
            "mask": canon(M, L, hhg.HHG_P2VEC, torch.ones_like(rhs))}
     for red in redundant:
+        # fresh start vectors: hhg_mg_create's power iterations overwrite them
+        pv = {l: v.clone() for l, v in pv0.items()}
         mg = hhg.MG(M, 1, L, etas, pv, pre=3, post=3, degree=3, power_iters=20, coarse_iters=50, coarse_redundant=red)
         x = mg.vcycle(rhs)
         torch.cuda.synchronize()
@@ -68,7 +71,7 @@ def _rank_main(rank, world, port, q):
         M.blend_map(hhg.HHG_BLEND_SHELL)
         M.set_bc(hhg.HHG_BND_OUTER, hhg.HHG_BC_DIRICHLET0)
         M.set_bc(hhg.HHG_BND_INNER, hhg.HHG_BC_FREESLIP)
-        out = _run(M, (True, False) if world <= 4 else (True,))
+        out = _run(M, (True, False) if world == 2 else (True,))
         out["rank"] = rank
         out["macros"] = M.local_macros()
         q.put(out)
@@ -133,7 +136,7 @@ def test_partitioned_vcycle_matches_single_rank(single_rank, world):
     assert rel(y, ref["apply"]) <= 1e-13
     for o in outs:
         assert abs(o["dot"] - ref["dot"]) <= 1e-12 * abs(ref["dot"])
-    for red in ((True, False) if world <= 4 else (True,)):
+    for red in ((True, False) if world == 2 else (True,)):
         k = f"vcycle{int(red)}"
         x, sp = _merge(outs, k)
         assert sp <= 1e-12 * np.abs(ref["vcycle1"]).max(), (k, sp)
