@@ -277,13 +277,20 @@ def main():
         e2e_ms = float(t.item())
     nbytes = rhs.numel() * 8
 
-    # roofline of the dominant kernel (fine-level element kernel, fp64 DFMA pipe)
+    # roofline of the dominant kernel (fine-level element kernel, fp64 DFMA pipe): flops per micro tet and
+    # DRAM bytes per launch from the committed ncu capture, DFMA peak from the committed microbenchmark
+    counts = elem_counts()
     n_tets = M.local_macros() * 8 ** L        # this rank's micro tets (the element kernel it times)
-    flops_per_tet = float(os.environ.get("HHG_FLOPS_PER_TET", "0")) or FLOPS_PER_TET
+    flops_per_tet = counts["epsilon_apply_L5"]["flops_per_tet"]
+    traffic = counts["epsilon_apply_L5"]["dram_bytes"] if L == 5 else None
     elem_ms = prof["apply_ms_sum"] / max(1, prof["apply_count"])
     achieved = flops_per_tet * n_tets / (elem_ms * 1e-3) / 1e12
     pk = peaks()
-    fp64_peak = pk.get("fp64_tflops") or FP64_PEAK_MEASURED
+    fp64 = fp64_peak_measured()
+    fp64_peak = pk.get("fp64_tflops") or fp64["fp64_dfma_tflops"]
+
+    # BASELINE config 2: stokes_apply (A + B^T, (B + C)) on shell(3,2) L4, contrast 1e4 x 10, gamma 0.3781
+    st = stokes_apply_line(counts, fp64_peak, s, dist) if world == 1 else None
     result = {
         "metric": METRIC, "value": value, "unit": "GDoF/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -298,11 +305,15 @@ def main():
                   "note": "epsilon_apply (memset + element kernel + interface sum/BC) standalone"},
         "vcycle_ms": ms, "setup_s": setup_s,
         "roofline": {"bound": "alu", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
-                     "frac": achieved / fp64_peak, "traffic": TRAFFIC_PER_LAUNCH,
-                     "kernel": "k_elem<blend,A,full> (fine level)", "elem_ms": elem_ms,
+                     "frac": achieved / fp64_peak, "traffic": traffic,
+                     "kernel": "k_elem_fp<blend,A,full> (fine level)", "elem_ms": elem_ms,
                      "flops_per_tet": flops_per_tet,
+                     "flops_source": "profiles/r02_elem_counts.json (ncu dfma/dadd/dmul thread instructions per launch "
+                                     "/ micro tets, DFMA = 2)",
                      "peak_source": "MEASURED_PEAKS.json fp64_tflops" if pk.get("fp64_tflops") else
-                     "measured: tools/fp64_peak DFMA microbenchmark (profiles/r01_fp64_peak.json)",
+                     f"measured DFMA microbenchmark, best of {fp64.get('reps')} launches at "
+                     f"{fp64.get('clocks', {}).get('sm_mhz_median_under_load')} MHz (profiles/r02_fp64_peak.json; "
+                     "nominal 148 SMs x 64 FP64 lanes x 2 x 1.965 GHz = 37.2 TF/s)",
                      "hbm_gbs_algorithmic": (2 * rhs.numel() + M.local_macros() * ((2 ** L + 1) * (2 ** L + 2)
                                                                                     * (2 ** L + 3) // 6)) * 8
                      / (elem_ms * 1e-3) / 1e9},
@@ -313,24 +324,87 @@ def main():
         "gpu_launches": kernels_per_cycle * args.steps,
         "clocks": clk.summary(),
     }
+    if st:
+        result["stokes_apply"] = st
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         ndof_c, ts, setup = cpu_oracle_vcycle(args.cpu_level, 2)
         v = ndof_c / min(ts) / 1e9
         result["cpu_baseline"] = {"value": v, "unit": "GDoF/s", "cores": len(os.sched_getaffinity(0)),
                                   "kind": "oracle",
                                   "sample": f"oracle V(3,3)-cycle shell(3,2) levels {args.cpu_level}->1 "
-                                            f"({ndof_c} dofs), best of 2; setup {setup:.1f} s excluded"}
+                                            f"({ndof_c} dofs), best of 2; setup {setup:.1f} s excluded",
+                                  "apply": cpu_oracle_apply(3)}
     if rank == 0:
         print(json.dumps(result))
     if dist:
         dist.destroy_process_group()
 
 
-# algorithmic DP flops per micro tet of the A element kernel (cross-checked
-# against ncu smsp__sass_thread_inst_executed_op_d{fma,add,mul}_pred_on)
-FLOPS_PER_TET = 1098.0      # 352 DFMA + 228 DADD + 166 DMUL per tet, element kernel v5 (ncu, profiles/r01_ncu_elem_v5_L5_summary.txt)
-FP64_PEAK_MEASURED = 34.16  # tools/fp64_peak on this pool's B200 (profiles/r01_fp64_peak.json); DMMA 37.1 (r01_fp64_dfma_vs_dmma.json)
-TRAFFIC_PER_LAUNCH = 762.25e6  # bytes: dram__bytes_read.sum + dram__bytes_write.sum of one L5 launch (ncu --set full, profiles/r01_ncu_elem_v6_L5_summary.txt)
+def elem_counts():
+    """Per-launch ncu counters of the element kernels (tools/ncu_counts.py on the committed captures)."""
+    return json.load(open(os.path.join(ROOT, "profiles", "r02_elem_counts.json")))
+
+
+def fp64_peak_measured():
+    """DFMA throughput of this pool's B200 (tools/fp64_peak_clocks.py: 200 launches, clocks sampled)."""
+    return json.load(open(os.path.join(ROOT, "profiles", "r02_fp64_peak.json")))
+
+
+def stokes_apply_line(counts, fp64_peak, s, dist, reps=20):
+    """BASELINE config 2: stokes_apply [A u + B^T p ; (B + C) u] on the blended shell(3,2) at level 4,
+    viscosity contrast 1e4 x 10, gamma = 0.3781 (whole C-ABI call: zeroing, fused element kernel,
+    interface sums + BCs), GDoF/s over the unique (u, p) dofs; roofline of the call against the DFMA peak
+    with the fused kernel's flops per micro tet (profiles/r02_elem_counts.json)."""
+    import torch
+    import paper_2506_04157_b200 as hhg
+    from tests.harness import BC_SHELL, lib_eta, lib_mesh, lib_p, lib_u
+    from workload import icoshell
+    L = 4
+    M = lib_mesh(icoshell(3, 2), L, True, BC_SHELL)
+    eta = lib_eta(M, L, (1e4, 10.0))
+    u, p = lib_u(M, L, 2), lib_p(M, L, 3)
+    yu, yp = M.zeros(L, hhg.HHG_P2VEC), M.zeros(L, hhg.HHG_P1)
+    n_dof = M.canonical_len(L, hhg.HHG_P2VEC) + M.canonical_len(L, hhg.HHG_P1)
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            hhg.stokes_apply(M, L, eta, GAMMA, u, p, yu, yp, stream=s)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for _ in range(reps):
+            hhg.stokes_apply(M, L, eta, GAMMA, u, p, yu, yp, stream=s)
+        e1.record(s)
+    s.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    c = counts["stokes_apply_L4"]
+    achieved = c["flops_per_tet"] * 240 * 8 ** L / (ms * 1e-3) / 1e12
+    return {"config": "config2: blended shell(3,2) L4, contrast 1e4 x 10, gamma 0.3781", "ms": ms,
+            "gdofs": n_dof / (ms * 1e-3) / 1e9, "dofs_u_p": n_dof,
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
+                         "frac": achieved / fp64_peak, "flops_per_tet": c["flops_per_tet"],
+                         "note": "whole stokes_apply call timed (zeroing + element kernel + interface sums); the fused "
+                                 "element kernel alone: %.1f us under ncu" % (1e6 * c["duration_s"])},
+            "l2": "level-4 vectors (97 MB) fit in L2"}
+
+
+def cpu_oracle_apply(level, reps=5):
+    """The oracle's epsilon apply: assembled CSR A of shell(3,2) at `level` (config-3 viscosity) times a
+    vector, scipy SpMV on the host (assembly excluded), best of `reps`."""
+    from tests.harness import BC_SHELL, oracle_case
+    from workload import icoshell, uniform_vec
+    t0 = time.perf_counter()
+    lm, d, _ = oracle_case(icoshell(3, 2), level, True, BC_SHELL, (1e6, 30.0), 0.0, build=("A",))
+    Ac = d.Ac()
+    setup = time.perf_counter() - t0
+    u = d.project(uniform_vec(lm.p2_keys, 2))
+    ts = []
+    for _ in range(reps):
+        t1 = time.perf_counter()
+        Ac @ u
+        ts.append(time.perf_counter() - t1)
+    ndof = 3 * lm.n_p2
+    return {"value": ndof / min(ts) / 1e9, "unit": "GDoF/s", "kind": "oracle",
+            "sample": f"oracle CSR SpMV (M P_v) A (P_v M) u, shell(3,2) level {level} ({ndof} dofs, nnz {Ac.nnz}), "
+                      f"best of {reps}; assembly {setup:.1f} s excluded; scipy (single thread)"}
 
 if __name__ == "__main__":
     main()

@@ -1,6 +1,9 @@
 // DFMA throughput microbenchmark for the fp64 roofline denominator (B200 has no fp64 entry in
 // MEASURED_PEAKS.json).  8 independent FMA chains per thread, 148*8 blocks x 256 threads.
 #include <cstdio>
+#include <cstdlib>
+#include <vector>
+#include <algorithm>
 #include <cuda_runtime.h>
 
 __global__ void k_dfma(double* out, int iters, double a, double b) {
@@ -15,7 +18,8 @@ __global__ void k_dfma(double* out, int iters, double a, double b) {
   if (s == 1.2345) out[0] = s;
 }
 
-int main() {
+int main(int argc, char** argv) {
+  const int reps = argc > 1 ? atoi(argv[1]) : 5;
   double* d;
   cudaMalloc(&d, 8);
   int sm = 0;
@@ -26,7 +30,8 @@ int main() {
   cudaEventCreate(&e1);
   k_dfma<<<blocks, threads>>>(d, 100, 0.999999, 1e-7);
   double best = 0;
-  for (int rep = 0; rep < 5; ++rep) {
+  std::vector<double> all;
+  for (int rep = 0; rep < reps; ++rep) {
     cudaEventRecord(e0);
     k_dfma<<<blocks, threads>>>(d, iters, 0.999999, 1e-7);
     cudaEventRecord(e1);
@@ -35,7 +40,10 @@ int main() {
     cudaEventElapsedTime(&ms, e0, e1);
     double tf = 2.0 * 8.0 * iters * (double)blocks * threads / (ms * 1e-3) / 1e12;
     if (tf > best) best = tf;
+    all.push_back(tf);
   }
-  printf("{\"fp64_dfma_tflops\": %.3f, \"sms\": %d}\n", best, sm);
+  std::sort(all.begin(), all.end());
+  printf("{\"fp64_dfma_tflops\": %.3f, \"fp64_dfma_tflops_median\": %.3f, \"reps\": %d, \"sms\": %d}\n", best,
+         all[all.size() / 2], reps, sm);
   return 0;
 }

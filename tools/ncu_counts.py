@@ -1,0 +1,30 @@
+"""Per-launch counters of the element kernel from an ncu report -> JSON (read by bench.py for the
+roofline): duration, DRAM bytes, thread-level DFMA / DADD / DMUL counts and flops per micro tet
+(DFMA = 2 flops).  python tools/ncu_counts.py <rep.ncu-rep> <n_tets> <label> > profiles/<out>.json"""
+import csv, io, json, subprocess, sys
+rep, n_tets, label = sys.argv[1], int(sys.argv[2]), sys.argv[3]
+out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(out)))
+h, u = rows[0], rows[1]
+res = []
+for v in rows[2:]:
+    d = dict(zip(h, v))
+    num = lambda k: float(d[k].replace(",", "")) if d.get(k) not in (None, "", "n/a") else None
+    def unit_scale(k):
+        un = u[h.index(k)] if k in h else ""
+        return {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "usecond": 1e-6, "msecond": 1e-3,
+                "nsecond": 1e-9, "second": 1, "us": 1e-6, "ms": 1e-3, "ns": 1e-9, "s": 1}.get(un, 1)
+    dfma = num("smsp__sass_thread_inst_executed_op_dfma_pred_on.sum")
+    dadd = num("smsp__sass_thread_inst_executed_op_dadd_pred_on.sum")
+    dmul = num("smsp__sass_thread_inst_executed_op_dmul_pred_on.sum")
+    dur = num("gpu__time_duration.sum") * unit_scale("gpu__time_duration.sum")
+    rd = num("dram__bytes_read.sum") * unit_scale("dram__bytes_read.sum")
+    wr = num("dram__bytes_write.sum") * unit_scale("dram__bytes_write.sum")
+    res.append({"label": label, "kernel": d.get("Kernel Name", "")[:160], "n_tets": n_tets, "duration_s": dur,
+                "dram_read_bytes": rd, "dram_write_bytes": wr, "dram_bytes": rd + wr,
+                "dfma": dfma, "dadd": dadd, "dmul": dmul,
+                "flops_per_tet": (2 * dfma + dadd + dmul) / n_tets if dfma is not None else None,
+                "fp64_pipe_active_pct": num("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+                "warps_active_per_sm": num("sm__warps_active.avg.per_cycle_active"),
+                "registers": num("launch__registers_per_thread"), "source": rep})
+print(json.dumps(res[0] if len(res) == 1 else res, indent=1))
