@@ -97,6 +97,7 @@ struct Level {
   int64_t nrows1 = 0, nrows2 = 0;
   Groups g1, g2;                    // P1 interface groups, P2 interface+BC groups
   int32_t* bcn2 = nullptr;          // per stored P2 node: -1 none, -2 Dirichlet, g >= 0 free-slip group
+  int32_t* gmap2 = nullptr;         // per stored P2 node: its group in g2 (interface and/or BC), -1 if none
   uint8_t* own1 = nullptr;          // owner mask per stored P1 node
   uint8_t* own2 = nullptr;          // owner mask per stored P2 node
   int64_t* canon1 = nullptr;        // canonical node index per stored node (lazy)
@@ -224,6 +225,21 @@ int launch_pcg_update_bc(const Mesh* m, const Level& L, int it, const double* sc
                          const double* p, const double* q, const double* dinv, double* z, cudaStream_t s);
 int launch_pcg_dir_zero(int64_t n, int it, const double* scal, const double* z, double* p, double* q_zero,
                         cudaStream_t s);
+// Consumers of an UNSUMMED element-kernel output t (single rank): each stored node reads its value as the sum
+// of its group's copies with the group's BC applied (= what k_fixup would have stored), so the separate
+// interface-sum pass disappears.  Same semantics as the *_bc kernels applied after launch_fixup(sum, BC).
+int launch_cheb0_fx(const Mesh* m, const Level& L, const double* f, const double* t, const double* dinv,
+                    double inv_theta, double* r, double* d, cudaStream_t s);
+int launch_chebk_fx(const Mesh* m, const Level& L, const double* t, const double* dinv, double c1, double c2, double* x,
+                    double* r, double* d, cudaStream_t s);
+int launch_chebk_last_fx(const Mesh* m, const Level& L, const double* t, const double* dinv, double c1, double c2,
+                         const double* r, const double* d, double* x, cudaStream_t s);
+int launch_cheb_deg1_fx(const Mesh* m, const Level& L, const double* f, const double* t, const double* dinv,
+                        double inv_theta, double* x, cudaStream_t s);
+int launch_sub_fx(const Mesh* m, const Level& L, const double* f, const double* t, double* r, cudaStream_t s);  // r = f - t
+// PCG update fused with the new r.z (single rank): writes r.z into the ping-pong slot of iteration `it`
+int launch_pcg_update_bc_dot(const Mesh* m, const Level& L, int it, double* scal, double* x, double* r, const double* p,
+                             const double* q, const double* dinv, double* z, double* red, cudaStream_t s);
 // eager one-time set-up of kernel tables / attributes (never from a hot call)
 int elem_prepare_all();
 int transfer_prepare();

@@ -962,3 +962,224 @@ int launch_pcg_dir(int64_t n, double* scal, const double* z, double* p, cudaStre
 }
 
 }  // namespace hhg
+
+namespace hhg {
+// ------------------------------------------------------------------ fused interface sum + BC consumers
+// t is the raw element-kernel output (per-copy partial sums).  tval() returns, for stored node i, the value
+// k_fixup<3, true> would have written: the sum of its group's copies (fixed copy order -> every copy gets
+// the bitwise same value) with the group's BC applied, or t[i] for nodes in no group.
+struct FxArgs {
+  const int32_t* __restrict__ gmap;
+  const int64_t* __restrict__ ptr;
+  const int64_t* __restrict__ copy;
+  const uint8_t* __restrict__ kind;
+  const double* __restrict__ normal;
+};
+__device__ __forceinline__ void tval(const FxArgs& a, int64_t i, int64_t cs, const double* __restrict__ t,
+                                     double (&v)[3]) {
+  const int g = a.gmap[i];
+  if (g < 0) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) v[c] = t[i + c * cs];
+    return;
+  }
+  group_sum<3>(a.ptr[g], a.ptr[g + 1], a.copy, cs, t, v);
+  group_bc<3>(a.kind[g], a.normal + 3 * g, v);
+}
+static FxArgs fx_args(const Level& L) { return FxArgs{L.gmap2, L.g2.ptr, L.g2.copy, L.g2.kind, L.g2.normal}; }
+
+__global__ void k_cheb0_fx(int64_t ns, int64_t cs, FxArgs a, const double* __restrict__ f, const double* __restrict__ t,
+                           const double* __restrict__ dinv, double it, double* __restrict__ r, double* __restrict__ d,
+                           const int32_t* __restrict__ bcn, const double* __restrict__ nrm) {
+  GRID_STRIDE(i, ns) {
+    double tv[3], dv[3];
+    tval(a, i, cs, t, tv);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const int64_t j = i + c * cs;
+      const double ri = f[j] - tv[c];
+      r[j] = ri;
+      dv[c] = dinv[j] * ri * it;
+    }
+    bc_project(bcn[i], nrm, dv[0], dv[1], dv[2]);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) d[i + c * cs] = dv[c];
+  }
+}
+__global__ void k_cheb_deg1_fx(int64_t ns, int64_t cs, FxArgs a, const double* __restrict__ f,
+                               const double* __restrict__ t, const double* __restrict__ dinv, double it,
+                               double* __restrict__ x, const int32_t* __restrict__ bcn, const double* __restrict__ nrm) {
+  GRID_STRIDE(i, ns) {
+    double tv[3], dv[3];
+    tval(a, i, cs, t, tv);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const int64_t j = i + c * cs;
+      dv[c] = dinv[j] * (f[j] - tv[c]) * it;
+    }
+    bc_project(bcn[i], nrm, dv[0], dv[1], dv[2]);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) x[i + c * cs] += dv[c];
+  }
+}
+__global__ void k_chebk_fx(int64_t ns, int64_t cs, FxArgs a, const double* __restrict__ t,
+                           const double* __restrict__ dinv, double c1, double c2, double* __restrict__ x,
+                           double* __restrict__ r, double* __restrict__ d, const int32_t* __restrict__ bcn,
+                           const double* __restrict__ nrm) {
+  GRID_STRIDE(i, ns) {
+    double tv[3], dv[3];
+    tval(a, i, cs, t, tv);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const int64_t j = i + c * cs;
+      const double di = d[j];
+      x[j] += di;
+      const double ri = r[j] - tv[c];
+      r[j] = ri;
+      dv[c] = c1 * di + c2 * dinv[j] * ri;
+    }
+    bc_project(bcn[i], nrm, dv[0], dv[1], dv[2]);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) d[i + c * cs] = dv[c];
+  }
+}
+__global__ void k_chebk_last_fx(int64_t ns, int64_t cs, FxArgs a, const double* __restrict__ t,
+                                const double* __restrict__ dinv, double c1, double c2, const double* __restrict__ r,
+                                const double* __restrict__ d, double* __restrict__ x, const int32_t* __restrict__ bcn,
+                                const double* __restrict__ nrm) {
+  GRID_STRIDE(i, ns) {
+    double tv[3], dn[3], dold[3];
+    tval(a, i, cs, t, tv);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const int64_t j = i + c * cs;
+      dold[c] = d[j];
+      dn[c] = c1 * dold[c] + c2 * dinv[j] * (r[j] - tv[c]);
+    }
+    bc_project(bcn[i], nrm, dn[0], dn[1], dn[2]);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) x[i + c * cs] += dold[c] + dn[c];
+  }
+}
+__global__ void k_sub_fx(int64_t ns, int64_t cs, FxArgs a, const double* __restrict__ f, const double* __restrict__ t,
+                         double* __restrict__ r) {
+  GRID_STRIDE(i, ns) {
+    double tv[3];
+    tval(a, i, cs, t, tv);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) r[i + c * cs] = f[i + c * cs] - tv[c];
+  }
+}
+int launch_cheb0_fx(const Mesh* m, const Level& L, const double* f, const double* t, const double* dinv,
+                    double inv_theta, double* r, double* d, cudaStream_t s) {
+  const int64_t ns = macro_count(m) * L.npts2;
+  k_cheb0_fx<<<ngrid(ns), 256, 0, s>>>(ns, ns, fx_args(L), f, t, dinv, inv_theta, r, d, L.bcn2, L.g2.normal);
+  count_launch();
+  HHG_CUDA(cudaGetLastError());
+  return HHG_OK;
+}
+int launch_cheb_deg1_fx(const Mesh* m, const Level& L, const double* f, const double* t, const double* dinv,
+                        double inv_theta, double* x, cudaStream_t s) {
+  const int64_t ns = macro_count(m) * L.npts2;
+  k_cheb_deg1_fx<<<ngrid(ns), 256, 0, s>>>(ns, ns, fx_args(L), f, t, dinv, inv_theta, x, L.bcn2, L.g2.normal);
+  count_launch();
+  HHG_CUDA(cudaGetLastError());
+  return HHG_OK;
+}
+int launch_chebk_fx(const Mesh* m, const Level& L, const double* t, const double* dinv, double c1, double c2, double* x,
+                    double* r, double* d, cudaStream_t s) {
+  const int64_t ns = macro_count(m) * L.npts2;
+  k_chebk_fx<<<ngrid(ns), 256, 0, s>>>(ns, ns, fx_args(L), t, dinv, c1, c2, x, r, d, L.bcn2, L.g2.normal);
+  count_launch();
+  HHG_CUDA(cudaGetLastError());
+  return HHG_OK;
+}
+int launch_chebk_last_fx(const Mesh* m, const Level& L, const double* t, const double* dinv, double c1, double c2,
+                         const double* r, const double* d, double* x, cudaStream_t s) {
+  const int64_t ns = macro_count(m) * L.npts2;
+  k_chebk_last_fx<<<ngrid(ns), 256, 0, s>>>(ns, ns, fx_args(L), t, dinv, c1, c2, r, d, x, L.bcn2, L.g2.normal);
+  count_launch();
+  HHG_CUDA(cudaGetLastError());
+  return HHG_OK;
+}
+int launch_sub_fx(const Mesh* m, const Level& L, const double* f, const double* t, double* r, cudaStream_t s) {
+  const int64_t ns = macro_count(m) * L.npts2;
+  k_sub_fx<<<ngrid(ns), 256, 0, s>>>(ns, ns, fx_args(L), f, t, r);
+  count_launch();
+  HHG_CUDA(cudaGetLastError());
+  return HHG_OK;
+}
+
+// PCG step x += a p, r -= a q, z = P_v M D^-1 r fused with the new r.z (owner-weighted, block partials in
+// `red`, the last block sums them in fixed order -- the same reduction as k_dot_fused) into rz_out; single
+// rank only (a multi-rank dot needs an allreduce after the kernel)
+__global__ void k_pcg_update_bc_dot(int64_t ns, int64_t cs, const double* __restrict__ rzp,
+                                    const double* __restrict__ pqp, double* __restrict__ x, double* __restrict__ r,
+                                    const double* __restrict__ p, const double* __restrict__ q,
+                                    const double* __restrict__ dinv, double* __restrict__ z,
+                                    const int32_t* __restrict__ bcn, const double* __restrict__ nrm,
+                                    const uint8_t* __restrict__ own, double* __restrict__ part,
+                                    unsigned* __restrict__ counter, double* __restrict__ rz_out) {
+  const double rz = *rzp, pq = *pqp;
+  const double alpha = (rz > 1e-300 && pq != 0.0) ? rz / pq : 0.0;
+  double acc = 0.0;
+  GRID_STRIDE(i, ns) {
+    double zv[3], rv[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const int64_t j = i + c * cs;
+      x[j] += alpha * p[j];
+      rv[c] = r[j] - alpha * q[j];
+      r[j] = rv[c];
+      zv[c] = dinv[j] * rv[c];
+    }
+    bc_project(bcn[i], nrm, zv[0], zv[1], zv[2]);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) z[i + c * cs] = zv[c];
+    if (own[i]) acc += rv[0] * zv[0] + rv[1] * zv[1] + rv[2] * zv[2];
+  }
+  __shared__ double sh[32];
+  __shared__ bool last;
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) {
+      part[blockIdx.x] = v;
+      __threadfence();
+      last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    }
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double t = 0.0;
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) t += ((volatile double*)part)[i];
+  t = warp_sum(t);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = t;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) {
+      *rz_out = v;
+      *counter = 0u;
+    }
+  }
+}
+int launch_pcg_update_bc_dot(const Mesh* m, const Level& L, int it, double* scal, double* x, double* r, const double* p,
+                             const double* q, const double* dinv, double* z, double* red, cudaStream_t s) {
+  const int64_t ns = macro_count(m) * L.npts2;
+  int64_t nb = (ns + 255) / 256;
+  nb = nb < 1 ? 1 : (nb > kRedBlocks ? kRedBlocks : nb);
+  k_pcg_update_bc_dot<<<(unsigned)nb, 256, 0, s>>>(ns, ns, scal + ((it & 1) ? 2 : 0), scal + 1, x, r, p, q, dinv, z,
+                                                   L.bcn2, L.g2.normal, L.own2, red,
+                                                   reinterpret_cast<unsigned*>(red + kRedBlocks + 4),
+                                                   scal + ((it & 1) ? 0 : 2));
+  count_launch();
+  HHG_CUDA(cudaGetLastError());
+  return HHG_OK;
+}
+}  // namespace hhg

@@ -82,6 +82,7 @@ void free_level(Level& L) {
   f(L.own1);
   f(L.own2);
   f(L.bcn2);
+  f(L.gmap2);
   f(L.canon1);
   f(L.canon2);
   f(L.red);
@@ -324,7 +325,7 @@ int build_host_groups(const Mesh* m, int level, int space, std::vector<int64_t>&
 }
 
 static int build_groups(const Mesh* m, const Prims& P, int N, bool with_bc, Groups& G, std::vector<uint8_t>& own,
-                        int64_t npts, int32_t** bcn = nullptr) {
+                        int64_t npts, int32_t** bcn = nullptr, int32_t** gmap = nullptr) {
   std::vector<int64_t> ptr, copy, slot_group;
   std::vector<uint8_t> kind;
   std::vector<double> normal;
@@ -336,6 +337,12 @@ static int build_groups(const Mesh* m, const Prims& P, int N, bool with_bc, Grou
       for (int64_t k = ptr[g]; k < ptr[g + 1]; ++k) map[copy[k]] = kind[g] == HHG_BC_DIRICHLET0 ? -2 : (int32_t)g;
     }
     HHG_TRY(upload(bcn, map));
+  }
+  if (gmap) {  // per stored node: its replicated-node / BC group, -1 if none (fused interface-sum consumers)
+    std::vector<int32_t> map((size_t)npts * m->local.size(), -1);
+    for (int64_t g = 0; g + 1 < (int64_t)ptr.size(); ++g)
+      for (int64_t k = ptr[g]; k < ptr[g + 1]; ++k) map[copy[k]] = (int32_t)g;
+    HHG_TRY(upload(gmap, map));
   }
   G.n = (int64_t)ptr.size() - 1;
   G.nbc = with_bc ? (int64_t)std::count_if(kind.begin(), kind.end(), [](uint8_t k) { return k != HHG_BC_NONE; }) : 0;
@@ -462,7 +469,7 @@ int ensure_level(Mesh* m, int level) {
   Prims P;
   build_prims(m, P);
   std::vector<uint8_t> own;
-  HHG_TRY(build_groups(m, P, L.n2, true, L.g2, own, L.npts2, &L.bcn2));
+  HHG_TRY(build_groups(m, P, L.n2, true, L.g2, own, L.npts2, &L.bcn2, &L.gmap2));
   HHG_TRY(upload(&L.own2, own));
   HHG_TRY(build_groups(m, P, L.n1, false, L.g1, own, L.npts1));
   HHG_TRY(upload(&L.own1, own));

@@ -87,6 +87,7 @@ struct hhg_mg {
   std::vector<Lv> lv;
   double* scal = nullptr;    // device scalars
   double* red = nullptr;     // this object's reduction scratch (dots never share it with other objects)
+  bool fuse_fx = false;      // single rank: smoother / residual kernels do the interface sum of A's output
   // redundant coarse solve (multi-rank, prm.coarse_redundant): the l_min problem of ALL macros on every
   // rank -- a single-rank mesh/hierarchy of the global macro mesh, the rank's local macro ids, global
   // coarse vectors (the agglomeration analogue of P:443)
@@ -149,7 +150,8 @@ struct hhg_mg {
   }
 };
 
-static int mg_apply(hhg_mg* mg, int l, const double* u, double* y, cudaStream_t s, bool y_zeroed = false) {
+static int mg_apply(hhg_mg* mg, int l, const double* u, double* y, cudaStream_t s, bool y_zeroed = false,
+                    bool fixup = true) {
   const bool timed = mg->prof && l == mg->prm.l_max;
   if (timed) {
     if (mg->ev_used + 2 > mg->ev.size()) {
@@ -173,6 +175,7 @@ static int mg_apply(hhg_mg* mg, int l, const double* u, double* y, cudaStream_t 
     HHG_CUDA(cudaEventRecord(mg->ev[mg->ev_used + 1], s));
     mg->ev_used += 2;
   }
+  if (!fixup) return HHG_OK;  // the consumer sums the interface copies itself (launch_*_fx)
   return launch_fixup(mg->mesh, L, HHG_P2VEC, true, true, y, s);
 }
 
@@ -187,19 +190,28 @@ static int mg_cheb(hhg_mg* mg, int l, double* x, const double* f, bool x_is_zero
   const double theta = 0.5 * (b + a), delta = 0.5 * (b - a), sigma = theta / delta;
   double rho = 1.0 / sigma;
   const Level& LL = m->levels[l];
+  const bool fx = mg->fuse_fx;  // consumers sum the interface copies of A's raw output themselves
   const double* t0 = nullptr;
   if (!x_is_zero) {
-    HHG_TRY(mg_apply(mg, l, x, L.t, s));
+    HHG_TRY(mg_apply(mg, l, x, L.t, s, false, !fx));
     t0 = L.t;
   }
   const int deg = mg->prm.degree;
-  if (deg == 1) return launch_cheb_deg1_bc(m, LL, f, t0, L.dinv, 1.0 / theta, x, s);
-  HHG_TRY(launch_cheb0_bc(m, LL, f, t0, L.dinv, 1.0 / theta, L.r, L.d, s));
+  if (deg == 1)
+    return fx && t0 ? launch_cheb_deg1_fx(m, LL, f, t0, L.dinv, 1.0 / theta, x, s)
+                    : launch_cheb_deg1_bc(m, LL, f, t0, L.dinv, 1.0 / theta, x, s);
+  if (fx && t0) HHG_TRY(launch_cheb0_fx(m, LL, f, t0, L.dinv, 1.0 / theta, L.r, L.d, s));
+  else HHG_TRY(launch_cheb0_bc(m, LL, f, t0, L.dinv, 1.0 / theta, L.r, L.d, s));
   for (int k = 1; k < deg; ++k) {
-    HHG_TRY(mg_apply(mg, l, L.d, L.t, s));
+    HHG_TRY(mg_apply(mg, l, L.d, L.t, s, false, !fx));
     const double rn = 1.0 / (2.0 * sigma - rho);
-    if (k < deg - 1) HHG_TRY(launch_chebk_bc(m, LL, L.t, L.dinv, rn * rho, 2.0 * rn / delta, x, L.r, L.d, s));
-    else HHG_TRY(launch_chebk_last_bc(m, LL, L.t, L.dinv, rn * rho, 2.0 * rn / delta, L.r, L.d, x, s));
+    if (fx) {
+      if (k < deg - 1) HHG_TRY(launch_chebk_fx(m, LL, L.t, L.dinv, rn * rho, 2.0 * rn / delta, x, L.r, L.d, s));
+      else HHG_TRY(launch_chebk_last_fx(m, LL, L.t, L.dinv, rn * rho, 2.0 * rn / delta, L.r, L.d, x, s));
+    } else {
+      if (k < deg - 1) HHG_TRY(launch_chebk_bc(m, LL, L.t, L.dinv, rn * rho, 2.0 * rn / delta, x, L.r, L.d, s));
+      else HHG_TRY(launch_chebk_last_bc(m, LL, L.t, L.dinv, rn * rho, 2.0 * rn / delta, L.r, L.d, x, s));
+    }
     rho = rn;
   }
   return HHG_OK;
@@ -225,8 +237,12 @@ static int mg_pcg(hhg_mg* mg, int l, const double* f, double* x, cudaStream_t s)
   for (int it = 0; it < mg->prm.coarse_iters; ++it) {
     HHG_TRY(mg_apply(mg, l, p, q, s, true));
     HHG_TRY(launch_dot_fused(m, LL, HHG_P2VEC, p, q, mg->scal + 1, s, mg->red));
-    HHG_TRY(launch_pcg_update_bc(m, LL, it, mg->scal, x, r, p, q, L.dinv, z, s));
-    HHG_TRY(launch_dot_fused(m, LL, HHG_P2VEC, r, z, mg->scal + ((it & 1) ? 0 : 2), s, mg->red));
+    if (mg->fuse_fx) {  // single rank: the new r.z comes out of the update kernel
+      HHG_TRY(launch_pcg_update_bc_dot(m, LL, it, mg->scal, x, r, p, q, L.dinv, z, mg->red, s));
+    } else {
+      HHG_TRY(launch_pcg_update_bc(m, LL, it, mg->scal, x, r, p, q, L.dinv, z, s));
+      HHG_TRY(launch_dot_fused(m, LL, HHG_P2VEC, r, z, mg->scal + ((it & 1) ? 0 : 2), s, mg->red));
+    }
     HHG_TRY(launch_pcg_dir_zero(n, it, mg->scal, z, p, q, s));
   }
   return HHG_OK;
@@ -277,9 +293,14 @@ static int mg_cycle(hhg_mg* mg, int l, const double* f, double* x, cudaStream_t 
   HHG_CUDA(cudaMemsetAsync(x, 0, n * sizeof(double), s));
   for (int i = 0; i < mg->prm.pre; ++i) HHG_TRY(mg_cheb(mg, l, x, f, i == 0, s));
   // r = f - A x  (into L.r), restrict into f_{l-1}
-  HHG_TRY(mg_apply(mg, l, x, L.t, s));
-  k_sub<<<vg(n), 256, 0, s>>>(n, f, L.t, L.r);
-  count_launch();
+  if (mg->fuse_fx) {
+    HHG_TRY(mg_apply(mg, l, x, L.t, s, false, false));
+    HHG_TRY(launch_sub_fx(m, m->levels[l], f, L.t, L.r, s));
+  } else {
+    HHG_TRY(mg_apply(mg, l, x, L.t, s));
+    k_sub<<<vg(n), 256, 0, s>>>(n, f, L.t, L.r);
+    count_launch();
+  }
   auto& C = mg->lv[l - 1];
   HHG_TRY(p2_restrict(mg->mesh, l, L.r, C.f, (hhg_stream_t)s));
   HHG_TRY(mg_cycle(mg, l - 1, C.f, C.x, s));
@@ -337,6 +358,10 @@ int hhg_mg_create_qeta(hhg_mesh* mesh, const hhg_mg_params* params, const double
     return code;
   };
   ++mesh->dependents;
+  {
+    const char* e = getenv("HHG_NO_FX");  // A/B switch for measurements
+    mg->fuse_fx = mesh->nranks == 1 && !(e && e[0] == '1');
+  }
   if (cudaMalloc(&mg->scal, 16 * sizeof(double)) != cudaSuccess) return bail(fail(HHG_ENOMEM, "scal"));
   if (red_alloc(&mg->red) != HHG_OK) return bail(HHG_ENOMEM);
   for (int l = P.l_min; l <= P.l_max; ++l) {
