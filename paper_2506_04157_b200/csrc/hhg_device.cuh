@@ -1,8 +1,28 @@
 // Device helpers shared by several kernel files (interface-group sums, per-node BC projection).
 #pragma once
+#include <cstdio>
+
 #include "hhg_internal.h"
 
 namespace hhg {
+
+// Bounds checks of our own (compute-sanitizer is closed on this pool): built with -DHHG_CHECKED, every
+// global index of the element kernels, interface sums and transfers is checked against its vector length
+// and a violation prints the kernel, index and bound and traps.  Compiled out otherwise.
+#ifdef HHG_CHECKED
+#define HHG_CHECK(cond, what, idx, bound)                                                                    \
+  do {                                                                                                      \
+    if (!(cond)) {                                                                                          \
+      printf("HHG_CHECKED: %s out of range: %lld (bound %lld) block (%d,%d) thread %d\n", what,            \
+             (long long)(idx), (long long)(bound), (int)blockIdx.x, (int)blockIdx.y, (int)threadIdx.x);     \
+      __trap();                                                                                             \
+    }                                                                                                       \
+  } while (0)
+#else
+#define HHG_CHECK(cond, what, idx, bound) \
+  do {                                    \
+  } while (0)
+#endif
 
 // Sum of the copies of group gi (copies gathered in chunks of 4 independent loads: macro vertices
 // have up to ~20 copies and a sequential dependent walk made coarse levels latency-bound).
@@ -16,6 +36,8 @@ __device__ __forceinline__ void group_sum(int64_t b, int64_t e, const int64_t* _
     int64_t idx[CH];
 #pragma unroll
     for (int j = 0; j < CH; ++j) idx[j] = (k0 + j < e) ? copy[k0 + j] : -1;
+#pragma unroll
+    for (int j = 0; j < CH; ++j) HHG_CHECK(idx[j] < cstride || NC == 1, "group copy", idx[j], cstride);
     double x[CH][NC];
 #pragma unroll
     for (int j = 0; j < CH; ++j)

@@ -640,6 +640,7 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
       const int gx = 2 * i0 + X, gy = 2 * j0 + Y, gz = 2 * k0 + Z;
       if (gx + gy + gz > n2) continue;
       const double* src = u + mb2 + rowstart32(n2, gy, gz) + gx;
+      HHG_CHECK(src - u >= mb2 && src - u < mb2 + npts2 && mb2 + npts2 <= cstride, "u stage", src - u, cstride);
       const int w = fword(X, Y, Z);
 #pragma unroll
       for (int c = 0; c < 3; ++c) cp_async8(su + c * kFU + w, src + c * cstride);
@@ -686,6 +687,7 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
     const int gx = i0 + X, gy = j0 + Y, gz = k0 + Z;
     if (gx + gy + gz > n1) continue;
     const int64_t ix = mb1 + rowstart32(n1, gy, gz) + gx;
+    HHG_CHECK(ix >= mb1 && ix < mb1 + npts1 && ix < (int64_t)gridDim.y * npts1, "P1 stage", ix, npts1);
     if (eta != nullptr) cp_async8(se + L, eta + ix);
     else se[L] = 1.0;
     if (NEED_P) cp_async8(sp + L, p + ix);
@@ -736,6 +738,7 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
         const int Z = o / kPZ, Y = (o % kPZ) / kPY, xw = o % kPY;
         const int X = xw >= 5 ? 2 * (xw - 5) + 1 : 2 * xw;
         double* dst = yu + mb2 + rowstart32(n2, 2 * (j0 + y) + Y, 2 * (k0 + z) + Z) + 2 * (i0 + x) + X;
+        HHG_CHECK(dst - yu >= mb2 && dst - yu < mb2 + npts2, "sparse RED", dst - yu, mb2 + npts2);
 #pragma unroll
         for (int c = 0; c < 3; ++c) atomicAdd(dst + c * cstride, acc[a][c]);
       }
@@ -832,6 +835,7 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
       if (gx + gy + gz > n2) continue;
       const int wxy = xs(X) + kPY * Y;
       double* dst = yu + mb2 + rowstart32(n2, gy, gz) + gx;
+      HHG_CHECK(dst - yu >= mb2 && dst - yu < mb2 + npts2, "write-out", dst - yu, mb2 + npts2);
       const bool border = X == 0 || Y == 0 || Z == 0 || X == 8 || Y == 8 || Z == 8;
 #pragma unroll
       for (int c = 0; c < 3; ++c) {

@@ -51,7 +51,10 @@ __global__ void k_halo_pack(int64_t nslots, const int64_t* __restrict__ slot_gro
 #pragma unroll
   for (int c = 0; c < NC; ++c) {
     double s = 0.0;
-    for (int64_t k = b; k < e; ++k) s += v[c * cstride + copy[k]];
+    for (int64_t k = b; k < e; ++k) {
+      HHG_CHECK(NC == 1 || copy[k] < cstride, "halo pack copy", copy[k], cstride);
+      s += v[c * cstride + copy[k]];
+    }
     sbuf[sl * NC + c] = s;
   }
 }
@@ -421,6 +424,7 @@ __global__ void k_prolong(const int32_t* __restrict__ rowsf, int64_t nrowsf, int
       if (e < n) {
         const int d = __ldg(&gPd[cls][e]);
         const int ci = srs[w][d / 3] + bx + d % 3;
+        HHG_CHECK(ci >= 0 && ci < nptsc, "prolong gather", ci, nptsc);
         const double wt = __ldg(&gPw[cls][e]);
         s0 += wt * __ldg(cm + ci);
         s1 += wt * __ldg(cm + cstridec + ci);
@@ -472,6 +476,7 @@ __global__ void k_restrict(const int32_t* __restrict__ rowsc, int64_t nrowsc, in
       const int rs = srs[w][(dy + 8) + 17 * (dz + 8)];
       const bool in = fx >= 0 && rs >= 0 && fx + dy + dz <= lim;
       const int fi = in ? rs + fx : 0;
+      HHG_CHECK(fi >= 0 && fi < nptsf, "restrict gather", fi, nptsf);
       const double wt = (in && om[fi]) ? __ldg(&gRw[pc][e]) : 0.0;
       s0 += wt * __ldg(rm + fi);
       s1 += wt * __ldg(rm + cstridef + fi);
