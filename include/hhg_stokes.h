@@ -298,6 +298,11 @@ typedef struct {
                                 zero-padded global vector) and solve it redundantly on every rank -- the analogue
                                 of the paper's coarse-grid agglomeration; 0: distributed PCG
                                 (an interface exchange + 2 allreduces per coarse iteration) */
+  double coarse_tol;         /* 0: exactly coarse_iters Jacobi-PCG iterations (BASELINE config 3).  > 0: stop as soon
+                                as sqrt(r.z) <= coarse_tol sqrt(r0.z0), at most coarse_iters iterations -- the paper's
+                                coarse solve "up to a relative tolerance tol_coarse" (Table 1: 1e-2; DESIGN.md
+                                R26).  Needs the cluster-resident coarse solver (single-rank mesh or
+                                coarse_redundant): HHG_EINVAL otherwise. */
 } hhg_mg_params;
 
 /* hhg_mg_create: builds per-level workspaces, diag(A) and D^-1, and lambda_hat per
@@ -319,6 +324,9 @@ int epsilon_apply_qeta(const hhg_mesh* mesh, int level, const double* T_p2, doub
                        const double* u, double* y, hhg_stream_t stream);
 int hhg_diag_qeta(const hhg_mesh* mesh, int level, const double* T_p2, double lnC, double jump, double r_jump,
                   double* diag, hhg_stream_t stream);
+/* Iterations taken by the most recent coarse solve of the hierarchy (coarse_tol > 0: data dependent).
+ * Synchronises the device.  HHG_EINVAL if the coarse level does not run the cluster-resident solver. */
+int hhg_mg_coarse_iterations(const hhg_mg* mg, int* iters_out);
 int hhg_mg_lambda(const hhg_mg* mg, int level, double* lambda_host);
 /* One V-cycle (fig:ASolverStructure) from x = 0: x = V(rhs). */
 int vcycle(hhg_mg* mg, const double* rhs, double* x, hhg_stream_t stream);

@@ -121,15 +121,19 @@ def power_iteration(Ac, dinv, Pm, v0, iters=20):
     return lam
 
 
-def pcg(Ac, dinv, Pm, f, iters=50):
-    """Exactly `iters` Jacobi-preconditioned CG iterations from x = 0 (stop early only if r.z <= 1e-300)."""
+def pcg(Ac, dinv, Pm, f, iters=50, tol=0.0, count=False):
+    """Jacobi-preconditioned CG from x = 0: exactly `iters` iterations (stop early only if r.z <= 1e-300), or,
+    with tol > 0, until sqrt(r.z) <= tol sqrt(r0.z0), at most `iters` -- the coarse solve "up to a relative
+    tolerance tol_coarse" of P:443 (Table 1: 1e-2; R26).  count=True also returns the iterations."""
     x = np.zeros_like(f)
     r = f.copy()
     z = Pm @ (dinv * r)
     p = z.copy()
     rz = float(r @ z)
-    for _ in range(iters):
-        if rz <= 1e-300:
+    rz0 = rz
+    it = 0
+    for it in range(iters + 1):
+        if it == iters or rz <= 1e-300 or (tol > 0 and rz <= tol * tol * rz0):
             break
         q = Ac @ p
         alpha = rz / float(p @ q)
@@ -140,14 +144,15 @@ def pcg(Ac, dinv, Pm, f, iters=50):
         beta = rz_new / rz
         p = z + beta * p
         rz = rz_new
-    return x
+    return (x, it) if count else x
 
 
 class Hierarchy:
     """Per-level constrained operators Ac, D^-1, P_v M, lambda_hat, and transfers between levels."""
 
     def __init__(self, discs: dict, power_v0: dict, pre=3, post=3, degree=3, power_iters=20,
-                 coarse_iters=50, hi_factor=1.1):
+                 coarse_iters=50, hi_factor=1.1, coarse_tol=0.0):
+        self.coarse_tol = coarse_tol
         self.levels = sorted(discs)
         self.lmin, self.lmax = self.levels[0], self.levels[-1]
         self.pre, self.post, self.degree, self.coarse_iters = pre, post, degree, coarse_iters
@@ -177,7 +182,7 @@ class Hierarchy:
         """fig:ASolverStructure (P:445-450) from x = 0."""
         l = self.lmax if l is None else l
         if l == self.lmin:
-            return pcg(self.Ac[l], self.dinv[l], self.Pm[l], f, self.coarse_iters)
+            return pcg(self.Ac[l], self.dinv[l], self.Pm[l], f, self.coarse_iters, self.coarse_tol)
         b = self.hi_factor * self.lam[l]
         x = np.zeros_like(f)
         for _ in range(self.pre):

@@ -36,7 +36,7 @@ EXPORTS = [
     "hhg_vec_len", "hhg_canonical_len", "hhg_canonical_keys", "hhg_to_canonical", "hhg_from_canonical",
     "hhg_node_coords", "hhg_apply_bc", "hhg_interface_sum", "epsilon_apply", "div_apply", "divT_apply",
     "stokes_apply", "hhg_diag", "hhg_dot", "p2_restrict", "p2_prolong", "chebyshev_smooth",
-    "hhg_power_iteration", "hhg_mg_create", "hhg_mg_lambda", "vcycle", "vcycle_host", "hhg_mg_profile",
+    "hhg_power_iteration", "hhg_mg_create", "hhg_mg_lambda", "hhg_mg_coarse_iterations", "vcycle", "vcycle_host", "hhg_mg_profile",
     "hhg_mg_profile_get", "hhg_mg_destroy", "hhg_launch_count",
     "hhg_mesh_create_part", "hhg_partition_rcb", "hhg_mesh_rank", "hhg_halo_info", "hhg_halo_keys",
     "hhg_owned_count", "hhg_halo_pack", "hhg_interface_sum_remote", "epsilon_apply_partial",
@@ -76,7 +76,7 @@ def _load():
         "p2_restrict": ([P, I, P, P, P], I), "p2_prolong": ([P, I, P, P, P], I),
         "chebyshev_smooth": ([P, I, P, P, I, D, D, P, P, P, P], I),
         "hhg_power_iteration": ([P, I, P, P, I, P, P, P], I),
-        "hhg_mg_create": ([P, P, P, P, P], I), "hhg_mg_lambda": ([P, I, P], I), "vcycle": ([P, P, P, P], I),
+        "hhg_mg_create": ([P, P, P, P, P], I), "hhg_mg_lambda": ([P, I, P], I), "hhg_mg_coarse_iterations": ([P, P], I), "vcycle": ([P, P, P, P], I),
         "vcycle_host": ([P, P, P, P], I), "hhg_mg_profile": ([P, I], I),
         "hhg_mg_profile_get": ([P, P, P, P, P], I), "hhg_mg_destroy": ([P], I),
         "hhg_mesh_create_part": ([P, I64, P, I64, P, I, P, I, I, P], I),
@@ -613,7 +613,7 @@ class _MGParams(ctypes.Structure):
                 ("cheb_hi_factor", ctypes.c_double), ("cheb_lo_ratio", ctypes.c_double),
                 ("visc_form", ctypes.c_int), ("use_graph", ctypes.c_int), ("l_eta", ctypes.c_int),
                 ("qeta_lnC", ctypes.c_double), ("qeta_jump", ctypes.c_double), ("qeta_rjump", ctypes.c_double),
-                ("coarse_redundant", ctypes.c_int)]
+                ("coarse_redundant", ctypes.c_int), ("coarse_tol", ctypes.c_double)]
 
 
 class MG:
@@ -621,14 +621,16 @@ class MG:
 
     def __init__(self, mesh, l_min, l_max, eta_per_level, power_v0, pre=3, post=3, degree=3, power_iters=20,
                  coarse_iters=50, hi=1.1, lo=0.1, form=HHG_VISC_FULL, use_graph=True, T2_per_level=None, l_eta=-1,
-                 qeta=(0.0, 1.0, 0.0), coarse_redundant=True):
+                 qeta=(0.0, 1.0, 0.0), coarse_redundant=True, coarse_tol=0.0):
         """T2_per_level / l_eta / qeta = (lnC, jump, r_jump): on levels <= l_eta the viscosity is evaluated
         at the quadrature points from the P2 temperature (NEXT-2 tier).  coarse_redundant
-        (multi-rank meshes): solve the gathered coarse problem on every rank."""
+        (multi-rank meshes): solve the gathered coarse problem on every rank.  coarse_tol > 0:
+        the coarse PCG stops at sqrt(r.z) <= coarse_tol sqrt(r0.z0), at most coarse_iters (Table 1)."""
         self.mesh = mesh
         self.l_min, self.l_max = l_min, l_max
         prm = _MGParams(l_min, l_max, pre, post, degree, power_iters, coarse_iters, hi, lo, form,
-                        1 if use_graph else 0, int(l_eta), *[float(v) for v in qeta], 1 if coarse_redundant else 0)
+                        1 if use_graph else 0, int(l_eta), *[float(v) for v in qeta], 1 if coarse_redundant else 0,
+                        float(coarse_tol))
         self._eta = dict(eta_per_level)
         self._v0 = dict(power_v0)
         self._T2 = dict(T2_per_level or {})
@@ -651,6 +653,12 @@ class MG:
     def lam(self, level):
         v = ctypes.c_double()
         _chk(_lib.hhg_mg_lambda(self.handle, level, ctypes.byref(v)))
+        return v.value
+
+    def coarse_iterations(self):
+        """iterations of the most recent coarse solve (synchronises)"""
+        v = ctypes.c_int()
+        _chk(_lib.hhg_mg_coarse_iterations(self.handle, ctypes.byref(v)))
         return v.value
 
     def vcycle(self, rhs, x=None, stream=None):

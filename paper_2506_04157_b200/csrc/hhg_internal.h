@@ -246,6 +246,14 @@ int transfer_prepare();
 int launch_dot_fused(const Mesh* m, const Level& L, int space, const double* x, const double* y, double* out,
                      cudaStream_t s, double* red);
 int launch_scalar_ops(int op, double* scal, cudaStream_t s);
+// cluster-resident coarse Jacobi-PCG (hhg_coarse.cu): one kernel per coarse solve on a single-rank mesh
+struct CoarseSolver;
+int coarse_create(const Mesh* m, int level, int form, const double* eta, const double* T2, double lnC, double jump,
+                  double rjump, const double* dinv, CoarseSolver** out);
+int coarse_run(CoarseSolver* c, const double* f, double* x, double* r, double* z, double* p, double* q, int iters,
+               double tol, cudaStream_t s);
+int coarse_iterations(const CoarseSolver* c, int* out);  // iterations of the last run (synchronises)
+void coarse_destroy(CoarseSolver* c);
 int launch_fill(int64_t n, double v, double* y, cudaStream_t s);
 int launch_recip(int64_t n, double* y, cudaStream_t s);                          // y = 1 / y
 int launch_pcg_scale(int64_t n, const double* d, const double* x, double* y, cudaStream_t s);  // y = d x

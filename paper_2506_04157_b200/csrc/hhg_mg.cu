@@ -88,6 +88,7 @@ struct hhg_mg {
   double* scal = nullptr;    // device scalars
   double* red = nullptr;     // this object's reduction scratch (dots never share it with other objects)
   bool fuse_fx = false;      // single rank: smoother / residual kernels do the interface sum of A's output
+  CoarseSolver* ccs = nullptr;  // single rank: the coarse PCG as one cluster-resident kernel (hhg_coarse.cu)
   // redundant coarse solve (multi-rank, prm.coarse_redundant): the l_min problem of ALL macros on every
   // rank -- a single-rank mesh/hierarchy of the global macro mesh, the rank's local macro ids, global
   // coarse vectors (the agglomeration analogue of P:443)
@@ -129,6 +130,7 @@ struct hhg_mg {
     for (void* p : {(void*)cids, (void*)cf, (void*)cx, (void*)ceta, (void*)cT2})
       if (p) cudaFree(p);
     if (mesh) --mesh->dependents;
+    if (ccs) coarse_destroy(ccs);
     if (hbuf_rhs) cudaFree(hbuf_rhs);
     if (hbuf_x) cudaFree(hbuf_x);
     if (gexec) cudaGraphExecDestroy(gexec);
@@ -229,6 +231,7 @@ static int mg_pcg(hhg_mg* mg, int l, const double* f, double* x, cudaStream_t s)
   double* z = L.d;
   double* p = L.p;
   double* q = L.t;
+  if (mg->ccs) return coarse_run(mg->ccs, f, x, r, z, p, q, mg->prm.coarse_iters, mg->prm.coarse_tol, s);
   HHG_CUDA(cudaMemsetAsync(x, 0, n * sizeof(double), s));
   HHG_TRY(launch_cheb0_bc(m, LL, f, nullptr, L.dinv, 1.0, r, z, s));  // r = f, z = PM dinv r
   HHG_CUDA(cudaMemcpyAsync(p, z, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
@@ -347,7 +350,7 @@ int hhg_mg_create_qeta(hhg_mesh* mesh, const hhg_mg_params* params, const double
   const hhg_mg_params& P = *params;
   if (P.l_min < 0 || P.l_max > mesh->level_max || P.l_min > P.l_max)
     return fail(HHG_ELEVEL, "hhg_mg_create: need 0 <= l_min <= l_max <= level_max");
-  if (P.degree < 1 || P.pre < 0 || P.post < 0 || P.coarse_iters < 0 || P.power_iters < 1)
+  if (P.degree < 1 || P.pre < 0 || P.post < 0 || P.coarse_iters < 0 || P.power_iters < 1 || !(P.coarse_tol >= 0.0))
     return fail(HHG_EINVAL, "hhg_mg_create: bad smoother parameters");
   auto* mg = new hhg_mg();
   mg->mesh = mesh;
@@ -393,6 +396,18 @@ int hhg_mg_create_qeta(hhg_mesh* mesh, const hhg_mg_params* params, const double
       if (r != HHG_OK) return bail(r);
     }
   }
+  {
+    const char* e = getenv("HHG_NO_CCL");  // A/B switch: the coarse PCG through the generic launches
+    if (mg->fuse_fx && !mesh->comm && !(e && e[0] == '1')) {
+      auto& C = mg->lv[P.l_min];
+      const int r = coarse_create(mesh, P.l_min, P.visc_form, C.eta, C.T2, P.qeta_lnC, P.qeta_jump, P.qeta_rjump,
+                                  C.dinv, &mg->ccs);
+      if (r != HHG_OK) return bail(r);
+    }
+  }
+  if (P.coarse_tol > 0.0 && !mg->ccs && !(P.coarse_redundant && mesh->nranks > 1))
+    return bail(fail(HHG_EINVAL, "hhg_mg_create: coarse_tol > 0 needs the cluster-resident coarse solver "
+                                 "(single-rank mesh or coarse_redundant)"));
   if (P.coarse_redundant && mesh->nranks > 1) {
     // the coarse level of all macros on every rank: global mesh (no communicator), global eta (and T2)
     const int lc = P.l_min;
@@ -441,6 +456,13 @@ int hhg_mg_create_qeta(hhg_mesh* mesh, const hhg_mg_params* params, const double
   if (cudaDeviceSynchronize() != cudaSuccess) return bail(fail(HHG_ECUDA, "hhg_mg_create: sync failed"));
   *out = mg;
   return HHG_OK;
+}
+
+int hhg_mg_coarse_iterations(const hhg_mg* mg, int* iters_out) {
+  if (!mg || !iters_out) return fail(HHG_EINVAL, "NULL argument");
+  if (mg->cmg) return hhg_mg_coarse_iterations(mg->cmg, iters_out);
+  if (!mg->ccs) return fail(HHG_EINVAL, "hhg_mg_coarse_iterations: the coarse level runs the generic PCG");
+  return coarse_iterations(mg->ccs, iters_out);
 }
 
 int hhg_mg_lambda(const hhg_mg* mg, int level, double* lambda_host) {

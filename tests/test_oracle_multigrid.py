@@ -76,6 +76,40 @@ def test_pcg_solves_small_spd_exactly():
     assert np.all(pcg(A, 1.0 / A.diagonal(), sp.identity(n, format="csr"), 0 * f, 50) == 0)
 
 
+def test_pcg_tolerance_stop_textbook_counts():
+    """Coarse PCG to a relative tolerance (Table 1 tol_coarse; R26).  Textbook pins: CG on an SPD
+    matrix with k distinct eigenvalues terminates in k steps (and not before), so with a tight tolerance the count
+    is exactly k and the solution exact; on a diagonal matrix Jacobi-PCG converges in ONE step.  Consistency: the tolerance run equals
+    the fixed-iteration run with that count, and its r.z meets the bound while one iteration fewer does not."""
+    rng = np.random.default_rng(5)
+    n, k = 40, 5
+    Q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    lam = np.repeat(np.array([1.0, 3.0, 10.0, 40.0, 200.0]), n // k)
+    A = sp.csr_matrix(Q @ np.diag(lam) @ Q.T)
+    I = sp.identity(n, format="csr")
+    f = rng.standard_normal(n)
+    ones = np.ones(n)
+    x, it = pcg(A, ones, I, f, 100, tol=1e-8, count=True)
+    assert it == k and np.abs(A @ x - f).max() < 1e-9 * np.abs(f).max()
+    D = sp.diags(rng.uniform(1.0, 100.0, n)).tocsr()
+    xd, itd = pcg(D, 1.0 / D.diagonal(), I, f, 100, tol=1e-12, count=True)
+    assert itd == 1 and np.allclose(D @ xd, f, rtol=0, atol=1e-13 * np.abs(f).max())
+    # ill-conditioned: a loose tolerance stops early; the stop is the first iteration meeting the bound
+    M = rng.standard_normal((n, n))
+    B = sp.csr_matrix(M @ M.T + 1e-3 * np.eye(n))
+    dB = 1.0 / B.diagonal()
+    xt, itt = pcg(B, dB, I, f, 500, tol=1e-2, count=True)
+    assert 1 < itt < 500
+    assert np.array_equal(xt, pcg(B, dB, I, f, itt))
+    rz0 = float(f @ (dB * f))
+    def rz_after(m):
+        xm = pcg(B, dB, I, f, m)
+        rm = f - B @ xm
+        return float(rm @ (dB * rm))
+    assert rz_after(itt) <= 1e-4 * rz0 * (1 + 1e-9)
+    assert rz_after(itt - 1) > 1e-4 * rz0 * (1 - 1e-9)
+
+
 @pytest.fixture(scope="module")
 def shell_hierarchy():
     m = icoshell(3, 2)
