@@ -301,7 +301,7 @@ typedef struct {
   double coarse_tol;         /* 0: exactly coarse_iters Jacobi-PCG iterations (BASELINE config 3).  > 0: stop as soon
                                 as sqrt(r.z) <= coarse_tol sqrt(r0.z0), at most coarse_iters iterations -- the paper's
                                 coarse solve "up to a relative tolerance tol_coarse" (Table 1: 1e-2; DESIGN.md
-                                R26).  Needs the cluster-resident coarse solver (single-rank mesh or
+                                R29).  Needs the cluster-resident coarse solver (single-rank mesh or
                                 coarse_redundant): HHG_EINVAL otherwise. */
 } hhg_mg_params;
 

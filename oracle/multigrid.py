@@ -124,7 +124,7 @@ def power_iteration(Ac, dinv, Pm, v0, iters=20):
 def pcg(Ac, dinv, Pm, f, iters=50, tol=0.0, count=False):
     """Jacobi-preconditioned CG from x = 0: exactly `iters` iterations (stop early only if r.z <= 1e-300), or,
     with tol > 0, until sqrt(r.z) <= tol sqrt(r0.z0), at most `iters` -- the coarse solve "up to a relative
-    tolerance tol_coarse" of P:443 (Table 1: 1e-2; R26).  count=True also returns the iterations."""
+    tolerance tol_coarse" of P:443 (Table 1: 1e-2; R29).  count=True also returns the iterations."""
     x = np.zeros_like(f)
     r = f.copy()
     z = Pm @ (dinv * r)

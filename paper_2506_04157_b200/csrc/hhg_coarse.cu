@@ -4,18 +4,21 @@
 // The coarsest level is tiny (shell(3,2) L1: 1 920 micro tets, 8 400 stored P2 nodes), so the generic path
 // -- element kernel, interface sum, fused dot, update, direction: five launches per iteration -- is bound by
 // launch gaps and tails (~36 us per iteration, ~1.8 ms of a 26 ms V-cycle).  Here every PCG iteration runs
-// inside one kernel on a cluster of kCl CTAs separated by hardware cluster barriers:
+// inside one kernel on ONE cluster of kCl CTAs (compile-time cluster shape: it is part of the function, so a
+// CUDA-graph capture of the launch cannot lose it), phases separated by hardware cluster barriers:
 //   A  q_e = A_e p'  per micro tet (tet_body, the same arithmetic as the brick kernel), p' = z + beta p
-//      formed on the fly; the 30 element outputs go to a per-tet buffer E (no atomics);
-//   B  per stored node: p = z + beta p (stored), q = sum of the E slots of every copy of the node's
-//      interface group in a fixed host-built order (so all copies are bitwise equal) + the group's BC
-//      (= element kernel + k_fixup(sum, BC)); partial p.q over owned nodes;
-//   C  alpha = r.z / p.q; x += alpha p, r -= alpha q, z = P_v M D^-1 r; partial r.z;
-// three cluster barriers per iteration; the dots are reduced in fixed order by every CTA (deterministic,
-// identical scalars everywhere).  Data written inside the kernel is read with ld.global.cg (L2), never
-// through the non-coherent L1.  Semantics = mg_pcg (hhg_mg.cu) with the brick element kernel.
+//      formed on the fly; the 30 element outputs go to a buffer E ordered by unique node (no atomics);
+//   B  per UNIQUE node u (an interface/BC group of g2, or a stored node in no group): q_u = the sum of u's
+//      contiguous E segment (the outputs of every tet of every copy, fixed host-built order) + the group's BC
+//      (= element kernel + k_fixup(sum, BC)); p = z + beta p; both written to every copy; partial p.q;
+//   C  alpha = r.z / p.q; x += alpha p, r -= alpha q, z = P_v M D^-1 r on every copy; partial r.z;
+// three cluster barriers per iteration; vectors stay consistent, so each scalar step runs once per unique node
+// and the dots need no owner mask; the dots are reduced in fixed order by every CTA (deterministic, identical
+// scalars everywhere).  Data written inside the kernel is read with ld.global.cg (L2), never through the
+// non-coherent L1.  Semantics = mg_pcg (hhg_mg.cu) with the brick element kernel.
 #include <cooperative_groups.h>
 
+#include <algorithm>
 #include <vector>
 
 #include "hhg_internal.h"
@@ -27,7 +30,8 @@ namespace cg = cooperative_groups;
 namespace hhg {
 
 constexpr int kCT = 256;   // threads per CTA
-constexpr int kClMax = 16; // non-portable cluster size (falls back to 8)
+constexpr int kCl = 8;     // CTAs per cluster (compile-time __cluster_dims__: kept by CUDA-graph capture)
+constexpr int kClMax = kCl;
 
 struct CoarseArgs {
   int64_t ns;               // stored P2 nodes (= component stride)
@@ -40,14 +44,18 @@ struct CoarseArgs {
   const int32_t* p1;        // [4][ntet] stored P1 index of vertex v
   const int32_t* info;      // [ntet] macro | type << 24
   const int32_t* anc;       // [ntet] cube anchor i | j << 10 | k << 20
-  const int32_t* sb;        // [ns] first slot of the node's gather list
-  const int32_t* se;        // [ns] one past the last slot
-  const int32_t* slot;      // slots a * ntet + tet
-  const int32_t* gmap;      // [ns] interface/BC group or -1
+  const int32_t* pos;       // [10][ntet] slot of element output (tet, a) in the node-ordered buffer E
+  int nu, ng;               // unique nodes; the first ng are the interface/BC groups of g2 (same ids)
+  const int32_t* ucp;       // [nu+1] CSR of the stored copies of u
+  const int32_t* ucopy;     // stored copies (the first is the representative)
+  const int32_t* urep;      // [nu] representative copy of u
+  const int32_t* ub;        // [kCl+1] unique nodes of CTA b: [ub[b], ub[b+1])
+  const int32_t* ib;        // [kCl+1] items of CTA b: [ib[b], ib[b+1])
+  const int32_t* item;      // [nitems+1] E range of item k: [item[k], item[k+1]) (<= kIt entries, one node each)
+  const int32_t* uitem;     // [nu+1] items of unique node u: [uitem[u], uitem[u+1])
   const uint8_t* kind;      // group BC kind
   const double* normal;     // group normals [3]
   const int32_t* bcn;       // per node BC for P_v M on directions
-  const uint8_t* own;
   const double* eta;        // P1 viscosity (nullptr: 1)
   const double* T2;         // P2 temperature (quadrature-point viscosity tier)
   EtaQ eq;
@@ -91,13 +99,17 @@ struct GT {
   __device__ __forceinline__ double operator()(int a) const { return t[a]; }
 };
 
+constexpr int kIt = 16;   // E entries per work item (one load round trip)
+constexpr int kNP = 4;    // unique nodes per thread per pass (their loads issued together)
+
 template <bool BLEND, bool FULL, bool ETAQ>
-__global__ void __launch_bounds__(kCT, 1) k_coarse_pcg(CoarseArgs a) {
+__global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kCT, 1) k_coarse_pcg(CoarseArgs a) {
   cg::cluster_group cl = cg::this_cluster();
   __shared__ double sh[kCT / 32];
+  extern __shared__ double dsm[];
   const int nthr = gridDim.x * blockDim.x;
-  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t ns = a.ns, cs = a.ns;
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x, tid = threadIdx.x;
+  const int64_t cs = a.ns;
   double* part = a.part;  // [3][kClMax] ping-pong partials (each buffer reused two barriers later)
   int pb = 0;
   auto next_part = [&]() {
@@ -105,32 +117,43 @@ __global__ void __launch_bounds__(kCT, 1) k_coarse_pcg(CoarseArgs a) {
     pb = (pb + 1) % 3;
     return P;
   };
+  // this CTA's unique nodes [u0, u1) and items [i0, i1); shared: item partials [3][ni], q [3][nl]
+  const int u0 = a.ub[blockIdx.x], u1 = a.ub[blockIdx.x + 1], nl = u1 - u0;
+  const int i0 = a.ib[blockIdx.x], i1 = a.ib[blockIdx.x + 1], ni = i1 - i0;
+  double* ps = dsm;             // [3][ni]
+  double* qs = dsm + 3 * ni;    // [3][nl]
+  auto store_all = [&](int u, double* v, const double (&val)[3]) {
+    for (int k = __ldg(a.ucp + u), ke = __ldg(a.ucp + u + 1); k < ke; ++k) {
+      const int64_t i = __ldg(a.ucopy + k);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) v[i + c * cs] = val[c];
+    }
+  };
 
-  // x = 0, r = f, z = P_v M D^-1 r, p = z, rz = r.z
+  // x = 0, r = f, z = P_v M D^-1 r, p = z (x, r at the representative; z, p on every copy); rz = r.z
   double acc = 0.0;
-  for (int64_t i = gt; i < ns; i += nthr) {
+  for (int l = tid; l < nl; l += kCT) {
+    const int u = u0 + l;
+    const int64_t i = __ldg(a.urep + u);
     double rv[3], zv[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      const int64_t j = i + c * cs;
-      rv[c] = a.f[j];
-      zv[c] = a.dinv[j] * rv[c];
-      a.x[j] = 0.0;
-      a.r[j] = rv[c];
+      rv[c] = a.f[i + c * cs];
+      zv[c] = __ldg(a.dinv + i + c * cs) * rv[c];
+      a.x[i + c * cs] = 0.0;
+      a.r[i + c * cs] = rv[c];
     }
-    bc_project(a.bcn[i], a.normal, zv[0], zv[1], zv[2]);
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      a.z[i + c * cs] = zv[c];
-      a.p[i + c * cs] = zv[c];
-    }
-    if (a.own[i]) acc += rv[0] * zv[0] + rv[1] * zv[1] + rv[2] * zv[2];
+    bc_project(__ldg(a.bcn + i), a.normal, zv[0], zv[1], zv[2]);
+    store_all(u, a.z, zv);
+    store_all(u, a.p, zv);
+    acc += rv[0] * zv[0] + rv[1] * zv[1] + rv[2] * zv[2];
   }
   double rz = cluster_sum(acc, next_part(), sh, cl);
   const double rz_stop = a.tol2 * rz;  // every thread holds the same rz: the exit below is uniform
   double beta = 0.0;
 
   const int nt = a.ntet;
+  const int64_t ne = 10 * (int64_t)nt;  // component stride of E
   int it = 0;
   for (; it < a.iters; ++it) {
     if (a.tol2 > 0.0 && (rz <= rz_stop || rz <= 1e-300)) break;
@@ -173,61 +196,117 @@ __global__ void __launch_bounds__(kCT, 1) k_coarse_pcg(CoarseArgs a) {
       double accE[10][3], gy[4];
       tet_body<BLEND, ELEM_A, FULL, GU, ETAQ, GT>(G, wdet, xa, nh, cK, 0.0, uu, et, pp, accE, gy, tt, a.eq);
 #pragma unroll
-      for (int k = 0; k < 10; ++k)
+      for (int k = 0; k < 10; ++k) {
+        const int64_t ps_ = __ldg(a.pos + k * nt + e);
 #pragma unroll
-        for (int c = 0; c < 3; ++c) a.E[(int64_t)(c * 10 + k) * nt + e] = accE[k][c];
+        for (int c = 0; c < 3; ++c) a.E[c * ne + ps_] = accE[k][c];
+      }
     }
     cl.sync();
-    // ---- B: p = z + beta p; q = interface sum of the element outputs + BC; partial p.q
+    // ---- B1: item partial sums (<= kIt contiguous E entries of one node, summed in order) into shared memory
+    for (int k = tid; k < ni; k += kCT) {
+      const int e0 = __ldg(a.item + i0 + k), e1 = __ldg(a.item + i0 + k + 1);
+      double v[kIt][3];
+#pragma unroll
+      for (int j = 0; j < kIt; ++j)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) v[j][c] = (e0 + j < e1) ? ldcg(a.E + c * ne + e0 + j) : 0.0;
+      double sv[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+      for (int j = 0; j < kIt; ++j)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) sv[c] += v[j][c];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) ps[c * ni + k] = sv[c];
+    }
+    __syncthreads();
+    // ---- B2: q_u = sum of u's item partials (in order) + the group's BC (= element kernel + k_fixup(sum, BC));
+    // p = z + beta p on every copy; partial p.q
     acc = 0.0;
-    for (int64_t i = gt; i < ns; i += nthr) {
-      double qv[3] = {0.0, 0.0, 0.0}, pv[3];
-      const int b0 = __ldg(a.sb + i), b1 = __ldg(a.se + i);
-      for (int k = b0; k < b1; ++k) {
-        const int64_t sl = __ldg(a.slot + k);
+    for (int l0 = tid; l0 < nl; l0 += kCT * kNP) {
+      double zr[kNP][3], pr[kNP][3];
 #pragma unroll
-        for (int c = 0; c < 3; ++c) qv[c] += ldcg(a.E + (int64_t)c * 10 * nt + sl);
-      }
-      const int g = __ldg(a.gmap + i);
-      if (g >= 0) group_bc<3>(__ldg(a.kind + g), a.normal + 3 * g, qv);
+      for (int n = 0; n < kNP; ++n) {
+        const int l = l0 + n * kCT;
+        const int64_t i = l < nl ? __ldg(a.urep + u0 + l) : 0;
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const int64_t j = i + c * cs;
-        pv[c] = fma(beta, ldcg(a.p + j), ldcg(a.z + j));
-        a.p[j] = pv[c];
-        a.q[j] = qv[c];
+        for (int c = 0; c < 3; ++c) {
+          zr[n][c] = l < nl ? ldcg(a.z + i + c * cs) : 0.0;
+          pr[n][c] = l < nl ? ldcg(a.p + i + c * cs) : 0.0;
+        }
       }
-      if (a.own[i]) acc += pv[0] * qv[0] + pv[1] * qv[1] + pv[2] * qv[2];
+#pragma unroll
+      for (int n = 0; n < kNP; ++n) {
+        const int l = l0 + n * kCT;
+        if (l >= nl) break;
+        const int u = u0 + l;
+        double qv[3] = {0.0, 0.0, 0.0}, pv[3];
+        for (int k = __ldg(a.uitem + u) - i0, ke = __ldg(a.uitem + u + 1) - i0; k < ke; ++k)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) qv[c] += ps[c * ni + k];
+        if (u < a.ng) group_bc<3>(__ldg(a.kind + u), a.normal + 3 * u, qv);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          pv[c] = fma(beta, pr[n][c], zr[n][c]);
+          qs[c * nl + l] = qv[c];
+        }
+        store_all(u, a.p, pv);
+        acc += pv[0] * qv[0] + pv[1] * qv[1] + pv[2] * qv[2];
+      }
     }
     const double pq = cluster_sum(acc, next_part(), sh, cl);
     const double alpha = (rz > 1e-300 && pq != 0.0) ? rz / pq : 0.0;
-    // ---- C: x += alpha p, r -= alpha q, z = P_v M D^-1 r; partial r.z
+    // ---- C: x += alpha p, r -= alpha q (representative), z = P_v M D^-1 r (every copy); partial r.z
     acc = 0.0;
-    for (int64_t i = gt; i < ns; i += nthr) {
-      double rv[3], zv[3];
+    for (int l0 = tid; l0 < nl; l0 += kCT * kNP) {
+      double pr[kNP][3], xr[kNP][3], rr[kNP][3];
+      int64_t ir[kNP];
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const int64_t j = i + c * cs;
-        a.x[j] = fma(alpha, ldcg(a.p + j), ldcg(a.x + j));
-        rv[c] = fma(-alpha, ldcg(a.q + j), ldcg(a.r + j));
-        a.r[j] = rv[c];
-        zv[c] = __ldg(a.dinv + j) * rv[c];
+      for (int n = 0; n < kNP; ++n) {
+        const int l = l0 + n * kCT;
+        ir[n] = l < nl ? __ldg(a.urep + u0 + l) : 0;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          pr[n][c] = l < nl ? ldcg(a.p + ir[n] + c * cs) : 0.0;
+          xr[n][c] = l < nl ? ldcg(a.x + ir[n] + c * cs) : 0.0;
+          rr[n][c] = l < nl ? ldcg(a.r + ir[n] + c * cs) : 0.0;
+        }
       }
-      bc_project(a.bcn[i], a.normal, zv[0], zv[1], zv[2]);
 #pragma unroll
-      for (int c = 0; c < 3; ++c) a.z[i + c * cs] = zv[c];
-      if (a.own[i]) acc += rv[0] * zv[0] + rv[1] * zv[1] + rv[2] * zv[2];
+      for (int n = 0; n < kNP; ++n) {
+        const int l = l0 + n * kCT;
+        if (l >= nl) break;
+        const int64_t i = ir[n];
+        double zv[3], rv[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          a.x[i + c * cs] = fma(alpha, pr[n][c], xr[n][c]);
+          rv[c] = fma(-alpha, qs[c * nl + l], rr[n][c]);
+          a.r[i + c * cs] = rv[c];
+          zv[c] = __ldg(a.dinv + i + c * cs) * rv[c];
+        }
+        bc_project(__ldg(a.bcn + i), a.normal, zv[0], zv[1], zv[2]);
+        store_all(u0 + l, a.z, zv);
+        acc += rv[0] * zv[0] + rv[1] * zv[1] + rv[2] * zv[2];
+      }
     }
     const double rzn = cluster_sum(acc, next_part(), sh, cl);
     beta = rz > 1e-300 ? rzn / rz : 0.0;
     rz = rzn;
+  }
+  // x lives at the representatives during the iteration: broadcast to every copy
+  for (int l = tid; l < nl; l += kCT) {
+    const int u = u0 + l;
+    const int64_t i = __ldg(a.urep + u);
+    const double xv[3] = {ldcg(a.x + i), ldcg(a.x + i + cs), ldcg(a.x + i + 2 * cs)};
+    store_all(u, a.x, xv);
   }
   if (gt == 0) *a.it_out = it;
 }
 
 struct CoarseSolver {
   CoarseArgs a{};
-  int cl = 0;
+  size_t smem = 0;
   bool blend = false, full = true, etaq = false;
   std::vector<void*> bufs;
   ~CoarseSolver() {
@@ -242,31 +321,6 @@ static int upload(CoarseSolver* c, const std::vector<T>& h, const T** d) {
   c->bufs.push_back(p);
   if (!h.empty()) HHG_CUDA(cudaMemcpy(p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
   *d = static_cast<const T*>(p);
-  return HHG_OK;
-}
-
-template <bool B, bool F, bool Q>
-static int coarse_attr(int* cl_out) {
-  auto k = k_coarse_pcg<B, F, Q>;
-  HHG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-  int cl = kClMax;
-  for (; cl >= 2; cl >>= 1) {
-    cudaLaunchConfig_t cfg{};
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = cl;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.gridDim = dim3(cl);
-    cfg.blockDim = dim3(kCT);
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, k, &cfg) == cudaSuccess && n >= 1) break;
-    cudaGetLastError();
-  }
-  if (cl < 2) return fail(HHG_ECUDA, "coarse solver: no cluster configuration fits");
-  *cl_out = cl;
   return HHG_OK;
 }
 
@@ -320,41 +374,68 @@ int coarse_create(const Mesh* m, int level, int form, const double* eta, const d
   const int nt = (int)tn.size();
   node.resize(10 * (size_t)nt);
   p1v.resize(4 * (size_t)nt);
-  std::vector<std::vector<int32_t>> own_slots(ns);
   for (int e = 0; e < nt; ++e) {
-    for (int q = 0; q < 10; ++q) {
-      node[(size_t)q * nt + e] = tn[e][q];
-      own_slots[tn[e][q]].push_back(q * nt + e);
-    }
+    for (int q = 0; q < 10; ++q) node[(size_t)q * nt + e] = tn[e][q];
     for (int v = 0; v < 4; ++v) p1v[(size_t)v * nt + e] = tp[e][v];
   }
-  // gather lists: a node in an interface/BC group sums the slots of every copy (group copy order), the same
-  // list for all copies; any other node its own slots
+  // unique nodes: the g2 groups (interface and/or BC, ids 0..ng-1), then every stored node in no group
   std::vector<int32_t> gmap(ns);
   HHG_CUDA(cudaMemcpy(gmap.data(), L.gmap2, ns * sizeof(int32_t), cudaMemcpyDeviceToHost));
-  std::vector<int64_t> gptr(L.g2.n + 1), gcopy(L.g2.ncopy);
-  if (L.g2.n > 0) {
+  const int64_t ng = L.g2.n;
+  std::vector<int64_t> gptr(ng + 1, 0), gcopy(L.g2.ncopy);
+  if (ng > 0) {
     HHG_CUDA(cudaMemcpy(gptr.data(), L.g2.ptr, gptr.size() * sizeof(int64_t), cudaMemcpyDeviceToHost));
     HHG_CUDA(cudaMemcpy(gcopy.data(), L.g2.copy, gcopy.size() * sizeof(int64_t), cudaMemcpyDeviceToHost));
   }
-  std::vector<int32_t> sb(ns), se(ns), slots;
-  std::vector<int32_t> gfirst(L.g2.n, -1), glast(L.g2.n, -1);
-  for (int64_t g = 0; g < L.g2.n; ++g) {
-    gfirst[g] = (int32_t)slots.size();
-    for (int64_t k = gptr[g]; k < gptr[g + 1]; ++k)
-      for (int32_t sl : own_slots[gcopy[k]]) slots.push_back(sl);
-    glast[g] = (int32_t)slots.size();
+  std::vector<int32_t> uof(ns), ucp(1, 0), ucopy;
+  for (int64_t g = 0; g < ng; ++g) {
+    for (int64_t k = gptr[g]; k < gptr[g + 1]; ++k) ucopy.push_back((int32_t)gcopy[k]);
+    ucp.push_back((int32_t)ucopy.size());
   }
+  int64_t nu = ng;
   for (int64_t i = 0; i < ns; ++i) {
     if (gmap[i] >= 0) {
-      sb[i] = gfirst[gmap[i]];
-      se[i] = glast[gmap[i]];
+      uof[i] = gmap[i];
     } else {
-      sb[i] = (int32_t)slots.size();
-      for (int32_t sl : own_slots[i]) slots.push_back(sl);
-      se[i] = (int32_t)slots.size();
+      uof[i] = (int32_t)nu++;
+      ucopy.push_back((int32_t)i);
+      ucp.push_back((int32_t)ucopy.size());
     }
   }
+  // E segments: element outputs grouped by unique node, in (tet, local node) order within a segment
+  std::vector<int32_t> useg(nu + 1, 0), pos(10 * (size_t)nt);
+  for (int e = 0; e < nt; ++e)
+    for (int q = 0; q < 10; ++q) ++useg[uof[tn[e][q]] + 1];
+  for (int64_t u = 0; u < nu; ++u) useg[u + 1] += useg[u];
+  {
+    std::vector<int32_t> fill(useg.begin(), useg.end() - 1);
+    for (int e = 0; e < nt; ++e)
+      for (int q = 0; q < 10; ++q) pos[(size_t)q * nt + e] = fill[uof[tn[e][q]]]++;
+  }
+  // CTA partition of the unique nodes (contiguous ranges, balanced by E entries + copies) and work items
+  std::vector<int32_t> urep(nu), ub(kCl + 1, 0), ib(kCl + 1, 0), item(1, 0), uitem(nu + 1, 0);
+  for (int64_t u = 0; u < nu; ++u) urep[u] = ucopy[ucp[u]];
+  {
+    std::vector<double> wcum(nu + 1, 0.0);
+    for (int64_t u = 0; u < nu; ++u) wcum[u + 1] = wcum[u] + (useg[u + 1] - useg[u]) + (ucp[u + 1] - ucp[u]);
+    for (int b = 1; b < kCl; ++b)
+      ub[b] = (int32_t)(std::lower_bound(wcum.begin(), wcum.end(), wcum[nu] * b / kCl) - wcum.begin());
+    ub[kCl] = (int32_t)nu;
+    for (int b = 1; b <= kCl; ++b) ub[b] = std::max(ub[b], ub[b - 1]);
+  }
+  size_t smem_max = 0;
+  for (int b = 0; b < kCl; ++b) {
+    ib[b] = (int32_t)(item.size() - 1);
+    for (int64_t u = ub[b]; u < ub[b + 1]; ++u) {
+      uitem[u] = (int32_t)(item.size() - 1);
+      for (int32_t e0 = useg[u]; e0 < useg[u + 1]; e0 += kIt) item.push_back(std::min(e0 + kIt, useg[u + 1]));
+      uitem[u + 1] = (int32_t)(item.size() - 1);
+    }
+    ib[b + 1] = (int32_t)(item.size() - 1);
+    smem_max = std::max(smem_max, (size_t)3 * sizeof(double) * ((ib[b + 1] - ib[b]) + (ub[b + 1] - ub[b])));
+  }
+  if (smem_max > 200 * 1024) return bail(fail(HHG_ENOMEM, "coarse solver: coarse level too large for one cluster"));
+  c->smem = smem_max;
   CoarseArgs& a = c->a;
   a.ns = ns;
   a.ntet = nt;
@@ -365,15 +446,16 @@ int coarse_create(const Mesh* m, int level, int form, const double* eta, const d
   a.mgeo = m->dgeo;
   a.lgeo = L.geo;
   int r;
+  a.nu = (int)nu;
+  a.ng = (int)ng;
   if ((r = upload(c, node, &a.node)) || (r = upload(c, p1v, &a.p1)) || (r = upload(c, info, &a.info)) ||
-      (r = upload(c, anc, &a.anc)) || (r = upload(c, sb, &a.sb)) || (r = upload(c, se, &a.se)) ||
-      (r = upload(c, slots, &a.slot)))
+      (r = upload(c, anc, &a.anc)) || (r = upload(c, pos, &a.pos)) || (r = upload(c, ucp, &a.ucp)) ||
+      (r = upload(c, ucopy, &a.ucopy)) || (r = upload(c, urep, &a.urep)) || (r = upload(c, ub, &a.ub)) ||
+      (r = upload(c, ib, &a.ib)) || (r = upload(c, item, &a.item)) || (r = upload(c, uitem, &a.uitem)))
     return bail(r);
-  a.gmap = L.gmap2;
   a.kind = L.g2.kind;
   a.normal = L.g2.normal;
   a.bcn = L.bcn2;
-  a.own = L.own2;
   a.eta = eta;
   a.T2 = T2;
   a.eq = EtaQ{lnC, jump, rjump};
@@ -390,15 +472,16 @@ int coarse_create(const Mesh* m, int level, int form, const double* eta, const d
   c->full = form == HHG_VISC_FULL;
   c->etaq = T2 != nullptr;
   if (c->etaq && !c->full) return bail(fail(HHG_EINVAL, "coarse solver: quadrature-point viscosity needs the full form"));
-#define HHG_CATTR(B, F, Q) r = coarse_attr<B, F, Q>(&c->cl);
+#define HHG_CSMEM(B, F, Q) \
+  r = cudaFuncSetAttribute(k_coarse_pcg<B, F, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem) == cudaSuccess ? HHG_OK : fail(HHG_ECUDA, "coarse solver: shared memory attribute");
   if (c->etaq) {
-    if (c->blend) HHG_CATTR(true, true, true) else HHG_CATTR(false, true, true)
+    if (c->blend) HHG_CSMEM(true, true, true) else HHG_CSMEM(false, true, true)
   } else if (c->blend) {
-    if (c->full) HHG_CATTR(true, true, false) else HHG_CATTR(true, false, false)
+    if (c->full) HHG_CSMEM(true, true, false) else HHG_CSMEM(true, false, false)
   } else {
-    if (c->full) HHG_CATTR(false, true, false) else HHG_CATTR(false, false, false)
+    if (c->full) HHG_CSMEM(false, true, false) else HHG_CSMEM(false, false, false)
   }
-#undef HHG_CATTR
+#undef HHG_CSMEM
   if (r != HHG_OK) return bail(r);
   *out = c;
   return HHG_OK;
@@ -406,19 +489,9 @@ int coarse_create(const Mesh* m, int level, int form, const double* eta, const d
 
 template <bool B, bool F, bool Q>
 static int coarse_launch(CoarseSolver* c, cudaStream_t s) {
-  cudaLaunchConfig_t cfg{};
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = c->cl;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  cfg.gridDim = dim3(c->cl);
-  cfg.blockDim = dim3(kCT);
-  cfg.stream = s;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  HHG_CUDA(cudaLaunchKernelEx(&cfg, k_coarse_pcg<B, F, Q>, c->a));
+  k_coarse_pcg<B, F, Q><<<kCl, kCT, c->smem, s>>>(c->a);
   count_launch();
+  HHG_CUDA(cudaGetLastError());
   return HHG_OK;
 }
 

@@ -2,6 +2,7 @@
 // inverse diagonal, P2 transfers with projections, coarse Jacobi-PCG (BASELINE
 // config 3; replaces the paper's AMG-CG of P:443), power-iteration spectrum estimate.
 // All scalars of the PCG stay on the device so the whole cycle can be captured in one CUDA graph.
+#include <chrono>
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -402,7 +403,8 @@ int hhg_mg_create_qeta(hhg_mesh* mesh, const hhg_mg_params* params, const double
       auto& C = mg->lv[P.l_min];
       const int r = coarse_create(mesh, P.l_min, P.visc_form, C.eta, C.T2, P.qeta_lnC, P.qeta_jump, P.qeta_rjump,
                                   C.dinv, &mg->ccs);
-      if (r != HHG_OK) return bail(r);
+      // a coarse level too large for one cluster keeps the generic path (unless a tolerance needs the kernel)
+      if (r != HHG_OK && !(r == HHG_ENOMEM && P.coarse_tol == 0.0)) return bail(r);
     }
   }
   if (P.coarse_tol > 0.0 && !mg->ccs && !(P.coarse_redundant && mesh->nranks > 1))
@@ -975,12 +977,38 @@ int km_power(hhg_kmg* K, int l) {  // lambda_max(D^-1 K) from a keyed consistent
   L.lam = std::sqrt(h);
   return HHG_OK;
 }
-// CG with device scalars and one host sync per iteration; op / prec write their outputs; proj (may
-// be empty) projects a vector in place (mean zero, or nothing)
+// CG with device scalars; op / prec write their outputs; proj (may be empty) projects a vector in place
+// (mean zero, or nothing).  check_every = 1: one host sync per iteration for the stopping test.  check_every
+// = k > 1 (cheap inner solves): the stopping test runs on the device every iteration (k_cg_check latches
+// done / iteration / |r|^2 in fl[0..2]) and freezes x and r once it holds (alpha = 0), and the host reads the
+// latch every k iterations -- same iterate, iteration count and residual as checking every iteration, with
+// k-1 of k host round trips removed (the frozen tail iterations do no harm: x and r stay put).
+constexpr int kCheckEvery = 8;  // host reads of the stopping latch in cheap inner solves (mass, vector mass, T)
+__global__ void k_cg_step_fz(int64_t n, const double* __restrict__ sc, const double* __restrict__ fl,
+                             double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
+                             const double* __restrict__ q) {
+  const double alpha = (fl[0] == 0.0 && sc[1] != 0.0) ? sc[0] / sc[1] : 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    x[i] += alpha * p[i];
+    r[i] -= alpha * q[i];
+  }
+}
+__global__ void k_cg_check(const double* __restrict__ sc, double* __restrict__ fl, int it, double r0, double tol,
+                           double tol_abs) {
+  if (threadIdx.x != 0 || fl[0] != 0.0) return;
+  const double rn = sqrt(fmax(sc[3], 0.0));
+  if (rn / r0 <= tol || rn <= tol_abs) {
+    fl[0] = 1.0;
+    fl[1] = it;
+    fl[2] = sc[3];
+  }
+}
 int dev_pcg(const Mesh* m, const Level& LL, int space, int64_t n, const std::function<int(const double*, double*)>& op,
             const std::function<int(const double*, double*)>& prec, const std::function<int(double*)>& proj,
             const double* rhs, double* x, double tol, double tol_abs, int max_iters, double* r, double* z, double* p,
-            double* q, double* sc, double* red, cudaStream_t s, int* iters_out, double* rel_out) {
+            double* q, double* sc, double* red, cudaStream_t s, int* iters_out, double* rel_out, int check_every = 1,
+            double* fl = nullptr) {
+  if (check_every > 1 && !fl) return fail(HHG_EINVAL, "dev_pcg: batched stopping test needs a latch");
   HHG_CUDA(cudaMemsetAsync(x, 0, n * sizeof(double), s));
   HHG_CUDA(cudaMemcpyAsync(r, rhs, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
   if (proj) HHG_TRY(proj(r));
@@ -997,19 +1025,39 @@ int dev_pcg(const Mesh* m, const Level& LL, int space, int64_t n, const std::fun
     HHG_CUDA(cudaMemcpyAsync(p, z, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
     HHG_TRY(launch_dot(m, LL, space, r, z, sc + 0, s, red));
     const unsigned nb = vg(n);
+    if (check_every > 1) HHG_CUDA(cudaMemsetAsync(fl, 0, 3 * sizeof(double), s));
     while (it < max_iters) {
       ++it;
       HHG_TRY(op(p, q));
       HHG_TRY(launch_dot(m, LL, space, p, q, sc + 1, s, red));
-      k_cg_step<<<nb, 256, 0, s>>>(n, sc, x, r, p, q);
+      if (check_every > 1) k_cg_step_fz<<<nb, 256, 0, s>>>(n, sc, fl, x, r, p, q);
+      else k_cg_step<<<nb, 256, 0, s>>>(n, sc, x, r, p, q);
       count_launch();
       HHG_TRY(launch_dot(m, LL, space, r, r, sc + 3, s, red));
-      double rr = 0.0;
-      HHG_CUDA(cudaMemcpyAsync(&rr, sc + 3, sizeof(double), cudaMemcpyDeviceToHost, s));
-      HHG_CUDA(cudaStreamSynchronize(s));
-      const double rn = std::sqrt(std::max(rr, 0.0));
-      rel = rn / r0;
-      if (rel <= tol || rn <= tol_abs) break;
+      if (check_every > 1) {
+        k_cg_check<<<1, 32, 0, s>>>(sc, fl, it, r0, tol, tol_abs);
+        count_launch();
+        if (it % check_every == 0 || it == max_iters) {
+          double h[3];
+          HHG_CUDA(cudaMemcpyAsync(h, fl, 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
+          HHG_CUDA(cudaStreamSynchronize(s));
+          if (h[0] != 0.0) {
+            it = (int)h[1];
+            rel = std::sqrt(std::max(h[2], 0.0)) / r0;
+            break;
+          }
+          double rr = 0.0;
+          HHG_CUDA(cudaMemcpy(&rr, sc + 3, sizeof(double), cudaMemcpyDeviceToHost));
+          rel = std::sqrt(std::max(rr, 0.0)) / r0;
+        }
+      } else {
+        double rr = 0.0;
+        HHG_CUDA(cudaMemcpyAsync(&rr, sc + 3, sizeof(double), cudaMemcpyDeviceToHost, s));
+        HHG_CUDA(cudaStreamSynchronize(s));
+        const double rn = std::sqrt(std::max(rr, 0.0));
+        rel = rn / r0;
+        if (rel <= tol || rn <= tol_abs) break;
+      }
       HHG_TRY(prec(r, z));
       if (proj) HHG_TRY(proj(z));
       HHG_TRY(launch_dot(m, LL, space, r, z, sc + 2, s, red));
@@ -1097,6 +1145,51 @@ int hhg_kmg_destroy(hhg_kmg* K) {
 }
 }  // extern "C"
 
+// ---------------------------------------------------------------- solve statistics (HHG_STATS=1)
+// Inner-solver call counts, iterations and host wall time (every inner CG synchronises on its stopping test,
+// so wall time = device time + launch/sync latency); printed as one JSON line per hhg_stokes_solve (stderr).
+namespace {
+struct SolveStat {
+  const char* name;
+  long calls, iters;
+  double sec;
+};
+SolveStat g_stat[] = {{"ablock_cg", 0, 0, 0}, {"bacbt_cg", 0, 0, 0}, {"mass_cg", 0, 0, 0}, {"vmass_cg", 0, 0, 0},
+                      {"kmg_cg", 0, 0, 0}};
+enum { ST_ABLOCK, ST_BACBT, ST_MASS, ST_VMASS, ST_KMG, ST_N };
+bool stats_on() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("HHG_STATS");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+struct StatScope {
+  int k;
+  const int* it;
+  std::chrono::steady_clock::time_point t0;
+  StatScope(int k_, const int* it_) : k(k_), it(it_), t0(std::chrono::steady_clock::now()) {}
+  ~StatScope() {
+    if (!stats_on()) return;
+    g_stat[k].calls += 1;
+    g_stat[k].iters += *it;
+    g_stat[k].sec += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  }
+};
+void stats_print(int fgmres_iters, double sec) {
+  if (!stats_on()) return;
+  fprintf(stderr, "{\"hhg_stats\": \"stokes_solve\", \"fgmres_iters\": %d, \"solve_s\": %.3f", fgmres_iters, sec);
+  for (int k = 0; k < ST_N; ++k) {
+    fprintf(stderr, ", \"%s\": {\"calls\": %ld, \"iters\": %ld, \"s\": %.3f}", g_stat[k].name, g_stat[k].calls,
+            g_stat[k].iters, g_stat[k].sec);
+    g_stat[k].calls = g_stat[k].iters = 0;
+    g_stat[k].sec = 0;
+  }
+  fprintf(stderr, "}\n");
+}
+}  // namespace
+
 // ================================================================ Stokes solve (NEXT-1)
 // FGMRES right-preconditioned by the symmetric Uzawa block preconditioner
 // (eq:SymmetricUzawaStep1) with B replaced by B + C in the pressure update:
@@ -1170,10 +1263,12 @@ int st_mass_solve(hhg_stokes* S, const double* rp, double* zp, cudaStream_t s) {
   const Level& L = m->levels[S->level];
   auto op = [&](const double* x, double* y) -> int { return hhg_mass_apply(S->mesh, S->level, S->eta, x, y, (hhg_stream_t)s); };
   auto jac = [&](const double* r, double* z) -> int { return launch_pcg_scale(S->n1, S->mdinv, r, z, s); };
-  int it;
+  int it = 0;
   double rel;
+  StatScope st(ST_MASS, &it);
   return dev_pcg(m, L, HHG_P1, S->n1, op, jac, std::function<int(double*)>(), rp, zp, S->prm.tol_mass, 0.0,
-                 S->prm.mass_max_iters, S->mr, S->mz, S->mp, S->mq, S->sc + 8, S->red, s, &it, &rel);
+                 S->prm.mass_max_iters, S->mr, S->mz, S->mp, S->mq, S->sc + 8, S->red, s, &it, &rel, kCheckEvery,
+                 S->sc + 24);
 }
 // w = P_p B A_C^-1 B^T y  (A_C^-1 = one cheap V-cycle, eq:schurV)
 int st_bacbt(hhg_stokes* S, const double* y, double* w, cudaStream_t s) {
@@ -1190,8 +1285,9 @@ int st_bacbt_solve(hhg_stokes* S, const double* t, double* y, cudaStream_t s) {
   auto op = [&](const double* x, double* w) -> int { return st_bacbt(S, x, w, s); };
   auto prec = [&](const double* r, double* z) -> int { return st_mass_solve(S, r, z, s); };
   auto proj = [&](double* v) -> int { return st_mean0(S, v, s); };
-  int it;
+  int it = 0;
   double rel;
+  StatScope st(ST_BACBT, &it);
   return dev_pcg(m, L, HHG_P1, S->n1, op, prec, proj, t, y, S->prm.tol_vbfbt, 0.0, S->prm.vbfbt_max_iters, S->br,
                  S->bz, S->bp, S->bq, S->sc + 12, S->red, s, &it, &rel);
 }
@@ -1216,24 +1312,30 @@ int st_vmass_solve(hhg_stokes* S, double a, const double* vdinv, const double* v
     HHG_TRY(launch_pcg_scale(S->n2, vdinv, r, z, s));
     return launch_fixup(m, L, HHG_P2VEC, false, true, z, s);
   };
-  int it;
+  int it = 0;
   double rel;
+  StatScope st(ST_VMASS, &it);
   return dev_pcg(m, L, HHG_P2VEC, S->n2, op, prec, std::function<int(double*)>(), v, x, S->prm.tol_vmass, 0.0,
-                 S->prm.vmass_max_iters, S->vr, S->vz, S->vp, S->vq, S->sc + 16, S->red, s, &it, &rel);
+                 S->prm.vmass_max_iters, S->vr, S->vz, S->vp, S->vq, S->sc + 16, S->red, s, &it, &rel, kCheckEvery,
+                 S->sc + 28);
 }
 // z = S_w^-1 t (eq:schurWBFBT with a_l / a_r):
 //   K_{1/sqrt(eta_l)}^-1 B M_{sqrt(eta_l)}^-1 A M_{sqrt(eta_r)}^-1 B^T K_{1/sqrt(eta_r)}^-1 t
 int st_wbfbt(hhg_stokes* S, const double* t, double* z, cudaStream_t s) {
-  int it;
+  int it = 0;
   double rel;
   const auto& P = S->prm;
-  HHG_TRY(hhg_kmg_solve(S->kr, t, S->bt, P.tol_wbfbt, P.tol_wbfbt_abs, P.wbfbt_max_iters, &it, &rel, (hhg_stream_t)s));
+  {
+    StatScope st(ST_KMG, &it);
+    HHG_TRY(hhg_kmg_solve(S->kr, t, S->bt, P.tol_wbfbt, P.tol_wbfbt_abs, P.wbfbt_max_iters, &it, &rel, (hhg_stream_t)s));
+  }
   HHG_TRY(divT_apply(S->mesh, S->level, S->bt, S->bu, 0, (hhg_stream_t)s));
   HHG_TRY(st_vmass_solve(S, P.a_r, S->vdr, S->bu, S->bv, s));
   HHG_TRY(epsilon_apply(S->mesh, S->level, HHG_VISC_FULL, S->eta, S->bv, S->bu, (hhg_stream_t)s));
   HHG_TRY(st_vmass_solve(S, P.a_l, S->vdl, S->bu, S->bv, s));
   HHG_TRY(div_apply(S->mesh, S->level, 0.0, S->bv, S->bt, (hhg_stream_t)s));
   HHG_TRY(st_mean0(S, S->bt, s));
+  StatScope st(ST_KMG, &it);
   return hhg_kmg_solve(S->kl, S->bt, z, P.tol_wbfbt, P.tol_wbfbt_abs, P.wbfbt_max_iters, &it, &rel, (hhg_stream_t)s);
 }
 
@@ -1263,11 +1365,17 @@ int st_prec(hhg_stokes* S, const double* r, double* z, cudaStream_t s) {
     HHG_TRY(st_schur(S, S->t + n2, z + n2, s));
     HHG_TRY(divT_apply(S->mesh, S->level, z + n2, S->t, 0, (hhg_stream_t)s));
     HHG_TRY(launch_axpby(n2, 1.0, r, -1.0, S->t, s));
-    HHG_TRY(hhg_ablock_cg(S->mg, S->t, z, S->prm.tol_A, S->prm.ablock_max_iters, &it, &rel, (hhg_stream_t)s));
+    {
+      StatScope st(ST_ABLOCK, &it);
+      HHG_TRY(hhg_ablock_cg(S->mg, S->t, z, S->prm.tol_A, S->prm.ablock_max_iters, &it, &rel, (hhg_stream_t)s));
+    }
     return launch_axpby(n2, 0.0, z, sig, z, s);
   }
   // u_hat = sigma A^-1 r_u  (z_u holds u_hat)
-  HHG_TRY(hhg_ablock_cg(S->mg, r, z, S->prm.tol_A, S->prm.ablock_max_iters, &it, &rel, (hhg_stream_t)s));
+  {
+    StatScope st(ST_ABLOCK, &it);
+    HHG_TRY(hhg_ablock_cg(S->mg, r, z, S->prm.tol_A, S->prm.ablock_max_iters, &it, &rel, (hhg_stream_t)s));
+  }
   HHG_TRY(launch_axpby(n2, 0.0, z, sig, z, s));
   // t_p = r_p - (B + C) u_hat ; p = -omega S^-1 t_p ; P_p
   HHG_TRY(div_apply(S->mesh, S->level, S->gamma, z, S->t + n2, (hhg_stream_t)s));
@@ -1278,7 +1386,10 @@ int st_prec(hhg_stokes* S, const double* r, double* z, cudaStream_t s) {
   // t_u = r_u - A u_hat - B^T p ; u = u_hat + sigma A^-1 t_u
   HHG_TRY(stokes_apply(S->mesh, S->level, S->eta, S->gamma, z, z + n2, S->t, S->a + n2, (hhg_stream_t)s));
   HHG_TRY(launch_axpby(n2, 1.0, r, -1.0, S->t, s));
-  HHG_TRY(hhg_ablock_cg(S->mg, S->t, S->a, S->prm.tol_A, S->prm.ablock_max_iters, &it, &rel, (hhg_stream_t)s));
+  {
+    StatScope st(ST_ABLOCK, &it);
+    HHG_TRY(hhg_ablock_cg(S->mg, S->t, S->a, S->prm.tol_A, S->prm.ablock_max_iters, &it, &rel, (hhg_stream_t)s));
+  }
   return launch_axpby(n2, sig, S->a, 1.0, z, s);
 }
 }  // namespace
@@ -1383,6 +1494,7 @@ int hhg_stokes_solve(hhg_stokes* S, const double* rhs, double* x, int* iters_out
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t n2 = S->n2, n1 = S->n1, nb = n2 + n1;
   const int m = S->prm.restart;
+  const auto t_start = std::chrono::steady_clock::now();
   // b = P rhs
   HHG_CUDA(cudaMemcpyAsync(S->b, rhs, nb * sizeof(double), cudaMemcpyDeviceToDevice, s));
   HHG_TRY(launch_fixup(S->mesh, S->mesh->levels[S->level], HHG_P2VEC, false, true, S->b, s));
@@ -1436,6 +1548,9 @@ int hhg_stokes_solve(hhg_stokes* S, const double* rhs, double* x, int* iters_out
       g[j + 1] = -sn[j] * g[j];
       g[j] = cs[j] * g[j];
       rel = std::fabs(g[j + 1]) / bn;
+      if (stats_on())
+        fprintf(stderr, "{\"hhg_stats\": \"fgmres\", \"it\": %d, \"rel\": %.6e, \"t_s\": %.3f}\n", total, rel,
+                std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count());
       if (rel <= S->prm.tol || hn == 0.0) {
         ++j;
         break;
@@ -1460,6 +1575,7 @@ int hhg_stokes_solve(hhg_stokes* S, const double* rhs, double* x, int* iters_out
   HHG_CUDA(cudaStreamSynchronize(s));
   if (iters_out) *iters_out = total;
   if (rel_res_out) *rel_res_out = rel;
+  stats_print(total, std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count());
   return HHG_OK;
 }
 
@@ -1664,7 +1780,7 @@ int hhg_temp_solve(hhg_temp_solver* S, const double* u, const double* b, double*
     int it;
     double rel;
     return dev_pcg(m, L, HHG_P2, n, opP, jac, std::function<int(double*)>(), r, z, tol_cg, 0.0, cg_max_iters, S->cr,
-                   S->cz, S->cp, S->cq, S->sc, S->red, s, &it, &rel);
+                   S->cz, S->cp, S->cq, S->sc, S->red, s, &it, &rel, kCheckEvery, S->sc + 8);
   };
   // T_D on the boundary, b' = mask_int(b - L T_D)
   HHG_TRY(mask(T, S->td, 1));

@@ -77,7 +77,7 @@ def test_pcg_solves_small_spd_exactly():
 
 
 def test_pcg_tolerance_stop_textbook_counts():
-    """Coarse PCG to a relative tolerance (Table 1 tol_coarse; R26).  Textbook pins: CG on an SPD
+    """Coarse PCG to a relative tolerance (Table 1 tol_coarse; R29).  Textbook pins: CG on an SPD
     matrix with k distinct eigenvalues terminates in k steps (and not before), so with a tight tolerance the count
     is exactly k and the solution exact; on a diagonal matrix Jacobi-PCG converges in ONE step.  Consistency: the tolerance run equals
     the fixed-iteration run with that count, and its r.z meets the bound while one iteration fewer does not."""

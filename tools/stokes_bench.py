@@ -25,6 +25,9 @@ ap.add_argument("--deg", type=int, default=2, help="Chebyshev degree of the A-bl
 ap.add_argument("--contrast", type=float, default=1e6)
 ap.add_argument("--jump", type=float, default=30.0)
 ap.add_argument("--l-eta", type=int, default=-1, help="levels <= l_eta use quadrature-point viscosity (NEXT-2)")
+ap.add_argument("--l-min", type=int, default=1, help="coarsest level of the V-cycles (P:661: l_min = 2 on 240 macros)")
+ap.add_argument("--coarse-tol", type=float, default=0.0, help="coarse PCG relative tolerance (Table 1: 1e-2; 0: 50 its)")
+ap.add_argument("--coarse-iters", type=int, default=50)
 a = ap.parse_args()
 L = a.level
 M, etas, v0, _, n_dof = build_case(L, 0, contrast=a.contrast, jump=a.jump)
@@ -37,9 +40,10 @@ import math
 T2s = {l: temp_p2(l) for l in range(1, a.l_eta + 1)} if a.l_eta >= 1 else None
 qeta = (math.log(a.contrast), a.jump, 0.9)
 t0 = time.perf_counter()
-mg = hhg.MG(M, 1, L, etas, v0, pre=3, post=3, degree=a.deg, T2_per_level=T2s, l_eta=a.l_eta, qeta=qeta)
+ck = dict(coarse_tol=a.coarse_tol, coarse_iters=a.coarse_iters)
+mg = hhg.MG(M, a.l_min, L, etas, v0, pre=3, post=3, degree=a.deg, T2_per_level=T2s, l_eta=a.l_eta, qeta=qeta, **ck)
 v0c = {l: v.clone() for l, v in build_case(L, 0, contrast=a.contrast, jump=a.jump)[2].items()} if a.schur == "vbfbt" else None
-mgc = hhg.MG(M, 1, L, etas, v0c, pre=1, post=1, degree=1, T2_per_level=T2s, l_eta=a.l_eta, qeta=qeta) \
+mgc = hhg.MG(M, a.l_min, L, etas, v0c, pre=1, post=1, degree=1, T2_per_level=T2s, l_eta=a.l_eta, qeta=qeta, **ck) \
     if a.schur == "vbfbt" else None
 keys = M.canonical_keys(L, hhg.HHG_P1)
 xyz = M.node_coords(L, hhg.HHG_P1)
@@ -61,6 +65,7 @@ s.synchronize()
 ms = e0.elapsed_time(e1)
 n_p = M.canonical_len(L, hhg.HHG_P1)
 x2, ita, rela = mg.ablock_cg(f, tol=1e-2, max_iters=200)
-print(json.dumps({"what": "stokes_solve", "l_eta": a.l_eta, "ablock_cg_iters_tol1e-2": ita, "ablock_rel": rela, "level": L, "schur": a.schur, "omega": a.omega, "a_l": a.a_l, "a_r": a.a_r, "uzawa": a.uzawa, "tol_A": a.tol_A, "velocity_dofs": n_dof, "pressure_dofs": n_p,
+print(json.dumps({"what": "stokes_solve", "l_eta": a.l_eta, "l_min": a.l_min, "coarse_tol": a.coarse_tol,
+                  "coarse_iters_max": a.coarse_iters, "ablock_cg_iters_tol1e-2": ita, "ablock_rel": rela, "level": L, "schur": a.schur, "omega": a.omega, "a_l": a.a_l, "a_r": a.a_r, "uzawa": a.uzawa, "tol_A": a.tol_A, "velocity_dofs": n_dof, "pressure_dofs": n_p,
                   "fgmres_iters": it, "rel_res": rel, "tol": a.tol, "solve_s": ms / 1e3, "setup_s": setup,
                   "viscosity": f"contrast {a.contrast:g} x {a.jump:g} jump", "rhs": "buoyancy (T - 1/2) x/|x|, g = 0"}))
