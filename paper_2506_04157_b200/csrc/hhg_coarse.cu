@@ -19,6 +19,8 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "hhg_internal.h"
@@ -53,6 +55,13 @@ struct CoarseArgs {
   const int32_t* ib;        // [kCl+1] items of CTA b: [ib[b], ib[b+1])
   const int32_t* item;      // [nitems+1] E range of item k: [item[k], item[k+1]) (<= kIt entries, one node each)
   const int32_t* uitem;     // [nu+1] items of unique node u: [uitem[u], uitem[u+1])
+  // shared-memory-resident variant (k_coarse_pcg_sm): owner CTA | local index of every tet node's unique node and
+  // of every element output's E slot, the CTAs' E starts, and the per-CTA capacities (array strides)
+  const int32_t* onode;     // [10][ntet]
+  const int32_t* opos;      // [10][ntet]
+  const int32_t* eb;        // [kCl+1]
+  int NL, NE, NI;
+  unsigned long long* dbg;  // HHG_CCL_TIMING=1: accumulated globaltimer ns per phase (CTA 0, thread 0)
   const uint8_t* kind;      // group BC kind
   const double* normal;     // group normals [3]
   const int32_t* bcn;       // per node BC for P_v M on directions
@@ -98,6 +107,41 @@ struct GT {
   double t[10];
   __device__ __forceinline__ double operator()(int a) const { return t[a]; }
 };
+
+// element outputs of micro tet e for the gathered p' (everything but the gather and the scatter)
+template <bool BLEND, bool FULL, bool ETAQ>
+__device__ __forceinline__ void coarse_tet(const CoarseArgs& a, int e, const GU& uu, double (&accE)[10][3]) {
+  const int nt = a.ntet;
+  const int inf = __ldg(a.info + e), an = __ldg(a.anc + e);
+  const int mac = inf & 0xffffff, t = inf >> 24;
+  GT tt;
+  if (ETAQ) {
+#pragma unroll
+    for (int k = 0; k < 10; ++k) tt.t[k] = __ldg(a.T2 + __ldg(a.node + k * nt + e));
+  }
+  double et[4], pp[4] = {0, 0, 0, 0};
+#pragma unroll
+  for (int v = 0; v < 4; ++v) et[v] = a.eta ? __ldg(a.eta + __ldg(a.p1 + v * nt + e)) : 1.0;
+  const MacroGeo& g = a.mgeo[mac];
+  double nh[3] = {0, 0, 0}, cK = 1.0;
+  if (BLEND) {
+    nh[0] = g.nhat[0];
+    nh[1] = g.nhat[1];
+    nh[2] = g.nhat[2];
+    cK = g.cK;
+  }
+  const double fa = (an & 1023) * a.inv_n1, fb = ((an >> 10) & 1023) * a.inv_n1, fc = (an >> 20) * a.inv_n1;
+  double xa[3];
+#pragma unroll
+  for (int r = 0; r < 3; ++r) xa[r] = g.X0[r] + g.Jm[3 * r] * fa + g.Jm[3 * r + 1] * fb + g.Jm[3 * r + 2] * fc;
+  const double* Gm = a.lgeo + (int64_t)mac * kLevelGeo;
+  double G[kTypeGeo];
+#pragma unroll
+  for (int k = 0; k < kTypeGeo; ++k) G[k] = __ldg(Gm + t * kTypeGeo + k);
+  const double wdet = EWQ * __ldg(Gm + 6 * kTypeGeo);
+  double gy[4];
+  tet_body<BLEND, ELEM_A, FULL, GU, ETAQ, GT>(G, wdet, xa, nh, cK, 0.0, uu, et, pp, accE, gy, tt, a.eq);
+}
 
 constexpr int kIt = 16;   // E entries per work item (one load round trip)
 constexpr int kNP = 4;    // unique nodes per thread per pass (their loads issued together)
@@ -159,8 +203,6 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kCT, 1) k_coarse_p
     if (a.tol2 > 0.0 && (rz <= rz_stop || rz <= 1e-300)) break;
     // ---- A: element outputs of p' = z + beta p
     for (int e = gt; e < nt; e += nthr) {
-      const int inf = __ldg(a.info + e), an = __ldg(a.anc + e);
-      const int mac = inf & 0xffffff, t = inf >> 24;
       GU uu;
 #pragma unroll
       for (int k = 0; k < 10; ++k) {
@@ -168,33 +210,8 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kCT, 1) k_coarse_p
 #pragma unroll
         for (int c = 0; c < 3; ++c) uu.u[k][c] = fma(beta, ldcg(a.p + j + c * cs), ldcg(a.z + j + c * cs));
       }
-      GT tt;
-      if (ETAQ) {
-#pragma unroll
-        for (int k = 0; k < 10; ++k) tt.t[k] = __ldg(a.T2 + __ldg(a.node + k * nt + e));
-      }
-      double et[4], pp[4] = {0, 0, 0, 0};
-#pragma unroll
-      for (int v = 0; v < 4; ++v) et[v] = a.eta ? __ldg(a.eta + __ldg(a.p1 + v * nt + e)) : 1.0;
-      const MacroGeo& g = a.mgeo[mac];
-      double nh[3] = {0, 0, 0}, cK = 1.0;
-      if (BLEND) {
-        nh[0] = g.nhat[0];
-        nh[1] = g.nhat[1];
-        nh[2] = g.nhat[2];
-        cK = g.cK;
-      }
-      const double fa = (an & 1023) * a.inv_n1, fb = ((an >> 10) & 1023) * a.inv_n1, fc = (an >> 20) * a.inv_n1;
-      double xa[3];
-#pragma unroll
-      for (int r = 0; r < 3; ++r) xa[r] = g.X0[r] + g.Jm[3 * r] * fa + g.Jm[3 * r + 1] * fb + g.Jm[3 * r + 2] * fc;
-      const double* Gm = a.lgeo + (int64_t)mac * kLevelGeo;
-      double G[kTypeGeo];
-#pragma unroll
-      for (int k = 0; k < kTypeGeo; ++k) G[k] = __ldg(Gm + t * kTypeGeo + k);
-      const double wdet = EWQ * __ldg(Gm + 6 * kTypeGeo);
-      double accE[10][3], gy[4];
-      tet_body<BLEND, ELEM_A, FULL, GU, ETAQ, GT>(G, wdet, xa, nh, cK, 0.0, uu, et, pp, accE, gy, tt, a.eq);
+      double accE[10][3];
+      coarse_tet<BLEND, FULL, ETAQ>(a, e, uu, accE);
 #pragma unroll
       for (int k = 0; k < 10; ++k) {
         const int64_t ps_ = __ldg(a.pos + k * nt + e);
@@ -304,9 +321,178 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kCT, 1) k_coarse_p
   if (gt == 0) *a.it_out = it;
 }
 
+
+// Shared-memory-resident variant (coarse levels whose per-CTA working set fits: shell(3,2) L1): every vector of a
+// unique node lives in its owner CTA's shared memory for the whole solve; the tet phase reads p, z and writes its
+// element outputs through distributed shared memory (DSMEM) of the owner CTAs; nothing but f, D^-1 and the final x
+// touches global memory.  Same arithmetic and summation order as k_coarse_pcg.
+template <bool BLEND, bool FULL, bool ETAQ>
+__global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kCT, 1) k_coarse_pcg_sm(CoarseArgs a) {
+  cg::cluster_group cl = cg::this_cluster();
+  __shared__ double sh[kCT / 32];
+  __shared__ double spart[3];
+  extern __shared__ double dsm[];
+  const int NL = a.NL, NE = a.NE, NI = a.NI;
+  double* xs = dsm;
+  double* rs = xs + 3 * NL;
+  double* zs = rs + 3 * NL;
+  double* ps = zs + 3 * NL;
+  double* qs = ps + 3 * NL;
+  double* ds = qs + 3 * NL;
+  double* Es = ds + 3 * NL;
+  double* pi = Es + 3 * NE;
+  const int nthr = gridDim.x * blockDim.x;
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x, tid = threadIdx.x;
+  const int b = blockIdx.x;
+  const int64_t cs = a.ns;
+  const int u0 = a.ub[b], nl = a.ub[b + 1] - u0;
+  const int i0 = a.ib[b], ni = a.ib[b + 1] - i0;
+  const int e0 = a.eb[b];
+  int pb = 0;
+  auto csum = [&](double v) {  // cluster sum through DSMEM, partials added in CTA order (identical everywhere)
+    const double t = block_sum(v, sh);
+    if (tid == 0) spart[pb] = t;
+    cl.sync();
+    double s = 0.0;
+    for (int r = 0; r < kCl; ++r) s += *cl.map_shared_rank(spart + pb, r);
+    pb = (pb + 1) % 3;
+    return s;
+  };
+  // x = 0, r = f, z = P_v M D^-1 r, p = z; rz = r.z
+  double acc = 0.0;
+  for (int l = tid; l < nl; l += kCT) {
+    const int64_t i = __ldg(a.urep + u0 + l);
+    double rv[3], zv[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      rv[c] = a.f[i + c * cs];
+      ds[c * NL + l] = __ldg(a.dinv + i + c * cs);
+      zv[c] = ds[c * NL + l] * rv[c];
+    }
+    bc_project(__ldg(a.bcn + i), a.normal, zv[0], zv[1], zv[2]);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      xs[c * NL + l] = 0.0;
+      rs[c * NL + l] = rv[c];
+      zs[c * NL + l] = zv[c];
+      ps[c * NL + l] = zv[c];
+    }
+    acc += rv[0] * zv[0] + rv[1] * zv[1] + rv[2] * zv[2];
+  }
+  double rz = csum(acc);
+  const double rz_stop = a.tol2 * rz;
+  double beta = 0.0;
+  const int nt = a.ntet;
+  int it = 0;
+  unsigned long long tA = 0;
+  auto tick = [&](int ph) {
+    if (a.dbg && gt == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (ph >= 0) a.dbg[ph] += t - tA;
+      tA = t;
+    }
+  };
+  for (; it < a.iters; ++it) {
+    if (a.tol2 > 0.0 && (rz <= rz_stop || rz <= 1e-300)) break;
+    tick(-1);
+    // ---- A: p' = z + beta p gathered from the owners (DSMEM), element outputs scattered to the owners' E
+    for (int e = gt; e < nt; e += nthr) {
+      GU uu;
+#pragma unroll
+      for (int k = 0; k < 10; ++k) {
+        const int o = __ldg(a.onode + k * nt + e);
+        const double* rp = cl.map_shared_rank(ps, o >> 24);
+        const double* rzz = cl.map_shared_rank(zs, o >> 24);
+        const int loc = o & 0xffffff;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) uu.u[k][c] = fma(beta, rp[c * NL + loc], rzz[c * NL + loc]);
+      }
+      double accE[10][3];
+      coarse_tet<BLEND, FULL, ETAQ>(a, e, uu, accE);
+#pragma unroll
+      for (int k = 0; k < 10; ++k) {
+        const int o = __ldg(a.opos + k * nt + e);
+        double* rE = cl.map_shared_rank(Es, o >> 24);
+        const int loc = o & 0xffffff;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) rE[c * NE + loc] = accE[k][c];
+      }
+    }
+    tick(0);
+    cl.sync();
+    tick(1);
+    // ---- B1: item partials (<= kIt E entries of one node, in order)
+    for (int k = tid; k < ni; k += kCT) {
+      const int ea = __ldg(a.item + i0 + k) - e0, eb_ = __ldg(a.item + i0 + k + 1) - e0;
+      double sv[3] = {0.0, 0.0, 0.0};
+      for (int j = ea; j < eb_; ++j)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) sv[c] += Es[c * NE + j];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) pi[c * NI + k] = sv[c];
+    }
+    __syncthreads();
+    // ---- B2: q = sum of the node's item partials + group BC; p = z + beta p; partial p.q
+    acc = 0.0;
+    for (int l = tid; l < nl; l += kCT) {
+      const int u = u0 + l;
+      double qv[3] = {0.0, 0.0, 0.0}, pv[3];
+      for (int k = __ldg(a.uitem + u) - i0, ke = __ldg(a.uitem + u + 1) - i0; k < ke; ++k)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) qv[c] += pi[c * NI + k];
+      if (u < a.ng) group_bc<3>(__ldg(a.kind + u), a.normal + 3 * u, qv);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        pv[c] = fma(beta, ps[c * NL + l], zs[c * NL + l]);
+        ps[c * NL + l] = pv[c];
+        qs[c * NL + l] = qv[c];
+      }
+      acc += pv[0] * qv[0] + pv[1] * qv[1] + pv[2] * qv[2];
+    }
+    tick(2);
+    const double pq = csum(acc);
+    tick(3);
+    const double alpha = (rz > 1e-300 && pq != 0.0) ? rz / pq : 0.0;
+    // ---- C: x += alpha p, r -= alpha q, z = P_v M D^-1 r; partial r.z
+    acc = 0.0;
+    for (int l = tid; l < nl; l += kCT) {
+      double rv[3], zv[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        xs[c * NL + l] = fma(alpha, ps[c * NL + l], xs[c * NL + l]);
+        rv[c] = fma(-alpha, qs[c * NL + l], rs[c * NL + l]);
+        rs[c * NL + l] = rv[c];
+        zv[c] = ds[c * NL + l] * rv[c];
+      }
+      bc_project(__ldg(a.bcn + __ldg(a.urep + u0 + l)), a.normal, zv[0], zv[1], zv[2]);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) zs[c * NL + l] = zv[c];
+      acc += rv[0] * zv[0] + rv[1] * zv[1] + rv[2] * zv[2];
+    }
+    tick(4);
+    const double rzn = csum(acc);
+    tick(5);
+    beta = rz > 1e-300 ? rzn / rz : 0.0;
+    rz = rzn;
+  }
+  // x to every copy
+  for (int l = tid; l < nl; l += kCT) {
+    const int u = u0 + l;
+    for (int k = __ldg(a.ucp + u), ke = __ldg(a.ucp + u + 1); k < ke; ++k) {
+      const int64_t i = __ldg(a.ucopy + k);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) a.x[i + c * cs] = xs[c * NL + l];
+    }
+  }
+  if (gt == 0) *a.it_out = it;
+  cl.sync();  // no CTA may exit while others still read its shared memory
+}
+
 struct CoarseSolver {
   CoarseArgs a{};
   size_t smem = 0;
+  bool sm = false;  // shared-memory-resident variant
   bool blend = false, full = true, etaq = false;
   std::vector<void*> bufs;
   ~CoarseSolver() {
@@ -436,6 +622,32 @@ int coarse_create(const Mesh* m, int level, int form, const double* eta, const d
   }
   if (smem_max > 200 * 1024) return bail(fail(HHG_ENOMEM, "coarse solver: coarse level too large for one cluster"));
   c->smem = smem_max;
+  // shared-memory-resident layout: owner CTA | local index of each tet node's unique node and E slot
+  std::vector<int32_t> onode(10 * (size_t)nt), opos(10 * (size_t)nt), eb(kCl + 1);
+  int NL = 0, NE = 0, NI = 0;
+  {
+    std::vector<int32_t> cta_of(nu);
+    for (int b = 0; b < kCl; ++b) {
+      for (int64_t u = ub[b]; u < ub[b + 1]; ++u) cta_of[u] = b;
+      eb[b] = useg[ub[b]];
+      NL = std::max(NL, ub[b + 1] - ub[b]);
+      NE = std::max(NE, useg[ub[b + 1]] - useg[ub[b]]);
+      NI = std::max(NI, ib[b + 1] - ib[b]);
+    }
+    eb[kCl] = useg[nu];
+    for (int e = 0; e < nt; ++e)
+      for (int q = 0; q < 10; ++q) {
+        const int u = uof[tn[e][q]], b = cta_of[u];
+        onode[(size_t)q * nt + e] = b << 24 | (u - ub[b]);
+        opos[(size_t)q * nt + e] = b << 24 | (pos[(size_t)q * nt + e] - eb[b]);
+      }
+  }
+  const size_t smem_sm = sizeof(double) * (18 * (size_t)NL + 3 * (size_t)NE + 3 * (size_t)NI);
+  {
+    const char* e = getenv("HHG_CCL_GLOBAL");  // A/B switch: force the global-memory variant
+    c->sm = smem_sm <= 200 * 1024 && !(e && e[0] == '1');
+  }
+  if (c->sm) c->smem = smem_sm;
   CoarseArgs& a = c->a;
   a.ns = ns;
   a.ntet = nt;
@@ -448,10 +660,14 @@ int coarse_create(const Mesh* m, int level, int form, const double* eta, const d
   int r;
   a.nu = (int)nu;
   a.ng = (int)ng;
+  a.NL = NL;
+  a.NE = NE;
+  a.NI = NI;
   if ((r = upload(c, node, &a.node)) || (r = upload(c, p1v, &a.p1)) || (r = upload(c, info, &a.info)) ||
       (r = upload(c, anc, &a.anc)) || (r = upload(c, pos, &a.pos)) || (r = upload(c, ucp, &a.ucp)) ||
       (r = upload(c, ucopy, &a.ucopy)) || (r = upload(c, urep, &a.urep)) || (r = upload(c, ub, &a.ub)) ||
-      (r = upload(c, ib, &a.ib)) || (r = upload(c, item, &a.item)) || (r = upload(c, uitem, &a.uitem)))
+      (r = upload(c, ib, &a.ib)) || (r = upload(c, item, &a.item)) || (r = upload(c, uitem, &a.uitem)) ||
+      (r = upload(c, onode, &a.onode)) || (r = upload(c, opos, &a.opos)) || (r = upload(c, eb, &a.eb)))
     return bail(r);
   a.kind = L.g2.kind;
   a.normal = L.g2.normal;
@@ -468,12 +684,25 @@ int coarse_create(const Mesh* m, int level, int form, const double* eta, const d
   a.part = a.E + (size_t)30 * std::max(nt, 1);
   a.it_out = reinterpret_cast<int*>(a.part + 3 * kClMax);
   HHG_CUDA(cudaMemset(a.it_out, 0, sizeof(int)));
+  {
+    const char* e = getenv("HHG_CCL_TIMING");
+    if (e && e[0] == '1') {
+      void* d = nullptr;
+      HHG_CUDA(cudaMalloc(&d, 6 * sizeof(unsigned long long)));
+      c->bufs.push_back(d);
+      HHG_CUDA(cudaMemset(d, 0, 6 * sizeof(unsigned long long)));
+      a.dbg = static_cast<unsigned long long*>(d);
+    }
+  }
   c->blend = m->blend == HHG_BLEND_SHELL;
   c->full = form == HHG_VISC_FULL;
   c->etaq = T2 != nullptr;
   if (c->etaq && !c->full) return bail(fail(HHG_EINVAL, "coarse solver: quadrature-point viscosity needs the full form"));
-#define HHG_CSMEM(B, F, Q) \
-  r = cudaFuncSetAttribute(k_coarse_pcg<B, F, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem) == cudaSuccess ? HHG_OK : fail(HHG_ECUDA, "coarse solver: shared memory attribute");
+#define HHG_CSMEM(B, F, Q)                                                                                    \
+  r = cudaFuncSetAttribute(c->sm ? k_coarse_pcg_sm<B, F, Q> : k_coarse_pcg<B, F, Q>,                         \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem) == cudaSuccess        \
+          ? HHG_OK                                                                                          \
+          : fail(HHG_ECUDA, "coarse solver: shared memory attribute");
   if (c->etaq) {
     if (c->blend) HHG_CSMEM(true, true, true) else HHG_CSMEM(false, true, true)
   } else if (c->blend) {
@@ -489,7 +718,8 @@ int coarse_create(const Mesh* m, int level, int form, const double* eta, const d
 
 template <bool B, bool F, bool Q>
 static int coarse_launch(CoarseSolver* c, cudaStream_t s) {
-  k_coarse_pcg<B, F, Q><<<kCl, kCT, c->smem, s>>>(c->a);
+  if (c->sm) k_coarse_pcg_sm<B, F, Q><<<kCl, kCT, c->smem, s>>>(c->a);
+  else k_coarse_pcg<B, F, Q><<<kCl, kCT, c->smem, s>>>(c->a);
   count_launch();
   HHG_CUDA(cudaGetLastError());
   return HHG_OK;
@@ -513,9 +743,22 @@ int coarse_run(CoarseSolver* c, const double* f, double* x, double* r, double* z
   return c->full ? coarse_launch<false, true, false>(c, s) : coarse_launch<false, false, false>(c, s);
 }
 
+int coarse_timing(const CoarseSolver* c, unsigned long long* ns6) {
+  if (!c->a.dbg) return fail(HHG_EINVAL, "coarse solver: built without HHG_CCL_TIMING=1");
+  HHG_CUDA(cudaDeviceSynchronize());
+  HHG_CUDA(cudaMemcpy(ns6, c->a.dbg, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  return HHG_OK;
+}
+
 int coarse_iterations(const CoarseSolver* c, int* out) {
   HHG_CUDA(cudaDeviceSynchronize());
   HHG_CUDA(cudaMemcpy(out, c->a.it_out, sizeof(int), cudaMemcpyDeviceToHost));
+  if (c->a.dbg) {  // HHG_CCL_TIMING=1 diagnostics (shared-memory variant): accumulated ns per phase
+    unsigned long long t[6];
+    HHG_TRY(coarse_timing(c, t));
+    fprintf(stderr, "{\"hhg_ccl_timing_ns\": {\"A\": %llu, \"sync_A\": %llu, \"B\": %llu, \"sum_pq\": %llu, \"C\": %llu, "
+            "\"sum_rz\": %llu}}\n", t[0], t[1], t[2], t[3], t[4], t[5]);
+  }
   return HHG_OK;
 }
 

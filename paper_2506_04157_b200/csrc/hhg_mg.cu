@@ -1407,6 +1407,11 @@ int hhg_stokes_create(hhg_mg* mg, hhg_mg* mg_cheap, const double* eta_p1, double
                           prm->wbfbt_max_iters < 1 || !(prm->tol_vmass > 0) || prm->vmass_max_iters < 1))
     return fail(HHG_EINVAL, "hhg_stokes_create: w-BFBT needs a_l, a_r > 0, a K tolerance, tol_vmass and iteration caps");
   if (prm->uzawa < 0 || prm->uzawa > 2) return fail(HHG_EINVAL, "hhg_stokes_create: uzawa must be 0, 1 or 2");
+  // the saddle-point operator applies A with the P1 viscosity eta_p1 on the finest level; a hierarchy that evaluates
+  // eta at the quadrature points there (l_eta >= l_max) would precondition a different A (l_eta < l_max)
+  if (mg->lv[mg->prm.l_max].T2 || (mg_cheap && mg_cheap->lv[mg_cheap->prm.l_max].T2))
+    return fail(HHG_EINVAL, "hhg_stokes_create: the hierarchies must use the P1 viscosity on the finest level "
+                            "(l_eta < l_max)");
   if (prm->schur == 1 && (!mg_cheap || mg_cheap->mesh != mg->mesh || mg_cheap->prm.l_max != mg->prm.l_max ||
                           !(prm->tol_vbfbt > 0) || prm->vbfbt_max_iters < 1))
     return fail(HHG_EINVAL, "hhg_stokes_create: V-BFBT needs a cheap hierarchy on the same mesh/levels and tol_vbfbt");

@@ -26,15 +26,17 @@ from workload import icoshell, uniform_vec  # noqa: E402
 C3 = (1e6, 30.0)
 
 
+def _with_env(var, make):
+    os.environ[var] = "1"
+    try:
+        return make()
+    finally:
+        del os.environ[var]
+
+
 def _pair(make):
     """(cluster-kernel object, generic-path object) built by make()"""
-    a = make()
-    os.environ["HHG_NO_CCL"] = "1"
-    try:
-        b = make()
-    finally:
-        del os.environ["HHG_NO_CCL"]
-    return a, b
+    return make(), _with_env("HHG_NO_CCL", make)
 
 
 @pytest.mark.parametrize("blend,form,level", [(True, hhg.HHG_VISC_FULL, 1), (False, hhg.HHG_VISC_EPS, 1),
@@ -57,17 +59,21 @@ def test_coarse_pcg_matches_oracle_and_generic_path(blend, form, level):
     eta = {level: lib_eta(M, level, C3)}
     mk = lambda: hhg.MG(M, level, level, eta, {}, coarse_iters=50, form=form)  # noqa: E731
     mg, mg_ref = _pair(mk)
+    mg_gl = _with_env("HHG_CCL_GLOBAL", mk)  # the global-memory variant of the cluster kernel
     assert mg.coarse_iterations() == 0  # the cluster kernel serves this level (the generic path raises)
     f = lib_u(M, level, 4)
-    x, x_ref = mg.vcycle(f), mg_ref.vcycle(f)
+    x, x_ref, x_gl = mg.vcycle(f), mg_ref.vcycle(f), mg_gl.vcycle(f)
     x2 = mg.vcycle(f)
     torch.cuda.synchronize()
     assert mg.coarse_iterations() == 50
     e_o = rel_l2(canon(M, level, hhg.HHG_P2VEC, x), x_o)
     e_g = float((x - x_ref).norm() / x_ref.norm())
-    print(f"coarse PCG level {level} blend={blend} form={form}: vs oracle {e_o:.2e}, vs generic path {e_g:.2e}")
+    print(f"coarse PCG level {level} blend={blend} form={form}: vs oracle {e_o:.2e}, vs generic path {e_g:.2e}, "
+          f"shared-memory vs global variant {float((x - x_gl).norm() / x_ref.norm()):.2e}")
     assert e_o <= 1e-9 and e_g <= 1e-9
     assert torch.equal(x, x2), "cluster coarse PCG must be bitwise reproducible"
+    # the two objects' D^-1 come from the (RED-summed) diag kernel, so they agree to rounding, not bitwise
+    assert float((x - x_gl).norm() / x_ref.norm()) <= 1e-14
 
 
 def test_coarse_pcg_quadrature_point_viscosity():

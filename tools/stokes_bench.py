@@ -28,6 +28,8 @@ ap.add_argument("--l-eta", type=int, default=-1, help="levels <= l_eta use quadr
 ap.add_argument("--l-min", type=int, default=1, help="coarsest level of the V-cycles (P:661: l_min = 2 on 240 macros)")
 ap.add_argument("--coarse-tol", type=float, default=0.0, help="coarse PCG relative tolerance (Table 1: 1e-2; 0: 50 its)")
 ap.add_argument("--coarse-iters", type=int, default=50)
+ap.add_argument("--tol-vbfbt", type=float, default=1e-1, help="Table 1: 1e-1")
+ap.add_argument("--cheap-coarse-iters", type=int, default=None, help="coarse PCG iterations of the A_C hierarchy")
 a = ap.parse_args()
 L = a.level
 M, etas, v0, _, n_dof = build_case(L, 0, contrast=a.contrast, jump=a.jump)
@@ -43,7 +45,8 @@ t0 = time.perf_counter()
 ck = dict(coarse_tol=a.coarse_tol, coarse_iters=a.coarse_iters)
 mg = hhg.MG(M, a.l_min, L, etas, v0, pre=3, post=3, degree=a.deg, T2_per_level=T2s, l_eta=a.l_eta, qeta=qeta, **ck)
 v0c = {l: v.clone() for l, v in build_case(L, 0, contrast=a.contrast, jump=a.jump)[2].items()} if a.schur == "vbfbt" else None
-mgc = hhg.MG(M, a.l_min, L, etas, v0c, pre=1, post=1, degree=1, T2_per_level=T2s, l_eta=a.l_eta, qeta=qeta, **ck) \
+ckc = dict(ck) if a.cheap_coarse_iters is None else dict(coarse_tol=0.0, coarse_iters=a.cheap_coarse_iters)
+mgc = hhg.MG(M, a.l_min, L, etas, v0c, pre=1, post=1, degree=1, T2_per_level=T2s, l_eta=a.l_eta, qeta=qeta, **ckc) \
     if a.schur == "vbfbt" else None
 keys = M.canonical_keys(L, hhg.HHG_P1)
 xyz = M.node_coords(L, hhg.HHG_P1)
@@ -52,7 +55,8 @@ T = M.from_canonical(L, hhg.HHG_P1, temperature(xc.cpu().numpy(), keys))
 f = hhg.hhg_buoyancy_load(M, L, T)
 rhs = torch.cat([f, M.zeros(L, hhg.HHG_P1)])
 S = hhg.StokesSolver(mg, etas[L], GAMMA, restart=a.restart, max_iters=a.max_iters, tol=a.tol, schur=a.schur,
-                     mg_cheap=mgc, omega=a.omega, a_l=a.a_l, a_r=a.a_r, uzawa=a.uzawa, tol_A=a.tol_A)
+                     mg_cheap=mgc, omega=a.omega, a_l=a.a_l, a_r=a.a_r, uzawa=a.uzawa, tol_A=a.tol_A,
+                     tol_vbfbt=a.tol_vbfbt)
 torch.cuda.synchronize()
 setup = time.perf_counter() - t0
 s = torch.cuda.Stream()
@@ -66,6 +70,7 @@ ms = e0.elapsed_time(e1)
 n_p = M.canonical_len(L, hhg.HHG_P1)
 x2, ita, rela = mg.ablock_cg(f, tol=1e-2, max_iters=200)
 print(json.dumps({"what": "stokes_solve", "l_eta": a.l_eta, "l_min": a.l_min, "coarse_tol": a.coarse_tol,
+                  "tol_vbfbt": a.tol_vbfbt, "cheap_coarse_iters": a.cheap_coarse_iters, "restart": a.restart,
                   "coarse_iters_max": a.coarse_iters, "ablock_cg_iters_tol1e-2": ita, "ablock_rel": rela, "level": L, "schur": a.schur, "omega": a.omega, "a_l": a.a_l, "a_r": a.a_r, "uzawa": a.uzawa, "tol_A": a.tol_A, "velocity_dofs": n_dof, "pressure_dofs": n_p,
                   "fgmres_iters": it, "rel_res": rel, "tol": a.tol, "solve_s": ms / 1e3, "setup_s": setup,
                   "viscosity": f"contrast {a.contrast:g} x {a.jump:g} jump", "rhs": "buoyancy (T - 1/2) x/|x|, g = 0"}))
