@@ -194,7 +194,9 @@ class StokesOracle:
         return np.concatenate([u, p])
 
     def solve(self, rhs, tol=1e-8, restart=30, max_iters=100):
-        """FGMRES from x = 0 -> (x, iterations, relative residual of the projected system)."""
+        """FGMRES from x = 0 -> (x, iterations, relative residual of the projected system); the residual estimate
+        of every iteration is appended to self.history."""
+        self.history = []
         b = np.concatenate([self.Pm @ rhs[:self.n2], mean0(rhs[self.n2:])])
         bn = float(np.linalg.norm(b))
         x = np.zeros_like(b)
@@ -232,6 +234,7 @@ class StokesOracle:
                 g[j + 1] = -sn[j] * g[j]
                 g[j] = cs[j] * g[j]
                 rel = abs(g[j + 1]) / bn
+                self.history.append(rel)
                 j += 1
                 if rel <= tol or hn == 0.0:
                     break

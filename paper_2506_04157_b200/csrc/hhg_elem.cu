@@ -129,16 +129,16 @@ static_assert(sizeof(MacroGeo) == kMG * sizeof(double), "MacroGeo layout");
 // (deterministic mode, one launch per brick colour -- bricks of one colour share no footprint point):
 // border points use plain load-add-store instead of fp64 REDs and sparse bricks take the dense path, so
 // the result is bitwise reproducible.
-template <bool BLEND, int MODE, bool FULL, bool ETAQ = false>
+template <bool BLEND, int MODE, bool FULL, bool ETAQ = false, int EPI = EPI_NONE>
 #ifndef HHG_FP_MINB
 #define HHG_FP_MINB 5
 #endif
 __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
     k_elem_fp(const MacroGeo* __restrict__ mgeo, const double* __restrict__ lgeo, const int32_t* __restrict__ bricks,
               int nb, int n1, double inv_n1, int64_t npts1, int64_t npts2, int64_t cstride,
-              const double* __restrict__ eta, const double* __restrict__ u, const double* __restrict__ p,
+              const double* __restrict__ eta, const double* u, const double* __restrict__ p,
               double* __restrict__ yu, double* __restrict__ yp, double gamma, const double* __restrict__ T2, EtaQ eq,
-              int det) {
+              int det, ChebEpi ep) {
   (void)nb;
   constexpr bool NEED_U = elem_need_u(MODE);
   constexpr bool NEED_P = elem_need_p(MODE);
@@ -394,8 +394,30 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
         if (Z < 4) v = sy[c * kFY + wxy + kPZ * Z];
         else if (Z > 4) v = sy[3 * kFY + c * kFY + wxy + kPZ * (Z - 4)];
         else v = sy[c * kFY + wxy + kPZ * 4] + sy[3 * kFY + c * kFY + wxy];
-        if (!border) dst[c * cstride] = v;
-        else if (v != 0.0) {
+        if (EPI != EPI_NONE && !border && !det && gx + gy + gz < n2) {
+          // fused consumer update (launch_elem_epi): this point is complete, inside the macro, BC-free
+          const int64_t j = (dst - yu) + c * cstride;
+          if (EPI == EPI_SUB) {
+            ep.r[j] = ep.f[j] - v;
+          } else if (EPI == EPI_CHEB0) {
+            const double ri = ep.f[j] - v;
+            ep.r[j] = ri;
+            ep.d[j] = ep.dinv[j] * ri * ep.c1;
+          } else {
+            const double di = su[c * kFU + xs(X) + kPY * Y + kPZ * Z];  // the apply input d at this point
+            if (EPI == EPI_CHEBK) {
+              ep.x[j] += di;
+              const double ri = ep.r[j] - v;
+              ep.r[j] = ri;
+              ep.d[j] = ep.c1 * di + ep.c2 * ep.dinv[j] * ri;
+            } else {
+              const double dn = ep.c1 * di + ep.c2 * ep.dinv[j] * (ep.r[j] - v);
+              ep.x[j] += di + dn;
+            }
+          }
+        } else if (!border) {
+          dst[c * cstride] = v;
+        } else if (v != 0.0) {
           if (det) dst[c * cstride] += v;
           else atomicAdd(dst + c * cstride, v);
         }
@@ -424,27 +446,27 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
 
 // Launch of one element-kernel instantiation: one CTA per (macro, brick) item, one launch over all bricks --
 // or, in deterministic mode, one launch per brick colour.
-template <bool BLEND, int MODE, bool FULL, bool ETAQ>
+template <bool BLEND, int MODE, bool FULL, bool ETAQ, int EPI = EPI_NONE>
 struct ElemKernel {
   static constexpr size_t smem = fp_smem_words<MODE, ETAQ>() * sizeof(double);
   static bool ready;
   static int prepare() {  // host-side attributes (eager: never under stream capture)
     if (ready) return HHG_OK;
-    auto k = k_elem_fp<BLEND, MODE, FULL, ETAQ>;
+    auto k = k_elem_fp<BLEND, MODE, FULL, ETAQ, EPI>;
     HHG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared));
     HHG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     ready = true;
     return HHG_OK;
   }
   static int launch(const Mesh* m, const Level& L, const double* eta, double gamma, const double* u, const double* p,
-                    double* yu, double* yp, const double* T2, EtaQ eq, cudaStream_t s) {
+                    double* yu, double* yp, const double* T2, EtaQ eq, cudaStream_t s, ChebEpi ep = ChebEpi{}) {
     HHG_TRY(prepare());
     const int64_t nm = macro_count(m);
     auto go = [&](const int32_t* list, int64_t nb, int det) {
       if (nm * nb == 0) return;
-      k_elem_fp<BLEND, MODE, FULL, ETAQ><<<dim3((unsigned)nb, (unsigned)nm), kBT, smem, s>>>(m->dgeo, L.geo, list, (int)nb, L.n1,
-                                                                           1.0 / L.n1, L.npts1, L.npts2, nm * L.npts2,
-                                                                           eta, u, p, yu, yp, gamma, T2, eq, det);
+      k_elem_fp<BLEND, MODE, FULL, ETAQ, EPI><<<dim3((unsigned)nb, (unsigned)nm), kBT, smem, s>>>(
+          m->dgeo, L.geo, list, (int)nb, L.n1, 1.0 / L.n1, L.npts1, L.npts2, nm * L.npts2, eta, u, p, yu, yp, gamma, T2,
+          eq, det, ep);
       count_launch();
     };
     if (!m->deterministic) {
@@ -456,8 +478,8 @@ struct ElemKernel {
     return HHG_OK;
   }
 };
-template <bool BLEND, int MODE, bool FULL, bool ETAQ>
-bool ElemKernel<BLEND, MODE, FULL, ETAQ>::ready = false;
+template <bool BLEND, int MODE, bool FULL, bool ETAQ, int EPI>
+bool ElemKernel<BLEND, MODE, FULL, ETAQ, EPI>::ready = false;
 
 static bool g_slots_ready = false;
 static int ensure_slots() {
@@ -598,6 +620,50 @@ int launch_elem(const Mesh* m, const Level& L, int mode, int form, const double*
 #undef HHG_DISPATCH
 }
 
+int launch_elem_epi(const Mesh* m, const Level& L, int kind, const ChebEpi& e, const double* eta, const double* u,
+                    double* yu, cudaStream_t s) {
+  if (macro_count(m) == 0) return HHG_OK;
+  if (m->deterministic || m->nranks != 1) return fail(HHG_EINVAL, "fused epilogue: single rank, non-deterministic only");
+  HHG_TRY(ensure_slots());
+  const bool bl = m->blend == HHG_BLEND_SHELL;
+  const EtaQ eq{0.0, 1.0, 0.0};
+#define HHG_EPI(K)                                                                                              \
+  return bl ? ElemKernel<true, ELEM_A, true, false, K>::launch(m, L, eta, 0.0, u, nullptr, yu, nullptr, nullptr, eq, s, e) \
+            : ElemKernel<false, ELEM_A, true, false, K>::launch(m, L, eta, 0.0, u, nullptr, yu, nullptr, nullptr, eq, s, e);
+  switch (kind) {
+    case EPI_SUB: HHG_EPI(EPI_SUB);
+    case EPI_CHEB0: HHG_EPI(EPI_CHEB0);
+    case EPI_CHEBK: HHG_EPI(EPI_CHEBK);
+    case EPI_CHEBK_LAST: HHG_EPI(EPI_CHEBK_LAST);
+    default: return fail(HHG_EINVAL, "bad fused epilogue");
+  }
+#undef HHG_EPI
+}
+
+// Nodes the fused epilogue updates: footprint-interior points (X, Y, Z in 1..7) of the dense bricks (delta > 4,
+// the ones k_elem_fp runs on the per-cube path), strictly inside the macro (i + j + k < n2).  Host-built, once.
+int elem_fused_mask(const Mesh* m, const Level& L, uint8_t** mask) {
+  const int64_t nm = macro_count(m), ns = nm * L.npts2;
+  std::vector<int32_t> br(L.n_bricks);
+  if (L.n_bricks) HHG_CUDA(cudaMemcpy(br.data(), L.bricks, L.n_bricks * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  std::vector<uint8_t> h(ns, 0), one(L.npts2, 0);
+  const int n1 = L.n1, n2 = L.n2;
+  for (int32_t bpk : br) {
+    const int i0 = bpk & 1023, j0 = (bpk >> 10) & 1023, k0 = bpk >> 20;
+    if (n1 - (i0 + j0 + k0) <= 4) continue;  // sparse brick: REDs only
+    for (int Z = 1; Z < 8; ++Z)
+      for (int Y = 1; Y < 8; ++Y)
+        for (int X = 1; X < 8; ++X) {
+          const int gx = 2 * i0 + X, gy = 2 * j0 + Y, gz = 2 * k0 + Z;
+          if (gx + gy + gz < n2) one[lidx(gx, gy, gz, n2)] = 1;
+        }
+  }
+  for (int64_t mc = 0; mc < nm; ++mc) std::copy(one.begin(), one.end(), h.begin() + mc * L.npts2);
+  HHG_CUDA(cudaMalloc(mask, std::max<int64_t>(ns, 1)));
+  if (ns) HHG_CUDA(cudaMemcpy(*mask, h.data(), ns, cudaMemcpyHostToDevice));
+  return HHG_OK;
+}
+
 // Eager one-time set-up of the element kernels (tables in __constant__ memory, kernel attributes,
 // occupancy): called from mesh/level construction so that no hot call -- in particular none under
 // CUDA-graph capture -- runs a synchronous host API.
@@ -619,6 +685,10 @@ int elem_prepare_all() {
   HHG_PREP(true, ELEM_VMASS, true, false) HHG_PREP(false, ELEM_VMASS, true, false)
   HHG_PREP(true, ELEM_VMASSD, true, false) HHG_PREP(false, ELEM_VMASSD, true, false)
   HHG_PREP(true, ELEM_A, true, true) HHG_PREP(false, ELEM_A, true, true)
+#define HHG_PREPE(K) HHG_TRY((ElemKernel<true, ELEM_A, true, false, K>::prepare())); \
+  HHG_TRY((ElemKernel<false, ELEM_A, true, false, K>::prepare()));
+  HHG_PREPE(EPI_SUB) HHG_PREPE(EPI_CHEB0) HHG_PREPE(EPI_CHEBK) HHG_PREPE(EPI_CHEBK_LAST)
+#undef HHG_PREPE
   HHG_PREP(true, ELEM_DIAG, true, true) HHG_PREP(false, ELEM_DIAG, true, true)
 #undef HHG_PREP4
 #undef HHG_PREP

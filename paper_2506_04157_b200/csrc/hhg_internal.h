@@ -164,6 +164,23 @@ int launch_p1_prolong(const Mesh* m, const Level& Lc, const Level& Lf, const dou
 int launch_p1_restrict(const Mesh* m, const Level& Lc, const Level& Lf, const double* rf, double* rc, cudaStream_t s);
 int launch_elem_qeta(const Mesh* m, const Level& L, int mode, const double* T2, double lnC, double jump, double r_jump,
                      const double* u, double* yu, cudaStream_t s);
+// Smoother / residual update fused into the A kernel's write-out (single rank, non-deterministic mode, full form):
+// at the footprint-interior points of dense bricks strictly inside the macro (complete after the brick, no interface
+// copy, no BC) the kernel applies the consumer's update itself instead of storing A u; every other node keeps A u in
+// yu for the *_fx consumer, which skips the fused nodes (elem_fused_mask).  kind: EPI_SUB r = f - Au; EPI_CHEB0
+// r = f - Au, d = D^-1 r c1; EPI_CHEBK x += d, r -= Au, d = c1 d + c2 D^-1 r (d = the apply input); EPI_CHEBK_LAST
+// x += d + c1 d + c2 D^-1 (r - Au).  Same arithmetic as launch_sub_fx / launch_cheb0_fx / launch_chebk_fx /
+// launch_chebk_last_fx.
+enum { EPI_NONE = 0, EPI_SUB = 1, EPI_CHEB0 = 2, EPI_CHEBK = 3, EPI_CHEBK_LAST = 4 };
+struct ChebEpi {
+  const double* f;
+  double *x, *r, *d;
+  const double* dinv;
+  double c1, c2;
+};
+int launch_elem_epi(const Mesh* m, const Level& L, int kind, const ChebEpi& e, const double* eta, const double* u,
+                    double* yu, cudaStream_t s);
+int elem_fused_mask(const Mesh* m, const Level& L, uint8_t** mask);  // device [stored P2 nodes], caller frees
 enum { ELEM_A = 1, ELEM_BT = 2, ELEM_DIV = 4, ELEM_DIAG = 8, ELEM_MASS = 16, ELEM_MASSD = 32, ELEM_LOAD = 64,
        ELEM_KP1 = 128, ELEM_KP1D = 256, ELEM_VMASS = 512, ELEM_VMASSD = 1024 };
 constexpr int ELEM_SURF = ELEM_KP1 | ELEM_KP1D | ELEM_VMASS | ELEM_VMASSD;  // w-BFBT operators (eta_a scaling)
@@ -225,18 +242,19 @@ int launch_pcg_update_bc(const Mesh* m, const Level& L, int it, const double* sc
                          const double* p, const double* q, const double* dinv, double* z, cudaStream_t s);
 int launch_pcg_dir_zero(int64_t n, int it, const double* scal, const double* z, double* p, double* q_zero,
                         cudaStream_t s);
-// Consumers of an UNSUMMED element-kernel output t (single rank): each stored node reads its value as the sum
+// Consumers of an UNSUMMED element-kernel output t (single rank; skip != nullptr: nodes with skip[i] != 0 were
+// updated by the element kernel's fused epilogue, launch_elem_epi, and are left alone): each stored node reads its value as the sum
 // of its group's copies with the group's BC applied (= what k_fixup would have stored), so the separate
 // interface-sum pass disappears.  Same semantics as the *_bc kernels applied after launch_fixup(sum, BC).
 int launch_cheb0_fx(const Mesh* m, const Level& L, const double* f, const double* t, const double* dinv,
-                    double inv_theta, double* r, double* d, cudaStream_t s);
+                    double inv_theta, double* r, double* d, cudaStream_t s, const uint8_t* skip = nullptr);
 int launch_chebk_fx(const Mesh* m, const Level& L, const double* t, const double* dinv, double c1, double c2, double* x,
-                    double* r, double* d, cudaStream_t s);
+                    double* r, double* d, cudaStream_t s, const uint8_t* skip = nullptr);
 int launch_chebk_last_fx(const Mesh* m, const Level& L, const double* t, const double* dinv, double c1, double c2,
-                         const double* r, const double* d, double* x, cudaStream_t s);
+                         const double* r, const double* d, double* x, cudaStream_t s, const uint8_t* skip = nullptr);
 int launch_cheb_deg1_fx(const Mesh* m, const Level& L, const double* f, const double* t, const double* dinv,
                         double inv_theta, double* x, cudaStream_t s);
-int launch_sub_fx(const Mesh* m, const Level& L, const double* f, const double* t, double* r, cudaStream_t s);  // r = f - t
+int launch_sub_fx(const Mesh* m, const Level& L, const double* f, const double* t, double* r, cudaStream_t s, const uint8_t* skip = nullptr);  // r = f - t
 // PCG update fused with the new r.z (single rank): writes r.z into the ping-pong slot of iteration `it`
 int launch_pcg_update_bc_dot(const Mesh* m, const Level& L, int it, double* scal, double* x, double* r, const double* p,
                              const double* q, const double* dinv, double* z, double* red, cudaStream_t s);

@@ -979,6 +979,7 @@ struct FxArgs {
   const int64_t* __restrict__ copy;
   const uint8_t* __restrict__ kind;
   const double* __restrict__ normal;
+  const uint8_t* __restrict__ skip;  // nodes already updated by the fused element-kernel epilogue (or nullptr)
 };
 __device__ __forceinline__ void tval(const FxArgs& a, int64_t i, int64_t cs, const double* __restrict__ t,
                                      double (&v)[3]) {
@@ -991,12 +992,17 @@ __device__ __forceinline__ void tval(const FxArgs& a, int64_t i, int64_t cs, con
   group_sum<3>(a.ptr[g], a.ptr[g + 1], a.copy, cs, t, v);
   group_bc<3>(a.kind[g], a.normal + 3 * g, v);
 }
-static FxArgs fx_args(const Level& L) { return FxArgs{L.gmap2, L.g2.ptr, L.g2.copy, L.g2.kind, L.g2.normal}; }
+static FxArgs fx_args(const Level& L, const uint8_t* skip) {
+  return FxArgs{L.gmap2, L.g2.ptr, L.g2.copy, L.g2.kind, L.g2.normal, skip};
+}
+#define FX_SKIP(a, i) \
+  if ((a).skip && (a).skip[i]) continue;
 
 __global__ void k_cheb0_fx(int64_t ns, int64_t cs, FxArgs a, const double* __restrict__ f, const double* __restrict__ t,
                            const double* __restrict__ dinv, double it, double* __restrict__ r, double* __restrict__ d,
                            const int32_t* __restrict__ bcn, const double* __restrict__ nrm) {
   GRID_STRIDE(i, ns) {
+    FX_SKIP(a, i)
     double tv[3], dv[3];
     tval(a, i, cs, t, tv);
 #pragma unroll
@@ -1015,6 +1021,7 @@ __global__ void k_cheb_deg1_fx(int64_t ns, int64_t cs, FxArgs a, const double* _
                                const double* __restrict__ t, const double* __restrict__ dinv, double it,
                                double* __restrict__ x, const int32_t* __restrict__ bcn, const double* __restrict__ nrm) {
   GRID_STRIDE(i, ns) {
+    FX_SKIP(a, i)
     double tv[3], dv[3];
     tval(a, i, cs, t, tv);
 #pragma unroll
@@ -1032,6 +1039,7 @@ __global__ void k_chebk_fx(int64_t ns, int64_t cs, FxArgs a, const double* __res
                            double* __restrict__ r, double* __restrict__ d, const int32_t* __restrict__ bcn,
                            const double* __restrict__ nrm) {
   GRID_STRIDE(i, ns) {
+    FX_SKIP(a, i)
     double tv[3], dv[3];
     tval(a, i, cs, t, tv);
 #pragma unroll
@@ -1053,6 +1061,7 @@ __global__ void k_chebk_last_fx(int64_t ns, int64_t cs, FxArgs a, const double* 
                                 const double* __restrict__ d, double* __restrict__ x, const int32_t* __restrict__ bcn,
                                 const double* __restrict__ nrm) {
   GRID_STRIDE(i, ns) {
+    FX_SKIP(a, i)
     double tv[3], dn[3], dold[3];
     tval(a, i, cs, t, tv);
 #pragma unroll
@@ -1069,6 +1078,7 @@ __global__ void k_chebk_last_fx(int64_t ns, int64_t cs, FxArgs a, const double* 
 __global__ void k_sub_fx(int64_t ns, int64_t cs, FxArgs a, const double* __restrict__ f, const double* __restrict__ t,
                          double* __restrict__ r) {
   GRID_STRIDE(i, ns) {
+    FX_SKIP(a, i)
     double tv[3];
     tval(a, i, cs, t, tv);
 #pragma unroll
@@ -1076,9 +1086,9 @@ __global__ void k_sub_fx(int64_t ns, int64_t cs, FxArgs a, const double* __restr
   }
 }
 int launch_cheb0_fx(const Mesh* m, const Level& L, const double* f, const double* t, const double* dinv,
-                    double inv_theta, double* r, double* d, cudaStream_t s) {
+                    double inv_theta, double* r, double* d, cudaStream_t s, const uint8_t* skip) {
   const int64_t ns = macro_count(m) * L.npts2;
-  k_cheb0_fx<<<ngrid(ns), 256, 0, s>>>(ns, ns, fx_args(L), f, t, dinv, inv_theta, r, d, L.bcn2, L.g2.normal);
+  k_cheb0_fx<<<ngrid(ns), 256, 0, s>>>(ns, ns, fx_args(L, skip), f, t, dinv, inv_theta, r, d, L.bcn2, L.g2.normal);
   count_launch();
   HHG_CUDA(cudaGetLastError());
   return HHG_OK;
@@ -1086,30 +1096,30 @@ int launch_cheb0_fx(const Mesh* m, const Level& L, const double* f, const double
 int launch_cheb_deg1_fx(const Mesh* m, const Level& L, const double* f, const double* t, const double* dinv,
                         double inv_theta, double* x, cudaStream_t s) {
   const int64_t ns = macro_count(m) * L.npts2;
-  k_cheb_deg1_fx<<<ngrid(ns), 256, 0, s>>>(ns, ns, fx_args(L), f, t, dinv, inv_theta, x, L.bcn2, L.g2.normal);
+  k_cheb_deg1_fx<<<ngrid(ns), 256, 0, s>>>(ns, ns, fx_args(L, nullptr), f, t, dinv, inv_theta, x, L.bcn2, L.g2.normal);
   count_launch();
   HHG_CUDA(cudaGetLastError());
   return HHG_OK;
 }
 int launch_chebk_fx(const Mesh* m, const Level& L, const double* t, const double* dinv, double c1, double c2, double* x,
-                    double* r, double* d, cudaStream_t s) {
+                    double* r, double* d, cudaStream_t s, const uint8_t* skip) {
   const int64_t ns = macro_count(m) * L.npts2;
-  k_chebk_fx<<<ngrid(ns), 256, 0, s>>>(ns, ns, fx_args(L), t, dinv, c1, c2, x, r, d, L.bcn2, L.g2.normal);
+  k_chebk_fx<<<ngrid(ns), 256, 0, s>>>(ns, ns, fx_args(L, skip), t, dinv, c1, c2, x, r, d, L.bcn2, L.g2.normal);
   count_launch();
   HHG_CUDA(cudaGetLastError());
   return HHG_OK;
 }
 int launch_chebk_last_fx(const Mesh* m, const Level& L, const double* t, const double* dinv, double c1, double c2,
-                         const double* r, const double* d, double* x, cudaStream_t s) {
+                         const double* r, const double* d, double* x, cudaStream_t s, const uint8_t* skip) {
   const int64_t ns = macro_count(m) * L.npts2;
-  k_chebk_last_fx<<<ngrid(ns), 256, 0, s>>>(ns, ns, fx_args(L), t, dinv, c1, c2, r, d, x, L.bcn2, L.g2.normal);
+  k_chebk_last_fx<<<ngrid(ns), 256, 0, s>>>(ns, ns, fx_args(L, skip), t, dinv, c1, c2, r, d, x, L.bcn2, L.g2.normal);
   count_launch();
   HHG_CUDA(cudaGetLastError());
   return HHG_OK;
 }
-int launch_sub_fx(const Mesh* m, const Level& L, const double* f, const double* t, double* r, cudaStream_t s) {
+int launch_sub_fx(const Mesh* m, const Level& L, const double* f, const double* t, double* r, cudaStream_t s, const uint8_t* skip) {
   const int64_t ns = macro_count(m) * L.npts2;
-  k_sub_fx<<<ngrid(ns), 256, 0, s>>>(ns, ns, fx_args(L), f, t, r);
+  k_sub_fx<<<ngrid(ns), 256, 0, s>>>(ns, ns, fx_args(L, skip), f, t, r);
   count_launch();
   HHG_CUDA(cudaGetLastError());
   return HHG_OK;

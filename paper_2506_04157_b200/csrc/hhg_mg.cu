@@ -84,6 +84,7 @@ struct hhg_mg {
     const double* eta = nullptr;
     const double* T2 = nullptr;   // P2 temperature: quadrature-point viscosity on this level (l <= l_eta)
     double lam = 0.0;
+    uint8_t* fmask = nullptr;     // nodes updated by the fused smoother epilogue (launch_elem_epi), or nullptr
   };
   std::vector<Lv> lv;
   double* scal = nullptr;    // device scalars
@@ -121,9 +122,11 @@ struct hhg_mg {
   double apply_ms = 0, cycle_ms = 0;
   int64_t apply_n = 0, cycle_n = 0;
   ~hhg_mg() {
-    for (auto& L : lv)
+    for (auto& L : lv) {
       for (double* p : {L.x, L.f, L.r, L.d, L.t, L.dinv, L.p})
         if (p) cudaFree(p);
+      if (L.fmask) cudaFree(L.fmask);
+    }
     if (scal) cudaFree(scal);
     if (red) cudaFree(red);
     if (cmg) delete cmg;
@@ -154,7 +157,7 @@ struct hhg_mg {
 };
 
 static int mg_apply(hhg_mg* mg, int l, const double* u, double* y, cudaStream_t s, bool y_zeroed = false,
-                    bool fixup = true) {
+                    bool fixup = true, int epi = EPI_NONE, const ChebEpi* ep = nullptr) {
   const bool timed = mg->prof && l == mg->prm.l_max;
   if (timed) {
     if (mg->ev_used + 2 > mg->ev.size()) {
@@ -172,6 +175,8 @@ static int mg_apply(hhg_mg* mg, int l, const double* u, double* y, cudaStream_t 
   if (mg->lv[l].T2)
     HHG_TRY(launch_elem_qeta(mg->mesh, L, ELEM_A, mg->lv[l].T2, mg->prm.qeta_lnC, mg->prm.qeta_jump, mg->prm.qeta_rjump,
                              u, y, s));
+  else if (epi != EPI_NONE)
+    HHG_TRY(launch_elem_epi(mg->mesh, L, epi, *ep, mg->lv[l].eta, u, y, s));
   else
     HHG_TRY(launch_elem(mg->mesh, L, ELEM_A, mg->prm.visc_form, mg->lv[l].eta, 0.0, u, nullptr, y, nullptr, s));
   if (timed) {
@@ -194,25 +199,30 @@ static int mg_cheb(hhg_mg* mg, int l, double* x, const double* f, bool x_is_zero
   double rho = 1.0 / sigma;
   const Level& LL = m->levels[l];
   const bool fx = mg->fuse_fx;  // consumers sum the interface copies of A's raw output themselves
+  // smoother updates of brick-interior nodes fused into the element kernel's write-out (launch_elem_epi)
+  const uint8_t* sk = fx ? L.fmask : nullptr;
+  const int deg = mg->prm.degree;
   const double* t0 = nullptr;
   if (!x_is_zero) {
-    HHG_TRY(mg_apply(mg, l, x, L.t, s, false, !fx));
+    const ChebEpi e0{f, x, L.r, L.d, L.dinv, 1.0 / theta, 0.0};
+    HHG_TRY(mg_apply(mg, l, x, L.t, s, false, !fx, (sk && deg > 1) ? EPI_CHEB0 : EPI_NONE, &e0));
     t0 = L.t;
   }
-  const int deg = mg->prm.degree;
   if (deg == 1)
     return fx && t0 ? launch_cheb_deg1_fx(m, LL, f, t0, L.dinv, 1.0 / theta, x, s)
                     : launch_cheb_deg1_bc(m, LL, f, t0, L.dinv, 1.0 / theta, x, s);
-  if (fx && t0) HHG_TRY(launch_cheb0_fx(m, LL, f, t0, L.dinv, 1.0 / theta, L.r, L.d, s));
+  if (fx && t0) HHG_TRY(launch_cheb0_fx(m, LL, f, t0, L.dinv, 1.0 / theta, L.r, L.d, s, sk));
   else HHG_TRY(launch_cheb0_bc(m, LL, f, t0, L.dinv, 1.0 / theta, L.r, L.d, s));
   for (int k = 1; k < deg; ++k) {
-    HHG_TRY(mg_apply(mg, l, L.d, L.t, s, false, !fx));
     const double rn = 1.0 / (2.0 * sigma - rho);
+    const bool last = k == deg - 1;
+    const ChebEpi ek{f, x, L.r, L.d, L.dinv, rn * rho, 2.0 * rn / delta};
+    HHG_TRY(mg_apply(mg, l, L.d, L.t, s, false, !fx, sk ? (last ? EPI_CHEBK_LAST : EPI_CHEBK) : EPI_NONE, &ek));
     if (fx) {
-      if (k < deg - 1) HHG_TRY(launch_chebk_fx(m, LL, L.t, L.dinv, rn * rho, 2.0 * rn / delta, x, L.r, L.d, s));
-      else HHG_TRY(launch_chebk_last_fx(m, LL, L.t, L.dinv, rn * rho, 2.0 * rn / delta, L.r, L.d, x, s));
+      if (!last) HHG_TRY(launch_chebk_fx(m, LL, L.t, L.dinv, rn * rho, 2.0 * rn / delta, x, L.r, L.d, s, sk));
+      else HHG_TRY(launch_chebk_last_fx(m, LL, L.t, L.dinv, rn * rho, 2.0 * rn / delta, L.r, L.d, x, s, sk));
     } else {
-      if (k < deg - 1) HHG_TRY(launch_chebk_bc(m, LL, L.t, L.dinv, rn * rho, 2.0 * rn / delta, x, L.r, L.d, s));
+      if (!last) HHG_TRY(launch_chebk_bc(m, LL, L.t, L.dinv, rn * rho, 2.0 * rn / delta, x, L.r, L.d, s));
       else HHG_TRY(launch_chebk_last_bc(m, LL, L.t, L.dinv, rn * rho, 2.0 * rn / delta, L.r, L.d, x, s));
     }
     rho = rn;
@@ -298,8 +308,9 @@ static int mg_cycle(hhg_mg* mg, int l, const double* f, double* x, cudaStream_t 
   for (int i = 0; i < mg->prm.pre; ++i) HHG_TRY(mg_cheb(mg, l, x, f, i == 0, s));
   // r = f - A x  (into L.r), restrict into f_{l-1}
   if (mg->fuse_fx) {
-    HHG_TRY(mg_apply(mg, l, x, L.t, s, false, false));
-    HHG_TRY(launch_sub_fx(m, m->levels[l], f, L.t, L.r, s));
+    const ChebEpi er{f, x, L.r, L.d, L.dinv, 0.0, 0.0};
+    HHG_TRY(mg_apply(mg, l, x, L.t, s, false, false, L.fmask ? EPI_SUB : EPI_NONE, &er));
+    HHG_TRY(launch_sub_fx(m, m->levels[l], f, L.t, L.r, s, L.fmask));
   } else {
     HHG_TRY(mg_apply(mg, l, x, L.t, s));
     k_sub<<<vg(n), 256, 0, s>>>(n, f, L.t, L.r);
@@ -396,6 +407,17 @@ int hhg_mg_create_qeta(hhg_mesh* mesh, const hhg_mg_params* params, const double
                : hhg_power_iteration(mesh, l, L.eta, L.dinv, P.power_iters, power_v0[l], &L.lam, nullptr);
       if (r != HHG_OK) return bail(r);
     }
+  }
+  {
+    // fused smoother epilogue: single rank (interface sums in the consumers), atomic element kernels, full form,
+    // P1 viscosity levels above l_min
+    const char* e = getenv("HHG_NO_EPI");  // A/B switch
+    if (mg->fuse_fx && !mesh->deterministic && P.visc_form == HHG_VISC_FULL && !(e && e[0] == '1'))
+      for (int l = P.l_min + 1; l <= P.l_max; ++l)
+        if (!mg->lv[l].T2) {
+          const int r = elem_fused_mask(mesh, mesh->levels[l], &mg->lv[l].fmask);
+          if (r != HHG_OK) return bail(r);
+        }
   }
   {
     const char* e = getenv("HHG_NO_CCL");  // A/B switch: the coarse PCG through the generic launches
