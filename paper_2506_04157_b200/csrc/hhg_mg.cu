@@ -411,8 +411,11 @@ int hhg_mg_create_qeta(hhg_mesh* mesh, const hhg_mg_params* params, const double
   {
     // fused smoother epilogue: single rank (interface sums in the consumers), atomic element kernels, full form,
     // P1 viscosity levels above l_min
-    const char* e = getenv("HHG_NO_EPI");  // A/B switch
-    if (mg->fuse_fx && !mesh->deterministic && P.visc_form == HHG_VISC_FULL && !(e && e[0] == '1'))
+    // Opt-in (HHG_EPI=1): measured SLOWER at L5 (V(3,3) 39.6 ms fused vs 25.8 ms unfused, profiles/r02_epi_ab.jsonl):
+    // the write-out's per-point read-modify-write of f, r, d, x, D^-1 serialises DRAM round trips inside a CTA that
+    // holds 43 KB of shared memory, and the *_fx consumers still stream every node (mask test) -- DESIGN.md §6.
+    const char* e = getenv("HHG_EPI");
+    if (mg->fuse_fx && !mesh->deterministic && P.visc_form == HHG_VISC_FULL && e && e[0] == '1')
       for (int l = P.l_min + 1; l <= P.l_max; ++l)
         if (!mg->lv[l].T2) {
           const int r = elem_fused_mask(mesh, mesh->levels[l], &mg->lv[l].fmask);

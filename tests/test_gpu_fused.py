@@ -1,5 +1,5 @@
 """GPU: the smoother / residual updates fused into the element kernel's write-out (launch_elem_epi)
-against the unfused path (HHG_NO_EPI=1 at hierarchy creation) and the oracle.  Fused nodes (footprint interiors of
+(opt-in: HHG_EPI=1 at hierarchy creation; measured slower) against the default unfused path and the oracle.  Fused nodes (footprint interiors of
 dense bricks) and consumer nodes (brick borders, macro interfaces, sparse bricks) together must reproduce the
 unfused V-cycle to rounding (the same arithmetic per node; only the fp64 RED order on brick borders differs)."""
 import os
@@ -20,15 +20,16 @@ C3 = (1e6, 30.0)
 
 
 def _mg(M, levels, degree, no_epi):
+    """no_epi=False: the fused epilogue (opt-in, HHG_EPI=1); True: the default unfused path."""
     etas = {L: lib_eta(M, L, C3) for L in levels}
     pv = {L: M.from_canonical(L, hhg.HHG_P2VEC, uniform_vec(M.canonical_keys(L, hhg.HHG_P2), 6)) for L in levels[1:]}
-    if no_epi:
-        os.environ["HHG_NO_EPI"] = "1"
+    if not no_epi:
+        os.environ["HHG_EPI"] = "1"
     try:
         return hhg.MG(M, levels[0], levels[-1], etas, pv, pre=3, post=3, degree=degree, power_iters=20,
                       coarse_iters=50)
     finally:
-        os.environ.pop("HHG_NO_EPI", None)
+        os.environ.pop("HHG_EPI", None)
 
 
 @pytest.mark.parametrize("degree", [2, 3])
