@@ -161,6 +161,21 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
   const int n2 = 2 * n1;
   const int64_t mb2 = (int64_t)mac * npts2, mb1 = (int64_t)mac * npts1;
 
+  // ---- row starts of the brick's footprint rows (P2: 9x9 rows (Y, Z), P1: 5x5), computed once per CTA and
+  // shared by the staging and write-out loops (rows outside the lattice hold garbage and are never used)
+#ifndef HHG_EXP_NOSROW
+  __shared__ int srow2[81], srow1[25];
+  for (int r = tid; r < 81 + 25; r += kBT) {
+    if (r < 81) srow2[r] = rowstart32(n2, 2 * j0 + r % 9, 2 * k0 + r / 9);
+    else srow1[r - 81] = rowstart32(n1, j0 + (r - 81) % 5, k0 + (r - 81) / 5);
+  }
+  __syncthreads();
+#define HHG_ROW2(gy, gz, Y, Z) srow2[(Y) + 9 * (Z)]
+#define HHG_ROW1(gy, gz, Y, Z) srow1[(Y) + 5 * (Z)]
+#else
+#define HHG_ROW2(gy, gz, Y, Z) rowstart32(n2, gy, gz)
+#define HHG_ROW1(gy, gz, Y, Z) rowstart32(n1, gy, gz)
+#endif
   // ---- stage: u footprint (cp.async), eta / p footprints, geometry; zero the output footprints
   const double* Gm = lgeo + (int64_t)mac * kLevelGeo;
   for (int r = tid; r < kGeoSm; r += kBT) cp_async8(sgeo + r, Gm + r);
@@ -190,7 +205,7 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
       const int X = L % 9, Y = (L / 9) % 9, Z = L / 81;
       const int gx = 2 * i0 + X, gy = 2 * j0 + Y, gz = 2 * k0 + Z;
       if (gx + gy + gz > n2) continue;
-      const double* src = u + mb2 + rowstart32(n2, gy, gz) + gx;
+      const double* src = u + mb2 + HHG_ROW2(gy, gz, Y, Z) + gx;
       HHG_CHECK(src - u >= mb2 && src - u < mb2 + npts2 && mb2 + npts2 <= cstride, "u stage", src - u, cstride);
       const int w = fword(X, Y, Z);
 #pragma unroll
@@ -203,7 +218,7 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
       const int X = L % 9, Y = (L / 9) % 9, Z = L / 81;
       const int gx = 2 * i0 + X, gy = 2 * j0 + Y, gz = 2 * k0 + Z;
       if (gx + gy + gz > n2) continue;
-      cp_async8(stt + fword(X, Y, Z), T2 + mb2 + rowstart32(n2, gy, gz) + gx);
+      cp_async8(stt + fword(X, Y, Z), T2 + mb2 + HHG_ROW2(gy, gz, Y, Z) + gx);
     }
   }
 #endif
@@ -237,7 +252,7 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
     const int X = L % 5, Y = (L / 5) % 5, Z = L / 25;
     const int gx = i0 + X, gy = j0 + Y, gz = k0 + Z;
     if (gx + gy + gz > n1) continue;
-    const int64_t ix = mb1 + rowstart32(n1, gy, gz) + gx;
+    const int64_t ix = mb1 + HHG_ROW1(gy, gz, Y, Z) + gx;
     HHG_CHECK(ix >= mb1 && ix < mb1 + npts1 && ix < (int64_t)gridDim.y * npts1, "P1 stage", ix, npts1);
     if (eta != nullptr) cp_async8(se + L, eta + ix);
     else se[L] = 1.0;
@@ -385,7 +400,7 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
       const int gx = 2 * i0 + X, gy = 2 * j0 + Y, gz = 2 * k0 + Z;
       if (gx + gy + gz > n2) continue;
       const int wxy = xs(X) + kPY * Y;
-      double* dst = yu + mb2 + rowstart32(n2, gy, gz) + gx;
+      double* dst = yu + mb2 + HHG_ROW2(gy, gz, Y, Z) + gx;
       HHG_CHECK(dst - yu >= mb2 && dst - yu < mb2 + npts2, "write-out", dst - yu, mb2 + npts2);
       const bool border = X == 0 || Y == 0 || Z == 0 || X == 8 || Y == 8 || Z == 8;
 #pragma unroll
@@ -433,7 +448,7 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
       if (Z < 2) v = syp[X + 5 * Y + 25 * Z];
       else if (Z > 2) v = syp[kF1Y + X + 5 * Y + 25 * (Z - 2)];
       else v = syp[X + 5 * Y + 50] + syp[kF1Y + X + 5 * Y];
-      double* dst = yp + mb1 + rowstart32(n1, gy, gz) + gx;
+      double* dst = yp + mb1 + HHG_ROW1(gy, gz, Y, Z) + gx;
       const bool border = X == 0 || Y == 0 || Z == 0 || X == 4 || Y == 4 || Z == 4;
       if (!border) *dst = v;
       else if (v != 0.0) {
@@ -442,10 +457,104 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
       }
     }
   }
+#undef HHG_ROW2
+#undef HHG_ROW1
 }
 
-// Launch of one element-kernel instantiation: one CTA per (macro, brick) item, one launch over all bricks --
-// or, in deterministic mode, one launch per brick colour.
+// ================================================================ sparse bricks without staging
+// The bricks cut by the macro's slanted face (delta <= 4, <= 64 tets: 30 % of the bricks at L5, all of them on
+// levels <= 2) hold few tets, so staging their 9x9x9 footprint in 43 KB of shared memory costs more than the
+// tets themselves.  k_elem_sparse runs them in a launch of their own without shared memory: one thread per tet
+// reads its 30 velocity dofs (+ eta, p, T at the nodes) straight from global memory (L1/L2 resident: the
+// brick's tets share their nodes) and adds its outputs with fp64 REDs, as the sparse path of k_elem_fp did.
+struct GlobU {  // u(a, c) = u[base + ix[a] + c * cs]
+  const double* b;
+  const int (&ix)[10];
+  int64_t cs;
+  __device__ __forceinline__ double operator()(int a, int c) const { return __ldg(b + ix[a] + c * cs); }
+};
+struct GlobT {
+  const double* b;
+  const int (&ix)[10];
+  __device__ __forceinline__ double operator()(int a) const { return __ldg(b + ix[a]); }
+};
+
+template <bool BLEND, int MODE, bool FULL, bool ETAQ = false>
+__global__ void __launch_bounds__(kBT)
+    k_elem_sparse(const MacroGeo* __restrict__ mgeo, const double* __restrict__ lgeo, const int32_t* __restrict__ bricks,
+                  int n1, double inv_n1, int64_t npts1, int64_t npts2, int64_t cstride, const double* __restrict__ eta,
+                  const double* __restrict__ u, const double* __restrict__ p, double* __restrict__ yu,
+                  double* __restrict__ yp, double gamma, const double* __restrict__ T2, EtaQ eq) {
+  constexpr bool NEED_P = elem_need_p(MODE);
+  const int mac = blockIdx.y;
+  const int32_t bpk = __ldg(bricks + blockIdx.x);
+  const int i0 = bpk & 1023, j0 = (bpk >> 10) & 1023, k0 = bpk >> 20;
+  const int delta = n1 - (i0 + j0 + k0);
+  const int tid = threadIdx.x;
+  if (tid >= eNItems[delta]) return;
+  const int item = eItems[delta][tid];
+  const int cube = item & 63, t = item >> 6;
+  const int x = i0 + (cube & 3), y = j0 + ((cube >> 2) & 3), z = k0 + (cube >> 4);
+  const int n2 = 2 * n1;
+  const int64_t mb2 = (int64_t)mac * npts2, mb1 = (int64_t)mac * npts1;
+  const MacroGeo& g = mgeo[mac];
+  const double* G = lgeo + (int64_t)mac * kLevelGeo;
+  double nh[3] = {0, 0, 0}, cK = 1.0;
+  if (BLEND) {
+    nh[0] = g.nhat[0];
+    nh[1] = g.nhat[1];
+    nh[2] = g.nhat[2];
+    cK = g.cK;
+  }
+  double xa[3];
+  {
+    const double fa = x * inv_n1, fb = y * inv_n1, fc = z * inv_n1;  // exact: n1 = 2^L
+#pragma unroll
+    for (int r = 0; r < 3; ++r) xa[r] = g.X0[r] + g.Jm[3 * r] * fa + g.Jm[3 * r + 1] * fb + g.Jm[3 * r + 2] * fc;
+  }
+  int ix[10];  // P2 node indices within the macro
+#pragma unroll
+  for (int a = 0; a < 10; ++a) {
+    const int sl = eSlot[t][a];
+    const int dx = sl % 3, dy = (sl / 3) % 3, dz = sl / 9;
+    ix[a] = rowstart32(n2, 2 * y + dy, 2 * z + dz) + 2 * x + dx;
+    HHG_CHECK(ix[a] >= 0 && ix[a] < npts2, "sparse node", ix[a], npts2);
+  }
+  int iv[4];  // P1 vertex indices within the macro
+  double et[4], pp[4] = {0, 0, 0, 0};
+#pragma unroll
+  for (int v = 0; v < 4; ++v) {
+    const int ps = ePSlot[t][v];
+    iv[v] = rowstart32(n1, y + ((ps >> 1) & 1), z + (ps >> 2)) + x + (ps & 1);
+    HHG_CHECK(iv[v] >= 0 && iv[v] < npts1, "sparse vertex", iv[v], npts1);
+    et[v] = eta != nullptr ? __ldg(eta + mb1 + iv[v]) : 1.0;
+    if (NEED_P) pp[v] = __ldg(p + mb1 + iv[v]);
+  }
+  double acc[10][3], gy[4];
+  tet_body<BLEND, MODE, FULL, GlobU, ETAQ, GlobT>(G + t * kTypeGeo, EWQ * __ldg(G + 6 * kTypeGeo), xa, nh, cK, gamma,
+                                                  GlobU{u ? u + mb2 : u, ix, cstride}, et, pp, acc, gy,
+                                                  GlobT{T2 ? T2 + mb2 : T2, ix}, eq);
+  if (elem_u_out(MODE)) {
+#pragma unroll
+    for (int a = 0; a < 10; ++a)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) atomicAdd(yu + mb2 + ix[a] + c * cstride, acc[a][c]);
+  }
+  if (elem_p_out(MODE)) {
+#pragma unroll
+    for (int v = 0; v < 4; ++v) atomicAdd(yp + mb1 + iv[v], gy[v]);
+  }
+}
+
+// Launch of one element-kernel instantiation: one CTA per (macro, brick) item, one launch over the dense bricks
+// plus one k_elem_sparse launch over the sparse ones -- or, in deterministic mode, one launch per brick colour
+// (sparse bricks on the dense path).
+// A/B switch: HHG_NO_SPLIT=1 runs the sparse bricks inside k_elem_fp (staged path) as before
+static const bool g_no_split = [] {
+  const char* e = getenv("HHG_NO_SPLIT");
+  return e && e[0] == '1';
+}();
+
 template <bool BLEND, int MODE, bool FULL, bool ETAQ, int EPI = EPI_NONE>
 struct ElemKernel {
   static constexpr size_t smem = fp_smem_words<MODE, ETAQ>() * sizeof(double);
@@ -469,7 +578,16 @@ struct ElemKernel {
           eq, det, ep);
       count_launch();
     };
-    if (!m->deterministic) {
+    if (!m->deterministic && !g_no_split) {
+      go(L.bricks, L.n_dense, 0);
+      const int64_t ns = L.n_bricks - L.n_dense;
+      if (nm * ns) {
+        k_elem_sparse<BLEND, MODE, FULL, ETAQ><<<dim3((unsigned)ns, (unsigned)nm), kBT, 0, s>>>(
+            m->dgeo, L.geo, L.bricks + L.n_dense, L.n1, 1.0 / L.n1, L.npts1, L.npts2, nm * L.npts2, eta, u, p, yu, yp,
+            gamma, T2, eq);
+        count_launch();
+      }
+    } else if (!m->deterministic) {
       go(L.bricks, L.n_bricks, 0);
     } else {
       for (int c = 0; c < 8; ++c) go(L.bricks_col + L.col_off[c], L.col_off[c + 1] - L.col_off[c], 1);

@@ -86,8 +86,10 @@ struct Level {
   int n1 = 0, n2 = 0;               // P1 / P2 lattice resolution
   int64_t npts1 = 0, npts2 = 0;     // per macro
   double* geo = nullptr;            // [n_macro][kLevelGeo]
-  int32_t* bricks = nullptr;        // 4x4x4-cube brick origins, packed i|j<<10|k<<20
+  int32_t* bricks = nullptr;        // 4x4x4-cube brick origins, packed i|j<<10|k<<20; dense bricks first
   int64_t n_bricks = 0;
+  int64_t n_dense = 0;              // bricks [0, n_dense): delta = n1 - (i0+j0+k0) > 4 (per-cube path); the rest
+                                    // (<= 64 tets, cut by the slanted face) go to k_elem_sparse
   int32_t* bricks_col = nullptr;    // the same bricks sorted by colour (bi&1 | (bj&1)<<1 | (bk&1)<<2)
   int64_t col_off[9] = {0};         // colour c: bricks_col[col_off[c] .. col_off[c+1])
   int32_t* rs1 = nullptr;           // row starts of the P1 / P2 lattices: index of (0, j, k) at [k (N+1) + j]

@@ -428,6 +428,12 @@ int ensure_level(Mesh* m, int level) {
     for (int k = 0; k <= n - 1; k += 4)
       for (int j = 0; j + k <= n - 1; j += 4)
         for (int i = 0; i + j + k <= n - 1; i += 4) b.push_back(i | (j << 10) | (k << 20));
+    // dense bricks first (same relative order), then the sparse ones (delta <= 4)
+    std::stable_partition(b.begin(), b.end(), [n](int32_t pk) {
+      return n - ((pk & 1023) + ((pk >> 10) & 1023) + (pk >> 20)) > 4;
+    });
+    L.n_dense = 0;
+    for (int32_t pk : b) L.n_dense += n - ((pk & 1023) + ((pk >> 10) & 1023) + (pk >> 20)) > 4;
     L.n_bricks = (int64_t)b.size();
     HHG_TRY(upload(&L.bricks, b));
     // colour classes for the deterministic mode: bricks of one colour are >= 8 cubes apart in some
