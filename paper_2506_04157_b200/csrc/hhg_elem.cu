@@ -37,7 +37,18 @@
 
 namespace hhg {
 
-constexpr int kBT = 64;  // threads per CTA; one CTA per brick of 4x4x4 lattice cubes
+constexpr int kBT = 64;  // threads per CTA of k_elem_sparse (one thread per tet of a sparse brick)
+// k_elem_fp: one CTA per brick of 4x4x4 lattice cubes, kWT thread groups of 64 (one thread per cube each); group g
+// evaluates tet types [g 6/kWT, (g+1) 6/kWT) of every cube into its own pair of per-warp output footprints, so more
+// warps share one staged u footprint.  kWT = 2 (4 warps, 3 CTAs = 12 warps per SM instead of 5 x 2) measured SLOWER
+// on B200 (L5 0.691 vs 0.644 ms, profiles/r02_tsplit_elem.jsonl: twice the footprint zeroing and write-out sums), so
+// the default stays kWT = 1; -DHHG_TSPLIT=2 builds the variant.
+#ifndef HHG_TSPLIT
+#define HHG_TSPLIT 1
+#endif
+constexpr int kWT = HHG_TSPLIT;
+static_assert(6 % kWT == 0, "type groups");
+constexpr int kBTD = 64 * kWT;
 
 // 32-bit lattice helpers (N <= 512 keeps (N+1)(N+2)(N+3) < 2^31)
 __device__ __forceinline__ int kbase32(int N, int k) {  // first index of plane k
@@ -110,8 +121,8 @@ struct FootT {  // scalar P2 footprint (temperature) for the quadrature-point vi
 
 template <int MODE, bool ETAQ = false>
 __host__ __device__ constexpr int fp_smem_words() {
-  return (elem_need_u(MODE) ? 3 * kFU : 0) + (elem_u_out(MODE) ? 2 * 3 * kFY : 0) +
-         kF1 + (elem_need_p(MODE) ? kF1 : 0) + (elem_p_out(MODE) ? 2 * kF1Y : 0) + kGeoSm +
+  return (elem_need_u(MODE) ? 3 * kFU : 0) + (elem_u_out(MODE) ? 2 * kWT * 3 * kFY : 0) +
+         kF1 + (elem_need_p(MODE) ? kF1 : 0) + (elem_p_out(MODE) ? 2 * kWT * kF1Y : 0) + kGeoSm +
          (ETAQ ? kFU : 0);
 }
 
@@ -131,9 +142,9 @@ static_assert(sizeof(MacroGeo) == kMG * sizeof(double), "MacroGeo layout");
 // the result is bitwise reproducible.
 template <bool BLEND, int MODE, bool FULL, bool ETAQ = false, int EPI = EPI_NONE>
 #ifndef HHG_FP_MINB
-#define HHG_FP_MINB 5
+#define HHG_FP_MINB (kWT == 1 ? 5 : 2)  // kWT = 2: (128, 3) makes ptxas spill at 168 registers; (128, 2) fits in <= 170 = 3 CTAs/SM
 #endif
-__global__ void __launch_bounds__(kBT, HHG_FP_MINB)
+__global__ void __launch_bounds__(kBTD, HHG_FP_MINB)
     k_elem_fp(const MacroGeo* __restrict__ mgeo, const double* __restrict__ lgeo, const int32_t* __restrict__ bricks,
               int nb, int n1, double inv_n1, int64_t npts1, int64_t npts2, int64_t cstride,
               const double* __restrict__ eta, const double* u, const double* __restrict__ p,
@@ -146,18 +157,18 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
   constexpr bool HAS_U_OUT = elem_u_out(MODE);
   extern __shared__ double sm[];
   double* su = sm;                                   // [3][kFU]
-  double* sy = su + (NEED_U ? 3 * kFU : 0);          // [2 warps][3][kFY]
-  double* se = sy + (HAS_U_OUT ? 6 * kFY : 0);       // [kF1]
+  double* sy = su + (NEED_U ? 3 * kFU : 0);          // [kWT groups][2 warps][3][kFY]
+  double* se = sy + (HAS_U_OUT ? 2 * kWT * 3 * kFY : 0);  // [kF1]
   double* sp = se + kF1;                             // [kF1]
-  double* syp = sp + (NEED_P ? kF1 : 0);             // [2 warps][kF1Y]
-  double* sgeo = syp + (HAS_P_OUT ? 2 * kF1Y : 0);   // [kGeoSm]
+  double* syp = sp + (NEED_P ? kF1 : 0);             // [kWT groups][2 warps][kF1Y]
+  double* sgeo = syp + (HAS_P_OUT ? 2 * kWT * kF1Y : 0);  // [kGeoSm]
   double* stt = sgeo + kGeoSm;                       // [kFU] temperature footprint (ETAQ)
 
   const int mac = blockIdx.y;
   const int32_t bpk = __ldg(bricks + blockIdx.x);
   const int i0 = bpk & 1023, j0 = (bpk >> 10) & 1023, k0 = bpk >> 20;
   const int delta = n1 - (i0 + j0 + k0);
-  const int tid = threadIdx.x, warp = tid >> 5;
+  const int tid = threadIdx.x;
   const int n2 = 2 * n1;
   const int64_t mb2 = (int64_t)mac * npts2, mb1 = (int64_t)mac * npts1;
 
@@ -165,7 +176,7 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
   // shared by the staging and write-out loops (rows outside the lattice hold garbage and are never used)
 #ifndef HHG_EXP_NOSROW
   __shared__ int srow2[81], srow1[25];
-  for (int r = tid; r < 81 + 25; r += kBT) {
+  for (int r = tid; r < 81 + 25; r += kBTD) {
     if (r < 81) srow2[r] = rowstart32(n2, 2 * j0 + r % 9, 2 * k0 + r / 9);
     else srow1[r - 81] = rowstart32(n1, j0 + (r - 81) % 5, k0 + (r - 81) / 5);
   }
@@ -178,13 +189,13 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
 #endif
   // ---- stage: u footprint (cp.async), eta / p footprints, geometry; zero the output footprints
   const double* Gm = lgeo + (int64_t)mac * kLevelGeo;
-  for (int r = tid; r < kGeoSm; r += kBT) cp_async8(sgeo + r, Gm + r);
+  for (int r = tid; r < kGeoSm; r += kBTD) cp_async8(sgeo + r, Gm + r);
 #ifdef HHG_EXP_ROWSTAGE
   // one (row, component) item per thread: 2 row-start evaluations per thread, 9 cp.async per item
   if (NEED_U || ETAQ) {
     constexpr int NI = (NEED_U ? 243 : 0) + (ETAQ ? 81 : 0);
 #pragma unroll 1
-    for (int it = tid; it < NI; it += kBT) {
+    for (int it = tid; it < NI; it += kBTD) {
       const int c = it / 81, r = it - 81 * c;
       const int Y = r % 9, Z = r / 9;
       const int gy = 2 * j0 + Y, gz = 2 * k0 + Z;
@@ -201,7 +212,7 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
 #else
   if (NEED_U) {
 #pragma unroll 1
-    for (int L = tid; L < 729; L += kBT) {
+    for (int L = tid; L < 729; L += kBTD) {
       const int X = L % 9, Y = (L / 9) % 9, Z = L / 81;
       const int gx = 2 * i0 + X, gy = 2 * j0 + Y, gz = 2 * k0 + Z;
       if (gx + gy + gz > n2) continue;
@@ -214,7 +225,7 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
   }
   if (ETAQ) {
 #pragma unroll 1
-    for (int L = tid; L < 729; L += kBT) {
+    for (int L = tid; L < 729; L += kBTD) {
       const int X = L % 9, Y = (L / 9) % 9, Z = L / 81;
       const int gx = 2 * i0 + X, gy = 2 * j0 + Y, gz = 2 * k0 + Z;
       if (gx + gy + gz > n2) continue;
@@ -232,7 +243,7 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
       const int32_t bp2 = __ldg(bricks + (b2 - mac2 * nbx));
       const int a2 = bp2 & 1023, c2 = (bp2 >> 10) & 1023, d2 = bp2 >> 20;
       const double* ub2 = u + (int64_t)mac2 * npts2;
-      for (int it = tid; it < 243; it += kBT) {
+      for (int it = tid; it < 243; it += kBTD) {
         const int c = it / 81, r = it - 81 * c;
         const int gy = 2 * c2 + r % 9, gz = 2 * d2 + r / 9;
         const int len = min(9, n2 - 2 * a2 - gy - gz + 1);
@@ -245,10 +256,10 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
   }
 #endif
   if (HAS_U_OUT)
-    for (int r = tid; r < 6 * kFY; r += kBT) sy[r] = 0.0;
+    for (int r = tid; r < 2 * kWT * 3 * kFY; r += kBTD) sy[r] = 0.0;
   if (HAS_P_OUT)
-    for (int r = tid; r < 2 * kF1Y; r += kBT) syp[r] = 0.0;
-  for (int L = tid; L < kF1; L += kBT) {  // P1 footprint (points outside the lattice are never read)
+    for (int r = tid; r < 2 * kWT * kF1Y; r += kBTD) syp[r] = 0.0;
+  for (int L = tid; L < kF1; L += kBTD) {  // P1 footprint (points outside the lattice are never read)
     const int X = L % 5, Y = (L / 5) % 5, Z = L / 25;
     const int gx = i0 + X, gy = j0 + Y, gz = k0 + Z;
     if (gx + gy + gz > n1) continue;
@@ -321,16 +332,19 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
   }
 
   // ---------------- dense brick: thread = cube, all lanes of a warp on the same tet type
-  const int x = tid & 3, y = (tid >> 2) & 3, z = tid >> 4;
+  const int x = tid & 3, y = (tid >> 2) & 3, z = (tid >> 4) & 3;
+  const int wz = z >> 1, grp = tid >> 6;  // cube-layer pair of this warp, type group
   const int s = i0 + j0 + k0 + x + y + z;
   const int ntypes = (s <= n1 - 3) ? 6 : ((s == n1 - 2) ? 5 : ((s == n1 - 1) ? 1 : 0));
   double xa[3];
   anchor(x, y, z, xa);
   const int cb2 = x + 2 * kPY * y + 2 * kPZ * z, cb1 = x + 5 * y + 25 * z;
-  double* yw = sy + warp * 3 * kFY + (x + 2 * kPY * y + 2 * kPZ * (z - 2 * warp));
-  double* ypw = syp + warp * kF1Y + (x + 5 * y + 25 * (z - 2 * warp));
+  const int fw = 2 * grp + wz;  // this warp's output footprints
+  double* yw = sy + fw * 3 * kFY + (x + 2 * kPY * y + 2 * kPZ * (z - 2 * wz));
+  double* ypw = syp + fw * kF1Y + (x + 5 * y + 25 * (z - 2 * wz));
+  constexpr int kTPG = 6 / kWT;
 #pragma unroll 1
-  for (int t = 0; t < 6; ++t) {
+  for (int t = grp * kTPG; t < (grp + 1) * kTPG; ++t) {
     const bool act = t < ntypes;
     double acc[10][3], gy[4];
     if (act) {
@@ -395,7 +409,7 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
   // are summed first
   if (HAS_U_OUT) {
 #pragma unroll 1
-    for (int L = tid; L < 729; L += kBT) {
+    for (int L = tid; L < 729; L += kBTD) {
       const int X = L % 9, Y = (L / 9) % 9, Z = L / 81;
       const int gx = 2 * i0 + X, gy = 2 * j0 + Y, gz = 2 * k0 + Z;
       if (gx + gy + gz > n2) continue;
@@ -405,10 +419,14 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
       const bool border = X == 0 || Y == 0 || Z == 0 || X == 8 || Y == 8 || Z == 8;
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        double v;
-        if (Z < 4) v = sy[c * kFY + wxy + kPZ * Z];
-        else if (Z > 4) v = sy[3 * kFY + c * kFY + wxy + kPZ * (Z - 4)];
-        else v = sy[c * kFY + wxy + kPZ * 4] + sy[3 * kFY + c * kFY + wxy];
+        double v = 0.0;
+#pragma unroll
+        for (int g2 = 0; g2 < kWT; ++g2) {  // type groups in fixed order
+          const double* f = sy + g2 * 6 * kFY + c * kFY + wxy;
+          if (Z < 4) v += f[kPZ * Z];
+          else if (Z > 4) v += f[3 * kFY + kPZ * (Z - 4)];
+          else v += f[kPZ * 4] + f[3 * kFY];
+        }
         if (EPI != EPI_NONE && !border && !det && gx + gy + gz < n2) {
           // fused consumer update (launch_elem_epi): this point is complete, inside the macro, BC-free
           const int64_t j = (dst - yu) + c * cstride;
@@ -440,14 +458,18 @@ __global__ void __launch_bounds__(kBT, HHG_FP_MINB)
     }
   }
   if (HAS_P_OUT) {
-    for (int L = tid; L < kF1; L += kBT) {
+    for (int L = tid; L < kF1; L += kBTD) {
       const int X = L % 5, Y = (L / 5) % 5, Z = L / 25;
       const int gx = i0 + X, gy = j0 + Y, gz = k0 + Z;
       if (gx + gy + gz > n1) continue;
-      double v;
-      if (Z < 2) v = syp[X + 5 * Y + 25 * Z];
-      else if (Z > 2) v = syp[kF1Y + X + 5 * Y + 25 * (Z - 2)];
-      else v = syp[X + 5 * Y + 50] + syp[kF1Y + X + 5 * Y];
+      double v = 0.0;
+#pragma unroll
+      for (int g2 = 0; g2 < kWT; ++g2) {
+        const double* f = syp + g2 * 2 * kF1Y + X + 5 * Y;
+        if (Z < 2) v += f[25 * Z];
+        else if (Z > 2) v += f[kF1Y + 25 * (Z - 2)];
+        else v += f[50] + f[kF1Y];
+      }
       double* dst = yp + mb1 + HHG_ROW1(gy, gz, Y, Z) + gx;
       const bool border = X == 0 || Y == 0 || Z == 0 || X == 4 || Y == 4 || Z == 4;
       if (!border) *dst = v;
@@ -573,7 +595,7 @@ struct ElemKernel {
     const int64_t nm = macro_count(m);
     auto go = [&](const int32_t* list, int64_t nb, int det) {
       if (nm * nb == 0) return;
-      k_elem_fp<BLEND, MODE, FULL, ETAQ, EPI><<<dim3((unsigned)nb, (unsigned)nm), kBT, smem, s>>>(
+      k_elem_fp<BLEND, MODE, FULL, ETAQ, EPI><<<dim3((unsigned)nb, (unsigned)nm), kBTD, smem, s>>>(
           m->dgeo, L.geo, list, (int)nb, L.n1, 1.0 / L.n1, L.npts1, L.npts2, nm * L.npts2, eta, u, p, yu, yp, gamma, T2,
           eq, det, ep);
       count_launch();

@@ -1,6 +1,7 @@
 """Per-launch counters of the element kernel from an ncu report -> JSON (read by bench.py for the
 roofline): duration, DRAM bytes, thread-level DFMA / DADD / DMUL counts and flops per micro tet
-(DFMA = 2 flops).  python tools/ncu_counts.py <rep.ncu-rep> <n_tets> <label> > profiles/<out>.json"""
+(DFMA = 2 flops); several captured kernels (one operator application split over launches) are summed.
+python tools/ncu_counts.py <rep.ncu-rep> <n_tets> <label> > profiles/<out>.json"""
 import csv, io, json, subprocess, sys
 rep, n_tets, label = sys.argv[1], int(sys.argv[2]), sys.argv[3]
 out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
@@ -27,4 +28,15 @@ for v in rows[2:]:
                 "fp64_pipe_active_pct": num("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
                 "warps_active_per_sm": num("sm__warps_active.avg.per_cycle_active"),
                 "registers": num("launch__registers_per_thread"), "source": rep})
-print(json.dumps(res[0] if len(res) == 1 else res, indent=1))
+if len(res) == 1:
+    print(json.dumps(res[0], indent=1))
+else:
+    # several kernels captured for one operator application (e.g. k_elem_fp over the dense bricks + k_elem_sparse
+    # over the sparse ones): the operator's counters are their sums, duration the sum of the launch durations
+    tot = {"label": label, "kernel": " + ".join(r["kernel"].split("(")[0] for r in res), "n_tets": n_tets}
+    for k in ("duration_s", "dram_read_bytes", "dram_write_bytes", "dram_bytes", "dfma", "dadd", "dmul"):
+        tot[k] = sum(r[k] for r in res)
+    tot["flops_per_tet"] = (2 * tot["dfma"] + tot["dadd"] + tot["dmul"]) / n_tets
+    tot["source"] = rep
+    tot["parts"] = res
+    print(json.dumps(tot, indent=1))
