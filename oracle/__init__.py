@@ -29,6 +29,6 @@ Every function cites the passage it follows.  Readings of silent/garbled
 passages are listed in DESIGN.md ("Readings").  All floating point is fp64.
 Parity status: every function is pinned by a ``-m "not gpu"`` test in
 tests/test_oracle_*.py against closed forms, exact rationals, invariants or
-brute force; none is "parity unpinned" except where DESIGN.md says so
-(blended C beyond its invariants).
+brute force; none is "parity unpinned" (the blended C is pinned by closed-form
+shell integrals, tests/test_oracle_operators.py).
 """

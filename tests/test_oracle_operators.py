@@ -137,6 +137,32 @@ def test_C_is_linear_in_gamma_and_converges_to_its_integral():
     assert errs[0] > errs[1] and all(errs[i] / errs[i + 1] > 10 for i in (1, 2)), errs
 
 
+def test_blended_C_against_closed_forms_on_the_shell():
+    """Blended C (-(grad ln rho . u, q) with grad ln rho = -gamma x/|x|, i.e. q^T C u = gamma ∫ (d.u) q on
+    the shell mapped exactly by the blending) against integrals known in closed form:
+    u = x/|x| (d.u = 1):  1^T C u -> gamma |Omega| = gamma 4/3 pi (r_o^3 - r_i^3),  r^T C u -> gamma pi (r_o^4 - r_i^4);
+    u = e_z x x (tangential, d.u = 0): C u -> 0.  Errors fall like O(h^4) (composite degree-2 rule, smooth
+    integrands); a missing |det J_B|, a wrong sign or a transposed J_B in the blended path fails the limits."""
+    from oracle.operators import node_coords
+    m = icoshell(3, 2)
+    ri, ro, g = 0.55, 1.0, 0.7
+    vol, rint = 4.0 / 3.0 * math.pi * (ro**3 - ri**3), math.pi * (ro**4 - ri**4)
+    e_vol, e_r, e_tan = [], [], []
+    for L in range(3):
+        lm = build_level(m.verts, m.tets, m.vtag, L)
+        d = Discretisation(lm, True, None, g, {}, build=("C",))
+        x2, x1 = node_coords(lm, "P2", True), node_coords(lm, "P1", True)
+        v = d.C @ (x2 / np.linalg.norm(x2, axis=1)[:, None]).ravel()
+        e_vol.append(abs(v.sum() / (g * vol) - 1.0))
+        e_r.append(abs(np.linalg.norm(x1, axis=1) @ v / (g * rint) - 1.0))
+        ut = np.stack([-x2[:, 1], x2[:, 0], np.zeros(x2.shape[0])], 1)
+        e_tan.append(np.abs(d.C @ ut.ravel()).max() / np.abs(v).max())
+    assert e_vol[-1] < 2e-5 and e_r[-1] < 2e-5 and e_tan[-1] < 1e-3, (e_vol, e_r, e_tan)
+    for e in (e_vol, e_r):
+        assert all(e[i] / e[i + 1] > 8 for i in (0, 1)), e
+    assert e_tan[0] > e_tan[1] > e_tan[2], e_tan
+
+
 def _manufactured():
     X, Y, Z = sy.symbols("x y z")
     b = X * Y * Z * (1 - X - Y - Z)
