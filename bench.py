@@ -306,7 +306,7 @@ def main():
         "vcycle_ms": ms, "setup_s": setup_s,
         "roofline": {"bound": "alu", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
                      "frac": achieved / fp64_peak, "traffic": traffic,
-                     "kernel": "k_elem_fp<blend,A,full> (fine level)", "elem_ms": elem_ms,
+                     "kernel": "k_elem_fp<blend,A,full> over the dense bricks + k_elem_sparse over the cut bricks (fine level, one operator application)", "elem_ms": elem_ms,
                      "flops_per_tet": flops_per_tet,
                      "flops_source": "profiles/r02_elem_counts.json (ncu dfma/dadd/dmul thread instructions per launch "
                                      "/ micro tets, DFMA = 2)",

@@ -176,11 +176,25 @@ __global__ void __launch_bounds__(kBTD, HHG_FP_MINB)
   // shared by the staging and write-out loops (rows outside the lattice hold garbage and are never used)
 #ifndef HHG_EXP_NOSROW
   __shared__ int srow2[81], srow1[25];
+#ifdef HHG_ROWWALK
+  __shared__ int sxm2[81];  // last footprint X of row r inside the lattice (negative: row outside)
+#endif
   for (int r = tid; r < 81 + 25; r += kBTD) {
-    if (r < 81) srow2[r] = rowstart32(n2, 2 * j0 + r % 9, 2 * k0 + r / 9);
-    else srow1[r - 81] = rowstart32(n1, j0 + (r - 81) % 5, k0 + (r - 81) / 5);
+    if (r < 81) {
+      srow2[r] = rowstart32(n2, 2 * j0 + r % 9, 2 * k0 + r / 9);
+#ifdef HHG_ROWWALK
+      sxm2[r] = n2 - 2 * (i0 + j0 + k0) - r % 9 - r / 9;
+#endif
+    } else srow1[r - 81] = rowstart32(n1, j0 + (r - 81) % 5, k0 + (r - 81) / 5);
   }
   __syncthreads();
+#ifdef HHG_ROWWALK
+  // row walk: thread = (footprint X = tid % 9 fixed, row slot tid / 9); a pass covers kRW rows (Y, Z), the next pass
+  // the following kRW rows -- no per-point div/mod, and word(X, Y, Z) = xs(X) + kPY (Y + 9 Z) = xs(X) + kPY r
+  constexpr int kRW = kBTD / 9;
+  const int wX = tid % 9, wR = tid / 9, wxs = xs(wX);
+  static_assert(kPZ == 9 * kPY, "row-walk addressing");
+#endif
 #define HHG_ROW2(gy, gz, Y, Z) srow2[(Y) + 9 * (Z)]
 #define HHG_ROW1(gy, gz, Y, Z) srow1[(Y) + 5 * (Z)]
 #else
@@ -209,6 +223,22 @@ __global__ void __launch_bounds__(kBTD, HHG_FP_MINB)
         if (X < len) cp_async8(d + xs(X), sr + X);
     }
   }
+#elif defined(HHG_ROWWALK)
+  if ((NEED_U || ETAQ) && wR < kRW) {
+    const int64_t ob = mb2 + 2 * i0 + wX;
+#pragma unroll 2
+    for (int r = wR; r < 81; r += kRW) {
+      if (wX > sxm2[r]) continue;
+      const int64_t o = ob + srow2[r];
+      HHG_CHECK(o >= mb2 && o < mb2 + npts2 && mb2 + npts2 <= cstride, "u stage", o, cstride);
+      const int w = wxs + kPY * r;
+      if (NEED_U) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) cp_async8(su + c * kFU + w, u + o + c * cstride);
+      }
+      if (ETAQ) cp_async8(stt + w, T2 + o);
+    }
+  }
 #else
   if (NEED_U) {
 #pragma unroll 1
@@ -225,7 +255,7 @@ __global__ void __launch_bounds__(kBTD, HHG_FP_MINB)
   }
   if (ETAQ) {
 #pragma unroll 1
-    for (int L = tid; L < 729; L += kBTD) {
+    for (int L = tid; L < 729; L += kBTD) {  // (not reached with HHG_ROWWALK: its branch above stages T too)
       const int X = L % 9, Y = (L / 9) % 9, Z = L / 81;
       const int gx = 2 * i0 + X, gy = 2 * j0 + Y, gz = 2 * k0 + Z;
       if (gx + gy + gz > n2) continue;
@@ -255,8 +285,15 @@ __global__ void __launch_bounds__(kBTD, HHG_FP_MINB)
     }
   }
 #endif
+#ifdef HHG_ROWWALK
+  if (HAS_U_OUT) {  // 16-byte stores (sy starts 16-byte aligned: 3 kFU and 6 kWT kFY are even)
+    double2* z2 = reinterpret_cast<double2*>(sy);
+    for (int r = tid; r < kWT * 3 * kFY; r += kBTD) z2[r] = make_double2(0.0, 0.0);
+  }
+#else
   if (HAS_U_OUT)
     for (int r = tid; r < 2 * kWT * 3 * kFY; r += kBTD) sy[r] = 0.0;
+#endif
   if (HAS_P_OUT)
     for (int r = tid; r < 2 * kWT * kF1Y; r += kBTD) syp[r] = 0.0;
   for (int L = tid; L < kF1; L += kBTD) {  // P1 footprint (points outside the lattice are never read)
@@ -408,6 +445,20 @@ __global__ void __launch_bounds__(kBTD, HHG_FP_MINB)
   // load-add-store) on the footprint border shared with neighbouring bricks; the two warps' Z = 4 planes
   // are summed first
   if (HAS_U_OUT) {
+#ifdef HHG_ROWWALK
+    const bool xborder = wX == 0 || wX == 8;
+    double* const yb = yu + mb2 + 2 * i0 + wX;
+#pragma unroll 1
+    for (int r = wR; r < (wR < kRW ? 81 : 0); r += kRW) {
+      const int xm = sxm2[r];
+      if (wX > xm) continue;
+      const int X = wX, Z = r / 9, Y = r - 9 * Z;
+      const bool inmac = wX < xm;  // strictly inside the macro's lattice (not on its slanted face)
+      const int wxy = wxs + kPY * Y;
+      double* dst = yb + srow2[r];
+      HHG_CHECK(dst - yu >= mb2 && dst - yu < mb2 + npts2, "write-out", dst - yu, mb2 + npts2);
+      const bool border = xborder || Y == 0 || Z == 0 || Y == 8 || Z == 8;
+#else
 #pragma unroll 1
     for (int L = tid; L < 729; L += kBTD) {
       const int X = L % 9, Y = (L / 9) % 9, Z = L / 81;
@@ -417,6 +468,8 @@ __global__ void __launch_bounds__(kBTD, HHG_FP_MINB)
       double* dst = yu + mb2 + HHG_ROW2(gy, gz, Y, Z) + gx;
       HHG_CHECK(dst - yu >= mb2 && dst - yu < mb2 + npts2, "write-out", dst - yu, mb2 + npts2);
       const bool border = X == 0 || Y == 0 || Z == 0 || X == 8 || Y == 8 || Z == 8;
+      const bool inmac = gx + gy + gz < n2;
+#endif
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         double v = 0.0;
@@ -427,7 +480,7 @@ __global__ void __launch_bounds__(kBTD, HHG_FP_MINB)
           else if (Z > 4) v += f[3 * kFY + kPZ * (Z - 4)];
           else v += f[kPZ * 4] + f[3 * kFY];
         }
-        if (EPI != EPI_NONE && !border && !det && gx + gy + gz < n2) {
+        if (EPI != EPI_NONE && !border && !det && inmac) {
           // fused consumer update (launch_elem_epi): this point is complete, inside the macro, BC-free
           const int64_t j = (dst - yu) + c * cstride;
           if (EPI == EPI_SUB) {
@@ -513,12 +566,37 @@ __global__ void __launch_bounds__(kBT)
   const int i0 = bpk & 1023, j0 = (bpk >> 10) & 1023, k0 = bpk >> 20;
   const int delta = n1 - (i0 + j0 + k0);
   const int tid = threadIdx.x;
+  const int n2 = 2 * n1;
+  const int64_t mb2 = (int64_t)mac * npts2, mb1 = (int64_t)mac * npts1;
+#ifdef HHG_SPARSE_STAGE
+  // the brick's u (and T) footprint inside the lattice -- the corner tetrahedron X + Y + Z <= 2 delta of the 9x9x9
+  // box, 165 points for delta = 4 -- staged row by row (thread = fixed X, rows (Y, Z) strided) in the dense
+  // kernel's layout, so the tets read their 30 dofs with LDS instead of 90 scattered global loads
+  constexpr bool STAGE_U = elem_need_u(MODE);
+  __shared__ double ssu[STAGE_U ? 3 * kFU : 1];
+  __shared__ double sst[ETAQ ? kFU : 1];
+  if (STAGE_U || ETAQ) {
+    const int wX = tid % 9, wxs = xs(wX);
+    for (int r = tid / 9; r < 81 && tid < 63; r += 7) {
+      const int Z = r / 9, Y = r - 9 * Z;
+      if (wX + Y + Z > 2 * delta) continue;
+      const int64_t o = mb2 + rowstart32(n2, 2 * j0 + Y, 2 * k0 + Z) + 2 * i0 + wX;
+      HHG_CHECK(o >= mb2 && o < mb2 + npts2, "sparse stage", o, mb2 + npts2);
+      const int w = wxs + kPY * r;
+      if (STAGE_U) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) cp_async8(ssu + c * kFU + w, u + o + c * cstride);
+      }
+      if (ETAQ) cp_async8(sst + w, T2 + o);
+    }
+    cp_async_wait_all();
+    __syncthreads();
+  }
+#endif
   if (tid >= eNItems[delta]) return;
   const int item = eItems[delta][tid];
   const int cube = item & 63, t = item >> 6;
   const int x = i0 + (cube & 3), y = j0 + ((cube >> 2) & 3), z = k0 + (cube >> 4);
-  const int n2 = 2 * n1;
-  const int64_t mb2 = (int64_t)mac * npts2, mb1 = (int64_t)mac * npts1;
   const MacroGeo& g = mgeo[mac];
   const double* G = lgeo + (int64_t)mac * kLevelGeo;
   double nh[3] = {0, 0, 0}, cK = 1.0;
@@ -553,9 +631,21 @@ __global__ void __launch_bounds__(kBT)
     if (NEED_P) pp[v] = __ldg(p + mb1 + iv[v]);
   }
   double acc[10][3], gy[4];
+#ifdef HHG_SPARSE_STAGE
+  {
+    const int cb2 = (cube & 3) + 2 * kPY * ((cube >> 2) & 3) + 2 * kPZ * (cube >> 4);
+    int offb[10];  // the type differs from lane to lane here: keep its 10 footprint offsets in registers
+#pragma unroll
+    for (int a = 0; a < 10; ++a) offb[a] = eOffB[t][a];
+    tet_body<BLEND, MODE, FULL, FootU, ETAQ, FootT>(G + t * kTypeGeo, EWQ * __ldg(G + 6 * kTypeGeo), xa, nh, cK, gamma,
+                                                    FootU{reinterpret_cast<const char*>(ssu + cb2), offb}, et, pp, acc,
+                                                    gy, FootT{reinterpret_cast<const char*>(sst + cb2), offb}, eq);
+  }
+#else
   tet_body<BLEND, MODE, FULL, GlobU, ETAQ, GlobT>(G + t * kTypeGeo, EWQ * __ldg(G + 6 * kTypeGeo), xa, nh, cK, gamma,
                                                   GlobU{u ? u + mb2 : u, ix, cstride}, et, pp, acc, gy,
                                                   GlobT{T2 ? T2 + mb2 : T2, ix}, eq);
+#endif
   if (elem_u_out(MODE)) {
 #pragma unroll
     for (int a = 0; a < 10; ++a)

@@ -15,9 +15,16 @@ for v in rows[2:]:
         un = u[h.index(k)] if k in h else ""
         return {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "usecond": 1e-6, "msecond": 1e-3,
                 "nsecond": 1e-9, "second": 1, "us": 1e-6, "ms": 1e-3, "ns": 1e-9, "s": 1}.get(un, 1)
-    dfma = num("smsp__sass_thread_inst_executed_op_dfma_pred_on.sum")
-    dadd = num("smsp__sass_thread_inst_executed_op_dadd_pred_on.sum")
-    dmul = num("smsp__sass_thread_inst_executed_op_dmul_pred_on.sum")
+    def count(op):
+        # thread-instruction count: the .sum metric when it was collected, else (--set full alone) the
+        # .sum.per_cycle_elapsed rate times the elapsed SMSP cycles it is normalised by
+        c = num("smsp__sass_thread_inst_executed_op_%s_pred_on.sum" % op)
+        if c is None:
+            r = num("smsp__sass_thread_inst_executed_op_%s_pred_on.sum.per_cycle_elapsed" % op)
+            cyc = num("smsp__cycles_elapsed.avg")
+            c = round(r * cyc) if r is not None and cyc is not None else None
+        return c
+    dfma, dadd, dmul = count("dfma"), count("dadd"), count("dmul")
     dur = num("gpu__time_duration.sum") * unit_scale("gpu__time_duration.sum")
     rd = num("dram__bytes_read.sum") * unit_scale("dram__bytes_read.sum")
     wr = num("dram__bytes_write.sum") * unit_scale("dram__bytes_write.sum")
