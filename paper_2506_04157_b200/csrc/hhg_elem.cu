@@ -74,6 +74,12 @@ __constant__ int eFirst[6];
 __constant__ int ePFirst[6];
 __device__ int eItems[5][64];  // delta = n - (i0+j0+k0) in 1..4: item = cube | type << 6
 __device__ int eNItems[5];
+// k_elem_sparse output gather: the footprint points of a sparse brick (X + Y + Z <= 2 delta; 165 for delta = 4),
+// each with the list of (item, local node) element outputs that land on it (640 = 10 nodes x 64 items slots)
+__device__ unsigned short eSpPt[5][165];    // X | (Y + 9 Z) << 4
+__device__ unsigned short eSpPtr[5][166];   // contribution list offsets
+__device__ unsigned short eSpCtr[5][640];   // slot = a * 64 + item
+__device__ int eSpNPt[5];
 
 constexpr int kGeoSm = 6 * kTypeGeo + 2;  // staged per-macro element geometry (doubles)
 
@@ -176,25 +182,11 @@ __global__ void __launch_bounds__(kBTD, HHG_FP_MINB)
   // shared by the staging and write-out loops (rows outside the lattice hold garbage and are never used)
 #ifndef HHG_EXP_NOSROW
   __shared__ int srow2[81], srow1[25];
-#ifdef HHG_ROWWALK
-  __shared__ int sxm2[81];  // last footprint X of row r inside the lattice (negative: row outside)
-#endif
   for (int r = tid; r < 81 + 25; r += kBTD) {
-    if (r < 81) {
-      srow2[r] = rowstart32(n2, 2 * j0 + r % 9, 2 * k0 + r / 9);
-#ifdef HHG_ROWWALK
-      sxm2[r] = n2 - 2 * (i0 + j0 + k0) - r % 9 - r / 9;
-#endif
-    } else srow1[r - 81] = rowstart32(n1, j0 + (r - 81) % 5, k0 + (r - 81) / 5);
+    if (r < 81) srow2[r] = rowstart32(n2, 2 * j0 + r % 9, 2 * k0 + r / 9);
+    else srow1[r - 81] = rowstart32(n1, j0 + (r - 81) % 5, k0 + (r - 81) / 5);
   }
   __syncthreads();
-#ifdef HHG_ROWWALK
-  // row walk: thread = (footprint X = tid % 9 fixed, row slot tid / 9); a pass covers kRW rows (Y, Z), the next pass
-  // the following kRW rows -- no per-point div/mod, and word(X, Y, Z) = xs(X) + kPY (Y + 9 Z) = xs(X) + kPY r
-  constexpr int kRW = kBTD / 9;
-  const int wX = tid % 9, wR = tid / 9, wxs = xs(wX);
-  static_assert(kPZ == 9 * kPY, "row-walk addressing");
-#endif
 #define HHG_ROW2(gy, gz, Y, Z) srow2[(Y) + 9 * (Z)]
 #define HHG_ROW1(gy, gz, Y, Z) srow1[(Y) + 5 * (Z)]
 #else
@@ -223,22 +215,6 @@ __global__ void __launch_bounds__(kBTD, HHG_FP_MINB)
         if (X < len) cp_async8(d + xs(X), sr + X);
     }
   }
-#elif defined(HHG_ROWWALK)
-  if ((NEED_U || ETAQ) && wR < kRW) {
-    const int64_t ob = mb2 + 2 * i0 + wX;
-#pragma unroll 2
-    for (int r = wR; r < 81; r += kRW) {
-      if (wX > sxm2[r]) continue;
-      const int64_t o = ob + srow2[r];
-      HHG_CHECK(o >= mb2 && o < mb2 + npts2 && mb2 + npts2 <= cstride, "u stage", o, cstride);
-      const int w = wxs + kPY * r;
-      if (NEED_U) {
-#pragma unroll
-        for (int c = 0; c < 3; ++c) cp_async8(su + c * kFU + w, u + o + c * cstride);
-      }
-      if (ETAQ) cp_async8(stt + w, T2 + o);
-    }
-  }
 #else
   if (NEED_U) {
 #pragma unroll 1
@@ -255,7 +231,7 @@ __global__ void __launch_bounds__(kBTD, HHG_FP_MINB)
   }
   if (ETAQ) {
 #pragma unroll 1
-    for (int L = tid; L < 729; L += kBTD) {  // (not reached with HHG_ROWWALK: its branch above stages T too)
+    for (int L = tid; L < 729; L += kBTD) {
       const int X = L % 9, Y = (L / 9) % 9, Z = L / 81;
       const int gx = 2 * i0 + X, gy = 2 * j0 + Y, gz = 2 * k0 + Z;
       if (gx + gy + gz > n2) continue;
@@ -285,15 +261,8 @@ __global__ void __launch_bounds__(kBTD, HHG_FP_MINB)
     }
   }
 #endif
-#ifdef HHG_ROWWALK
-  if (HAS_U_OUT) {  // 16-byte stores (sy starts 16-byte aligned: 3 kFU and 6 kWT kFY are even)
-    double2* z2 = reinterpret_cast<double2*>(sy);
-    for (int r = tid; r < kWT * 3 * kFY; r += kBTD) z2[r] = make_double2(0.0, 0.0);
-  }
-#else
   if (HAS_U_OUT)
     for (int r = tid; r < 2 * kWT * 3 * kFY; r += kBTD) sy[r] = 0.0;
-#endif
   if (HAS_P_OUT)
     for (int r = tid; r < 2 * kWT * kF1Y; r += kBTD) syp[r] = 0.0;
   for (int L = tid; L < kF1; L += kBTD) {  // P1 footprint (points outside the lattice are never read)
@@ -445,20 +414,6 @@ __global__ void __launch_bounds__(kBTD, HHG_FP_MINB)
   // load-add-store) on the footprint border shared with neighbouring bricks; the two warps' Z = 4 planes
   // are summed first
   if (HAS_U_OUT) {
-#ifdef HHG_ROWWALK
-    const bool xborder = wX == 0 || wX == 8;
-    double* const yb = yu + mb2 + 2 * i0 + wX;
-#pragma unroll 1
-    for (int r = wR; r < (wR < kRW ? 81 : 0); r += kRW) {
-      const int xm = sxm2[r];
-      if (wX > xm) continue;
-      const int X = wX, Z = r / 9, Y = r - 9 * Z;
-      const bool inmac = wX < xm;  // strictly inside the macro's lattice (not on its slanted face)
-      const int wxy = wxs + kPY * Y;
-      double* dst = yb + srow2[r];
-      HHG_CHECK(dst - yu >= mb2 && dst - yu < mb2 + npts2, "write-out", dst - yu, mb2 + npts2);
-      const bool border = xborder || Y == 0 || Z == 0 || Y == 8 || Z == 8;
-#else
 #pragma unroll 1
     for (int L = tid; L < 729; L += kBTD) {
       const int X = L % 9, Y = (L / 9) % 9, Z = L / 81;
@@ -469,7 +424,6 @@ __global__ void __launch_bounds__(kBTD, HHG_FP_MINB)
       HHG_CHECK(dst - yu >= mb2 && dst - yu < mb2 + npts2, "write-out", dst - yu, mb2 + npts2);
       const bool border = X == 0 || Y == 0 || Z == 0 || X == 8 || Y == 8 || Z == 8;
       const bool inmac = gx + gy + gz < n2;
-#endif
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         double v = 0.0;
@@ -573,7 +527,11 @@ __global__ void __launch_bounds__(kBT)
   // box, 165 points for delta = 4 -- staged row by row (thread = fixed X, rows (Y, Z) strided) in the dense
   // kernel's layout, so the tets read their 30 dofs with LDS instead of 90 scattered global loads
   constexpr bool STAGE_U = elem_need_u(MODE);
+#ifdef HHG_SPARSE_GATHER
+  __shared__ double ssu[(STAGE_U || elem_u_out(MODE)) ? 3 * kFU : 1];  // also the output slots of the gather
+#else
   __shared__ double ssu[STAGE_U ? 3 * kFU : 1];
+#endif
   __shared__ double sst[ETAQ ? kFU : 1];
   if (STAGE_U || ETAQ) {
     const int wX = tid % 9, wxs = xs(wX);
@@ -593,8 +551,13 @@ __global__ void __launch_bounds__(kBT)
     __syncthreads();
   }
 #endif
+#ifdef HHG_SPARSE_GATHER
+  const bool live = tid < eNItems[delta];
+  const int item = eItems[delta][live ? tid : 0];  // idle threads shadow item 0 and skip every output
+#else
   if (tid >= eNItems[delta]) return;
   const int item = eItems[delta][tid];
+#endif
   const int cube = item & 63, t = item >> 6;
   const int x = i0 + (cube & 3), y = j0 + ((cube >> 2) & 3), z = k0 + (cube >> 4);
   const MacroGeo& g = mgeo[mac];
@@ -646,6 +609,40 @@ __global__ void __launch_bounds__(kBT)
                                                   GlobU{u ? u + mb2 : u, ix, cstride}, et, pp, acc, gy,
                                                   GlobT{T2 ? T2 + mb2 : T2, ix}, eq);
 #endif
+#ifdef HHG_SPARSE_GATHER
+  if (elem_u_out(MODE)) {
+    // element outputs to shared-memory slots [c][a][item] (over the u footprint, no longer needed), then one
+    // thread per footprint point sums that point's contributions in fixed order: 3 REDs per point instead of 90 per tet
+    static_assert(3 * kFU >= 3 * 640, "slot array fits the u footprint");
+    double* sa = ssu;
+    if (STAGE_U) __syncthreads();  // every tet has read its dofs
+    if (live) {
+#pragma unroll
+      for (int a = 0; a < 10; ++a)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) sa[c * 640 + a * 64 + tid] = acc[a][c];
+    }
+    __syncthreads();
+    const int np = eSpNPt[delta];
+    for (int q = tid; q < np; q += kBT) {
+      const int pk = eSpPt[delta][q], X = pk & 15, r = pk >> 4, Z = r / 9, Y = r - 9 * Z;
+      double v[3] = {0.0, 0.0, 0.0};
+      for (int k = eSpPtr[delta][q], ke = eSpPtr[delta][q + 1]; k < ke; ++k) {
+        const int sl = eSpCtr[delta][k];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) v[c] += sa[c * 640 + sl];
+      }
+      double* dst = yu + mb2 + rowstart32(n2, 2 * j0 + Y, 2 * k0 + Z) + 2 * i0 + X;
+      HHG_CHECK(dst - yu >= mb2 && dst - yu < mb2 + npts2, "sparse gather", dst - yu, mb2 + npts2);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) atomicAdd(dst + c * cstride, v[c]);
+    }
+  }
+  if (elem_p_out(MODE) && live) {
+#pragma unroll
+    for (int v = 0; v < 4; ++v) atomicAdd(yp + mb1 + iv[v], gy[v]);
+  }
+#else
   if (elem_u_out(MODE)) {
 #pragma unroll
     for (int a = 0; a < 10; ++a)
@@ -656,6 +653,7 @@ __global__ void __launch_bounds__(kBT)
 #pragma unroll
     for (int v = 0; v < 4; ++v) atomicAdd(yp + mb1 + iv[v], gy[v]);
   }
+#endif
 }
 
 // Launch of one element-kernel instantiation: one CTA per (macro, brick) item, one launch over the dense bricks
@@ -781,6 +779,36 @@ static int ensure_slots() {
   HHG_CUDA(cudaMemcpyToSymbol(ePFirst, pfirst, sizeof(pfirst)));
   HHG_CUDA(cudaMemcpyToSymbol(eItems, items, sizeof(items)));
   HHG_CUDA(cudaMemcpyToSymbol(eNItems, nitems, sizeof(nitems)));
+  {  // sparse-brick output gather lists (fixed order: item-major within a point)
+    static unsigned short spt[5][165], sptr[5][166], sctr[5][640];
+    int snpt[5] = {0};
+    for (int delta = 1; delta <= 4; ++delta) {
+      int np = 0, nc = 0;
+      for (int Z = 0; Z < 9; ++Z)
+        for (int Y = 0; Y < 9; ++Y)
+          for (int X = 0; X < 9; ++X) {
+            if (X + Y + Z > 2 * delta) continue;
+            spt[delta][np] = (unsigned short)(X | ((Y + 9 * Z) << 4));
+            sptr[delta][np++] = (unsigned short)nc;
+            for (int i = 0; i < nitems[delta]; ++i) {
+              const int cube = items[delta][i] & 63, t = items[delta][i] >> 6;
+              for (int a = 0; a < 10; ++a) {
+                const int sl = slot[t][a];
+                if (2 * (cube & 3) + sl % 3 == X && 2 * ((cube >> 2) & 3) + (sl / 3) % 3 == Y &&
+                    2 * (cube >> 4) + sl / 9 == Z)
+                  sctr[delta][nc++] = (unsigned short)(a * 64 + i);
+              }
+            }
+          }
+      sptr[delta][np] = (unsigned short)nc;
+      snpt[delta] = np;
+      if (np > 165 || nc != 10 * nitems[delta]) return fail(HHG_EINVAL, "sparse gather table");
+    }
+    HHG_CUDA(cudaMemcpyToSymbol(eSpPt, spt, sizeof(spt)));
+    HHG_CUDA(cudaMemcpyToSymbol(eSpPtr, sptr, sizeof(sptr)));
+    HHG_CUDA(cudaMemcpyToSymbol(eSpCtr, sctr, sizeof(sctr)));
+    HHG_CUDA(cudaMemcpyToSymbol(eSpNPt, snpt, sizeof(snpt)));
+  }
   g_slots_ready = true;
   return HHG_OK;
 }
