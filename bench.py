@@ -283,8 +283,20 @@ def main():
     n_tets = M.local_macros() * 8 ** L        # this rank's micro tets (the element kernel it times)
     flops_per_tet = counts["epsilon_apply_L5"]["flops_per_tet"]
     traffic = counts["epsilon_apply_L5"]["dram_bytes"] if L == 5 else None
-    elem_ms = prof["apply_ms_sum"] / max(1, prof["apply_count"])
-    achieved = flops_per_tet * n_tets / (elem_ms * 1e-3) / 1e12
+    elem_ms = prof["apply_ms_sum"] / max(1, prof["apply_count"])       # dense + sparse launches of one application
+    achieved_op = flops_per_tet * n_tets / (elem_ms * 1e-3) / 1e12
+    # the dominant kernel alone: k_elem_fp over the dense bricks (its own tets and flops from the capture's first
+    # part, its own CUDA-event duration: an event is recorded between it and the sparse-brick launch)
+    parts = counts["epsilon_apply_L5"].get("parts") or []
+    dense_ms = prof["dense_ms_sum"] / max(1, prof["apply_count"])
+    n_sparse_tets = M.local_macros() * sparse_tets_per_macro(L)
+    if parts and L == 5 and dense_ms > 0:
+        dense_flops = 2 * parts[0]["dfma"] + parts[0]["dadd"] + parts[0]["dmul"]   # per launch, 240 macros
+        dense_flops *= M.local_macros() / 240.0
+        traffic = parts[0]["dram_bytes"]
+    else:
+        dense_flops = flops_per_tet * (n_tets - n_sparse_tets)
+    achieved = dense_flops / (dense_ms * 1e-3) / 1e12 if dense_ms > 0 else achieved_op
     pk = peaks()
     fp64 = fp64_peak_measured()
     fp64_peak = pk.get("fp64_tflops") or fp64["fp64_dfma_tflops"]
@@ -306,7 +318,14 @@ def main():
         "vcycle_ms": ms, "setup_s": setup_s,
         "roofline": {"bound": "alu", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
                      "frac": achieved / fp64_peak, "traffic": traffic,
-                     "kernel": "k_elem_fp<blend,A,full> over the dense bricks + k_elem_sparse over the cut bricks (fine level, one operator application)", "elem_ms": elem_ms,
+                     "kernel": "k_elem_fp<blend,A,full> over the dense bricks of the fine level (the dominant kernel)",
+                     "kernel_ms": dense_ms, "kernel_tets": n_tets - n_sparse_tets,
+                     "kernel_flops_per_launch": dense_flops,
+                     "operator": {"what": "one epsilon_apply element pass = k_elem_fp (dense bricks) + k_elem_sparse "
+                                          "(bricks cut by the macro's slanted face)", "elem_ms": elem_ms,
+                                  "achieved": achieved_op, "frac": achieved_op / fp64_peak,
+                                  "traffic": counts["epsilon_apply_L5"]["dram_bytes"] if L == 5 else None},
+                     "elem_ms": elem_ms,
                      "flops_per_tet": flops_per_tet,
                      "flops_source": "profiles/r02_elem_counts.json (ncu dfma/dadd/dmul thread instructions per launch "
                                      "/ micro tets, DFMA = 2)",
@@ -338,6 +357,22 @@ def main():
         print(json.dumps(result))
     if dist:
         dist.destroy_process_group()
+
+
+def sparse_tets_per_macro(L):
+    """Micro tets of one macro that lie in sparse bricks (4x4x4-cube bricks with delta = n - (i0+j0+k0) <= 4)."""
+    n = 2 ** L
+    tot = 0
+    for i0 in range(0, n, 4):
+        for j0 in range(0, n - i0, 4):
+            for k0 in range(0, n - i0 - j0, 4):
+                delta = n - (i0 + j0 + k0)
+                if delta > 4:
+                    continue
+                for c in range(64):
+                    ts = (c & 3) + ((c >> 2) & 3) + (c >> 4)
+                    tot += 6 if ts <= delta - 3 else (5 if ts == delta - 2 else (1 if ts == delta - 1 else 0))
+    return tot
 
 
 def elem_counts():

@@ -349,6 +349,10 @@ int vcycle_host_batch(hhg_mg* mg, const double* const* rhs_host, double* const* 
 int hhg_mg_profile(hhg_mg* mg, int enable);
 int hhg_mg_profile_get(hhg_mg* mg, double* apply_ms_sum, int64_t* apply_count, double* cycle_ms_sum,
                        int64_t* cycle_count);
+/* Of apply_ms_sum, the part spent in the dense-brick launch (k_elem_fp, the dominant kernel of the path:
+ * P:275-287 evaluated brick by brick) -- an event is recorded between it and the sparse-brick launch
+ * (k_elem_sparse).  Same count as apply_count.  dense_ms_sum: host pointer. */
+int hhg_mg_profile_get_dense(hhg_mg* mg, double* dense_ms_sum);
 int hhg_mg_destroy(hhg_mg* mg);
 
 /* ------------------------------------------------------------------ Stokes solve

@@ -37,7 +37,7 @@ EXPORTS = [
     "hhg_node_coords", "hhg_apply_bc", "hhg_interface_sum", "epsilon_apply", "div_apply", "divT_apply",
     "stokes_apply", "hhg_diag", "hhg_dot", "p2_restrict", "p2_prolong", "chebyshev_smooth",
     "hhg_power_iteration", "hhg_mg_create", "hhg_mg_lambda", "hhg_mg_coarse_iterations", "vcycle", "vcycle_host", "hhg_mg_profile",
-    "hhg_mg_profile_get", "hhg_mg_destroy", "hhg_launch_count",
+    "hhg_mg_profile_get", "hhg_mg_profile_get_dense", "hhg_mg_destroy", "hhg_launch_count",
     "hhg_mesh_create_part", "hhg_partition_rcb", "hhg_mesh_rank", "hhg_halo_info", "hhg_halo_keys",
     "hhg_owned_count", "hhg_halo_pack", "hhg_interface_sum_remote", "epsilon_apply_partial",
     "hhg_ablock_cg", "hhg_mass_apply", "hhg_mass_diag", "hhg_stokes_create", "hhg_stokes_solve",
@@ -78,7 +78,8 @@ def _load():
         "hhg_power_iteration": ([P, I, P, P, I, P, P, P], I),
         "hhg_mg_create": ([P, P, P, P, P], I), "hhg_mg_lambda": ([P, I, P], I), "hhg_mg_coarse_iterations": ([P, P], I), "vcycle": ([P, P, P, P], I),
         "vcycle_host": ([P, P, P, P], I), "hhg_mg_profile": ([P, I], I),
-        "hhg_mg_profile_get": ([P, P, P, P, P], I), "hhg_mg_destroy": ([P], I),
+        "hhg_mg_profile_get": ([P, P, P, P, P], I), "hhg_mg_profile_get_dense": ([P, P], I),
+        "hhg_mg_destroy": ([P], I),
         "hhg_mesh_create_part": ([P, I64, P, I64, P, I, P, I, I, P], I),
         "hhg_partition_rcb": ([P, I64, P, I64, I, I, P], I), "hhg_mesh_rank": ([P, P, P], I),
         "hhg_halo_info": ([P, I, I, P, P, P], I), "hhg_halo_keys": ([P, I, I, P], I),
@@ -716,7 +717,10 @@ class MG:
         na, nc = ctypes.c_int64(), ctypes.c_int64()
         _chk(_lib.hhg_mg_profile_get(self.handle, ctypes.byref(a), ctypes.byref(na), ctypes.byref(c),
                                      ctypes.byref(nc)))
-        return dict(apply_ms_sum=a.value, apply_count=na.value, cycle_ms_sum=c.value, cycle_count=nc.value)
+        d = ctypes.c_double()
+        _chk(_lib.hhg_mg_profile_get_dense(self.handle, ctypes.byref(d)))
+        return dict(apply_ms_sum=a.value, apply_count=na.value, cycle_ms_sum=c.value, cycle_count=nc.value,
+                    dense_ms_sum=d.value)
 
 
 class KMG:

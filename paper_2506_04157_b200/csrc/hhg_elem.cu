@@ -74,12 +74,6 @@ __constant__ int eFirst[6];
 __constant__ int ePFirst[6];
 __device__ int eItems[5][64];  // delta = n - (i0+j0+k0) in 1..4: item = cube | type << 6
 __device__ int eNItems[5];
-// k_elem_sparse output gather: the footprint points of a sparse brick (X + Y + Z <= 2 delta; 165 for delta = 4),
-// each with the list of (item, local node) element outputs that land on it (640 = 10 nodes x 64 items slots)
-__device__ unsigned short eSpPt[5][165];    // X | (Y + 9 Z) << 4
-__device__ unsigned short eSpPtr[5][166];   // contribution list offsets
-__device__ unsigned short eSpCtr[5][640];   // slot = a * 64 + item
-__device__ int eSpNPt[5];
 
 constexpr int kGeoSm = 6 * kTypeGeo + 2;  // staged per-macro element geometry (doubles)
 
@@ -423,7 +417,6 @@ __global__ void __launch_bounds__(kBTD, HHG_FP_MINB)
       double* dst = yu + mb2 + HHG_ROW2(gy, gz, Y, Z) + gx;
       HHG_CHECK(dst - yu >= mb2 && dst - yu < mb2 + npts2, "write-out", dst - yu, mb2 + npts2);
       const bool border = X == 0 || Y == 0 || Z == 0 || X == 8 || Y == 8 || Z == 8;
-      const bool inmac = gx + gy + gz < n2;
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         double v = 0.0;
@@ -434,7 +427,7 @@ __global__ void __launch_bounds__(kBTD, HHG_FP_MINB)
           else if (Z > 4) v += f[3 * kFY + kPZ * (Z - 4)];
           else v += f[kPZ * 4] + f[3 * kFY];
         }
-        if (EPI != EPI_NONE && !border && !det && inmac) {
+        if (EPI != EPI_NONE && !border && !det && gx + gy + gz < n2) {
           // fused consumer update (launch_elem_epi): this point is complete, inside the macro, BC-free
           const int64_t j = (dst - yu) + c * cstride;
           if (EPI == EPI_SUB) {
@@ -520,46 +513,12 @@ __global__ void __launch_bounds__(kBT)
   const int i0 = bpk & 1023, j0 = (bpk >> 10) & 1023, k0 = bpk >> 20;
   const int delta = n1 - (i0 + j0 + k0);
   const int tid = threadIdx.x;
-  const int n2 = 2 * n1;
-  const int64_t mb2 = (int64_t)mac * npts2, mb1 = (int64_t)mac * npts1;
-#ifdef HHG_SPARSE_STAGE
-  // the brick's u (and T) footprint inside the lattice -- the corner tetrahedron X + Y + Z <= 2 delta of the 9x9x9
-  // box, 165 points for delta = 4 -- staged row by row (thread = fixed X, rows (Y, Z) strided) in the dense
-  // kernel's layout, so the tets read their 30 dofs with LDS instead of 90 scattered global loads
-  constexpr bool STAGE_U = elem_need_u(MODE);
-#ifdef HHG_SPARSE_GATHER
-  __shared__ double ssu[(STAGE_U || elem_u_out(MODE)) ? 3 * kFU : 1];  // also the output slots of the gather
-#else
-  __shared__ double ssu[STAGE_U ? 3 * kFU : 1];
-#endif
-  __shared__ double sst[ETAQ ? kFU : 1];
-  if (STAGE_U || ETAQ) {
-    const int wX = tid % 9, wxs = xs(wX);
-    for (int r = tid / 9; r < 81 && tid < 63; r += 7) {
-      const int Z = r / 9, Y = r - 9 * Z;
-      if (wX + Y + Z > 2 * delta) continue;
-      const int64_t o = mb2 + rowstart32(n2, 2 * j0 + Y, 2 * k0 + Z) + 2 * i0 + wX;
-      HHG_CHECK(o >= mb2 && o < mb2 + npts2, "sparse stage", o, mb2 + npts2);
-      const int w = wxs + kPY * r;
-      if (STAGE_U) {
-#pragma unroll
-        for (int c = 0; c < 3; ++c) cp_async8(ssu + c * kFU + w, u + o + c * cstride);
-      }
-      if (ETAQ) cp_async8(sst + w, T2 + o);
-    }
-    cp_async_wait_all();
-    __syncthreads();
-  }
-#endif
-#ifdef HHG_SPARSE_GATHER
-  const bool live = tid < eNItems[delta];
-  const int item = eItems[delta][live ? tid : 0];  // idle threads shadow item 0 and skip every output
-#else
   if (tid >= eNItems[delta]) return;
   const int item = eItems[delta][tid];
-#endif
   const int cube = item & 63, t = item >> 6;
   const int x = i0 + (cube & 3), y = j0 + ((cube >> 2) & 3), z = k0 + (cube >> 4);
+  const int n2 = 2 * n1;
+  const int64_t mb2 = (int64_t)mac * npts2, mb1 = (int64_t)mac * npts1;
   const MacroGeo& g = mgeo[mac];
   const double* G = lgeo + (int64_t)mac * kLevelGeo;
   double nh[3] = {0, 0, 0}, cK = 1.0;
@@ -594,55 +553,9 @@ __global__ void __launch_bounds__(kBT)
     if (NEED_P) pp[v] = __ldg(p + mb1 + iv[v]);
   }
   double acc[10][3], gy[4];
-#ifdef HHG_SPARSE_STAGE
-  {
-    const int cb2 = (cube & 3) + 2 * kPY * ((cube >> 2) & 3) + 2 * kPZ * (cube >> 4);
-    int offb[10];  // the type differs from lane to lane here: keep its 10 footprint offsets in registers
-#pragma unroll
-    for (int a = 0; a < 10; ++a) offb[a] = eOffB[t][a];
-    tet_body<BLEND, MODE, FULL, FootU, ETAQ, FootT>(G + t * kTypeGeo, EWQ * __ldg(G + 6 * kTypeGeo), xa, nh, cK, gamma,
-                                                    FootU{reinterpret_cast<const char*>(ssu + cb2), offb}, et, pp, acc,
-                                                    gy, FootT{reinterpret_cast<const char*>(sst + cb2), offb}, eq);
-  }
-#else
   tet_body<BLEND, MODE, FULL, GlobU, ETAQ, GlobT>(G + t * kTypeGeo, EWQ * __ldg(G + 6 * kTypeGeo), xa, nh, cK, gamma,
                                                   GlobU{u ? u + mb2 : u, ix, cstride}, et, pp, acc, gy,
                                                   GlobT{T2 ? T2 + mb2 : T2, ix}, eq);
-#endif
-#ifdef HHG_SPARSE_GATHER
-  if (elem_u_out(MODE)) {
-    // element outputs to shared-memory slots [c][a][item] (over the u footprint, no longer needed), then one
-    // thread per footprint point sums that point's contributions in fixed order: 3 REDs per point instead of 90 per tet
-    static_assert(3 * kFU >= 3 * 640, "slot array fits the u footprint");
-    double* sa = ssu;
-    if (STAGE_U) __syncthreads();  // every tet has read its dofs
-    if (live) {
-#pragma unroll
-      for (int a = 0; a < 10; ++a)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) sa[c * 640 + a * 64 + tid] = acc[a][c];
-    }
-    __syncthreads();
-    const int np = eSpNPt[delta];
-    for (int q = tid; q < np; q += kBT) {
-      const int pk = eSpPt[delta][q], X = pk & 15, r = pk >> 4, Z = r / 9, Y = r - 9 * Z;
-      double v[3] = {0.0, 0.0, 0.0};
-      for (int k = eSpPtr[delta][q], ke = eSpPtr[delta][q + 1]; k < ke; ++k) {
-        const int sl = eSpCtr[delta][k];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) v[c] += sa[c * 640 + sl];
-      }
-      double* dst = yu + mb2 + rowstart32(n2, 2 * j0 + Y, 2 * k0 + Z) + 2 * i0 + X;
-      HHG_CHECK(dst - yu >= mb2 && dst - yu < mb2 + npts2, "sparse gather", dst - yu, mb2 + npts2);
-#pragma unroll
-      for (int c = 0; c < 3; ++c) atomicAdd(dst + c * cstride, v[c]);
-    }
-  }
-  if (elem_p_out(MODE) && live) {
-#pragma unroll
-    for (int v = 0; v < 4; ++v) atomicAdd(yp + mb1 + iv[v], gy[v]);
-  }
-#else
   if (elem_u_out(MODE)) {
 #pragma unroll
     for (int a = 0; a < 10; ++a)
@@ -653,13 +566,13 @@ __global__ void __launch_bounds__(kBT)
 #pragma unroll
     for (int v = 0; v < 4; ++v) atomicAdd(yp + mb1 + iv[v], gy[v]);
   }
-#endif
 }
 
 // Launch of one element-kernel instantiation: one CTA per (macro, brick) item, one launch over the dense bricks
 // plus one k_elem_sparse launch over the sparse ones -- or, in deterministic mode, one launch per brick colour
 // (sparse bricks on the dense path).
 // A/B switch: HHG_NO_SPLIT=1 runs the sparse bricks inside k_elem_fp (staged path) as before
+cudaEvent_t g_elem_mid_event = nullptr;
 static const bool g_no_split = [] {
   const char* e = getenv("HHG_NO_SPLIT");
   return e && e[0] == '1';
@@ -690,6 +603,10 @@ struct ElemKernel {
     };
     if (!m->deterministic && !g_no_split) {
       go(L.bricks, L.n_dense, 0);
+      if (g_elem_mid_event) {  // profiling: the dense-brick kernel is timed alone
+        HHG_CUDA(cudaEventRecord(g_elem_mid_event, s));
+        g_elem_mid_event = nullptr;
+      }
       const int64_t ns = L.n_bricks - L.n_dense;
       if (nm * ns) {
         k_elem_sparse<BLEND, MODE, FULL, ETAQ><<<dim3((unsigned)ns, (unsigned)nm), kBT, 0, s>>>(
@@ -779,36 +696,6 @@ static int ensure_slots() {
   HHG_CUDA(cudaMemcpyToSymbol(ePFirst, pfirst, sizeof(pfirst)));
   HHG_CUDA(cudaMemcpyToSymbol(eItems, items, sizeof(items)));
   HHG_CUDA(cudaMemcpyToSymbol(eNItems, nitems, sizeof(nitems)));
-  {  // sparse-brick output gather lists (fixed order: item-major within a point)
-    static unsigned short spt[5][165], sptr[5][166], sctr[5][640];
-    int snpt[5] = {0};
-    for (int delta = 1; delta <= 4; ++delta) {
-      int np = 0, nc = 0;
-      for (int Z = 0; Z < 9; ++Z)
-        for (int Y = 0; Y < 9; ++Y)
-          for (int X = 0; X < 9; ++X) {
-            if (X + Y + Z > 2 * delta) continue;
-            spt[delta][np] = (unsigned short)(X | ((Y + 9 * Z) << 4));
-            sptr[delta][np++] = (unsigned short)nc;
-            for (int i = 0; i < nitems[delta]; ++i) {
-              const int cube = items[delta][i] & 63, t = items[delta][i] >> 6;
-              for (int a = 0; a < 10; ++a) {
-                const int sl = slot[t][a];
-                if (2 * (cube & 3) + sl % 3 == X && 2 * ((cube >> 2) & 3) + (sl / 3) % 3 == Y &&
-                    2 * (cube >> 4) + sl / 9 == Z)
-                  sctr[delta][nc++] = (unsigned short)(a * 64 + i);
-              }
-            }
-          }
-      sptr[delta][np] = (unsigned short)nc;
-      snpt[delta] = np;
-      if (np > 165 || nc != 10 * nitems[delta]) return fail(HHG_EINVAL, "sparse gather table");
-    }
-    HHG_CUDA(cudaMemcpyToSymbol(eSpPt, spt, sizeof(spt)));
-    HHG_CUDA(cudaMemcpyToSymbol(eSpPtr, sptr, sizeof(sptr)));
-    HHG_CUDA(cudaMemcpyToSymbol(eSpCtr, sctr, sizeof(sctr)));
-    HHG_CUDA(cudaMemcpyToSymbol(eSpNPt, snpt, sizeof(snpt)));
-  }
   g_slots_ready = true;
   return HHG_OK;
 }

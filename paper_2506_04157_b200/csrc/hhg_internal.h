@@ -147,6 +147,9 @@ void free_level(Level& L);
 int64_t macro_count(const Mesh* m);
 
 // ---------------------------------------------------------------- kernel launchers (hhg_kernels.cu)
+// Profiling hook (hhg_mg_profile): when set, the element launcher records this event on its stream after the
+// dense-brick launch (k_elem_fp) and before the sparse-brick launch (k_elem_sparse), then clears it.
+extern cudaEvent_t g_elem_mid_event;
 int launch_elem(const Mesh* m, const Level& L, int mode, int form, const double* eta, double gamma,
                 const double* u, const double* p, double* yu, double* yp, cudaStream_t s);
 // w-BFBT operators (eq:schurWBFBT): K_{1/sqrt(eta_a)} (ELEM_KP1/KP1D, P1 -> P1) and the vector

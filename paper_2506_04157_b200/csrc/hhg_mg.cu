@@ -119,7 +119,7 @@ struct hhg_mg {
   bool prof = false;
   std::vector<cudaEvent_t> ev;
   size_t ev_used = 0;
-  double apply_ms = 0, cycle_ms = 0;
+  double apply_ms = 0, cycle_ms = 0, dense_ms = 0;  // dense_ms: k_elem_fp over the dense bricks alone
   int64_t apply_n = 0, cycle_n = 0;
   ~hhg_mg() {
     for (auto& L : lv) {
@@ -160,7 +160,7 @@ static int mg_apply(hhg_mg* mg, int l, const double* u, double* y, cudaStream_t 
                     bool fixup = true, int epi = EPI_NONE, const ChebEpi* ep = nullptr) {
   const bool timed = mg->prof && l == mg->prm.l_max;
   if (timed) {
-    if (mg->ev_used + 2 > mg->ev.size()) {
+    if (mg->ev_used + 3 > mg->ev.size()) {
       for (int i = 0; i < 64; ++i) {
         cudaEvent_t e;
         HHG_CUDA(cudaEventCreate(&e));
@@ -171,7 +171,10 @@ static int mg_apply(hhg_mg* mg, int l, const double* u, double* y, cudaStream_t 
   // y = (M P_v) A u : zero, element kernel (timed alone when profiling), interface sum + BC
   const Level& L = mg->mesh->levels[l];
   if (!y_zeroed) HHG_CUDA(cudaMemsetAsync(y, 0, p2vec_len(mg->mesh, l) * sizeof(double), s));
-  if (timed) HHG_CUDA(cudaEventRecord(mg->ev[mg->ev_used], s));
+  if (timed) {
+    HHG_CUDA(cudaEventRecord(mg->ev[mg->ev_used], s));
+    g_elem_mid_event = mg->ev[mg->ev_used + 1];
+  }
   if (mg->lv[l].T2)
     HHG_TRY(launch_elem_qeta(mg->mesh, L, ELEM_A, mg->lv[l].T2, mg->prm.qeta_lnC, mg->prm.qeta_jump, mg->prm.qeta_rjump,
                              u, y, s));
@@ -180,8 +183,12 @@ static int mg_apply(hhg_mg* mg, int l, const double* u, double* y, cudaStream_t 
   else
     HHG_TRY(launch_elem(mg->mesh, L, ELEM_A, mg->prm.visc_form, mg->lv[l].eta, 0.0, u, nullptr, y, nullptr, s));
   if (timed) {
-    HHG_CUDA(cudaEventRecord(mg->ev[mg->ev_used + 1], s));
-    mg->ev_used += 2;
+    if (g_elem_mid_event) {  // no separate sparse launch (deterministic mode, HHG_NO_SPLIT): dense = the whole
+      HHG_CUDA(cudaEventRecord(g_elem_mid_event, s));
+      g_elem_mid_event = nullptr;
+    }
+    HHG_CUDA(cudaEventRecord(mg->ev[mg->ev_used + 2], s));
+    mg->ev_used += 3;
   }
   if (!fixup) return HHG_OK;  // the consumer sums the interface copies itself (launch_*_fx)
   return launch_fixup(mg->mesh, L, HHG_P2VEC, true, true, y, s);
@@ -528,9 +535,11 @@ int vcycle(hhg_mg* mg, const double* rhs, double* x, hhg_stream_t stream) {
       HHG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
       mg->cycle_ms += ms;
       mg->cycle_n += 1;
-      for (size_t i = first_apply_ev; i + 1 < mg->ev_used; i += 2) {
-        HHG_CUDA(cudaEventElapsedTime(&ms, mg->ev[i], mg->ev[i + 1]));
+      for (size_t i = first_apply_ev; i + 2 < mg->ev_used; i += 3) {  // [start, after the dense launch, end]
+        HHG_CUDA(cudaEventElapsedTime(&ms, mg->ev[i], mg->ev[i + 2]));
         mg->apply_ms += ms;
+        HHG_CUDA(cudaEventElapsedTime(&ms, mg->ev[i], mg->ev[i + 1]));
+        mg->dense_ms += ms;
         mg->apply_n += 1;
       }
       mg->ev_used = 0;
@@ -739,7 +748,7 @@ int vcycle_host_batch(hhg_mg* mg, const double* const* rhs_host, double* const* 
 int hhg_mg_profile(hhg_mg* mg, int enable) {
   if (!mg) return fail(HHG_EINVAL, "NULL mg");
   mg->prof = enable != 0;
-  mg->apply_ms = mg->cycle_ms = 0;
+  mg->apply_ms = mg->cycle_ms = mg->dense_ms = 0;
   mg->apply_n = mg->cycle_n = 0;
   mg->ev_used = 0;
   return HHG_OK;
@@ -752,6 +761,12 @@ int hhg_mg_profile_get(hhg_mg* mg, double* apply_ms_sum, int64_t* apply_count, d
   if (apply_count) *apply_count = mg->apply_n;
   if (cycle_ms_sum) *cycle_ms_sum = mg->cycle_ms;
   if (cycle_count) *cycle_count = mg->cycle_n;
+  return HHG_OK;
+}
+
+int hhg_mg_profile_get_dense(hhg_mg* mg, double* dense_ms_sum) {
+  if (!mg || !dense_ms_sum) return fail(HHG_EINVAL, "NULL argument");
+  *dense_ms_sum = mg->dense_ms;
   return HHG_OK;
 }
 
