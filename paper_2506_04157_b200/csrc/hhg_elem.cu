@@ -573,6 +573,26 @@ __global__ void __launch_bounds__(kBT)
 // (sparse bricks on the dense path).
 // A/B switch: HHG_NO_SPLIT=1 runs the sparse bricks inside k_elem_fp (staged path) as before
 cudaEvent_t g_elem_mid_event = nullptr;
+// The dense and the sparse launch of one operator application touch common points only through fp64 REDs (brick
+// borders), so they are order-independent: the sparse launch (latency-bound, 12 warps/SM of 165 registers, no shared
+// memory) runs on a side stream and its CTAs fill the register space the shared-memory-limited dense CTAs leave free.
+// A/B switch: HHG_NO_CONC=1 launches them one after the other on the caller's stream.
+static const bool g_no_conc = [] {
+  const char* e = getenv("HHG_NO_CONC");
+  return e && e[0] == '1';
+}();
+int elem_side_prepare(const Mesh* m, cudaStream_t s) {
+  if (g_no_conc || m->side.count(s)) return HHG_OK;
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  HHG_CUDA(cudaStreamIsCapturing(s, &st));
+  if (st != cudaStreamCaptureStatusNone) return HHG_OK;  // never create under capture
+  Mesh::Side sd;
+  HHG_CUDA(cudaStreamCreateWithFlags(&sd.s, cudaStreamNonBlocking));
+  HHG_CUDA(cudaEventCreateWithFlags(&sd.fork, cudaEventDisableTiming));
+  HHG_CUDA(cudaEventCreateWithFlags(&sd.join, cudaEventDisableTiming));
+  m->side[s] = sd;
+  return HHG_OK;
+}
 static const bool g_no_split = [] {
   const char* e = getenv("HHG_NO_SPLIT");
   return e && e[0] == '1';
@@ -602,17 +622,33 @@ struct ElemKernel {
       count_launch();
     };
     if (!m->deterministic && !g_no_split) {
+      const int64_t ns = L.n_bricks - L.n_dense;
+      // fork: the sparse launch on the side stream, concurrent with the dense one (serial when profiling times the
+      // dense kernel alone, when one of the two is empty, or when no side stream exists for s yet under capture)
+      const Mesh::Side* sd = nullptr;
+      if (nm * ns && nm * L.n_dense && !g_elem_mid_event && !g_no_conc) {
+        HHG_TRY(elem_side_prepare(m, s));
+        auto it = m->side.find(s);
+        if (it != m->side.end()) sd = &it->second;
+      }
+      if (sd) {
+        HHG_CUDA(cudaEventRecord(sd->fork, s));
+        HHG_CUDA(cudaStreamWaitEvent(sd->s, sd->fork, 0));
+      }
       go(L.bricks, L.n_dense, 0);
       if (g_elem_mid_event) {  // profiling: the dense-brick kernel is timed alone
         HHG_CUDA(cudaEventRecord(g_elem_mid_event, s));
         g_elem_mid_event = nullptr;
       }
-      const int64_t ns = L.n_bricks - L.n_dense;
       if (nm * ns) {
-        k_elem_sparse<BLEND, MODE, FULL, ETAQ><<<dim3((unsigned)ns, (unsigned)nm), kBT, 0, s>>>(
+        k_elem_sparse<BLEND, MODE, FULL, ETAQ><<<dim3((unsigned)ns, (unsigned)nm), kBT, 0, sd ? sd->s : s>>>(
             m->dgeo, L.geo, L.bricks + L.n_dense, L.n1, 1.0 / L.n1, L.npts1, L.npts2, nm * L.npts2, eta, u, p, yu, yp,
             gamma, T2, eq);
         count_launch();
+      }
+      if (sd) {  // join
+        HHG_CUDA(cudaEventRecord(sd->join, sd->s));
+        HHG_CUDA(cudaStreamWaitEvent(s, sd->join, 0));
       }
     } else if (!m->deterministic) {
       go(L.bricks, L.n_bricks, 0);

@@ -133,8 +133,18 @@ struct Mesh {
   bool dgeo_dirty = true;
   std::vector<Level> levels;
   int device = 0;
+  // Side streams of the element launcher, one per caller stream: the sparse-brick launch runs on it concurrently
+  // with the dense-brick launch (fork / join by events; captured into CUDA graphs as parallel branches).
+  struct Side {
+    cudaStream_t s = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+  };
+  mutable std::map<cudaStream_t, Side> side;
   ~Mesh();
 };
+// Creates the side stream of caller stream `s` if missing; call before a stream capture that launches element
+// kernels (the launcher itself never creates one under capture and falls back to serial launches there).
+int elem_side_prepare(const Mesh* m, cudaStream_t s);
 
 int ensure_level(Mesh* m, int level);
 int ensure_device_geo(Mesh* m);

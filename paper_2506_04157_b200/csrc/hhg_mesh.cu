@@ -95,6 +95,11 @@ void free_level(Level& L) {
 Mesh::~Mesh() {
   for (auto& L : levels) free_level(L);
   if (dgeo) cudaFree(dgeo);
+  for (auto& kv : side) {
+    if (kv.second.fork) cudaEventDestroy(kv.second.fork);
+    if (kv.second.join) cudaEventDestroy(kv.second.join);
+    if (kv.second.s) cudaStreamDestroy(kv.second.s);
+  }
 }
 
 // ------------------------------------------------------------------ primitives

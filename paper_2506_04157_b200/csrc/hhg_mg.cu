@@ -550,6 +550,7 @@ int vcycle(hhg_mg* mg, const double* rhs, double* x, hhg_stream_t stream) {
     if (mg->gexec) cudaGraphExecDestroy(mg->gexec);
     mg->gexec = nullptr;
     cudaGraph_t g;
+    HHG_TRY(elem_side_prepare(mg->mesh, s));  // the element launcher forks its sparse launch: side stream before capture
     HHG_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     int r = mg_cycle(mg, mg->prm.l_max, rhs, x, s);
     cudaError_t ce = cudaStreamEndCapture(s, &g);
@@ -592,6 +593,7 @@ static int cg_precond(hhg_mg* mg, cudaStream_t s) {  // z = V(r) with a cached g
     if (mg->cg_gexec) cudaGraphExecDestroy(mg->cg_gexec);
     mg->cg_gexec = nullptr;
     cudaGraph_t g;
+    HHG_TRY(elem_side_prepare(mg->mesh, s));  // the element launcher forks its sparse launch: side stream before capture
     HHG_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     int r = mg_cycle(mg, mg->prm.l_max, mg->cg_r, mg->cg_z, s);
     cudaError_t ce = cudaStreamEndCapture(s, &g);
@@ -705,6 +707,7 @@ int vcycle_host_batch(hhg_mg* mg, const double* const* rhs_host, double* const* 
       if (mg->pipe_gexec[b]) cudaGraphExecDestroy(mg->pipe_gexec[b]);
       mg->pipe_gexec[b] = nullptr;
       cudaGraph_t g;
+      HHG_TRY(elem_side_prepare(mg->mesh, s));  // the element launcher forks its sparse launch: side stream before capture
       HHG_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
       int r = mg_cycle(mg, mg->prm.l_max, mg->st_in[b], mg->st_out[b], s);
       cudaError_t ce = cudaStreamEndCapture(s, &g);
