@@ -53,6 +53,28 @@ def test_two_solver_objects_on_two_streams():
         assert float((x2 - ref2).norm()) <= 1e-12 * float(ref2.norm())
 
 
+def test_profiled_serial_vcycle_equals_forked_graph_vcycle_and_times_the_dense_kernel():
+    """The element launcher forks the sparse-brick launch onto a side stream (parallel graph branches); with
+    hhg_mg_profile on, the launches stay serial and the dense-brick kernel is timed alone.  Both orders give the
+    same V-cycle up to the rounding order of the border REDs, and 0 < dense time <= element time."""
+    M = lib_mesh(icoshell(3, 2), 3, True, BC_SHELL)
+    mg, _ = _mg(M, (1, 2, 3))
+    f = lib_u(M, 3, 4)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        x_graph = mg.vcycle(f, stream=s).clone()
+    s.synchronize()
+    mg.profile(True)
+    with torch.cuda.stream(s):
+        x_prof = mg.vcycle(f, stream=s).clone()
+    s.synchronize()
+    p = mg.profile_get()
+    mg.profile(False)
+    assert float((x_prof - x_graph).norm()) <= 1e-12 * float(x_graph.norm())
+    assert p["apply_count"] > 0 and p["cycle_count"] == 1
+    assert 0.0 < p["dense_ms_sum"] <= p["apply_ms_sum"] <= p["cycle_ms_sum"]
+
+
 def test_deterministic_mode_is_bitwise_reproducible_and_matches_oracle():
     from oracle.multigrid import Hierarchy
     mac = icoshell(3, 2)
