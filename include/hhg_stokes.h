@@ -28,6 +28,12 @@
  *    mesh may run concurrently on different streams (they share no scratch).
  *    hhg_dot uses the level's scratch: concurrent hhg_dot calls on one (mesh, level)
  *    must be ordered by the caller.
+ *  - Operator applications launch their sparse-brick kernel on a library-owned side
+ *    stream forked from and joined back to the caller's stream by events (one side
+ *    stream per caller stream, created on the first application outside stream capture;
+ *    an application captured on a stream without one launches serially).  The result
+ *    is ordered on the caller's stream as if everything ran there.  Calls on one mesh
+ *    from several HOST threads must be serialised by the caller.
  *  - Hot calls are asynchronous on the caller's cudaStream_t (pass NULL for the
  *    legacy default stream).  Calls that return host scalars synchronise and say so.
  *  - Outputs must not alias inputs unless stated.
