@@ -322,7 +322,9 @@ def main():
                      "kernel_ms": dense_ms, "kernel_tets": n_tets - n_sparse_tets,
                      "kernel_flops_per_launch": dense_flops,
                      "operator": {"what": "one epsilon_apply element pass = k_elem_fp (dense bricks) + k_elem_sparse "
-                                          "(bricks cut by the macro's slanted face)", "elem_ms": elem_ms,
+                                          "(bricks cut by the macro's slanted face); timed with the two launches in series "
+                                          "(profiling mode) -- the timed V-cycle forks the sparse launch onto a side "
+                                          "stream", "elem_ms": elem_ms,
                                   "achieved": achieved_op, "frac": achieved_op / fp64_peak,
                                   "traffic": counts["epsilon_apply_L5"]["dram_bytes"] if L == 5 else None},
                      "elem_ms": elem_ms,
